@@ -1,0 +1,772 @@
+// C ABI (include/fsk_b200.h): validation with the reference's messages, IO
+// ledger accounting at the caller's TileConfig, host<->device staging, and the
+// device-resident solver loop. Every numeric result comes from the CUDA kernels.
+#include <climits>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/fsk_b200.h"
+#include "common.h"
+#include "core_kernels.h"
+#include "device_ops.h"
+#include "hostlib.h"
+#include "tc_engine.h"
+
+namespace fskb {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return FSK_OK;
+    } catch (const ValidationFailure& e) {
+        g_err = e.what();
+        return FSK_EVALIDATION;
+    } catch (const NumericalFailure& e) {
+        g_err = e.what();
+        return FSK_ENUMERICAL;
+    } catch (const CudaFailure& e) {
+        g_err = e.what();
+        return FSK_ECUDA;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return FSK_ECUDA;
+    }
+}
+
+int tensor_mode_from_env() {
+    const char* s = std::getenv("FSK_TENSOR_MODE");
+    if (!s) return 0;
+    const std::string v(s);
+    if (v == "fma" || v == "fp32" || v == "1") return 1;
+    if (v == "tensor" || v == "split3" || v == "2") return 2;
+    return 0;
+}
+
+namespace {
+
+std::vector<double> host_sqnorm(const fsk_measure& m, double scale) {
+    std::vector<double> out((size_t)(m.n));
+    for (int64_t i = 0; i < m.n; ++i) {
+        double s = 0.0;
+        for (int64_t t = 0; t < m.d; ++t) s += m.points[i * m.d + t] * m.points[i * m.d + t];
+        out[size_t(i)] = scale != 1.0 ? s * scale : s;
+    }
+    return out;
+}
+
+template <typename T>
+DevBuf<T> dev_from(const double* h, int64_t n, cudaStream_t s) {
+    DevBuf<T> b(size_t(n), s);
+    if constexpr (std::is_same_v<T, double>) {
+        b.upload(h, size_t(n));
+    } else {
+        std::vector<T> tmp((size_t)(n));
+        for (int64_t i = 0; i < n; ++i) tmp[size_t(i)] = T(h[i]);
+        b.upload(tmp.data(), size_t(n));
+        FSKB_CUDA(cudaStreamSynchronize(s));
+    }
+    return b;
+}
+
+template <typename T>
+void dev_to(const DevBuf<T>& b, double* h, int64_t n, cudaStream_t s) {
+    if constexpr (std::is_same_v<T, double>) {
+        b.download(h, size_t(n));
+        FSKB_CUDA(cudaStreamSynchronize(s));
+    } else {
+        std::vector<T> tmp((size_t)(n));
+        b.download(tmp.data(), size_t(n));
+        FSKB_CUDA(cudaStreamSynchronize(s));
+        for (int64_t i = 0; i < n; ++i) h[i] = double(tmp[size_t(i)]);
+    }
+}
+
+void sync_and_check(ExecCtx& C, int ignore = 0, const std::string& suffix = "") {
+    throw_for_flags(read_and_clear_flags(C) & ~ignore, suffix);
+}
+
+int bad_iteration(ExecCtx& C) {
+    int h[2];
+    FSKB_CUDA(cudaMemcpyAsync(h, C.flags, sizeof(h), cudaMemcpyDeviceToHost, C.s));
+    FSKB_CUDA(cudaStreamSynchronize(C.s));
+    return h[1];
+}
+
+void common_checks(const fsk_measure* src, const fsk_measure* tgt, const fsk_cost* cost,
+                   const fsk_tiles* tiles) {
+    if (!src || !tgt) throw ValidationFailure("null measure");
+    validate_problem_raw(*src, *tgt, cost);
+    validate_tiles_raw(tiles);
+}
+
+// r (n) and c (m) of the induced marginals at (f, g), all on device.
+template <typename T>
+void dev_marginals(DevProblem<T>& P, const T* f, const T* g, T eps, T* r, T* c, T* lse_f,
+                   T* mx_f, int* flags) {
+    FinalizeArgs<T> fa{};
+    fa.eps = eps;
+    fa.flags = flags;
+    fa.old_pot = f;
+    fa.w = P.src.w.get();
+    fa.out_marg = r;
+    fa.marg_flag = kFlagNonFiniteRowMarginal;
+    fa.out_lse = lse_f;
+    fa.out_max = mx_f;
+    half_step<T>(P, 0, g, eps, fa);
+    FinalizeArgs<T> fb{};
+    fb.eps = eps;
+    fb.flags = flags;
+    fb.old_pot = g;
+    fb.w = P.tgt.w.get();
+    fb.out_marg = c;
+    fb.marg_flag = kFlagNonFiniteColMarginal;
+    half_step<T>(P, 1, f, eps, fb);
+}
+
+struct HostMarginals {
+    std::vector<double> r, c;
+};
+
+double violation(const HostMarginals& hm, const fsk_measure& a, const fsk_measure& b) {
+    double v = 0.0;
+    for (int64_t i = 0; i < a.n; ++i) v += std::abs(hm.r[size_t(i)] - a.weights[i]);
+    for (int64_t j = 0; j < b.n; ++j) v += std::abs(hm.c[size_t(j)] - b.weights[j]);
+    return v;
+}
+
+// <f,a> + <g,b> - eps (sum r - 1) with unshifted potentials (solver.cpp:131-143)
+double dual_value(const fsk_measure& a, const fsk_measure& b, const double* fh, const double* gh,
+                  const std::vector<double>& alpha, const std::vector<double>& beta,
+                  const std::vector<double>& r, double eps) {
+    const double mass = cascade_sum(r.data(), r.size());
+    double value = 0.0;
+    for (int64_t i = 0; i < a.n; ++i) value += (fh[i] + alpha[size_t(i)]) * a.weights[i];
+    for (int64_t j = 0; j < b.n; ++j) value += (gh[j] + beta[size_t(j)]) * b.weights[j];
+    return value - eps * (mass - 1.0);
+}
+
+template <typename T>
+HostMarginals marginals_to_host(DevProblem<T>& P, const T* f, const T* g, T eps, ExecCtx& C,
+                                DevBuf<T>* lse_keep = nullptr, DevBuf<T>* mx_keep = nullptr) {
+    const int64_t n = P.src.n, m = P.tgt.n;
+    DevBuf<T> r(size_t(n), C.s), c(size_t(m), C.s);
+    dev_marginals<T>(P, f, g, eps, r.get(), c.get(), lse_keep ? lse_keep->get() : nullptr,
+                     mx_keep ? mx_keep->get() : nullptr, C.flags);
+    HostMarginals hm;
+    hm.r.resize(size_t(n));
+    hm.c.resize(size_t(m));
+    dev_to<T>(r, hm.r.data(), n, C.s);
+    dev_to<T>(c, hm.c.data(), m, C.s);
+    return hm;
+}
+
+// Device-resident Sinkhorn (solver.cpp:21-117). T = double: Precision::Double;
+// T = float: Precision::Single (tensor-core or FMA half-steps).
+template <typename T>
+void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* cost,
+                const fsk_config& cfg, const fsk_tiles& tiles, fsk_ledger* ledger,
+                fsk_report* rep, double* grad_out) {
+    constexpr bool kSingle = std::is_same_v<T, float>;
+    const int64_t n = src.n, m = tgt.n, d = src.d;
+    auto& C = exec_ctx();
+    DevProblem<T> P;
+    P.upload(src, tgt, cost, C.s);
+    if constexpr (kSingle) enable_tensor_path(P, tensor_mode_from_env());
+
+    const double fs = feature_scale(cost);
+    const std::vector<double> alpha = host_sqnorm(src, fs), beta = host_sqnorm(tgt, fs);
+    std::vector<double> f0((size_t)(n)), g0((size_t)(m));
+    for (int64_t i = 0; i < n; ++i) f0[size_t(i)] = -alpha[size_t(i)];
+    for (int64_t j = 0; j < m; ++j) g0[size_t(j)] = -beta[size_t(j)];
+    DevBuf<T> f = dev_from<T>(f0.data(), n, C.s), g = dev_from<T>(g0.data(), m, C.s);
+    DevBuf<T> f2, g2;
+    if (cfg.schedule == 1) {
+        f2.alloc(size_t(n), C.s);
+        g2.alloc(size_t(m), C.s);
+    }
+
+    const auto schedule =
+        eps_schedule_raw(cfg, joint_sq_diameter_raw(src.points, n, tgt.points, m, d));
+    int iters = 0;
+    double viol = 0.0, dual = 0.0, final_eps = 0.0;
+    bool stopped = false;
+    std::vector<double> hist;
+    double cur_tc_eps = -1.0;
+    for (double eps_d : schedule) {
+        const T eps = T(eps_d);
+        final_eps = eps_d;
+        if constexpr (kSingle) {
+            if (P.tc && cur_tc_eps != eps_d) {
+                P.tc->set_eps(P, eps_d);
+                cur_tc_eps = eps_d;
+            }
+        }
+        FinalizeArgs<T> fa{};
+        fa.eps = eps;
+        fa.flags = C.flags;
+        fa.bad_iter = C.bad_iter;
+        fa.iter = iters + 1;
+        if (cfg.schedule == 0) {
+            fa.out_pot = f.get();
+            half_step<T>(P, 0, g.get(), eps, fa);
+            fa.out_pot = g.get();
+            half_step<T>(P, 1, f.get(), eps, fa);
+            if (kSingle) {
+                ledger_update_f32(ledger, n, m, d, tiles.block_rows, tiles.block_cols);
+                ledger_update_f32(ledger, m, n, d, tiles.block_cols, tiles.block_rows);
+            } else {
+                ledger_update_f(ledger, n, m, d, tiles, cost);
+                ledger_update_g(ledger, n, m, d, tiles, cost);
+            }
+        } else {
+            fa.out_pot = f2.get();
+            fa.sym_old = f.get();
+            half_step<T>(P, 0, g.get(), eps, fa);
+            fa.out_pot = g2.get();
+            fa.sym_old = g.get();
+            half_step<T>(P, 1, f.get(), eps, fa);
+            std::swap(f, f2);
+            std::swap(g, g2);
+            if (kSingle) {
+                ledger_update_f32(ledger, n, m, d, tiles.block_rows, tiles.block_cols);
+                ledger_update_f32(ledger, m, n, d, tiles.block_cols, tiles.block_rows);
+                if (ledger) ledger->slow_to_fast_scalars += uint64_t(n + m);
+            } else {
+                ledger_symmetric(ledger, n, m, d, tiles, cost);
+            }
+        }
+        ++iters;
+        hist.push_back(eps_d);
+        // early stopping is checked at the final eps only; the reference's
+        // single-precision loop ignores it (solver.cpp:87-108)
+        if (!kSingle && cfg.marginal_tol > 0.0 && eps_d == cfg.eps) {
+            const int fl = read_and_clear_flags(C);
+            if (fl) throw_for_flags(fl, " at iteration " + std::to_string(iters));
+            HostMarginals hm = marginals_to_host<T>(P, f.get(), g.get(), eps, C);
+            ledger_marginals(ledger, n, m, d, tiles, cost);
+            sync_and_check(C);
+            viol = violation(hm, src, tgt);
+            if (viol <= cfg.marginal_tol) {
+                std::vector<double> fh((size_t)(n)), gh((size_t)(m));
+                dev_to<T>(f, fh.data(), n, C.s);
+                dev_to<T>(g, gh.data(), m, C.s);
+                // dual_cost recomputes the same marginals (deterministic kernels)
+                ledger_marginals(ledger, n, m, d, tiles, cost);
+                dual = dual_value(src, tgt, fh.data(), gh.data(), alpha, beta, hm.r, eps_d);
+                stopped = true;
+                break;
+            }
+        }
+    }
+    {
+        const int bad = bad_iteration(C);
+        const int fl = read_and_clear_flags(C);
+        if (fl) throw_for_flags(fl, bad != INT_MAX ? " at iteration " + std::to_string(bad) : "");
+    }
+    const double pot_eps = kSingle ? cfg.eps : final_eps;
+    std::vector<double> fh((size_t)(n)), gh((size_t)(m));
+    dev_to<T>(f, fh.data(), n, C.s);
+    dev_to<T>(g, gh.data(), m, C.s);
+    DevBuf<T> lse_f(size_t(n), C.s), mx_f(size_t(n), C.s);
+    if (!stopped) {
+        if constexpr (kSingle) {
+            if (P.tc && cur_tc_eps != pot_eps) P.tc->set_eps(P, pot_eps);
+        }
+        HostMarginals hm = marginals_to_host<T>(P, f.get(), g.get(), T(pot_eps), C, &lse_f, &mx_f);
+        sync_and_check(C);
+        ledger_marginals(ledger, n, m, d, tiles, cost);
+        viol = violation(hm, src, tgt);
+        ledger_marginals(ledger, n, m, d, tiles, cost);
+        dual = dual_value(src, tgt, fh.data(), gh.data(), alpha, beta, hm.r, pot_eps);
+    }
+    if (rep) {
+        rep->iterations = iters;
+        rep->marginal_violation = viol;
+        rep->dual_cost = dual;
+        rep->eps = pot_eps;
+        if (rep->f_hat) std::memcpy(rep->f_hat, fh.data(), sizeof(double) * size_t(n));
+        if (rep->g_hat) std::memcpy(rep->g_hat, gh.data(), sizeof(double) * size_t(m));
+        if (rep->eps_history)
+            for (int64_t k = 0; k < rep->eps_history_cap && k < int64_t(hist.size()); ++k)
+                rep->eps_history[k] = hist[size_t(k)];
+    }
+    if (grad_out) {
+        // grad_X = 2 r (X - softmax(S) Y) at the returned potentials
+        const T eps = T(pot_eps);
+        if (stopped) {
+            FinalizeArgs<T> fa{};
+            fa.eps = eps;
+            fa.flags = C.flags;
+            fa.out_lse = lse_f.get();
+            fa.out_max = mx_f.get();
+            half_step<T>(P, 0, g.get(), eps, fa);
+        }
+        DevBuf<T> O(size_t(n * d), C.s), G(size_t(n * d), C.s);
+        launch_apply<T>(P.params(0, g.get(), eps), lse_f.get(), P.tgt.pts.get(), d, nullptr,
+                        nullptr, 0, O.get(), C.s);
+        launch_grad_epilogue<T>(P.src.pts.get(), O.get(), P.src.w.get(), f.get(), lse_f.get(), n,
+                                d, eps, G.get(), C.flags, C.s);
+        dev_to<T>(G, grad_out, n * d, C.s);
+        sync_and_check(C);
+        if (ledger) {
+            ledger_marginals(ledger, n, m, d, tiles, cost);
+            ledger_apply(ledger, n, m, d, d, tiles, cost, false);
+        }
+    }
+}
+
+}  // namespace
+}  // namespace fskb
+
+using namespace fskb;
+
+extern "C" {
+
+const char* fsk_last_error(void) { return g_err.c_str(); }
+
+int fsk_update_f_hat(const fsk_measure* src, const fsk_measure* tgt, const double* g_hat,
+                     const fsk_cost* cost, double eps, const fsk_tiles* tiles, fsk_ledger* ledger,
+                     double* out) {
+    return guarded([&] {
+        common_checks(src, tgt, cost, tiles);
+        if (!(eps > 0.0)) throw ValidationFailure("eps must be positive");
+        if (!all_finite(g_hat, tgt->n)) throw ValidationFailure("non-finite g_hat entry");
+        ledger_update_f(ledger, src->n, tgt->n, src->d, *tiles, cost);
+        auto& C = exec_ctx();
+        DevProblem<double> P;
+        P.upload(*src, *tgt, cost, C.s);
+        DevBuf<double> g = dev_from<double>(g_hat, tgt->n, C.s), f(size_t(src->n), C.s);
+        FinalizeArgs<double> fa{};
+        fa.eps = eps;
+        fa.out_pot = f.get();
+        fa.flags = C.flags;
+        half_step<double>(P, 0, g.get(), eps, fa);
+        dev_to<double>(f, out, src->n, C.s);
+        sync_and_check(C);
+    });
+}
+
+int fsk_update_g_hat(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat,
+                     const fsk_cost* cost, double eps, const fsk_tiles* tiles, fsk_ledger* ledger,
+                     double* out) {
+    return guarded([&] {
+        common_checks(src, tgt, cost, tiles);
+        if (!(eps > 0.0)) throw ValidationFailure("eps must be positive");
+        if (!all_finite(f_hat, src->n)) throw ValidationFailure("non-finite f_hat entry");
+        ledger_update_g(ledger, src->n, tgt->n, src->d, *tiles, cost);
+        auto& C = exec_ctx();
+        DevProblem<double> P;
+        P.upload(*src, *tgt, cost, C.s);
+        DevBuf<double> f = dev_from<double>(f_hat, src->n, C.s), g(size_t(tgt->n), C.s);
+        FinalizeArgs<double> fa{};
+        fa.eps = eps;
+        fa.out_pot = g.get();
+        fa.flags = C.flags;
+        half_step<double>(P, 1, f.get(), eps, fa);
+        dev_to<double>(g, out, tgt->n, C.s);
+        sync_and_check(C);
+    });
+}
+
+int fsk_symmetric_update(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat,
+                         const double* g_hat, double eps, const fsk_cost* cost,
+                         const fsk_tiles* tiles, fsk_ledger* ledger, double* out_f,
+                         double* out_g) {
+    return guarded([&] {
+        common_checks(src, tgt, cost, tiles);
+        check_potentials_raw(f_hat, src->n, g_hat, tgt->n, eps);
+        ledger_symmetric(ledger, src->n, tgt->n, src->d, *tiles, cost);
+        auto& C = exec_ctx();
+        DevProblem<double> P;
+        P.upload(*src, *tgt, cost, C.s);
+        DevBuf<double> f = dev_from<double>(f_hat, src->n, C.s);
+        DevBuf<double> g = dev_from<double>(g_hat, tgt->n, C.s);
+        DevBuf<double> fn(size_t(src->n), C.s), gn(size_t(tgt->n), C.s);
+        FinalizeArgs<double> fa{};
+        fa.eps = eps;
+        fa.flags = C.flags;
+        fa.out_pot = fn.get();
+        fa.sym_old = f.get();
+        half_step<double>(P, 0, g.get(), eps, fa);
+        fa.out_pot = gn.get();
+        fa.sym_old = g.get();
+        half_step<double>(P, 1, f.get(), eps, fa);
+        dev_to<double>(fn, out_f, src->n, C.s);
+        dev_to<double>(gn, out_g, tgt->n, C.s);
+        sync_and_check(C);
+    });
+}
+
+namespace {
+// P V (side 0) or P^T U (side 1) with optional Hadamard factors, host buffers.
+int transport_host(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat,
+                   const double* g_hat, double eps, const fsk_cost* cost, const double* A,
+                   const double* B, int64_t r, const double* V, int64_t p, int side,
+                   double* out) {
+    auto& C = exec_ctx();
+    DevProblem<double> P;
+    P.upload(*src, *tgt, cost, C.s);
+    const int64_t R = side == 0 ? src->n : tgt->n, Cn = side == 0 ? tgt->n : src->n;
+    DevBuf<double> f = dev_from<double>(f_hat, src->n, C.s);
+    DevBuf<double> g = dev_from<double>(g_hat, tgt->n, C.s);
+    DevBuf<double> Vd = dev_from<double>(V, Cn * p, C.s);
+    DevBuf<double> Ad, Bd;
+    if (A) {
+        Ad = dev_from<double>(A, src->n * r, C.s);
+        Bd = dev_from<double>(B, tgt->n * r, C.s);
+    }
+    DevBuf<double> lse(size_t(R), C.s), mx(size_t(R), C.s), o(size_t(R * p), C.s);
+    const double* kpot = side == 0 ? g.get() : f.get();
+    const double* pot = side == 0 ? f.get() : g.get();
+    FinalizeArgs<double> fa{};
+    fa.eps = eps;
+    fa.flags = C.flags;
+    fa.out_lse = lse.get();
+    fa.out_max = mx.get();
+    half_step<double>(P, side, kpot, eps, fa);
+    if (p > 0)
+        transport<double>(P, side, kpot, pot, eps, lse.get(), mx.get(), Vd.get(), p, Ad.get(),
+                          Bd.get(), r, o.get(), C.flags);
+    dev_to<double>(o, out, R * p, C.s);
+    sync_and_check(C, kFlagNonFinitePotential);
+    return 0;
+}
+}  // namespace
+
+int fsk_apply_plan(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat,
+                   const double* g_hat, double eps, const fsk_cost* cost, const double* V,
+                   int64_t p, const fsk_tiles* tiles, fsk_ledger* ledger, double* out) {
+    return guarded([&] {
+        common_checks(src, tgt, cost, tiles);
+        check_potentials_raw(f_hat, src->n, g_hat, tgt->n, eps);
+        if (!all_finite(V, tgt->n * p)) throw ValidationFailure("apply_plan: non-finite V");
+        ledger_apply(ledger, src->n, tgt->n, src->d, p, *tiles, cost, false);
+        transport_host(src, tgt, f_hat, g_hat, eps, cost, nullptr, nullptr, 0, V, p, 0, out);
+    });
+}
+
+int fsk_apply_plan_adjoint(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat,
+                           const double* g_hat, double eps, const fsk_cost* cost, const double* U,
+                           int64_t p, const fsk_tiles* tiles, fsk_ledger* ledger, double* out) {
+    return guarded([&] {
+        common_checks(src, tgt, cost, tiles);
+        check_potentials_raw(f_hat, src->n, g_hat, tgt->n, eps);
+        if (!all_finite(U, src->n * p))
+            throw ValidationFailure("apply_plan_adjoint: non-finite U");
+        ledger_apply(ledger, src->n, tgt->n, src->d, p, *tiles, cost, true);
+        transport_host(src, tgt, f_hat, g_hat, eps, cost, nullptr, nullptr, 0, U, p, 1, out);
+    });
+}
+
+int fsk_apply_hadamard_plan(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat,
+                            const double* g_hat, double eps, const fsk_cost* cost,
+                            const double* A, const double* B, int64_t r, const double* V,
+                            int64_t p, const fsk_tiles* tiles, fsk_ledger* ledger, double* out) {
+    return guarded([&] {
+        common_checks(src, tgt, cost, tiles);
+        check_potentials_raw(f_hat, src->n, g_hat, tgt->n, eps);
+        if (r < 1) throw ValidationFailure("apply_hadamard_plan: rank factor r must be >= 1");
+        ledger_hadamard(ledger, src->n, tgt->n, src->d, r, p, *tiles, cost);
+        transport_host(src, tgt, f_hat, g_hat, eps, cost, A, B, r, V, p, 0, out);
+    });
+}
+
+int fsk_induced_marginals(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat,
+                          const double* g_hat, double eps, const fsk_cost* cost,
+                          const fsk_tiles* tiles, fsk_ledger* ledger, double* out_r,
+                          double* out_c) {
+    return guarded([&] {
+        common_checks(src, tgt, cost, tiles);
+        check_potentials_raw(f_hat, src->n, g_hat, tgt->n, eps);
+        ledger_marginals(ledger, src->n, tgt->n, src->d, *tiles, cost);
+        auto& C = exec_ctx();
+        DevProblem<double> P;
+        P.upload(*src, *tgt, cost, C.s);
+        DevBuf<double> f = dev_from<double>(f_hat, src->n, C.s);
+        DevBuf<double> g = dev_from<double>(g_hat, tgt->n, C.s);
+        HostMarginals hm = marginals_to_host<double>(P, f.get(), g.get(), eps, C);
+        sync_and_check(C);
+        std::memcpy(out_r, hm.r.data(), sizeof(double) * hm.r.size());
+        std::memcpy(out_c, hm.c.data(), sizeof(double) * hm.c.size());
+    });
+}
+
+namespace {
+int half_step_f32_host(const float* sp, const float* sw, int64_t n, const float* tp,
+                       const float* tw, int64_t m, int64_t d, const float* pot, float eps,
+                       int side, float* out) {
+    auto& C = exec_ctx();
+    DevProblem<float> P;
+    P.upload_f32(sp, sw, n, tp, tw, m, d, C.s);
+    if (enable_tensor_path(P, tensor_mode_from_env())) P.tc->set_eps(P, eps);
+    const int64_t R = side == 0 ? n : m, Cn = side == 0 ? m : n;
+    DevBuf<float> k(size_t(Cn), C.s), o(size_t(R), C.s);
+    k.upload(pot, size_t(Cn));
+    FinalizeArgs<float> fa{};
+    fa.eps = eps;
+    fa.out_pot = o.get();
+    fa.flags = C.flags;
+    half_step<float>(P, side, k.get(), eps, fa);
+    o.download(out, size_t(R));
+    sync_and_check(C);
+    return 0;
+}
+}  // namespace
+
+int fsk_update_f_hat_f32(const float* src_points, const float* src_weights, int64_t n,
+                         const float* tgt_points, const float* tgt_weights, int64_t m, int64_t d,
+                         const float* g_hat, float eps, const fsk_tiles* tiles,
+                         fsk_ledger* ledger, float* out) {
+    return guarded([&] {
+        ledger_update_f32(ledger, n, m, d, tiles ? tiles->block_rows : 64,
+                          tiles ? tiles->block_cols : 64);
+        half_step_f32_host(src_points, src_weights, n, tgt_points, tgt_weights, m, d, g_hat, eps,
+                           0, out);
+    });
+}
+
+int fsk_update_g_hat_f32(const float* src_points, const float* src_weights, int64_t n,
+                         const float* tgt_points, const float* tgt_weights, int64_t m, int64_t d,
+                         const float* f_hat, float eps, const fsk_tiles* tiles,
+                         fsk_ledger* ledger, float* out) {
+    return guarded([&] {
+        ledger_update_f32(ledger, m, n, d, tiles ? tiles->block_cols : 64,
+                          tiles ? tiles->block_rows : 64);
+        half_step_f32_host(src_points, src_weights, n, tgt_points, tgt_weights, m, d, f_hat, eps,
+                           1, out);
+    });
+}
+
+uint64_t fsk_io_count_f_update(int64_t n, int64_t m, int64_t d, const fsk_tiles* t) {
+    const Counts c = lse_counts(n, m, d, t->block_rows, t->block_cols, false);
+    return c.load + c.store;
+}
+uint64_t fsk_io_count_g_update(int64_t n, int64_t m, int64_t d, const fsk_tiles* t) {
+    const Counts c = lse_counts(m, n, d, t->block_cols, t->block_rows, false);
+    return c.load + c.store;
+}
+uint64_t fsk_io_count_symmetric_update(int64_t n, int64_t m, int64_t d, const fsk_tiles* t) {
+    return fsk_io_count_f_update(n, m, d, t) + fsk_io_count_g_update(n, m, d, t) + uint64_t(n + m);
+}
+uint64_t fsk_io_count_apply_plan(int64_t n, int64_t m, int64_t d, int64_t p, const fsk_tiles* t) {
+    const Counts c = apply_counts(n, m, d, p, 0, t->block_rows, t->block_cols, false);
+    return c.load + c.store;
+}
+uint64_t fsk_io_count_apply_plan_adjoint(int64_t n, int64_t m, int64_t d, int64_t p,
+                                         const fsk_tiles* t) {
+    const Counts c = apply_counts(m, n, d, p, 0, t->block_cols, t->block_rows, false);
+    return c.load + c.store;
+}
+uint64_t fsk_io_count_apply_hadamard(int64_t n, int64_t m, int64_t d, int64_t r, int64_t p,
+                                     const fsk_tiles* t) {
+    const Counts c = apply_counts(n, m, d, p, r, t->block_rows, t->block_cols, false);
+    return c.load + c.store;
+}
+uint64_t fsk_io_count_induced_marginals(int64_t n, int64_t m, int64_t d, const fsk_tiles* t) {
+    return fsk_io_count_f_update(n, m, d, t) + 2 * uint64_t(n) + fsk_io_count_g_update(n, m, d, t) +
+           2 * uint64_t(m);
+}
+
+int fsk_tiles_fit_sram(const fsk_tiles* t, int64_t d, int64_t sram_scalars) {
+    const uint64_t need = uint64_t(t->block_cols) * d + uint64_t(t->block_rows) * d +
+                          uint64_t(t->block_cols) + 2 * uint64_t(t->block_rows);
+    return need <= uint64_t(sram_scalars) ? 1 : 0;
+}
+
+void fsk_debug_break_lse(int broken) { break_lse_flag() = broken != 0; }
+
+int fsk_sinkhorn_solve(const fsk_measure* src, const fsk_measure* tgt, const fsk_cost* cost,
+                       const fsk_config* cfg, const fsk_tiles* tiles, fsk_ledger* ledger,
+                       fsk_report* report) {
+    return guarded([&] {
+        common_checks(src, tgt, cost, tiles);
+        validate_config_raw(*cfg);
+        if (cfg->precision == 0) {
+            if (labeled_cost(cost))
+                throw ValidationFailure(
+                    "single-precision solve supports the squared-Euclidean cost only");
+            solve_impl<float>(*src, *tgt, cost, *cfg, *tiles, ledger, report, nullptr);
+        } else {
+            solve_impl<double>(*src, *tgt, cost, *cfg, *tiles, ledger, report, nullptr);
+        }
+    });
+}
+
+int fsk_sinkhorn_solve_grad(const fsk_measure* src, const fsk_measure* tgt, const fsk_cost* cost,
+                            const fsk_config* cfg, const fsk_tiles* tiles, fsk_ledger* ledger,
+                            fsk_report* report, double* out_grad) {
+    return guarded([&] {
+        common_checks(src, tgt, cost, tiles);
+        validate_config_raw(*cfg);
+        if (cfg->precision == 0) {
+            if (labeled_cost(cost))
+                throw ValidationFailure(
+                    "single-precision solve supports the squared-Euclidean cost only");
+            solve_impl<float>(*src, *tgt, cost, *cfg, *tiles, ledger, report, out_grad);
+        } else {
+            solve_impl<double>(*src, *tgt, cost, *cfg, *tiles, ledger, report, out_grad);
+        }
+    });
+}
+
+int fsk_dual_cost(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat,
+                  const double* g_hat, double eps, const fsk_cost* cost, const fsk_tiles* tiles,
+                  fsk_ledger* ledger, double* out) {
+    return guarded([&] {
+        common_checks(src, tgt, cost, tiles);
+        check_potentials_raw(f_hat, src->n, g_hat, tgt->n, eps);
+        ledger_marginals(ledger, src->n, tgt->n, src->d, *tiles, cost);
+        auto& C = exec_ctx();
+        DevProblem<double> P;
+        P.upload(*src, *tgt, cost, C.s);
+        DevBuf<double> f = dev_from<double>(f_hat, src->n, C.s);
+        DevBuf<double> g = dev_from<double>(g_hat, tgt->n, C.s);
+        HostMarginals hm = marginals_to_host<double>(P, f.get(), g.get(), eps, C);
+        sync_and_check(C);
+        const double fs = feature_scale(cost);
+        *out = dual_value(*src, *tgt, f_hat, g_hat, host_sqnorm(*src, fs), host_sqnorm(*tgt, fs),
+                          hm.r, eps);
+    });
+}
+
+namespace {
+double solve_dual(const fsk_measure& a, const fsk_measure& b, const fsk_cost* cost,
+                  const fsk_config& cfg, const fsk_tiles& tiles, fsk_ledger* ledger) {
+    fsk_report rep{};
+    if (cfg.precision == 0) {
+        if (labeled_cost(cost))
+            throw ValidationFailure(
+                "single-precision solve supports the squared-Euclidean cost only");
+        solve_impl<float>(a, b, cost, cfg, tiles, ledger, &rep, nullptr);
+    } else {
+        solve_impl<double>(a, b, cost, cfg, tiles, ledger, &rep, nullptr);
+    }
+    return rep.dual_cost;
+}
+}  // namespace
+
+int fsk_sinkhorn_divergence_mixed(const fsk_measure* mu, const fsk_measure* nu,
+                                  const fsk_cost* cost_cross, const fsk_cost* cost_mu,
+                                  const fsk_cost* cost_nu, const fsk_config* cfg,
+                                  const fsk_tiles* tiles, fsk_ledger* ledger, double* out) {
+    return guarded([&] {
+        common_checks(mu, nu, cost_cross, tiles);
+        validate_config_raw(*cfg);
+        const double cross = solve_dual(*mu, *nu, cost_cross, *cfg, *tiles, ledger);
+        common_checks(mu, mu, cost_mu, tiles);
+        const double smu = solve_dual(*mu, *mu, cost_mu, *cfg, *tiles, ledger);
+        common_checks(nu, nu, cost_nu, tiles);
+        const double snu = solve_dual(*nu, *nu, cost_nu, *cfg, *tiles, ledger);
+        *out = cross - 0.5 * smu - 0.5 * snu;
+    });
+}
+
+int fsk_sinkhorn_divergence_batch(const fsk_measure* mus, const fsk_measure* nus, int64_t pairs,
+                                  const fsk_cost* cost, const fsk_config* cfg,
+                                  const fsk_tiles* tiles, fsk_ledger* ledger, double* out) {
+    return guarded([&] {
+        validate_config_raw(*cfg);
+        for (int64_t k = 0; k < pairs; ++k) {
+            common_checks(&mus[k], &nus[k], cost, tiles);
+            const double cross = solve_dual(mus[k], nus[k], cost, *cfg, *tiles, ledger);
+            const double smu = solve_dual(mus[k], mus[k], cost, *cfg, *tiles, ledger);
+            const double snu = solve_dual(nus[k], nus[k], cost, *cfg, *tiles, ledger);
+            out[k] = cross - 0.5 * smu - 0.5 * snu;
+        }
+    });
+}
+
+namespace {
+// side 0: grad_source / barycentric (rows of X, V = Y); side 1: grad_target (rows of Y, V = X)
+int autodiff_host(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat,
+                  const double* g_hat, double eps, const fsk_cost* cost, int side, bool grad,
+                  double* out) {
+    auto& C = exec_ctx();
+    DevProblem<double> P;
+    P.upload(*src, *tgt, cost, C.s);
+    const int64_t R = side == 0 ? src->n : tgt->n, d = src->d;
+    DevBuf<double> f = dev_from<double>(f_hat, src->n, C.s);
+    DevBuf<double> g = dev_from<double>(g_hat, tgt->n, C.s);
+    const double* kpot = side == 0 ? g.get() : f.get();
+    const double* pot = side == 0 ? f.get() : g.get();
+    DevBuf<double> lse(size_t(R), C.s), mx(size_t(R), C.s), O(size_t(R * d), C.s);
+    FinalizeArgs<double> fa{};
+    fa.eps = eps;
+    fa.flags = C.flags;
+    fa.out_lse = lse.get();
+    fa.out_max = mx.get();
+    half_step<double>(P, side, kpot, eps, fa);
+    const double* Q = side == 0 ? P.src.pts.get() : P.tgt.pts.get();
+    const double* V = side == 0 ? P.tgt.pts.get() : P.src.pts.get();
+    const double* w = side == 0 ? P.src.w.get() : P.tgt.w.get();
+    launch_apply<double>(P.params(side, kpot, eps), lse.get(), V, d, nullptr, nullptr, 0, O.get(),
+                         C.s);
+    if (grad) {
+        DevBuf<double> G(size_t(R * d), C.s);
+        launch_grad_epilogue<double>(Q, O.get(), w, pot, lse.get(), R, d, eps, G.get(), C.flags,
+                                     C.s);
+        dev_to<double>(G, out, R * d, C.s);
+    } else {
+        dev_to<double>(O, out, R * d, C.s);
+    }
+    sync_and_check(C);
+    return 0;
+}
+}  // namespace
+
+int fsk_grad_source(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat,
+                    const double* g_hat, double eps, const fsk_cost* cost, const fsk_tiles* tiles,
+                    fsk_ledger* ledger, double* out) {
+    return guarded([&] {
+        common_checks(src, tgt, cost, tiles);
+        check_potentials_raw(f_hat, src->n, g_hat, tgt->n, eps);
+        ledger_marginals(ledger, src->n, tgt->n, src->d, *tiles, cost);
+        ledger_apply(ledger, src->n, tgt->n, src->d, src->d, *tiles, cost, false);
+        autodiff_host(src, tgt, f_hat, g_hat, eps, cost, 0, true, out);
+    });
+}
+
+int fsk_grad_target(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat,
+                    const double* g_hat, double eps, const fsk_cost* cost, const fsk_tiles* tiles,
+                    fsk_ledger* ledger, double* out) {
+    return guarded([&] {
+        common_checks(src, tgt, cost, tiles);
+        check_potentials_raw(f_hat, src->n, g_hat, tgt->n, eps);
+        ledger_marginals(ledger, src->n, tgt->n, src->d, *tiles, cost);
+        ledger_apply(ledger, src->n, tgt->n, src->d, src->d, *tiles, cost, true);
+        autodiff_host(src, tgt, f_hat, g_hat, eps, cost, 1, true, out);
+    });
+}
+
+int fsk_barycentric_projection(const fsk_measure* src, const fsk_measure* tgt,
+                               const double* f_hat, const double* g_hat, double eps,
+                               const fsk_cost* cost, const fsk_tiles* tiles, fsk_ledger* ledger,
+                               double* out) {
+    return guarded([&] {
+        common_checks(src, tgt, cost, tiles);
+        check_potentials_raw(f_hat, src->n, g_hat, tgt->n, eps);
+        ledger_marginals(ledger, src->n, tgt->n, src->d, *tiles, cost);
+        ledger_apply(ledger, src->n, tgt->n, src->d, src->d, *tiles, cost, false);
+        autodiff_host(src, tgt, f_hat, g_hat, eps, cost, 0, false, out);
+    });
+}
+
+void fsk_rng_normal_fill(uint64_t seed, double* out, int64_t count) {
+    rng_normal_fill(seed, out, count);
+}
+
+const char* fsk_version(void) { return "fsk_b200 0.1 (sm_100a; tcgen05 split-fp16 + fp64/fp32 CUDA-core)"; }
+
+int fsk_device_count(void) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+    return c;
+}
+
+}  // extern "C"

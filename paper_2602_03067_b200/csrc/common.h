@@ -1,0 +1,97 @@
+// Shared host-side helpers for the B200 FlashSinkhorn engine.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace fskb {
+
+// Exceptions used inside the library; capi.cpp maps them to status codes.
+struct ValidationFailure : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct NumericalFailure : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct CudaFailure : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw CudaFailure(std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define FSKB_CUDA(call) ::fskb::cuda_check((call), #call)
+
+// Device-status bits written by kernels (atomicOr into a device int).
+enum : int {
+    kFlagNonFinitePotential = 1,
+    kFlagTransportOverflow = 2,
+    kFlagNonFiniteTransport = 4,
+    kFlagNonFiniteRowMarginal = 8,
+    kFlagNonFiniteColMarginal = 16,
+};
+
+// Plain owning device buffer (stream-ordered allocation).
+template <typename T>
+class DevBuf {
+public:
+    DevBuf() = default;
+    DevBuf(std::size_t n, cudaStream_t s) { alloc(n, s); }
+    ~DevBuf() { release(); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_), s_(o.s_) { o.p_ = nullptr; o.n_ = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p_ = o.p_;
+            n_ = o.n_;
+            s_ = o.s_;
+            o.p_ = nullptr;
+            o.n_ = 0;
+        }
+        return *this;
+    }
+    void alloc(std::size_t n, cudaStream_t s) {
+        release();
+        s_ = s;
+        n_ = n;
+        if (n) FSKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), s));
+    }
+    void release() {
+        if (p_) cudaFreeAsync(p_, s_);
+        p_ = nullptr;
+        n_ = 0;
+    }
+    T* get() const { return p_; }
+    std::size_t size() const { return n_; }
+    void upload(const T* host, std::size_t n) {
+        if (n) FSKB_CUDA(cudaMemcpyAsync(p_, host, n * sizeof(T), cudaMemcpyHostToDevice, s_));
+    }
+    void download(T* host, std::size_t n) const {
+        if (n) FSKB_CUDA(cudaMemcpyAsync(host, p_, n * sizeof(T), cudaMemcpyDeviceToHost, s_));
+    }
+    void zero() {
+        if (n_) FSKB_CUDA(cudaMemsetAsync(p_, 0, n_ * sizeof(T), s_));
+    }
+
+private:
+    T* p_ = nullptr;
+    std::size_t n_ = 0;
+    cudaStream_t s_ = nullptr;
+};
+
+// Global launch counter (the bench reports how many of our kernels ran).
+int64_t& launch_counter();
+inline void count_launch(int k = 1) { launch_counter() += k; }
+
+// Negative-control toggle (fsk::stream::debug_break_lse).
+bool& break_lse_flag();
+
+int num_sms();
+
+}  // namespace fskb

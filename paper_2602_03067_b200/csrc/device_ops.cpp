@@ -1,0 +1,244 @@
+#include "device_ops.h"
+
+#include <climits>
+#include <cmath>
+#include <vector>
+
+#include "tc_engine.h"
+
+namespace fskb {
+
+int64_t& launch_counter() {
+    static int64_t c = 0;
+    return c;
+}
+
+bool& break_lse_flag() {
+    static bool b = false;
+    return b;
+}
+
+int num_sms() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess)
+            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
+ExecCtx& exec_ctx() {
+    thread_local ExecCtx c;
+    if (!c.s) {
+        int count = 0;
+        if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+            throw CudaFailure("no CUDA device available (the B200 engine has no CPU fallback)");
+        FSKB_CUDA(cudaStreamCreateWithFlags(&c.s, cudaStreamNonBlocking));
+        FSKB_CUDA(cudaMalloc(reinterpret_cast<void**>(&c.flags), 2 * sizeof(int)));
+        c.bad_iter = c.flags + 1;
+        int init[2] = {0, INT_MAX};
+        FSKB_CUDA(cudaMemcpy(c.flags, init, sizeof(init), cudaMemcpyHostToDevice));
+    }
+    return c;
+}
+
+int read_and_clear_flags(ExecCtx& c) {
+    int h[2];
+    FSKB_CUDA(cudaMemcpyAsync(h, c.flags, sizeof(h), cudaMemcpyDeviceToHost, c.s));
+    FSKB_CUDA(cudaStreamSynchronize(c.s));
+    if (h[0] != 0 || h[1] != INT_MAX) {
+        int init[2] = {0, INT_MAX};
+        FSKB_CUDA(cudaMemcpyAsync(c.flags, init, sizeof(init), cudaMemcpyHostToDevice, c.s));
+        FSKB_CUDA(cudaStreamSynchronize(c.s));
+    }
+    return h[0];
+}
+
+void throw_for_flags(int flags, const std::string& suffix) {
+    if (!flags) return;
+    if (flags & kFlagNonFinitePotential)
+        throw NumericalFailure("non-finite potential produced by streaming LSE update" + suffix);
+    if (flags & kFlagTransportOverflow)
+        throw NumericalFailure("overflow in transport application, potentials are not stabilized" +
+                               suffix);
+    if (flags & kFlagNonFiniteTransport)
+        throw NumericalFailure("non-finite entry in transport application output" + suffix);
+    if (flags & kFlagNonFiniteRowMarginal)
+        throw NumericalFailure("non-finite induced row marginal" + suffix);
+    if (flags & kFlagNonFiniteColMarginal)
+        throw NumericalFailure("non-finite induced column marginal" + suffix);
+}
+
+namespace {
+
+template <typename T>
+void upload_side(DevSide<T>& side, const fsk_measure& m, bool want_labels, cudaStream_t s) {
+    side.n = m.n;
+    side.d = m.d;
+    side.pts.alloc(size_t(m.n * m.d), s);
+    side.w.alloc(size_t(m.n), s);
+    side.logw.alloc(size_t(m.n), s);
+    if constexpr (std::is_same_v<T, double>) {
+        side.pts.upload(m.points, size_t(m.n * m.d));
+        side.w.upload(m.weights, size_t(m.n));
+    } else {
+        std::vector<T> tmp((size_t)(m.n * m.d));
+        for (size_t i = 0; i < tmp.size(); ++i) tmp[i] = T(m.points[i]);
+        side.pts.upload(tmp.data(), tmp.size());
+        std::vector<T> w((size_t)(m.n));
+        for (size_t i = 0; i < w.size(); ++i) w[i] = T(m.weights[i]);
+        side.w.upload(w.data(), w.size());
+        FSKB_CUDA(cudaStreamSynchronize(s));  // tmp buffers leave scope
+    }
+    launch_log<T>(side.w.get(), side.logw.get(), m.n, s);
+    if (want_labels && m.labels) {
+        side.lab.alloc(size_t(m.n), s);
+        side.lab.upload(m.labels, size_t(m.n));
+    }
+}
+
+}  // namespace
+
+template <typename T>
+void DevProblem<T>::upload(const fsk_measure& a, const fsk_measure& b, const fsk_cost* cost,
+                           cudaStream_t stream) {
+    s = stream;
+    labeled = cost && cost->kind == 1;
+    fscale = labeled ? cost->lambda1 : 1.0;
+    lambda2 = labeled ? cost->lambda2 : 0.0;
+    upload_side(src, a, labeled, s);
+    upload_side(tgt, b, labeled, s);
+    if (labeled) {
+        wdim = cost->num_labels;
+        wtab.alloc(size_t(wdim * wdim), s);
+        wtab.upload(cost->label_cost, size_t(wdim * wdim));
+    }
+    FSKB_CUDA(cudaStreamSynchronize(s));
+}
+
+template <typename T>
+void DevProblem<T>::upload_f32(const float* xa, const float* wa, int64_t n, const float* xb,
+                               const float* wb, int64_t m, int64_t d, cudaStream_t stream) {
+    if constexpr (!std::is_same_v<T, float>) throw CudaFailure("upload_f32 on a double problem");
+    else {
+    s = stream;
+    labeled = false;
+    fscale = 1.0;
+    src.n = n;
+    src.d = d;
+    tgt.n = m;
+    tgt.d = d;
+    src.pts.alloc(size_t(n * d), s);
+    src.pts.upload(xa, size_t(n * d));
+    tgt.pts.alloc(size_t(m * d), s);
+    tgt.pts.upload(xb, size_t(m * d));
+    src.w.alloc(size_t(n), s);
+    src.w.upload(wa, size_t(n));
+    tgt.w.alloc(size_t(m), s);
+    tgt.w.upload(wb, size_t(m));
+    src.logw.alloc(size_t(n), s);
+    tgt.logw.alloc(size_t(m), s);
+    launch_log<T>(src.w.get(), src.logw.get(), n, s);
+    launch_log<T>(tgt.w.get(), tgt.logw.get(), m, s);
+    }
+}
+
+template <typename T>
+ScoreParams<T> DevProblem<T>::params(int side, const T* kpot, T eps) const {
+    ScoreParams<T> p{};
+    const DevSide<T>& q = side == 0 ? src : tgt;
+    const DevSide<T>& k = side == 0 ? tgt : src;
+    p.Q = q.pts.get();
+    p.K = k.pts.get();
+    p.R = q.n;
+    p.C = k.n;
+    p.d = q.d;
+    p.kscale = T(2.0 * fscale / double(eps));
+    if constexpr (std::is_same_v<T, float>) p.kscale = 2.0f * float(fscale) / eps;
+    p.kpot = kpot;
+    p.klogw = k.logw.get();
+    p.eps = eps;
+    if (labeled) {
+        p.qlab = q.lab.get();
+        p.klab = k.lab.get();
+        p.wtab = wtab.get();
+        p.wdim = wdim;
+        p.lam2_eps = T(lambda2 / double(eps));
+    }
+    return p;
+}
+
+template <typename T>
+void half_step(DevProblem<T>& P, int side, const T* kpot, T eps, const FinalizeArgs<T>& fa) {
+    if constexpr (std::is_same_v<T, float>) {
+        if (P.tc) {
+            P.tc->run(P, side, kpot, eps, fa, 0, P.rows(side));
+            return;
+        }
+    }
+    const ScoreParams<T> sp = P.params(side, kpot, eps);
+    const int splits = lse_splits(sp.R, sp.C);
+    DevBuf<T> pm(size_t(splits) * size_t(sp.R), P.s), ps(size_t(splits) * size_t(sp.R), P.s);
+    launch_lse<T>(sp, splits, pm.get(), ps.get(), P.s);
+    launch_lse_finalize<T>(pm.get(), ps.get(), splits, sp.R, fa, P.s);
+}
+
+template <typename T>
+void half_step_rows(DevProblem<T>& P, int side, const T* kpot, T eps, const FinalizeArgs<T>& fa,
+                    int64_t row_begin, int64_t row_end) {
+    if (row_end <= row_begin) return;
+    if constexpr (std::is_same_v<T, float>) {
+        if (P.tc) {
+            P.tc->run(P, side, kpot, eps, fa, row_begin, row_end);
+            return;
+        }
+    }
+    ScoreParams<T> sp = P.params(side, kpot, eps);
+    sp.Q += row_begin * sp.d;
+    sp.R = row_end - row_begin;
+    if (sp.qlab) sp.qlab += row_begin;
+    FinalizeArgs<T> f = fa;
+    auto off = [&](auto* p) { return p ? p + row_begin : p; };
+    f.out_pot = off(f.out_pot);
+    f.sym_old = off(f.sym_old);
+    f.out_lse = off(f.out_lse);
+    f.out_max = off(f.out_max);
+    f.old_pot = off(f.old_pot);
+    f.w = off(f.w);
+    f.out_marg = off(f.out_marg);
+    const int splits = lse_splits(sp.R, sp.C);
+    DevBuf<T> pm(size_t(splits) * size_t(sp.R), P.s), ps(size_t(splits) * size_t(sp.R), P.s);
+    launch_lse<T>(sp, splits, pm.get(), ps.get(), P.s);
+    launch_lse_finalize<T>(pm.get(), ps.get(), splits, sp.R, f, P.s);
+}
+
+template <typename T>
+void transport(DevProblem<T>& P, int side, const T* kpot, const T* pot, T eps, const T* lse,
+               const T* mx, const T* V, int64_t p, const T* A, const T* B, int64_t r, T* out,
+               int* flags) {
+    const ScoreParams<T> sp = P.params(side, kpot, eps);
+    DevBuf<T> O(size_t(sp.R) * size_t(p), P.s);
+    launch_apply<T>(sp, lse, V, p, A, B, r, O.get(), P.s);
+    const T* w = side == 0 ? P.src.w.get() : P.tgt.w.get();
+    launch_apply_finalize<T>(O.get(), sp.R, p, w, pot, lse, mx, eps, out, flags, P.s);
+}
+
+template struct DevProblem<float>;
+template struct DevProblem<double>;
+template void half_step<float>(DevProblem<float>&, int, const float*, float,
+                               const FinalizeArgs<float>&);
+template void half_step<double>(DevProblem<double>&, int, const double*, double,
+                                const FinalizeArgs<double>&);
+template void half_step_rows<float>(DevProblem<float>&, int, const float*, float,
+                                    const FinalizeArgs<float>&, int64_t, int64_t);
+template void half_step_rows<double>(DevProblem<double>&, int, const double*, double,
+                                     const FinalizeArgs<double>&, int64_t, int64_t);
+template void transport<float>(DevProblem<float>&, int, const float*, const float*, float,
+                               const float*, const float*, const float*, int64_t, const float*,
+                               const float*, int64_t, float*, int*);
+template void transport<double>(DevProblem<double>&, int, const double*, const double*, double,
+                                const double*, const double*, const double*, int64_t,
+                                const double*, const double*, int64_t, double*, int*);
+
+}  // namespace fskb

@@ -1,0 +1,78 @@
+// Device-resident problem and the operations composed from the kernels.
+// Used by capi.cpp (host-buffer C ABI) and engine.cpp (device engine).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "../../include/fsk_b200.h"
+#include "common.h"
+#include "core_kernels.h"
+
+namespace fskb {
+
+class TcHalfStep;  // tcgen05 split-fp16 half-step (tc_engine.h)
+
+// Per-thread execution context: one non-blocking stream on the current device
+// and a device status word.
+struct ExecCtx {
+    cudaStream_t s = nullptr;
+    int* flags = nullptr;  // device int
+    int* bad_iter = nullptr;
+};
+ExecCtx& exec_ctx();
+int read_and_clear_flags(ExecCtx& c);
+void throw_for_flags(int flags, const std::string& suffix = "");
+
+template <typename T>
+struct DevSide {
+    DevBuf<T> pts, w, logw;
+    DevBuf<int32_t> lab;
+    int64_t n = 0, d = 0;
+};
+
+template <typename T>
+struct DevProblem {
+    DevSide<T> src, tgt;
+    DevBuf<double> wtab;
+    int64_t wdim = 0;
+    bool labeled = false;
+    double fscale = 1.0, lambda2 = 0.0;
+    cudaStream_t s = nullptr;
+    std::shared_ptr<TcHalfStep> tc;  // tensor-core half-step (float only), null = FMA path
+    double tc_eps = 0.0;
+
+    void upload(const fsk_measure& a, const fsk_measure& b, const fsk_cost* cost,
+                cudaStream_t stream);
+    // float clouds straight from FloatCloud buffers (squared Euclidean)
+    void upload_f32(const float* xa, const float* wa, int64_t n, const float* xb,
+                    const float* wb, int64_t m, int64_t d, cudaStream_t stream);
+
+    ScoreParams<T> params(int side, const T* kpot, T eps) const;
+    int64_t rows(int side) const { return side == 0 ? src.n : tgt.n; }
+    int64_t cols(int side) const { return side == 0 ? tgt.n : src.n; }
+};
+
+// One LSE pass over all key columns for every row of `side`, plus epilogues.
+template <typename T>
+void half_step(DevProblem<T>& P, int side, const T* kpot, T eps, const FinalizeArgs<T>& fa);
+
+// Rows [row_begin, row_end) only; FinalizeArgs pointers address full-length
+// vectors. Used by the sharded device engine.
+template <typename T>
+void half_step_rows(DevProblem<T>& P, int side, const T* kpot, T eps, const FinalizeArgs<T>& fa,
+                    int64_t row_begin, int64_t row_end);
+
+// Transport application out = P V (side 0) or P^T V (side 1) given the LSE of
+// that orientation (lse, mx from a half_step pass).
+template <typename T>
+void transport(DevProblem<T>& P, int side, const T* kpot, const T* pot, T eps, const T* lse,
+               const T* mx, const T* V, int64_t p, const T* A, const T* B, int64_t r, T* out,
+               int* flags);
+
+// Enables the tcgen05 path for a float problem when the shape allows it.
+// mode: 0 auto, 1 force FMA, 2 force tensor. Returns true when enabled.
+bool enable_tensor_path(DevProblem<float>& P, int mode);
+const char* tensor_path_name(const DevProblem<float>& P);
+
+}  // namespace fskb

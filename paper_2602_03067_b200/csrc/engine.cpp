@@ -1,0 +1,178 @@
+// Device engine (fsk_engine_*): one problem resident in HBM, potentials in
+// caller-owned device buffers, half-steps over row ranges. This is the unit a
+// multi-GPU driver shards: rank k updates rows [k n/N, (k+1) n/N) of f, the
+// collective library all-gathers the length-n vector in place, then the same
+// for g. No collective lives in here.
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "../../include/fsk_b200.h"
+#include "common.h"
+#include "core_kernels.h"
+#include "device_ops.h"
+#include "hostlib.h"
+#include "tc_engine.h"
+
+namespace fskb {
+extern thread_local std::string g_err;
+}
+
+using namespace fskb;
+
+struct fsk_engine {
+    int device = 0;
+    DevProblem<float> P;
+    float* f = nullptr;
+    float* g = nullptr;
+    double eps = 0.0;
+    cudaStream_t own = nullptr;
+    int* flags = nullptr;
+    int64_t launches_at_create = 0;
+};
+
+namespace {
+
+template <typename F>
+int eguard(F&& f) {
+    try {
+        f();
+        return FSK_OK;
+    } catch (const ValidationFailure& e) {
+        g_err = e.what();
+        return FSK_EVALIDATION;
+    } catch (const NumericalFailure& e) {
+        g_err = e.what();
+        return FSK_ENUMERICAL;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return FSK_ECUDA;
+    }
+}
+
+cudaStream_t pick(fsk_engine* e, void* stream) {
+    return stream ? static_cast<cudaStream_t>(stream) : e->own;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fsk_engine_create(int device, const double* X, const double* a, int64_t n, const double* Y,
+                      const double* b, int64_t m, int64_t d, int mode, fsk_engine** out) {
+    return eguard([&] {
+        fsk_measure src{X, a, nullptr, n, d}, tgt{Y, b, nullptr, m, d};
+        validate_problem_raw(src, tgt, nullptr);
+        FSKB_CUDA(cudaSetDevice(device));
+        auto* e = new fsk_engine();
+        e->device = device;
+        FSKB_CUDA(cudaStreamCreateWithFlags(&e->own, cudaStreamNonBlocking));
+        FSKB_CUDA(cudaMalloc(reinterpret_cast<void**>(&e->flags), 2 * sizeof(int)));
+        FSKB_CUDA(cudaMemset(e->flags, 0, 2 * sizeof(int)));
+        e->P.upload(src, tgt, nullptr, e->own);
+        enable_tensor_path(e->P, mode);
+        FSKB_CUDA(cudaStreamSynchronize(e->own));
+        *out = e;
+    });
+}
+
+void fsk_engine_destroy(fsk_engine* e) {
+    if (!e) return;
+    cudaSetDevice(e->device);
+    cudaStreamSynchronize(e->own);
+    e->P.tc.reset();
+    e->P.src = DevSide<float>();
+    e->P.tgt = DevSide<float>();
+    cudaStreamSynchronize(e->own);
+    cudaFree(e->flags);
+    cudaStreamDestroy(e->own);
+    delete e;
+}
+
+int fsk_engine_set_eps(fsk_engine* e, double eps) {
+    return eguard([&] {
+        if (!(eps > 0.0)) throw ValidationFailure("eps must be positive");
+        e->eps = eps;
+        e->P.s = e->own;
+        if (e->P.tc) e->P.tc->set_eps(e->P, eps);
+        FSKB_CUDA(cudaStreamSynchronize(e->own));
+    });
+}
+
+int fsk_engine_bind_potentials(fsk_engine* e, float* f_dev, float* g_dev) {
+    e->f = f_dev;
+    e->g = g_dev;
+    return FSK_OK;
+}
+
+int fsk_engine_init_potentials(fsk_engine* e, void* stream) {
+    return eguard([&] {
+        cudaStream_t s = pick(e, stream);
+        launch_neg_sqnorm<float>(e->P.src.pts.get(), e->P.src.n, e->P.src.d, 1.0f, e->f, s);
+        launch_neg_sqnorm<float>(e->P.tgt.pts.get(), e->P.tgt.n, e->P.tgt.d, 1.0f, e->g, s);
+    });
+}
+
+int fsk_engine_half_step(fsk_engine* e, int side, int64_t row_begin, int64_t row_end,
+                         double* viol_accum, void* stream) {
+    return eguard([&] {
+        if (!e->f || !e->g) throw ValidationFailure("engine potentials not bound");
+        if (!(e->eps > 0.0)) throw ValidationFailure("engine eps not set");
+        const int64_t R = side == 0 ? e->P.src.n : e->P.tgt.n;
+        if (row_begin < 0 || row_end > R || row_begin > row_end)
+            throw ValidationFailure("engine row range out of bounds");
+        e->P.s = pick(e, stream);
+        const float eps = float(e->eps);
+        float* pot = side == 0 ? e->f : e->g;
+        const float* kpot = side == 0 ? e->g : e->f;
+        FinalizeArgs<float> fa{};
+        fa.eps = eps;
+        fa.flags = e->flags;
+        fa.out_pot = pot;
+        if (viol_accum) {
+            fa.old_pot = pot;
+            fa.w = side == 0 ? e->P.src.w.get() : e->P.tgt.w.get();
+            fa.viol = viol_accum;
+            fa.marg_flag = side == 0 ? kFlagNonFiniteRowMarginal : kFlagNonFiniteColMarginal;
+        }
+        half_step_rows<float>(e->P, side, kpot, eps, fa, row_begin, row_end);
+    });
+}
+
+int fsk_engine_grad(fsk_engine* e, int64_t row_begin, int64_t row_end, float* grad_dev,
+                    void* stream) {
+    return eguard([&] {
+        if (!e->f || !e->g) throw ValidationFailure("engine potentials not bound");
+        const int64_t n = e->P.src.n, d = e->P.src.d;
+        if (row_begin < 0 || row_end > n || row_begin > row_end)
+            throw ValidationFailure("engine row range out of bounds");
+        const int64_t R = row_end - row_begin;
+        if (R == 0) return;
+        cudaStream_t s = pick(e, stream);
+        e->P.s = s;
+        const float eps = float(e->eps);
+        DevBuf<float> lse(size_t(n), s), O(size_t(R * d), s);
+        FinalizeArgs<float> fa{};
+        fa.eps = eps;
+        fa.flags = e->flags;
+        fa.out_lse = lse.get();
+        half_step_rows<float>(e->P, 0, e->g, eps, fa, row_begin, row_end);
+        ScoreParams<float> sp = e->P.params(0, e->g, eps);
+        sp.Q += row_begin * d;
+        sp.R = R;
+        launch_apply<float>(sp, lse.get() + row_begin, e->P.tgt.pts.get(), d, nullptr, nullptr, 0,
+                            O.get(), s);
+        launch_grad_epilogue<float>(e->P.src.pts.get() + row_begin * d, O.get(),
+                                    e->P.src.w.get() + row_begin, e->f + row_begin,
+                                    lse.get() + row_begin, R, d, eps, grad_dev, e->flags, s);
+    });
+}
+
+int64_t fsk_engine_kernel_launches(const fsk_engine* e) {
+    (void)e;
+    return launch_counter();
+}
+
+const char* fsk_engine_path(const fsk_engine* e) { return tensor_path_name(e->P); }
+
+}  // extern "C"

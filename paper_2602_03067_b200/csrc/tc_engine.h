@@ -1,0 +1,43 @@
+// tcgen05 half-step engine (fp32-accurate split-fp16 tensor-core path).
+//
+// The X Y^T contraction of a half-step runs on the 5th-gen tensor cores as a
+// K = 3d + 16 fp16 GEMM (hi/lo split of both operands, three products, bias
+// folded in as three extra K columns), accumulated in fp32 in TMEM; the
+// epilogue warps keep the online max / sum-exp per row in registers and write
+// only the new potential. Operands are pre-formatted once per eps into
+// UMMA-canonical SW128/SW32 tile images so one bulk copy (TMA engine) moves a
+// whole key tile. See DESIGN.md "K1 lse_half_step (tcgen05)".
+#pragma once
+
+#include <cstdint>
+
+#include "common.h"
+#include "core_kernels.h"
+
+namespace fskb {
+
+template <typename T>
+struct DevProblem;
+
+class TcHalfStep {
+public:
+    // d must satisfy 1 <= d <= 64 (padded to 64 in the images).
+    explicit TcHalfStep(DevProblem<float>& P);
+    ~TcHalfStep();
+    static bool supported(int64_t d);
+
+    // (Re)builds the scaled key images for this eps (O((n+m) d) work).
+    void set_eps(DevProblem<float>& P, double eps);
+
+    // One half-step for rows [row_begin, row_end) of `side` (0: f from g over
+    // keys Y, 1: g from f over keys X). FinalizeArgs pointers address full-length
+    // vectors (row i of the side is element i).
+    void run(DevProblem<float>& P, int side, const float* kpot, float eps,
+             const FinalizeArgs<float>& fa, int64_t row_begin, int64_t row_end);
+
+private:
+    struct Impl;
+    Impl* impl_;
+};
+
+}  // namespace fskb
