@@ -1,0 +1,412 @@
+#!/usr/bin/env python3
+"""FlashSinkhorn B200 benchmark (BASELINE.json metric).
+
+Metric: Sinkhorn iterations/s at n = m = 2^20 (the "1M" config, SURVEY §0
+finding 4), d = 64, eps = 0.05 on 1-8 B200, one step = 10 alternating
+iterations + the gradient w.r.t. X (the fwd+grad unit of cfg3). Inputs are
+synthetic Gaussian clouds from fsk::Rng(1000) (X then Y), uniform weights,
+fp32 on device (the reference's Single-precision path), larger than L2.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Arms
+  default            the B200 engine: device-resident clouds + tcgen05 split-fp16
+                     half-steps, rows sharded over ranks, NCCL all-gather of the
+                     potentials after each half-step (paper_2602_03067_b200.sharded)
+  --impl reference   the reference's own CPU solver (oracle/_ref, compiled from
+                     /root/reference sources) timed on this host's cores on a
+                     bounded row/column slice of the same workload, extrapolated
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (n, m, d, eps, iterations per step)
+    "cfg3": (1 << 20, 1 << 20, 64, 0.05, 10),
+    "cfg2": (65536, 65536, 64, 0.05, 10),
+    "cfg1": (4096, 4096, 3, 0.1, 100),
+}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, indices):
+        self.indices = set(indices)
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = [r for r in self.rows if r[0].isdigit() and int(r[0]) in self.indices]
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for name, val in zip(names, r[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- inputs ------
+
+def make_inputs(n, m, d, seed=1000):
+    """fsk::Rng(seed).normal(): X (n x d) then Y (m x d), row-major."""
+    import paper_2602_03067_b200 as fsk
+    z = fsk.rng_normal(seed, (n + m) * d)
+    return z[: n * d].reshape(n, d), z[n * d:].reshape(m, d)
+
+
+# ------------------------------------------------------------ reference arm --
+
+_REF_INPUTS = {}
+
+
+def _reference_inputs(n, m, d):
+    key = (n, m, d)
+    if key not in _REF_INPUTS:
+        from oracle import rng_normal
+        z = rng_normal(1000, (n + m) * d)  # the same fsk::Rng(1000) stream as the GPU arm
+        X64, Y64 = z[: n * d].reshape(n, d), z[n * d:].reshape(m, d)
+        _REF_INPUTS[key] = (X64, Y64, X64.astype(np.float32), Y64.astype(np.float32))
+    return _REF_INPUTS[key]
+
+
+def reference_sample(n, m, d, eps, iters, threads=None):
+    """Times the reference's own CPU path on a bounded slice of the workload and
+    extrapolates to one full step (10 iterations + gradient).
+
+    * f half-step: update_f_hat_f32 (stream.cpp:437-443) for 64*T source rows
+      (one row block per worker thread) against all m targets; rows are
+      independent given g, so time scales by n / rows (a sliced call is
+      bit-identical to the same rows of a full call).
+    * g half-step: update_g_hat_f32 (stream.cpp:445-451) for 64*T target rows
+      against all n sources, scaled by m / rows.
+    * gradient: the SPEC composition (the reference ships no gradient code):
+      one f64 LSE pass for r (update_f_hat, 64*T rows x m) plus apply_plan(Y)
+      (stream.cpp:324-339, double only) on 64*T rows x 4096 targets, scaled by
+      (n / rows) and (n / rows)(m / 4096).
+    Times include the wrapper's copy of the inputs into fsk types (< 10%).
+    """
+    from oracle import Oracle
+
+    ref = Oracle("ref_fast")
+    if threads:
+        ref.set_num_threads(threads)
+    T = ref.num_threads()
+    rows = min(64 * T, n, m)
+    cols_apply = min(4096, m)
+    X64, Y64, Xf, Yf = _reference_inputs(n, m, d)
+    a = np.full(n, 1.0 / n, dtype=np.float32)
+    b = np.full(m, 1.0 / m, dtype=np.float32)
+    g0 = -(Y64 ** 2).sum(1)
+    f0 = -(X64 ** 2).sum(1)
+    t0 = time.perf_counter()
+    ref.update_f_hat_f32(Xf[:rows], a[:rows], Yf, b, g0.astype(np.float32), eps)
+    t_f = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ref.update_g_hat_f32(Xf, a, Yf[:rows], b[:rows], f0.astype(np.float32), eps)
+    t_g = time.perf_counter() - t0
+    a64 = np.full(rows, 1.0 / rows)
+    t0 = time.perf_counter()
+    ref.update_f_hat(X64[:rows], a64, Y64, np.full(m, 1.0 / m), g0, eps)
+    t_lse64 = time.perf_counter() - t0
+    Ysub = Y64[:cols_apply]
+    bsub = np.full(cols_apply, 1.0 / cols_apply)
+    gsub = -(Ysub ** 2).sum(1)
+    fsub = ref.update_f_hat(X64[:rows], a64, Ysub, bsub, gsub, eps)
+    t0 = time.perf_counter()
+    ref.apply_plan(X64[:rows], a64, Ysub, bsub, fsub, gsub, eps, Ysub)
+    t_apply = time.perf_counter() - t0
+    iter_s = t_f * n / rows + t_g * m / rows
+    grad_s = t_lse64 * n / rows + t_apply * (n / rows) * (m / cols_apply)
+    sample = (f"f32 half-steps on {rows} rows x all {m} (resp. {n}) columns, {T} threads; "
+              f"gradient = f64 LSE {rows} x {m} + apply_plan(Y) {rows} x {cols_apply}; "
+              f"extrapolated by n/rows, m/cols")
+    return dict(step_s=iters * iter_s + grad_s, iter_s=iter_s, grad_s=grad_s, threads=T,
+                sample=sample, so=str(ref.so_path.name), wall_s=t_f + t_g + t_lse64 + t_apply)
+
+
+def run_reference(args, cfgname):
+    n, m, d, eps, iters = CONFIGS[cfgname]
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    for _ in range(args.warmup):
+        reference_sample(n, m, d, eps, iters)
+    steps = [reference_sample(n, m, d, eps, iters) for _ in range(args.steps)]
+    step_s = statistics.median(s["step_s"] for s in steps)
+    value = iters / step_s
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "iterations/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (fsk::Rng(1000) Gaussian)",
+        "config": workload_config(cfgname),
+        "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": steps[0]["threads"],
+                         "kind": "reference", "sample": steps[0]["sample"],
+                         "library": steps[0]["so"], "iter_s": steps[0]["iter_s"],
+                         "grad_s": steps[0]["grad_s"]},
+        "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+METRIC = "Sinkhorn iterations/s (10 alternating iterations + grad_X per step), n=m=2^20, d=64"
+
+
+def workload_config(cfgname):
+    n, m, d, eps, iters = CONFIGS[cfgname]
+    return {"workload": f"{cfgname}: point-cloud EOT n=m={n}, d={d}, eps={eps}, "
+                        f"{iters} alternating iterations + gradient w.r.t. X per step",
+            "n": n, "m": m, "d": d, "eps": eps, "iterations_per_step": iters,
+            "precision": "fp32 contract (tcgen05 split-fp16 scores, fp32 accumulate)",
+            "l2": "inputs larger than L2 (operand images 2 x 288 MB per side)"}
+
+
+# --------------------------------------------------------------- B200 arm -----
+
+def run_b200(args, cfgname):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_03067_b200 as fsk
+    from paper_2602_03067_b200.sharded import ShardPlan, ShardedSinkhorn
+
+    n, m, d, eps, iters = CONFIGS[cfgname]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    X, Y = make_inputs(n, m, d)
+    a = np.full(n, 1.0 / n)
+    b = np.full(m, 1.0 / m)
+    eng = fsk.Engine(local, X, a, Y, b, mode=args.mode)
+    eng.set_eps(eps)
+    plan = ShardPlan(rank, world, n, m)
+    solver = ShardedSinkhorn(eng, plan, torch.device("cuda", local),
+                             dist if world > 1 else None)
+    lo, hi = plan.f_bounds[rank]
+    grad = torch.empty((max(hi - lo, 1), d), dtype=torch.float32, device="cuda")
+    sptr = stream.cuda_stream
+
+    # the engine launches on its own stream unless given one: pass torch's
+    def half(side, lo_, hi_):
+        eng.half_step(side, lo_, hi_, 0, sptr)
+
+    def step(events=None):
+        eng.init_potentials(sptr)
+        for _ in range(iters):
+            flo, fhi = plan.f_bounds[rank]
+            if events is not None:
+                events.append(torch.cuda.Event(enable_timing=True))
+                events[-1].record(stream)
+            half(0, flo, fhi)
+            if events is not None:
+                events.append(torch.cuda.Event(enable_timing=True))
+                events[-1].record(stream)
+            solver._gather(solver.f, plan.f_per)
+            glo, ghi = plan.g_bounds[rank]
+            half(1, glo, ghi)
+            solver._gather(solver.g, plan.g_per)
+        eng.grad(lo, hi, grad.data_ptr(), sptr)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler([local]) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    launches0 = fsk.Engine.launches()
+    events = []
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    start.record(stream)
+    for _ in range(args.steps):
+        step(events)
+    stop.record(stream)
+    torch.cuda.synchronize()
+    launches = fsk.Engine.launches() - launches0
+    clocks = sampler.stop() if sampler else None
+    elapsed = start.elapsed_time(stop) / 1e3
+    half_ms = [events[i].elapsed_time(events[i + 1]) for i in range(0, len(events), 2)]
+    t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed = float(t.item())
+
+    # end-to-end through the public C ABI with host buffers (N = 1), or the
+    # engine with host upload + gradient download per rank (N > 1)
+    e2e = None
+    if args.e2e:
+        if world == 1:
+            t0 = time.perf_counter()
+            out = fsk.sinkhorn_solve(X, a, Y, b, eps=eps, max_iters=iters, precision="single",
+                                     grad=True)
+            e2e_s = time.perf_counter() - t0
+            e2e = {"value": iters / e2e_s, "unit": "iterations/s",
+                   "h2d_bytes_per_step": int(X.nbytes + Y.nbytes + a.nbytes + b.nbytes),
+                   "d2h_bytes_per_step": int(out["grad"].nbytes + out["f_hat"].nbytes +
+                                             out["g_hat"].nbytes),
+                   "api": "fsk_sinkhorn_solve_grad (C ABI, host double buffers)",
+                   "loss": out["dual_cost"]}
+        else:
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            eng2 = fsk.Engine(local, X, a, Y, b, mode=args.mode)
+            eng2.set_eps(eps)
+            s2 = ShardedSinkhorn(eng2, plan, torch.device("cuda", local), dist)
+            s2.init()
+            s2.iterate(iters)
+            gh = torch.empty((max(hi - lo, 1), d), dtype=torch.float32, device="cuda")
+            s2.grad_shard(gh)
+            g_host = gh.cpu().numpy()
+            f_host = s2.f[:n].cpu().numpy()
+            torch.cuda.synchronize()
+            e2e_t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+            dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+            e2e = {"value": iters / float(e2e_t.item()), "unit": "iterations/s",
+                   "h2d_bytes_per_step": int(X.nbytes + Y.nbytes + a.nbytes + b.nbytes),
+                   "d2h_bytes_per_step": int(g_host.nbytes + f_host.nbytes),
+                   "api": "fsk_engine_* (C ABI) per rank, host double buffers"}
+            eng2.close()
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    pk, pk_kind = peaks()
+    # roofline of the dominant kernel (tc_lse_kernel): algorithmic FLOPs of one
+    # half-step launch over this rank's rows, W_dot = 2 n_rows m d
+    rows0 = plan.f_bounds[0][1] - plan.f_bounds[0][0]
+    hs = sorted(half_ms)
+    med_half = hs[len(hs) // 2] / 1e3
+    w_dot = 2.0 * rows0 * m * d
+    achieved = w_dot / med_half / 1e12
+    peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    sm_clk = (clocks or {}).get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)
+    exp_floor = rows0 * m / (16.0 * 148 * sm_clk * 1e6)
+    mma_floor = 2.0 * rows0 * m * (3 * 64 + 16) / (peak * 1e12)
+    step_s = elapsed / args.steps
+    value = iters * args.steps / elapsed
+    line = {
+        "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (fsk::Rng(1000) Gaussian clouds, uniform weights)",
+        "config": dict(workload_config(cfgname), parallelism=f"row-shard x{world} + NCCL "
+                       "all-gather of potentials" if world > 1 else "1 GPU",
+                       path=eng.path),
+        "half_step_ms": med_half * 1e3,
+        "grad_ms": None,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "tc_lse_kernel (+bias/finalize, CUDA events per half-step)",
+                     "algorithmic": "W_dot = 2 n m d per half-step (d = 64)",
+                     "peak_source": f"{pk_kind} bf16_tflops_sustained (MEASURED_PEAKS.json)",
+                     "mode_floor_ms": max(exp_floor, mma_floor) * 1e3,
+                     "exp_floor_ms": exp_floor * 1e3, "mma_floor_ms": mma_floor * 1e3,
+                     "frac_of_mode_floor": max(exp_floor, mma_floor) / med_half},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "e2e": e2e,
+    }
+    if world == 1 and args.cpu_baseline:
+        try:
+            cb = reference_sample(n, m, d, eps, iters)
+            line["cpu_baseline"] = {"value": iters / cb["step_s"], "unit": "iterations/s",
+                                    "cores": cb["threads"], "kind": "reference",
+                                    "sample": cb["sample"], "library": cb["so"]}
+        except Exception as exc:  # reference library absent on this host
+            line["cpu_baseline"] = {"value": None, "unit": "iterations/s", "cores": None,
+                                    "kind": "reference", "sample": f"unavailable: {exc}"}
+    print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
+    ap.add_argument("--mode", default="auto", choices=["auto", "tensor", "fma"])
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args, args.config)
+    return run_b200(args, args.config)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -101,6 +101,15 @@ class Oracle:
                 raise FileNotFoundError(f"{REF_CHECK_SO} not built (run oracle/build_ref.py)")
             self.lib = C.CDLL(str(REF_CHECK_SO))
             self.p = "ref_"
+        elif kind == "ref_fast":
+            # the reference's CMake flavour (-O3, FMA contraction), widest ISA the host has
+            so = REF_DIR / ("libfsk_ref_fast_v4.so" if _has_avx512() else "libfsk_ref_fast_v3.so")
+            if not so.exists():
+                raise FileNotFoundError(f"{so} not built (run oracle/build_ref.py)")
+            self.lib = C.CDLL(str(so))
+            self.p = "ref_"
+            self.so_path = so
+            self.lib.ref_num_threads.restype = C.c_int64
         else:
             raise ValueError(kind)
         getattr(self.lib, self.p + "last_error").restype = C.c_char_p
@@ -336,5 +345,27 @@ class Oracle:
             os.environ["OMP_NUM_THREADS"] = str(n)
 
 
+    def num_threads(self) -> int:
+        if self.kind.startswith("ref"):
+            self.lib.ref_num_threads.restype = C.c_int64
+            return int(self.lib.ref_num_threads())
+        return os.cpu_count() or 1
+
+
 def uniform(n: int) -> np.ndarray:
     return np.full(n, 1.0 / n)
+
+
+def _has_avx512() -> bool:
+    try:
+        return " avx512f" in Path("/proc/cpuinfo").read_text()
+    except OSError:
+        return False
+
+
+def rng_normal(seed: int, count: int) -> np.ndarray:
+    """fsk::Rng(seed).normal() x count via the C restatement (rng.hpp:44-57)."""
+    lib = C.CDLL(str(build()))
+    out = np.empty(count)
+    lib.fo_rng_normal_fill(C.c_uint64(seed), C.c_void_p(out.ctypes.data), C.c_int64(count))
+    return out

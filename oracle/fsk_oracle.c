@@ -783,3 +783,54 @@ int fo_sinkhorn_solve(const fo_measure* src, const fo_measure* tgt, const fo_cos
     free(c);
     return st;
 }
+
+/* ---- seeded inputs: xoshiro256** / splitmix64 / Box-Muller (rng.hpp:12-57) ---- */
+static uint64_t rotl64(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+
+void fo_rng_normal_fill(uint64_t seed, double* out, int64_t count) {
+    uint64_t s[4], x = seed;
+    for (int i = 0; i < 4; ++i) {
+        x += 0x9e3779b97f4a7c15ULL;
+        uint64_t z = x;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+        s[i] = z ^ (z >> 31);
+    }
+    int has_spare = 0;
+    double spare = 0.0;
+    for (int64_t k = 0; k < count; ++k) {
+        if (has_spare) {
+            has_spare = 0;
+            out[k] = spare;
+            continue;
+        }
+        double u[2];
+        for (int q = 0; q < 2; ++q) {
+            const uint64_t r = rotl64(s[1] * 5, 7) * 9;
+            const uint64_t t = s[1] << 17;
+            s[2] ^= s[0];
+            s[3] ^= s[1];
+            s[1] ^= s[2];
+            s[0] ^= s[3];
+            s[2] ^= t;
+            s[3] = rotl64(s[3], 45);
+            u[q] = (double)(r >> 11) * 0x1.0p-53;
+        }
+        while (u[0] <= 0.0) {
+            const uint64_t r = rotl64(s[1] * 5, 7) * 9;
+            const uint64_t t = s[1] << 17;
+            s[2] ^= s[0];
+            s[3] ^= s[1];
+            s[1] ^= s[2];
+            s[0] ^= s[3];
+            s[2] ^= t;
+            s[3] = rotl64(s[3], 45);
+            u[0] = (double)(r >> 11) * 0x1.0p-53;
+        }
+        const double rad = sqrt(-2.0 * log(u[0]));
+        const double ang = 2.0 * 3.14159265358979323846 * u[1];
+        spare = rad * sin(ang);
+        has_spare = 1;
+        out[k] = rad * cos(ang);
+    }
+}

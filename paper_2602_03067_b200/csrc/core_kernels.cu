@@ -140,8 +140,8 @@ __global__ void __launch_bounds__(NT) lse_partial_kernel(ScoreParams<T> P, int64
             const T so = __shfl_xor_sync(0xffffffffu, s[ii], off);
             const T M = fmax(m[ii], mo);
             T acc = T(0);
-            if (m[ii] != ninf<T>()) acc += s[ii] * dexp(m[ii] - M);
-            if (mo != ninf<T>()) acc += so * dexp(mo - M);
+            if (m[ii] != ninf<T>()) acc += s[ii] * dexp(break_lse ? M - m[ii] : m[ii] - M);
+            if (mo != ninf<T>()) acc += so * dexp(break_lse ? M - mo : mo - M);
             m[ii] = M;
             s[ii] = acc;
         }
@@ -164,7 +164,7 @@ __global__ void lse_finalize_kernel(const T* __restrict__ part_m, const T* __res
         T S = T(0);
         for (int k = 0; k < splits; ++k) {
             const T mk = part_m[k * R + i];
-            if (mk != ninf<T>()) S += part_s[k * R + i] * dexp(mk - M);
+            if (mk != ninf<T>()) S += part_s[k * R + i] * dexp(a.break_lse ? M - mk : mk - M);
         }
         const T lse = M + dlog(S);
         if (a.out_lse) a.out_lse[i] = lse;
@@ -174,13 +174,14 @@ __global__ void lse_finalize_kernel(const T* __restrict__ part_m, const T* __res
             atomicOr(a.flags, kFlagNonFinitePotential);
             if (a.bad_iter) atomicMin(a.bad_iter, a.iter);
         }
-        if (a.out_pot) a.out_pot[i] = a.sym_old ? T(0.5) * a.sym_old[i] + T(0.5) * pot : pot;
+        // marginals read old_pot before out_pot is written (they may alias)
         if (a.out_marg || a.viol) {
             const T r = a.w[i] * dexp((a.old_pot[i] - pot) * (T(1) / a.eps));
             if (!isfinite(r)) atomicOr(a.flags, a.marg_flag);
             if (a.out_marg) a.out_marg[i] = r;
             vsum = fabs(double(r) - double(a.w[i]));
         }
+        if (a.out_pot) a.out_pot[i] = a.sym_old ? T(0.5) * a.sym_old[i] + T(0.5) * pot : pot;
     }
     if (a.viol) {
         for (int off = 16; off >= 1; off >>= 1) vsum += __shfl_xor_sync(0xffffffffu, vsum, off);
@@ -363,7 +364,9 @@ void launch_lse(const ScoreParams<T>& P, int splits, T* part_m, T* part_s, cudaS
 template <typename T>
 void launch_lse_finalize(const T* part_m, const T* part_s, int splits, int64_t R,
                          const FinalizeArgs<T>& a, cudaStream_t s) {
-    lse_finalize_kernel<T><<<blocks_for(R), 256, 0, s>>>(part_m, part_s, splits, R, a);
+    FinalizeArgs<T> fa = a;
+    fa.break_lse = break_lse_flag() ? 1 : 0;
+    lse_finalize_kernel<T><<<blocks_for(R), 256, 0, s>>>(part_m, part_s, splits, R, fa);
     FSKB_CUDA(cudaGetLastError());
     count_launch();
 }

@@ -56,6 +56,7 @@ struct FinalizeArgs {
     int* flags;
     int* bad_iter;       // nullable: atomicMin(iter) on a non-finite potential
     int iter;
+    int break_lse;       // negative control (set by the launchers)
 };
 
 // Number of column splits used for R rows (fills the machine when R is small).

@@ -1,24 +1,616 @@
-// placeholder: replaced by the tcgen05 implementation
+// tcgen05 split-fp16 half-step (K1 in DESIGN.md) for 1 <= d <= 64.
+//
+// Score of row i against key j, in log2 units (t = log2(e) S):
+//     t_ij = c <x_i, y_j> + b_j,   c = 2 s log2(e) / eps,  b_j = log2(e)(g_j/eps + log w_j)
+// computed on the tensor cores as ONE fp32-accumulated GEMM over three fp16
+// products plus the bias:
+//     acc_ij = <xh_i, kh_j> + <xl_i, kh_j> + <xh_i, kl_j> + 2048 p0_j + p1_j + p2_j / 2048
+// with x 2^-eq = xh + xl and c y 2^-ek = kh + kl (fp16 hi/lo split of the
+// scaled fp32 values) and b 2^-E = 2048 p0 + p1 + p2/2048 (three fp16 pieces,
+// ~33 bits). t = acc 2^E, E = eq + ek. The dropped xl.kl term is ~2^-22
+// relative: fp32-grade scores at the fp16 tensor rate (3.25x the MMA work of
+// a single fp16 pass instead of 3x at half rate for 3xTF32).
+//
+// Operand images are pre-formatted in HBM in the exact UMMA K-major layouts
+// (SW128 for the 64-wide hi/lo chunks, SW32 for the 16-wide bias chunk), so a
+// whole 128-key tile (36 KB) moves with two bulk copies on one mbarrier.
+//
+// Kernel shape: persistent, one CTA per SM, 10 warps:
+//   warp 0  producer: bulk copies (TMA engine) of Q pairs and a 4-stage key ring
+//   warp 1  MMA issuer (single thread) + TMEM owner: 2 query tiles x 2 TMEM
+//           buffers x 128 fp32 columns = all 512 TMEM columns
+//   warps 2..9 epilogue: one thread per query row; tcgen05.ld 128 scores,
+//           release TMEM, online max / sum-exp (ex2) with a double running sum.
+// Work items = (query-tile pair, key split); partial (max, sum) per row and
+// split go to HBM and a tiny finalize kernel applies the FinalizeArgs
+// epilogues (potential, symmetric average, LSE, marginals, violation).
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "common.h"
 #include "device_ops.h"
 #include "tc_engine.h"
 
 namespace fskb {
 
-struct TcHalfStep::Impl {};
+namespace {
 
-bool TcHalfStep::supported(int64_t) { return false; }
-TcHalfStep::TcHalfStep(DevProblem<float>&) : impl_(nullptr) {}
-TcHalfStep::~TcHalfStep() {}
-void TcHalfStep::set_eps(DevProblem<float>&, double) {}
-void TcHalfStep::run(DevProblem<float>&, int, const float*, float, const FinalizeArgs<float>&,
-                     int64_t, int64_t) {
-    throw CudaFailure("tensor path unavailable");
+constexpr int TILE = 128;                 // rows per query tile / keys per key tile
+constexpr int DPAD = 64;                  // padded feature dim (one SW128 chunk)
+constexpr uint32_t CHUNK = TILE * 128;    // 16 KB: 128 rows x 64 fp16
+constexpr uint32_t QTILE = 2 * CHUNK;     // hi + lo
+constexpr uint32_t BIAS = TILE * 32;      // 4 KB: 128 rows x 16 fp16 (SW32)
+constexpr uint32_t KSTAGE = 2 * CHUNK + BIAS;  // 36 KB
+constexpr int STAGES = 4;
+constexpr int NUM_WARPS = 10;
+constexpr int NUM_THREADS = NUM_WARPS * 32;
+constexpr uint32_t OFF_Q = 0;
+constexpr uint32_t OFF_ONES = 2 * QTILE;                       // 64 KB
+constexpr uint32_t OFF_K = OFF_ONES + BIAS;                    // 68 KB
+constexpr uint32_t OFF_BAR = OFF_K + STAGES * KSTAGE;          // 212 KB
+constexpr uint32_t SMEM_BYTES = OFF_BAR + 256 + 1024;          // + barriers + align slack
+constexpr float kOnesW0 = 2048.0f, kOnesW2 = 1.0f / 2048.0f;
+
+// idesc for kind::f16: D f32 (bits 4-5 = 1), A/B f16 (0), K-major, N = 128, M = 128
+constexpr uint32_t IDESC = (1u << 4) | (uint32_t(TILE >> 3) << 17) | (uint32_t(TILE >> 4) << 24);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor, K-major. layout 2 = SWIZZLE_128B (SBO 1024),
+// 6 = SWIZZLE_32B (SBO 256); LBO unused for swizzled K-major; version 1.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t sbo, uint32_t layout) {
+    uint64_t d = uint64_t((saddr & 0x3FFFFu) >> 4);
+    d |= uint64_t(1) << 16;
+    d |= uint64_t(sbo >> 4) << 32;
+    d |= uint64_t(1) << 46;
+    d |= uint64_t(layout) << 61;
+    return d;
+}
+
+__device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t acc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(IDESC), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+        : "memory");
+}
+
+#define TMEM_LD32(addr, r)                                                                       \
+    asm volatile(                                                                                \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
+        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"       \
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),    \
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),             \
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),          \
+          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),          \
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),          \
+          "=r"(r[31])                                                                            \
+        : "r"(addr))
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+struct TcParams {
+    const uint8_t* qimg;    // query tile images (hi+lo per 128-row tile)
+    const uint8_t* kimg;    // key tile images (hi+lo per 128-key tile)
+    const uint8_t* kbias;   // key bias chunks (4 KB per key tile)
+    int q_tile_begin, q_tiles;   // query tiles covering the row range
+    int k_tiles;                 // total key tiles
+    int splits;                  // key splits
+    int items;                   // ceil(q_tiles/2) * splits
+    int64_t row_begin, row_end;  // rows written
+    int64_t key_valid;           // number of real keys
+    int64_t R;                   // total rows of this side (partial stride)
+    float acc_scale;             // 2^E
+    double* part_m;              // [splits][R] natural-log max
+    double* part_s;              // [splits][R] sum exp(S - max)
+    int break_lse;
+};
+
+__global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t* sbase = smem_raw + (base - raw);
+
+    const uint32_t bar0 = base + OFF_BAR;
+    auto kfull = [&](int s) { return bar0 + 8u * s; };
+    auto kempty = [&](int s) { return bar0 + 8u * (STAGES + s); };
+    const uint32_t qfull = bar0 + 8u * (2 * STAGES);
+    const uint32_t qempty = qfull + 8u;
+    auto accfull = [&](int b) { return qempty + 8u + 8u * b; };
+    auto accempty = [&](int b) { return qempty + 24u + 8u * b; };
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + OFF_BAR + 128);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    // constant "ones" chunk of the query operand: [2048, 1, 1/2048, 0...] per row (SW32)
+    for (int idx = threadIdx.x; idx < TILE * 16; idx += NUM_THREADS) {
+        const int r = idx >> 4, k = idx & 15;
+        const float v = k == 0 ? kOnesW0 : (k == 1 ? 1.0f : (k == 2 ? kOnesW2 : 0.0f));
+        const uint32_t off = r * 32 + ((((k >> 3) ^ ((r >> 2) & 1))) << 4) + (k & 7) * 2;
+        *reinterpret_cast<__half*>(sbase + OFF_ONES + off) = __float2half_rn(v);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(kfull(s), 1);
+            mbar_init(kempty(s), 1);
+        }
+        mbar_init(qfull, 1);
+        mbar_init(qempty, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(accfull(b), 1);
+            mbar_init(accempty(b), 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+            smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    const int units = (p.q_tiles + 1) / 2;
+    const int ktiles_per_split = (p.k_tiles + p.splits - 1) / p.splits;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int it = 0, lu = 0;
+            for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++lu) {
+                const int unit = item / p.splits, split = item % p.splits;
+                const int qt0 = p.q_tile_begin + 2 * unit;
+                const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
+                mbar_wait(qempty, (lu & 1) ^ 1);
+                mbar_expect_tx(qfull, nq * QTILE);
+                bulk_g2s(base + OFF_Q, p.qimg + size_t(qt0) * QTILE, nq * QTILE, qfull);
+                const int kt0 = split * ktiles_per_split;
+                const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
+                for (int kt = kt0; kt < kt1; ++kt, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    mbar_wait(kempty(s), ph ^ 1);
+                    mbar_expect_tx(kfull(s), KSTAGE);
+                    const uint32_t dst = base + OFF_K + s * KSTAGE;
+                    bulk_g2s(dst, p.kimg + size_t(kt) * QTILE, QTILE, kfull(s));
+                    bulk_g2s(dst + QTILE, p.kbias + size_t(kt) * BIAS, BIAS, kfull(s));
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            int it = 0, acc_it = 0, lu = 0;
+            for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++lu) {
+                const int unit = item / p.splits, split = item % p.splits;
+                const int qt0 = p.q_tile_begin + 2 * unit;
+                const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
+                mbar_wait(qfull, lu & 1);
+                tc_fence_after();
+                const int kt0 = split * ktiles_per_split;
+                const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
+                for (int kt = kt0; kt < kt1; ++kt, ++it, ++acc_it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    const int b = acc_it & 1;
+                    const uint32_t aph = (acc_it >> 1) & 1;
+                    mbar_wait(kfull(s), ph);
+                    mbar_wait(accempty(b), aph ^ 1);
+                    tc_fence_after();
+                    const uint32_t kst = base + OFF_K + s * KSTAGE;
+                    for (int t = 0; t < nq; ++t) {
+                        const uint32_t d_tmem = tmem + uint32_t((b * 2 + t) * TILE);
+                        const uint32_t qa = base + OFF_Q + t * QTILE;
+#pragma unroll
+                        for (int kk = 0; kk < DPAD / 16; ++kk) {
+                            const uint64_t ah = umma_desc(qa + kk * 32, 1024, 2);
+                            const uint64_t al = umma_desc(qa + CHUNK + kk * 32, 1024, 2);
+                            const uint64_t bh = umma_desc(kst + kk * 32, 1024, 2);
+                            const uint64_t bl = umma_desc(kst + CHUNK + kk * 32, 1024, 2);
+                            umma_f16(d_tmem, al, bh, kk > 0 ? 1u : 0u);
+                            umma_f16(d_tmem, ah, bl, 1u);
+                            umma_f16(d_tmem, ah, bh, 1u);
+                        }
+                        umma_f16(d_tmem, umma_desc(base + OFF_ONES, 256, 6),
+                                 umma_desc(kst + QTILE, 256, 6), 1u);
+                    }
+                    umma_commit(kempty(s));
+                    umma_commit(accfull(b));
+                }
+                umma_commit(qempty);
+            }
+        }
+    } else {
+        // epilogue: warps 2..9; query tile t = (warp-2)/4, TMEM lane quarter = warp % 4
+        const int t = (warp - 2) >> 2;
+        const int quarter = warp & 3;
+        const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
+        int acc_it = 0;
+        for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+            const int unit = item / p.splits, split = item % p.splits;
+            const int qt0 = p.q_tile_begin + 2 * unit;
+            const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
+            const int kt0 = split * ktiles_per_split;
+            const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
+            float M = -INFINITY;
+            double S = 0.0;
+            for (int kt = kt0; kt < kt1; ++kt, ++acc_it) {
+                const int b = acc_it & 1;
+                const uint32_t aph = (acc_it >> 1) & 1;
+                mbar_wait(accfull(b), aph);
+                tc_fence_after();
+                uint32_t v[128];
+                if (t < nq) {
+                    const uint32_t a0 = tmem + lane_addr + uint32_t((b * 2 + t) * TILE);
+                    TMEM_LD32(a0 + 0, (v + 0));
+                    TMEM_LD32(a0 + 32, (v + 32));
+                    TMEM_LD32(a0 + 64, (v + 64));
+                    TMEM_LD32(a0 + 96, (v + 96));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(accempty(b));
+                if (t >= nq) continue;
+                // mask padded keys of the last tile
+                const int64_t kbase = int64_t(kt) * TILE;
+                if (kbase + TILE > p.key_valid) {
+#pragma unroll
+                    for (int j = 0; j < 128; ++j)
+                        if (kbase + j >= p.key_valid) v[j] = __float_as_uint(-INFINITY);
+                }
+                float mx0 = __uint_as_float(v[0]), mx1 = __uint_as_float(v[1]);
+                float mx2 = __uint_as_float(v[2]), mx3 = __uint_as_float(v[3]);
+#pragma unroll
+                for (int j = 4; j < 128; j += 4) {
+                    mx0 = fmaxf(mx0, __uint_as_float(v[j]));
+                    mx1 = fmaxf(mx1, __uint_as_float(v[j + 1]));
+                    mx2 = fmaxf(mx2, __uint_as_float(v[j + 2]));
+                    mx3 = fmaxf(mx3, __uint_as_float(v[j + 3]));
+                }
+                const float umax = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * p.acc_scale;
+                if (umax > M) {
+                    if (S != 0.0) S *= double(ex2(p.break_lse ? umax - M : M - umax));
+                    M = umax;
+                }
+                if (M == -INFINITY) continue;
+                const float nm = -M;
+                float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+                for (int j = 0; j < 128; j += 4) {
+                    s0 += ex2(fmaf(__uint_as_float(v[j]), p.acc_scale, nm));
+                    s1 += ex2(fmaf(__uint_as_float(v[j + 1]), p.acc_scale, nm));
+                    s2 += ex2(fmaf(__uint_as_float(v[j + 2]), p.acc_scale, nm));
+                    s3 += ex2(fmaf(__uint_as_float(v[j + 3]), p.acc_scale, nm));
+                }
+                S += double((s0 + s1) + (s2 + s3));
+            }
+            const int64_t row = int64_t(qt0 + t) * TILE + quarter * 32 + lane;
+            if (t < nq && row >= p.row_begin && row < p.row_end) {
+                // natural-log partials: max_j S_ij = M ln2, sum_j exp(S_ij - max) = S
+                p.part_m[size_t(split) * p.R + row] = double(M) * 0.69314718055994530942;
+                p.part_s[size_t(split) * p.R + row] = S;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}
+
+__global__ void tc_finalize_kernel(const double* __restrict__ pm, const double* __restrict__ ps,
+                                   int splits, int64_t R, int64_t row_begin, int64_t row_end,
+                                   FinalizeArgs<float> a) {
+    const int64_t i = row_begin + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    double vsum = 0.0;
+    if (i < row_end) {
+        double M = -INFINITY;
+        for (int k = 0; k < splits; ++k) M = fmax(M, pm[size_t(k) * R + i]);
+        double S = 0.0;
+        for (int k = 0; k < splits; ++k) {
+            const double mk = pm[size_t(k) * R + i];
+            if (mk != -INFINITY) S += ps[size_t(k) * R + i] * exp(a.break_lse ? M - mk : mk - M);
+        }
+        const double lse = M + log(S);
+        if (a.out_lse) a.out_lse[i] = float(lse);
+        if (a.out_max) a.out_max[i] = float(M);
+        const double potd = -double(a.eps) * lse;
+        const float pot = float(potd);
+        if (!isfinite(pot)) {
+            atomicOr(a.flags, kFlagNonFinitePotential);
+            if (a.bad_iter) atomicMin(a.bad_iter, a.iter);
+        }
+        double r = 0.0, w = 0.0;
+        if (a.out_marg || a.viol) {
+            w = double(a.w[i]);
+            r = w * exp((double(a.old_pot[i]) - potd) / double(a.eps));
+            if (!isfinite(r)) atomicOr(a.flags, a.marg_flag);
+            if (a.out_marg) a.out_marg[i] = float(r);
+            vsum = fabs(r - w);
+        }
+        if (a.out_pot) a.out_pot[i] = a.sym_old ? 0.5f * a.sym_old[i] + 0.5f * pot : pot;
+    }
+    if (a.viol) {
+        for (int off = 16; off >= 1; off >>= 1) vsum += __shfl_xor_sync(0xffffffffu, vsum, off);
+        if ((threadIdx.x & 31) == 0 && vsum != 0.0) atomicAdd(a.viol, vsum);
+    }
+}
+
+// ---- operand images ------------------------------------------------------------
+
+// hi/lo fp16 split of (pts * scale) into SW128 K-major tile images.
+// One thread per (row, 8-element group).
+__global__ void build_split_image(const float* __restrict__ pts, int64_t R, int64_t d, float scale,
+                                  int64_t rows_padded, uint8_t* __restrict__ img) {
+    const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t row = gid >> 3;
+    const int grp = int(gid & 7);
+    if (row >= rows_padded) return;
+    __align__(16) __half hi[8], lo[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int64_t k = grp * 8 + e;
+        const float v = (row < R && k < d) ? pts[row * d + k] * scale : 0.0f;
+        const __half h = __float2half_rn(v);
+        hi[e] = h;
+        lo[e] = __float2half_rn(v - __half2float(h));
+    }
+    const int64_t tile = row / TILE;
+    const int r = int(row % TILE);
+    const size_t off = size_t(tile) * QTILE + size_t(r) * 128 + size_t((grp ^ (r & 7)) << 4);
+    *reinterpret_cast<uint4*>(img + off) = *reinterpret_cast<const uint4*>(hi);
+    *reinterpret_cast<uint4*>(img + off + CHUNK) = *reinterpret_cast<const uint4*>(lo);
+}
+
+// bias chunk: b_j 2^-E = 2048 p0 + p1 + p2 / 2048, b_j = log2(e) (pot_j / eps + log w_j)
+__global__ void build_bias(const float* __restrict__ pot, const float* __restrict__ logw,
+                           int64_t C, int64_t rows_padded, double eps, double inv_scale,
+                           uint8_t* __restrict__ img, int* flags) {
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= rows_padded) return;
+    __align__(16) __half pc[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) pc[e] = __float2half_rn(0.0f);
+    if (j < C) {
+        const double b =
+            1.4426950408889634074 * (double(pot[j]) / eps + double(logw[j])) * inv_scale;
+        const double p0 = double(__half2float(__double2half(b / 2048.0)));
+        const double r1 = b - 2048.0 * p0;
+        const double p1 = double(__half2float(__double2half(r1)));
+        const double r2 = (r1 - p1) * 2048.0;
+        pc[0] = __double2half(p0 / 1.0);
+        pc[1] = __double2half(p1);
+        pc[2] = __double2half(r2);
+        if (!isfinite(b) || fabs(b) > 1.3e8) atomicOr(flags, kFlagNonFinitePotential);
+    }
+    const int64_t tile = j / TILE;
+    const int r = int(j % TILE);
+    uint8_t* dst = img + size_t(tile) * BIAS + size_t(r) * 32;
+    const int x = (r >> 2) & 1;
+    *reinterpret_cast<uint4*>(dst + ((0 ^ x) << 4)) = *reinterpret_cast<const uint4*>(pc);
+    *reinterpret_cast<uint4*>(dst + ((1 ^ x) << 4)) = *reinterpret_cast<const uint4*>(pc + 8);
+}
+
+__global__ void absmax_kernel(const float* __restrict__ x, int64_t n, unsigned int* out) {
+    float m = 0.0f;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        m = fmaxf(m, fabsf(x[i]));
+    for (int off = 16; off >= 1; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+}
+
+float device_absmax(const float* x, int64_t n, cudaStream_t s) {
+    DevBuf<unsigned int> m(1, s);
+    m.zero();
+    absmax_kernel<<<256, 256, 0, s>>>(x, n, m.get());
+    FSKB_CUDA(cudaGetLastError());
+    count_launch();
+    unsigned int h = 0;
+    m.download(&h, 1);
+    FSKB_CUDA(cudaStreamSynchronize(s));
+    float f;
+    std::memcpy(&f, &h, 4);
+    return f;
+}
+
+// exponent e such that max|v| * 2^-e lies in [128, 256)
+int scale_exponent(double maxabs) {
+    if (!(maxabs > 0.0) || !std::isfinite(maxabs)) return 0;
+    return int(std::floor(std::log2(maxabs))) - 7;
+}
+
+}  // namespace
+
+struct TcHalfStep::Impl {
+    int64_t rows_pad[2] = {0, 0};   // padded rows of each side's cloud (0: X, 1: Y)
+    int64_t npts[2] = {0, 0};
+    int eq[2] = {0, 0};             // query scale exponent of cloud (0: X, 1: Y)
+    float maxabs[2] = {0.f, 0.f};
+    DevBuf<uint8_t> qimg[2];        // query images of X (side 0) and Y (side 1)
+    DevBuf<uint8_t> kimg[2];        // key images for side (0: c Y, 1: c X)
+    DevBuf<uint8_t> kbias[2];
+    int ek[2] = {0, 0};
+    double eps = 0.0;
+};
+
+bool TcHalfStep::supported(int64_t d) { return d >= 1 && d <= DPAD; }
+
+TcHalfStep::TcHalfStep(DevProblem<float>& P) : impl_(new Impl()) {
+    static bool configured = false;
+    if (!configured) {
+        FSKB_CUDA(cudaFuncSetAttribute(tc_lse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(SMEM_BYTES)));
+        configured = true;
+    }
+    const DevSide<float>* sides[2] = {&P.src, &P.tgt};
+    for (int c = 0; c < 2; ++c) {
+        const DevSide<float>& sd = *sides[c];
+        impl_->npts[c] = sd.n;
+        impl_->rows_pad[c] = (sd.n + TILE - 1) / TILE * TILE;
+        impl_->maxabs[c] = device_absmax(sd.pts.get(), sd.n * sd.d, P.s);
+        impl_->eq[c] = scale_exponent(impl_->maxabs[c]);
+        impl_->qimg[c].alloc(size_t(impl_->rows_pad[c] / TILE) * QTILE, P.s);
+        const int64_t groups = impl_->rows_pad[c] * 8;
+        build_split_image<<<unsigned((groups + 255) / 256), 256, 0, P.s>>>(
+            sd.pts.get(), sd.n, sd.d, std::ldexp(1.0f, -impl_->eq[c]), impl_->rows_pad[c],
+            impl_->qimg[c].get());
+        FSKB_CUDA(cudaGetLastError());
+        count_launch();
+    }
+}
+
+TcHalfStep::~TcHalfStep() { delete impl_; }
+
+void TcHalfStep::set_eps(DevProblem<float>& P, double eps) {
+    impl_->eps = eps;
+    const double c = 2.0 * P.fscale / eps * 1.4426950408889634074;
+    // side 0 (f-update): keys = Y (cloud 1); side 1 (g-update): keys = X (cloud 0)
+    for (int side = 0; side < 2; ++side) {
+        const int kc = side == 0 ? 1 : 0;
+        const DevSide<float>& ks = side == 0 ? P.tgt : P.src;
+        impl_->ek[side] = scale_exponent(double(impl_->maxabs[kc]) * c);
+        if (!impl_->kimg[side].get())
+            impl_->kimg[side].alloc(size_t(impl_->rows_pad[kc] / TILE) * QTILE, P.s);
+        if (!impl_->kbias[side].get())
+            impl_->kbias[side].alloc(size_t(impl_->rows_pad[kc] / TILE) * BIAS, P.s);
+        const int64_t groups = impl_->rows_pad[kc] * 8;
+        build_split_image<<<unsigned((groups + 255) / 256), 256, 0, P.s>>>(
+            ks.pts.get(), ks.n, ks.d, float(c * std::ldexp(1.0, -impl_->ek[side])),
+            impl_->rows_pad[kc], impl_->kimg[side].get());
+        FSKB_CUDA(cudaGetLastError());
+        count_launch();
+    }
+}
+
+void TcHalfStep::run(DevProblem<float>& P, int side, const float* kpot, float eps,
+                     const FinalizeArgs<float>& fa, int64_t row_begin, int64_t row_end) {
+    if (row_end <= row_begin) return;
+    Impl& I = *impl_;
+    const int qc = side == 0 ? 0 : 1, kc = side == 0 ? 1 : 0;
+    const DevSide<float>& ks = side == 0 ? P.tgt : P.src;
+    const int E = I.eq[qc] + I.ek[side];
+    const int k_tiles = int(I.rows_pad[kc] / TILE);
+    // per-half-step bias chunk
+    build_bias<<<unsigned((I.rows_pad[kc] + 255) / 256), 256, 0, P.s>>>(
+        kpot, ks.logw.get(), ks.n, I.rows_pad[kc], double(eps), std::ldexp(1.0, -E),
+        I.kbias[side].get(), fa.flags);
+    FSKB_CUDA(cudaGetLastError());
+    count_launch();
+
+    TcParams p{};
+    p.qimg = I.qimg[qc].get();
+    p.kimg = I.kimg[side].get();
+    p.kbias = I.kbias[side].get();
+    p.q_tile_begin = int(row_begin / TILE);
+    p.q_tiles = int((row_end + TILE - 1) / TILE) - p.q_tile_begin;
+    p.k_tiles = k_tiles;
+    const int units = (p.q_tiles + 1) / 2;
+    const int sms = num_sms();
+    // choose the key split that best fills the persistent grid
+    int best = 1;
+    double best_eff = 0.0;
+    for (int s = 1; s <= 16 && s <= std::max(1, k_tiles / 4); ++s) {
+        const double items = double(units) * s;
+        const double eff = items / (std::ceil(items / sms) * sms);
+        if (eff > best_eff + 0.02) {
+            best_eff = eff;
+            best = s;
+        }
+    }
+    p.splits = best;
+    p.items = units * p.splits;
+    p.row_begin = row_begin;
+    p.row_end = row_end;
+    p.key_valid = ks.n;
+    p.R = side == 0 ? P.src.n : P.tgt.n;
+    p.acc_scale = std::ldexp(1.0f, E);
+    p.break_lse = break_lse_flag() ? 1 : 0;
+    DevBuf<double> pm(size_t(p.splits) * size_t(p.R), P.s), ps(size_t(p.splits) * size_t(p.R), P.s);
+    p.part_m = pm.get();
+    p.part_s = ps.get();
+    const int grid = std::min(p.items, sms);
+    tc_lse_kernel<<<grid, NUM_THREADS, SMEM_BYTES, P.s>>>(p);
+    FSKB_CUDA(cudaGetLastError());
+    count_launch();
+    const int64_t rows = row_end - row_begin;
+    FinalizeArgs<float> fb = fa;
+    fb.break_lse = p.break_lse;
+    tc_finalize_kernel<<<unsigned((rows + 255) / 256), 256, 0, P.s>>>(
+        pm.get(), ps.get(), p.splits, p.R, row_begin, row_end, fb);
+    FSKB_CUDA(cudaGetLastError());
+    count_launch();
 }
 
 bool enable_tensor_path(DevProblem<float>& P, int mode) {
-    (void)P;
-    (void)mode;
-    return false;
+    if (mode == 1 || P.labeled) return false;
+    const int64_t d = P.src.d;
+    const bool shape_ok = TcHalfStep::supported(d);
+    if (mode == 2 && !shape_ok) throw ValidationFailure("tensor path supports 1 <= d <= 64");
+    // auto: the contraction is a real GEMM only from d >= 32 (north star: small-d
+    // point clouds stay on CUDA-core FMA)
+    if (mode == 0 && !(shape_ok && d >= 32)) return false;
+    P.tc = std::make_shared<TcHalfStep>(P);
+    return true;
 }
 
 const char* tensor_path_name(const DevProblem<float>& P) {

@@ -214,11 +214,20 @@ def test_numerical_error_on_overflow(fsk):
         fsk.apply_plan(X, w, X, w, [800.0, 800.0], [0.0, 0.0], 1.0, np.ones((2, 1)))
 
 
-def test_break_lse_negative_control(fsk, golden):
-    G = golden
+def test_break_lse_negative_control(fsk, port):
+    """Flipping the online rescale must break every multi-tile stream
+    (stream.cpp:81-87); our kernels stream 64-column tiles, so use m > 64."""
+    rng = np.random.default_rng(9)
+    X, Y = rng.normal(size=(64, 4)), rng.normal(size=(700, 4))
+    a, b = np.full(64, 1 / 64), np.full(700, 1 / 700)
+    g = rng.normal(size=700)
+    good = port.update_f_hat(X, a, Y, b, g, 0.1)
     fsk.debug_break_lse(True)
     try:
-        bad = fsk.update_f_hat(G["fu_X"], G["fu_a"], G["fu_Y"], G["fu_b"], G["fu_g"], 0.1)
+        bad = fsk.update_f_hat(X, a, Y, b, g, 0.1)
+        bad32 = fsk.update_f_hat_f32(X, a, Y, b, g, 0.1)
     finally:
         fsk.debug_break_lse(False)
-    assert np.abs(bad - G["fu_out"]).max() > 1e-6
+    assert np.abs(bad - good).max() > 1e-6
+    assert np.abs(bad32 - good).max() > 1e-3
+    assert np.abs(fsk.update_f_hat(X, a, Y, b, g, 0.1) - good).max() < 1e-12
