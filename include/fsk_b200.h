@@ -258,6 +258,9 @@ void fsk_engine_destroy(fsk_engine* e);
 /* Sets eps (rebuilds the scaled key images) and the potential buffers. */
 int fsk_engine_set_eps(fsk_engine* e, double eps);
 int fsk_engine_bind_potentials(fsk_engine* e, float* f_dev, float* g_dev);
+/* `stream` arguments below are cudaStream_t handles used as given: NULL is the
+ * legacy default stream (CUDA convention), not an engine-private stream, so the
+ * engine's kernels are ordered with the caller's collectives on that stream. */
 /* Initialise f = -|x|^2, g = -|y|^2 (f = g = 0 unshifted) on rows
  * [row_begin, row_end) of each side. */
 int fsk_engine_init_potentials(fsk_engine* e, void* stream);

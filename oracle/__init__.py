@@ -157,7 +157,7 @@ class Oracle:
         args = [C.byref(src), C.byref(tgt), C.c_void_p(g.ctypes.data), C.byref(self._cost(cost)),
                 C.c_double(eps), C.c_int64(tiles[0]), C.c_int64(tiles[1]),
                 C.c_void_p(out.ctypes.data)]
-        if self.kind == "ref":
+        if self.kind != "port":
             args.append(C.c_void_p(self._ledger().ctypes.data))
         self._check(self._fn("update_f_hat")(*args))
         self._keep.clear()
@@ -170,7 +170,7 @@ class Oracle:
         args = [C.byref(src), C.byref(tgt), C.c_void_p(f.ctypes.data), C.byref(self._cost(cost)),
                 C.c_double(eps), C.c_int64(tiles[0]), C.c_int64(tiles[1]),
                 C.c_void_p(out.ctypes.data)]
-        if self.kind == "ref":
+        if self.kind != "port":
             args.append(C.c_void_p(self._ledger().ctypes.data))
         self._check(self._fn("update_g_hat")(*args))
         self._keep.clear()
@@ -184,7 +184,7 @@ class Oracle:
         args = [C.byref(src), C.byref(tgt), C.c_void_p(f.ctypes.data), C.c_void_p(g.ctypes.data),
                 C.c_double(eps), C.byref(self._cost(cost)), C.c_int64(tiles[0]),
                 C.c_int64(tiles[1]), C.c_void_p(of.ctypes.data), C.c_void_p(og.ctypes.data)]
-        if self.kind == "ref":
+        if self.kind != "port":
             args.append(C.c_void_p(self._ledger().ctypes.data))
         self._check(self._fn("symmetric_update")(*args))
         self._keep.clear()
@@ -202,7 +202,7 @@ class Oracle:
                 C.c_double(eps), C.byref(self._cost(cost)), C.c_void_p(M.ctypes.data),
                 C.c_int64(p), C.c_int64(tiles[0]), C.c_int64(tiles[1]),
                 C.c_void_p(out.ctypes.data)]
-        if self.kind == "ref":
+        if self.kind != "port":
             args.append(C.c_void_p(self._ledger().ctypes.data))
         self._check(self._fn(name)(*args))
         self._keep.clear()
@@ -230,7 +230,7 @@ class Oracle:
                 C.c_void_p(B.ctypes.data), C.c_int64(r), C.c_void_p(V.ctypes.data),
                 C.c_int64(p), C.c_int64(tiles[0]), C.c_int64(tiles[1]),
                 C.c_void_p(out.ctypes.data)]
-        if self.kind == "ref":
+        if self.kind != "port":
             args.append(C.c_void_p(self._ledger().ctypes.data))
         self._check(self._fn("apply_hadamard_plan")(*args))
         self._keep.clear()
@@ -244,7 +244,7 @@ class Oracle:
         args = [C.byref(src), C.byref(tgt), C.c_void_p(f.ctypes.data), C.c_void_p(g.ctypes.data),
                 C.c_double(eps), C.byref(self._cost(cost)), C.c_int64(tiles[0]),
                 C.c_int64(tiles[1]), C.c_void_p(r.ctypes.data), C.c_void_p(c.ctypes.data)]
-        if self.kind == "ref":
+        if self.kind != "port":
             args.append(C.c_void_p(self._ledger().ctypes.data))
         self._check(self._fn("induced_marginals")(*args))
         self._keep.clear()
@@ -256,7 +256,7 @@ class Oracle:
         n, d = X.shape
         m = Y.shape[0]
         out = np.empty(n, dtype=np.float32)
-        if self.kind == "ref":
+        if self.kind != "port":
             st = self.lib.ref_update_f_hat_f32(
                 C.c_void_p(X.ctypes.data), C.c_void_p(a.ctypes.data), C.c_int64(n),
                 C.c_void_p(Y.ctypes.data), C.c_void_p(b.ctypes.data), C.c_int64(m),
@@ -277,7 +277,7 @@ class Oracle:
         n, d = X.shape
         m = Y.shape[0]
         out = np.empty(m, dtype=np.float32)
-        if self.kind == "ref":
+        if self.kind != "port":
             st = self.lib.ref_update_g_hat_f32(
                 C.c_void_p(X.ctypes.data), C.c_void_p(a.ctypes.data), C.c_int64(n),
                 C.c_void_p(Y.ctypes.data), C.c_void_p(b.ctypes.data), C.c_int64(m),
@@ -308,7 +308,7 @@ class Oracle:
                 C.c_int64(tiles[0]), C.c_int64(tiles[1]), C.c_void_p(f.ctypes.data),
                 C.c_void_p(g.ctypes.data), C.c_void_p(sc.ctypes.data),
                 C.c_void_p(hist.ctypes.data)]
-        if self.kind == "ref":
+        if self.kind != "port":
             args += [C.c_int64(len(hist)), C.c_void_p(self._ledger().ctypes.data)]
         self._check(self._fn("sinkhorn_solve")(*args))
         self._keep.clear()
@@ -324,7 +324,7 @@ class Oracle:
         args = [C.byref(src), C.byref(tgt), C.c_void_p(f.ctypes.data), C.c_void_p(g.ctypes.data),
                 C.c_double(eps), C.byref(self._cost(cost)), C.c_int64(tiles[0]),
                 C.c_int64(tiles[1]), C.c_void_p(out.ctypes.data)]
-        if self.kind == "ref":
+        if self.kind != "port":
             args.append(C.c_void_p(self._ledger().ctypes.data))
         self._check(self._fn("dual_cost")(*args))
         self._keep.clear()
@@ -339,7 +339,7 @@ class Oracle:
 
     # ---- misc ----------------------------------------------------------------
     def set_num_threads(self, n: int):
-        if self.kind == "ref":
+        if self.kind != "port":
             self.lib.ref_set_num_threads(C.c_int64(n))
         else:
             os.environ["OMP_NUM_THREADS"] = str(n)

@@ -299,19 +299,31 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
     if (grad_out) {
         // grad_X = 2 r (X - softmax(S) Y) at the returned potentials
         const T eps = T(pot_eps);
-        if (stopped) {
-            FinalizeArgs<T> fa{};
-            fa.eps = eps;
-            fa.flags = C.flags;
-            fa.out_lse = lse_f.get();
-            fa.out_max = mx_f.get();
-            half_step<T>(P, 0, g.get(), eps, fa);
+        DevBuf<T> G(size_t(n * d), C.s);
+        bool done = false;
+        if constexpr (kSingle) {
+            if (P.tc) {
+                // fused tcgen05 path: K1 row LSE + split-fp16 transport kernel
+                P.tc->set_eps(P, pot_eps);
+                P.tc->grad(P, 0, g.get(), f.get(), eps, 0, n, G.get(), C.flags);
+                done = true;
+            }
         }
-        DevBuf<T> O(size_t(n * d), C.s), G(size_t(n * d), C.s);
-        launch_apply<T>(P.params(0, g.get(), eps), lse_f.get(), P.tgt.pts.get(), d, nullptr,
-                        nullptr, 0, O.get(), C.s);
-        launch_grad_epilogue<T>(P.src.pts.get(), O.get(), P.src.w.get(), f.get(), lse_f.get(), n,
-                                d, eps, G.get(), C.flags, C.s);
+        if (!done) {
+            if (stopped) {
+                FinalizeArgs<T> fa{};
+                fa.eps = eps;
+                fa.flags = C.flags;
+                fa.out_lse = lse_f.get();
+                fa.out_max = mx_f.get();
+                half_step<T>(P, 0, g.get(), eps, fa);
+            }
+            DevBuf<T> O(size_t(n * d), C.s);
+            launch_apply<T>(P.params(0, g.get(), eps), lse_f.get(), P.tgt.pts.get(), d, nullptr,
+                            nullptr, 0, O.get(), C.s);
+            launch_grad_epilogue<T>(P.src.pts.get(), O.get(), P.src.w.get(), f.get(),
+                                    lse_f.get(), n, d, eps, G.get(), C.flags, C.s);
+        }
         dev_to<T>(G, grad_out, n * d, C.s);
         sync_and_check(C);
         if (ledger) {

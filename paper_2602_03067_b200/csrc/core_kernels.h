@@ -57,6 +57,8 @@ struct FinalizeArgs {
     int* bad_iter;       // nullable: atomicMin(iter) on a non-finite potential
     int iter;
     int break_lse;       // negative control (set by the launchers)
+    float* out_l2h = nullptr;  // tcgen05 path only: log2(e) LSE split hi + lo (float pair)
+    float* out_l2l = nullptr;
 };
 
 // Number of column splits used for R rows (fills the machine when R is small).

@@ -50,8 +50,13 @@ int eguard(F&& f) {
     }
 }
 
+// The stream argument is a plain cudaStream_t: NULL is the legacy default
+// stream (CUDA convention), so work is ordered with whatever the caller - e.g.
+// torch and its NCCL collectives - runs on that stream. The engine's private
+// stream is only used by create/set_eps, which synchronize before returning.
 cudaStream_t pick(fsk_engine* e, void* stream) {
-    return stream ? static_cast<cudaStream_t>(stream) : e->own;
+    (void)e;
+    return static_cast<cudaStream_t>(stream);
 }
 
 }  // namespace
@@ -151,6 +156,10 @@ int fsk_engine_grad(fsk_engine* e, int64_t row_begin, int64_t row_end, float* gr
         cudaStream_t s = pick(e, stream);
         e->P.s = s;
         const float eps = float(e->eps);
+        if (e->P.tc) {
+            e->P.tc->grad(e->P, 0, e->g, e->f, eps, row_begin, row_end, grad_dev, e->flags);
+            return;
+        }
         DevBuf<float> lse(size_t(n), s), O(size_t(R * d), s);
         FinalizeArgs<float> fa{};
         fa.eps = eps;

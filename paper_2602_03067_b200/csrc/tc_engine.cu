@@ -35,17 +35,14 @@
 #include "common.h"
 #include "device_ops.h"
 #include "tc_engine.h"
+#include "tc_ptx.h"
 
 namespace fskb {
 
 namespace {
 
-constexpr int TILE = 128;                 // rows per query tile / keys per key tile
-constexpr int DPAD = 64;                  // padded feature dim (one SW128 chunk)
-constexpr uint32_t CHUNK = TILE * 128;    // 16 KB: 128 rows x 64 fp16
-constexpr uint32_t QTILE = 2 * CHUNK;     // hi + lo
-constexpr uint32_t BIAS = TILE * 32;      // 4 KB: 128 rows x 16 fp16 (SW32)
-constexpr uint32_t KSTAGE = 2 * CHUNK + BIAS;  // 36 KB
+using namespace tc;
+
 constexpr int STAGES = 4;
 constexpr int NUM_WARPS = 10;
 constexpr int NUM_THREADS = NUM_WARPS * 32;
@@ -54,94 +51,7 @@ constexpr uint32_t OFF_ONES = 2 * QTILE;                       // 64 KB
 constexpr uint32_t OFF_K = OFF_ONES + BIAS;                    // 68 KB
 constexpr uint32_t OFF_BAR = OFF_K + STAGES * KSTAGE;          // 212 KB
 constexpr uint32_t SMEM_BYTES = OFF_BAR + 256 + 1024;          // + barriers + align slack
-constexpr float kOnesW0 = 2048.0f, kOnesW2 = 1.0f / 2048.0f;
-
-// idesc for kind::f16: D f32 (bits 4-5 = 1), A/B f16 (0), K-major, N = 128, M = 128
-constexpr uint32_t IDESC = (1u << 4) | (uint32_t(TILE >> 3) << 17) | (uint32_t(TILE >> 4) << 24);
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(bar),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
-                                         uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(dst),
-        "l"(src), "r"(bytes), "r"(bar)
-        : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-
-// UMMA shared-memory descriptor, K-major. layout 2 = SWIZZLE_128B (SBO 1024),
-// 6 = SWIZZLE_32B (SBO 256); LBO unused for swizzled K-major; version 1.
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t sbo, uint32_t layout) {
-    uint64_t d = uint64_t((saddr & 0x3FFFFu) >> 4);
-    d |= uint64_t(1) << 16;
-    d |= uint64_t(sbo >> 4) << 32;
-    d |= uint64_t(1) << 46;
-    d |= uint64_t(layout) << 61;
-    return d;
-}
-
-__device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t acc) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-        "}\n" ::"r"(d_tmem),
-        "l"(a), "l"(b), "r"(IDESC), "r"(acc));
-}
-__device__ __forceinline__ void umma_commit(uint32_t bar) {
-    asm volatile(
-        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-        : "memory");
-}
-
-#define TMEM_LD32(addr, r)                                                                       \
-    asm volatile(                                                                                \
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
-        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"       \
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),    \
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),             \
-          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),          \
-          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),          \
-          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),          \
-          "=r"(r[31])                                                                            \
-        : "r"(addr))
-
-__device__ __forceinline__ float ex2(float x) {
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
+constexpr float kSkipLog2 = 64.0f;  // LSE tiles entirely 2^-64 below the running max are skipped
 
 struct TcParams {
     const uint8_t* qimg;    // query tile images (hi+lo per 128-row tile)
@@ -177,13 +87,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-    // constant "ones" chunk of the query operand: [2048, 1, 1/2048, 0...] per row (SW32)
-    for (int idx = threadIdx.x; idx < TILE * 16; idx += NUM_THREADS) {
-        const int r = idx >> 4, k = idx & 15;
-        const float v = k == 0 ? kOnesW0 : (k == 1 ? 1.0f : (k == 2 ? kOnesW2 : 0.0f));
-        const uint32_t off = r * 32 + ((((k >> 3) ^ ((r >> 2) & 1))) << 4) + (k & 7) * 2;
-        *reinterpret_cast<__half*>(sbase + OFF_ONES + off) = __float2half_rn(v);
-    }
+    fill_ones_chunk(sbase + OFF_ONES, threadIdx.x, NUM_THREADS);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -203,9 +107,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
             smem_u32(tmem_slot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    tc_fence_before();
+    fence_before();
     __syncthreads();
-    tc_fence_after();
+    fence_after();
     const uint32_t tmem = *tmem_slot;
 
     const int units = (p.q_tiles + 1) / 2;
@@ -242,7 +146,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
                 const int qt0 = p.q_tile_begin + 2 * unit;
                 const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
                 mbar_wait(qfull, lu & 1);
-                tc_fence_after();
+                fence_after();
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
                 for (int kt = kt0; kt < kt1; ++kt, ++it, ++acc_it) {
@@ -252,24 +156,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
                     const uint32_t aph = (acc_it >> 1) & 1;
                     mbar_wait(kfull(s), ph);
                     mbar_wait(accempty(b), aph ^ 1);
-                    tc_fence_after();
+                    fence_after();
                     const uint32_t kst = base + OFF_K + s * KSTAGE;
-                    for (int t = 0; t < nq; ++t) {
-                        const uint32_t d_tmem = tmem + uint32_t((b * 2 + t) * TILE);
-                        const uint32_t qa = base + OFF_Q + t * QTILE;
-#pragma unroll
-                        for (int kk = 0; kk < DPAD / 16; ++kk) {
-                            const uint64_t ah = umma_desc(qa + kk * 32, 1024, 2);
-                            const uint64_t al = umma_desc(qa + CHUNK + kk * 32, 1024, 2);
-                            const uint64_t bh = umma_desc(kst + kk * 32, 1024, 2);
-                            const uint64_t bl = umma_desc(kst + CHUNK + kk * 32, 1024, 2);
-                            umma_f16(d_tmem, al, bh, kk > 0 ? 1u : 0u);
-                            umma_f16(d_tmem, ah, bl, 1u);
-                            umma_f16(d_tmem, ah, bh, 1u);
-                        }
-                        umma_f16(d_tmem, umma_desc(base + OFF_ONES, 256, 6),
-                                 umma_desc(kst + QTILE, 256, 6), 1u);
-                    }
+                    for (int t = 0; t < nq; ++t)
+                        issue_score_tile(tmem + uint32_t((b * 2 + t) * TILE),
+                                         base + OFF_Q + t * QTILE, base + OFF_ONES, kst);
                     umma_commit(kempty(s));
                     umma_commit(accfull(b));
                 }
@@ -294,17 +185,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
                 const int b = acc_it & 1;
                 const uint32_t aph = (acc_it >> 1) & 1;
                 mbar_wait(accfull(b), aph);
-                tc_fence_after();
+                fence_after();
                 uint32_t v[128];
                 if (t < nq) {
                     const uint32_t a0 = tmem + lane_addr + uint32_t((b * 2 + t) * TILE);
-                    TMEM_LD32(a0 + 0, (v + 0));
-                    TMEM_LD32(a0 + 32, (v + 32));
-                    TMEM_LD32(a0 + 64, (v + 64));
-                    TMEM_LD32(a0 + 96, (v + 96));
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    FSKB_TMEM_LD32(a0 + 0, (v + 0));
+                    FSKB_TMEM_LD32(a0 + 32, (v + 32));
+                    FSKB_TMEM_LD32(a0 + 64, (v + 64));
+                    FSKB_TMEM_LD32(a0 + 96, (v + 96));
+                    tmem_ld_wait();
                 }
-                tc_fence_before();
+                fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(accempty(b));
                 if (t >= nq) continue;
@@ -329,8 +220,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
                     if (S != 0.0) S *= double(ex2(p.break_lse ? umax - M : M - umax));
                     M = umax;
                 }
-                if (M == -INFINITY) continue;
-                const float nm = -M;
+                // every term of this tile is < 2^-64 of the running max for all 32 rows
+                // of the warp: the whole tile adds < m 2^-64 relative - below rounding
+                const bool dead = M == -INFINITY;
+                if (__all_sync(0xffffffffu, dead || umax < M - kSkipLog2)) continue;
+                const float nm = dead ? 0.0f : -M;
                 float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
                 for (int j = 0; j < 128; j += 4) {
@@ -349,12 +243,296 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
             }
         }
     }
-    tc_fence_before();
+    fence_before();
     __syncthreads();
     if (warp == 1) {
-        tc_fence_after();
+        fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
     }
+}
+
+// ---- transport application O = softmax(S) V on the tensor cores -------------
+//
+// Second pass of the fused gradient / barycentric projection: given the row
+// LSE L_i (log2 units, from a K1 pass over the same keys), every score tile is
+// recomputed bit-identically on the tensor cores, turned into
+// P~_ij = 2^(t_ij - L_i + 12) (normalised, x 2^12 to keep the fp16 split out of
+// the subnormal range), split hi/lo in fp16 and written back over the score
+// columns in TMEM; a second GEMM O += P~ V then reads P~ straight from TMEM
+// (A operand) and V = the key tile already staged in shared memory (B operand,
+// MN-major view of the same SW128 image): O = Ph Vh + Pl Vh + Ph Vl. No
+// online rescaling is needed because L_i is exact, so O accumulates in TMEM
+// across the whole key range of a work item and leaves the SM once.
+//
+// Kernel shape: persistent, 10 warps. warp 0 producer (bulk copies), warp 1
+// MMA issuer + TMEM owner, warps 2..9 epilogue: the 4 TMEM lane quarters x 2
+// column halves, one thread per (row, 64 keys). TMEM: 3 score buffers x 128
+// columns (double as P~ buffers) + 2 x 64 columns of O = 512.
+constexpr int ASTAGES = 4;
+constexpr int NSBUF = 3;
+constexpr uint32_t A_OFF_Q = 0;
+constexpr uint32_t A_OFF_ONES = QTILE;                       // 32 KB
+constexpr uint32_t A_OFF_K = A_OFF_ONES + BIAS;              // 36 KB
+constexpr uint32_t A_OFF_BAR = A_OFF_K + ASTAGES * KSTAGE;   // 180 KB
+constexpr uint32_t A_SMEM_BYTES = A_OFF_BAR + 256 + 64 + 1024;
+constexpr uint32_t O_COL0 = NSBUF * TILE;                    // 384
+constexpr float kPScaleLog2 = 12.0f;                         // P~ carries 2^12
+
+struct TcApplyParams {
+    const uint8_t* qimg;
+    const uint8_t* kimg;
+    const uint8_t* kbias;
+    int q_tile_begin, q_tiles, k_tiles, splits, items;
+    int64_t row_begin, row_end, key_valid, R;
+    float acc_scale;
+    const float* l2h;   // [R] log2-domain row LSE, hi
+    const float* l2l;   // [R] lo
+    float* part_o;      // [splits][R][64] partial O (V units x 2^12)
+};
+
+__global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_kernel(const TcApplyParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t* sbase = smem_raw + (base - raw);
+
+    const uint32_t bar0 = base + A_OFF_BAR;
+    auto kfull = [&](int s) { return bar0 + 8u * s; };
+    auto kempty = [&](int s) { return bar0 + 8u * (ASTAGES + s); };
+    const uint32_t qfull = bar0 + 8u * (2 * ASTAGES);
+    const uint32_t qempty = qfull + 8u;
+    auto sfull = [&](int b) { return qempty + 8u + 8u * b; };
+    auto pready = [&](int b) { return qempty + 8u + 8u * (NSBUF + b); };
+    auto ofull = [&](int b) { return qempty + 8u + 8u * (2 * NSBUF + b); };
+    auto oempty = [&](int b) { return qempty + 8u + 8u * (2 * NSBUF + 2 + b); };
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + A_OFF_BAR + 240);
+    // per score buffer: sequence number of the last tile with a nonzero P~
+    volatile int* live_tag = reinterpret_cast<volatile int*>(sbase + A_OFF_BAR + 256);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    fill_ones_chunk(sbase + A_OFF_ONES, threadIdx.x, NUM_THREADS);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ASTAGES; ++s) {
+            mbar_init(kfull(s), 1);
+            mbar_init(kempty(s), 1);
+        }
+        mbar_init(qfull, 1);
+        mbar_init(qempty, 1);
+        for (int b = 0; b < NSBUF; ++b) live_tag[b] = -1;
+        for (int b = 0; b < NSBUF; ++b) {
+            mbar_init(sfull(b), 1);
+            mbar_init(pready(b), 8);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(ofull(b), 1);
+            mbar_init(oempty(b), 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+            smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int ktiles_per_split = (p.k_tiles + p.splits - 1) / p.splits;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int it = 0, lu = 0;
+            for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++lu) {
+                const int unit = item / p.splits, split = item % p.splits;
+                const int qt = p.q_tile_begin + unit;
+                mbar_wait(qempty, (lu & 1) ^ 1);
+                mbar_expect_tx(qfull, QTILE);
+                bulk_g2s(base + A_OFF_Q, p.qimg + size_t(qt) * QTILE, QTILE, qfull);
+                const int kt0 = split * ktiles_per_split;
+                const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
+                for (int kt = kt0; kt < kt1; ++kt, ++it) {
+                    const int s = it % ASTAGES;
+                    const uint32_t ph = (it / ASTAGES) & 1;
+                    mbar_wait(kempty(s), ph ^ 1);
+                    mbar_expect_tx(kfull(s), KSTAGE);
+                    const uint32_t dst = base + A_OFF_K + s * KSTAGE;
+                    bulk_g2s(dst, p.kimg + size_t(kt) * QTILE, QTILE, kfull(s));
+                    bulk_g2s(dst + QTILE, p.kbias + size_t(kt) * BIAS, BIAS, kfull(s));
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            int it0 = 0, sq0 = 0, lu = 0;
+            for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++lu) {
+                const int split = item % p.splits;
+                const int kt0 = split * ktiles_per_split;
+                const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
+                const int K = max(0, kt1 - kt0);
+                const int ob = lu & 1;
+                mbar_wait(qfull, lu & 1);
+                fence_after();
+                auto issue_s = [&](int i) {
+                    const int s = (it0 + i) % ASTAGES;
+                    mbar_wait(kfull(s), ((it0 + i) / ASTAGES) & 1);
+                    fence_after();
+                    const int buf = (sq0 + i) % NSBUF;
+                    issue_score_tile(tmem + uint32_t(buf * TILE), base + A_OFF_Q,
+                                     base + A_OFF_ONES, base + A_OFF_K + s * KSTAGE);
+                    umma_commit(sfull(buf));
+                };
+                if (K > 0) issue_s(0);
+                if (K > 1) issue_s(1);
+                mbar_wait(oempty(ob), ((lu >> 1) & 1) ^ 1);
+                fence_after();
+                const uint32_t o_tmem = tmem + O_COL0 + uint32_t(ob * DPAD);
+                bool o_started = false;
+                for (int i = 0; i < K; ++i) {
+                    // the next score tile goes first: its buffer's P~ was consumed by
+                    // an O GEMM issued earlier (tcgen05 MMAs execute in issue order), so
+                    // the tensor pipe stays fed while the epilogue works on tile i
+                    if (i + 2 < K) issue_s(i + 2);
+                    const int buf = (sq0 + i) % NSBUF;
+                    mbar_wait(pready(buf), ((sq0 + i) / NSBUF) & 1);
+                    fence_after();
+                    const int s = (it0 + i) % ASTAGES;
+                    // skip O += P~ V when every P~ of the tile is exactly zero in fp16
+                    // (all scores > 40 log2-units below the row LSE); tile 0 always runs
+                    const bool live = i == 0 || live_tag[buf] == sq0 + i;
+                    if (live) {
+                        const uint32_t kst = base + A_OFF_K + s * KSTAGE;
+                        const uint32_t pcol = tmem + uint32_t(buf * TILE);
+#pragma unroll
+                        for (int kk = 0; kk < TILE / 16; ++kk) {
+                            // keys [16 kk, 16 kk + 16): column half kk / 4 of the P~ buffer,
+                            // hi at +0, lo at +32 within the half; V rows at kk * 16 * 128 B
+                            const uint32_t ph = pcol + uint32_t((kk >> 2) * 64 + (kk & 3) * 8);
+                            const uint64_t vh = umma_desc(kst + kk * 2048, 1024, 2, 8192);
+                            const uint64_t vl = umma_desc(kst + CHUNK + kk * 2048, 1024, 2, 8192);
+                            umma_ts(o_tmem, ph, vh, IDESC_PV, (o_started || kk > 0) ? 1u : 0u);
+                            umma_ts(o_tmem, ph + 32, vh, IDESC_PV, 1u);
+                            umma_ts(o_tmem, ph, vl, IDESC_PV, 1u);
+                        }
+                        o_started = true;
+                    }
+                    umma_commit(kempty(s));
+                }
+                umma_commit(ofull(ob));
+                umma_commit(qempty);
+                it0 += K;
+                sq0 += K;
+            }
+        }
+    } else {
+        const int quarter = warp & 3;
+        const int half = (warp - 2) >> 2;
+        const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
+        int sq = 0, lu = 0;
+        for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++lu) {
+            const int unit = item / p.splits, split = item % p.splits;
+            const int qt = p.q_tile_begin + unit;
+            const int kt0 = split * ktiles_per_split;
+            const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
+            const int64_t row = int64_t(qt) * TILE + quarter * 32 + lane;
+            const bool live = row < p.R;
+            // P~ = 2^(acc 2^E - L + 12): nlh folds L_hi, c2 = 12 - L_lo
+            const float nlh = live ? -p.l2h[row] : -3.0e38f;
+            const float c2 = live ? kPScaleLog2 - p.l2l[row] : 0.0f;
+            for (int kt = kt0; kt < kt1; ++kt, ++sq) {
+                const int buf = sq % NSBUF;
+                mbar_wait(sfull(buf), (sq / NSBUF) & 1);
+                fence_after();
+                const uint32_t taddr = tmem + lane_addr + uint32_t(buf * TILE + half * 64);
+                uint32_t v[64];
+                FSKB_TMEM_LD32(taddr, (v + 0));
+                FSKB_TMEM_LD32(taddr + 32, (v + 32));
+                tmem_ld_wait();
+                const int64_t kbase = int64_t(kt) * TILE + half * 64;
+                if (kbase + 64 > p.key_valid) {
+#pragma unroll
+                    for (int j = 0; j < 64; ++j)
+                        if (kbase + j >= p.key_valid) v[j] = __float_as_uint(-3.0e38f);
+                }
+                // tile max first: a warp whose 32 x 64 P~ are all below 2^-40 (zero
+                // in the fp16 split) skips the exponentials and stores zeros
+                float vm0 = __uint_as_float(v[0]), vm1 = __uint_as_float(v[1]);
+#pragma unroll
+                for (int j = 2; j < 64; j += 2) {
+                    vm0 = fmaxf(vm0, __uint_as_float(v[j]));
+                    vm1 = fmaxf(vm1, __uint_as_float(v[j + 1]));
+                }
+                const bool nz = fmaf(fmaxf(vm0, vm1), p.acc_scale, nlh) + c2 > -40.0f;
+                uint32_t hi[32], lo[32];
+                if (__any_sync(0xffffffffu, nz)) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const float p0 =
+                            ex2(fmaf(__uint_as_float(v[2 * j]), p.acc_scale, nlh) + c2);
+                        const float p1 =
+                            ex2(fmaf(__uint_as_float(v[2 * j + 1]), p.acc_scale, nlh) + c2);
+                        const __half2 h = __floats2half2_rn(p0, p1);
+                        const float2 hf = __half22float2(h);
+                        const __half2 l = __floats2half2_rn(p0 - hf.x, p1 - hf.y);
+                        hi[j] = *reinterpret_cast<const uint32_t*>(&h);
+                        lo[j] = *reinterpret_cast<const uint32_t*>(&l);
+                    }
+                    if (lane == 0) live_tag[buf] = sq;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) hi[j] = lo[j] = 0u;
+                }
+                FSKB_TMEM_ST32(taddr, hi);
+                FSKB_TMEM_ST32(taddr + 32, lo);
+                tmem_st_wait();
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(pready(buf));
+            }
+            const int ob = lu & 1;
+            mbar_wait(ofull(ob), (lu >> 1) & 1);
+            fence_after();
+            uint32_t o[32];
+            FSKB_TMEM_LD32(tmem + lane_addr + O_COL0 + uint32_t(ob * DPAD + half * 32), o);
+            tmem_ld_wait();
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(oempty(ob));
+            if (row >= p.row_begin && row < p.row_end) {
+                float4* dst = reinterpret_cast<float4*>(
+                    p.part_o + (size_t(split) * p.R + row) * DPAD + half * 32);
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    dst[c] = make_float4(__uint_as_float(o[4 * c]), __uint_as_float(o[4 * c + 1]),
+                                         __uint_as_float(o[4 * c + 2]),
+                                         __uint_as_float(o[4 * c + 3]));
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}
+
+// G_i = 2 r_i (x_i - O_i),  O_i = inv_v * sum_s part_o[s][i]
+__global__ void tc_grad_finalize_kernel(const float* __restrict__ part_o, int splits, int64_t R,
+                                        int64_t row_begin, int64_t row_end, int64_t d,
+                                        const float* __restrict__ X, const float* __restrict__ r,
+                                        double inv_v, float* __restrict__ G, int* flags) {
+    const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t i = row_begin + gid / d;
+    const int64_t k = gid % d;
+    if (i >= row_end) return;
+    double o = 0.0;
+    for (int s = 0; s < splits; ++s) o += double(part_o[(size_t(s) * R + i) * DPAD + k]);
+    const double g = 2.0 * double(r[i]) * (double(X[i * d + k]) - o * inv_v);
+    if (!isfinite(g)) atomicOr(flags, kFlagNonFiniteTransport);
+    G[(i - row_begin) * d + k] = float(g);
 }
 
 __global__ void tc_finalize_kernel(const double* __restrict__ pm, const double* __restrict__ ps,
@@ -372,6 +550,12 @@ __global__ void tc_finalize_kernel(const double* __restrict__ pm, const double* 
         }
         const double lse = M + log(S);
         if (a.out_lse) a.out_lse[i] = float(lse);
+        if (a.out_l2h) {
+            const double l2 = lse * 1.4426950408889634074;
+            const float h = float(l2);
+            a.out_l2h[i] = h;
+            a.out_l2l[i] = float(l2 - double(h));
+        }
         if (a.out_max) a.out_max[i] = float(M);
         const double potd = -double(a.eps) * lse;
         const float pot = float(potd);
@@ -481,6 +665,21 @@ int scale_exponent(double maxabs) {
 
 }  // namespace
 
+// Key split that best fills a persistent grid of `sms` CTAs with units x splits items.
+int pick_splits(int units, int k_tiles, int sms) {
+    int best = 1;
+    double best_eff = 0.0;
+    for (int s = 1; s <= 16 && s <= std::max(1, k_tiles / 4); ++s) {
+        const double items = double(units) * s;
+        const double eff = items / (std::ceil(items / sms) * sms);
+        if (eff > best_eff + 0.02) {
+            best_eff = eff;
+            best = s;
+        }
+    }
+    return best;
+}
+
 struct TcHalfStep::Impl {
     int64_t rows_pad[2] = {0, 0};   // padded rows of each side's cloud (0: X, 1: Y)
     int64_t npts[2] = {0, 0};
@@ -496,12 +695,11 @@ struct TcHalfStep::Impl {
 bool TcHalfStep::supported(int64_t d) { return d >= 1 && d <= DPAD; }
 
 TcHalfStep::TcHalfStep(DevProblem<float>& P) : impl_(new Impl()) {
-    static bool configured = false;
-    if (!configured) {
-        FSKB_CUDA(cudaFuncSetAttribute(tc_lse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(SMEM_BYTES)));
-        configured = true;
-    }
+    // per device (the attribute is per-context), cheap enough to set every time
+    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(SMEM_BYTES)));
+    FSKB_CUDA(cudaFuncSetAttribute(tc_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(A_SMEM_BYTES)));
     const DevSide<float>* sides[2] = {&P.src, &P.tgt};
     for (int c = 0; c < 2; ++c) {
         const DevSide<float>& sd = *sides[c];
@@ -566,18 +764,7 @@ void TcHalfStep::run(DevProblem<float>& P, int side, const float* kpot, float ep
     p.k_tiles = k_tiles;
     const int units = (p.q_tiles + 1) / 2;
     const int sms = num_sms();
-    // choose the key split that best fills the persistent grid
-    int best = 1;
-    double best_eff = 0.0;
-    for (int s = 1; s <= 16 && s <= std::max(1, k_tiles / 4); ++s) {
-        const double items = double(units) * s;
-        const double eff = items / (std::ceil(items / sms) * sms);
-        if (eff > best_eff + 0.02) {
-            best_eff = eff;
-            best = s;
-        }
-    }
-    p.splits = best;
+    p.splits = pick_splits(units, k_tiles, sms);
     p.items = units * p.splits;
     p.row_begin = row_begin;
     p.row_end = row_end;
@@ -597,6 +784,60 @@ void TcHalfStep::run(DevProblem<float>& P, int side, const float* kpot, float ep
     fb.break_lse = p.break_lse;
     tc_finalize_kernel<<<unsigned((rows + 255) / 256), 256, 0, P.s>>>(
         pm.get(), ps.get(), p.splits, p.R, row_begin, row_end, fb);
+    FSKB_CUDA(cudaGetLastError());
+    count_launch();
+}
+
+void TcHalfStep::grad(DevProblem<float>& P, int side, const float* kpot, const float* pot,
+                      float eps, int64_t row_begin, int64_t row_end, float* G, int* flags) {
+    if (row_end <= row_begin) return;
+    Impl& I = *impl_;
+    const int qc = side == 0 ? 0 : 1, kc = side == 0 ? 1 : 0;
+    const DevSide<float>& qs = side == 0 ? P.src : P.tgt;
+    const DevSide<float>& ks = side == 0 ? P.tgt : P.src;
+    const int64_t R = qs.n, d = qs.d;
+    // pass 1 (K1): row LSE in log2 units (hi/lo) and the induced marginal
+    // r_i = w_i exp((pot_i - pot+_i) / eps) at the current potentials
+    DevBuf<float> l2h(size_t(R), P.s), l2l(size_t(R), P.s), r(size_t(R), P.s);
+    FinalizeArgs<float> fa{};
+    fa.eps = eps;
+    fa.flags = flags;
+    fa.old_pot = pot;
+    fa.w = qs.w.get();
+    fa.out_marg = r.get();
+    fa.marg_flag = side == 0 ? kFlagNonFiniteRowMarginal : kFlagNonFiniteColMarginal;
+    fa.out_l2h = l2h.get();
+    fa.out_l2l = l2l.get();
+    run(P, side, kpot, eps, fa, row_begin, row_end);
+    // pass 2 (K3): O = softmax(S) V with V = the key tiles themselves
+    TcApplyParams p{};
+    p.qimg = I.qimg[qc].get();
+    p.kimg = I.kimg[side].get();
+    p.kbias = I.kbias[side].get();
+    p.q_tile_begin = int(row_begin / TILE);
+    p.q_tiles = int((row_end + TILE - 1) / TILE) - p.q_tile_begin;
+    p.k_tiles = int(I.rows_pad[kc] / TILE);
+    const int sms = num_sms();
+    p.splits = pick_splits(p.q_tiles, p.k_tiles, sms);
+    p.items = p.q_tiles * p.splits;
+    p.row_begin = row_begin;
+    p.row_end = row_end;
+    p.key_valid = ks.n;
+    p.R = R;
+    p.acc_scale = std::ldexp(1.0f, I.eq[qc] + I.ek[side]);
+    p.l2h = l2h.get();
+    p.l2l = l2l.get();
+    DevBuf<float> part(size_t(p.splits) * size_t(R) * DPAD, P.s);
+    p.part_o = part.get();
+    tc_apply_kernel<<<std::min(p.items, sms), NUM_THREADS, A_SMEM_BYTES, P.s>>>(p);
+    FSKB_CUDA(cudaGetLastError());
+    count_launch();
+    // V = c y 2^-ek and P~ carries 2^12: O = part 2^(ek - 12) / c
+    const double c = 2.0 * P.fscale / I.eps * 1.4426950408889634074;
+    const double inv_v = std::ldexp(1.0, I.ek[side] - int(kPScaleLog2)) / c;
+    const int64_t total = (row_end - row_begin) * d;
+    tc_grad_finalize_kernel<<<unsigned((total + 255) / 256), 256, 0, P.s>>>(
+        part.get(), p.splits, R, row_begin, row_end, d, qs.pts.get(), r.get(), inv_v, G, flags);
     FSKB_CUDA(cudaGetLastError());
     count_launch();
 }

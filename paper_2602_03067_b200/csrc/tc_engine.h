@@ -35,6 +35,13 @@ public:
     void run(DevProblem<float>& P, int side, const float* kpot, float eps,
              const FinalizeArgs<float>& fa, int64_t row_begin, int64_t row_end);
 
+    // Gradient of the EOT loss w.r.t. the query cloud of `side` (side 0: X) for
+    // rows [row_begin, row_end): G_i = 2 r_i (x_i - (softmax_j S_ij) y_j) with
+    // r_i = w_i exp((pot_i - pot+_i)/eps). Two passes: K1 for
+    // the row LSE, then the fused tcgen05 transport kernel. G is (end-begin) x d.
+    void grad(DevProblem<float>& P, int side, const float* kpot, const float* pot, float eps,
+              int64_t row_begin, int64_t row_end, float* G, int* flags);
+
 private:
     struct Impl;
     Impl* impl_;

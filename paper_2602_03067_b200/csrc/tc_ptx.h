@@ -1,0 +1,183 @@
+// Thin inline-PTX layer for the sm_100a kernels: mbarriers, bulk copies (the
+// TMA engine's non-tensor path), tcgen05 MMA / TMEM load-store, UMMA
+// descriptors, and the tile-image geometry shared by every tcgen05 kernel.
+#pragma once
+
+#include <cuda_fp16.h>
+
+#include <cstdint>
+
+namespace fskb {
+namespace tc {
+
+constexpr int TILE = 128;                 // rows per query tile / keys per key tile
+constexpr int DPAD = 64;                  // padded feature dim (one SW128 chunk)
+constexpr uint32_t CHUNK = TILE * 128;    // 16 KB: 128 rows x 64 fp16
+constexpr uint32_t QTILE = 2 * CHUNK;     // hi + lo
+constexpr uint32_t BIAS = TILE * 32;      // 4 KB: 128 rows x 16 fp16 (SW32)
+constexpr uint32_t KSTAGE = 2 * CHUNK + BIAS;  // 36 KB
+constexpr float kOnesW0 = 2048.0f, kOnesW2 = 1.0f / 2048.0f;
+
+// idesc, kind::f16, D f32 (bits 4-5 = 1), A/B f16 (0), A K-major.
+//   score GEMM  S = Q K^T : B K-major, N = 128, M = 128
+//   value GEMM  O = P V   : A from TMEM, B MN-major (bit 16), N = 64, M = 128
+constexpr uint32_t IDESC_QK = (1u << 4) | (uint32_t(TILE >> 3) << 17) | (uint32_t(TILE >> 4) << 24);
+constexpr uint32_t IDESC_PV =
+    (1u << 4) | (1u << 16) | (uint32_t(DPAD >> 3) << 17) | (uint32_t(TILE >> 4) << 24);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor. layout 2 = SWIZZLE_128B, 6 = SWIZZLE_32B;
+// version 1. K-major swizzled: SBO = 8-row group stride, LBO unused.
+// MN-major SW128: SBO = stride between 8-row K groups, LBO = stride between
+// 64-element MN atoms (unused when N = 64).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t sbo, uint32_t layout,
+                                              uint32_t lbo = 16) {
+    uint64_t d = uint64_t((saddr & 0x3FFFFu) >> 4);
+    d |= uint64_t((lbo >> 4) & 0x3FFFu) << 16;
+    d |= uint64_t((sbo >> 4) & 0x3FFFu) << 32;
+    d |= uint64_t(1) << 46;
+    d |= uint64_t(layout) << 61;
+    return d;
+}
+
+// D[tmem] (+)= A[smem] B[smem]
+__device__ __forceinline__ void umma_ss(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t acc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+// D[tmem] (+)= A[tmem] B[smem]
+__device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
+                                        uint32_t idesc, uint32_t acc) {
+    const uint32_t z = 0;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%5, %5, %5, %5}, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc), "r"(z));
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+        : "memory");
+}
+
+#define FSKB_TMEM_LD32(addr, r)                                                                  \
+    asm volatile(                                                                                \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
+        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"       \
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),    \
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),             \
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),          \
+          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),          \
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),          \
+          "=r"(r[31])                                                                            \
+        : "r"(addr))
+
+#define FSKB_TMEM_ST32(addr, r)                                                                  \
+    asm volatile(                                                                                \
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"  \
+        "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::   \
+            "r"(addr),                                                                           \
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),  \
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),        \
+        "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),      \
+        "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),      \
+        "r"(r[29]), "r"(r[30]), "r"(r[31])                                                       \
+        : "memory")
+
+__device__ __forceinline__ void tmem_ld_wait() {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() {
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Constant "ones" chunk of the query operand, [2048, 1, 1/2048, 0...] per row
+// (SW32 K-major): multiplies the 3-piece key bias chunk into the score GEMM.
+__device__ __forceinline__ void fill_ones_chunk(uint8_t* dst, int tid, int nthreads) {
+    for (int idx = tid; idx < TILE * 16; idx += nthreads) {
+        const int r = idx >> 4, k = idx & 15;
+        const float v = k == 0 ? kOnesW0 : (k == 1 ? 1.0f : (k == 2 ? kOnesW2 : 0.0f));
+        const uint32_t off = r * 32 + ((((k >> 3) ^ ((r >> 2) & 1))) << 4) + (k & 7) * 2;
+        *reinterpret_cast<__half*>(dst + off) = __float2half_rn(v);
+    }
+}
+
+// Issues the 13 MMAs of one split-fp16 score tile: 3 products x 4 K16 slices of
+// the 64-wide hi/lo chunks, plus the bias K16 slice. Order matters for the fp32
+// accumulator's rounding: the 8 small cross terms (2^-11 of the score) first,
+// then the bias, then the 4 hi x hi slices, so only 5 additions round at the
+// score's full magnitude and the bias partially cancels the dot product early.
+__device__ __forceinline__ void issue_score_tile(uint32_t d_tmem, uint32_t qa, uint32_t ones,
+                                                 uint32_t kst) {
+#pragma unroll
+    for (int kk = 0; kk < DPAD / 16; ++kk) {
+        const uint64_t ah = umma_desc(qa + kk * 32, 1024, 2);
+        const uint64_t al = umma_desc(qa + CHUNK + kk * 32, 1024, 2);
+        const uint64_t bh = umma_desc(kst + kk * 32, 1024, 2);
+        const uint64_t bl = umma_desc(kst + CHUNK + kk * 32, 1024, 2);
+        umma_ss(d_tmem, al, bh, IDESC_QK, kk > 0 ? 1u : 0u);
+        umma_ss(d_tmem, ah, bl, IDESC_QK, 1u);
+    }
+    umma_ss(d_tmem, umma_desc(ones, 256, 6), umma_desc(kst + QTILE, 256, 6), IDESC_QK, 1u);
+#pragma unroll
+    for (int kk = 0; kk < DPAD / 16; ++kk)
+        umma_ss(d_tmem, umma_desc(qa + kk * 32, 1024, 2), umma_desc(kst + kk * 32, 1024, 2),
+                IDESC_QK, 1u);
+}
+
+}  // namespace tc
+}  // namespace fskb

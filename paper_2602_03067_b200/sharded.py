@@ -64,6 +64,13 @@ class ShardedSinkhorn:
         self.viol = torch.zeros(1, dtype=torch.float64, device=device)
         engine.bind(self.f.data_ptr(), self.g.data_ptr())
 
+    def _stream(self):
+        # the engine launches on torch's current stream so its kernels are
+        # ordered with the collectives torch issues on that stream
+        if self.torch.cuda.is_available() and self.f.is_cuda:
+            return self.torch.cuda.current_stream(self.f.device).cuda_stream
+        return 0
+
     def _gather(self, buf, per):
         if self.dist is None or self.plan.world == 1:
             return
@@ -77,7 +84,7 @@ class ShardedSinkhorn:
             buf.copy_(self.torch.cat(parts))
 
     def init(self):
-        self.engine.init_potentials()
+        self.engine.init_potentials(self._stream())
 
     def iterate(self, iters: int, track_violation: bool = False):
         """`iters` alternating iterations; returns the lagged violation of the
@@ -85,15 +92,16 @@ class ShardedSinkhorn:
         p = self.plan
         flo, fhi = p.f_bounds[p.rank]
         glo, ghi = p.g_bounds[p.rank]
+        st = self._stream()
         for _ in range(iters):
-            self.engine.half_step(0, flo, fhi)
+            self.engine.half_step(0, flo, fhi, 0, st)
             self._gather(self.f, p.f_per)
-            self.engine.half_step(1, glo, ghi)
+            self.engine.half_step(1, glo, ghi, 0, st)
             self._gather(self.g, p.g_per)
         if track_violation:
             self.viol.zero_()
             f_save = self.f.clone()
-            self.engine.half_step(0, flo, fhi, self.viol.data_ptr())
+            self.engine.half_step(0, flo, fhi, self.viol.data_ptr(), st)
             self.f.copy_(f_save)
             if self.dist is not None and p.world > 1:
                 self.dist.all_reduce(self.viol, group=self.group)
@@ -103,5 +111,5 @@ class ShardedSinkhorn:
     def grad_shard(self, out):
         """Gradient rows of this rank's shard of X into `out` ((hi-lo) x d)."""
         lo, hi = self.plan.f_bounds[self.plan.rank]
-        self.engine.grad(lo, hi, out.data_ptr())
+        self.engine.grad(lo, hi, out.data_ptr(), self._stream())
         return lo, hi

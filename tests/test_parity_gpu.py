@@ -163,9 +163,16 @@ def test_solve_grad_single(fsk, port):
     r = port.sinkhorn_solve(X, a, Y, b, eps=1.0, max_iters=10, precision="double")
     assert np.abs(s["f_hat"] - r["f_hat"]).max() <= 1e-5 * np.abs(r["f_hat"]).max()
     assert abs(s["dual_cost"] - r["dual_cost"]) <= 1e-5 * abs(r["dual_cost"])
-    ws = compose.Workspace(port, X, a, Y, b, r["f_hat"], r["g_hat"], 1.0)
-    Gw = compose.grad_source(ws)
-    assert np.abs(s["grad"] - Gw).max() <= 1e-5 * np.abs(Gw).max()
+    # gradient contract (SURVEY §8d ii): at the returned (fp32) potentials, within
+    # max(1e-5, 2x) the error of the reference's own fp32 arithmetic
+    from test_tensor_gpu import grad_errors
+    e_gpu, e32, _ = grad_errors(port, X, a, Y, b, s["f_hat"], s["g_hat"], 1.0, s["grad"])
+    assert e_gpu <= max(1e-5, 2.0 * e32)
+    # end to end against the fp64 solve: dominated by the fp32 storage of the
+    # potentials (|f_hat| ~ |x|^2 ~ 64, ulp 7.6e-6, enters r through exp(df/eps))
+    ws64 = compose.Workspace(port, X, a, Y, b, r["f_hat"], r["g_hat"], 1.0)
+    G64 = compose.grad_source(ws64)
+    assert np.abs(s["grad"] - G64).max() <= 1e-4 * np.abs(G64).max()
 
 
 def test_hvp_against_dense_and_composition(fsk, port):
@@ -224,10 +231,15 @@ def test_break_lse_negative_control(fsk, port):
     good = port.update_f_hat(X, a, Y, b, g, 0.1)
     fsk.debug_break_lse(True)
     try:
-        bad = fsk.update_f_hat(X, a, Y, b, g, 0.1)
-        bad32 = fsk.update_f_hat_f32(X, a, Y, b, g, 0.1)
+        # a broken recurrence must be caught: either wrong potentials or the
+        # reference's own NumericalError on a non-finite one (stream.cpp:127-130);
+        # which one depends on how often the running max moves, i.e. on tiling
+        for fn, tol in ((fsk.update_f_hat, 1e-6), (fsk.update_f_hat_f32, 1e-3)):
+            try:
+                bad = fn(X, a, Y, b, g, 0.1)
+                assert np.abs(bad - good).max() > tol
+            except fsk.NumericalError:
+                pass
     finally:
         fsk.debug_break_lse(False)
-    assert np.abs(bad - good).max() > 1e-6
-    assert np.abs(bad32 - good).max() > 1e-3
     assert np.abs(fsk.update_f_hat(X, a, Y, b, g, 0.1) - good).max() < 1e-12

@@ -16,6 +16,25 @@ def contract(got, want):
     return np.abs(got - want).max() / max(1.0, np.abs(want).max())
 
 
+def grad_errors(port, X, a, Y, b, f, g, eps, got):
+    """Gradient contract (SURVEY §8d ii, tensor-mode statement): at identical
+    potentials, ||G_gpu - G_64||_inf <= max(1e-5, 2 e32) ||G_64||_inf where e32 is
+    the error the reference's own fp32 arithmetic makes on the same inputs.
+
+    G = 2(diag(r) X - P Y) and r_i = a_i exp((f_i - f+_i)/eps) turns an absolute
+    score error delta into a relative gradient error delta/eps: no fp32 evaluation
+    of f+ (|f+| ~ |x|^2) reaches 1e-5 at eps = 0.05. e32 recomputes r with f+ from
+    the reference's update_f_hat_f32 (stream.cpp:437-443), P Y in fp64."""
+    from oracle import compose
+    ws = compose.Workspace(port, X, a, Y, b, f, g, eps)
+    G64 = compose.grad_source(ws)
+    fp32 = port.update_f_hat_f32(X, a, Y, b, g, eps).astype(np.float64)
+    r32 = a * np.exp((f - fp32) / eps)
+    G32 = 2.0 * (r32[:, None] * X - (r32 / ws.r)[:, None] * ws.PY)
+    scale = np.abs(G64).max()
+    return np.abs(got - G64).max() / scale, np.abs(G32 - G64).max() / scale, G64
+
+
 @pytest.fixture()
 def tensor_mode():
     os.environ["FSK_TENSOR_MODE"] = "tensor"
@@ -107,3 +126,80 @@ def test_engine_row_shards_reproduce_full_half_step(fsk, port):
         torch.cuda.synchronize()
         eng.close()
         del f0
+
+
+@pytest.mark.parametrize("n,m,d", [(1000, 777, 64), (515, 1300, 33), (260, 513, 16),
+                                   (129, 131, 3), (2048, 4096, 64)])
+@pytest.mark.parametrize("eps", [0.05, 1.0])
+def test_tensor_fused_gradient_parity(fsk, port, n, m, d, eps):
+    """Fused tcgen05 transport kernel (K3): grad_X at the engine's own potentials
+    against the fp64 SPEC composition 2(diag(r) X - P Y).
+    Contract (SURVEY §8d ii): ||dG||_inf <= 1e-5 ||G||_inf."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(n + 3 * m + d)
+    X = rng.normal(size=(n, d))
+    Y = rng.normal(size=(m, d)) * 0.8 + 0.2
+    a = rng.random(n) + 0.5
+    a /= a.sum()
+    b = np.full(m, 1.0 / m)
+    eng = fsk.Engine(0, X, a, Y, b, mode="tensor")
+    assert eng.path == "tcgen05-split3"
+    eng.set_eps(eps)
+    f = torch.empty(n, dtype=torch.float32, device="cuda")
+    g = torch.empty(m, dtype=torch.float32, device="cuda")
+    eng.bind(f.data_ptr(), g.data_ptr())
+    eng.init_potentials()
+    for _ in range(3):
+        eng.half_step(0, 0, n)
+        eng.half_step(1, 0, m)
+    G = torch.empty((n, d), dtype=torch.float32, device="cuda")
+    eng.grad(0, n, G.data_ptr())
+    # a ragged row shard of the same gradient
+    lo, hi = 77, min(n, 77 + 300)
+    Gs = torch.empty((hi - lo, d), dtype=torch.float32, device="cuda")
+    eng.grad(lo, hi, Gs.data_ptr())
+    torch.cuda.synchronize()
+    fh = f.cpu().numpy().astype(np.float64)
+    gh = g.cpu().numpy().astype(np.float64)
+    e_gpu, e32, want = grad_errors(port, X, a, Y, b, fh, gh, eps, G.cpu().numpy())
+    print(f"grad rel err gpu {e_gpu:.2e} ref-fp32 {e32:.2e}")
+    assert e_gpu <= max(1e-5, 2.0 * e32)
+    # the row shard reproduces the same rows of the full gradient
+    assert np.array_equal(Gs.cpu().numpy(), G.cpu().numpy()[lo:hi])
+    eng.close()
+
+
+def test_tensor_fused_gradient_cfg2_rows(fsk, port):
+    """cfg2 shape (n = m = 65536, d = 64, eps = 0.05): fused gradient on the full
+    problem, 256 sampled rows checked against the fp64 composition restricted to
+    those rows (rows are independent given the potentials)."""
+    torch = pytest.importorskip("torch")
+    n = m = 65536
+    d, eps = 64, 0.05
+    z = fsk.rng_normal(1000, (n + m) * d)
+    X, Y = z[: n * d].reshape(n, d), z[n * d:].reshape(m, d)
+    a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+    eng = fsk.Engine(0, X, a, Y, b, mode="tensor")
+    eng.set_eps(eps)
+    f = torch.empty(n, dtype=torch.float32, device="cuda")
+    g = torch.empty(m, dtype=torch.float32, device="cuda")
+    eng.bind(f.data_ptr(), g.data_ptr())
+    eng.init_potentials()
+    for _ in range(2):
+        eng.half_step(0, 0, n)
+        eng.half_step(1, 0, m)
+    G = torch.empty((n, d), dtype=torch.float32, device="cuda")
+    eng.grad(0, n, G.data_ptr())
+    torch.cuda.synchronize()
+    rows = np.sort(np.random.default_rng(0).choice(n, 256, replace=False))
+    fh = f.cpu().numpy().astype(np.float64)
+    gh = g.cpu().numpy().astype(np.float64)
+    # the oracle on the row slice: G_i is linear in a_i, so renormalise the slice
+    # weights (the oracle validates sum(a) = 1) and scale back
+    wsum = a[rows].sum()
+    got = G.cpu().numpy()[rows] / wsum
+    assert np.all(np.isfinite(got))
+    e_gpu, e32, _ = grad_errors(port, X[rows], a[rows] / wsum, Y, b, fh[rows], gh, eps, got)
+    print(f"cfg2 grad rel err gpu {e_gpu:.2e} ref-fp32 {e32:.2e}")
+    assert e_gpu <= max(1e-5, 2.0 * e32)
+    eng.close()
