@@ -302,7 +302,7 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
         DevBuf<T> G(size_t(n * d), C.s);
         bool done = false;
         if constexpr (kSingle) {
-            if (P.tc) {
+            if (P.tc && P.tc->chunks() == 1) {
                 // fused tcgen05 path: K1 row LSE + split-fp16 transport kernel
                 P.tc->set_eps(P, pot_eps);
                 P.tc->grad(P, 0, g.get(), f.get(), eps, 0, n, G.get(), C.flags);

@@ -51,6 +51,12 @@ constexpr uint32_t OFF_ONES = 2 * QTILE;                       // 64 KB
 constexpr uint32_t OFF_K = OFF_ONES + BIAS;                    // 68 KB
 constexpr uint32_t OFF_BAR = OFF_K + STAGES * KSTAGE;          // 212 KB
 constexpr uint32_t SMEM_BYTES = OFF_BAR + 256 + 1024;          // + barriers + align slack
+// chunked layout (d > 64): stage = Q chunk of 2 query tiles + key chunk + bias
+constexpr int CSTAGES = 2;
+constexpr uint32_t CSTAGE = 3 * QTILE + BIAS;                  // 100 KB
+constexpr uint32_t C_OFF_ONES = CSTAGES * CSTAGE;              // 200 KB
+constexpr uint32_t C_OFF_BAR = C_OFF_ONES + BIAS;              // 204 KB
+constexpr uint32_t C_SMEM_BYTES = C_OFF_BAR + 256 + 1024;
 constexpr float kSkipLog2 = 64.0f;  // LSE tiles entirely 2^-64 below the running max are skipped
 
 struct TcParams {
@@ -68,29 +74,39 @@ struct TcParams {
     double* part_m;              // [splits][R] natural-log max
     double* part_s;              // [splits][R] sum exp(S - max)
     int break_lse;
+    int chunks;                  // 64-wide feature chunks per row (images are [tile][chunk])
 };
 
+// CHUNKED = false: d <= 64, the query tile pair stays resident for a work item
+// and 36 KB key stages stream through a 4-deep ring.
+// CHUNKED = true: d > 64, every (key tile, feature chunk) step streams the
+// query chunk of both tiles with the key chunk (100 KB stages, 2-deep ring);
+// the score accumulates over chunks in TMEM before the epilogue sees it.
+template <bool CHUNKED>
 __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t* sbase = smem_raw + (base - raw);
+    constexpr int NST = CHUNKED ? CSTAGES : STAGES;
+    constexpr uint32_t BAR_OFF = CHUNKED ? C_OFF_BAR : OFF_BAR;
+    constexpr uint32_t ONES_OFF = CHUNKED ? C_OFF_ONES : OFF_ONES;
 
-    const uint32_t bar0 = base + OFF_BAR;
+    const uint32_t bar0 = base + BAR_OFF;
     auto kfull = [&](int s) { return bar0 + 8u * s; };
-    auto kempty = [&](int s) { return bar0 + 8u * (STAGES + s); };
-    const uint32_t qfull = bar0 + 8u * (2 * STAGES);
+    auto kempty = [&](int s) { return bar0 + 8u * (NST + s); };
+    const uint32_t qfull = bar0 + 8u * (2 * NST);
     const uint32_t qempty = qfull + 8u;
     auto accfull = [&](int b) { return qempty + 8u + 8u * b; };
     auto accempty = [&](int b) { return qempty + 24u + 8u * b; };
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + OFF_BAR + 128);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + BAR_OFF + 128);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-    fill_ones_chunk(sbase + OFF_ONES, threadIdx.x, NUM_THREADS);
+    fill_ones_chunk(sbase + ONES_OFF, threadIdx.x, NUM_THREADS);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) {
+        for (int s = 0; s < NST; ++s) {
             mbar_init(kfull(s), 1);
             mbar_init(kempty(s), 1);
         }
@@ -122,19 +138,39 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
                 const int unit = item / p.splits, split = item % p.splits;
                 const int qt0 = p.q_tile_begin + 2 * unit;
                 const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
-                mbar_wait(qempty, (lu & 1) ^ 1);
-                mbar_expect_tx(qfull, nq * QTILE);
-                bulk_g2s(base + OFF_Q, p.qimg + size_t(qt0) * QTILE, nq * QTILE, qfull);
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
-                for (int kt = kt0; kt < kt1; ++kt, ++it) {
-                    const int s = it % STAGES;
-                    const uint32_t ph = (it / STAGES) & 1;
-                    mbar_wait(kempty(s), ph ^ 1);
-                    mbar_expect_tx(kfull(s), KSTAGE);
-                    const uint32_t dst = base + OFF_K + s * KSTAGE;
-                    bulk_g2s(dst, p.kimg + size_t(kt) * QTILE, QTILE, kfull(s));
-                    bulk_g2s(dst + QTILE, p.kbias + size_t(kt) * BIAS, BIAS, kfull(s));
+                if constexpr (CHUNKED) {
+                    const int C = p.chunks;
+                    for (int kt = kt0; kt < kt1; ++kt) {
+                        for (int c = 0; c < C; ++c, ++it) {
+                            const int s = it % NST;
+                            mbar_wait(kempty(s), ((it / NST) & 1) ^ 1);
+                            mbar_expect_tx(kfull(s), (nq + 1) * QTILE + BIAS);
+                            const uint32_t dst = base + s * CSTAGE;
+                            for (int t = 0; t < nq; ++t)
+                                bulk_g2s(dst + t * QTILE,
+                                         p.qimg + (size_t(qt0 + t) * C + c) * QTILE, QTILE,
+                                         kfull(s));
+                            bulk_g2s(dst + 2 * QTILE, p.kimg + (size_t(kt) * C + c) * QTILE,
+                                     QTILE, kfull(s));
+                            bulk_g2s(dst + 3 * QTILE, p.kbias + size_t(kt) * BIAS, BIAS,
+                                     kfull(s));
+                        }
+                    }
+                } else {
+                    mbar_wait(qempty, (lu & 1) ^ 1);
+                    mbar_expect_tx(qfull, nq * QTILE);
+                    bulk_g2s(base + OFF_Q, p.qimg + size_t(qt0) * QTILE, nq * QTILE, qfull);
+                    for (int kt = kt0; kt < kt1; ++kt, ++it) {
+                        const int s = it % STAGES;
+                        const uint32_t ph = (it / STAGES) & 1;
+                        mbar_wait(kempty(s), ph ^ 1);
+                        mbar_expect_tx(kfull(s), KSTAGE);
+                        const uint32_t dst = base + OFF_K + s * KSTAGE;
+                        bulk_g2s(dst, p.kimg + size_t(kt) * QTILE, QTILE, kfull(s));
+                        bulk_g2s(dst + QTILE, p.kbias + size_t(kt) * BIAS, BIAS, kfull(s));
+                    }
                 }
             }
         }
@@ -145,26 +181,43 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
                 const int unit = item / p.splits, split = item % p.splits;
                 const int qt0 = p.q_tile_begin + 2 * unit;
                 const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
-                mbar_wait(qfull, lu & 1);
-                fence_after();
+                if constexpr (!CHUNKED) {
+                    mbar_wait(qfull, lu & 1);
+                    fence_after();
+                }
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
-                for (int kt = kt0; kt < kt1; ++kt, ++it, ++acc_it) {
-                    const int s = it % STAGES;
-                    const uint32_t ph = (it / STAGES) & 1;
+                for (int kt = kt0; kt < kt1; ++kt, ++acc_it) {
                     const int b = acc_it & 1;
                     const uint32_t aph = (acc_it >> 1) & 1;
-                    mbar_wait(kfull(s), ph);
                     mbar_wait(accempty(b), aph ^ 1);
                     fence_after();
-                    const uint32_t kst = base + OFF_K + s * KSTAGE;
-                    for (int t = 0; t < nq; ++t)
-                        issue_score_tile(tmem + uint32_t((b * 2 + t) * TILE),
-                                         base + OFF_Q + t * QTILE, base + OFF_ONES, kst);
-                    umma_commit(kempty(s));
+                    if constexpr (CHUNKED) {
+                        for (int c = 0; c < p.chunks; ++c, ++it) {
+                            const int s = it % NST;
+                            mbar_wait(kfull(s), (it / NST) & 1);
+                            fence_after();
+                            const uint32_t st = base + s * CSTAGE;
+                            for (int t = 0; t < nq; ++t)
+                                issue_score_chunk(tmem + uint32_t((b * 2 + t) * TILE),
+                                                  st + t * QTILE, st + 2 * QTILE,
+                                                  base + ONES_OFF, st + 3 * QTILE, c == 0);
+                            umma_commit(kempty(s));
+                        }
+                    } else {
+                        const int s = it % STAGES;
+                        mbar_wait(kfull(s), (it / STAGES) & 1);
+                        fence_after();
+                        const uint32_t kst = base + OFF_K + s * KSTAGE;
+                        for (int t = 0; t < nq; ++t)
+                            issue_score_tile(tmem + uint32_t((b * 2 + t) * TILE),
+                                             base + OFF_Q + t * QTILE, base + OFF_ONES, kst);
+                        umma_commit(kempty(s));
+                        ++it;
+                    }
                     umma_commit(accfull(b));
                 }
-                umma_commit(qempty);
+                if constexpr (!CHUNKED) umma_commit(qempty);
             }
         }
     } else {
@@ -581,18 +634,20 @@ __global__ void tc_finalize_kernel(const double* __restrict__ pm, const double* 
 
 // ---- operand images ------------------------------------------------------------
 
-// hi/lo fp16 split of (pts * scale) into SW128 K-major tile images.
-// One thread per (row, 8-element group).
+// hi/lo fp16 split of (pts * scale) into SW128 K-major tile images, laid out
+// [row tile][64-wide feature chunk][hi 16 KB | lo 16 KB]. One thread per
+// (row, chunk, 8-element group).
 __global__ void build_split_image(const float* __restrict__ pts, int64_t R, int64_t d, float scale,
-                                  int64_t rows_padded, uint8_t* __restrict__ img) {
+                                  int64_t rows_padded, int chunks, uint8_t* __restrict__ img) {
     const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t row = gid >> 3;
-    const int grp = int(gid & 7);
+    const int64_t row = gid / (int64_t(chunks) * 8);
+    const int g = int(gid % (int64_t(chunks) * 8));
+    const int c = g >> 3, grp = g & 7;
     if (row >= rows_padded) return;
     __align__(16) __half hi[8], lo[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-        const int64_t k = grp * 8 + e;
+        const int64_t k = int64_t(c) * DPAD + grp * 8 + e;
         const float v = (row < R && k < d) ? pts[row * d + k] * scale : 0.0f;
         const __half h = __float2half_rn(v);
         hi[e] = h;
@@ -600,7 +655,8 @@ __global__ void build_split_image(const float* __restrict__ pts, int64_t R, int6
     }
     const int64_t tile = row / TILE;
     const int r = int(row % TILE);
-    const size_t off = size_t(tile) * QTILE + size_t(r) * 128 + size_t((grp ^ (r & 7)) << 4);
+    const size_t off = (size_t(tile) * chunks + c) * QTILE + size_t(r) * 128 +
+                       size_t((grp ^ (r & 7)) << 4);
     *reinterpret_cast<uint4*>(img + off) = *reinterpret_cast<const uint4*>(hi);
     *reinterpret_cast<uint4*>(img + off + CHUNK) = *reinterpret_cast<const uint4*>(lo);
 }
@@ -666,10 +722,12 @@ int scale_exponent(double maxabs) {
 }  // namespace
 
 // Key split that best fills a persistent grid of `sms` CTAs with units x splits items.
-int pick_splits(int units, int k_tiles, int sms) {
-    int best = 1;
+int pick_splits(int units, int k_tiles, int sms, int min_splits = 1) {
+    const int max_s = std::max(1, std::min(32, k_tiles / 4));
+    min_splits = std::min(std::max(1, min_splits), max_s);
+    int best = min_splits;
     double best_eff = 0.0;
-    for (int s = 1; s <= 16 && s <= std::max(1, k_tiles / 4); ++s) {
+    for (int s = min_splits; s <= max_s && s <= std::max(min_splits, 16); ++s) {
         const double items = double(units) * s;
         const double eff = items / (std::ceil(items / sms) * sms);
         if (eff > best_eff + 0.02) {
@@ -690,27 +748,33 @@ struct TcHalfStep::Impl {
     DevBuf<uint8_t> kbias[2];
     int ek[2] = {0, 0};
     double eps = 0.0;
+    int chunks = 1;                 // 64-wide feature chunks (d > 64: chunked kernels)
 };
 
-bool TcHalfStep::supported(int64_t d) { return d >= 1 && d <= DPAD; }
+bool TcHalfStep::supported(int64_t d) { return d >= 1 && d <= 64 * 64; }
+int TcHalfStep::chunks() const { return impl_->chunks; }
 
 TcHalfStep::TcHalfStep(DevProblem<float>& P) : impl_(new Impl()) {
     // per device (the attribute is per-context), cheap enough to set every time
-    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(SMEM_BYTES)));
+    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_kernel<false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES)));
+    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_kernel<true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(C_SMEM_BYTES)));
     FSKB_CUDA(cudaFuncSetAttribute(tc_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(A_SMEM_BYTES)));
     const DevSide<float>* sides[2] = {&P.src, &P.tgt};
+    impl_->chunks = int((P.src.d + DPAD - 1) / DPAD);
     for (int c = 0; c < 2; ++c) {
         const DevSide<float>& sd = *sides[c];
         impl_->npts[c] = sd.n;
         impl_->rows_pad[c] = (sd.n + TILE - 1) / TILE * TILE;
         impl_->maxabs[c] = device_absmax(sd.pts.get(), sd.n * sd.d, P.s);
         impl_->eq[c] = scale_exponent(impl_->maxabs[c]);
-        impl_->qimg[c].alloc(size_t(impl_->rows_pad[c] / TILE) * QTILE, P.s);
-        const int64_t groups = impl_->rows_pad[c] * 8;
+        const int C = impl_->chunks;
+        impl_->qimg[c].alloc(size_t(impl_->rows_pad[c] / TILE) * C * QTILE, P.s);
+        const int64_t groups = impl_->rows_pad[c] * 8 * C;
         build_split_image<<<unsigned((groups + 255) / 256), 256, 0, P.s>>>(
-            sd.pts.get(), sd.n, sd.d, std::ldexp(1.0f, -impl_->eq[c]), impl_->rows_pad[c],
+            sd.pts.get(), sd.n, sd.d, std::ldexp(1.0f, -impl_->eq[c]), impl_->rows_pad[c], C,
             impl_->qimg[c].get());
         FSKB_CUDA(cudaGetLastError());
         count_launch();
@@ -727,14 +791,15 @@ void TcHalfStep::set_eps(DevProblem<float>& P, double eps) {
         const int kc = side == 0 ? 1 : 0;
         const DevSide<float>& ks = side == 0 ? P.tgt : P.src;
         impl_->ek[side] = scale_exponent(double(impl_->maxabs[kc]) * c);
+        const int C = impl_->chunks;
         if (!impl_->kimg[side].get())
-            impl_->kimg[side].alloc(size_t(impl_->rows_pad[kc] / TILE) * QTILE, P.s);
+            impl_->kimg[side].alloc(size_t(impl_->rows_pad[kc] / TILE) * C * QTILE, P.s);
         if (!impl_->kbias[side].get())
             impl_->kbias[side].alloc(size_t(impl_->rows_pad[kc] / TILE) * BIAS, P.s);
-        const int64_t groups = impl_->rows_pad[kc] * 8;
+        const int64_t groups = impl_->rows_pad[kc] * 8 * C;
         build_split_image<<<unsigned((groups + 255) / 256), 256, 0, P.s>>>(
             ks.pts.get(), ks.n, ks.d, float(c * std::ldexp(1.0, -impl_->ek[side])),
-            impl_->rows_pad[kc], impl_->kimg[side].get());
+            impl_->rows_pad[kc], C, impl_->kimg[side].get());
         FSKB_CUDA(cudaGetLastError());
         count_launch();
     }
@@ -764,7 +829,12 @@ void TcHalfStep::run(DevProblem<float>& P, int side, const float* kpot, float ep
     p.k_tiles = k_tiles;
     const int units = (p.q_tiles + 1) / 2;
     const int sms = num_sms();
-    p.splits = pick_splits(units, k_tiles, sms);
+    p.chunks = I.chunks;
+    // chunked: keep the query chunks of the concurrently running work items
+    // L2-resident (~48 MB) by letting several CTAs share a query tile pair
+    const double q_bytes = 2.0 * I.chunks * QTILE;
+    const int min_s = I.chunks > 1 ? int(std::ceil(sms * q_bytes / (48.0 * (1 << 20)))) : 1;
+    p.splits = pick_splits(units, k_tiles, sms, min_s);
     p.items = units * p.splits;
     p.row_begin = row_begin;
     p.row_end = row_end;
@@ -776,7 +846,10 @@ void TcHalfStep::run(DevProblem<float>& P, int side, const float* kpot, float ep
     p.part_m = pm.get();
     p.part_s = ps.get();
     const int grid = std::min(p.items, sms);
-    tc_lse_kernel<<<grid, NUM_THREADS, SMEM_BYTES, P.s>>>(p);
+    if (I.chunks == 1)
+        tc_lse_kernel<false><<<grid, NUM_THREADS, SMEM_BYTES, P.s>>>(p);
+    else
+        tc_lse_kernel<true><<<grid, NUM_THREADS, C_SMEM_BYTES, P.s>>>(p);
     FSKB_CUDA(cudaGetLastError());
     count_launch();
     const int64_t rows = row_end - row_begin;
@@ -792,6 +865,7 @@ void TcHalfStep::grad(DevProblem<float>& P, int side, const float* kpot, const f
                       float eps, int64_t row_begin, int64_t row_end, float* G, int* flags) {
     if (row_end <= row_begin) return;
     Impl& I = *impl_;
+    if (I.chunks != 1) throw ValidationFailure("fused tcgen05 gradient needs d <= 64");
     const int qc = side == 0 ? 0 : 1, kc = side == 0 ? 1 : 0;
     const DevSide<float>& qs = side == 0 ? P.src : P.tgt;
     const DevSide<float>& ks = side == 0 ? P.tgt : P.src;
@@ -846,7 +920,7 @@ bool enable_tensor_path(DevProblem<float>& P, int mode) {
     if (mode == 1 || P.labeled) return false;
     const int64_t d = P.src.d;
     const bool shape_ok = TcHalfStep::supported(d);
-    if (mode == 2 && !shape_ok) throw ValidationFailure("tensor path supports 1 <= d <= 64");
+    if (mode == 2 && !shape_ok) throw ValidationFailure("tensor path supports 1 <= d <= 4096");
     // auto: the contraction is a real GEMM only from d >= 32 (north star: small-d
     // point clouds stay on CUDA-core FMA)
     if (mode == 0 && !(shape_ok && d >= 32)) return false;

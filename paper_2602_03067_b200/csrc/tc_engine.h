@@ -21,10 +21,12 @@ struct DevProblem;
 
 class TcHalfStep {
 public:
-    // d must satisfy 1 <= d <= 64 (padded to 64 in the images).
+    // 1 <= d <= 4096; d is padded to a multiple of 64 in the images and d > 64
+    // runs the chunked kernels (operands streamed 64 features at a time).
     explicit TcHalfStep(DevProblem<float>& P);
     ~TcHalfStep();
     static bool supported(int64_t d);
+    int chunks() const;
 
     // (Re)builds the scaled key images for this eps (O((n+m) d) work).
     void set_eps(DevProblem<float>& P, double eps);

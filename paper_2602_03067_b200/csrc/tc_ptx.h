@@ -179,5 +179,24 @@ __device__ __forceinline__ void issue_score_tile(uint32_t d_tmem, uint32_t qa, u
                 IDESC_QK, 1u);
 }
 
+// One 64-wide feature chunk of a score tile for d > 64 (operands streamed chunk
+// by chunk): the bias slice opens the accumulator on the first chunk, then the
+// 8 cross terms and the 4 hi x hi slices of this chunk.
+__device__ __forceinline__ void issue_score_chunk(uint32_t d_tmem, uint32_t qa, uint32_t ka,
+                                                  uint32_t ones, uint32_t bias, bool first) {
+    if (first) umma_ss(d_tmem, umma_desc(ones, 256, 6), umma_desc(bias, 256, 6), IDESC_QK, 0u);
+#pragma unroll
+    for (int kk = 0; kk < DPAD / 16; ++kk) {
+        umma_ss(d_tmem, umma_desc(qa + CHUNK + kk * 32, 1024, 2), umma_desc(ka + kk * 32, 1024, 2),
+                IDESC_QK, 1u);
+        umma_ss(d_tmem, umma_desc(qa + kk * 32, 1024, 2), umma_desc(ka + CHUNK + kk * 32, 1024, 2),
+                IDESC_QK, 1u);
+    }
+#pragma unroll
+    for (int kk = 0; kk < DPAD / 16; ++kk)
+        umma_ss(d_tmem, umma_desc(qa + kk * 32, 1024, 2), umma_desc(ka + kk * 32, 1024, 2),
+                IDESC_QK, 1u);
+}
+
 }  // namespace tc
 }  // namespace fskb

@@ -43,7 +43,10 @@ def tensor_mode():
 
 
 @pytest.mark.parametrize("n,m,d", [(128, 128, 64), (384, 320, 64), (1000, 777, 64),
-                                   (515, 1300, 33), (260, 513, 16), (129, 131, 3)])
+                                   (515, 1300, 33), (260, 513, 16), (129, 131, 3),
+                                   # chunked kernel (d > 64): cfg4 / cfg5 feature dims
+                                   (300, 421, 784), (260, 300, 1024), (129, 200, 100),
+                                   (640, 700, 128)])
 @pytest.mark.parametrize("eps", [0.05, 1.0])
 def test_tensor_half_step_parity(fsk, port, tensor_mode, n, m, d, eps):
     rng = np.random.default_rng(n * 7 + m + d)
