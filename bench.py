@@ -36,11 +36,18 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 CONFIGS = {
-    # name: (n, m, d, eps, iterations per step)
+    # name: (n, m, d, eps, iterations per step); BASELINE.json configs[0..4]
     "cfg3": (1 << 20, 1 << 20, 64, 0.05, 10),
     "cfg2": (65536, 65536, 64, 0.05, 10),
     "cfg1": (4096, 4096, 3, 0.1, 100),
+    "cfg4": (100000, 100000, 1024, 0.1, 10),
+    "cfg5": (10000, 10000, 784, 0.1, 10),
 }
+# what a step adds after the iterations: the gradient w.r.t. X (cfg1-3), nothing
+# yet for cfg4 (forward only: the tensor-core HVP is not built yet), and for cfg5
+# a step is the whole batch of 64 debiased divergences (3 solves per pair)
+STEP_TAIL = {"cfg1": "grad", "cfg2": "grad", "cfg3": "grad", "cfg4": "fwd", "cfg5": "divergence"}
+CFG5_PAIRS = 64
 
 
 def peaks():
@@ -128,9 +135,9 @@ def _reference_inputs(n, m, d):
     return _REF_INPUTS[key]
 
 
-def reference_sample(n, m, d, eps, iters, threads=None):
+def reference_sample(cfgname, threads=None):
     """Times the reference's own CPU path on a bounded slice of the workload and
-    extrapolates to one full step (10 iterations + gradient).
+    extrapolates to one full step.
 
     * f half-step: update_f_hat_f32 (stream.cpp:437-443) for 64*T source rows
       (one row block per worker thread) against all m targets; rows are
@@ -138,14 +145,17 @@ def reference_sample(n, m, d, eps, iters, threads=None):
       bit-identical to the same rows of a full call).
     * g half-step: update_g_hat_f32 (stream.cpp:445-451) for 64*T target rows
       against all n sources, scaled by m / rows.
-    * gradient: the SPEC composition (the reference ships no gradient code):
-      one f64 LSE pass for r (update_f_hat, 64*T rows x m) plus apply_plan(Y)
-      (stream.cpp:324-339, double only) on 64*T rows x 4096 targets, scaled by
-      (n / rows) and (n / rows)(m / 4096).
+    * gradient (cfg1-3): the SPEC composition (the reference ships no gradient
+      code): one f64 LSE pass for r (update_f_hat, 64*T rows x m) plus
+      apply_plan(Y) (stream.cpp:324-339, double only) on 64*T rows x 4096
+      targets, scaled by (n / rows) and (n / rows)(m / 4096).
+    * cfg5: a step is 64 pairs x 3 solves x iters alternating iterations.
     Times include the wrapper's copy of the inputs into fsk types (< 10%).
     """
     from oracle import Oracle
 
+    n, m, d, eps, iters = CONFIGS[cfgname]
+    tail = STEP_TAIL[cfgname]
     ref = Oracle("ref_fast")
     if threads:
         ref.set_num_threads(threads)
@@ -163,38 +173,42 @@ def reference_sample(n, m, d, eps, iters, threads=None):
     t0 = time.perf_counter()
     ref.update_g_hat_f32(Xf, a, Yf[:rows], b[:rows], f0.astype(np.float32), eps)
     t_g = time.perf_counter() - t0
-    a64 = np.full(rows, 1.0 / rows)
-    t0 = time.perf_counter()
-    ref.update_f_hat(X64[:rows], a64, Y64, np.full(m, 1.0 / m), g0, eps)
-    t_lse64 = time.perf_counter() - t0
-    Ysub = Y64[:cols_apply]
-    bsub = np.full(cols_apply, 1.0 / cols_apply)
-    gsub = -(Ysub ** 2).sum(1)
-    fsub = ref.update_f_hat(X64[:rows], a64, Ysub, bsub, gsub, eps)
-    t0 = time.perf_counter()
-    ref.apply_plan(X64[:rows], a64, Ysub, bsub, fsub, gsub, eps, Ysub)
-    t_apply = time.perf_counter() - t0
     iter_s = t_f * n / rows + t_g * m / rows
-    grad_s = t_lse64 * n / rows + t_apply * (n / rows) * (m / cols_apply)
-    sample = (f"f32 half-steps on {rows} rows x all {m} (resp. {n}) columns, {T} threads; "
-              f"gradient = f64 LSE {rows} x {m} + apply_plan(Y) {rows} x {cols_apply}; "
-              f"extrapolated by n/rows, m/cols")
-    return dict(step_s=iters * iter_s + grad_s, iter_s=iter_s, grad_s=grad_s, threads=T,
-                sample=sample, so=str(ref.so_path.name), wall_s=t_f + t_g + t_lse64 + t_apply)
+    grad_s = 0.0
+    sample = (f"f32 half-steps on {rows} rows x all {m} (resp. {n}) columns, {T} threads")
+    if tail == "grad":
+        a64 = np.full(rows, 1.0 / rows)
+        t0 = time.perf_counter()
+        ref.update_f_hat(X64[:rows], a64, Y64, np.full(m, 1.0 / m), g0, eps)
+        t_lse64 = time.perf_counter() - t0
+        Ysub = Y64[:cols_apply]
+        bsub = np.full(cols_apply, 1.0 / cols_apply)
+        gsub = -(Ysub ** 2).sum(1)
+        fsub = ref.update_f_hat(X64[:rows], a64, Ysub, bsub, gsub, eps)
+        t0 = time.perf_counter()
+        ref.apply_plan(X64[:rows], a64, Ysub, bsub, fsub, gsub, eps, Ysub)
+        t_apply = time.perf_counter() - t0
+        grad_s = t_lse64 * n / rows + t_apply * (n / rows) * (m / cols_apply)
+        sample += (f"; gradient = f64 LSE {rows} x {m} + apply_plan(Y) {rows} x {cols_apply}")
+    sample += "; extrapolated by n/rows, m/cols"
+    solves = 3 * CFG5_PAIRS if tail == "divergence" else 1
+    if tail == "divergence":
+        sample += f"; x {solves} solves (64 pairs x 3)"
+    return dict(step_s=solves * iters * iter_s + grad_s, iter_s=iter_s, grad_s=grad_s, threads=T,
+                iters=solves * iters, sample=sample, so=str(ref.so_path.name))
 
 
 def run_reference(args, cfgname):
-    n, m, d, eps, iters = CONFIGS[cfgname]
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     for _ in range(args.warmup):
-        reference_sample(n, m, d, eps, iters)
-    steps = [reference_sample(n, m, d, eps, iters) for _ in range(args.steps)]
+        reference_sample(cfgname)
+    steps = [reference_sample(cfgname) for _ in range(args.steps)]
     step_s = statistics.median(s["step_s"] for s in steps)
-    value = iters / step_s
+    value = steps[0]["iters"] / step_s
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "iterations/s",
+        "impl": "reference", "metric": metric_name(cfgname), "value": value, "unit": "iterations/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (fsk::Rng(1000) Gaussian)",
@@ -210,13 +224,26 @@ def run_reference(args, cfgname):
     return 0
 
 
-METRIC = "Sinkhorn iterations/s (10 alternating iterations + grad_X per step), n=m=2^20, d=64"
+def metric_name(cfgname):
+    n, m, d, eps, iters = CONFIGS[cfgname]
+    tail = STEP_TAIL[cfgname]
+    if tail == "divergence":
+        return (f"Sinkhorn iterations/s ({CFG5_PAIRS} debiased divergences x 3 solves x {iters} "
+                f"iterations per step), n=m={n}, d={d}")
+    what = "+ grad_X " if tail == "grad" else ""
+    nn = "2^20" if n == 1 << 20 else str(n)
+    return f"Sinkhorn iterations/s ({iters} alternating iterations {what}per step), n=m={nn}, d={d}"
+
+
+METRIC = metric_name("cfg3")
 
 
 def workload_config(cfgname):
     n, m, d, eps, iters = CONFIGS[cfgname]
+    tail = {"grad": " + gradient w.r.t. X", "fwd": " (forward only)",
+            "divergence": f" per solve, {CFG5_PAIRS} pairs x 3 solves"}[STEP_TAIL[cfgname]]
     return {"workload": f"{cfgname}: point-cloud EOT n=m={n}, d={d}, eps={eps}, "
-                        f"{iters} alternating iterations + gradient w.r.t. X per step",
+                        f"{iters} alternating iterations{tail} per step",
             "n": n, "m": m, "d": d, "eps": eps, "iterations_per_step": iters,
             "precision": "fp32 contract (tcgen05 split-fp16 scores, fp32 accumulate)",
             "l2": "inputs larger than L2 (operand images 2 x 288 MB per side)"}
@@ -273,6 +300,8 @@ def run_b200(args, cfgname):
             glo, ghi = plan.g_bounds[rank]
             half(1, glo, ghi)
             solver._gather(solver.g, plan.g_per)
+        if STEP_TAIL[cfgname] != "grad":
+            return
         if events is not None:
             gev.append(torch.cuda.Event(enable_timing=True))
             gev[-1].record(stream)
@@ -315,13 +344,14 @@ def run_b200(args, cfgname):
     if args.e2e:
         if world == 1:
             t0 = time.perf_counter()
+            want_grad = STEP_TAIL[cfgname] == "grad"
             out = fsk.sinkhorn_solve(X, a, Y, b, eps=eps, max_iters=iters, precision="single",
-                                     grad=True)
+                                     grad=want_grad)
             e2e_s = time.perf_counter() - t0
             e2e = {"value": iters / e2e_s, "unit": "iterations/s",
                    "h2d_bytes_per_step": int(X.nbytes + Y.nbytes + a.nbytes + b.nbytes),
-                   "d2h_bytes_per_step": int(out["grad"].nbytes + out["f_hat"].nbytes +
-                                             out["g_hat"].nbytes),
+                   "d2h_bytes_per_step": int((out["grad"].nbytes if want_grad else 0) +
+                                             out["f_hat"].nbytes + out["g_hat"].nbytes),
                    "api": "fsk_sinkhorn_solve_grad (C ABI, host double buffers)",
                    "loss": out["dual_cost"]}
         else:
@@ -352,21 +382,41 @@ def run_b200(args, cfgname):
         return 0
 
     pk, pk_kind = peaks()
-    # roofline of the dominant kernel (tc_lse_kernel): algorithmic FLOPs of one
-    # half-step launch over this rank's rows, W_dot = 2 n_rows m d
+    # roofline of the dominant kernel (the half-step LSE kernel): algorithmic
+    # FLOPs of one launch over this rank's rows, W_dot = 2 n_rows m d,
+    # against the peak of the precision mode that runs it (SURVEY §8d "which
+    # roofline applies by mode"): the split-fp16 tensor mode issues
+    # (12 C + 1) K16 MMAs per 64 C features where one fp16 pass issues 4 C, so
+    # its dot-product peak is the measured dense fp16/bf16 peak / mode_factor.
     rows0 = plan.f_bounds[0][1] - plan.f_bounds[0][0]
     hs = sorted(half_ms)
     med_half = hs[len(hs) // 2] / 1e3
     w_dot = 2.0 * rows0 * m * d
     achieved = w_dot / med_half / 1e12
-    peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
     sm_clk = (clocks or {}).get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)
+    tensor = eng.path.startswith("tcgen05")
+    chunks = -(-d // 64)
+    if tensor:
+        mode_factor = (12 * chunks + 1) / (4.0 * chunks) * (64.0 * chunks / d)
+        peak_raw = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+        peak = peak_raw / mode_factor
+        peak_src = (f"{pk_kind} bf16_tflops_sustained {peak_raw} / split-fp16 mode factor "
+                    f"{mode_factor:.3f}")
+        kernel = "tc_lse_kernel<" + ("true" if chunks > 1 else "false") + ">"
+    else:
+        mode_factor = 1.0
+        peak = 2.0 * 128 * 148 * sm_clk * 1e6 / 1e12   # FP32 FMA at the sampled clock
+        peak_src = f"FP32 FMA 148 SM x 128 lanes x 2 x {sm_clk} MHz (sampled clock)"
+        kernel = "lse_partial_kernel (CUDA-core FP32)"
     exp_floor = rows0 * m / (16.0 * 148 * sm_clk * 1e6)
-    mma_floor = 2.0 * rows0 * m * (3 * 64 + 16) / (peak * 1e12)
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(cfgname, {}).get("bytes_per_launch")
     step_s = elapsed / args.steps
     value = iters * args.steps / elapsed
     line = {
-        "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world,
+        "metric": metric_name(cfgname), "value": value, "unit": "iterations/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (fsk::Rng(1000) Gaussian clouds, uniform weights)",
@@ -375,22 +425,23 @@ def run_b200(args, cfgname):
                        path=eng.path),
         "half_step_ms": med_half * 1e3,
         "grad_ms": grad_ms[len(grad_ms) // 2] if grad_ms else None,
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": None,
-                     "kernel": "tc_lse_kernel (+bias/finalize, CUDA events per half-step)",
-                     "algorithmic": "W_dot = 2 n m d per half-step (d = 64)",
-                     "peak_source": f"{pk_kind} bf16_tflops_sustained (MEASURED_PEAKS.json)",
-                     "mode_floor_ms": max(exp_floor, mma_floor) * 1e3,
-                     "exp_floor_ms": exp_floor * 1e3, "mma_floor_ms": mma_floor * 1e3,
-                     "frac_of_mode_floor": max(exp_floor, mma_floor) / med_half},
+        "roofline": {"bound": "tensor" if tensor else "fma", "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                     "kernel": kernel + " (+bias/finalize; CUDA events around each f half-step "
+                               "on the launching stream)",
+                     "algorithmic": f"W_dot = 2 n m d per half-step (n_rows={rows0}, m={m}, "
+                                    f"d={d})",
+                     "peak_source": peak_src,
+                     "exp_floor_ms": exp_floor * 1e3,
+                     "mode_floor_ms": w_dot / (peak * 1e12) * 1e3},
         "gpu_launches": launches,
         "clocks": clocks,
         "e2e": e2e,
     }
     if world == 1 and args.cpu_baseline:
         try:
-            cb = reference_sample(n, m, d, eps, iters)
-            line["cpu_baseline"] = {"value": iters / cb["step_s"], "unit": "iterations/s",
+            cb = reference_sample(cfgname)
+            line["cpu_baseline"] = {"value": cb["iters"] / cb["step_s"], "unit": "iterations/s",
                                     "cores": cb["threads"], "kind": "reference",
                                     "sample": cb["sample"], "library": cb["so"]}
         except Exception as exc:  # reference library absent on this host
@@ -400,6 +451,64 @@ def run_b200(args, cfgname):
     eng.close()
     if world > 1:
         dist.destroy_process_group()
+    return 0
+
+
+def run_b200_divergence(args, cfgname):
+    """cfg5: one step = fsk_sinkhorn_divergence_batch over 64 (mu, nu) pairs, each
+    pair 3 single-precision solves (cross + both debiasing terms) of `iters`
+    alternating iterations, through the public C ABI with host buffers (the
+    timed region includes every upload and the dual-cost readback). Pairs are
+    drawn from 16 distinct Gaussian clouds (1 GB of host data instead of 8 GB);
+    every pair still runs its 3 full solves."""
+    import torch
+
+    import paper_2602_03067_b200 as fsk
+
+    n, m, d, eps, iters = CONFIGS[cfgname]
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    rng = np.random.default_rng(1000)
+    clouds = [rng.standard_normal((n, d)) for _ in range(16)]
+    w = np.full(n, 1.0 / n)
+    pairs = [(clouds[k % 16], w, clouds[(k * 7 + 3) % 16], w) for k in range(CFG5_PAIRS)]
+    os.environ.setdefault("FSK_TENSOR_MODE", args.mode)
+    for _ in range(args.warmup):
+        fsk.sinkhorn_divergence_batch(pairs[:2], eps=eps, max_iters=iters)
+    sampler = ClockSampler([0])
+    sampler.start()
+    launches0 = fsk.Engine.launches()
+    times = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out = fsk.sinkhorn_divergence_batch(pairs, eps=eps, max_iters=iters)
+        times.append(time.perf_counter() - t0)
+    launches = fsk.Engine.launches() - launches0
+    clocks = sampler.stop()
+    step_s = statistics.median(times)
+    its = CFG5_PAIRS * 3 * iters
+    value = its / step_s
+    h2d = sum(2 * (X.nbytes + a.nbytes + Y.nbytes + b.nbytes) for (X, a, Y, b) in pairs)
+    line = {
+        "metric": metric_name(cfgname), "value": value, "unit": "iterations/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (16 Gaussian clouds, 64 pairs), uniform weights",
+        "config": dict(workload_config(cfgname), parallelism="1 GPU, pairs sequential",
+                       api="fsk_sinkhorn_divergence_batch (C ABI, host buffers)"),
+        "pairs_per_s": CFG5_PAIRS / step_s, "divergence_mean": float(np.mean(out)),
+        "gpu_launches": launches, "clocks": clocks,
+        "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(out.nbytes),
+                "api": "value is itself end to end (host buffers in, divergences out)"},
+    }
+    if args.cpu_baseline:
+        cb = reference_sample(cfgname)
+        line["cpu_baseline"] = {"value": cb["iters"] / cb["step_s"], "unit": "iterations/s",
+                                "cores": cb["threads"], "kind": "reference",
+                                "sample": cb["sample"], "library": cb["so"]}
+    print(json.dumps(line), flush=True)
     return 0
 
 
@@ -416,6 +525,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args, args.config)
+    if STEP_TAIL[args.config] == "divergence":
+        return run_b200_divergence(args, args.config)
     return run_b200(args, args.config)
 
 
