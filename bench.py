@@ -113,6 +113,15 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- inputs ------
 
+def uniform_weights(n):
+    """1/n weights whose naive running sum passes the reference's |sum - 1| <= 1e-12
+    check (core.cpp:27-33): plain 1/n fails at n = 1e5 (SURVEY §0 finding 4), so
+    the last weight absorbs the sequential-sum residual."""
+    w = np.full(n, 1.0 / n)
+    w[-1] = 1.0 - np.cumsum(w[:-1])[-1] if n > 1 else 1.0
+    return w
+
+
 def make_inputs(n, m, d, seed=1000):
     """fsk::Rng(seed).normal(): X (n x d) then Y (m x d), row-major."""
     import paper_2602_03067_b200 as fsk
@@ -270,8 +279,8 @@ def run_b200(args, cfgname):
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     X, Y = make_inputs(n, m, d)
-    a = np.full(n, 1.0 / n)
-    b = np.full(m, 1.0 / m)
+    a = uniform_weights(n)
+    b = uniform_weights(m)
     eng = fsk.Engine(local, X, a, Y, b, mode=args.mode)
     eng.set_eps(eps)
     plan = ShardPlan(rank, world, n, m)
@@ -470,7 +479,7 @@ def run_b200_divergence(args, cfgname):
         return 0
     rng = np.random.default_rng(1000)
     clouds = [rng.standard_normal((n, d)) for _ in range(16)]
-    w = np.full(n, 1.0 / n)
+    w = uniform_weights(n)
     pairs = [(clouds[k % 16], w, clouds[(k * 7 + 3) % 16], w) for k in range(CFG5_PAIRS)]
     os.environ.setdefault("FSK_TENSOR_MODE", args.mode)
     for _ in range(args.warmup):
