@@ -242,6 +242,14 @@ int fsk_hvp_apply(const fsk_measure* src, const fsk_measure* tgt, const double* 
                   const double* g_hat, double eps, const fsk_cost* cost, const double* A,
                   const fsk_hvp_config* hcfg, const fsk_tiles* tiles, fsk_ledger* ledger,
                   double* out, fsk_hvp_report* hrep);
+/* Same contract in single precision (the paper's strict-FP32 HVP):
+ * fp32 device problem; when the tensor path is enabled (FSK_TENSOR_MODE / d >= 32)
+ * every transport-vector application runs on the tcgen05 split-fp16 kernel.
+ * Squared-Euclidean cost only. */
+int fsk_hvp_apply_single(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat,
+                         const double* g_hat, double eps, const fsk_cost* cost, const double* A,
+                         const fsk_hvp_config* hcfg, const fsk_tiles* tiles, fsk_ledger* ledger,
+                         double* out, fsk_hvp_report* hrep);
 
 /* ---- device engine (device-resident, sharded; used for multi-GPU) ---------- */
 
@@ -273,6 +281,11 @@ int fsk_engine_half_step(fsk_engine* e, int side, int64_t row_begin, int64_t row
 /* Gradient w.r.t. X for rows [row_begin,row_end): grad_dev (float, (end-begin) x d). */
 int fsk_engine_grad(fsk_engine* e, int64_t row_begin, int64_t row_end, float* grad_dev,
                     void* stream);
+/* Transport-vector application at the bound potentials: out_dev (double, device)
+ * = P v (side 0, v indexed by Y, out by X) or P^T v (side 1). One LSE pass for the
+ * row marginal, then the tcgen05 VEC pass (or the fp32 CUDA-core apply). */
+int fsk_engine_transport_vec(fsk_engine* e, int side, const float* v_dev, double* out_dev,
+                             void* stream);
 /* Launch counter of this engine's kernels (for bench accounting). */
 int64_t fsk_engine_kernel_launches(const fsk_engine* e);
 /* Name of the kernel path the engine uses for half-steps ("tcgen05-split3" / "fma-f32"). */

@@ -410,17 +410,19 @@ def barycentric_projection(X, a, Y, b, f_hat, g_hat, eps, tiles=(64, 64), cost=N
 
 
 def hvp_apply(X, a, Y, b, f_hat, g_hat, eps, A, tau=1e-5, cg_tol=1e-6, cg_max_iters=50,
-              tiles=(64, 64), cost=None, ledger=None):
+              tiles=(64, 64), cost=None, ledger=None, precision="double"):
+    """SPEC hvp_apply. precision="single" runs the fp32 engine
+    (tcgen05 transport-vector applications when the tensor path is enabled)."""
     k = _Keep()
     src, tgt = k.measure(X, a), k.measure(Y, b)
     f, g, A = k.arr(f_hat), k.arr(g_hat), k.arr(A)
     out = np.empty((src.n, src.d))
     h = _HvpConfig(tau, cg_tol, cg_max_iters)
     rep = _HvpReport()
-    _check(lib().fsk_hvp_apply(C.byref(src), C.byref(tgt), C.c_void_p(f.ctypes.data),
-                               C.c_void_p(g.ctypes.data), C.c_double(eps), C.byref(k.cost(cost)),
-                               C.c_void_p(A.ctypes.data), C.byref(h), C.byref(_tiles(tiles)),
-                               _lp(ledger), C.c_void_p(out.ctypes.data), C.byref(rep)))
+    fn = lib().fsk_hvp_apply_single if precision == "single" else lib().fsk_hvp_apply
+    _check(fn(C.byref(src), C.byref(tgt), C.c_void_p(f.ctypes.data), C.c_void_p(g.ctypes.data),
+              C.c_double(eps), C.byref(k.cost(cost)), C.c_void_p(A.ctypes.data), C.byref(h),
+              C.byref(_tiles(tiles)), _lp(ledger), C.c_void_p(out.ctypes.data), C.byref(rep)))
     return out, dict(cg_iters=rep.cg_iters, cg_rel_residual=rep.cg_rel_residual,
                      converged=bool(rep.converged))
 
@@ -491,6 +493,11 @@ class Engine:
                                           C.c_int64(row_end),
                                           C.c_void_p(viol_ptr) if viol_ptr else None,
                                           C.c_void_p(stream)))
+
+    def transport_vec(self, side: int, v_ptr: int, out_ptr: int, stream: int = 0):
+        """out (double, device) = P v (side 0) or P^T v (side 1) at the bound potentials."""
+        _check(lib().fsk_engine_transport_vec(self.h, C.c_int(side), C.c_void_p(v_ptr),
+                                              C.c_void_p(out_ptr), C.c_void_p(stream)))
 
     def grad(self, row_begin: int, row_end: int, grad_ptr: int, stream: int = 0):
         _check(lib().fsk_engine_grad(self.h, C.c_int64(row_begin), C.c_int64(row_end),

@@ -177,6 +177,47 @@ int fsk_engine_grad(fsk_engine* e, int64_t row_begin, int64_t row_end, float* gr
     });
 }
 
+int fsk_engine_transport_vec(fsk_engine* e, int side, const float* v_dev, double* out_dev,
+                             void* stream) {
+    return eguard([&] {
+        if (!e->f || !e->g) throw ValidationFailure("engine potentials not bound");
+        if (side != 0 && side != 1) throw ValidationFailure("side must be 0 or 1");
+        cudaStream_t s = pick(e, stream);
+        e->P.s = s;
+        const float eps = float(e->eps);
+        const int64_t R = side == 0 ? e->P.src.n : e->P.tgt.n;
+        const float* kpot = side == 0 ? e->g : e->f;
+        const float* pot = side == 0 ? e->f : e->g;
+        DevBuf<float> marg(size_t(R), s), lse(size_t(R), s), mx(size_t(R), s);
+        DevBuf<float> l2h, l2l;
+        FinalizeArgs<float> fa{};
+        fa.eps = eps;
+        fa.flags = e->flags;
+        fa.old_pot = pot;
+        fa.w = side == 0 ? e->P.src.w.get() : e->P.tgt.w.get();
+        fa.out_marg = marg.get();
+        fa.marg_flag = side == 0 ? kFlagNonFiniteRowMarginal : kFlagNonFiniteColMarginal;
+        fa.out_lse = lse.get();
+        fa.out_max = mx.get();
+        if (e->P.tc) {
+            l2h.alloc(size_t(R), s);
+            l2l.alloc(size_t(R), s);
+            fa.out_l2h = l2h.get();
+            fa.out_l2l = l2l.get();
+        }
+        half_step_rows<float>(e->P, side, kpot, eps, fa, 0, R);
+        if (e->P.tc) {
+            e->P.tc->vec(e->P, side, kpot, eps, l2h.get(), l2l.get(), marg.get(), v_dev, out_dev,
+                         e->flags);
+        } else {
+            DevBuf<float> outf(size_t(R), s);
+            transport<float>(e->P, side, kpot, pot, eps, lse.get(), mx.get(), v_dev, 1, nullptr,
+                             nullptr, 0, outf.get(), e->flags);
+            launch_f32_to_f64(outf.get(), out_dev, R, s);
+        }
+    });
+}
+
 int64_t fsk_engine_kernel_launches(const fsk_engine* e) {
     (void)e;
     return launch_counter();

@@ -6,6 +6,7 @@
 // (PY, P^T A, P(diag(w2) Y)) and 1 Hadamard-weighted transport.
 #include <cmath>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/fsk_b200.h"
@@ -13,6 +14,9 @@
 #include "core_kernels.h"
 #include "device_ops.h"
 #include "hostlib.h"
+#include "tc_engine.h"
+
+int tensor_mode_from_env();
 
 namespace fskb {
 extern thread_local std::string g_err;
@@ -22,43 +26,79 @@ using namespace fskb;
 
 namespace {
 
+template <typename T>
+std::vector<T> to_t(const double* p, int64_t n) {
+    return std::vector<T>(p, p + n);
+}
+
+// T = double: the fp64 CUDA-core engine (reference tolerances).
+// T = float: single precision; with the tcgen05 path enabled every
+// transport-vector application (2 K_CG + 3 per HVP) runs on the split-fp16
+// tensor-core kernel (K1 VEC mode), transport-matrix / Hadamard ones on the
+// fp32 CUDA-core kernels.
+template <typename T>
 struct HvpCtx {
     const fsk_measure& src;
     const fsk_measure& tgt;
-    DevProblem<double>& P;
+    DevProblem<T>& P;
     ExecCtx& C;
     double eps;
-    const double* fd;
-    const double* gd;
-    const double* lse_f;
-    const double* mx_f;
-    const double* lse_g;
-    const double* mx_g;
+    const T* fd;
+    const T* gd;
+    const T* lse_f;
+    const T* mx_f;
+    const T* lse_g;
+    const T* mx_g;
     fsk_ledger* ledger;
     const fsk_tiles& tiles;
     const fsk_cost* cost;
+    const float* l2h[2] = {nullptr, nullptr};   // tensor path: log2 LSE per orientation
+    const float* l2l[2] = {nullptr, nullptr};
+    const T* marg[2] = {nullptr, nullptr};      // r (side 0), c (side 1)
 
     // side 0: out (n x p) = P V ; side 1: out (m x p) = P^T V
     std::vector<double> apply(int side, const std::vector<double>& V, int64_t p,
                               const double* A = nullptr, const double* B = nullptr, int64_t r = 0) {
         const int64_t rows = side == 0 ? src.n : tgt.n, cols = side == 0 ? tgt.n : src.n;
-        DevBuf<double> Vd(size_t(cols * p), C.s), out(size_t(rows * p), C.s);
-        Vd.upload(V.data(), size_t(cols * p));
-        DevBuf<double> Ad, Bd;
-        if (A) {
-            Ad.alloc(size_t(src.n * r), C.s);
-            Ad.upload(A, size_t(src.n * r));
-            Bd.alloc(size_t(tgt.n * r), C.s);
-            Bd.upload(B, size_t(tgt.n * r));
-        }
-        const double* kpot = side == 0 ? gd : fd;
-        const double* pot = side == 0 ? fd : gd;
-        transport<double>(P, side, kpot, pot, eps, side == 0 ? lse_f : lse_g,
-                          side == 0 ? mx_f : mx_g, Vd.get(), p, Ad.get(), Bd.get(), r, out.get(),
-                          C.flags);
+        const T* kpot = side == 0 ? gd : fd;
+        const T* pot = side == 0 ? fd : gd;
         std::vector<double> h((size_t)(rows * p));
-        out.download(h.data(), h.size());
-        FSKB_CUDA(cudaStreamSynchronize(C.s));
+        bool done = false;
+        if constexpr (std::is_same_v<T, float>) {
+            if (P.tc && !A && p == 1) {
+                DevBuf<float> vd(size_t(cols), C.s);
+                const std::vector<float> vf(V.begin(), V.end());
+                vd.upload(vf.data(), size_t(cols));
+                DevBuf<double> out(size_t(rows), C.s);
+                P.s = C.s;
+                P.tc->vec(P, side, kpot, float(eps), l2h[side], l2l[side], marg[side], vd.get(),
+                          out.get(), C.flags);
+                out.download(h.data(), h.size());
+                FSKB_CUDA(cudaStreamSynchronize(C.s));
+                done = true;
+            }
+        }
+        if (!done) {
+            DevBuf<T> Vd(size_t(cols * p), C.s), out(size_t(rows * p), C.s);
+            const std::vector<T> Vt(V.begin(), V.end());
+            Vd.upload(Vt.data(), size_t(cols * p));
+            DevBuf<T> Ad, Bd;
+            if (A) {
+                const std::vector<T> At = to_t<T>(A, src.n * r), Bt = to_t<T>(B, tgt.n * r);
+                Ad.alloc(size_t(src.n * r), C.s);
+                Ad.upload(At.data(), size_t(src.n * r));
+                Bd.alloc(size_t(tgt.n * r), C.s);
+                Bd.upload(Bt.data(), size_t(tgt.n * r));
+                FSKB_CUDA(cudaStreamSynchronize(C.s));
+            }
+            transport<T>(P, side, kpot, pot, T(eps), side == 0 ? lse_f : lse_g,
+                         side == 0 ? mx_f : mx_g, Vd.get(), p, Ad.get(), Bd.get(), r, out.get(),
+                         C.flags);
+            std::vector<T> ht((size_t)(rows * p));
+            out.download(ht.data(), ht.size());
+            FSKB_CUDA(cudaStreamSynchronize(C.s));
+            h.assign(ht.begin(), ht.end());
+        }
         if (A)
             ledger_hadamard(ledger, src.n, tgt.n, src.d, r, p, tiles, cost);
         else
@@ -73,13 +113,11 @@ double dotv(const std::vector<double>& a, const std::vector<double>& b) {
     return s;
 }
 
-}  // namespace
-
-extern "C" int fsk_hvp_apply(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat,
-                             const double* g_hat, double eps, const fsk_cost* cost,
-                             const double* A, const fsk_hvp_config* hcfg, const fsk_tiles* tiles,
-                             fsk_ledger* ledger, double* out, fsk_hvp_report* hrep) {
-    try {
+template <typename T>
+void hvp_run(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat,
+             const double* g_hat, double eps, const fsk_cost* cost, const double* A,
+             const fsk_hvp_config* hcfg, const fsk_tiles* tiles, fsk_ledger* ledger, double* out,
+             fsk_hvp_report* hrep) {
         if (!src || !tgt || !hcfg) throw ValidationFailure("null argument");
         validate_problem_raw(*src, *tgt, cost);
         validate_tiles_raw(tiles);
@@ -88,18 +126,35 @@ extern "C" int fsk_hvp_apply(const fsk_measure* src, const fsk_measure* tgt, con
         if (!(hcfg->cg_tol > 0.0)) throw ValidationFailure("hvp: cg_tol must be positive");
         if (hcfg->cg_max_iters < 1) throw ValidationFailure("hvp: cg_max_iters must be positive");
         if (!all_finite(A, src->n * src->d)) throw ValidationFailure("hvp: non-finite direction");
+        constexpr bool kSingle = std::is_same_v<T, float>;
+        if (kSingle && cost && cost->kind != 0)
+            throw ValidationFailure("single-precision hvp supports the squared-Euclidean cost only");
         const int64_t n = src->n, m = tgt->n, d = src->d;
         auto& C = exec_ctx();
-        DevProblem<double> P;
+        DevProblem<T> P;
         P.upload(*src, *tgt, cost, C.s);
-        DevBuf<double> f(size_t(n), C.s), g(size_t(m), C.s);
-        f.upload(f_hat, size_t(n));
-        g.upload(g_hat, size_t(m));
-        DevBuf<double> lse_f(size_t(n), C.s), mx_f(size_t(n), C.s), r_d(size_t(n), C.s);
-        DevBuf<double> lse_g(size_t(m), C.s), mx_g(size_t(m), C.s), c_d(size_t(m), C.s);
+        DevBuf<float> l2h_f, l2l_f, l2h_g, l2l_g;
+        if constexpr (kSingle) {
+            if (enable_tensor_path(P, tensor_mode_from_env())) {
+                P.tc->set_eps(P, eps);
+                l2h_f.alloc(size_t(n), C.s);
+                l2l_f.alloc(size_t(n), C.s);
+                l2h_g.alloc(size_t(m), C.s);
+                l2l_g.alloc(size_t(m), C.s);
+            }
+        }
+        DevBuf<T> f(size_t(n), C.s), g(size_t(m), C.s);
+        {
+            const std::vector<T> ft = to_t<T>(f_hat, n), gt = to_t<T>(g_hat, m);
+            f.upload(ft.data(), size_t(n));
+            g.upload(gt.data(), size_t(m));
+            FSKB_CUDA(cudaStreamSynchronize(C.s));
+        }
+        DevBuf<T> lse_f(size_t(n), C.s), mx_f(size_t(n), C.s), r_d(size_t(n), C.s);
+        DevBuf<T> lse_g(size_t(m), C.s), mx_g(size_t(m), C.s), c_d(size_t(m), C.s);
         // workspace: induced marginals (and the per-orientation LSE, cached)
-        FinalizeArgs<double> fa{};
-        fa.eps = eps;
+        FinalizeArgs<T> fa{};
+        fa.eps = T(eps);
         fa.flags = C.flags;
         fa.out_lse = lse_f.get();
         fa.out_max = mx_f.get();
@@ -107,9 +162,11 @@ extern "C" int fsk_hvp_apply(const fsk_measure* src, const fsk_measure* tgt, con
         fa.w = P.src.w.get();
         fa.out_marg = r_d.get();
         fa.marg_flag = kFlagNonFiniteRowMarginal;
-        half_step<double>(P, 0, g.get(), eps, fa);
-        FinalizeArgs<double> fb{};
-        fb.eps = eps;
+        fa.out_l2h = l2h_f.get();
+        fa.out_l2l = l2l_f.get();
+        half_step<T>(P, 0, g.get(), T(eps), fa);
+        FinalizeArgs<T> fb{};
+        fb.eps = T(eps);
         fb.flags = C.flags;
         fb.out_lse = lse_g.get();
         fb.out_max = mx_g.get();
@@ -117,18 +174,31 @@ extern "C" int fsk_hvp_apply(const fsk_measure* src, const fsk_measure* tgt, con
         fb.w = P.tgt.w.get();
         fb.out_marg = c_d.get();
         fb.marg_flag = kFlagNonFiniteColMarginal;
-        half_step<double>(P, 1, f.get(), eps, fb);
+        fb.out_l2h = l2h_g.get();
+        fb.out_l2l = l2l_g.get();
+        half_step<T>(P, 1, f.get(), T(eps), fb);
         ledger_marginals(ledger, n, m, d, *tiles, cost);
         std::vector<double> r((size_t)(n)), c((size_t)(m));
-        r_d.download(r.data(), r.size());
-        c_d.download(c.data(), c.size());
-        FSKB_CUDA(cudaStreamSynchronize(C.s));
+        {
+            std::vector<T> rt((size_t)(n)), ct((size_t)(m));
+            r_d.download(rt.data(), rt.size());
+            c_d.download(ct.data(), ct.size());
+            FSKB_CUDA(cudaStreamSynchronize(C.s));
+            r.assign(rt.begin(), rt.end());
+            c.assign(ct.begin(), ct.end());
+        }
         throw_for_flags(read_and_clear_flags(C));
         for (double v : r)
             if (!(v > 0.0)) throw NumericalFailure("hvp: zero induced row marginal");
 
-        HvpCtx H{*src, *tgt, P, C, eps, f.get(), g.get(), lse_f.get(), mx_f.get(), lse_g.get(),
-                 mx_g.get(), ledger, *tiles, cost};
+        HvpCtx<T> H{*src, *tgt, P, C, eps, f.get(), g.get(), lse_f.get(), mx_f.get(),
+                    lse_g.get(), mx_g.get(), ledger, *tiles, cost};
+        H.l2h[0] = l2h_f.get();
+        H.l2l[0] = l2l_f.get();
+        H.l2h[1] = l2h_g.get();
+        H.l2l[1] = l2l_g.get();
+        H.marg[0] = r_d.get();
+        H.marg[1] = c_d.get();
         const std::vector<double> X(src->points, src->points + n * d);
         const std::vector<double> Y(tgt->points, tgt->points + m * d);
         const std::vector<double> Av(A, A + n * d);
@@ -226,6 +296,12 @@ extern "C" int fsk_hvp_apply(const fsk_measure* src, const fsk_measure* tgt, con
             hrep->cg_rel_residual = relres;
             hrep->converged = converged ? 1 : 0;
         }
+}
+
+template <typename F>
+int hvp_guard(F&& f) {
+    try {
+        f();
         return FSK_OK;
     } catch (const ValidationFailure& e) {
         g_err = e.what();
@@ -237,4 +313,25 @@ extern "C" int fsk_hvp_apply(const fsk_measure* src, const fsk_measure* tgt, con
         g_err = e.what();
         return FSK_ECUDA;
     }
+}
+
+}  // namespace
+
+extern "C" int fsk_hvp_apply(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat,
+                             const double* g_hat, double eps, const fsk_cost* cost,
+                             const double* A, const fsk_hvp_config* hcfg, const fsk_tiles* tiles,
+                             fsk_ledger* ledger, double* out, fsk_hvp_report* hrep) {
+    return hvp_guard([&] {
+        hvp_run<double>(src, tgt, f_hat, g_hat, eps, cost, A, hcfg, tiles, ledger, out, hrep);
+    });
+}
+
+extern "C" int fsk_hvp_apply_single(const fsk_measure* src, const fsk_measure* tgt,
+                                    const double* f_hat, const double* g_hat, double eps,
+                                    const fsk_cost* cost, const double* A,
+                                    const fsk_hvp_config* hcfg, const fsk_tiles* tiles,
+                                    fsk_ledger* ledger, double* out, fsk_hvp_report* hrep) {
+    return hvp_guard([&] {
+        hvp_run<float>(src, tgt, f_hat, g_hat, eps, cost, A, hcfg, tiles, ledger, out, hrep);
+    });
 }

@@ -50,13 +50,14 @@ constexpr uint32_t OFF_Q = 0;
 constexpr uint32_t OFF_ONES = 2 * QTILE;                       // 64 KB
 constexpr uint32_t OFF_K = OFF_ONES + BIAS;                    // 68 KB
 constexpr uint32_t OFF_BAR = OFF_K + STAGES * KSTAGE;          // 212 KB
-constexpr uint32_t SMEM_BYTES = OFF_BAR + 256 + 1024;          // + barriers + align slack
+constexpr uint32_t VBUF = 8 * TILE * 4;                        // per epilogue warp: 128 floats
+constexpr uint32_t SMEM_BYTES = OFF_BAR + 256 + VBUF + 1024;   // + barriers, v buffers, slack
 // chunked layout (d > 64): stage = Q chunk of 2 query tiles + key chunk + bias
 constexpr int CSTAGES = 2;
 constexpr uint32_t CSTAGE = 3 * QTILE + BIAS;                  // 100 KB
 constexpr uint32_t C_OFF_ONES = CSTAGES * CSTAGE;              // 200 KB
 constexpr uint32_t C_OFF_BAR = C_OFF_ONES + BIAS;              // 204 KB
-constexpr uint32_t C_SMEM_BYTES = C_OFF_BAR + 256 + 1024;
+constexpr uint32_t C_SMEM_BYTES = C_OFF_BAR + 256 + VBUF + 1024;
 constexpr float kSkipLog2 = 64.0f;  // LSE tiles entirely 2^-64 below the running max are skipped
 
 struct TcParams {
@@ -75,6 +76,11 @@ struct TcParams {
     double* part_s;              // [splits][R] sum exp(S - max)
     int break_lse;
     int chunks;                  // 64-wide feature chunks per row (images are [tile][chunk])
+    // transport-vector mode (VEC): out_i = sum_j 2^(t_ij - L_i) v_j with the row
+    // LSE L_i known (log2 units, hi + lo); the sum goes to part_m[split][row]
+    const float* l2h;
+    const float* l2l;
+    const float* vvec;           // [key_valid] values on the key side
 };
 
 // CHUNKED = false: d <= 64, the query tile pair stays resident for a work item
@@ -82,7 +88,8 @@ struct TcParams {
 // CHUNKED = true: d > 64, every (key tile, feature chunk) step streams the
 // query chunk of both tiles with the key chunk (100 KB stages, 2-deep ring);
 // the score accumulates over chunks in TMEM before the epilogue sees it.
-template <bool CHUNKED>
+// VEC = true: transport-vector pass (P v / P^T u) over the same score tiles.
+template <bool CHUNKED, bool VEC>
 __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -234,6 +241,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
             const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
             float M = -INFINITY;
             double S = 0.0;
+            const int64_t row = int64_t(qt0 + t) * TILE + quarter * 32 + lane;
+            float nlh = 0.0f, nll = 0.0f;
+            float* vb = reinterpret_cast<float*>(sbase + BAR_OFF + 256) + (warp - 2) * TILE;
+            if constexpr (VEC) {
+                const bool live = t < nq && row < p.R;
+                nlh = live ? -p.l2h[row] : -3.0e38f;
+                nll = live ? -p.l2l[row] : 0.0f;
+            }
             for (int kt = kt0; kt < kt1; ++kt, ++acc_it) {
                 const int b = acc_it & 1;
                 const uint32_t aph = (acc_it >> 1) & 1;
@@ -269,30 +284,65 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
                     mx3 = fmaxf(mx3, __uint_as_float(v[j + 3]));
                 }
                 const float umax = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * p.acc_scale;
-                if (umax > M) {
-                    if (S != 0.0) S *= double(ex2(p.break_lse ? umax - M : M - umax));
-                    M = umax;
-                }
-                // every term of this tile is < 2^-64 of the running max for all 32 rows
-                // of the warp: the whole tile adds < m 2^-64 relative - below rounding
-                const bool dead = M == -INFINITY;
-                if (__all_sync(0xffffffffu, dead || umax < M - kSkipLog2)) continue;
-                const float nm = dead ? 0.0f : -M;
-                float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+                if constexpr (VEC) {
+                    // P~ = 2^(t - L) <= 1; a tile whose P~ are all < 2^-64 for the warp's
+                    // rows adds < m 2^-64 max|v| - below the fp32 result's rounding
+                    if (__all_sync(0xffffffffu, umax + nlh < -kSkipLog2)) continue;
+                    // the tile's 128 values of v, broadcast through a per-warp buffer
+                    float4 vv = make_float4(0.f, 0.f, 0.f, 0.f);
+                    const int64_t j0 = kbase + 4 * lane;
+                    if (j0 + 3 < p.key_valid) {
+                        vv = *reinterpret_cast<const float4*>(p.vvec + j0);
+                    } else {
+                        if (j0 < p.key_valid) vv.x = p.vvec[j0];
+                        if (j0 + 1 < p.key_valid) vv.y = p.vvec[j0 + 1];
+                        if (j0 + 2 < p.key_valid) vv.z = p.vvec[j0 + 2];
+                    }
+                    reinterpret_cast<float4*>(vb)[lane] = vv;
+                    __syncwarp();
+                    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
-                for (int j = 0; j < 128; j += 4) {
-                    s0 += ex2(fmaf(__uint_as_float(v[j]), p.acc_scale, nm));
-                    s1 += ex2(fmaf(__uint_as_float(v[j + 1]), p.acc_scale, nm));
-                    s2 += ex2(fmaf(__uint_as_float(v[j + 2]), p.acc_scale, nm));
-                    s3 += ex2(fmaf(__uint_as_float(v[j + 3]), p.acc_scale, nm));
+                    for (int j = 0; j < 128; j += 4) {
+                        const float4 w = reinterpret_cast<const float4*>(vb)[j >> 2];
+                        s0 = fmaf(ex2(fmaf(__uint_as_float(v[j]), p.acc_scale, nlh) + nll), w.x, s0);
+                        s1 = fmaf(ex2(fmaf(__uint_as_float(v[j + 1]), p.acc_scale, nlh) + nll), w.y,
+                                  s1);
+                        s2 = fmaf(ex2(fmaf(__uint_as_float(v[j + 2]), p.acc_scale, nlh) + nll), w.z,
+                                  s2);
+                        s3 = fmaf(ex2(fmaf(__uint_as_float(v[j + 3]), p.acc_scale, nlh) + nll), w.w,
+                                  s3);
+                    }
+                    S += double((s0 + s1) + (s2 + s3));
+                    __syncwarp();
+                } else {
+                    if (umax > M) {
+                        if (S != 0.0) S *= double(ex2(p.break_lse ? umax - M : M - umax));
+                        M = umax;
+                    }
+                    // every term of this tile is < 2^-64 of the running max for all 32
+                    // rows of the warp: the whole tile adds < m 2^-64 relative
+                    const bool dead = M == -INFINITY;
+                    if (__all_sync(0xffffffffu, dead || umax < M - kSkipLog2)) continue;
+                    const float nm = dead ? 0.0f : -M;
+                    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+                    for (int j = 0; j < 128; j += 4) {
+                        s0 += ex2(fmaf(__uint_as_float(v[j]), p.acc_scale, nm));
+                        s1 += ex2(fmaf(__uint_as_float(v[j + 1]), p.acc_scale, nm));
+                        s2 += ex2(fmaf(__uint_as_float(v[j + 2]), p.acc_scale, nm));
+                        s3 += ex2(fmaf(__uint_as_float(v[j + 3]), p.acc_scale, nm));
+                    }
+                    S += double((s0 + s1) + (s2 + s3));
                 }
-                S += double((s0 + s1) + (s2 + s3));
             }
-            const int64_t row = int64_t(qt0 + t) * TILE + quarter * 32 + lane;
             if (t < nq && row >= p.row_begin && row < p.row_end) {
-                // natural-log partials: max_j S_ij = M ln2, sum_j exp(S_ij - max) = S
-                p.part_m[size_t(split) * p.R + row] = double(M) * 0.69314718055994530942;
-                p.part_s[size_t(split) * p.R + row] = S;
+                if constexpr (VEC) {
+                    p.part_m[size_t(split) * p.R + row] = S;
+                } else {
+                    // natural-log partials: max_j S_ij = M ln2, sum_j exp(S_ij - max) = S
+                    p.part_m[size_t(split) * p.R + row] = double(M) * 0.69314718055994530942;
+                    p.part_s[size_t(split) * p.R + row] = S;
+                }
             }
         }
     }
@@ -572,6 +622,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_kernel(const TcApplyP
     }
 }
 
+// transport-vector epilogue: out_i = r_i sum_s part[s][i]  (P v = diag(r) P~ v)
+__global__ void tc_vec_finalize_kernel(const double* __restrict__ part, int splits, int64_t R,
+                                       const float* __restrict__ marg, double* __restrict__ out) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= R) return;
+    double s = 0.0;
+    for (int k = 0; k < splits; ++k) s += part[size_t(k) * R + i];
+    out[i] = double(marg[i]) * s;
+}
+
 // G_i = 2 r_i (x_i - O_i),  O_i = inv_v * sum_s part_o[s][i]
 __global__ void tc_grad_finalize_kernel(const float* __restrict__ part_o, int splits, int64_t R,
                                         int64_t row_begin, int64_t row_end, int64_t d,
@@ -756,9 +816,13 @@ int TcHalfStep::chunks() const { return impl_->chunks; }
 
 TcHalfStep::TcHalfStep(DevProblem<float>& P) : impl_(new Impl()) {
     // per device (the attribute is per-context), cheap enough to set every time
-    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_kernel<false>,
+    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_kernel<false, false>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES)));
-    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_kernel<true>,
+    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_kernel<false, true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES)));
+    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_kernel<true, false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(C_SMEM_BYTES)));
+    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_kernel<true, true>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(C_SMEM_BYTES)));
     FSKB_CUDA(cudaFuncSetAttribute(tc_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(A_SMEM_BYTES)));
@@ -805,18 +869,20 @@ void TcHalfStep::set_eps(DevProblem<float>& P, double eps) {
     }
 }
 
-void TcHalfStep::run(DevProblem<float>& P, int side, const float* kpot, float eps,
-                     const FinalizeArgs<float>& fa, int64_t row_begin, int64_t row_end) {
-    if (row_end <= row_begin) return;
+// One pass of K1 over rows [row_begin, row_end): LSE partials (vec == null) or
+// transport-vector partials (vec = {l2h, l2l, v}) into pm (and ps), per key split.
+int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float eps,
+                     int64_t row_begin, int64_t row_end, const float* const* vec, int* flags,
+                     DevBuf<double>& pm, DevBuf<double>& ps) {
     Impl& I = *impl_;
     const int qc = side == 0 ? 0 : 1, kc = side == 0 ? 1 : 0;
     const DevSide<float>& ks = side == 0 ? P.tgt : P.src;
     const int E = I.eq[qc] + I.ek[side];
     const int k_tiles = int(I.rows_pad[kc] / TILE);
-    // per-half-step bias chunk
+    // per-pass bias chunk (bit-identical scores for the same potentials)
     build_bias<<<unsigned((I.rows_pad[kc] + 255) / 256), 256, 0, P.s>>>(
         kpot, ks.logw.get(), ks.n, I.rows_pad[kc], double(eps), std::ldexp(1.0, -E),
-        I.kbias[side].get(), fa.flags);
+        I.kbias[side].get(), flags);
     FSKB_CUDA(cudaGetLastError());
     count_launch();
 
@@ -842,21 +908,57 @@ void TcHalfStep::run(DevProblem<float>& P, int side, const float* kpot, float ep
     p.R = side == 0 ? P.src.n : P.tgt.n;
     p.acc_scale = std::ldexp(1.0f, E);
     p.break_lse = break_lse_flag() ? 1 : 0;
-    DevBuf<double> pm(size_t(p.splits) * size_t(p.R), P.s), ps(size_t(p.splits) * size_t(p.R), P.s);
+    if (vec) {
+        p.l2h = vec[0];
+        p.l2l = vec[1];
+        p.vvec = vec[2];
+    }
+    pm.alloc(size_t(p.splits) * size_t(p.R), P.s);
+    if (!vec) ps.alloc(size_t(p.splits) * size_t(p.R), P.s);
     p.part_m = pm.get();
     p.part_s = ps.get();
     const int grid = std::min(p.items, sms);
-    if (I.chunks == 1)
-        tc_lse_kernel<false><<<grid, NUM_THREADS, SMEM_BYTES, P.s>>>(p);
-    else
-        tc_lse_kernel<true><<<grid, NUM_THREADS, C_SMEM_BYTES, P.s>>>(p);
+    if (I.chunks == 1) {
+        if (vec)
+            tc_lse_kernel<false, true><<<grid, NUM_THREADS, SMEM_BYTES, P.s>>>(p);
+        else
+            tc_lse_kernel<false, false><<<grid, NUM_THREADS, SMEM_BYTES, P.s>>>(p);
+    } else {
+        if (vec)
+            tc_lse_kernel<true, true><<<grid, NUM_THREADS, C_SMEM_BYTES, P.s>>>(p);
+        else
+            tc_lse_kernel<true, false><<<grid, NUM_THREADS, C_SMEM_BYTES, P.s>>>(p);
+    }
     FSKB_CUDA(cudaGetLastError());
     count_launch();
+    return p.splits;
+}
+
+void TcHalfStep::run(DevProblem<float>& P, int side, const float* kpot, float eps,
+                     const FinalizeArgs<float>& fa, int64_t row_begin, int64_t row_end) {
+    if (row_end <= row_begin) return;
+    DevBuf<double> pm, ps;
+    const int splits = pass(P, side, kpot, eps, row_begin, row_end, nullptr, fa.flags, pm, ps);
     const int64_t rows = row_end - row_begin;
+    const int64_t R = side == 0 ? P.src.n : P.tgt.n;
     FinalizeArgs<float> fb = fa;
-    fb.break_lse = p.break_lse;
+    fb.break_lse = break_lse_flag() ? 1 : 0;
     tc_finalize_kernel<<<unsigned((rows + 255) / 256), 256, 0, P.s>>>(
-        pm.get(), ps.get(), p.splits, p.R, row_begin, row_end, fb);
+        pm.get(), ps.get(), splits, R, row_begin, row_end, fb);
+    FSKB_CUDA(cudaGetLastError());
+    count_launch();
+}
+
+void TcHalfStep::vec(DevProblem<float>& P, int side, const float* kpot, float eps,
+                     const float* l2h, const float* l2l, const float* marg, const float* v,
+                     double* out, int* flags) {
+    const int64_t R = side == 0 ? P.src.n : P.tgt.n;
+    if (R == 0) return;
+    DevBuf<double> pm, ps;
+    const float* args[3] = {l2h, l2l, v};
+    const int splits = pass(P, side, kpot, eps, 0, R, args, flags, pm, ps);
+    tc_vec_finalize_kernel<<<unsigned((R + 255) / 256), 256, 0, P.s>>>(pm.get(), splits, R, marg,
+                                                                        out);
     FSKB_CUDA(cudaGetLastError());
     count_launch();
 }

@@ -44,7 +44,18 @@ public:
     void grad(DevProblem<float>& P, int side, const float* kpot, const float* pot, float eps,
               int64_t row_begin, int64_t row_end, float* G, int* flags);
 
+    // Transport-vector application with fixed potentials: out_i = marg_i sum_j
+    // 2^(t_ij - L_i) v_j = (P v)_i (side 0) or (P^T v)_j (side 1), given the row
+    // LSE of that orientation in log2 units (l2h + l2l) and its induced marginal
+    // (from a `run` with out_l2h/out_l2l/out_marg at the same potentials). v is
+    // indexed by the key side; out (double) by the updated side.
+    void vec(DevProblem<float>& P, int side, const float* kpot, float eps, const float* l2h,
+             const float* l2l, const float* marg, const float* v, double* out, int* flags);
+
 private:
+    int pass(DevProblem<float>& P, int side, const float* kpot, float eps, int64_t row_begin,
+             int64_t row_end, const float* const* vec, int* flags, DevBuf<double>& pm,
+             DevBuf<double>& ps);
     struct Impl;
     Impl* impl_;
 };

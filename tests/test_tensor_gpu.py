@@ -206,3 +206,66 @@ def test_tensor_fused_gradient_cfg2_rows(fsk, port):
     print(f"cfg2 grad rel err gpu {e_gpu:.2e} ref-fp32 {e32:.2e}")
     assert e_gpu <= max(1e-5, 2.0 * e32)
     eng.close()
+
+
+@pytest.mark.parametrize("n,m,d", [(700, 513, 64), (300, 421, 100), (515, 260, 33)])
+@pytest.mark.parametrize("side", [0, 1])
+def test_tensor_transport_vector_parity(fsk, port, n, m, d, side):
+    """K1 VEC mode: P v / P^T u on the tensor cores against the fp64 apply_plan /
+    apply_plan_adjoint (stream.cpp:324-357) at the engine's potentials. Signed v:
+    the bound is relative to (P |v|) so cancellation is not charged to the kernel."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(7 * n + m + d + side)
+    X = rng.normal(size=(n, d)) * 0.4
+    Y = rng.normal(size=(m, d)) * 0.4 + 0.1
+    a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+    eps = 0.5
+    eng = fsk.Engine(0, X, a, Y, b, mode="tensor")
+    eng.set_eps(eps)
+    f = torch.empty(n, dtype=torch.float32, device="cuda")
+    g = torch.empty(m, dtype=torch.float32, device="cuda")
+    eng.bind(f.data_ptr(), g.data_ptr())
+    eng.init_potentials()
+    for _ in range(4):
+        eng.half_step(0, 0, n)
+        eng.half_step(1, 0, m)
+    cols, rows = (m, n) if side == 0 else (n, m)
+    v = rng.normal(size=cols)
+    vd = torch.tensor(v, dtype=torch.float32, device="cuda")
+    out = torch.empty(rows, dtype=torch.float64, device="cuda")
+    eng.transport_vec(side, vd.data_ptr(), out.data_ptr())
+    torch.cuda.synchronize()
+    fh = f.cpu().numpy().astype(np.float64)
+    gh = g.cpu().numpy().astype(np.float64)
+    v32 = v.astype(np.float32).astype(np.float64)
+    fn = port.apply_plan if side == 0 else port.apply_plan_adjoint
+    want = fn(X, a, Y, b, fh, gh, eps, v32[:, None])[:, 0]
+    scale = fn(X, a, Y, b, fh, gh, eps, np.abs(v32)[:, None])[:, 0]
+    err = np.abs(out.cpu().numpy() - want) / scale
+    print(f"transport-vector side {side}: max rel err {err.max():.2e}")
+    assert err.max() <= 1e-5
+    eng.close()
+
+
+@pytest.mark.parametrize("d", [64, 100])
+def test_single_precision_hvp_matches_fp64(fsk, port, tensor_mode, d):
+    """fsk_hvp_apply_single (tcgen05 transport-vector applies, fp32 matrix applies)
+    against the fp64 engine on the same inputs; CG run to convergence in both."""
+    rng = np.random.default_rng(d)
+    n, m = 400, 300
+    X = rng.normal(size=(n, d)) * 0.3
+    Y = rng.normal(size=(m, d)) * 0.3 + 0.05
+    a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+    eps = 0.5
+    s = port.sinkhorn_solve(X, a, Y, b, eps=eps, max_iters=200)
+    f, g = s["f_hat"], s["g_hat"]
+    A = rng.normal(size=X.shape)
+    H64, i64 = fsk.hvp_apply(X, a, Y, b, f, g, eps, A, tau=1e-5, cg_tol=1e-9, cg_max_iters=400)
+    led = fsk.Ledger()
+    H32, i32 = fsk.hvp_apply(X, a, Y, b, f, g, eps, A, tau=1e-5, cg_tol=1e-9, cg_max_iters=400,
+                             precision="single", ledger=led)
+    rel = np.linalg.norm(H32 - H64) / np.linalg.norm(H64)
+    print(f"single-precision HVP d={d}: rel Frobenius {rel:.2e}, CG {i32['cg_iters']} vs "
+          f"{i64['cg_iters']}")
+    assert rel <= 1e-3
+    assert led.transport_vector_applies == 2 * i32["cg_iters"] + 3
