@@ -73,6 +73,8 @@ void transport(DevProblem<T>& P, int side, const T* kpot, const T* pot, T eps, c
 // Enables the tcgen05 path for a float problem when the shape allows it.
 // mode: 0 auto, 1 force FMA, 2 force tensor. Returns true when enabled.
 bool enable_tensor_path(DevProblem<float>& P, int mode);
+// FSK_TENSOR_MODE (auto | fma | tensor) -> the mode argument above (capi.cpp).
+int tensor_mode_from_env();
 const char* tensor_path_name(const DevProblem<float>& P);
 
 }  // namespace fskb

@@ -16,8 +16,6 @@
 #include "hostlib.h"
 #include "tc_engine.h"
 
-int tensor_mode_from_env();
-
 namespace fskb {
 extern thread_local std::string g_err;
 }
