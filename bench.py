@@ -43,10 +43,12 @@ CONFIGS = {
     "cfg4": (100000, 100000, 1024, 0.1, 10),
     "cfg5": (10000, 10000, 784, 0.1, 10),
 }
-# what a step adds after the iterations: the gradient w.r.t. X (cfg1-3), nothing
-# yet for cfg4 (forward only: the tensor-core HVP is not built yet), and for cfg5
-# a step is the whole batch of 64 debiased divergences (3 solves per pair)
-STEP_TAIL = {"cfg1": "grad", "cfg2": "grad", "cfg3": "grad", "cfg4": "fwd", "cfg5": "divergence"}
+# what a step adds after the iterations: the gradient w.r.t. X (cfg1-3), one
+# Hessian-vector product (cfg4: K_CG = 50 fixed, tau = 1e-5, PAPER.md:1614-1616,
+# single-precision engine), and for cfg5 a step is the whole batch of 64
+# debiased divergences (3 solves per pair)
+STEP_TAIL = {"cfg1": "grad", "cfg2": "grad", "cfg3": "grad", "cfg4": "hvp", "cfg5": "divergence"}
+HVP_CG_ITERS = 50
 CFG5_PAIRS = 64
 
 
@@ -199,6 +201,29 @@ def reference_sample(cfgname, threads=None):
         t_apply = time.perf_counter() - t0
         grad_s = t_lse64 * n / rows + t_apply * (n / rows) * (m / cols_apply)
         sample += (f"; gradient = f64 LSE {rows} x {m} + apply_plan(Y) {rows} x {cols_apply}")
+    if tail == "hvp":
+        # the reference ships no HVP (SURVEY §0 finding 5): the SPEC composition is
+        # (2 K + 3) transport-vector + 3 transport-matrix + 1 Hadamard applies of
+        # apply_plan (stream.cpp:324-339, f64); time one vector apply on the row
+        # slice and one matrix apply (p = d) on rows x 4096 columns
+        a64 = np.full(rows, 1.0 / rows)
+        bm = np.full(m, 1.0 / m)
+        fr = ref.update_f_hat(X64[:rows], a64, Y64, bm, g0, eps)
+        v = np.ones((m, 1))
+        t0 = time.perf_counter()
+        ref.apply_plan(X64[:rows], a64, Y64, bm, fr, g0, eps, v)
+        t_vec = time.perf_counter() - t0
+        Ysub = Y64[:cols_apply]
+        bsub = np.full(cols_apply, 1.0 / cols_apply)
+        gsub = -(Ysub ** 2).sum(1)
+        fsub = ref.update_f_hat(X64[:rows], a64, Ysub, bsub, gsub, eps)
+        t0 = time.perf_counter()
+        ref.apply_plan(X64[:rows], a64, Ysub, bsub, fsub, gsub, eps, Ysub)
+        t_mat = time.perf_counter() - t0
+        grad_s = ((2 * HVP_CG_ITERS + 3) * t_vec * n / rows +
+                  4 * t_mat * (n / rows) * (m / cols_apply))
+        sample += (f"; HVP = {2 * HVP_CG_ITERS + 3} x apply_plan(p=1) {rows} x {m} + 4 x "
+                   f"apply_plan(p={d}) {rows} x {cols_apply}")
     sample += "; extrapolated by n/rows, m/cols"
     solves = 3 * CFG5_PAIRS if tail == "divergence" else 1
     if tail == "divergence":
@@ -239,7 +264,7 @@ def metric_name(cfgname):
     if tail == "divergence":
         return (f"Sinkhorn iterations/s ({CFG5_PAIRS} debiased divergences x 3 solves x {iters} "
                 f"iterations per step), n=m={n}, d={d}")
-    what = "+ grad_X " if tail == "grad" else ""
+    what = {"grad": "+ grad_X ", "hvp": "+ 1 HVP "}.get(tail, "")
     nn = "2^20" if n == 1 << 20 else str(n)
     return f"Sinkhorn iterations/s ({iters} alternating iterations {what}per step), n=m={nn}, d={d}"
 
@@ -250,6 +275,7 @@ METRIC = metric_name("cfg3")
 def workload_config(cfgname):
     n, m, d, eps, iters = CONFIGS[cfgname]
     tail = {"grad": " + gradient w.r.t. X", "fwd": " (forward only)",
+            "hvp": f" + one HVP (K_CG = {HVP_CG_ITERS}, tau = 1e-5)",
             "divergence": f" per solve, {CFG5_PAIRS} pairs x 3 solves"}[STEP_TAIL[cfgname]]
     return {"workload": f"{cfgname}: point-cloud EOT n=m={n}, d={d}, eps={eps}, "
                         f"{iters} alternating iterations{tail} per step",
@@ -288,6 +314,8 @@ def run_b200(args, cfgname):
                              dist if world > 1 else None)
     lo, hi = plan.f_bounds[rank]
     grad = torch.empty((max(hi - lo, 1), d), dtype=torch.float32, device="cuda")
+    hvp_dir = np.random.default_rng(7).standard_normal((n, d)) if STEP_TAIL[cfgname] == "hvp" \
+        else None
     sptr = stream.cuda_stream
 
     # the engine launches on its own stream unless given one: pass torch's
@@ -309,6 +337,20 @@ def run_b200(args, cfgname):
             glo, ghi = plan.g_bounds[rank]
             half(1, glo, ghi)
             solver._gather(solver.g, plan.g_per)
+        if STEP_TAIL[cfgname] == "hvp":
+            # SPEC hvp_apply at the step's potentials through the public C ABI
+            # (fsk_hvp_apply_single: tcgen05 transport-vector applies)
+            if events is not None:
+                gev.append(torch.cuda.Event(enable_timing=True))
+                gev[-1].record(stream)
+            fh = solver.f[:n].double().cpu().numpy()
+            gh = solver.g[:m].double().cpu().numpy()
+            fsk.hvp_apply(X, a, Y, b, fh, gh, eps, hvp_dir, tau=1e-5, cg_tol=1e-30,
+                          cg_max_iters=HVP_CG_ITERS, precision="single")
+            if events is not None:
+                gev.append(torch.cuda.Event(enable_timing=True))
+                gev[-1].record(stream)
+            return
         if STEP_TAIL[cfgname] != "grad":
             return
         if events is not None:
@@ -433,7 +475,8 @@ def run_b200(args, cfgname):
                        "all-gather of potentials" if world > 1 else "1 GPU",
                        path=eng.path),
         "half_step_ms": med_half * 1e3,
-        "grad_ms": grad_ms[len(grad_ms) // 2] if grad_ms else None,
+        ("hvp_ms" if STEP_TAIL[cfgname] == "hvp" else "grad_ms"):
+            grad_ms[len(grad_ms) // 2] if grad_ms else None,
         "roofline": {"bound": "tensor" if tensor else "fma", "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                      "kernel": kernel + " (+bias/finalize; CUDA events around each f half-step "
