@@ -195,8 +195,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
                 for (int kt = kt0; kt < kt1; ++kt, ++acc_it) {
-                    const int b = acc_it & 1;
-                    const uint32_t aph = (acc_it >> 1) & 1;
+                    // chunked: one (big, small) accumulator pair per query tile =
+                    // all 512 columns, single-buffered (MMA time per tile >> epilogue)
+                    const int b = CHUNKED ? 0 : (acc_it & 1);
+                    const uint32_t aph = CHUNKED ? (acc_it & 1) : ((acc_it >> 1) & 1);
                     mbar_wait(accempty(b), aph ^ 1);
                     fence_after();
                     if constexpr (CHUNKED) {
@@ -206,7 +208,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
                             fence_after();
                             const uint32_t st = base + s * CSTAGE;
                             for (int t = 0; t < nq; ++t)
-                                issue_score_chunk(tmem + uint32_t((b * 2 + t) * TILE),
+                                issue_score_chunk(tmem + uint32_t(t * 2 * TILE),
+                                                  tmem + uint32_t((t * 2 + 1) * TILE),
                                                   st + t * QTILE, st + 2 * QTILE,
                                                   base + ONES_OFF, st + 3 * QTILE, c == 0);
                             umma_commit(kempty(s));
@@ -250,18 +253,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
                 nll = live ? -p.l2l[row] : 0.0f;
             }
             for (int kt = kt0; kt < kt1; ++kt, ++acc_it) {
-                const int b = acc_it & 1;
-                const uint32_t aph = (acc_it >> 1) & 1;
+                const int b = CHUNKED ? 0 : (acc_it & 1);
+                const uint32_t aph = CHUNKED ? (acc_it & 1) : ((acc_it >> 1) & 1);
                 mbar_wait(accfull(b), aph);
                 fence_after();
                 uint32_t v[128];
                 if (t < nq) {
-                    const uint32_t a0 = tmem + lane_addr + uint32_t((b * 2 + t) * TILE);
-                    FSKB_TMEM_LD32(a0 + 0, (v + 0));
-                    FSKB_TMEM_LD32(a0 + 32, (v + 32));
-                    FSKB_TMEM_LD32(a0 + 64, (v + 64));
-                    FSKB_TMEM_LD32(a0 + 96, (v + 96));
-                    tmem_ld_wait();
+                    if constexpr (CHUNKED) {
+                        // score = big + small accumulator
+                        const uint32_t a0 = tmem + lane_addr + uint32_t(t * 2 * TILE);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            uint32_t w[32];
+                            FSKB_TMEM_LD32(a0 + 32 * q, (v + 32 * q));
+                            FSKB_TMEM_LD32(a0 + TILE + 32 * q, w);
+                            tmem_ld_wait();
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                v[32 * q + j] = __float_as_uint(__uint_as_float(v[32 * q + j]) +
+                                                                __uint_as_float(w[j]));
+                        }
+                    } else {
+                        const uint32_t a0 = tmem + lane_addr + uint32_t((b * 2 + t) * TILE);
+                        FSKB_TMEM_LD32(a0 + 0, (v + 0));
+                        FSKB_TMEM_LD32(a0 + 32, (v + 32));
+                        FSKB_TMEM_LD32(a0 + 64, (v + 64));
+                        FSKB_TMEM_LD32(a0 + 96, (v + 96));
+                        tmem_ld_wait();
+                    }
                 }
                 fence_before();
                 __syncwarp();

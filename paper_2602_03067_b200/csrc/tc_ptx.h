@@ -180,21 +180,24 @@ __device__ __forceinline__ void issue_score_tile(uint32_t d_tmem, uint32_t qa, u
 }
 
 // One 64-wide feature chunk of a score tile for d > 64 (operands streamed chunk
-// by chunk): the bias slice opens the accumulator on the first chunk, then the
-// 8 cross terms and the 4 hi x hi slices of this chunk.
-__device__ __forceinline__ void issue_score_chunk(uint32_t d_tmem, uint32_t qa, uint32_t ka,
-                                                  uint32_t ones, uint32_t bias, bool first) {
-    if (first) umma_ss(d_tmem, umma_desc(ones, 256, 6), umma_desc(bias, 256, 6), IDESC_QK, 0u);
+// by chunk). Two accumulators keep the fp32 rounding at the scale of each part:
+// d_big = bias + sum of hi x hi slices (opened by the bias on the first chunk),
+// d_small = the 8 cross terms per chunk (2^-11 of the score), summed by the
+// epilogue, so only 4 C + 1 additions round at the score's magnitude.
+__device__ __forceinline__ void issue_score_chunk(uint32_t d_big, uint32_t d_small, uint32_t qa,
+                                                  uint32_t ka, uint32_t ones, uint32_t bias,
+                                                  bool first) {
 #pragma unroll
     for (int kk = 0; kk < DPAD / 16; ++kk) {
-        umma_ss(d_tmem, umma_desc(qa + CHUNK + kk * 32, 1024, 2), umma_desc(ka + kk * 32, 1024, 2),
-                IDESC_QK, 1u);
-        umma_ss(d_tmem, umma_desc(qa + kk * 32, 1024, 2), umma_desc(ka + CHUNK + kk * 32, 1024, 2),
+        umma_ss(d_small, umma_desc(qa + CHUNK + kk * 32, 1024, 2), umma_desc(ka + kk * 32, 1024, 2),
+                IDESC_QK, (first && kk == 0) ? 0u : 1u);
+        umma_ss(d_small, umma_desc(qa + kk * 32, 1024, 2), umma_desc(ka + CHUNK + kk * 32, 1024, 2),
                 IDESC_QK, 1u);
     }
+    if (first) umma_ss(d_big, umma_desc(ones, 256, 6), umma_desc(bias, 256, 6), IDESC_QK, 0u);
 #pragma unroll
     for (int kk = 0; kk < DPAD / 16; ++kk)
-        umma_ss(d_tmem, umma_desc(qa + kk * 32, 1024, 2), umma_desc(ka + kk * 32, 1024, 2),
+        umma_ss(d_big, umma_desc(qa + kk * 32, 1024, 2), umma_desc(ka + kk * 32, 1024, 2),
                 IDESC_QK, 1u);
 }
 
