@@ -218,6 +218,10 @@ int fsk_engine_transport_vec(fsk_engine* e, int side, const float* v_dev, double
     });
 }
 
+uint64_t fsk_engine_screen_live_tiles(const fsk_engine* e) {
+    return e && e->P.tc ? uint64_t(e->P.tc->live_tiles()) : 0;
+}
+
 int64_t fsk_engine_kernel_launches(const fsk_engine* e) {
     (void)e;
     return launch_counter();

@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -51,7 +52,9 @@ constexpr uint32_t OFF_ONES = 2 * QTILE;                       // 64 KB
 constexpr uint32_t OFF_K = OFF_ONES + BIAS;                    // 68 KB
 constexpr uint32_t OFF_BAR = OFF_K + STAGES * KSTAGE;          // 212 KB
 constexpr uint32_t VBUF = 8 * TILE * 4;                        // per epilogue warp: 128 floats
-constexpr uint32_t SMEM_BYTES = OFF_BAR + 256 + VBUF + 1024;   // + barriers, v buffers, slack
+constexpr uint32_t SBITS = 4096;                               // screened: live-tile bitmask
+constexpr int kMaxScreenTiles = int(SBITS * 8);
+constexpr uint32_t SMEM_BYTES = OFF_BAR + 256 + VBUF + SBITS + 1024;  // + barriers, buffers, slack
 // chunked layout (d > 64): stage = Q chunk of 2 query tiles + key chunk + bias
 constexpr int CSTAGES = 2;
 constexpr uint32_t CSTAGE = 3 * QTILE + BIAS;                  // 100 KB
@@ -81,6 +84,10 @@ struct TcParams {
     const float* l2h;
     const float* l2l;
     const float* vvec;           // [key_valid] values on the key side
+    // screened LSE (SCREEN): tiles whose approximate (hi x hi + bias) max is below
+    // the running approximate row max - screen_thr for every row are not scored
+    float screen_thr;
+    unsigned long long* live_count;  // += live key tiles (diagnostics), nullable
 };
 
 // CHUNKED = false: d <= 64, the query tile pair stays resident for a work item
@@ -89,8 +96,15 @@ struct TcParams {
 // query chunk of both tiles with the key chunk (100 KB stages, 2-deep ring);
 // the score accumulates over chunks in TMEM before the epilogue sees it.
 // VEC = true: transport-vector pass (P v / P^T u) over the same score tiles.
-template <bool CHUNKED, bool VEC>
-__global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p) {
+// SCREEN = true (d <= 64 LSE only): two phases per work item. Phase 1 runs the
+// 5-MMA approximation t~ = hi x hi + bias over every key tile (20 KB loads) and
+// marks a tile live when some row has max_j t~_ij >= M~_i - screen_thr (M~ the
+// running approximate row max). With |t - t~| <= delta and screen_thr >= 64 +
+// 2 delta, every key within 2^-64 of a row's true max lies in a live tile, so
+// phase 2 - the full 13-MMA split score + online LSE on live tiles only - is the
+// exact pass up to terms below 2^-64 relative.
+template <bool CHUNKED, bool VEC, bool SCREEN = false>
+__global__ void __maxnreg__(200) tc_lse_kernel(const TcParams p) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -106,11 +120,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
     const uint32_t qempty = qfull + 8u;
     auto accfull = [&](int b) { return qempty + 8u + 8u * b; };
     auto accempty = [&](int b) { return qempty + 24u + 8u * b; };
+    const uint32_t screen_done = qempty + 40u;
+    const uint32_t bits_free = qempty + 48u;   // producer + MMA are done reading the bits
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + BAR_OFF + 128);
+    uint32_t* live_bits = reinterpret_cast<uint32_t*>(sbase + BAR_OFF + 256 + VBUF);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     fill_ones_chunk(sbase + ONES_OFF, threadIdx.x, NUM_THREADS);
+    if constexpr (SCREEN)
+        for (int i = threadIdx.x; i < int(SBITS / 4); i += NUM_THREADS) live_bits[i] = 0u;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (threadIdx.x == 0) {
         for (int s = 0; s < NST; ++s) {
@@ -123,6 +142,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
             mbar_init(accfull(b), 1);
             mbar_init(accempty(b), 8);
         }
+        mbar_init(screen_done, 8);
+        mbar_init(bits_free, 2);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -134,6 +155,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
     __syncthreads();
     fence_after();
     const uint32_t tmem = *tmem_slot;
+    // phase-2 tile list of work item `lu` (after screen_done): next live tile >= kt
+    auto next_live = [&](int kt, int kt0, int kt1) {
+        while (kt < kt1) {
+            const int rel = kt - kt0;
+            const uint32_t w = live_bits[rel >> 5] >> (rel & 31);
+            if (w) return kt + __ffs(w) - 1;
+            kt += 32 - (rel & 31);
+        }
+        return kt1;
+    };
 
     const int units = (p.q_tiles + 1) / 2;
     const int ktiles_per_split = (p.k_tiles + p.splits - 1) / p.splits;
@@ -169,7 +200,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
                     mbar_wait(qempty, (lu & 1) ^ 1);
                     mbar_expect_tx(qfull, nq * QTILE);
                     bulk_g2s(base + OFF_Q, p.qimg + size_t(qt0) * QTILE, nq * QTILE, qfull);
-                    for (int kt = kt0; kt < kt1; ++kt, ++it) {
+                    if constexpr (SCREEN) {
+                        // phase 1: hi chunk + bias only
+                        for (int kt = kt0; kt < kt1; ++kt, ++it) {
+                            const int s = it % STAGES;
+                            mbar_wait(kempty(s), ((it / STAGES) & 1) ^ 1);
+                            mbar_expect_tx(kfull(s), CHUNK + BIAS);
+                            const uint32_t dst = base + OFF_K + s * KSTAGE;
+                            bulk_g2s(dst, p.kimg + size_t(kt) * QTILE, CHUNK, kfull(s));
+                            bulk_g2s(dst + QTILE, p.kbias + size_t(kt) * BIAS, BIAS, kfull(s));
+                        }
+                        mbar_wait(screen_done, lu & 1);
+                    }
+                    int nlive = 0;
+                    for (int kt = SCREEN ? next_live(kt0, kt0, kt1) : kt0; kt < kt1;
+                         kt = SCREEN ? next_live(kt + 1, kt0, kt1) : kt + 1, ++it, ++nlive) {
                         const int s = it % STAGES;
                         const uint32_t ph = (it / STAGES) & 1;
                         mbar_wait(kempty(s), ph ^ 1);
@@ -177,6 +222,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
                         const uint32_t dst = base + OFF_K + s * KSTAGE;
                         bulk_g2s(dst, p.kimg + size_t(kt) * QTILE, QTILE, kfull(s));
                         bulk_g2s(dst + QTILE, p.kbias + size_t(kt) * BIAS, BIAS, kfull(s));
+                    }
+                    if constexpr (SCREEN) {
+                        mbar_arrive(bits_free);
+                        if (p.live_count) atomicAdd(p.live_count, (unsigned long long)nlive);
                     }
                 }
             }
@@ -194,7 +243,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
                 }
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
-                for (int kt = kt0; kt < kt1; ++kt, ++acc_it) {
+                if constexpr (SCREEN) {
+                    for (int kt = kt0; kt < kt1; ++kt, ++acc_it, ++it) {
+                        const int b = acc_it & 1;
+                        mbar_wait(accempty(b), ((acc_it >> 1) & 1) ^ 1);
+                        const int s = it % STAGES;
+                        mbar_wait(kfull(s), (it / STAGES) & 1);
+                        fence_after();
+                        const uint32_t kst = base + OFF_K + s * KSTAGE;
+                        for (int t = 0; t < nq; ++t)
+                            issue_screen_tile(tmem + uint32_t((b * 2 + t) * TILE),
+                                              base + OFF_Q + t * QTILE, base + OFF_ONES, kst);
+                        umma_commit(kempty(s));
+                        umma_commit(accfull(b));
+                    }
+                    mbar_wait(screen_done, lu & 1);
+                }
+                for (int kt = SCREEN ? next_live(kt0, kt0, kt1) : kt0; kt < kt1;
+                     kt = SCREEN ? next_live(kt + 1, kt0, kt1) : kt + 1, ++acc_it) {
                     // chunked: one (big, small) accumulator pair per query tile =
                     // all 512 columns, single-buffered (MMA time per tile >> epilogue)
                     const int b = CHUNKED ? 0 : (acc_it & 1);
@@ -227,6 +293,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
                     }
                     umma_commit(accfull(b));
                 }
+                if constexpr (SCREEN) mbar_arrive(bits_free);
                 if constexpr (!CHUNKED) umma_commit(qempty);
             }
         }
@@ -235,8 +302,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
         const int t = (warp - 2) >> 2;
         const int quarter = warp & 3;
         const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
-        int acc_it = 0;
-        for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+        int acc_it = 0, lu = 0;
+        for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++lu) {
             const int unit = item / p.splits, split = item % p.splits;
             const int qt0 = p.q_tile_begin + 2 * unit;
             const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
@@ -245,6 +312,53 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
             float M = -INFINITY;
             double S = 0.0;
             const int64_t row = int64_t(qt0 + t) * TILE + quarter * 32 + lane;
+            if constexpr (SCREEN) {
+                // phase 1: approximate running max, live-tile marking
+                float Ma = -INFINITY;
+                const bool row_ok = t < nq && row < p.R;
+                for (int kt = kt0; kt < kt1; ++kt, ++acc_it) {
+                    const int b = acc_it & 1;
+                    mbar_wait(accfull(b), (acc_it >> 1) & 1);
+                    fence_after();
+                    // only the tile max is needed: stream the 128 columns 32 at a time
+                    float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+                    const int64_t kbase = int64_t(kt) * TILE;
+                    if (t < nq) {
+                        const uint32_t a0 = tmem + lane_addr + uint32_t((b * 2 + t) * TILE);
+#pragma unroll 1
+                        for (int q = 0; q < 4; ++q) {
+                            uint32_t v[32];
+                            FSKB_TMEM_LD32(a0 + 32 * q, v);
+                            tmem_ld_wait();
+                            if (kbase + 32 * q + 32 > p.key_valid) {
+#pragma unroll
+                                for (int j = 0; j < 32; ++j)
+                                    if (kbase + 32 * q + j >= p.key_valid)
+                                        v[j] = __float_as_uint(-INFINITY);
+                            }
+#pragma unroll
+                            for (int j = 0; j < 32; j += 4) {
+                                mx0 = fmaxf(mx0, __uint_as_float(v[j]));
+                                mx1 = fmaxf(mx1, __uint_as_float(v[j + 1]));
+                                mx2 = fmaxf(mx2, __uint_as_float(v[j + 2]));
+                                mx3 = fmaxf(mx3, __uint_as_float(v[j + 3]));
+                            }
+                        }
+                    }
+                    fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(accempty(b));
+                    if (t >= nq) continue;
+                    const float tmax = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * p.acc_scale;
+                    Ma = fmaxf(Ma, tmax);
+                    const bool live = row_ok && tmax >= Ma - p.screen_thr;
+                    if (__any_sync(0xffffffffu, live) && lane == 0)
+                        atomicOr(&live_bits[(kt - kt0) >> 5], 1u << ((kt - kt0) & 31));
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(screen_done);
+                mbar_wait(screen_done, lu & 1);
+            }
             float nlh = 0.0f, nll = 0.0f;
             float* vb = reinterpret_cast<float*>(sbase + BAR_OFF + 256) + (warp - 2) * TILE;
             if constexpr (VEC) {
@@ -252,7 +366,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
                 nlh = live ? -p.l2h[row] : -3.0e38f;
                 nll = live ? -p.l2l[row] : 0.0f;
             }
-            for (int kt = kt0; kt < kt1; ++kt, ++acc_it) {
+            for (int kt = SCREEN ? next_live(kt0, kt0, kt1) : kt0; kt < kt1;
+                 kt = SCREEN ? next_live(kt + 1, kt0, kt1) : kt + 1, ++acc_it) {
                 const int b = CHUNKED ? 0 : (acc_it & 1);
                 const uint32_t aph = CHUNKED ? (acc_it & 1) : ((acc_it >> 1) & 1);
                 mbar_wait(accfull(b), aph);
@@ -353,6 +468,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
                     }
                     S += double((s0 + s1) + (s2 + s3));
                 }
+            }
+            if constexpr (SCREEN) {
+                // recycle the bitmask once nobody reads this item's list any more
+                mbar_wait(bits_free, lu & 1);
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+                for (int i = threadIdx.x - 64; i < int(SBITS / 4); i += 256) live_bits[i] = 0u;
+                asm volatile("bar.sync 1, 256;" ::: "memory");
             }
             if (t < nq && row >= p.row_begin && row < p.row_end) {
                 if constexpr (VEC) {
@@ -778,6 +900,33 @@ __global__ void absmax_kernel(const float* __restrict__ x, int64_t n, unsigned i
     if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
 }
 
+__global__ void rownorm_max_kernel(const float* __restrict__ x, int64_t n, int64_t d,
+                                   unsigned int* out) {
+    float m = 0.0f;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        double s = 0.0;
+        for (int64_t k = 0; k < d; ++k) s += double(x[i * d + k]) * double(x[i * d + k]);
+        m = fmaxf(m, float(sqrt(s)));
+    }
+    for (int off = 16; off >= 1; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+}
+
+float device_rownorm_max(const float* x, int64_t n, int64_t d, cudaStream_t s) {
+    DevBuf<unsigned int> m(1, s);
+    m.zero();
+    rownorm_max_kernel<<<256, 256, 0, s>>>(x, n, d, m.get());
+    FSKB_CUDA(cudaGetLastError());
+    count_launch();
+    unsigned int h = 0;
+    m.download(&h, 1);
+    FSKB_CUDA(cudaStreamSynchronize(s));
+    float f;
+    std::memcpy(&f, &h, 4);
+    return f;
+}
+
 float device_absmax(const float* x, int64_t n, cudaStream_t s) {
     DevBuf<unsigned int> m(1, s);
     m.zero();
@@ -828,16 +977,28 @@ struct TcHalfStep::Impl {
     int ek[2] = {0, 0};
     double eps = 0.0;
     int chunks = 1;                 // 64-wide feature chunks (d > 64: chunked kernels)
+    float rownorm[2] = {0.f, 0.f};  // max_i ||x_i|| of each cloud
+    float screen_thr[2] = {0.f, 0.f};  // per side, log2 units; 0 = no screening
+    DevBuf<unsigned long long> live_count;  // live key tiles of screened passes
 };
 
 bool TcHalfStep::supported(int64_t d) { return d >= 1 && d <= 64 * 64; }
 int TcHalfStep::chunks() const { return impl_->chunks; }
+
+unsigned long long TcHalfStep::live_tiles() const {
+    unsigned long long h = 0;
+    if (impl_->live_count.get())
+        FSKB_CUDA(cudaMemcpy(&h, impl_->live_count.get(), sizeof(h), cudaMemcpyDeviceToHost));
+    return h;
+}
 
 TcHalfStep::TcHalfStep(DevProblem<float>& P) : impl_(new Impl()) {
     // per device (the attribute is per-context), cheap enough to set every time
     FSKB_CUDA(cudaFuncSetAttribute(tc_lse_kernel<false, false>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES)));
     FSKB_CUDA(cudaFuncSetAttribute(tc_lse_kernel<false, true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES)));
+    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_kernel<false, false, true>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES)));
     FSKB_CUDA(cudaFuncSetAttribute(tc_lse_kernel<true, false>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(C_SMEM_BYTES)));
@@ -852,6 +1013,7 @@ TcHalfStep::TcHalfStep(DevProblem<float>& P) : impl_(new Impl()) {
         impl_->npts[c] = sd.n;
         impl_->rows_pad[c] = (sd.n + TILE - 1) / TILE * TILE;
         impl_->maxabs[c] = device_absmax(sd.pts.get(), sd.n * sd.d, P.s);
+        impl_->rownorm[c] = device_rownorm_max(sd.pts.get(), sd.n, sd.d, P.s);
         impl_->eq[c] = scale_exponent(impl_->maxabs[c]);
         const int C = impl_->chunks;
         impl_->qimg[c].alloc(size_t(impl_->rows_pad[c] / TILE) * C * QTILE, P.s);
@@ -869,6 +1031,19 @@ TcHalfStep::~TcHalfStep() { delete impl_; }
 void TcHalfStep::set_eps(DevProblem<float>& P, double eps) {
     impl_->eps = eps;
     const double c = 2.0 * P.fscale / eps * 1.4426950408889634074;
+    // screening threshold: |t - t~| <= delta = 2^-10 (1 + 2^-11) ||x|| ||c y|| (the
+    // dropped cross terms, Cauchy-Schwarz) -> thr = 64 + 2 delta + 8 (fp32 slack)
+    const char* env = std::getenv("FSK_SCREEN");
+    const bool screen_on = !(env && env[0] == '0') && impl_->chunks == 1;
+    for (int side = 0; side < 2; ++side) {
+        const double delta = std::ldexp(1.0, -10) * 1.001 * double(impl_->rownorm[side]) *
+                             double(impl_->rownorm[1 - side]) * c;
+        impl_->screen_thr[side] = screen_on ? float(64.0 + 2.0 * delta + 8.0) : 0.0f;
+    }
+    if (!impl_->live_count.get()) {
+        impl_->live_count.alloc(1, P.s);
+        impl_->live_count.zero();
+    }
     // side 0 (f-update): keys = Y (cloud 1); side 1 (g-update): keys = X (cloud 0)
     for (int side = 0; side < 2; ++side) {
         const int kc = side == 0 ? 1 : 0;
@@ -937,9 +1112,16 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
     p.part_m = pm.get();
     p.part_s = ps.get();
     const int grid = std::min(p.items, sms);
+    const int kps = (k_tiles + p.splits - 1) / p.splits;
+    p.screen_thr = I.screen_thr[side];
+    p.live_count = I.live_count.get();
+    const bool screen = !vec && p.screen_thr > 0.0f && kps <= kMaxScreenTiles &&
+                        !p.break_lse;
     if (I.chunks == 1) {
         if (vec)
             tc_lse_kernel<false, true><<<grid, NUM_THREADS, SMEM_BYTES, P.s>>>(p);
+        else if (screen)
+            tc_lse_kernel<false, false, true><<<grid, NUM_THREADS, SMEM_BYTES, P.s>>>(p);
         else
             tc_lse_kernel<false, false><<<grid, NUM_THREADS, SMEM_BYTES, P.s>>>(p);
     } else {

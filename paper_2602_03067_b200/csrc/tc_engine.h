@@ -27,6 +27,8 @@ public:
     ~TcHalfStep();
     static bool supported(int64_t d);
     int chunks() const;
+    // Cumulative number of key tiles scored in phase 2 of screened passes.
+    unsigned long long live_tiles() const;
 
     // (Re)builds the scaled key images for this eps (O((n+m) d) work).
     void set_eps(DevProblem<float>& P, double eps);

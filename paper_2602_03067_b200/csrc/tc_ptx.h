@@ -179,6 +179,17 @@ __device__ __forceinline__ void issue_score_tile(uint32_t d_tmem, uint32_t qa, u
                 IDESC_QK, 1u);
 }
 
+// Screening approximation t~ = bias + hi x hi (5 MMAs): only the hi chunk and the
+// bias chunk of the key stage are read.
+__device__ __forceinline__ void issue_screen_tile(uint32_t d_tmem, uint32_t qa, uint32_t ones,
+                                                  uint32_t kst) {
+    umma_ss(d_tmem, umma_desc(ones, 256, 6), umma_desc(kst + QTILE, 256, 6), IDESC_QK, 0u);
+#pragma unroll
+    for (int kk = 0; kk < DPAD / 16; ++kk)
+        umma_ss(d_tmem, umma_desc(qa + kk * 32, 1024, 2), umma_desc(kst + kk * 32, 1024, 2),
+                IDESC_QK, 1u);
+}
+
 // One 64-wide feature chunk of a score tile for d > 64 (operands streamed chunk
 // by chunk). Two accumulators keep the fp32 rounding at the scale of each part:
 // d_big = bias + sum of hi x hi slices (opened by the bias on the first chunk),
