@@ -104,7 +104,7 @@ struct TcParams {
 // phase 2 - the full 13-MMA split score + online LSE on live tiles only - is the
 // exact pass up to terms below 2^-64 relative.
 template <bool CHUNKED, bool VEC, bool SCREEN = false>
-__global__ void __maxnreg__(192) tc_lse_kernel(const TcParams p) {
+__global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
