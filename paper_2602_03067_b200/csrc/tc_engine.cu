@@ -1033,8 +1033,11 @@ void TcHalfStep::set_eps(DevProblem<float>& P, double eps) {
     const double c = 2.0 * P.fscale / eps * 1.4426950408889634074;
     // screening threshold: |t - t~| <= delta = 2^-10 (1 + 2^-11) ||x|| ||c y|| (the
     // dropped cross terms, Cauchy-Schwarz) -> thr = 64 + 2 delta + 8 (fp32 slack)
+    // opt-in (FSK_SCREEN=1): measured on B200 the two-phase pass only pays off when
+    // well under ~25% of the key tiles are live (cfg3: 29% live, 392 vs 345 ms per
+    // half-step; cfg2: 99.9% live) - see DESIGN.md
     const char* env = std::getenv("FSK_SCREEN");
-    const bool screen_on = !(env && env[0] == '0') && impl_->chunks == 1;
+    const bool screen_on = env && env[0] == '1' && impl_->chunks == 1;
     for (int side = 0; side < 2; ++side) {
         const double delta = std::ldexp(1.0, -10) * 1.001 * double(impl_->rownorm[side]) *
                              double(impl_->rownorm[1 - side]) * c;

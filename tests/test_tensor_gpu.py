@@ -293,7 +293,7 @@ def test_screened_lse_matches_unscreened(fsk):
     a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
     out = {}
     for flag in ("1", "0"):
-        os.environ["FSK_SCREEN"] = flag
+        os.environ["FSK_SCREEN"] = flag  # opt-in screening vs the default kernel
         try:
             eng = fsk.Engine(0, X, a, Y, b, mode="tensor")
             eng.set_eps(eps)
