@@ -495,6 +495,360 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
     }
 }
 
+// ---- K1 for d <= 64 with the query operand in TMEM ----------------------------
+//
+// The query tile pair of a work item is resident for thousands of key tiles, so
+// it lives in TMEM as the A operand of every score MMA (tcgen05.mma with A from
+// TMEM): each M128 N128 K16 MMA then reads only the 4 KB key slice from shared
+// memory instead of 8 KB, taking the kernel off the 128 B/clk shared-memory
+// roofline that bounds the SS form. TMEM: accumulator of tile t at column
+// 128 t (single-buffered per tile; the two tiles alternate so the MMA of one
+// overlaps the epilogue of the other), query operand of tile t at 256 + 72 t:
+// hi (32 columns of fp16 pairs), lo (32), ones (8). The epilogue warps stage the
+// query operand themselves (tcgen05.st from the pre-split image) per work item.
+constexpr int TQ_STAGES = 6;
+constexpr uint32_t TQ_OFF_K = 0;
+constexpr uint32_t TQ_OFF_BAR = TQ_OFF_K + TQ_STAGES * KSTAGE;   // 216 KB
+constexpr uint32_t TQ_SMEM_BYTES = TQ_OFF_BAR + 256 + VBUF + SBITS + 1024;
+constexpr uint32_t TQ_QCOL = 2 * TILE;                           // 256
+constexpr uint32_t TQ_QSTRIDE = 72;
+
+template <bool VEC, bool SCREEN>
+__global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t* sbase = smem_raw + (base - raw);
+
+    const uint32_t bar0 = base + TQ_OFF_BAR;
+    auto kfull = [&](int s) { return bar0 + 8u * s; };
+    auto kempty = [&](int s) { return bar0 + 8u * (TQ_STAGES + s); };
+    const uint32_t qready = bar0 + 8u * (2 * TQ_STAGES);          // epilogue -> MMA
+    const uint32_t qfree = qready + 8u;                            // MMA -> epilogue
+    auto accfull = [&](int t) { return qready + 16u + 8u * t; };
+    auto accempty = [&](int t) { return qready + 32u + 8u * t; };
+    const uint32_t screen_done = qready + 48u;
+    const uint32_t bits_free = qready + 56u;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + TQ_OFF_BAR + 192);
+    uint32_t* live_bits = reinterpret_cast<uint32_t*>(sbase + TQ_OFF_BAR + 256 + VBUF);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if constexpr (SCREEN)
+        for (int i = threadIdx.x; i < int(SBITS / 4); i += NUM_THREADS) live_bits[i] = 0u;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TQ_STAGES; ++s) {
+            mbar_init(kfull(s), 1);
+            mbar_init(kempty(s), 1);
+        }
+        mbar_init(qready, 8);
+        mbar_init(qfree, 1);
+        for (int t = 0; t < 2; ++t) {
+            mbar_init(accfull(t), 1);
+            mbar_init(accempty(t), 4);
+        }
+        mbar_init(screen_done, 8);
+        mbar_init(bits_free, 2);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+            smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+    auto next_live = [&](int kt, int kt0, int kt1) {
+        while (kt < kt1) {
+            const int rel = kt - kt0;
+            const uint32_t w = live_bits[rel >> 5] >> (rel & 31);
+            if (w) return kt + __ffs(w) - 1;
+            kt += 32 - (rel & 31);
+        }
+        return kt1;
+    };
+    const int ktiles_per_split = (p.k_tiles + p.splits - 1) / p.splits;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int it = 0;
+            for (int item = blockIdx.x, lu = 0; item < p.items; item += gridDim.x, ++lu) {
+                const int split = item % p.splits;
+                const int kt0 = split * ktiles_per_split;
+                const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
+                if constexpr (SCREEN) {
+                    for (int kt = kt0; kt < kt1; ++kt, ++it) {
+                        const int s = it % TQ_STAGES;
+                        mbar_wait(kempty(s), ((it / TQ_STAGES) & 1) ^ 1);
+                        mbar_expect_tx(kfull(s), CHUNK + BIAS);
+                        const uint32_t dst = base + TQ_OFF_K + s * KSTAGE;
+                        bulk_g2s(dst, p.kimg + size_t(kt) * QTILE, CHUNK, kfull(s));
+                        bulk_g2s(dst + QTILE, p.kbias + size_t(kt) * BIAS, BIAS, kfull(s));
+                    }
+                    mbar_wait(screen_done, lu & 1);
+                }
+                int nlive = 0;
+                for (int kt = SCREEN ? next_live(kt0, kt0, kt1) : kt0; kt < kt1;
+                     kt = SCREEN ? next_live(kt + 1, kt0, kt1) : kt + 1, ++it, ++nlive) {
+                    const int s = it % TQ_STAGES;
+                    mbar_wait(kempty(s), ((it / TQ_STAGES) & 1) ^ 1);
+                    mbar_expect_tx(kfull(s), KSTAGE);
+                    const uint32_t dst = base + TQ_OFF_K + s * KSTAGE;
+                    bulk_g2s(dst, p.kimg + size_t(kt) * QTILE, QTILE, kfull(s));
+                    bulk_g2s(dst + QTILE, p.kbias + size_t(kt) * BIAS, BIAS, kfull(s));
+                }
+                if constexpr (SCREEN) {
+                    mbar_arrive(bits_free);
+                    if (p.live_count) atomicAdd(p.live_count, (unsigned long long)nlive);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            int it = 0;
+            int acc_n[2] = {0, 0};
+            for (int item = blockIdx.x, lu = 0; item < p.items; item += gridDim.x, ++lu) {
+                const int unit = item / p.splits, split = item % p.splits;
+                const int qt0 = p.q_tile_begin + 2 * unit;
+                const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
+                const int kt0 = split * ktiles_per_split;
+                const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
+                mbar_wait(qready, lu & 1);
+                fence_after();
+                auto tile_mmas = [&](int kt_unused, bool screen_phase) {
+                    (void)kt_unused;
+                    const int s = it % TQ_STAGES;
+                    mbar_wait(kfull(s), (it / TQ_STAGES) & 1);
+                    fence_after();
+                    const uint32_t kst = base + TQ_OFF_K + s * KSTAGE;
+                    for (int t = 0; t < nq; ++t) {
+                        mbar_wait(accempty(t), (acc_n[t] & 1) ^ 1);
+                        fence_after();
+                        const uint32_t d = tmem + uint32_t(t * TILE);
+                        const uint32_t q = tmem + TQ_QCOL + uint32_t(t) * TQ_QSTRIDE;
+                        if (screen_phase)
+                            issue_screen_tile_tq(d, q, kst);
+                        else
+                            issue_score_tile_tq(d, q, kst);
+                        umma_commit(accfull(t));
+                        ++acc_n[t];
+                    }
+                    umma_commit(kempty(s));
+                    ++it;
+                };
+                if constexpr (SCREEN) {
+                    for (int kt = kt0; kt < kt1; ++kt) tile_mmas(kt, true);
+                    mbar_wait(screen_done, lu & 1);
+                }
+                for (int kt = SCREEN ? next_live(kt0, kt0, kt1) : kt0; kt < kt1;
+                     kt = SCREEN ? next_live(kt + 1, kt0, kt1) : kt + 1)
+                    tile_mmas(kt, false);
+                if constexpr (SCREEN) mbar_arrive(bits_free);
+                umma_commit(qfree);
+            }
+        }
+    } else {
+        // epilogue: warps 2..9; query tile t = (warp-2)/4, TMEM lane quarter = warp % 4
+        const int t = (warp - 2) >> 2;
+        const int quarter = warp & 3;
+        const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
+        const uint32_t acc_addr = tmem + lane_addr + uint32_t(t * TILE);
+        const uint32_t q_addr = tmem + lane_addr + TQ_QCOL + uint32_t(t) * TQ_QSTRIDE;
+        float* vb = reinterpret_cast<float*>(sbase + TQ_OFF_BAR + 256) + (warp - 2) * TILE;
+        int acc_n = 0;
+        for (int item = blockIdx.x, lu = 0; item < p.items; item += gridDim.x, ++lu) {
+            const int unit = item / p.splits, split = item % p.splits;
+            const int qt0 = p.q_tile_begin + 2 * unit;
+            const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
+            const int kt0 = split * ktiles_per_split;
+            const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
+            const int64_t row = int64_t(qt0 + t) * TILE + quarter * 32 + lane;
+            // stage this item's query operand (after the previous item's MMAs)
+            if (lu > 0) mbar_wait(qfree, (lu - 1) & 1);
+            fence_after();
+            if (t < nq) {
+                const int r = quarter * 32 + lane;
+                const uint8_t* src = p.qimg + size_t(qt0 + t) * QTILE + size_t(r) * 128;
+                uint32_t qh[32], ql[32];
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {
+                    const uint4 h = *reinterpret_cast<const uint4*>(src + ((g ^ (r & 7)) << 4));
+                    const uint4 l =
+                        *reinterpret_cast<const uint4*>(src + CHUNK + ((g ^ (r & 7)) << 4));
+                    qh[4 * g] = h.x, qh[4 * g + 1] = h.y, qh[4 * g + 2] = h.z, qh[4 * g + 3] = h.w;
+                    ql[4 * g] = l.x, ql[4 * g + 1] = l.y, ql[4 * g + 2] = l.z, ql[4 * g + 3] = l.w;
+                }
+                FSKB_TMEM_ST32(q_addr, qh);
+                FSKB_TMEM_ST32(q_addr + 32, ql);
+                // ones operand: K slots 0..2 = [2048, 1, 1/2048] (fp16 pairs, low = even)
+                const uint32_t ones01 = uint32_t(__half_as_ushort(__float2half_rn(kOnesW0))) |
+                                        (uint32_t(__half_as_ushort(__float2half_rn(1.0f))) << 16);
+                const uint32_t ones2 = uint32_t(__half_as_ushort(__float2half_rn(kOnesW2)));
+                asm volatile(
+                    "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%3,%3,%3,%3,%3};" ::"r"(
+                        q_addr + 64),
+                    "r"(ones01), "r"(ones2), "r"(0u)
+                    : "memory");
+                tmem_st_wait();
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(qready);
+
+            float M = -INFINITY;
+            double S = 0.0;
+            float nlh = 0.0f, nll = 0.0f;
+            if constexpr (VEC) {
+                const bool live = t < nq && row < p.R;
+                nlh = live ? -p.l2h[row] : -3.0e38f;
+                nll = live ? -p.l2l[row] : 0.0f;
+            }
+            if constexpr (SCREEN) {
+                float Ma = -INFINITY;
+                const bool row_ok = t < nq && row < p.R;
+                for (int kt = kt0; kt < kt1; ++kt) {
+                    float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+                    if (t < nq) {
+                        mbar_wait(accfull(t), acc_n & 1);
+                        fence_after();
+                        const int64_t kbase = int64_t(kt) * TILE;
+#pragma unroll 1
+                        for (int q = 0; q < 4; ++q) {
+                            uint32_t v[32];
+                            FSKB_TMEM_LD32(acc_addr + 32 * q, v);
+                            tmem_ld_wait();
+                            if (kbase + 32 * q + 32 > p.key_valid) {
+#pragma unroll
+                                for (int j = 0; j < 32; ++j)
+                                    if (kbase + 32 * q + j >= p.key_valid)
+                                        v[j] = __float_as_uint(-INFINITY);
+                            }
+#pragma unroll
+                            for (int j = 0; j < 32; j += 4) {
+                                mx0 = fmaxf(mx0, __uint_as_float(v[j]));
+                                mx1 = fmaxf(mx1, __uint_as_float(v[j + 1]));
+                                mx2 = fmaxf(mx2, __uint_as_float(v[j + 2]));
+                                mx3 = fmaxf(mx3, __uint_as_float(v[j + 3]));
+                            }
+                        }
+                        fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(accempty(t));
+                        ++acc_n;
+                        const float tmax =
+                            fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * p.acc_scale;
+                        Ma = fmaxf(Ma, tmax);
+                        const bool live = row_ok && tmax >= Ma - p.screen_thr;
+                        if (__any_sync(0xffffffffu, live) && lane == 0)
+                            atomicOr(&live_bits[(kt - kt0) >> 5], 1u << ((kt - kt0) & 31));
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(screen_done);
+                mbar_wait(screen_done, lu & 1);
+            }
+            for (int kt = SCREEN ? next_live(kt0, kt0, kt1) : kt0; kt < kt1;
+                 kt = SCREEN ? next_live(kt + 1, kt0, kt1) : kt + 1) {
+                if (t >= nq) continue;
+                mbar_wait(accfull(t), acc_n & 1);
+                fence_after();
+                uint32_t v[128];
+                FSKB_TMEM_LD32(acc_addr + 0, (v + 0));
+                FSKB_TMEM_LD32(acc_addr + 32, (v + 32));
+                FSKB_TMEM_LD32(acc_addr + 64, (v + 64));
+                FSKB_TMEM_LD32(acc_addr + 96, (v + 96));
+                tmem_ld_wait();
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(accempty(t));
+                ++acc_n;
+                const int64_t kbase = int64_t(kt) * TILE;
+                if (kbase + TILE > p.key_valid) {
+#pragma unroll
+                    for (int j = 0; j < 128; ++j)
+                        if (kbase + j >= p.key_valid) v[j] = __float_as_uint(-INFINITY);
+                }
+                float mx0 = __uint_as_float(v[0]), mx1 = __uint_as_float(v[1]);
+                float mx2 = __uint_as_float(v[2]), mx3 = __uint_as_float(v[3]);
+#pragma unroll
+                for (int j = 4; j < 128; j += 4) {
+                    mx0 = fmaxf(mx0, __uint_as_float(v[j]));
+                    mx1 = fmaxf(mx1, __uint_as_float(v[j + 1]));
+                    mx2 = fmaxf(mx2, __uint_as_float(v[j + 2]));
+                    mx3 = fmaxf(mx3, __uint_as_float(v[j + 3]));
+                }
+                const float umax = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * p.acc_scale;
+                if constexpr (VEC) {
+                    if (__all_sync(0xffffffffu, umax + nlh < -kSkipLog2)) continue;
+                    float4 vv = make_float4(0.f, 0.f, 0.f, 0.f);
+                    const int64_t j0 = kbase + 4 * lane;
+                    if (j0 + 3 < p.key_valid) {
+                        vv = *reinterpret_cast<const float4*>(p.vvec + j0);
+                    } else {
+                        if (j0 < p.key_valid) vv.x = p.vvec[j0];
+                        if (j0 + 1 < p.key_valid) vv.y = p.vvec[j0 + 1];
+                        if (j0 + 2 < p.key_valid) vv.z = p.vvec[j0 + 2];
+                    }
+                    reinterpret_cast<float4*>(vb)[lane] = vv;
+                    __syncwarp();
+                    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+                    for (int j = 0; j < 128; j += 4) {
+                        const float4 w = reinterpret_cast<const float4*>(vb)[j >> 2];
+                        s0 = fmaf(ex2(fmaf(__uint_as_float(v[j]), p.acc_scale, nlh) + nll), w.x, s0);
+                        s1 = fmaf(ex2(fmaf(__uint_as_float(v[j + 1]), p.acc_scale, nlh) + nll), w.y,
+                                  s1);
+                        s2 = fmaf(ex2(fmaf(__uint_as_float(v[j + 2]), p.acc_scale, nlh) + nll), w.z,
+                                  s2);
+                        s3 = fmaf(ex2(fmaf(__uint_as_float(v[j + 3]), p.acc_scale, nlh) + nll), w.w,
+                                  s3);
+                    }
+                    S += double((s0 + s1) + (s2 + s3));
+                    __syncwarp();
+                } else {
+                    if (umax > M) {
+                        if (S != 0.0) S *= double(ex2(p.break_lse ? umax - M : M - umax));
+                        M = umax;
+                    }
+                    const bool dead = M == -INFINITY;
+                    if (__all_sync(0xffffffffu, dead || umax < M - kSkipLog2)) continue;
+                    const float nm = dead ? 0.0f : -M;
+                    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+                    for (int j = 0; j < 128; j += 4) {
+                        s0 += ex2(fmaf(__uint_as_float(v[j]), p.acc_scale, nm));
+                        s1 += ex2(fmaf(__uint_as_float(v[j + 1]), p.acc_scale, nm));
+                        s2 += ex2(fmaf(__uint_as_float(v[j + 2]), p.acc_scale, nm));
+                        s3 += ex2(fmaf(__uint_as_float(v[j + 3]), p.acc_scale, nm));
+                    }
+                    S += double((s0 + s1) + (s2 + s3));
+                }
+            }
+            if constexpr (SCREEN) {
+                mbar_wait(bits_free, lu & 1);
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+                for (int i = threadIdx.x - 64; i < int(SBITS / 4); i += 256) live_bits[i] = 0u;
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+            }
+            if (t < nq && row >= p.row_begin && row < p.row_end) {
+                if constexpr (VEC) {
+                    p.part_m[size_t(split) * p.R + row] = S;
+                } else {
+                    p.part_m[size_t(split) * p.R + row] = double(M) * 0.69314718055994530942;
+                    p.part_s[size_t(split) * p.R + row] = S;
+                }
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}
+
 // ---- transport application O = softmax(S) V on the tensor cores -------------
 //
 // Second pass of the fused gradient / barycentric projection: given the row
@@ -994,12 +1348,12 @@ unsigned long long TcHalfStep::live_tiles() const {
 
 TcHalfStep::TcHalfStep(DevProblem<float>& P) : impl_(new Impl()) {
     // per device (the attribute is per-context), cheap enough to set every time
-    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_kernel<false, false>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES)));
-    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_kernel<false, true>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES)));
-    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_kernel<false, false, true>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES)));
+    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_tq_kernel<false, false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(TQ_SMEM_BYTES)));
+    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_tq_kernel<true, false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(TQ_SMEM_BYTES)));
+    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_tq_kernel<false, true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(TQ_SMEM_BYTES)));
     FSKB_CUDA(cudaFuncSetAttribute(tc_lse_kernel<true, false>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(C_SMEM_BYTES)));
     FSKB_CUDA(cudaFuncSetAttribute(tc_lse_kernel<true, true>,
@@ -1122,11 +1476,11 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
                         !p.break_lse;
     if (I.chunks == 1) {
         if (vec)
-            tc_lse_kernel<false, true><<<grid, NUM_THREADS, SMEM_BYTES, P.s>>>(p);
+            tc_lse_tq_kernel<true, false><<<grid, NUM_THREADS, TQ_SMEM_BYTES, P.s>>>(p);
         else if (screen)
-            tc_lse_kernel<false, false, true><<<grid, NUM_THREADS, SMEM_BYTES, P.s>>>(p);
+            tc_lse_tq_kernel<false, true><<<grid, NUM_THREADS, TQ_SMEM_BYTES, P.s>>>(p);
         else
-            tc_lse_kernel<false, false><<<grid, NUM_THREADS, SMEM_BYTES, P.s>>>(p);
+            tc_lse_tq_kernel<false, false><<<grid, NUM_THREADS, TQ_SMEM_BYTES, P.s>>>(p);
     } else {
         if (vec)
             tc_lse_kernel<true, true><<<grid, NUM_THREADS, C_SMEM_BYTES, P.s>>>(p);

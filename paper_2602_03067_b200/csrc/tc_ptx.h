@@ -179,6 +179,27 @@ __device__ __forceinline__ void issue_score_tile(uint32_t d_tmem, uint32_t qa, u
                 IDESC_QK, 1u);
 }
 
+// Score tile with the query operand in TMEM (A from TMEM at column q: hi at +0,
+// lo at +32, ones at +64; 8 columns per K16 slice), same 13-MMA order as above.
+__device__ __forceinline__ void issue_score_tile_tq(uint32_t d_tmem, uint32_t q, uint32_t kst) {
+#pragma unroll
+    for (int kk = 0; kk < DPAD / 16; ++kk) {
+        umma_ts(d_tmem, q + 32 + kk * 8, umma_desc(kst + kk * 32, 1024, 2), IDESC_QK,
+                kk > 0 ? 1u : 0u);
+        umma_ts(d_tmem, q + kk * 8, umma_desc(kst + CHUNK + kk * 32, 1024, 2), IDESC_QK, 1u);
+    }
+    umma_ts(d_tmem, q + 64, umma_desc(kst + QTILE, 256, 6), IDESC_QK, 1u);
+#pragma unroll
+    for (int kk = 0; kk < DPAD / 16; ++kk)
+        umma_ts(d_tmem, q + kk * 8, umma_desc(kst + kk * 32, 1024, 2), IDESC_QK, 1u);
+}
+__device__ __forceinline__ void issue_screen_tile_tq(uint32_t d_tmem, uint32_t q, uint32_t kst) {
+    umma_ts(d_tmem, q + 64, umma_desc(kst + QTILE, 256, 6), IDESC_QK, 0u);
+#pragma unroll
+    for (int kk = 0; kk < DPAD / 16; ++kk)
+        umma_ts(d_tmem, q + kk * 8, umma_desc(kst + kk * 32, 1024, 2), IDESC_QK, 1u);
+}
+
 // Screening approximation t~ = bias + hi x hi (5 MMAs): only the hi chunk and the
 // bias chunk of the key stage are read.
 __device__ __forceinline__ void issue_screen_tile(uint32_t d_tmem, uint32_t qa, uint32_t ones,
