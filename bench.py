@@ -370,7 +370,7 @@ def run_b200(args, cfgname):
     if sampler:
         sampler.start()
     launches0 = fsk.Engine.launches()
-    live0 = eng.live_tiles()
+    live0, sblk0 = eng.live_tiles(), eng.screened_blocks()
     events = []
     gev = []
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -381,7 +381,7 @@ def run_b200(args, cfgname):
     stop.record(stream)
     torch.cuda.synchronize()
     launches = fsk.Engine.launches() - launches0
-    live = eng.live_tiles() - live0
+    live, sblk = eng.live_tiles() - live0, eng.screened_blocks() - sblk0
     clocks = sampler.stop() if sampler else None
     elapsed = start.elapsed_time(stop) / 1e3
     half_ms = [events[i].elapsed_time(events[i + 1]) for i in range(0, len(events), 2)]
@@ -493,11 +493,11 @@ def run_b200(args, cfgname):
         "e2e": e2e,
     }
     if tensor and chunks == 1:
-        # screened LSE passes: fraction of (query tile pair, key tile) blocks scored in
-        # full after the 5-MMA hi x hi screen (the rest are provably < 2^-64 of the max)
-        passes = args.steps * (2 * iters + (1 if STEP_TAIL[cfgname] == "grad" else 0))
-        blocks = -(-(hi - lo) // 256) * -(-m // 128)
-        line["screen_live_fraction"] = live / max(1, passes * blocks)
+        # adaptive screening: of the (query tile pair, key tile) blocks of the screened
+        # LSE passes, the fraction scored in full after the 5-MMA hi x hi screen (the
+        # rest are provably < 2^-64 of every row's max)
+        line["screen"] = {"screened_blocks": sblk, "live_blocks": live,
+                          "live_fraction": live / sblk if sblk else None}
     if world == 1 and args.cpu_baseline:
         try:
             cb = reference_sample(cfgname)

@@ -286,10 +286,13 @@ int fsk_engine_grad(fsk_engine* e, int64_t row_begin, int64_t row_end, float* gr
  * row marginal, then the tcgen05 VEC pass (or the fp32 CUDA-core apply). */
 int fsk_engine_transport_vec(fsk_engine* e, int side, const float* v_dev, double* out_dev,
                              void* stream);
-/* Cumulative count of key tiles scored in full by screened tcgen05 LSE passes
- * (phase 2); the rest were proven below 2^-64 of every row's max by the
- * 5-MMA hi x hi screen (diagnostics for the bench line). */
+/* Cumulative count of (query tile pair, key tile) blocks scored in full by
+ * screened tcgen05 LSE passes (phase 2); the rest were proven below 2^-64 of
+ * every row's max by the 5-MMA hi x hi screen (diagnostics for the bench line).
+ * Screening is adaptive (on while the live fraction stays below 0.45). */
 uint64_t fsk_engine_screen_live_tiles(const fsk_engine* e);
+/* (query tile pair, key tile) blocks covered by those screened passes. */
+uint64_t fsk_engine_screen_blocks(const fsk_engine* e);
 /* Launch counter of this engine's kernels (for bench accounting). */
 int64_t fsk_engine_kernel_launches(const fsk_engine* e);
 /* Name of the kernel path the engine uses for half-steps ("tcgen05-split3" / "fma-f32"). */

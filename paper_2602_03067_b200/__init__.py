@@ -103,6 +103,7 @@ def lib() -> C.CDLL:
         L.fsk_engine_path.restype = C.c_char_p
         L.fsk_engine_kernel_launches.restype = C.c_int64
         L.fsk_engine_screen_live_tiles.restype = C.c_uint64
+        L.fsk_engine_screen_blocks.restype = C.c_uint64
         for name in ("fsk_io_count_f_update", "fsk_io_count_g_update",
                      "fsk_io_count_symmetric_update", "fsk_io_count_apply_plan",
                      "fsk_io_count_apply_plan_adjoint", "fsk_io_count_apply_hadamard",
@@ -476,8 +477,12 @@ class Engine:
         return lib().fsk_engine_path(self.h).decode()
 
     def live_tiles(self) -> int:
-        """Key tiles scored in full by screened LSE passes so far."""
+        """Blocks scored in full by screened LSE passes so far."""
         return int(lib().fsk_engine_screen_live_tiles(self.h))
+
+    def screened_blocks(self) -> int:
+        """Blocks covered by screened LSE passes so far."""
+        return int(lib().fsk_engine_screen_blocks(self.h))
 
     @staticmethod
     def launches() -> int:

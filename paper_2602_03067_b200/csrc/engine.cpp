@@ -222,6 +222,12 @@ uint64_t fsk_engine_screen_live_tiles(const fsk_engine* e) {
     return e && e->P.tc ? uint64_t(e->P.tc->live_tiles()) : 0;
 }
 
+uint64_t fsk_engine_screen_blocks(const fsk_engine* e) {
+    if (!e || !e->P.tc) return 0;
+    e->P.tc->live_tiles();  // drains the pending read-backs
+    return uint64_t(e->P.tc->screened_blocks());
+}
+
 int64_t fsk_engine_kernel_launches(const fsk_engine* e) {
     (void)e;
     return launch_counter();

@@ -1333,17 +1333,56 @@ struct TcHalfStep::Impl {
     int chunks = 1;                 // 64-wide feature chunks (d > 64: chunked kernels)
     float rownorm[2] = {0.f, 0.f};  // max_i ||x_i|| of each cloud
     float screen_thr[2] = {0.f, 0.f};  // per side, log2 units; 0 = no screening
-    DevBuf<unsigned long long> live_count;  // live key tiles of screened passes
+    // adaptive screening, per side: live fraction of the last screened pass (read
+    // back asynchronously: counter -> pinned host word -> event, never a host sync)
+    DevBuf<unsigned long long> live_count;  // [2] live key tiles of the last pass
+    unsigned long long* h_live = nullptr;   // [2] pinned
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    bool pending[2] = {false, false};
+    double pending_blocks[2] = {0.0, 0.0};
+    double live_est[2] = {0.0, 0.0};         // 0 -> screen the first pass (probe)
+    int skip_left[2] = {0, 0}, backoff[2] = {8, 8};
+    unsigned long long live_total = 0, screened_blocks = 0;
+    ~Impl() {
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        if (h_live) cudaFreeHost(h_live);
+    }
 };
+
+// Screening pays when the live fraction is below ~0.45 (phase 1 costs ~0.4 of a
+// full pass): cfg3 2^20 x 2^20, eps 0.05: 29% live, 280 vs 333 ms per half-step;
+// cfg2 65536^2: 99.9% live, 2.24 vs 1.42 ms. Passes with a high measured live
+// fraction run unscreened and re-probe after an exponentially growing backoff.
+constexpr double kScreenMaxLive = 0.45;
 
 bool TcHalfStep::supported(int64_t d) { return d >= 1 && d <= 64 * 64; }
 int TcHalfStep::chunks() const { return impl_->chunks; }
 
 unsigned long long TcHalfStep::live_tiles() const {
-    unsigned long long h = 0;
-    if (impl_->live_count.get())
-        FSKB_CUDA(cudaMemcpy(&h, impl_->live_count.get(), sizeof(h), cudaMemcpyDeviceToHost));
-    return h;
+    for (int side = 0; side < 2; ++side)
+        if (impl_->pending[side]) FSKB_CUDA(cudaEventSynchronize(impl_->ev[side]));
+    const_cast<TcHalfStep*>(this)->poll_screen(0);
+    const_cast<TcHalfStep*>(this)->poll_screen(1);
+    return impl_->live_total;
+}
+
+unsigned long long TcHalfStep::screened_blocks() const { return impl_->screened_blocks; }
+
+void TcHalfStep::poll_screen(int side) {
+    Impl& I = *impl_;
+    if (!I.pending[side] || cudaEventQuery(I.ev[side]) != cudaSuccess) return;
+    const double live = double(I.h_live[side]);
+    I.live_total += I.h_live[side];
+    I.screened_blocks += (unsigned long long)I.pending_blocks[side];
+    I.live_est[side] = live / std::max(1.0, I.pending_blocks[side]);
+    I.pending[side] = false;
+    if (I.live_est[side] >= kScreenMaxLive) {
+        I.skip_left[side] = I.backoff[side];
+        I.backoff[side] = std::min(I.backoff[side] * 2, 1 << 12);
+    } else {
+        I.backoff[side] = 8;
+    }
 }
 
 TcHalfStep::TcHalfStep(DevProblem<float>& P) : impl_(new Impl()) {
@@ -1387,19 +1426,20 @@ void TcHalfStep::set_eps(DevProblem<float>& P, double eps) {
     const double c = 2.0 * P.fscale / eps * 1.4426950408889634074;
     // screening threshold: |t - t~| <= delta = 2^-10 (1 + 2^-11) ||x|| ||c y|| (the
     // dropped cross terms, Cauchy-Schwarz) -> thr = 64 + 2 delta + 8 (fp32 slack)
-    // opt-in (FSK_SCREEN=1): measured on B200 the two-phase pass only pays off when
-    // well under ~25% of the key tiles are live (cfg3: 29% live, 392 vs 345 ms per
-    // half-step; cfg2: 99.9% live) - see DESIGN.md
+    // adaptive (kScreenMaxLive), FSK_SCREEN=0 disables it
     const char* env = std::getenv("FSK_SCREEN");
-    const bool screen_on = env && env[0] == '1' && impl_->chunks == 1;
+    const bool screen_on = !(env && env[0] == '0') && impl_->chunks == 1;
     for (int side = 0; side < 2; ++side) {
         const double delta = std::ldexp(1.0, -10) * 1.001 * double(impl_->rownorm[side]) *
                              double(impl_->rownorm[1 - side]) * c;
         impl_->screen_thr[side] = screen_on ? float(64.0 + 2.0 * delta + 8.0) : 0.0f;
     }
     if (!impl_->live_count.get()) {
-        impl_->live_count.alloc(1, P.s);
+        impl_->live_count.alloc(2, P.s);
         impl_->live_count.zero();
+        FSKB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&impl_->h_live),
+                                2 * sizeof(unsigned long long), cudaHostAllocDefault));
+        for (auto& e : impl_->ev) FSKB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     // side 0 (f-update): keys = Y (cloud 1); side 1 (g-update): keys = X (cloud 0)
     for (int side = 0; side < 2; ++side) {
@@ -1471,9 +1511,22 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
     const int grid = std::min(p.items, sms);
     const int kps = (k_tiles + p.splits - 1) / p.splits;
     p.screen_thr = I.screen_thr[side];
-    p.live_count = I.live_count.get();
-    const bool screen = !vec && p.screen_thr > 0.0f && kps <= kMaxScreenTiles &&
-                        !p.break_lse;
+    bool screen = !vec && I.chunks == 1 && p.screen_thr > 0.0f && kps <= kMaxScreenTiles &&
+                  !p.break_lse;
+    if (screen) {
+        poll_screen(side);
+        if (I.pending[side]) {
+            screen = I.live_est[side] < kScreenMaxLive;  // last estimate still in flight
+        } else if (I.live_est[side] >= kScreenMaxLive) {
+            screen = I.skip_left[side] <= 0;               // re-probe after the backoff
+            --I.skip_left[side];
+        }
+    }
+    if (screen) {
+        p.live_count = I.live_count.get() + side;
+        if (!I.pending[side])
+            FSKB_CUDA(cudaMemsetAsync(p.live_count, 0, sizeof(unsigned long long), P.s));
+    }
     if (I.chunks == 1) {
         if (vec)
             tc_lse_tq_kernel<true, false><<<grid, NUM_THREADS, TQ_SMEM_BYTES, P.s>>>(p);
@@ -1481,6 +1534,14 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
             tc_lse_tq_kernel<false, true><<<grid, NUM_THREADS, TQ_SMEM_BYTES, P.s>>>(p);
         else
             tc_lse_tq_kernel<false, false><<<grid, NUM_THREADS, TQ_SMEM_BYTES, P.s>>>(p);
+        if (screen && !I.pending[side]) {
+            FSKB_CUDA(cudaGetLastError());
+            FSKB_CUDA(cudaMemcpyAsync(I.h_live + side, p.live_count, sizeof(unsigned long long),
+                                      cudaMemcpyDeviceToHost, P.s));
+            FSKB_CUDA(cudaEventRecord(I.ev[side], P.s));
+            I.pending[side] = true;
+            I.pending_blocks[side] = double(units) * double(k_tiles);
+        }
     } else {
         if (vec)
             tc_lse_kernel<true, true><<<grid, NUM_THREADS, C_SMEM_BYTES, P.s>>>(p);

@@ -27,8 +27,10 @@ public:
     ~TcHalfStep();
     static bool supported(int64_t d);
     int chunks() const;
-    // Cumulative number of key tiles scored in phase 2 of screened passes.
+    // Screening diagnostics: (query tile pair, key tile) blocks scored in full by
+    // phase 2 of screened passes, and blocks those passes covered.
     unsigned long long live_tiles() const;
+    unsigned long long screened_blocks() const;
 
     // (Re)builds the scaled key images for this eps (O((n+m) d) work).
     void set_eps(DevProblem<float>& P, double eps);
@@ -55,6 +57,7 @@ public:
              const float* l2l, const float* marg, const float* v, double* out, int* flags);
 
 private:
+    void poll_screen(int side);
     int pass(DevProblem<float>& P, int side, const float* kpot, float eps, int64_t row_begin,
              int64_t row_end, const float* const* vec, int* flags, DevBuf<double>& pm,
              DevBuf<double>& ps);
