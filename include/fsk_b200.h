@@ -286,6 +286,12 @@ int fsk_engine_grad(fsk_engine* e, int64_t row_begin, int64_t row_end, float* gr
  * row marginal, then the tcgen05 VEC pass (or the fp32 CUDA-core apply). */
 int fsk_engine_transport_vec(fsk_engine* e, int side, const float* v_dev, double* out_dev,
                              void* stream);
+/* Transport-matrix application at the bound potentials: out_dev (float, rows x p,
+ * device) = P V (side 0; V indexed by Y, m x p) or P^T V (side 1; V n x p). One LSE
+ * pass, then the tcgen05 general apply kernel (any d, p in passes of 128 columns)
+ * or the fp32 CUDA-core apply. */
+int fsk_engine_transport_mat(fsk_engine* e, int side, const float* v_dev, int64_t p,
+                             float* out_dev, void* stream);
 /* Cumulative count of (query tile pair, key tile) blocks scored in full by
  * screened tcgen05 LSE passes (phase 2); the rest were proven below 2^-64 of
  * every row's max by the 5-MMA hi x hi screen (diagnostics for the bench line).

@@ -509,6 +509,12 @@ class Engine:
         _check(lib().fsk_engine_transport_vec(self.h, C.c_int(side), C.c_void_p(v_ptr),
                                               C.c_void_p(out_ptr), C.c_void_p(stream)))
 
+    def transport_mat(self, side: int, v_ptr: int, p: int, out_ptr: int, stream: int = 0):
+        """out (float, device, rows x p) = P V (side 0) or P^T V (side 1)."""
+        _check(lib().fsk_engine_transport_mat(self.h, C.c_int(side), C.c_void_p(v_ptr),
+                                              C.c_int64(p), C.c_void_p(out_ptr),
+                                              C.c_void_p(stream)))
+
     def grad(self, row_begin: int, row_end: int, grad_ptr: int, stream: int = 0):
         _check(lib().fsk_engine_grad(self.h, C.c_int64(row_begin), C.c_int64(row_end),
                                      C.c_void_p(grad_ptr), C.c_void_p(stream)))

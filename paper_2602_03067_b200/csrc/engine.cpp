@@ -177,6 +177,60 @@ int fsk_engine_grad(fsk_engine* e, int64_t row_begin, int64_t row_end, float* gr
     });
 }
 
+namespace {
+// One LSE pass of `side` at the bound potentials: marginal, natural LSE/max and
+// (tensor path) the log2 LSE split, as consumed by the transport applications.
+struct SideLse {
+    DevBuf<float> marg, lse, mx, l2h, l2l;
+};
+SideLse side_lse(fsk_engine* e, int side, cudaStream_t s) {
+    const int64_t R = side == 0 ? e->P.src.n : e->P.tgt.n;
+    SideLse o;
+    o.marg.alloc(size_t(R), s);
+    o.lse.alloc(size_t(R), s);
+    o.mx.alloc(size_t(R), s);
+    FinalizeArgs<float> fa{};
+    fa.eps = float(e->eps);
+    fa.flags = e->flags;
+    fa.old_pot = side == 0 ? e->f : e->g;
+    fa.w = side == 0 ? e->P.src.w.get() : e->P.tgt.w.get();
+    fa.out_marg = o.marg.get();
+    fa.marg_flag = side == 0 ? kFlagNonFiniteRowMarginal : kFlagNonFiniteColMarginal;
+    fa.out_lse = o.lse.get();
+    fa.out_max = o.mx.get();
+    if (e->P.tc) {
+        o.l2h.alloc(size_t(R), s);
+        o.l2l.alloc(size_t(R), s);
+        fa.out_l2h = o.l2h.get();
+        fa.out_l2l = o.l2l.get();
+    }
+    half_step_rows<float>(e->P, side, side == 0 ? e->g : e->f, float(e->eps), fa, 0, R);
+    return o;
+}
+}  // namespace
+
+int fsk_engine_transport_mat(fsk_engine* e, int side, const float* v_dev, int64_t p,
+                             float* out_dev, void* stream) {
+    return eguard([&] {
+        if (!e->f || !e->g) throw ValidationFailure("engine potentials not bound");
+        if (side != 0 && side != 1) throw ValidationFailure("side must be 0 or 1");
+        if (p < 1) throw ValidationFailure("p must be positive");
+        cudaStream_t s = pick(e, stream);
+        e->P.s = s;
+        const float eps = float(e->eps);
+        const float* kpot = side == 0 ? e->g : e->f;
+        const float* pot = side == 0 ? e->f : e->g;
+        SideLse L = side_lse(e, side, s);
+        if (e->P.tc) {
+            e->P.tc->apply_mat(e->P, side, kpot, eps, L.l2h.get(), L.l2l.get(), L.marg.get(),
+                               v_dev, p, out_dev, e->flags);
+        } else {
+            transport<float>(e->P, side, kpot, pot, eps, L.lse.get(), L.mx.get(), v_dev, p,
+                             nullptr, nullptr, 0, out_dev, e->flags);
+        }
+    });
+}
+
 int fsk_engine_transport_vec(fsk_engine* e, int side, const float* v_dev, double* out_dev,
                              void* stream) {
     return eguard([&] {

@@ -63,7 +63,20 @@ struct HvpCtx {
         std::vector<double> h((size_t)(rows * p));
         bool done = false;
         if constexpr (std::is_same_v<T, float>) {
-            if (P.tc && !A && p == 1) {
+            if (P.tc && !A && p > 1) {
+                DevBuf<float> vd(size_t(cols * p), C.s);
+                const std::vector<float> vf(V.begin(), V.end());
+                vd.upload(vf.data(), size_t(cols * p));
+                DevBuf<float> out(size_t(rows * p), C.s);
+                P.s = C.s;
+                P.tc->apply_mat(P, side, kpot, float(eps), l2h[side], l2l[side], marg[side],
+                                vd.get(), p, out.get(), C.flags);
+                std::vector<float> hf((size_t)(rows * p));
+                out.download(hf.data(), hf.size());
+                FSKB_CUDA(cudaStreamSynchronize(C.s));
+                h.assign(hf.begin(), hf.end());
+                done = true;
+            } else if (P.tc && !A && p == 1) {
                 DevBuf<float> vd(size_t(cols), C.s);
                 const std::vector<float> vf(V.begin(), V.end());
                 vd.upload(vf.data(), size_t(cols));

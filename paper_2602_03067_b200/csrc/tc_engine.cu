@@ -44,17 +44,14 @@ namespace {
 
 using namespace tc;
 
-constexpr int STAGES = 4;
+// 10 warps per CTA (producer, MMA issuer, 8 epilogue warps): 3 warps land on
+// some SM sub-partition, whose 64 KB register file then caps the kernels at 168
+// registers per thread.
 constexpr int NUM_WARPS = 10;
 constexpr int NUM_THREADS = NUM_WARPS * 32;
-constexpr uint32_t OFF_Q = 0;
-constexpr uint32_t OFF_ONES = 2 * QTILE;                       // 64 KB
-constexpr uint32_t OFF_K = OFF_ONES + BIAS;                    // 68 KB
-constexpr uint32_t OFF_BAR = OFF_K + STAGES * KSTAGE;          // 212 KB
 constexpr uint32_t VBUF = 8 * TILE * 4;                        // per epilogue warp: 128 floats
 constexpr uint32_t SBITS = 4096;                               // screened: live-tile bitmask
 constexpr int kMaxScreenTiles = int(SBITS * 8);
-constexpr uint32_t SMEM_BYTES = OFF_BAR + 256 + VBUF + SBITS + 1024;  // + barriers, buffers, slack
 // chunked layout (d > 64): stage = Q chunk of 2 query tiles + key chunk + bias
 constexpr int CSTAGES = 2;
 constexpr uint32_t CSTAGE = 3 * QTILE + BIAS;                  // 100 KB
@@ -90,60 +87,107 @@ struct TcParams {
     unsigned long long* live_count;  // += live key tiles (diagnostics), nullable
 };
 
-// CHUNKED = false: d <= 64, the query tile pair stays resident for a work item
-// and 36 KB key stages stream through a 4-deep ring.
-// CHUNKED = true: d > 64, every (key tile, feature chunk) step streams the
-// query chunk of both tiles with the key chunk (100 KB stages, 2-deep ring);
-// the score accumulates over chunks in TMEM before the epilogue sees it.
-// VEC = true: transport-vector pass (P v / P^T u) over the same score tiles.
-// SCREEN = true (d <= 64 LSE only): two phases per work item. Phase 1 runs the
-// 5-MMA approximation t~ = hi x hi + bias over every key tile (20 KB loads) and
-// marks a tile live when some row has max_j t~_ij >= M~_i - screen_thr (M~ the
-// running approximate row max). With |t - t~| <= delta and screen_thr >= 64 +
-// 2 delta, every key within 2^-64 of a row's true max lies in a live tile, so
-// phase 2 - the full 13-MMA split score + online LSE on live tiles only - is the
-// exact pass up to terms below 2^-64 relative.
-template <bool CHUNKED, bool VEC, bool SCREEN = false>
-__global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p) {
+// Per-tile epilogue math shared by the K1 kernels: mask the padded keys of the
+// last tile, then either the online (max, sum-exp) update (LSE) or, with the row
+// LSE known, the transport-vector sum sum_j 2^(t - L) v_j (VEC). `v` holds the 128
+// fp32 scores of this thread's row (acc units; t = acc * acc_scale).
+template <bool VEC>
+__device__ __forceinline__ void k1_tile_update(uint32_t (&v)[128], int64_t kbase, const TcParams& p,
+                                               float& M, double& S, float nlh, float nll,
+                                               float* vb, int lane) {
+    if (kbase + TILE > p.key_valid) {
+#pragma unroll
+        for (int j = 0; j < 128; ++j)
+            if (kbase + j >= p.key_valid) v[j] = __float_as_uint(-INFINITY);
+    }
+    float mx0 = __uint_as_float(v[0]), mx1 = __uint_as_float(v[1]);
+    float mx2 = __uint_as_float(v[2]), mx3 = __uint_as_float(v[3]);
+#pragma unroll
+    for (int j = 4; j < 128; j += 4) {
+        mx0 = fmaxf(mx0, __uint_as_float(v[j]));
+        mx1 = fmaxf(mx1, __uint_as_float(v[j + 1]));
+        mx2 = fmaxf(mx2, __uint_as_float(v[j + 2]));
+        mx3 = fmaxf(mx3, __uint_as_float(v[j + 3]));
+    }
+    const float umax = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * p.acc_scale;
+    if constexpr (VEC) {
+        // P~ = 2^(t - L) <= 1; a tile whose P~ are all < 2^-64 for the warp's rows
+        // adds < m 2^-64 max|v| - below the fp32 result's rounding
+        if (__all_sync(0xffffffffu, umax + nlh < -kSkipLog2)) return;
+        // the tile's 128 values of v, broadcast through a per-warp buffer
+        float4 vv = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int64_t j0 = kbase + 4 * lane;
+        if (j0 + 3 < p.key_valid) {
+            vv = *reinterpret_cast<const float4*>(p.vvec + j0);
+        } else {
+            if (j0 < p.key_valid) vv.x = p.vvec[j0];
+            if (j0 + 1 < p.key_valid) vv.y = p.vvec[j0 + 1];
+            if (j0 + 2 < p.key_valid) vv.z = p.vvec[j0 + 2];
+        }
+        reinterpret_cast<float4*>(vb)[lane] = vv;
+        __syncwarp();
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+        for (int j = 0; j < 128; j += 4) {
+            const float4 w = reinterpret_cast<const float4*>(vb)[j >> 2];
+            s0 = fmaf(ex2(fmaf(__uint_as_float(v[j]), p.acc_scale, nlh) + nll), w.x, s0);
+            s1 = fmaf(ex2(fmaf(__uint_as_float(v[j + 1]), p.acc_scale, nlh) + nll), w.y, s1);
+            s2 = fmaf(ex2(fmaf(__uint_as_float(v[j + 2]), p.acc_scale, nlh) + nll), w.z, s2);
+            s3 = fmaf(ex2(fmaf(__uint_as_float(v[j + 3]), p.acc_scale, nlh) + nll), w.w, s3);
+        }
+        S += double((s0 + s1) + (s2 + s3));
+        __syncwarp();
+    } else {
+        if (umax > M) {
+            if (S != 0.0) S *= double(ex2(p.break_lse ? umax - M : M - umax));
+            M = umax;
+        }
+        // every term of this tile is < 2^-64 of the running max for all 32 rows of
+        // the warp: the whole tile adds < m 2^-64 relative - below rounding
+        const bool dead = M == -INFINITY;
+        if (__all_sync(0xffffffffu, dead || umax < M - kSkipLog2)) return;
+        const float nm = dead ? 0.0f : -M;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+        for (int j = 0; j < 128; j += 4) {
+            s0 += ex2(fmaf(__uint_as_float(v[j]), p.acc_scale, nm));
+            s1 += ex2(fmaf(__uint_as_float(v[j + 1]), p.acc_scale, nm));
+            s2 += ex2(fmaf(__uint_as_float(v[j + 2]), p.acc_scale, nm));
+            s3 += ex2(fmaf(__uint_as_float(v[j + 3]), p.acc_scale, nm));
+        }
+        S += double((s0 + s1) + (s2 + s3));
+    }
+}
+
+// K1 for d > 64: every (key tile, feature chunk) step streams the query chunk of
+// both tiles with the key chunk (100 KB stages, 2-deep ring); the score of each
+// query tile accumulates over chunks in a (big, small) TMEM accumulator pair (all
+// 512 columns, single-buffered: the MMA time per tile >> the epilogue's load).
+template <bool VEC>
+__global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const TcParams p) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t* sbase = smem_raw + (base - raw);
-    constexpr int NST = CHUNKED ? CSTAGES : STAGES;
-    constexpr uint32_t BAR_OFF = CHUNKED ? C_OFF_BAR : OFF_BAR;
-    constexpr uint32_t ONES_OFF = CHUNKED ? C_OFF_ONES : OFF_ONES;
 
-    const uint32_t bar0 = base + BAR_OFF;
+    const uint32_t bar0 = base + C_OFF_BAR;
     auto kfull = [&](int s) { return bar0 + 8u * s; };
-    auto kempty = [&](int s) { return bar0 + 8u * (NST + s); };
-    const uint32_t qfull = bar0 + 8u * (2 * NST);
-    const uint32_t qempty = qfull + 8u;
-    auto accfull = [&](int b) { return qempty + 8u + 8u * b; };
-    auto accempty = [&](int b) { return qempty + 24u + 8u * b; };
-    const uint32_t screen_done = qempty + 40u;
-    const uint32_t bits_free = qempty + 48u;   // producer + MMA are done reading the bits
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + BAR_OFF + 128);
-    uint32_t* live_bits = reinterpret_cast<uint32_t*>(sbase + BAR_OFF + 256 + VBUF);
+    auto kempty = [&](int s) { return bar0 + 8u * (CSTAGES + s); };
+    const uint32_t accfull = bar0 + 8u * (2 * CSTAGES);
+    const uint32_t accempty = accfull + 8u;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + C_OFF_BAR + 128);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-    fill_ones_chunk(sbase + ONES_OFF, threadIdx.x, NUM_THREADS);
-    if constexpr (SCREEN)
-        for (int i = threadIdx.x; i < int(SBITS / 4); i += NUM_THREADS) live_bits[i] = 0u;
+    fill_ones_chunk(sbase + C_OFF_ONES, threadIdx.x, NUM_THREADS);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (threadIdx.x == 0) {
-        for (int s = 0; s < NST; ++s) {
+        for (int s = 0; s < CSTAGES; ++s) {
             mbar_init(kfull(s), 1);
             mbar_init(kempty(s), 1);
         }
-        mbar_init(qfull, 1);
-        mbar_init(qempty, 1);
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(accfull(b), 1);
-            mbar_init(accempty(b), 8);
-        }
-        mbar_init(screen_done, 8);
-        mbar_init(bits_free, 2);
+        mbar_init(accfull, 1);
+        mbar_init(accempty, 8);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -155,326 +199,107 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_kernel(const TcParams p
     __syncthreads();
     fence_after();
     const uint32_t tmem = *tmem_slot;
-    // phase-2 tile list of work item `lu` (after screen_done): next live tile >= kt
-    auto next_live = [&](int kt, int kt0, int kt1) {
-        while (kt < kt1) {
-            const int rel = kt - kt0;
-            const uint32_t w = live_bits[rel >> 5] >> (rel & 31);
-            if (w) return kt + __ffs(w) - 1;
-            kt += 32 - (rel & 31);
-        }
-        return kt1;
-    };
-
-    const int units = (p.q_tiles + 1) / 2;
     const int ktiles_per_split = (p.k_tiles + p.splits - 1) / p.splits;
+    const int C = p.chunks;
 
     if (warp == 0) {
         if (lane == 0) {
-            int it = 0, lu = 0;
-            for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++lu) {
+            int it = 0;
+            for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
                 const int unit = item / p.splits, split = item % p.splits;
                 const int qt0 = p.q_tile_begin + 2 * unit;
                 const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
-                if constexpr (CHUNKED) {
-                    const int C = p.chunks;
-                    for (int kt = kt0; kt < kt1; ++kt) {
-                        for (int c = 0; c < C; ++c, ++it) {
-                            const int s = it % NST;
-                            mbar_wait(kempty(s), ((it / NST) & 1) ^ 1);
-                            mbar_expect_tx(kfull(s), (nq + 1) * QTILE + BIAS);
-                            const uint32_t dst = base + s * CSTAGE;
-                            for (int t = 0; t < nq; ++t)
-                                bulk_g2s(dst + t * QTILE,
-                                         p.qimg + (size_t(qt0 + t) * C + c) * QTILE, QTILE,
-                                         kfull(s));
-                            bulk_g2s(dst + 2 * QTILE, p.kimg + (size_t(kt) * C + c) * QTILE,
+                for (int kt = kt0; kt < kt1; ++kt) {
+                    for (int c = 0; c < C; ++c, ++it) {
+                        const int s = it % CSTAGES;
+                        mbar_wait(kempty(s), ((it / CSTAGES) & 1) ^ 1);
+                        mbar_expect_tx(kfull(s), (nq + 1) * QTILE + BIAS);
+                        const uint32_t dst = base + s * CSTAGE;
+                        for (int t = 0; t < nq; ++t)
+                            bulk_g2s(dst + t * QTILE, p.qimg + (size_t(qt0 + t) * C + c) * QTILE,
                                      QTILE, kfull(s));
-                            bulk_g2s(dst + 3 * QTILE, p.kbias + size_t(kt) * BIAS, BIAS,
-                                     kfull(s));
-                        }
-                    }
-                } else {
-                    mbar_wait(qempty, (lu & 1) ^ 1);
-                    mbar_expect_tx(qfull, nq * QTILE);
-                    bulk_g2s(base + OFF_Q, p.qimg + size_t(qt0) * QTILE, nq * QTILE, qfull);
-                    if constexpr (SCREEN) {
-                        // phase 1: hi chunk + bias only
-                        for (int kt = kt0; kt < kt1; ++kt, ++it) {
-                            const int s = it % STAGES;
-                            mbar_wait(kempty(s), ((it / STAGES) & 1) ^ 1);
-                            mbar_expect_tx(kfull(s), CHUNK + BIAS);
-                            const uint32_t dst = base + OFF_K + s * KSTAGE;
-                            bulk_g2s(dst, p.kimg + size_t(kt) * QTILE, CHUNK, kfull(s));
-                            bulk_g2s(dst + QTILE, p.kbias + size_t(kt) * BIAS, BIAS, kfull(s));
-                        }
-                        mbar_wait(screen_done, lu & 1);
-                    }
-                    int nlive = 0;
-                    for (int kt = SCREEN ? next_live(kt0, kt0, kt1) : kt0; kt < kt1;
-                         kt = SCREEN ? next_live(kt + 1, kt0, kt1) : kt + 1, ++it, ++nlive) {
-                        const int s = it % STAGES;
-                        const uint32_t ph = (it / STAGES) & 1;
-                        mbar_wait(kempty(s), ph ^ 1);
-                        mbar_expect_tx(kfull(s), KSTAGE);
-                        const uint32_t dst = base + OFF_K + s * KSTAGE;
-                        bulk_g2s(dst, p.kimg + size_t(kt) * QTILE, QTILE, kfull(s));
-                        bulk_g2s(dst + QTILE, p.kbias + size_t(kt) * BIAS, BIAS, kfull(s));
-                    }
-                    if constexpr (SCREEN) {
-                        mbar_arrive(bits_free);
-                        if (p.live_count) atomicAdd(p.live_count, (unsigned long long)nlive);
+                        bulk_g2s(dst + 2 * QTILE, p.kimg + (size_t(kt) * C + c) * QTILE, QTILE,
+                                 kfull(s));
+                        bulk_g2s(dst + 3 * QTILE, p.kbias + size_t(kt) * BIAS, BIAS, kfull(s));
                     }
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            int it = 0, acc_it = 0, lu = 0;
-            for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++lu) {
+            int it = 0, acc_it = 0;
+            for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
                 const int unit = item / p.splits, split = item % p.splits;
                 const int qt0 = p.q_tile_begin + 2 * unit;
                 const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
-                if constexpr (!CHUNKED) {
-                    mbar_wait(qfull, lu & 1);
-                    fence_after();
-                }
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
-                if constexpr (SCREEN) {
-                    for (int kt = kt0; kt < kt1; ++kt, ++acc_it, ++it) {
-                        const int b = acc_it & 1;
-                        mbar_wait(accempty(b), ((acc_it >> 1) & 1) ^ 1);
-                        const int s = it % STAGES;
-                        mbar_wait(kfull(s), (it / STAGES) & 1);
-                        fence_after();
-                        const uint32_t kst = base + OFF_K + s * KSTAGE;
-                        for (int t = 0; t < nq; ++t)
-                            issue_screen_tile(tmem + uint32_t((b * 2 + t) * TILE),
-                                              base + OFF_Q + t * QTILE, base + OFF_ONES, kst);
-                        umma_commit(kempty(s));
-                        umma_commit(accfull(b));
-                    }
-                    mbar_wait(screen_done, lu & 1);
-                }
-                for (int kt = SCREEN ? next_live(kt0, kt0, kt1) : kt0; kt < kt1;
-                     kt = SCREEN ? next_live(kt + 1, kt0, kt1) : kt + 1, ++acc_it) {
-                    // chunked: one (big, small) accumulator pair per query tile =
-                    // all 512 columns, single-buffered (MMA time per tile >> epilogue)
-                    const int b = CHUNKED ? 0 : (acc_it & 1);
-                    const uint32_t aph = CHUNKED ? (acc_it & 1) : ((acc_it >> 1) & 1);
-                    mbar_wait(accempty(b), aph ^ 1);
+                for (int kt = kt0; kt < kt1; ++kt, ++acc_it) {
+                    mbar_wait(accempty, (acc_it & 1) ^ 1);
                     fence_after();
-                    if constexpr (CHUNKED) {
-                        for (int c = 0; c < p.chunks; ++c, ++it) {
-                            const int s = it % NST;
-                            mbar_wait(kfull(s), (it / NST) & 1);
-                            fence_after();
-                            const uint32_t st = base + s * CSTAGE;
-                            for (int t = 0; t < nq; ++t)
-                                issue_score_chunk(tmem + uint32_t(t * 2 * TILE),
-                                                  tmem + uint32_t((t * 2 + 1) * TILE),
-                                                  st + t * QTILE, st + 2 * QTILE,
-                                                  base + ONES_OFF, st + 3 * QTILE, c == 0);
-                            umma_commit(kempty(s));
-                        }
-                    } else {
-                        const int s = it % STAGES;
-                        mbar_wait(kfull(s), (it / STAGES) & 1);
+                    for (int c = 0; c < C; ++c, ++it) {
+                        const int s = it % CSTAGES;
+                        mbar_wait(kfull(s), (it / CSTAGES) & 1);
                         fence_after();
-                        const uint32_t kst = base + OFF_K + s * KSTAGE;
+                        const uint32_t st = base + s * CSTAGE;
                         for (int t = 0; t < nq; ++t)
-                            issue_score_tile(tmem + uint32_t((b * 2 + t) * TILE),
-                                             base + OFF_Q + t * QTILE, base + OFF_ONES, kst);
+                            issue_score_chunk(tmem + uint32_t(t * 2 * TILE),
+                                              tmem + uint32_t((t * 2 + 1) * TILE), st + t * QTILE,
+                                              st + 2 * QTILE, base + C_OFF_ONES, st + 3 * QTILE,
+                                              c == 0);
                         umma_commit(kempty(s));
-                        ++it;
                     }
-                    umma_commit(accfull(b));
+                    umma_commit(accfull);
                 }
-                if constexpr (SCREEN) mbar_arrive(bits_free);
-                if constexpr (!CHUNKED) umma_commit(qempty);
             }
         }
     } else {
         // epilogue: warps 2..9; query tile t = (warp-2)/4, TMEM lane quarter = warp % 4
         const int t = (warp - 2) >> 2;
         const int quarter = warp & 3;
-        const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
-        int acc_it = 0, lu = 0;
-        for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++lu) {
+        const uint32_t a0 = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(t * 2 * TILE);
+        float* vb = reinterpret_cast<float*>(sbase + C_OFF_BAR + 256) + (warp - 2) * TILE;
+        int acc_it = 0;
+        for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
             const int unit = item / p.splits, split = item % p.splits;
             const int qt0 = p.q_tile_begin + 2 * unit;
             const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
             const int kt0 = split * ktiles_per_split;
             const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
+            const int64_t row = int64_t(qt0 + t) * TILE + quarter * 32 + lane;
             float M = -INFINITY;
             double S = 0.0;
-            const int64_t row = int64_t(qt0 + t) * TILE + quarter * 32 + lane;
-            if constexpr (SCREEN) {
-                // phase 1: approximate running max, live-tile marking
-                float Ma = -INFINITY;
-                const bool row_ok = t < nq && row < p.R;
-                for (int kt = kt0; kt < kt1; ++kt, ++acc_it) {
-                    const int b = acc_it & 1;
-                    mbar_wait(accfull(b), (acc_it >> 1) & 1);
-                    fence_after();
-                    // only the tile max is needed: stream the 128 columns 32 at a time
-                    float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
-                    const int64_t kbase = int64_t(kt) * TILE;
-                    if (t < nq) {
-                        const uint32_t a0 = tmem + lane_addr + uint32_t((b * 2 + t) * TILE);
-#pragma unroll 1
-                        for (int q = 0; q < 4; ++q) {
-                            uint32_t v[32];
-                            FSKB_TMEM_LD32(a0 + 32 * q, v);
-                            tmem_ld_wait();
-                            if (kbase + 32 * q + 32 > p.key_valid) {
-#pragma unroll
-                                for (int j = 0; j < 32; ++j)
-                                    if (kbase + 32 * q + j >= p.key_valid)
-                                        v[j] = __float_as_uint(-INFINITY);
-                            }
-#pragma unroll
-                            for (int j = 0; j < 32; j += 4) {
-                                mx0 = fmaxf(mx0, __uint_as_float(v[j]));
-                                mx1 = fmaxf(mx1, __uint_as_float(v[j + 1]));
-                                mx2 = fmaxf(mx2, __uint_as_float(v[j + 2]));
-                                mx3 = fmaxf(mx3, __uint_as_float(v[j + 3]));
-                            }
-                        }
-                    }
-                    fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(accempty(b));
-                    if (t >= nq) continue;
-                    const float tmax = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * p.acc_scale;
-                    Ma = fmaxf(Ma, tmax);
-                    const bool live = row_ok && tmax >= Ma - p.screen_thr;
-                    if (__any_sync(0xffffffffu, live) && lane == 0)
-                        atomicOr(&live_bits[(kt - kt0) >> 5], 1u << ((kt - kt0) & 31));
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(screen_done);
-                mbar_wait(screen_done, lu & 1);
-            }
             float nlh = 0.0f, nll = 0.0f;
-            float* vb = reinterpret_cast<float*>(sbase + BAR_OFF + 256) + (warp - 2) * TILE;
             if constexpr (VEC) {
                 const bool live = t < nq && row < p.R;
                 nlh = live ? -p.l2h[row] : -3.0e38f;
                 nll = live ? -p.l2l[row] : 0.0f;
             }
-            for (int kt = SCREEN ? next_live(kt0, kt0, kt1) : kt0; kt < kt1;
-                 kt = SCREEN ? next_live(kt + 1, kt0, kt1) : kt + 1, ++acc_it) {
-                const int b = CHUNKED ? 0 : (acc_it & 1);
-                const uint32_t aph = CHUNKED ? (acc_it & 1) : ((acc_it >> 1) & 1);
-                mbar_wait(accfull(b), aph);
+            for (int kt = kt0; kt < kt1; ++kt, ++acc_it) {
+                mbar_wait(accfull, acc_it & 1);
                 fence_after();
                 uint32_t v[128];
                 if (t < nq) {
-                    if constexpr (CHUNKED) {
-                        // score = big + small accumulator
-                        const uint32_t a0 = tmem + lane_addr + uint32_t(t * 2 * TILE);
+                    // score = big + small accumulator
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            uint32_t w[32];
-                            FSKB_TMEM_LD32(a0 + 32 * q, (v + 32 * q));
-                            FSKB_TMEM_LD32(a0 + TILE + 32 * q, w);
-                            tmem_ld_wait();
-#pragma unroll
-                            for (int j = 0; j < 32; ++j)
-                                v[32 * q + j] = __float_as_uint(__uint_as_float(v[32 * q + j]) +
-                                                                __uint_as_float(w[j]));
-                        }
-                    } else {
-                        const uint32_t a0 = tmem + lane_addr + uint32_t((b * 2 + t) * TILE);
-                        FSKB_TMEM_LD32(a0 + 0, (v + 0));
-                        FSKB_TMEM_LD32(a0 + 32, (v + 32));
-                        FSKB_TMEM_LD32(a0 + 64, (v + 64));
-                        FSKB_TMEM_LD32(a0 + 96, (v + 96));
+                    for (int q = 0; q < 4; ++q) {
+                        uint32_t w[32];
+                        FSKB_TMEM_LD32(a0 + 32 * q, (v + 32 * q));
+                        FSKB_TMEM_LD32(a0 + TILE + 32 * q, w);
                         tmem_ld_wait();
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            v[32 * q + j] = __float_as_uint(__uint_as_float(v[32 * q + j]) +
+                                                            __uint_as_float(w[j]));
                     }
                 }
                 fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(accempty(b));
+                if (lane == 0) mbar_arrive(accempty);
                 if (t >= nq) continue;
-                // mask padded keys of the last tile
-                const int64_t kbase = int64_t(kt) * TILE;
-                if (kbase + TILE > p.key_valid) {
-#pragma unroll
-                    for (int j = 0; j < 128; ++j)
-                        if (kbase + j >= p.key_valid) v[j] = __float_as_uint(-INFINITY);
-                }
-                float mx0 = __uint_as_float(v[0]), mx1 = __uint_as_float(v[1]);
-                float mx2 = __uint_as_float(v[2]), mx3 = __uint_as_float(v[3]);
-#pragma unroll
-                for (int j = 4; j < 128; j += 4) {
-                    mx0 = fmaxf(mx0, __uint_as_float(v[j]));
-                    mx1 = fmaxf(mx1, __uint_as_float(v[j + 1]));
-                    mx2 = fmaxf(mx2, __uint_as_float(v[j + 2]));
-                    mx3 = fmaxf(mx3, __uint_as_float(v[j + 3]));
-                }
-                const float umax = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * p.acc_scale;
-                if constexpr (VEC) {
-                    // P~ = 2^(t - L) <= 1; a tile whose P~ are all < 2^-64 for the warp's
-                    // rows adds < m 2^-64 max|v| - below the fp32 result's rounding
-                    if (__all_sync(0xffffffffu, umax + nlh < -kSkipLog2)) continue;
-                    // the tile's 128 values of v, broadcast through a per-warp buffer
-                    float4 vv = make_float4(0.f, 0.f, 0.f, 0.f);
-                    const int64_t j0 = kbase + 4 * lane;
-                    if (j0 + 3 < p.key_valid) {
-                        vv = *reinterpret_cast<const float4*>(p.vvec + j0);
-                    } else {
-                        if (j0 < p.key_valid) vv.x = p.vvec[j0];
-                        if (j0 + 1 < p.key_valid) vv.y = p.vvec[j0 + 1];
-                        if (j0 + 2 < p.key_valid) vv.z = p.vvec[j0 + 2];
-                    }
-                    reinterpret_cast<float4*>(vb)[lane] = vv;
-                    __syncwarp();
-                    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-#pragma unroll
-                    for (int j = 0; j < 128; j += 4) {
-                        const float4 w = reinterpret_cast<const float4*>(vb)[j >> 2];
-                        s0 = fmaf(ex2(fmaf(__uint_as_float(v[j]), p.acc_scale, nlh) + nll), w.x, s0);
-                        s1 = fmaf(ex2(fmaf(__uint_as_float(v[j + 1]), p.acc_scale, nlh) + nll), w.y,
-                                  s1);
-                        s2 = fmaf(ex2(fmaf(__uint_as_float(v[j + 2]), p.acc_scale, nlh) + nll), w.z,
-                                  s2);
-                        s3 = fmaf(ex2(fmaf(__uint_as_float(v[j + 3]), p.acc_scale, nlh) + nll), w.w,
-                                  s3);
-                    }
-                    S += double((s0 + s1) + (s2 + s3));
-                    __syncwarp();
-                } else {
-                    if (umax > M) {
-                        if (S != 0.0) S *= double(ex2(p.break_lse ? umax - M : M - umax));
-                        M = umax;
-                    }
-                    // every term of this tile is < 2^-64 of the running max for all 32
-                    // rows of the warp: the whole tile adds < m 2^-64 relative
-                    const bool dead = M == -INFINITY;
-                    if (__all_sync(0xffffffffu, dead || umax < M - kSkipLog2)) continue;
-                    const float nm = dead ? 0.0f : -M;
-                    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-#pragma unroll
-                    for (int j = 0; j < 128; j += 4) {
-                        s0 += ex2(fmaf(__uint_as_float(v[j]), p.acc_scale, nm));
-                        s1 += ex2(fmaf(__uint_as_float(v[j + 1]), p.acc_scale, nm));
-                        s2 += ex2(fmaf(__uint_as_float(v[j + 2]), p.acc_scale, nm));
-                        s3 += ex2(fmaf(__uint_as_float(v[j + 3]), p.acc_scale, nm));
-                    }
-                    S += double((s0 + s1) + (s2 + s3));
-                }
-            }
-            if constexpr (SCREEN) {
-                // recycle the bitmask once nobody reads this item's list any more
-                mbar_wait(bits_free, lu & 1);
-                asm volatile("bar.sync 1, 256;" ::: "memory");
-                for (int i = threadIdx.x - 64; i < int(SBITS / 4); i += 256) live_bits[i] = 0u;
-                asm volatile("bar.sync 1, 256;" ::: "memory");
+                k1_tile_update<VEC>(v, int64_t(kt) * TILE, p, M, S, nlh, nll, vb, lane);
             }
             if (t < nq && row >= p.row_begin && row < p.row_end) {
                 if constexpr (VEC) {
@@ -763,67 +588,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 __syncwarp();
                 if (lane == 0) mbar_arrive(accempty(t));
                 ++acc_n;
-                const int64_t kbase = int64_t(kt) * TILE;
-                if (kbase + TILE > p.key_valid) {
-#pragma unroll
-                    for (int j = 0; j < 128; ++j)
-                        if (kbase + j >= p.key_valid) v[j] = __float_as_uint(-INFINITY);
-                }
-                float mx0 = __uint_as_float(v[0]), mx1 = __uint_as_float(v[1]);
-                float mx2 = __uint_as_float(v[2]), mx3 = __uint_as_float(v[3]);
-#pragma unroll
-                for (int j = 4; j < 128; j += 4) {
-                    mx0 = fmaxf(mx0, __uint_as_float(v[j]));
-                    mx1 = fmaxf(mx1, __uint_as_float(v[j + 1]));
-                    mx2 = fmaxf(mx2, __uint_as_float(v[j + 2]));
-                    mx3 = fmaxf(mx3, __uint_as_float(v[j + 3]));
-                }
-                const float umax = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * p.acc_scale;
-                if constexpr (VEC) {
-                    if (__all_sync(0xffffffffu, umax + nlh < -kSkipLog2)) continue;
-                    float4 vv = make_float4(0.f, 0.f, 0.f, 0.f);
-                    const int64_t j0 = kbase + 4 * lane;
-                    if (j0 + 3 < p.key_valid) {
-                        vv = *reinterpret_cast<const float4*>(p.vvec + j0);
-                    } else {
-                        if (j0 < p.key_valid) vv.x = p.vvec[j0];
-                        if (j0 + 1 < p.key_valid) vv.y = p.vvec[j0 + 1];
-                        if (j0 + 2 < p.key_valid) vv.z = p.vvec[j0 + 2];
-                    }
-                    reinterpret_cast<float4*>(vb)[lane] = vv;
-                    __syncwarp();
-                    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-#pragma unroll
-                    for (int j = 0; j < 128; j += 4) {
-                        const float4 w = reinterpret_cast<const float4*>(vb)[j >> 2];
-                        s0 = fmaf(ex2(fmaf(__uint_as_float(v[j]), p.acc_scale, nlh) + nll), w.x, s0);
-                        s1 = fmaf(ex2(fmaf(__uint_as_float(v[j + 1]), p.acc_scale, nlh) + nll), w.y,
-                                  s1);
-                        s2 = fmaf(ex2(fmaf(__uint_as_float(v[j + 2]), p.acc_scale, nlh) + nll), w.z,
-                                  s2);
-                        s3 = fmaf(ex2(fmaf(__uint_as_float(v[j + 3]), p.acc_scale, nlh) + nll), w.w,
-                                  s3);
-                    }
-                    S += double((s0 + s1) + (s2 + s3));
-                    __syncwarp();
-                } else {
-                    if (umax > M) {
-                        if (S != 0.0) S *= double(ex2(p.break_lse ? umax - M : M - umax));
-                        M = umax;
-                    }
-                    const bool dead = M == -INFINITY;
-                    if (__all_sync(0xffffffffu, dead || umax < M - kSkipLog2)) continue;
-                    const float nm = dead ? 0.0f : -M;
-                    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-#pragma unroll
-                    for (int j = 0; j < 128; j += 4) {
-                        s0 += ex2(fmaf(__uint_as_float(v[j]), p.acc_scale, nm));
-                        s1 += ex2(fmaf(__uint_as_float(v[j + 1]), p.acc_scale, nm));
-                        s2 += ex2(fmaf(__uint_as_float(v[j + 2]), p.acc_scale, nm));
-                        s3 += ex2(fmaf(__uint_as_float(v[j + 3]), p.acc_scale, nm));
-                    }
-                    S += double((s0 + s1) + (s2 + s3));
-                }
+                k1_tile_update<VEC>(v, int64_t(kt) * TILE, p, M, S, nlh, nll, vb, lane);
             }
             if constexpr (SCREEN) {
                 mbar_wait(bits_free, lu & 1);
@@ -1117,6 +882,257 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_kernel(const TcApplyP
     }
 }
 
+// ---- general transport-matrix application (any d, any V) -----------------------
+//
+// O = softmax(S) V for a general V (cols x p) and any d: the score tile streams
+// 64-wide feature chunks (query chunk + key chunk + bias per step, 2 x 68 KB
+// stages) into a (big, small) TMEM accumulator pair, bit-identical to the
+// chunked K1 so P~ = 2^(t - L + 12) normalises exactly against that pass's L.
+// P~ is split hi/lo into fp16 over the big accumulator and a second GEMM
+// O += P~ V reads it from TMEM (A operand) against VC <= 2 64-column chunks of
+// V's own split image (64 KB stage). p > 128 takes several passes (the score is
+// recomputed per pass; P~ never leaves TMEM). 1 query tile per work item; the
+// epilogue is the 4 lane quarters x 2 column halves of tc_apply_kernel.
+constexpr uint32_t G_STAGE = 2 * QTILE + BIAS;                  // 68 KB
+constexpr int G_STAGES = 2;
+constexpr uint32_t G_OFF_V = G_STAGES * G_STAGE;                // 136 KB
+constexpr uint32_t G_OFF_ONES = G_OFF_V + 2 * QTILE;            // 200 KB
+constexpr uint32_t G_OFF_BAR = G_OFF_ONES + BIAS;               // 204 KB
+constexpr uint32_t G_SMEM_BYTES = G_OFF_BAR + 256 + 1024;
+constexpr uint32_t G_OCOL = 2 * TILE;                            // O at column 256
+
+struct TcApplyGenParams {
+    const uint8_t* qimg;    // [q tile][chunk][hi|lo]
+    const uint8_t* kimg;    // [k tile][chunk][hi|lo]
+    const uint8_t* kbias;   // [k tile] 4 KB
+    const uint8_t* vimg;    // [k tile][V chunk][hi|lo]
+    int chunks;             // feature chunks
+    int v_chunks;           // V chunks in the image
+    int v_chunk0, vc;       // this pass: V chunks [v_chunk0, v_chunk0 + vc), vc <= 2
+    int q_tile_begin, q_tiles, k_tiles, splits, items;
+    int64_t row_begin, row_end, key_valid, R;
+    float acc_scale;
+    const float* l2h;
+    const float* l2l;
+    float* part_o;          // [splits][R][vc * 64]
+};
+
+__global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcApplyGenParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t* sbase = smem_raw + (base - raw);
+
+    const uint32_t bar0 = base + G_OFF_BAR;
+    auto kfull = [&](int s) { return bar0 + 8u * s; };
+    auto kempty = [&](int s) { return bar0 + 8u * (G_STAGES + s); };
+    const uint32_t vfull = bar0 + 8u * (2 * G_STAGES);
+    const uint32_t vempty = vfull + 8u;
+    const uint32_t sfull = vfull + 16u;
+    const uint32_t pready = vfull + 24u;
+    const uint32_t ofull = vfull + 32u;
+    const uint32_t oempty = vfull + 40u;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + G_OFF_BAR + 128);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    fill_ones_chunk(sbase + G_OFF_ONES, threadIdx.x, NUM_THREADS);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < G_STAGES; ++s) {
+            mbar_init(kfull(s), 1);
+            mbar_init(kempty(s), 1);
+        }
+        mbar_init(vfull, 1);
+        mbar_init(vempty, 1);
+        mbar_init(sfull, 1);
+        mbar_init(pready, 8);
+        mbar_init(ofull, 1);
+        mbar_init(oempty, 8);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+            smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int ktiles_per_split = (p.k_tiles + p.splits - 1) / p.splits;
+    const int C = p.chunks;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int it = 0, vt = 0;
+            for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+                const int unit = item / p.splits, split = item % p.splits;
+                const int qt = p.q_tile_begin + unit;
+                const int kt0 = split * ktiles_per_split;
+                const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
+                for (int kt = kt0; kt < kt1; ++kt, ++vt) {
+                    for (int c = 0; c < C; ++c, ++it) {
+                        const int s = it % G_STAGES;
+                        mbar_wait(kempty(s), ((it / G_STAGES) & 1) ^ 1);
+                        mbar_expect_tx(kfull(s), 2 * QTILE + BIAS);
+                        const uint32_t dst = base + s * G_STAGE;
+                        bulk_g2s(dst, p.qimg + (size_t(qt) * C + c) * QTILE, QTILE, kfull(s));
+                        bulk_g2s(dst + QTILE, p.kimg + (size_t(kt) * C + c) * QTILE, QTILE,
+                                 kfull(s));
+                        bulk_g2s(dst + 2 * QTILE, p.kbias + size_t(kt) * BIAS, BIAS, kfull(s));
+                    }
+                    mbar_wait(vempty, (vt & 1) ^ 1);
+                    mbar_expect_tx(vfull, p.vc * QTILE);
+                    bulk_g2s(base + G_OFF_V,
+                             p.vimg + (size_t(kt) * p.v_chunks + p.v_chunk0) * QTILE,
+                             p.vc * QTILE, vfull);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            int it = 0, vt = 0, lu = 0;
+            for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++lu) {
+                const int split = item % p.splits;
+                const int kt0 = split * ktiles_per_split;
+                const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
+                mbar_wait(oempty, (lu & 1) ^ 1);
+                fence_after();
+                for (int kt = kt0; kt < kt1; ++kt, ++vt) {
+                    for (int c = 0; c < C; ++c, ++it) {
+                        const int s = it % G_STAGES;
+                        mbar_wait(kfull(s), (it / G_STAGES) & 1);
+                        fence_after();
+                        const uint32_t st = base + s * G_STAGE;
+                        issue_score_chunk(tmem, tmem + TILE, st, st + QTILE, base + G_OFF_ONES,
+                                          st + 2 * QTILE, c == 0);
+                        umma_commit(kempty(s));
+                    }
+                    umma_commit(sfull);
+                    mbar_wait(pready, vt & 1);
+                    mbar_wait(vfull, vt & 1);
+                    fence_after();
+                    for (int j = 0; j < p.vc; ++j) {
+                        const uint32_t vst = base + G_OFF_V + j * QTILE;
+                        const uint32_t o = tmem + G_OCOL + uint32_t(j * DPAD);
+#pragma unroll
+                        for (int kk = 0; kk < TILE / 16; ++kk) {
+                            const uint32_t ph = tmem + uint32_t((kk >> 2) * 64 + (kk & 3) * 8);
+                            const uint64_t vh = umma_desc(vst + kk * 2048, 1024, 2, 8192);
+                            const uint64_t vl = umma_desc(vst + CHUNK + kk * 2048, 1024, 2, 8192);
+                            umma_ts(o, ph, vh, IDESC_PV, (kt > kt0 || kk > 0) ? 1u : 0u);
+                            umma_ts(o, ph + 32, vh, IDESC_PV, 1u);
+                            umma_ts(o, ph, vl, IDESC_PV, 1u);
+                        }
+                    }
+                    umma_commit(vempty);
+                }
+                umma_commit(ofull);
+            }
+        }
+    } else {
+        const int quarter = warp & 3;
+        const int half = (warp - 2) >> 2;
+        const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
+        int vt = 0, lu = 0;
+        for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++lu) {
+            const int unit = item / p.splits, split = item % p.splits;
+            const int qt = p.q_tile_begin + unit;
+            const int kt0 = split * ktiles_per_split;
+            const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
+            const int64_t row = int64_t(qt) * TILE + quarter * 32 + lane;
+            const bool live = row < p.R;
+            const float nlh = live ? -p.l2h[row] : -3.0e38f;
+            const float c2 = live ? kPScaleLog2 - p.l2l[row] : 0.0f;
+            for (int kt = kt0; kt < kt1; ++kt, ++vt) {
+                mbar_wait(sfull, vt & 1);
+                fence_after();
+                const uint32_t taddr = tmem + lane_addr + uint32_t(half * 64);
+                uint32_t v[64];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    uint32_t w[32];
+                    FSKB_TMEM_LD32(taddr + 32 * q, (v + 32 * q));
+                    FSKB_TMEM_LD32(taddr + TILE + 32 * q, w);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        v[32 * q + j] =
+                            __float_as_uint(__uint_as_float(v[32 * q + j]) + __uint_as_float(w[j]));
+                }
+                const int64_t kbase = int64_t(kt) * TILE + half * 64;
+                if (kbase + 64 > p.key_valid) {
+#pragma unroll
+                    for (int j = 0; j < 64; ++j)
+                        if (kbase + j >= p.key_valid) v[j] = __float_as_uint(-3.0e38f);
+                }
+                uint32_t hi[32], lo[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float p0 = ex2(fmaf(__uint_as_float(v[2 * j]), p.acc_scale, nlh) + c2);
+                    const float p1 =
+                        ex2(fmaf(__uint_as_float(v[2 * j + 1]), p.acc_scale, nlh) + c2);
+                    const __half2 h = __floats2half2_rn(p0, p1);
+                    const float2 hf = __half22float2(h);
+                    const __half2 l = __floats2half2_rn(p0 - hf.x, p1 - hf.y);
+                    hi[j] = *reinterpret_cast<const uint32_t*>(&h);
+                    lo[j] = *reinterpret_cast<const uint32_t*>(&l);
+                }
+                FSKB_TMEM_ST32(taddr, hi);
+                FSKB_TMEM_ST32(taddr + 32, lo);
+                tmem_st_wait();
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(pready);
+            }
+            mbar_wait(ofull, lu & 1);
+            fence_after();
+            const int width = p.vc * DPAD;          // 64 or 128 output columns
+            const int per_half = width / 2;         // 32 or 64
+            uint32_t o[64];
+            const uint32_t oaddr = tmem + lane_addr + G_OCOL + uint32_t(half * per_half);
+            FSKB_TMEM_LD32(oaddr, o);
+            if (per_half == 64) FSKB_TMEM_LD32(oaddr + 32, (o + 32));
+            tmem_ld_wait();
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(oempty);
+            if (row >= p.row_begin && row < p.row_end) {
+                float* dst = p.part_o + (size_t(split) * p.R + row) * width + half * per_half;
+#pragma unroll
+                for (int c = 0; c < 64; c += 4) {
+                    if (c >= per_half) break;
+                    *reinterpret_cast<float4*>(dst + c) =
+                        make_float4(__uint_as_float(o[c]), __uint_as_float(o[c + 1]),
+                                    __uint_as_float(o[c + 2]), __uint_as_float(o[c + 3]));
+                }
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}
+
+// out[i][col0 + c] = marg_i * inv_v * sum_s part[s][i][c]   (P V = diag(r) P~ V)
+__global__ void tc_apply_gen_finalize(const float* __restrict__ part, int splits, int64_t R,
+                                      int width, int cols, int col0, int64_t p_total,
+                                      const float* __restrict__ marg, double inv_v,
+                                      float* __restrict__ out, int* flags) {
+    const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t i = gid / cols;
+    const int c = int(gid % cols);
+    if (i >= R) return;
+    double s = 0.0;
+    for (int k = 0; k < splits; ++k) s += double(part[(size_t(k) * R + i) * width + c]);
+    const double v = double(marg[i]) * s * inv_v;
+    if (!isfinite(v)) atomicOr(flags, kFlagNonFiniteTransport);
+    out[i * p_total + col0 + c] = float(v);
+}
+
 // transport-vector epilogue: out_i = r_i sum_s part[s][i]  (P v = diag(r) P~ v)
 __global__ void tc_vec_finalize_kernel(const double* __restrict__ part, int splits, int64_t R,
                                        const float* __restrict__ marg, double* __restrict__ out) {
@@ -1393,12 +1409,14 @@ TcHalfStep::TcHalfStep(DevProblem<float>& P) : impl_(new Impl()) {
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(TQ_SMEM_BYTES)));
     FSKB_CUDA(cudaFuncSetAttribute(tc_lse_tq_kernel<false, true>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(TQ_SMEM_BYTES)));
-    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_kernel<true, false>,
+    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_chunked_kernel<false>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(C_SMEM_BYTES)));
-    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_kernel<true, true>,
+    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_chunked_kernel<true>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(C_SMEM_BYTES)));
     FSKB_CUDA(cudaFuncSetAttribute(tc_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(A_SMEM_BYTES)));
+    FSKB_CUDA(cudaFuncSetAttribute(tc_apply_gen_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(G_SMEM_BYTES)));
     const DevSide<float>* sides[2] = {&P.src, &P.tgt};
     impl_->chunks = int((P.src.d + DPAD - 1) / DPAD);
     for (int c = 0; c < 2; ++c) {
@@ -1544,9 +1562,9 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         }
     } else {
         if (vec)
-            tc_lse_kernel<true, true><<<grid, NUM_THREADS, C_SMEM_BYTES, P.s>>>(p);
+            tc_lse_chunked_kernel<true><<<grid, NUM_THREADS, C_SMEM_BYTES, P.s>>>(p);
         else
-            tc_lse_kernel<true, false><<<grid, NUM_THREADS, C_SMEM_BYTES, P.s>>>(p);
+            tc_lse_chunked_kernel<false><<<grid, NUM_THREADS, C_SMEM_BYTES, P.s>>>(p);
     }
     FSKB_CUDA(cudaGetLastError());
     count_launch();
@@ -1580,6 +1598,72 @@ void TcHalfStep::vec(DevProblem<float>& P, int side, const float* kpot, float ep
                                                                         out);
     FSKB_CUDA(cudaGetLastError());
     count_launch();
+}
+
+void TcHalfStep::apply_mat(DevProblem<float>& P, int side, const float* kpot, float eps,
+                           const float* l2h, const float* l2l, const float* marg, const float* V,
+                           int64_t p_cols, float* out, int* flags) {
+    Impl& I = *impl_;
+    const int qc = side == 0 ? 0 : 1, kc = side == 0 ? 1 : 0;
+    const DevSide<float>& ks = side == 0 ? P.tgt : P.src;
+    const int64_t R = side == 0 ? P.src.n : P.tgt.n;
+    if (R == 0 || p_cols == 0) return;
+    const int E = I.eq[qc] + I.ek[side];
+    const int k_tiles = int(I.rows_pad[kc] / TILE);
+    build_bias<<<unsigned((I.rows_pad[kc] + 255) / 256), 256, 0, P.s>>>(
+        kpot, ks.logw.get(), ks.n, I.rows_pad[kc], double(eps), std::ldexp(1.0, -E),
+        I.kbias[side].get(), flags);
+    FSKB_CUDA(cudaGetLastError());
+    count_launch();
+    // V's own split image, [key tile][64-column chunk][hi | lo], scaled by 2^-ev
+    const int VC = int((p_cols + DPAD - 1) / DPAD);
+    const int ev = scale_exponent(double(device_absmax(V, ks.n * p_cols, P.s)));
+    DevBuf<uint8_t> vimg(size_t(k_tiles) * VC * QTILE, P.s);
+    const int64_t groups = I.rows_pad[kc] * 8 * VC;
+    build_split_image<<<unsigned((groups + 255) / 256), 256, 0, P.s>>>(
+        V, ks.n, p_cols, std::ldexp(1.0f, -ev), I.rows_pad[kc], VC, vimg.get());
+    FSKB_CUDA(cudaGetLastError());
+    count_launch();
+
+    TcApplyGenParams g{};
+    g.qimg = I.qimg[qc].get();
+    g.kimg = I.kimg[side].get();
+    g.kbias = I.kbias[side].get();
+    g.vimg = vimg.get();
+    g.chunks = I.chunks;
+    g.v_chunks = VC;
+    g.q_tile_begin = 0;
+    g.q_tiles = int(I.rows_pad[qc] / TILE);
+    g.k_tiles = k_tiles;
+    const int sms = num_sms();
+    const double q_bytes = double(I.chunks) * QTILE;
+    const int min_s = I.chunks > 1 ? int(std::ceil(sms * q_bytes / (48.0 * (1 << 20)))) : 1;
+    g.splits = pick_splits(g.q_tiles, k_tiles, sms, min_s);
+    g.items = g.q_tiles * g.splits;
+    g.row_begin = 0;
+    g.row_end = R;
+    g.key_valid = ks.n;
+    g.R = R;
+    g.acc_scale = std::ldexp(1.0f, E);
+    g.l2h = l2h;
+    g.l2l = l2l;
+    const double inv_v = std::ldexp(1.0, ev - int(kPScaleLog2));
+    DevBuf<float> part(size_t(g.splits) * size_t(R) * 2 * DPAD, P.s);
+    g.part_o = part.get();
+    for (int v0 = 0; v0 < VC; v0 += 2) {
+        g.v_chunk0 = v0;
+        g.vc = std::min(2, VC - v0);
+        tc_apply_gen_kernel<<<std::min(g.items, sms), NUM_THREADS, G_SMEM_BYTES, P.s>>>(g);
+        FSKB_CUDA(cudaGetLastError());
+        count_launch();
+        const int width = g.vc * DPAD;
+        const int cols = int(std::min<int64_t>(width, p_cols - int64_t(v0) * DPAD));
+        const int64_t total = R * cols;
+        tc_apply_gen_finalize<<<unsigned((total + 255) / 256), 256, 0, P.s>>>(
+            part.get(), g.splits, R, width, cols, v0 * DPAD, p_cols, marg, inv_v, out, flags);
+        FSKB_CUDA(cudaGetLastError());
+        count_launch();
+    }
 }
 
 void TcHalfStep::grad(DevProblem<float>& P, int side, const float* kpot, const float* pot,

@@ -56,6 +56,13 @@ public:
     void vec(DevProblem<float>& P, int side, const float* kpot, float eps, const float* l2h,
              const float* l2l, const float* marg, const float* v, double* out, int* flags);
 
+    // Transport-matrix application with fixed potentials: out (rows x p, float) =
+    // P V (side 0) or P^T V (side 1) for a general V (key rows x p, float, device),
+    // any d, via the tcgen05 general apply kernel (p in passes of 128 columns).
+    void apply_mat(DevProblem<float>& P, int side, const float* kpot, float eps, const float* l2h,
+                   const float* l2l, const float* marg, const float* V, int64_t p_cols,
+                   float* out, int* flags);
+
 private:
     void poll_screen(int side);
     int pass(DevProblem<float>& P, int side, const float* kpot, float eps, int64_t row_begin,

@@ -317,3 +317,51 @@ def test_screened_lse_matches_unscreened(fsk):
     assert live < blocks
     assert np.abs(fs - fu).max() <= 1e-6 * max(1.0, np.abs(fu).max())
     assert np.abs(gs - gu).max() <= 1e-6 * max(1.0, np.abs(gu).max())
+
+
+@pytest.mark.parametrize("n,m,d,p", [(700, 513, 64, 64), (300, 421, 100, 130), (515, 260, 33, 1),
+                                     (260, 300, 1024, 200)])
+@pytest.mark.parametrize("side", [0, 1])
+def test_tensor_transport_matrix_parity(fsk, port, n, m, d, p, side):
+    """General tcgen05 transport-matrix kernel (any d, any V, p in passes of 128
+    columns) against the fp64 apply_plan / apply_plan_adjoint (stream.cpp:324-357),
+    with the marginal-scaled contract of the transport-vector test."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(3 * n + m + d + p + side)
+    X = rng.normal(size=(n, d)) * 0.4
+    Y = rng.normal(size=(m, d)) * 0.4 + 0.1
+    a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+    eps = 0.5 if d < 512 else 2.0
+    eng = fsk.Engine(0, X, a, Y, b, mode="tensor")
+    eng.set_eps(eps)
+    f = torch.empty(n, dtype=torch.float32, device="cuda")
+    g = torch.empty(m, dtype=torch.float32, device="cuda")
+    eng.bind(f.data_ptr(), g.data_ptr())
+    eng.init_potentials()
+    for _ in range(4):
+        eng.half_step(0, 0, n)
+        eng.half_step(1, 0, m)
+    cols, rows = (m, n) if side == 0 else (n, m)
+    V = rng.normal(size=(cols, p))
+    Vd = torch.tensor(V, dtype=torch.float32, device="cuda")
+    out = torch.empty((rows, p), dtype=torch.float32, device="cuda")
+    eng.transport_mat(side, Vd.data_ptr(), p, out.data_ptr())
+    torch.cuda.synchronize()
+    fh = f.cpu().numpy().astype(np.float64)
+    gh = g.cpu().numpy().astype(np.float64)
+    V32 = V.astype(np.float32).astype(np.float64)
+    fn = port.apply_plan if side == 0 else port.apply_plan_adjoint
+    want = fn(X, a, Y, b, fh, gh, eps, V32)
+    scale = fn(X, a, Y, b, fh, gh, eps, np.abs(V32))
+    err = (np.abs(out.cpu().numpy() - want) / scale).max()
+    r64, c64 = port.induced_marginals(X, a, Y, b, fh, gh, eps)
+    if side == 0:
+        p32 = port.update_f_hat_f32(X, a, Y, b, gh, eps).astype(np.float64)
+        m32 = a * np.exp((fh - p32) / eps) / r64
+    else:
+        p32 = port.update_g_hat_f32(X, a, Y, b, fh, eps).astype(np.float64)
+        m32 = b * np.exp((gh - p32) / eps) / c64
+    e32 = (np.abs(want * (m32 - 1.0)[:, None]) / scale).max()
+    print(f"transport-matrix side {side} d={d} p={p}: max rel err {err:.2e} (ref-fp32 {e32:.2e})")
+    assert err <= max(1e-5, 2.0 * e32)
+    eng.close()
