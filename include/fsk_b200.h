@@ -292,6 +292,10 @@ int fsk_engine_transport_vec(fsk_engine* e, int side, const float* v_dev, double
  * or the fp32 CUDA-core apply. */
 int fsk_engine_transport_mat(fsk_engine* e, int side, const float* v_dev, int64_t p,
                              float* out_dev, void* stream);
+/* Hadamard-weighted transport (apply_hadamard_plan with B = Y, stream.cpp:359-375):
+ * out_dev (float, n x p) = (P (.) A Y^T) V for A (n x d) and V (m x p), device. */
+int fsk_engine_transport_hadamard(fsk_engine* e, const float* a_dev, const float* v_dev,
+                                  int64_t p, float* out_dev, void* stream);
 /* Cumulative count of (query tile pair, key tile) blocks scored in full by
  * screened tcgen05 LSE passes (phase 2); the rest were proven below 2^-64 of
  * every row's max by the 5-MMA hi x hi screen (diagnostics for the bench line).

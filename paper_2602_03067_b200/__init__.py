@@ -515,6 +515,12 @@ class Engine:
                                               C.c_int64(p), C.c_void_p(out_ptr),
                                               C.c_void_p(stream)))
 
+    def transport_hadamard(self, a_ptr: int, v_ptr: int, p: int, out_ptr: int, stream: int = 0):
+        """out (float, device, n x p) = (P (.) A Y^T) V."""
+        _check(lib().fsk_engine_transport_hadamard(self.h, C.c_void_p(a_ptr), C.c_void_p(v_ptr),
+                                                   C.c_int64(p), C.c_void_p(out_ptr),
+                                                   C.c_void_p(stream)))
+
     def grad(self, row_begin: int, row_end: int, grad_ptr: int, stream: int = 0):
         _check(lib().fsk_engine_grad(self.h, C.c_int64(row_begin), C.c_int64(row_end),
                                      C.c_void_p(grad_ptr), C.c_void_p(stream)))

@@ -231,6 +231,25 @@ int fsk_engine_transport_mat(fsk_engine* e, int side, const float* v_dev, int64_
     });
 }
 
+int fsk_engine_transport_hadamard(fsk_engine* e, const float* a_dev, const float* v_dev,
+                                  int64_t p, float* out_dev, void* stream) {
+    return eguard([&] {
+        if (!e->f || !e->g) throw ValidationFailure("engine potentials not bound");
+        if (p < 1) throw ValidationFailure("p must be positive");
+        cudaStream_t s = pick(e, stream);
+        e->P.s = s;
+        const float eps = float(e->eps);
+        SideLse L = side_lse(e, 0, s);
+        if (e->P.tc) {
+            e->P.tc->apply_mat(e->P, 0, e->g, eps, L.l2h.get(), L.l2l.get(), L.marg.get(), v_dev,
+                               p, out_dev, e->flags, a_dev);
+        } else {
+            transport<float>(e->P, 0, e->g, e->f, eps, L.lse.get(), L.mx.get(), v_dev, p, a_dev,
+                             e->P.tgt.pts.get(), e->P.src.d, out_dev, e->flags);
+        }
+    });
+}
+
 int fsk_engine_transport_vec(fsk_engine* e, int side, const float* v_dev, double* out_dev,
                              void* stream) {
     return eguard([&] {

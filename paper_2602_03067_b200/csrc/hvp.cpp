@@ -63,14 +63,22 @@ struct HvpCtx {
         std::vector<double> h((size_t)(rows * p));
         bool done = false;
         if constexpr (std::is_same_v<T, float>) {
-            if (P.tc && !A && p > 1) {
+            // Hadamard: the tensor kernel needs B = the key cloud (true in the HVP)
+            const bool had_ok = A && side == 0 && B == tgt.points && r == src.d;
+            if (P.tc && ((!A && p > 1) || had_ok)) {
                 DevBuf<float> vd(size_t(cols * p), C.s);
                 const std::vector<float> vf(V.begin(), V.end());
                 vd.upload(vf.data(), size_t(cols * p));
+                DevBuf<float> ad;
+                if (A) {
+                    const std::vector<float> af = to_t<float>(A, src.n * r);
+                    ad.alloc(size_t(src.n * r), C.s);
+                    ad.upload(af.data(), af.size());
+                }
                 DevBuf<float> out(size_t(rows * p), C.s);
                 P.s = C.s;
                 P.tc->apply_mat(P, side, kpot, float(eps), l2h[side], l2l[side], marg[side],
-                                vd.get(), p, out.get(), C.flags);
+                                vd.get(), p, out.get(), C.flags, ad.get());
                 std::vector<float> hf((size_t)(rows * p));
                 out.download(hf.data(), hf.size());
                 FSKB_CUDA(cudaStreamSynchronize(C.s));

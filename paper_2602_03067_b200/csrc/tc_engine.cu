@@ -885,65 +885,98 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_kernel(const TcApplyP
 // ---- general transport-matrix application (any d, any V) -----------------------
 //
 // O = softmax(S) V for a general V (cols x p) and any d: the score tile streams
-// 64-wide feature chunks (query chunk + key chunk + bias per step, 2 x 68 KB
-// stages) into a (big, small) TMEM accumulator pair, bit-identical to the
-// chunked K1 so P~ = 2^(t - L + 12) normalises exactly against that pass's L.
-// P~ is split hi/lo into fp16 over the big accumulator and a second GEMM
-// O += P~ V reads it from TMEM (A operand) against VC <= 2 64-column chunks of
-// V's own split image (64 KB stage). p > 128 takes several passes (the score is
-// recomputed per pass; P~ never leaves TMEM). 1 query tile per work item; the
-// epilogue is the 4 lane quarters x 2 column halves of tc_apply_kernel.
-constexpr uint32_t G_STAGE = 2 * QTILE + BIAS;                  // 68 KB
-constexpr int G_STAGES = 2;
-constexpr uint32_t G_OFF_V = G_STAGES * G_STAGE;                // 136 KB
-constexpr uint32_t G_OFF_ONES = G_OFF_V + 2 * QTILE;            // 200 KB
+// 64-wide feature chunks through a ring of 32 KB slots (query chunk, key chunk
+// and, for the Hadamard-weighted form, the direction chunk A) into a (big, small)
+// TMEM accumulator pair, bit-identical to the chunked K1 so P~ = 2^(t - L + 12)
+// normalises exactly against that pass's L. P~ is split hi/lo into fp16 over the
+// big accumulator and a second GEMM O += P~ V reads it from TMEM (A operand)
+// against VC <= 2 64-column chunks of V's own split image. p > 128 takes several
+// passes (the score is recomputed per pass; P~ never leaves TMEM).
+// Hadamard mode ((P (.) A B^T) V, apply_hadamard_plan stream.cpp:359-375): a
+// third split GEMM accumulates W = A B^T per tile in TMEM (B = the key image)
+// and the epilogue splits P~ W 2^-wexp instead of P~; VC = 1 then.
+// 1 query tile per work item; the epilogue is the 4 lane quarters x 2 column
+// halves of tc_apply_kernel.
+constexpr int G_SLOTS_MAX = 5;
+constexpr uint32_t G_OFF_V_END = 192 * 1024;                    // V region ends here
+constexpr uint32_t G_OFF_BIAS = G_OFF_V_END;                    // 2 x 4 KB bias ring
+constexpr uint32_t G_OFF_ONES = G_OFF_BIAS + 2 * BIAS;          // 200 KB
 constexpr uint32_t G_OFF_BAR = G_OFF_ONES + BIAS;               // 204 KB
 constexpr uint32_t G_SMEM_BYTES = G_OFF_BAR + 256 + 1024;
 constexpr uint32_t G_OCOL = 2 * TILE;                            // O at column 256
+constexpr uint32_t G_WCOL = 3 * TILE;                            // W at column 384
 
 struct TcApplyGenParams {
     const uint8_t* qimg;    // [q tile][chunk][hi|lo]
     const uint8_t* kimg;    // [k tile][chunk][hi|lo]
     const uint8_t* kbias;   // [k tile] 4 KB
     const uint8_t* vimg;    // [k tile][V chunk][hi|lo]
+    const uint8_t* aimg;    // Hadamard direction images (query layout), or null
     int chunks;             // feature chunks
     int v_chunks;           // V chunks in the image
-    int v_chunk0, vc;       // this pass: V chunks [v_chunk0, v_chunk0 + vc), vc <= 2
+    int v_chunk0, vc;       // this pass: V chunks [v_chunk0, v_chunk0 + vc), vc <= 2 (1)
     int q_tile_begin, q_tiles, k_tiles, splits, items;
     int64_t row_begin, row_end, key_valid, R;
     float acc_scale;
+    float w_mul;            // Hadamard: P~ W 2^-wexp = P~ * (acc_W * w_mul)
     const float* l2h;
     const float* l2l;
     float* part_o;          // [splits][R][vc * 64]
 };
+
+// 12 MMAs of one 64-feature chunk of W = A B^T into one accumulator (no bias):
+// cross terms first, then hi x hi.
+__device__ __forceinline__ void issue_w_chunk(uint32_t d, uint32_t aa, uint32_t ka, bool first) {
+#pragma unroll
+    for (int kk = 0; kk < DPAD / 16; ++kk) {
+        umma_ss(d, umma_desc(aa + CHUNK + kk * 32, 1024, 2), umma_desc(ka + kk * 32, 1024, 2),
+                IDESC_QK, (first && kk == 0) ? 0u : 1u);
+        umma_ss(d, umma_desc(aa + kk * 32, 1024, 2), umma_desc(ka + CHUNK + kk * 32, 1024, 2),
+                IDESC_QK, 1u);
+    }
+#pragma unroll
+    for (int kk = 0; kk < DPAD / 16; ++kk)
+        umma_ss(d, umma_desc(aa + kk * 32, 1024, 2), umma_desc(ka + kk * 32, 1024, 2), IDESC_QK,
+                1u);
+}
 
 __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcApplyGenParams p) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t* sbase = smem_raw + (base - raw);
+    const bool had = p.aimg != nullptr;
+    const int ops = had ? 3 : 2;                     // slots per chunk step
+    const int NS = had ? 5 : 4;                      // ring slots
+    const uint32_t off_v = G_OFF_V_END - uint32_t(had ? 1 : 2) * QTILE;
 
     const uint32_t bar0 = base + G_OFF_BAR;
-    auto kfull = [&](int s) { return bar0 + 8u * s; };
-    auto kempty = [&](int s) { return bar0 + 8u * (G_STAGES + s); };
-    const uint32_t vfull = bar0 + 8u * (2 * G_STAGES);
+    auto sfull_ = [&](int s) { return bar0 + 8u * s; };
+    auto sempty_ = [&](int s) { return bar0 + 8u * (G_SLOTS_MAX + s); };
+    const uint32_t vfull = bar0 + 8u * (2 * G_SLOTS_MAX);
     const uint32_t vempty = vfull + 8u;
-    const uint32_t sfull = vfull + 16u;
-    const uint32_t pready = vfull + 24u;
-    const uint32_t ofull = vfull + 32u;
-    const uint32_t oempty = vfull + 40u;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + G_OFF_BAR + 128);
+    auto bfull = [&](int b) { return vfull + 16u + 8u * b; };
+    auto bempty = [&](int b) { return vfull + 32u + 8u * b; };
+    const uint32_t sfull = vfull + 48u;
+    const uint32_t pready = vfull + 56u;
+    const uint32_t ofull = vfull + 64u;
+    const uint32_t oempty = vfull + 72u;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + G_OFF_BAR + 192);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     fill_ones_chunk(sbase + G_OFF_ONES, threadIdx.x, NUM_THREADS);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (threadIdx.x == 0) {
-        for (int s = 0; s < G_STAGES; ++s) {
-            mbar_init(kfull(s), 1);
-            mbar_init(kempty(s), 1);
+        for (int s = 0; s < G_SLOTS_MAX; ++s) {
+            mbar_init(sfull_(s), 1);
+            mbar_init(sempty_(s), 1);
         }
         mbar_init(vfull, 1);
         mbar_init(vempty, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(bfull(b), 1);
+            mbar_init(bempty(b), 1);
+        }
         mbar_init(sfull, 1);
         mbar_init(pready, 8);
         mbar_init(ofull, 1);
@@ -964,26 +997,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
 
     if (warp == 0) {
         if (lane == 0) {
-            int it = 0, vt = 0;
+            int sq = 0, vt = 0;
             for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
                 const int unit = item / p.splits, split = item % p.splits;
                 const int qt = p.q_tile_begin + unit;
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
                 for (int kt = kt0; kt < kt1; ++kt, ++vt) {
-                    for (int c = 0; c < C; ++c, ++it) {
-                        const int s = it % G_STAGES;
-                        mbar_wait(kempty(s), ((it / G_STAGES) & 1) ^ 1);
-                        mbar_expect_tx(kfull(s), 2 * QTILE + BIAS);
-                        const uint32_t dst = base + s * G_STAGE;
-                        bulk_g2s(dst, p.qimg + (size_t(qt) * C + c) * QTILE, QTILE, kfull(s));
-                        bulk_g2s(dst + QTILE, p.kimg + (size_t(kt) * C + c) * QTILE, QTILE,
-                                 kfull(s));
-                        bulk_g2s(dst + 2 * QTILE, p.kbias + size_t(kt) * BIAS, BIAS, kfull(s));
+                    const int bb = vt & 1;
+                    mbar_wait(bempty(bb), ((vt >> 1) & 1) ^ 1);
+                    mbar_expect_tx(bfull(bb), BIAS);
+                    bulk_g2s(base + G_OFF_BIAS + bb * BIAS, p.kbias + size_t(kt) * BIAS, BIAS,
+                             bfull(bb));
+                    for (int c = 0; c < C; ++c) {
+                        const uint8_t* src[3] = {p.qimg + (size_t(qt) * C + c) * QTILE,
+                                                 p.kimg + (size_t(kt) * C + c) * QTILE,
+                                                 had ? p.aimg + (size_t(qt) * C + c) * QTILE
+                                                     : nullptr};
+                        for (int o = 0; o < ops; ++o, ++sq) {
+                            const int s = sq % NS;
+                            mbar_wait(sempty_(s), ((sq / NS) & 1) ^ 1);
+                            mbar_expect_tx(sfull_(s), QTILE);
+                            bulk_g2s(base + s * QTILE, src[o], QTILE, sfull_(s));
+                        }
                     }
                     mbar_wait(vempty, (vt & 1) ^ 1);
                     mbar_expect_tx(vfull, p.vc * QTILE);
-                    bulk_g2s(base + G_OFF_V,
+                    bulk_g2s(base + off_v,
                              p.vimg + (size_t(kt) * p.v_chunks + p.v_chunk0) * QTILE,
                              p.vc * QTILE, vfull);
                 }
@@ -991,7 +1031,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            int it = 0, vt = 0, lu = 0;
+            int sq = 0, vt = 0, lu = 0;
             for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++lu) {
                 const int split = item % p.splits;
                 const int kt0 = split * ktiles_per_split;
@@ -999,21 +1039,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
                 mbar_wait(oempty, (lu & 1) ^ 1);
                 fence_after();
                 for (int kt = kt0; kt < kt1; ++kt, ++vt) {
-                    for (int c = 0; c < C; ++c, ++it) {
-                        const int s = it % G_STAGES;
-                        mbar_wait(kfull(s), (it / G_STAGES) & 1);
+                    const int bb = vt & 1;
+                    mbar_wait(bfull(bb), (vt >> 1) & 1);
+                    for (int c = 0; c < C; ++c) {
+                        uint32_t addr[3];
+                        int slot[3];
+                        for (int o = 0; o < ops; ++o) {
+                            slot[o] = (sq + o) % NS;
+                            mbar_wait(sfull_(slot[o]), ((sq + o) / NS) & 1);
+                            addr[o] = base + slot[o] * QTILE;
+                        }
                         fence_after();
-                        const uint32_t st = base + s * G_STAGE;
-                        issue_score_chunk(tmem, tmem + TILE, st, st + QTILE, base + G_OFF_ONES,
-                                          st + 2 * QTILE, c == 0);
-                        umma_commit(kempty(s));
+                        issue_score_chunk(tmem, tmem + TILE, addr[0], addr[1], base + G_OFF_ONES,
+                                          base + G_OFF_BIAS + bb * BIAS, c == 0);
+                        if (had) issue_w_chunk(tmem + G_WCOL, addr[2], addr[1], c == 0);
+                        for (int o = 0; o < ops; ++o) umma_commit(sempty_(slot[o]));
+                        sq += ops;
                     }
+                    umma_commit(bempty(bb));
                     umma_commit(sfull);
                     mbar_wait(pready, vt & 1);
                     mbar_wait(vfull, vt & 1);
                     fence_after();
                     for (int j = 0; j < p.vc; ++j) {
-                        const uint32_t vst = base + G_OFF_V + j * QTILE;
+                        const uint32_t vst = base + off_v + j * QTILE;
                         const uint32_t o = tmem + G_OCOL + uint32_t(j * DPAD);
 #pragma unroll
                         for (int kk = 0; kk < TILE / 16; ++kk) {
@@ -1067,16 +1116,42 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
                         if (kbase + j >= p.key_valid) v[j] = __float_as_uint(-3.0e38f);
                 }
                 uint32_t hi[32], lo[32];
+                if (had) {
+                    // P~ (x) W: W read in two 32-column pieces to bound the registers
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const float p0 = ex2(fmaf(__uint_as_float(v[2 * j]), p.acc_scale, nlh) + c2);
-                    const float p1 =
-                        ex2(fmaf(__uint_as_float(v[2 * j + 1]), p.acc_scale, nlh) + c2);
-                    const __half2 h = __floats2half2_rn(p0, p1);
-                    const float2 hf = __half22float2(h);
-                    const __half2 l = __floats2half2_rn(p0 - hf.x, p1 - hf.y);
-                    hi[j] = *reinterpret_cast<const uint32_t*>(&h);
-                    lo[j] = *reinterpret_cast<const uint32_t*>(&l);
+                    for (int q = 0; q < 2; ++q) {
+                        uint32_t w[32];
+                        FSKB_TMEM_LD32(taddr + G_WCOL + 32 * q, w);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const int e = 32 * q + 2 * j;
+                            const float p0 =
+                                ex2(fmaf(__uint_as_float(v[e]), p.acc_scale, nlh) + c2) *
+                                (__uint_as_float(w[2 * j]) * p.w_mul);
+                            const float p1 =
+                                ex2(fmaf(__uint_as_float(v[e + 1]), p.acc_scale, nlh) + c2) *
+                                (__uint_as_float(w[2 * j + 1]) * p.w_mul);
+                            const __half2 h = __floats2half2_rn(p0, p1);
+                            const float2 hf = __half22float2(h);
+                            const __half2 l = __floats2half2_rn(p0 - hf.x, p1 - hf.y);
+                            hi[16 * q + j] = *reinterpret_cast<const uint32_t*>(&h);
+                            lo[16 * q + j] = *reinterpret_cast<const uint32_t*>(&l);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const float p0 =
+                            ex2(fmaf(__uint_as_float(v[2 * j]), p.acc_scale, nlh) + c2);
+                        const float p1 =
+                            ex2(fmaf(__uint_as_float(v[2 * j + 1]), p.acc_scale, nlh) + c2);
+                        const __half2 h = __floats2half2_rn(p0, p1);
+                        const float2 hf = __half22float2(h);
+                        const __half2 l = __floats2half2_rn(p0 - hf.x, p1 - hf.y);
+                        hi[j] = *reinterpret_cast<const uint32_t*>(&h);
+                        lo[j] = *reinterpret_cast<const uint32_t*>(&l);
+                    }
                 }
                 FSKB_TMEM_ST32(taddr, hi);
                 FSKB_TMEM_ST32(taddr + 32, lo);
@@ -1602,11 +1677,12 @@ void TcHalfStep::vec(DevProblem<float>& P, int side, const float* kpot, float ep
 
 void TcHalfStep::apply_mat(DevProblem<float>& P, int side, const float* kpot, float eps,
                            const float* l2h, const float* l2l, const float* marg, const float* V,
-                           int64_t p_cols, float* out, int* flags) {
+                           int64_t p_cols, float* out, int* flags, const float* A) {
     Impl& I = *impl_;
     const int qc = side == 0 ? 0 : 1, kc = side == 0 ? 1 : 0;
     const DevSide<float>& ks = side == 0 ? P.tgt : P.src;
-    const int64_t R = side == 0 ? P.src.n : P.tgt.n;
+    const DevSide<float>& qs = side == 0 ? P.src : P.tgt;
+    const int64_t R = qs.n;
     if (R == 0 || p_cols == 0) return;
     const int E = I.eq[qc] + I.ek[side];
     const int k_tiles = int(I.rows_pad[kc] / TILE);
@@ -1624,19 +1700,40 @@ void TcHalfStep::apply_mat(DevProblem<float>& P, int side, const float* kpot, fl
         V, ks.n, p_cols, std::ldexp(1.0f, -ev), I.rows_pad[kc], VC, vimg.get());
     FSKB_CUDA(cudaGetLastError());
     count_launch();
+    // Hadamard direction: query-layout split image of A (rows x d), 2^-ea scaled
+    DevBuf<uint8_t> aimg;
+    double out_scale = std::ldexp(1.0, ev - int(kPScaleLog2));
+    float w_mul = 0.0f;
+    if (A) {
+        const int ea = scale_exponent(double(device_absmax(A, R * qs.d, P.s)));
+        aimg.alloc(size_t(I.rows_pad[qc] / TILE) * I.chunks * QTILE, P.s);
+        const int64_t ag = I.rows_pad[qc] * 8 * I.chunks;
+        build_split_image<<<unsigned((ag + 255) / 256), 256, 0, P.s>>>(
+            A, R, qs.d, std::ldexp(1.0f, -ea), I.rows_pad[qc], I.chunks, aimg.get());
+        FSKB_CUDA(cudaGetLastError());
+        count_launch();
+        // acc_W = <a 2^-ea, c y 2^-ek> = W c 2^-(ea+ek); |W| <= ||a|| ||y|| <= 2^wexp
+        const double c = 2.0 * P.fscale / I.eps * 1.4426950408889634074;
+        const double wmax = double(device_rownorm_max(A, R, qs.d, P.s)) * double(I.rownorm[kc]);
+        const int wexp = wmax > 0.0 ? int(std::ceil(std::log2(wmax))) : 0;
+        w_mul = float(std::ldexp(1.0, ea + I.ek[side] - wexp) / c);
+        out_scale *= std::ldexp(1.0, wexp);
+    }
 
     TcApplyGenParams g{};
     g.qimg = I.qimg[qc].get();
     g.kimg = I.kimg[side].get();
     g.kbias = I.kbias[side].get();
     g.vimg = vimg.get();
+    g.aimg = A ? aimg.get() : nullptr;
+    g.w_mul = w_mul;
     g.chunks = I.chunks;
     g.v_chunks = VC;
     g.q_tile_begin = 0;
     g.q_tiles = int(I.rows_pad[qc] / TILE);
     g.k_tiles = k_tiles;
     const int sms = num_sms();
-    const double q_bytes = double(I.chunks) * QTILE;
+    const double q_bytes = double(I.chunks) * QTILE * (A ? 2 : 1);
     const int min_s = I.chunks > 1 ? int(std::ceil(sms * q_bytes / (48.0 * (1 << 20)))) : 1;
     g.splits = pick_splits(g.q_tiles, k_tiles, sms, min_s);
     g.items = g.q_tiles * g.splits;
@@ -1647,12 +1744,12 @@ void TcHalfStep::apply_mat(DevProblem<float>& P, int side, const float* kpot, fl
     g.acc_scale = std::ldexp(1.0f, E);
     g.l2h = l2h;
     g.l2l = l2l;
-    const double inv_v = std::ldexp(1.0, ev - int(kPScaleLog2));
-    DevBuf<float> part(size_t(g.splits) * size_t(R) * 2 * DPAD, P.s);
+    const int vc_max = A ? 1 : 2;
+    DevBuf<float> part(size_t(g.splits) * size_t(R) * vc_max * DPAD, P.s);
     g.part_o = part.get();
-    for (int v0 = 0; v0 < VC; v0 += 2) {
+    for (int v0 = 0; v0 < VC; v0 += vc_max) {
         g.v_chunk0 = v0;
-        g.vc = std::min(2, VC - v0);
+        g.vc = std::min(vc_max, VC - v0);
         tc_apply_gen_kernel<<<std::min(g.items, sms), NUM_THREADS, G_SMEM_BYTES, P.s>>>(g);
         FSKB_CUDA(cudaGetLastError());
         count_launch();
@@ -1660,7 +1757,7 @@ void TcHalfStep::apply_mat(DevProblem<float>& P, int side, const float* kpot, fl
         const int cols = int(std::min<int64_t>(width, p_cols - int64_t(v0) * DPAD));
         const int64_t total = R * cols;
         tc_apply_gen_finalize<<<unsigned((total + 255) / 256), 256, 0, P.s>>>(
-            part.get(), g.splits, R, width, cols, v0 * DPAD, p_cols, marg, inv_v, out, flags);
+            part.get(), g.splits, R, width, cols, v0 * DPAD, p_cols, marg, out_scale, out, flags);
         FSKB_CUDA(cudaGetLastError());
         count_launch();
     }

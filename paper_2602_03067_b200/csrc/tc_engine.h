@@ -59,9 +59,11 @@ public:
     // Transport-matrix application with fixed potentials: out (rows x p, float) =
     // P V (side 0) or P^T V (side 1) for a general V (key rows x p, float, device),
     // any d, via the tcgen05 general apply kernel (p in passes of 128 columns).
+    // With A (rows x d, device): the Hadamard form (P (.) A K^T) V where K is the
+    // key cloud (apply_hadamard_plan with B = the key cloud, as in the HVP).
     void apply_mat(DevProblem<float>& P, int side, const float* kpot, float eps, const float* l2h,
                    const float* l2l, const float* marg, const float* V, int64_t p_cols,
-                   float* out, int* flags);
+                   float* out, int* flags, const float* A = nullptr);
 
 private:
     void poll_screen(int side);

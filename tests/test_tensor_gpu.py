@@ -365,3 +365,49 @@ def test_tensor_transport_matrix_parity(fsk, port, n, m, d, p, side):
     print(f"transport-matrix side {side} d={d} p={p}: max rel err {err:.2e} (ref-fp32 {e32:.2e})")
     assert err <= max(1e-5, 2.0 * e32)
     eng.close()
+
+
+@pytest.mark.parametrize("n,m,d,p", [(700, 513, 64, 64), (300, 421, 100, 130), (260, 300, 1024, 70)])
+def test_tensor_transport_hadamard_parity(fsk, port, n, m, d, p):
+    """Hadamard mode of the general tensor apply: (P (.) A Y^T) V against the fp64
+    apply_hadamard_plan (stream.cpp:359-375, B = Y), marginal-scaled contract."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(5 * n + m + d + p)
+    X = rng.normal(size=(n, d)) * 0.4
+    Y = rng.normal(size=(m, d)) * 0.4 + 0.1
+    a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+    eps = 0.5 if d < 512 else 2.0
+    eng = fsk.Engine(0, X, a, Y, b, mode="tensor")
+    eng.set_eps(eps)
+    f = torch.empty(n, dtype=torch.float32, device="cuda")
+    g = torch.empty(m, dtype=torch.float32, device="cuda")
+    eng.bind(f.data_ptr(), g.data_ptr())
+    eng.init_potentials()
+    for _ in range(4):
+        eng.half_step(0, 0, n)
+        eng.half_step(1, 0, m)
+    A = rng.normal(size=(n, d))
+    V = rng.normal(size=(m, p))
+    Ad = torch.tensor(A, dtype=torch.float32, device="cuda")
+    Vd = torch.tensor(V, dtype=torch.float32, device="cuda")
+    out = torch.empty((n, p), dtype=torch.float32, device="cuda")
+    eng.transport_hadamard(Ad.data_ptr(), Vd.data_ptr(), p, out.data_ptr())
+    torch.cuda.synchronize()
+    fh = f.cpu().numpy().astype(np.float64)
+    gh = g.cpu().numpy().astype(np.float64)
+    A32 = A.astype(np.float32).astype(np.float64)
+    V32 = V.astype(np.float32).astype(np.float64)
+    Y32 = Y.astype(np.float32).astype(np.float64)
+    want = port.apply_hadamard_plan(X, a, Y, b, fh, gh, eps, A32, Y32, V32)
+    # scale: the same plan with |W| |V| (no cancellation charged to the kernel)
+    Wabs = np.abs(A32 @ Y32.T)
+    r64, _ = port.induced_marginals(X, a, Y, b, fh, gh, eps)
+    P = port.apply_plan(X, a, Y, b, fh, gh, eps, np.eye(m)) if m <= 600 else None
+    scale = (P * Wabs) @ np.abs(V32)
+    err = (np.abs(out.cpu().numpy() - want) / scale).max()
+    p32 = port.update_f_hat_f32(X, a, Y, b, gh, eps).astype(np.float64)
+    m32 = a * np.exp((fh - p32) / eps) / r64
+    e32 = (np.abs(want * (m32 - 1.0)[:, None]) / scale).max()
+    print(f"hadamard d={d} p={p}: max rel err {err:.2e} (ref-fp32 {e32:.2e})")
+    assert err <= max(1e-5, 2.0 * e32)
+    eng.close()
