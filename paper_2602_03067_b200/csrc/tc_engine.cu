@@ -85,6 +85,8 @@ struct TcParams {
     // the running approximate row max - screen_thr for every row are not scored
     float screen_thr;
     unsigned long long* live_count;  // += live key tiles (diagnostics), nullable
+    uint32_t* live_global;       // screened: per item, the phase-1 bitmask (kwords words)
+    int kwords;
 };
 
 // Per-tile epilogue math shared by the K1 kernels: mask the padded keys of the
@@ -538,24 +540,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                         mbar_wait(accfull(t), acc_n & 1);
                         fence_after();
                         const int64_t kbase = int64_t(kt) * TILE;
-#pragma unroll 1
-                        for (int q = 0; q < 4; ++q) {
-                            uint32_t v[32];
-                            FSKB_TMEM_LD32(acc_addr + 32 * q, v);
-                            tmem_ld_wait();
-                            if (kbase + 32 * q + 32 > p.key_valid) {
+                        // all four 32-column loads in flight before one wait
+                        uint32_t v[128];
+                        FSKB_TMEM_LD32(acc_addr + 0, (v + 0));
+                        FSKB_TMEM_LD32(acc_addr + 32, (v + 32));
+                        FSKB_TMEM_LD32(acc_addr + 64, (v + 64));
+                        FSKB_TMEM_LD32(acc_addr + 96, (v + 96));
+                        tmem_ld_wait();
+                        if (kbase + TILE > p.key_valid) {
 #pragma unroll
-                                for (int j = 0; j < 32; ++j)
-                                    if (kbase + 32 * q + j >= p.key_valid)
-                                        v[j] = __float_as_uint(-INFINITY);
-                            }
+                            for (int j = 0; j < 128; ++j)
+                                if (kbase + j >= p.key_valid) v[j] = __float_as_uint(-INFINITY);
+                        }
 #pragma unroll
-                            for (int j = 0; j < 32; j += 4) {
-                                mx0 = fmaxf(mx0, __uint_as_float(v[j]));
-                                mx1 = fmaxf(mx1, __uint_as_float(v[j + 1]));
-                                mx2 = fmaxf(mx2, __uint_as_float(v[j + 2]));
-                                mx3 = fmaxf(mx3, __uint_as_float(v[j + 3]));
-                            }
+                        for (int j = 0; j < 128; j += 4) {
+                            mx0 = fmaxf(mx0, __uint_as_float(v[j]));
+                            mx1 = fmaxf(mx1, __uint_as_float(v[j + 1]));
+                            mx2 = fmaxf(mx2, __uint_as_float(v[j + 2]));
+                            mx3 = fmaxf(mx3, __uint_as_float(v[j + 3]));
                         }
                         fence_before();
                         __syncwarp();
@@ -572,6 +574,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 __syncwarp();
                 if (lane == 0) mbar_arrive(screen_done);
                 mbar_wait(screen_done, lu & 1);
+                // publish the live set for the gradient's transport pass (K3)
+                if (p.live_global)
+                    for (int w = threadIdx.x - 64; w < p.kwords; w += 256)
+                        p.live_global[size_t(item) * p.kwords + w] = live_bits[w];
             }
             for (int kt = SCREEN ? next_live(kt0, kt0, kt1) : kt0; kt < kt1;
                  kt = SCREEN ? next_live(kt + 1, kt0, kt1) : kt + 1) {
@@ -651,7 +657,33 @@ struct TcApplyParams {
     const float* l2h;   // [R] log2-domain row LSE, hi
     const float* l2l;   // [R] lo
     float* part_o;      // [splits][R][64] partial O (V units x 2^12)
+    // live key tiles from the screened LSE pass over the same rows and potentials
+    // (nullable): query tile u uses the bitmask of the pass's work item
+    // (u / 2) * lse_splits + kt / lse_kps, bit kt % lse_kps
+    const uint32_t* live_global;
+    int lse_splits, lse_kps, lse_kwords;
 };
+
+// next key tile >= kt (< kt1) the screened LSE pass marked live for query tile u
+__device__ __forceinline__ int apply_next_live(const TcApplyParams& p, int u, int kt, int kt1) {
+    if (!p.live_global) return kt;
+    while (kt < kt1) {
+        const int ls = kt / p.lse_kps, rel = kt - ls * p.lse_kps;
+        const uint32_t w = __ldg(p.live_global + (size_t(u >> 1) * p.lse_splits + ls) * p.lse_kwords +
+                                 (rel >> 5)) >> (rel & 31);
+        if (w) return kt + __ffs(w) - 1;
+        kt += 32 - (rel & 31);
+        if (rel + 32 - (rel & 31) > p.lse_kps) kt = (ls + 1) * p.lse_kps;
+    }
+    return kt1;
+}
+__device__ __forceinline__ int apply_count_live(const TcApplyParams& p, int u, int kt0, int kt1) {
+    if (!p.live_global) return max(0, kt1 - kt0);
+    int n = 0;
+    for (int kt = apply_next_live(p, u, kt0, kt1); kt < kt1; kt = apply_next_live(p, u, kt + 1, kt1))
+        ++n;
+    return n;
+}
 
 __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_kernel(const TcApplyParams p) {
     extern __shared__ uint8_t smem_raw[];
@@ -716,7 +748,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_kernel(const TcApplyP
                 bulk_g2s(base + A_OFF_Q, p.qimg + size_t(qt) * QTILE, QTILE, qfull);
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
-                for (int kt = kt0; kt < kt1; ++kt, ++it) {
+                for (int kt = apply_next_live(p, unit, kt0, kt1); kt < kt1;
+                     kt = apply_next_live(p, unit, kt + 1, kt1), ++it) {
                     const int s = it % ASTAGES;
                     const uint32_t ph = (it / ASTAGES) & 1;
                     mbar_wait(kempty(s), ph ^ 1);
@@ -731,10 +764,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_kernel(const TcApplyP
         if (lane == 0) {
             int it0 = 0, sq0 = 0, lu = 0;
             for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++lu) {
-                const int split = item % p.splits;
+                const int unit = item / p.splits, split = item % p.splits;
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
-                const int K = max(0, kt1 - kt0);
+                const int K = apply_count_live(p, unit, kt0, kt1);
                 const int ob = lu & 1;
                 mbar_wait(qfull, lu & 1);
                 fence_after();
@@ -804,7 +837,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_kernel(const TcApplyP
             // P~ = 2^(acc 2^E - L + 12): nlh folds L_hi, c2 = 12 - L_lo
             const float nlh = live ? -p.l2h[row] : -3.0e38f;
             const float c2 = live ? kPScaleLog2 - p.l2l[row] : 0.0f;
-            for (int kt = kt0; kt < kt1; ++kt, ++sq) {
+            const int K = apply_count_live(p, unit, kt0, kt1);
+            for (int kt = apply_next_live(p, unit, kt0, kt1); kt < kt1;
+                 kt = apply_next_live(p, unit, kt + 1, kt1), ++sq) {
                 const int buf = sq % NSBUF;
                 mbar_wait(sfull(buf), (sq / NSBUF) & 1);
                 fence_after();
@@ -863,6 +898,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_kernel(const TcApplyP
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(oempty(ob));
+            if (K == 0) {  // no live key tile in this split range: O = 0
+#pragma unroll
+                for (int c = 0; c < 32; ++c) o[c] = 0u;
+            }
             if (row >= p.row_begin && row < p.row_end) {
                 float4* dst = reinterpret_cast<float4*>(
                     p.part_o + (size_t(split) * p.R + row) * DPAD + half * 32);
@@ -1434,6 +1473,11 @@ struct TcHalfStep::Impl {
     double live_est[2] = {0.0, 0.0};         // 0 -> screen the first pass (probe)
     int skip_left[2] = {0, 0}, backoff[2] = {8, 8};
     unsigned long long live_total = 0, screened_blocks = 0;
+    // live set of the last LSE pass per side (valid when that pass was screened)
+    DevBuf<uint32_t> live_glob[2];
+    bool live_valid[2] = {false, false};
+    int live_splits[2] = {1, 1}, live_kps[2] = {1, 1}, live_kwords[2] = {1, 1};
+    int64_t live_row_begin[2] = {0, 0}, live_row_end[2] = {0, 0};
     ~Impl() {
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
@@ -1619,7 +1663,17 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         p.live_count = I.live_count.get() + side;
         if (!I.pending[side])
             FSKB_CUDA(cudaMemsetAsync(p.live_count, 0, sizeof(unsigned long long), P.s));
+        p.kwords = (kps + 31) / 32;
+        const size_t words = size_t(p.items) * size_t(p.kwords);
+        if (I.live_glob[side].size() < words) I.live_glob[side].alloc(words, P.s);
+        p.live_global = I.live_glob[side].get();
+        I.live_splits[side] = p.splits;
+        I.live_kps[side] = kps;
+        I.live_kwords[side] = p.kwords;
+        I.live_row_begin[side] = row_begin;
+        I.live_row_end[side] = row_end;
     }
+    if (!vec) I.live_valid[side] = screen;
     if (I.chunks == 1) {
         if (vec)
             tc_lse_tq_kernel<true, false><<<grid, NUM_THREADS, TQ_SMEM_BYTES, P.s>>>(p);
@@ -1803,6 +1857,14 @@ void TcHalfStep::grad(DevProblem<float>& P, int side, const float* kpot, const f
     p.acc_scale = std::ldexp(1.0f, I.eq[qc] + I.ek[side]);
     p.l2h = l2h.get();
     p.l2l = l2l.get();
+    if (I.live_valid[side] && I.live_row_begin[side] == row_begin &&
+        I.live_row_end[side] == row_end) {
+        // the LSE pass above was screened: stream only its live key tiles
+        p.live_global = I.live_glob[side].get();
+        p.lse_splits = I.live_splits[side];
+        p.lse_kps = I.live_kps[side];
+        p.lse_kwords = I.live_kwords[side];
+    }
     DevBuf<float> part(size_t(p.splits) * size_t(R) * DPAD, P.s);
     p.part_o = part.get();
     tc_apply_kernel<<<std::min(p.items, sms), NUM_THREADS, A_SMEM_BYTES, P.s>>>(p);

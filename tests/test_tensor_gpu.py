@@ -307,11 +307,16 @@ def test_screened_lse_matches_unscreened(fsk):
         for _ in range(3):
             eng.half_step(0, 0, n)
             eng.half_step(1, 0, m)
+        # gradient: with screening its K3 pass streams only the LSE pass's live tiles
+        G = torch.empty((n, d), dtype=torch.float32, device="cuda")
+        eng.grad(0, n, G.data_ptr())
         torch.cuda.synchronize()
-        out[flag] = (f.cpu().numpy(), g.cpu().numpy(), eng.live_tiles(), eng.screened_blocks())
+        out[flag] = (f.cpu().numpy(), g.cpu().numpy(), eng.live_tiles(), eng.screened_blocks(),
+                     G.cpu().numpy())
         eng.close()
-    fs, gs, live, blocks = out["1"]
-    fu, gu, live_u, blocks_u = out["0"]
+    fs, gs, live, blocks, Gs = out["1"]
+    fu, gu, live_u, blocks_u, Gu = out["0"]
+    assert np.abs(Gs - Gu).max() <= 1e-5 * np.abs(Gu).max()
     assert blocks_u == 0 and blocks > 0
     print(f"screen live fraction {live / blocks:.3f}")
     assert live < blocks
