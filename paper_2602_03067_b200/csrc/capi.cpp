@@ -1,3 +1,6 @@
+#include <thread>
+#include <chrono>
+#include <cstdio>
 // C ABI (include/fsk_b200.h): validation with the reference's messages, IO
 // ledger accounting at the caller's TileConfig, host<->device staging, and the
 // device-resident solver loop. Every numeric result comes from the CUDA kernels.
@@ -50,13 +53,30 @@ int tensor_mode_from_env() {
 
 namespace {
 
+// |x_i|^2 (core.cpp:83-96 squared_norms; same per-row summation order), rows
+// split across host threads for the large clouds.
 std::vector<double> host_sqnorm(const fsk_measure& m, double scale) {
     std::vector<double> out((size_t)(m.n));
-    for (int64_t i = 0; i < m.n; ++i) {
-        double s = 0.0;
-        for (int64_t t = 0; t < m.d; ++t) s += m.points[i * m.d + t] * m.points[i * m.d + t];
-        out[size_t(i)] = scale != 1.0 ? s * scale : s;
+    auto rows = [&](int64_t i0, int64_t i1) {
+        for (int64_t i = i0; i < i1; ++i) {
+            double s = 0.0;
+            for (int64_t t = 0; t < m.d; ++t) s += m.points[i * m.d + t] * m.points[i * m.d + t];
+            out[size_t(i)] = scale != 1.0 ? s * scale : s;
+        }
+    };
+    const int64_t work = m.n * m.d;
+    const int nt = work < (int64_t(1) << 22)
+                       ? 1
+                       : int(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+    if (nt == 1) {
+        rows(0, m.n);
+        return out;
     }
+    std::vector<std::thread> th;
+    const int64_t per = (m.n + nt - 1) / nt;
+    for (int k = 0; k < nt; ++k)
+        th.emplace_back(rows, std::min(m.n, k * per), std::min(m.n, (k + 1) * per));
+    for (auto& t : th) t.join();
     return out;
 }
 
@@ -80,10 +100,11 @@ void dev_to(const DevBuf<T>& b, double* h, int64_t n, cudaStream_t s) {
         b.download(h, size_t(n));
         FSKB_CUDA(cudaStreamSynchronize(s));
     } else {
-        std::vector<T> tmp((size_t)(n));
-        b.download(tmp.data(), size_t(n));
+        // widen on the device, then one copy straight into the caller's buffer
+        DevBuf<double> wide(size_t(n), s);
+        launch_f32_to_f64(b.get(), wide.get(), n, s);
+        wide.download(h, size_t(n));
         FSKB_CUDA(cudaStreamSynchronize(s));
-        for (int64_t i = 0; i < n; ++i) h[i] = double(tmp[size_t(i)]);
     }
 }
 
@@ -108,7 +129,7 @@ void common_checks(const fsk_measure* src, const fsk_measure* tgt, const fsk_cos
 // r (n) and c (m) of the induced marginals at (f, g), all on device.
 template <typename T>
 void dev_marginals(DevProblem<T>& P, const T* f, const T* g, T eps, T* r, T* c, T* lse_f,
-                   T* mx_f, int* flags) {
+                   T* mx_f, int* flags, float* l2h_f = nullptr, float* l2l_f = nullptr) {
     FinalizeArgs<T> fa{};
     fa.eps = eps;
     fa.flags = flags;
@@ -118,6 +139,8 @@ void dev_marginals(DevProblem<T>& P, const T* f, const T* g, T eps, T* r, T* c, 
     fa.marg_flag = kFlagNonFiniteRowMarginal;
     fa.out_lse = lse_f;
     fa.out_max = mx_f;
+    fa.out_l2h = l2h_f;
+    fa.out_l2l = l2l_f;
     half_step<T>(P, 0, g, eps, fa);
     FinalizeArgs<T> fb{};
     fb.eps = eps;
@@ -152,19 +175,43 @@ double dual_value(const fsk_measure& a, const fsk_measure& b, const double* fh, 
 }
 
 template <typename T>
+// r_keep / l2 keeps (tensor path): the f-side pass's marginal and log2 LSE, so the
+// gradient at the same potentials does not repeat that pass.
 HostMarginals marginals_to_host(DevProblem<T>& P, const T* f, const T* g, T eps, ExecCtx& C,
-                                DevBuf<T>* lse_keep = nullptr, DevBuf<T>* mx_keep = nullptr) {
+                                DevBuf<T>* lse_keep = nullptr, DevBuf<T>* mx_keep = nullptr,
+                                DevBuf<T>* r_keep = nullptr, DevBuf<float>* l2h_keep = nullptr,
+                                DevBuf<float>* l2l_keep = nullptr) {
     const int64_t n = P.src.n, m = P.tgt.n;
     DevBuf<T> r(size_t(n), C.s), c(size_t(m), C.s);
     dev_marginals<T>(P, f, g, eps, r.get(), c.get(), lse_keep ? lse_keep->get() : nullptr,
-                     mx_keep ? mx_keep->get() : nullptr, C.flags);
+                     mx_keep ? mx_keep->get() : nullptr, C.flags,
+                     l2h_keep ? l2h_keep->get() : nullptr, l2l_keep ? l2l_keep->get() : nullptr);
     HostMarginals hm;
     hm.r.resize(size_t(n));
     hm.c.resize(size_t(m));
     dev_to<T>(r, hm.r.data(), n, C.s);
     dev_to<T>(c, hm.c.data(), m, C.s);
+    if (r_keep) *r_keep = std::move(r);
     return hm;
 }
+
+// FSK_TIMING=1: host wall-clock per solve phase on stderr (synchronizes the stream).
+struct PhaseTimer {
+    bool on;
+    cudaStream_t s;
+    std::chrono::steady_clock::time_point t0;
+    explicit PhaseTimer(cudaStream_t st) : on(std::getenv("FSK_TIMING") != nullptr), s(st) {
+        t0 = std::chrono::steady_clock::now();
+    }
+    void mark(const char* what) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const auto t1 = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[fsk timing] %-24s %9.3f ms\n", what,
+                     std::chrono::duration<double, std::milli>(t1 - t0).count());
+        t0 = t1;
+    }
+};
 
 // Device-resident Sinkhorn (solver.cpp:21-117). T = double: Precision::Double;
 // T = float: Precision::Single (tensor-core or FMA half-steps).
@@ -175,9 +222,12 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
     constexpr bool kSingle = std::is_same_v<T, float>;
     const int64_t n = src.n, m = tgt.n, d = src.d;
     auto& C = exec_ctx();
+    PhaseTimer timer(C.s);
     DevProblem<T> P;
     P.upload(src, tgt, cost, C.s);
+    timer.mark("upload");
     if constexpr (kSingle) enable_tensor_path(P, tensor_mode_from_env());
+    timer.mark("operand images");
 
     const double fs = feature_scale(cost);
     const std::vector<double> alpha = host_sqnorm(src, fs), beta = host_sqnorm(tgt, fs);
@@ -191,8 +241,12 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
         g2.alloc(size_t(m), C.s);
     }
 
-    const auto schedule =
-        eps_schedule_raw(cfg, joint_sq_diameter_raw(src.points, n, tgt.points, m, d));
+    timer.mark("initial potentials");
+    // the squared diameter only feeds the geometric eps decay (schedule.cpp:27-44)
+    const double diam2 =
+        cfg.eps_scaling_factor < 1.0 ? joint_sq_diameter_raw(src.points, n, tgt.points, m, d) : 0.0;
+    const auto schedule = eps_schedule_raw(cfg, diam2);
+    timer.mark("eps schedule");
     int iters = 0;
     double viol = 0.0, dual = 0.0, final_eps = 0.0;
     bool stopped = false;
@@ -264,6 +318,7 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
             }
         }
     }
+    timer.mark("iterations");
     {
         const int bad = bad_iteration(C);
         const int fl = read_and_clear_flags(C);
@@ -274,11 +329,21 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
     dev_to<T>(f, fh.data(), n, C.s);
     dev_to<T>(g, gh.data(), m, C.s);
     DevBuf<T> lse_f(size_t(n), C.s), mx_f(size_t(n), C.s);
+    DevBuf<T> r_keep;
+    DevBuf<float> l2h_keep, l2l_keep;
     if (!stopped) {
         if constexpr (kSingle) {
             if (P.tc && cur_tc_eps != pot_eps) P.tc->set_eps(P, pot_eps);
         }
-        HostMarginals hm = marginals_to_host<T>(P, f.get(), g.get(), T(pot_eps), C, &lse_f, &mx_f);
+        const bool keep = kSingle && P.tc && P.tc->chunks() == 1 && grad_out;
+        if (keep) {
+            l2h_keep.alloc(size_t(n), C.s);
+            l2l_keep.alloc(size_t(n), C.s);
+        }
+        HostMarginals hm = marginals_to_host<T>(P, f.get(), g.get(), T(pot_eps), C, &lse_f, &mx_f,
+                                                keep ? &r_keep : nullptr,
+                                                keep ? &l2h_keep : nullptr,
+                                                keep ? &l2l_keep : nullptr);
         sync_and_check(C);
         ledger_marginals(ledger, n, m, d, tiles, cost);
         viol = violation(hm, src, tgt);
@@ -296,6 +361,7 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
             for (int64_t k = 0; k < rep->eps_history_cap && k < int64_t(hist.size()); ++k)
                 rep->eps_history[k] = hist[size_t(k)];
     }
+    timer.mark("marginals + dual");
     if (grad_out) {
         // grad_X = 2 r (X - softmax(S) Y) at the returned potentials
         const T eps = T(pot_eps);
@@ -304,8 +370,10 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
         if constexpr (kSingle) {
             if (P.tc && P.tc->chunks() == 1) {
                 // fused tcgen05 path: K1 row LSE + split-fp16 transport kernel
-                P.tc->set_eps(P, pot_eps);
-                P.tc->grad(P, 0, g.get(), f.get(), eps, 0, n, G.get(), C.flags);
+                if (!r_keep.get()) P.tc->set_eps(P, pot_eps);
+                if constexpr (kSingle)
+                    P.tc->grad(P, 0, g.get(), f.get(), eps, 0, n, G.get(), C.flags, l2h_keep.get(),
+                               l2l_keep.get(), r_keep.get());
                 done = true;
             }
         }
@@ -325,6 +393,7 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
                                     lse_f.get(), n, d, eps, G.get(), C.flags, C.s);
         }
         dev_to<T>(G, grad_out, n * d, C.s);
+        timer.mark("gradient + download");
         sync_and_check(C);
         if (ledger) {
             ledger_marginals(ledger, n, m, d, tiles, cost);

@@ -83,13 +83,14 @@ void upload_side(DevSide<T>& side, const fsk_measure& m, bool want_labels, cudaS
         side.pts.upload(m.points, size_t(m.n * m.d));
         side.w.upload(m.weights, size_t(m.n));
     } else {
-        std::vector<T> tmp((size_t)(m.n * m.d));
-        for (size_t i = 0; i < tmp.size(); ++i) tmp[i] = T(m.points[i]);
-        side.pts.upload(tmp.data(), tmp.size());
-        std::vector<T> w((size_t)(m.n));
-        for (size_t i = 0; i < w.size(); ++i) w[i] = T(m.weights[i]);
-        side.w.upload(w.data(), w.size());
-        FSKB_CUDA(cudaStreamSynchronize(s));  // tmp buffers leave scope
+        // ship the caller's doubles as they are and narrow on the device (no host
+        // conversion pass over n x d values)
+        DevBuf<double> tmp(size_t(m.n * m.d), s), wtmp(size_t(m.n), s);
+        tmp.upload(m.points, size_t(m.n * m.d));
+        wtmp.upload(m.weights, size_t(m.n));
+        launch_f64_to_f32(tmp.get(), side.pts.get(), m.n * m.d, s);
+        launch_f64_to_f32(wtmp.get(), side.w.get(), m.n, s);
+        FSKB_CUDA(cudaStreamSynchronize(s));
     }
     launch_log<T>(side.w.get(), side.logw.get(), m.n, s);
     if (want_labels && m.labels) {

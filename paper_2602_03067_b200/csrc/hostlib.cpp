@@ -184,22 +184,23 @@ void ledger_update_f32(fsk_ledger* l, int64_t R, int64_t C, int64_t d, int64_t b
 
 // ---- schedule -----------------------------------------------------------------
 
+// schedule.cpp:8-25, one row-major pass (min / max are order-independent, so the
+// result is identical to the reference's per-column scans)
 double joint_sq_diameter_raw(const double* X, int64_t n, const double* Y, int64_t m, int64_t d) {
+    std::vector<double> lo(size_t(d), std::numeric_limits<double>::infinity());
+    std::vector<double> hi(size_t(d), -std::numeric_limits<double>::infinity());
+    auto scan = [&](const double* P, int64_t rows) {
+        for (int64_t i = 0; i < rows; ++i)
+            for (int64_t t = 0; t < d; ++t) {
+                const double v = P[i * d + t];
+                lo[size_t(t)] = v < lo[size_t(t)] ? v : lo[size_t(t)];
+                hi[size_t(t)] = hi[size_t(t)] < v ? v : hi[size_t(t)];
+            }
+    };
+    scan(X, n);
+    scan(Y, m);
     double diam2 = 0.0;
-    for (int64_t t = 0; t < d; ++t) {
-        double lo = std::numeric_limits<double>::infinity(), hi = -lo;
-        for (int64_t i = 0; i < n; ++i) {
-            const double v = X[i * d + t];
-            lo = v < lo ? v : lo;
-            hi = hi < v ? v : hi;
-        }
-        for (int64_t j = 0; j < m; ++j) {
-            const double v = Y[j * d + t];
-            lo = v < lo ? v : lo;
-            hi = hi < v ? v : hi;
-        }
-        diam2 += (hi - lo) * (hi - lo);
-    }
+    for (int64_t t = 0; t < d; ++t) diam2 += (hi[size_t(t)] - lo[size_t(t)]) * (hi[size_t(t)] - lo[size_t(t)]);
     return diam2;
 }
 

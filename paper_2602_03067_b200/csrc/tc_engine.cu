@@ -1818,7 +1818,8 @@ void TcHalfStep::apply_mat(DevProblem<float>& P, int side, const float* kpot, fl
 }
 
 void TcHalfStep::grad(DevProblem<float>& P, int side, const float* kpot, const float* pot,
-                      float eps, int64_t row_begin, int64_t row_end, float* G, int* flags) {
+                      float eps, int64_t row_begin, int64_t row_end, float* G, int* flags,
+                      const float* pre_l2h, const float* pre_l2l, const float* pre_r) {
     if (row_end <= row_begin) return;
     Impl& I = *impl_;
     if (I.chunks != 1) throw ValidationFailure("fused tcgen05 gradient needs d <= 64");
@@ -1828,17 +1829,26 @@ void TcHalfStep::grad(DevProblem<float>& P, int side, const float* kpot, const f
     const int64_t R = qs.n, d = qs.d;
     // pass 1 (K1): row LSE in log2 units (hi/lo) and the induced marginal
     // r_i = w_i exp((pot_i - pot+_i) / eps) at the current potentials
-    DevBuf<float> l2h(size_t(R), P.s), l2l(size_t(R), P.s), r(size_t(R), P.s);
-    FinalizeArgs<float> fa{};
-    fa.eps = eps;
-    fa.flags = flags;
-    fa.old_pot = pot;
-    fa.w = qs.w.get();
-    fa.out_marg = r.get();
-    fa.marg_flag = side == 0 ? kFlagNonFiniteRowMarginal : kFlagNonFiniteColMarginal;
-    fa.out_l2h = l2h.get();
-    fa.out_l2l = l2l.get();
-    run(P, side, kpot, eps, fa, row_begin, row_end);
+    DevBuf<float> l2h, l2l, r;
+    const float *L2h = pre_l2h, *L2l = pre_l2l, *Rm = pre_r;
+    if (!(pre_l2h && pre_l2l && pre_r)) {
+        l2h.alloc(size_t(R), P.s);
+        l2l.alloc(size_t(R), P.s);
+        r.alloc(size_t(R), P.s);
+        FinalizeArgs<float> fa{};
+        fa.eps = eps;
+        fa.flags = flags;
+        fa.old_pot = pot;
+        fa.w = qs.w.get();
+        fa.out_marg = r.get();
+        fa.marg_flag = side == 0 ? kFlagNonFiniteRowMarginal : kFlagNonFiniteColMarginal;
+        fa.out_l2h = l2h.get();
+        fa.out_l2l = l2l.get();
+        run(P, side, kpot, eps, fa, row_begin, row_end);
+        L2h = l2h.get();
+        L2l = l2l.get();
+        Rm = r.get();
+    }
     // pass 2 (K3): O = softmax(S) V with V = the key tiles themselves
     TcApplyParams p{};
     p.qimg = I.qimg[qc].get();
@@ -1855,8 +1865,8 @@ void TcHalfStep::grad(DevProblem<float>& P, int side, const float* kpot, const f
     p.key_valid = ks.n;
     p.R = R;
     p.acc_scale = std::ldexp(1.0f, I.eq[qc] + I.ek[side]);
-    p.l2h = l2h.get();
-    p.l2l = l2l.get();
+    p.l2h = L2h;
+    p.l2l = L2l;
     if (I.live_valid[side] && I.live_row_begin[side] == row_begin &&
         I.live_row_end[side] == row_end) {
         // the LSE pass above was screened: stream only its live key tiles
@@ -1875,7 +1885,7 @@ void TcHalfStep::grad(DevProblem<float>& P, int side, const float* kpot, const f
     const double inv_v = std::ldexp(1.0, I.ek[side] - int(kPScaleLog2)) / c;
     const int64_t total = (row_end - row_begin) * d;
     tc_grad_finalize_kernel<<<unsigned((total + 255) / 256), 256, 0, P.s>>>(
-        part.get(), p.splits, R, row_begin, row_end, d, qs.pts.get(), r.get(), inv_v, G, flags);
+        part.get(), p.splits, R, row_begin, row_end, d, qs.pts.get(), Rm, inv_v, G, flags);
     FSKB_CUDA(cudaGetLastError());
     count_launch();
 }

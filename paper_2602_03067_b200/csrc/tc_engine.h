@@ -45,8 +45,12 @@ public:
     // rows [row_begin, row_end): G_i = 2 r_i (x_i - (softmax_j S_ij) y_j) with
     // r_i = w_i exp((pot_i - pot+_i)/eps). Two passes: K1 for
     // the row LSE, then the fused tcgen05 transport kernel. G is (end-begin) x d.
+    // pre_*: the row log2 LSE (hi, lo) and marginal of a pass over the same rows
+    // at the same potentials (e.g. the solver's final marginals) - skips pass 1.
     void grad(DevProblem<float>& P, int side, const float* kpot, const float* pot, float eps,
-              int64_t row_begin, int64_t row_end, float* G, int* flags);
+              int64_t row_begin, int64_t row_end, float* G, int* flags,
+              const float* pre_l2h = nullptr, const float* pre_l2l = nullptr,
+              const float* pre_r = nullptr);
 
     // Transport-vector application with fixed potentials: out_i = marg_i sum_j
     // 2^(t_ij - L_i) v_j = (P v)_i (side 0) or (P^T v)_j (side 1), given the row
