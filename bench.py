@@ -190,7 +190,7 @@ def reference_sample(cfgname, threads=None):
     if tail == "grad":
         a64 = np.full(rows, 1.0 / rows)
         t0 = time.perf_counter()
-        ref.update_f_hat(X64[:rows], a64, Y64, np.full(m, 1.0 / m), g0, eps)
+        ref.update_f_hat(X64[:rows], a64, Y64, uniform_weights(m), g0, eps)
         t_lse64 = time.perf_counter() - t0
         Ysub = Y64[:cols_apply]
         bsub = np.full(cols_apply, 1.0 / cols_apply)
@@ -207,7 +207,7 @@ def reference_sample(cfgname, threads=None):
         # apply_plan (stream.cpp:324-339, f64); time one vector apply on the row
         # slice and one matrix apply (p = d) on rows x 4096 columns
         a64 = np.full(rows, 1.0 / rows)
-        bm = np.full(m, 1.0 / m)
+        bm = uniform_weights(m)
         fr = ref.update_f_hat(X64[:rows], a64, Y64, bm, g0, eps)
         v = np.ones((m, 1))
         t0 = time.perf_counter()
@@ -400,12 +400,19 @@ def run_b200(args, cfgname):
             want_grad = STEP_TAIL[cfgname] == "grad"
             out = fsk.sinkhorn_solve(X, a, Y, b, eps=eps, max_iters=iters, precision="single",
                                      grad=want_grad)
+            if STEP_TAIL[cfgname] == "hvp":
+                hv, _ = fsk.hvp_apply(X, a, Y, b, out["f_hat"], out["g_hat"], eps, hvp_dir,
+                                      tau=1e-5, cg_tol=1e-30, cg_max_iters=HVP_CG_ITERS,
+                                      precision="single")
             e2e_s = time.perf_counter() - t0
             e2e = {"value": iters / e2e_s, "unit": "iterations/s",
-                   "h2d_bytes_per_step": int(X.nbytes + Y.nbytes + a.nbytes + b.nbytes),
+                   "h2d_bytes_per_step": int(X.nbytes + Y.nbytes + a.nbytes + b.nbytes) *
+                   (2 if STEP_TAIL[cfgname] == "hvp" else 1),
                    "d2h_bytes_per_step": int((out["grad"].nbytes if want_grad else 0) +
-                                             out["f_hat"].nbytes + out["g_hat"].nbytes),
-                   "api": "fsk_sinkhorn_solve_grad (C ABI, host double buffers)",
+                                             out["f_hat"].nbytes + out["g_hat"].nbytes +
+                                             (hv.nbytes if STEP_TAIL[cfgname] == "hvp" else 0)),
+                   "api": "fsk_sinkhorn_solve_grad (+ fsk_hvp_apply_single for cfg4), C ABI, "
+                          "host double buffers",
                    "loss": out["dual_cost"]}
         else:
             torch.cuda.synchronize()
