@@ -278,6 +278,11 @@ int fsk_engine_init_potentials(fsk_engine* e, void* stream);
  * over those rows (the lagged marginal violation of the previous iterate). */
 int fsk_engine_half_step(fsk_engine* e, int side, int64_t row_begin, int64_t row_end,
                          double* viol_accum, void* stream);
+/* `iters` alternating iterations over all rows (single GPU). On the CUDA-core
+ * path the loop is captured once into a CUDA graph and replayed (launch-bound
+ * small problems; FSK_GRAPH=0 disables); the tensor path runs it eagerly.
+ * `stream` must be a non-NULL stream for graph capture. */
+int fsk_engine_iterate(fsk_engine* e, int iters, void* stream);
 /* Gradient w.r.t. X for rows [row_begin,row_end): grad_dev (float, (end-begin) x d). */
 int fsk_engine_grad(fsk_engine* e, int64_t row_begin, int64_t row_end, float* grad_dev,
                     void* stream);

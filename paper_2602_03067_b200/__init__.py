@@ -504,6 +504,10 @@ class Engine:
                                           C.c_void_p(viol_ptr) if viol_ptr else None,
                                           C.c_void_p(stream)))
 
+    def iterate(self, iters: int, stream: int = 0):
+        """`iters` alternating iterations over all rows (CUDA graph on the CUDA-core path)."""
+        _check(lib().fsk_engine_iterate(self.h, C.c_int(iters), C.c_void_p(stream)))
+
     def transport_vec(self, side: int, v_ptr: int, out_ptr: int, stream: int = 0):
         """out (double, device) = P v (side 0) or P^T v (side 1) at the bound potentials."""
         _check(lib().fsk_engine_transport_vec(self.h, C.c_int(side), C.c_void_p(v_ptr),

@@ -4,6 +4,7 @@
 // collective library all-gathers the length-n vector in place, then the same
 // for g. No collective lives in here.
 #include <cmath>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -21,6 +22,11 @@ extern thread_local std::string g_err;
 using namespace fskb;
 
 struct fsk_engine {
+    // CUDA graph of `iterate` (CUDA-core path only): the whole f/g loop as one launch
+    cudaGraphExec_t graph = nullptr;
+    int graph_iters = 0;
+    cudaStream_t graph_stream = nullptr;
+    const float* graph_f = nullptr;
     int device = 0;
     DevProblem<float> P;
     float* f = nullptr;
@@ -84,6 +90,7 @@ int fsk_engine_create(int device, const double* X, const double* a, int64_t n, c
 void fsk_engine_destroy(fsk_engine* e) {
     if (!e) return;
     cudaSetDevice(e->device);
+    if (e->graph) cudaGraphExecDestroy(e->graph);
     cudaStreamSynchronize(e->own);
     e->P.tc.reset();
     e->P.src = DevSide<float>();
@@ -141,6 +148,58 @@ int fsk_engine_half_step(fsk_engine* e, int side, int64_t row_begin, int64_t row
             fa.marg_flag = side == 0 ? kFlagNonFiniteRowMarginal : kFlagNonFiniteColMarginal;
         }
         half_step_rows<float>(e->P, side, kpot, eps, fa, row_begin, row_end);
+    });
+}
+
+int fsk_engine_iterate(fsk_engine* e, int iters, void* stream) {
+    return eguard([&] {
+        if (!e->f || !e->g) throw ValidationFailure("engine potentials not bound");
+        if (!(e->eps > 0.0)) throw ValidationFailure("engine eps not set");
+        if (iters < 1) throw ValidationFailure("iters must be positive");
+        cudaStream_t s = pick(e, stream);
+        e->P.s = s;
+        const float eps = float(e->eps);
+        auto body = [&] {
+            for (int k = 0; k < iters; ++k) {
+                FinalizeArgs<float> fa{};
+                fa.eps = eps;
+                fa.flags = e->flags;
+                fa.out_pot = e->f;
+                half_step_rows<float>(e->P, 0, e->g, eps, fa, 0, e->P.src.n);
+                fa.out_pot = e->g;
+                half_step_rows<float>(e->P, 1, e->f, eps, fa, 0, e->P.tgt.n);
+            }
+        };
+        // the tensor path decides screening per pass on the host: run it eagerly;
+        // the CUDA-core path (small / low-d problems, launch-bound) replays a graph
+        const char* env = std::getenv("FSK_GRAPH");
+        const bool use_graph = !e->P.tc && s != nullptr && !(env && env[0] == '0');
+        if (!use_graph) {
+            body();
+            return;
+        }
+        if (!e->graph || e->graph_iters != iters || e->graph_stream != s || e->graph_f != e->f) {
+            if (e->graph) cudaGraphExecDestroy(e->graph);
+            e->graph = nullptr;
+            cudaGraph_t g = nullptr;
+            FSKB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            try {
+                body();
+            } catch (...) {
+                cudaStreamEndCapture(s, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            FSKB_CUDA(cudaStreamEndCapture(s, &g));
+            FSKB_CUDA(cudaGraphInstantiate(&e->graph, g, 0));
+            cudaGraphDestroy(g);
+            e->graph_iters = iters;
+            e->graph_stream = s;
+            e->graph_f = e->f;
+        } else {
+            count_launch(4 * iters);  // the captured launches (host-side counter)
+        }
+        FSKB_CUDA(cudaGraphLaunch(e->graph, s));
     });
 }
 

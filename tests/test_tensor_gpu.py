@@ -416,3 +416,34 @@ def test_tensor_transport_hadamard_parity(fsk, port, n, m, d, p):
     print(f"hadamard d={d} p={p}: max rel err {err:.2e} (ref-fp32 {e32:.2e})")
     assert err <= max(1e-5, 2.0 * e32)
     eng.close()
+
+
+def test_engine_iterate_graph_matches_loop(fsk):
+    """fsk_engine_iterate (CUDA graph on the CUDA-core path) reproduces the per-call
+    half-step loop bit for bit, on first capture and on replay."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(21)
+    n, m, d = 1000, 900, 3
+    X, Y = rng.normal(size=(n, d)), rng.normal(size=(m, d))
+    a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+    s = torch.cuda.Stream()
+    res = []
+    for use_iterate in (False, True, True):
+        eng = fsk.Engine(0, X, a, Y, b, mode="fma")
+        eng.set_eps(0.1)
+        f = torch.empty(n, dtype=torch.float32, device="cuda")
+        g = torch.empty(m, dtype=torch.float32, device="cuda")
+        eng.bind(f.data_ptr(), g.data_ptr())
+        for rep in range(2):  # second round replays the captured graph
+            eng.init_potentials(s.cuda_stream)
+            if use_iterate:
+                eng.iterate(7, s.cuda_stream)
+            else:
+                for _ in range(7):
+                    eng.half_step(0, 0, n, 0, s.cuda_stream)
+                    eng.half_step(1, 0, m, 0, s.cuda_stream)
+        s.synchronize()
+        res.append((f.cpu().numpy(), g.cpu().numpy()))
+        eng.close()
+    for fr, gr in res[1:]:
+        assert np.array_equal(fr, res[0][0]) and np.array_equal(gr, res[0][1])
