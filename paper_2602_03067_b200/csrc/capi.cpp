@@ -195,24 +195,6 @@ HostMarginals marginals_to_host(DevProblem<T>& P, const T* f, const T* g, T eps,
     return hm;
 }
 
-// FSK_TIMING=1: host wall-clock per solve phase on stderr (synchronizes the stream).
-struct PhaseTimer {
-    bool on;
-    cudaStream_t s;
-    std::chrono::steady_clock::time_point t0;
-    explicit PhaseTimer(cudaStream_t st) : on(std::getenv("FSK_TIMING") != nullptr), s(st) {
-        t0 = std::chrono::steady_clock::now();
-    }
-    void mark(const char* what) {
-        if (!on) return;
-        cudaStreamSynchronize(s);
-        const auto t1 = std::chrono::steady_clock::now();
-        std::fprintf(stderr, "[fsk timing] %-24s %9.3f ms\n", what,
-                     std::chrono::duration<double, std::milli>(t1 - t0).count());
-        t0 = t1;
-    }
-};
-
 // Device-resident Sinkhorn (solver.cpp:21-117). T = double: Precision::Double;
 // T = float: Precision::Single (tensor-core or FMA half-steps).
 template <typename T>

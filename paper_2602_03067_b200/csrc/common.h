@@ -3,7 +3,10 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -93,5 +96,24 @@ inline void count_launch(int k = 1) { launch_counter() += k; }
 bool& break_lse_flag();
 
 int num_sms();
+
+// FSK_TIMING=1: host wall-clock per solve phase on stderr (synchronizes the stream).
+struct PhaseTimer {
+    bool on;
+    cudaStream_t s;
+    std::chrono::steady_clock::time_point t0;
+    explicit PhaseTimer(cudaStream_t st) : on(std::getenv("FSK_TIMING") != nullptr), s(st) {
+        t0 = std::chrono::steady_clock::now();
+    }
+    void mark(const char* what) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const auto t1 = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[fsk timing] %-24s %9.3f ms\n", what,
+                     std::chrono::duration<double, std::milli>(t1 - t0).count());
+        t0 = t1;
+    }
+};
+
 
 }  // namespace fskb

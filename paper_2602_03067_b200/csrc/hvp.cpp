@@ -150,6 +150,7 @@ void hvp_run(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat
             throw ValidationFailure("single-precision hvp supports the squared-Euclidean cost only");
         const int64_t n = src->n, m = tgt->n, d = src->d;
         auto& C = exec_ctx();
+        PhaseTimer timer(C.s);
         DevProblem<T> P;
         P.upload(*src, *tgt, cost, C.s);
         DevBuf<float> l2h_f, l2l_f, l2h_g, l2l_g;
@@ -209,6 +210,7 @@ void hvp_run(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat
         throw_for_flags(read_and_clear_flags(C));
         for (double v : r)
             if (!(v > 0.0)) throw NumericalFailure("hvp: zero induced row marginal");
+        timer.mark("hvp setup + 2 LSE");
 
         HvpCtx<T> H{*src, *tgt, P, C, eps, f.get(), g.get(), lse_f.get(), mx_f.get(),
                     lse_g.get(), mx_g.get(), ledger, *tiles, cost};
@@ -222,6 +224,7 @@ void hvp_run(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat
         const std::vector<double> Y(tgt->points, tgt->points + m * d);
         const std::vector<double> Av(A, A + n * d);
         const std::vector<double> PY = H.apply(0, Y, d);  // cached transport-matrix product
+        timer.mark("hvp P Y");
 
         // build_rhs
         std::vector<double> u((size_t)(n)), uP((size_t)(n)), r1((size_t)(n));
@@ -249,6 +252,7 @@ void hvp_run(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat
         std::vector<double> rhs = H.apply(1, tmp, 1);
         for (int64_t j = 0; j < m; ++j) rhs[size_t(j)] = r2[size_t(j)] - rhs[size_t(j)];
 
+        timer.mark("hvp rhs (P^T u, P^T A, P^T r1/r)");
         // CG on S_tau = diag(c) - P^T diag(r)^-1 P + tau I
         auto schur = [&](const std::vector<double>& v) {
             std::vector<double> pv = H.apply(0, v, 1);
@@ -288,6 +292,7 @@ void hvp_run(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat
             }
             relres = std::sqrt(rs) / rn0;
         }
+        timer.mark("hvp CG");
         // w1 = diag(r)^-1 (r1 - P w2) ; R^T w
         const std::vector<double> Pw2 = H.apply(0, w2, 1);
         std::vector<double> w1((size_t)(n));
@@ -297,7 +302,9 @@ void hvp_run(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat
             for (int64_t t = 0; t < d; ++t) w2Y[size_t(j * d + t)] = w2[size_t(j)] * Y[size_t(j * d + t)];
         const std::vector<double> Pw2Y = H.apply(0, w2Y, d);
         // explicit term: B5 = (P (.) A Y^T) Y
+        timer.mark("hvp P w2, P (w2 Y)");
         const std::vector<double> B5 = H.apply(0, Y, d, A, tgt->points, d);
+        timer.mark("hvp Hadamard");
         for (int64_t i = 0; i < n; ++i) {
             const double ri = r[size_t(i)], ui = u[size_t(i)], upi = uP[size_t(i)];
             for (int64_t t = 0; t < d; ++t) {
@@ -309,6 +316,7 @@ void hvp_run(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat
                 out[k] = rtw / eps + ea;
             }
         }
+        timer.mark("hvp assemble");
         throw_for_flags(read_and_clear_flags(C) & ~kFlagNonFinitePotential);
         if (hrep) {
             hrep->cg_iters = iters;
