@@ -317,7 +317,7 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
         if constexpr (kSingle) {
             if (P.tc && cur_tc_eps != pot_eps) P.tc->set_eps(P, pot_eps);
         }
-        const bool keep = kSingle && P.tc && P.tc->chunks() == 1 && grad_out;
+        const bool keep = kSingle && P.tc && grad_out;
         if (keep) {
             l2h_keep.alloc(size_t(n), C.s);
             l2l_keep.alloc(size_t(n), C.s);
@@ -350,7 +350,7 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
         DevBuf<T> G(size_t(n * d), C.s);
         bool done = false;
         if constexpr (kSingle) {
-            if (P.tc && P.tc->chunks() == 1) {
+            if (P.tc) {
                 // fused tcgen05 path: K1 row LSE + split-fp16 transport kernel
                 if (!r_keep.get()) P.tc->set_eps(P, pot_eps);
                 if constexpr (kSingle)

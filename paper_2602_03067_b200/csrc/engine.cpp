@@ -215,7 +215,7 @@ int fsk_engine_grad(fsk_engine* e, int64_t row_begin, int64_t row_end, float* gr
         cudaStream_t s = pick(e, stream);
         e->P.s = s;
         const float eps = float(e->eps);
-        if (e->P.tc && e->P.tc->chunks() == 1) {
+        if (e->P.tc) {
             e->P.tc->grad(e->P, 0, e->g, e->f, eps, row_begin, row_end, grad_dev, e->flags);
             return;
         }

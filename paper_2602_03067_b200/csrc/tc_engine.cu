@@ -1257,6 +1257,20 @@ __global__ void tc_vec_finalize_kernel(const double* __restrict__ part, int spli
     out[i] = double(marg[i]) * s;
 }
 
+// G = 2 (diag(r) X - P Y) from the transport output PY (rows x d)
+__global__ void tc_grad_from_py_kernel(const float* __restrict__ PY, const float* __restrict__ X,
+                                       const float* __restrict__ r, int64_t row_begin,
+                                       int64_t row_end, int64_t d, float* __restrict__ G,
+                                       int* flags) {
+    const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t i = row_begin + gid / d;
+    const int64_t k = gid % d;
+    if (i >= row_end) return;
+    const double g = 2.0 * (double(r[i]) * double(X[i * d + k]) - double(PY[i * d + k]));
+    if (!isfinite(g)) atomicOr(flags, kFlagNonFiniteTransport);
+    G[(i - row_begin) * d + k] = float(g);
+}
+
 // G_i = 2 r_i (x_i - O_i),  O_i = inv_v * sum_s part_o[s][i]
 __global__ void tc_grad_finalize_kernel(const float* __restrict__ part_o, int splits, int64_t R,
                                         int64_t row_begin, int64_t row_end, int64_t d,
@@ -1822,7 +1836,33 @@ void TcHalfStep::grad(DevProblem<float>& P, int side, const float* kpot, const f
                       const float* pre_l2h, const float* pre_l2l, const float* pre_r) {
     if (row_end <= row_begin) return;
     Impl& I = *impl_;
-    if (I.chunks != 1) throw ValidationFailure("fused tcgen05 gradient needs d <= 64");
+    if (I.chunks != 1) {
+        // d > 64: P V with V = the key cloud through the general apply kernel (all
+        // rows), then G = 2 (diag(r) X - P Y) on the requested rows
+        const DevSide<float>& qs = side == 0 ? P.src : P.tgt;
+        const DevSide<float>& ks = side == 0 ? P.tgt : P.src;
+        const int64_t R = qs.n, d = qs.d;
+        DevBuf<float> l2h(size_t(R), P.s), l2l(size_t(R), P.s), r(size_t(R), P.s);
+        FinalizeArgs<float> fa{};
+        fa.eps = eps;
+        fa.flags = flags;
+        fa.old_pot = pot;
+        fa.w = qs.w.get();
+        fa.out_marg = r.get();
+        fa.marg_flag = side == 0 ? kFlagNonFiniteRowMarginal : kFlagNonFiniteColMarginal;
+        fa.out_l2h = l2h.get();
+        fa.out_l2l = l2l.get();
+        run(P, side, kpot, eps, fa, 0, R);
+        DevBuf<float> PY(size_t(R * d), P.s);
+        apply_mat(P, side, kpot, eps, l2h.get(), l2l.get(), r.get(), ks.pts.get(), d, PY.get(),
+                  flags);
+        const int64_t total = (row_end - row_begin) * d;
+        tc_grad_from_py_kernel<<<unsigned((total + 255) / 256), 256, 0, P.s>>>(
+            PY.get(), qs.pts.get(), r.get(), row_begin, row_end, d, G, flags);
+        FSKB_CUDA(cudaGetLastError());
+        count_launch();
+        return;
+    }
     const int qc = side == 0 ? 0 : 1, kc = side == 0 ? 1 : 0;
     const DevSide<float>& qs = side == 0 ? P.src : P.tgt;
     const DevSide<float>& ks = side == 0 ? P.tgt : P.src;

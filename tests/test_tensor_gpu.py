@@ -132,7 +132,9 @@ def test_engine_row_shards_reproduce_full_half_step(fsk, port):
 
 
 @pytest.mark.parametrize("n,m,d", [(1000, 777, 64), (515, 1300, 33), (260, 513, 16),
-                                   (129, 131, 3), (2048, 4096, 64)])
+                                   (129, 131, 3), (2048, 4096, 64),
+                                   # d > 64: general apply kernel (V = Y) + gradient epilogue
+                                   (400, 350, 100), (260, 300, 1024)])
 @pytest.mark.parametrize("eps", [0.05, 1.0])
 def test_tensor_fused_gradient_parity(fsk, port, n, m, d, eps):
     """Fused tcgen05 transport kernel (K3): grad_X at the engine's own potentials
