@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
                             issue_score_chunk(tmem + uint32_t(t * 2 * TILE),
                                               tmem + uint32_t((t * 2 + 1) * TILE), st + t * QTILE,
                                               st + 2 * QTILE, base + C_OFF_ONES, st + 3 * QTILE,
-                                              c == 0);
+                                              c == 0, c == C - 1);
                         umma_commit(kempty(s));
                     }
                     umma_commit(accfull);
@@ -1090,7 +1090,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
                         }
                         fence_after();
                         issue_score_chunk(tmem, tmem + TILE, addr[0], addr[1], base + G_OFF_ONES,
-                                          base + G_OFF_BIAS + bb * BIAS, c == 0);
+                                          base + G_OFF_BIAS + bb * BIAS, c == 0, c == C - 1);
                         if (had) issue_w_chunk(tmem + G_WCOL, addr[2], addr[1], c == 0);
                         for (int o = 0; o < ops; ++o) umma_commit(sempty_(slot[o]));
                         sq += ops;

@@ -213,12 +213,14 @@ __device__ __forceinline__ void issue_screen_tile(uint32_t d_tmem, uint32_t qa, 
 
 // One 64-wide feature chunk of a score tile for d > 64 (operands streamed chunk
 // by chunk). Two accumulators keep the fp32 rounding at the scale of each part:
-// d_big = bias + sum of hi x hi slices (opened by the bias on the first chunk),
-// d_small = the 8 cross terms per chunk (2^-11 of the score), summed by the
-// epilogue, so only 4 C + 1 additions round at the score's magnitude.
+// d_big = sum of hi x hi slices, then the bias on the last chunk (the bias
+// ~ g/eps carries |y|^2/eps and can dwarf the dot product at large d, so adding
+// it last keeps the 4 C roundings of the dot product at the dot product's own
+// magnitude); d_small = the 8 cross terms per chunk (2^-11 of the score),
+// summed by the epilogue.
 __device__ __forceinline__ void issue_score_chunk(uint32_t d_big, uint32_t d_small, uint32_t qa,
                                                   uint32_t ka, uint32_t ones, uint32_t bias,
-                                                  bool first) {
+                                                  bool first, bool last) {
 #pragma unroll
     for (int kk = 0; kk < DPAD / 16; ++kk) {
         umma_ss(d_small, umma_desc(qa + CHUNK + kk * 32, 1024, 2), umma_desc(ka + kk * 32, 1024, 2),
@@ -226,11 +228,11 @@ __device__ __forceinline__ void issue_score_chunk(uint32_t d_big, uint32_t d_sma
         umma_ss(d_small, umma_desc(qa + kk * 32, 1024, 2), umma_desc(ka + CHUNK + kk * 32, 1024, 2),
                 IDESC_QK, 1u);
     }
-    if (first) umma_ss(d_big, umma_desc(ones, 256, 6), umma_desc(bias, 256, 6), IDESC_QK, 0u);
 #pragma unroll
     for (int kk = 0; kk < DPAD / 16; ++kk)
         umma_ss(d_big, umma_desc(qa + kk * 32, 1024, 2), umma_desc(ka + kk * 32, 1024, 2),
-                IDESC_QK, 1u);
+                IDESC_QK, (first && kk == 0) ? 0u : 1u);
+    if (last) umma_ss(d_big, umma_desc(ones, 256, 6), umma_desc(bias, 256, 6), IDESC_QK, 1u);
 }
 
 }  // namespace tc
