@@ -85,16 +85,33 @@ struct TcParams {
     // the running approximate row max - screen_thr for every row are not scored
     float screen_thr;
     unsigned long long* live_count;  // += live key tiles (diagnostics), nullable
-    uint32_t* live_global;       // screened: per item, the phase-1 bitmask (kwords words)
-    int kwords;
+    uint32_t* live_global;       // LSE passes: per item, the key tiles not proven negligible
+    int kwords;                  //   (kwords words per item; bit kt - kt0)
+    // VEC passes at the same potentials: only key tiles of that live set are scored
+    // (unit u of this pass = unit u of the LSE pass; item index u * in_splits + kt / in_kps)
+    const uint32_t* live_in;
+    int in_splits, in_kps, in_kwords;
 };
+
+// next key tile >= kt (< kt1) in the live set `live_in` of LSE-pass unit u
+__device__ __forceinline__ int live_in_next(const TcParams& p, int u, int kt, int kt1) {
+    while (kt < kt1) {
+        const int ls = kt / p.in_kps, rel = kt - ls * p.in_kps;
+        const uint32_t w =
+            __ldg(p.live_in + (size_t(u) * p.in_splits + ls) * p.in_kwords + (rel >> 5)) >> (rel & 31);
+        if (w) return kt + __ffs(w) - 1;
+        kt += 32 - (rel & 31);
+        if (rel + 32 - (rel & 31) > p.in_kps) kt = (ls + 1) * p.in_kps;
+    }
+    return kt1;
+}
 
 // Per-tile epilogue math shared by the K1 kernels: mask the padded keys of the
 // last tile, then either the online (max, sum-exp) update (LSE) or, with the row
 // LSE known, the transport-vector sum sum_j 2^(t - L) v_j (VEC). `v` holds the 128
 // fp32 scores of this thread's row (acc units; t = acc * acc_scale).
 template <bool VEC>
-__device__ __forceinline__ void k1_tile_update(uint32_t (&v)[128], int64_t kbase, const TcParams& p,
+__device__ __forceinline__ bool k1_tile_update(uint32_t (&v)[128], int64_t kbase, const TcParams& p,
                                                float& M, double& S, float nlh, float nll,
                                                float* vb, int lane) {
     if (kbase + TILE > p.key_valid) {
@@ -115,7 +132,7 @@ __device__ __forceinline__ void k1_tile_update(uint32_t (&v)[128], int64_t kbase
     if constexpr (VEC) {
         // P~ = 2^(t - L) <= 1; a tile whose P~ are all < 2^-64 for the warp's rows
         // adds < m 2^-64 max|v| - below the fp32 result's rounding
-        if (__all_sync(0xffffffffu, umax + nlh < -kSkipLog2)) return;
+        if (__all_sync(0xffffffffu, umax + nlh < -kSkipLog2)) return false;
         // the tile's 128 values of v, broadcast through a per-warp buffer
         float4 vv = make_float4(0.f, 0.f, 0.f, 0.f);
         const int64_t j0 = kbase + 4 * lane;
@@ -139,6 +156,7 @@ __device__ __forceinline__ void k1_tile_update(uint32_t (&v)[128], int64_t kbase
         }
         S += double((s0 + s1) + (s2 + s3));
         __syncwarp();
+        return true;
     } else {
         if (umax > M) {
             if (S != 0.0) S *= double(ex2(p.break_lse ? umax - M : M - umax));
@@ -147,7 +165,7 @@ __device__ __forceinline__ void k1_tile_update(uint32_t (&v)[128], int64_t kbase
         // every term of this tile is < 2^-64 of the running max for all 32 rows of
         // the warp: the whole tile adds < m 2^-64 relative - below rounding
         const bool dead = M == -INFINITY;
-        if (__all_sync(0xffffffffu, dead || umax < M - kSkipLog2)) return;
+        if (__all_sync(0xffffffffu, dead || umax < M - kSkipLog2)) return false;
         const float nm = dead ? 0.0f : -M;
         float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
@@ -158,6 +176,7 @@ __device__ __forceinline__ void k1_tile_update(uint32_t (&v)[128], int64_t kbase
             s3 += ex2(fmaf(__uint_as_float(v[j + 3]), p.acc_scale, nm));
         }
         S += double((s0 + s1) + (s2 + s3));
+        return true;
     }
 }
 
@@ -203,6 +222,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
     const uint32_t tmem = *tmem_slot;
     const int ktiles_per_split = (p.k_tiles + p.splits - 1) / p.splits;
     const int C = p.chunks;
+    // VEC at fixed potentials: only the key tiles of the LSE pass's live set
+    auto nxt = [&](int unit, int kt, int kt1) {
+        return (VEC && p.live_in) ? live_in_next(p, unit, kt, kt1) : kt;
+    };
 
     if (warp == 0) {
         if (lane == 0) {
@@ -213,7 +236,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
                 const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
-                for (int kt = kt0; kt < kt1; ++kt) {
+                for (int kt = nxt(unit, kt0, kt1); kt < kt1; kt = nxt(unit, kt + 1, kt1)) {
                     for (int c = 0; c < C; ++c, ++it) {
                         const int s = it % CSTAGES;
                         mbar_wait(kempty(s), ((it / CSTAGES) & 1) ^ 1);
@@ -238,7 +261,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
                 const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
-                for (int kt = kt0; kt < kt1; ++kt, ++acc_it) {
+                for (int kt = nxt(unit, kt0, kt1); kt < kt1; kt = nxt(unit, kt + 1, kt1), ++acc_it) {
                     mbar_wait(accempty, (acc_it & 1) ^ 1);
                     fence_after();
                     for (int c = 0; c < C; ++c, ++it) {
@@ -279,7 +302,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
                 nlh = live ? -p.l2h[row] : -3.0e38f;
                 nll = live ? -p.l2l[row] : 0.0f;
             }
-            for (int kt = kt0; kt < kt1; ++kt, ++acc_it) {
+            for (int kt = nxt(unit, kt0, kt1); kt < kt1; kt = nxt(unit, kt + 1, kt1), ++acc_it) {
                 mbar_wait(accfull, acc_it & 1);
                 fence_after();
                 uint32_t v[128];
@@ -301,7 +324,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
                 __syncwarp();
                 if (lane == 0) mbar_arrive(accempty);
                 if (t >= nq) continue;
-                k1_tile_update<VEC>(v, int64_t(kt) * TILE, p, M, S, nlh, nll, vb, lane);
+                const bool hit = k1_tile_update<VEC>(v, int64_t(kt) * TILE, p, M, S, nlh, nll, vb,
+                                                     lane);
+                if (!VEC && hit && p.live_global && lane == 0)
+                    atomicOr(&p.live_global[size_t(item) * p.kwords + ((kt - kt0) >> 5)],
+                             1u << ((kt - kt0) & 31));
             }
             if (t < nq && row >= p.row_begin && row < p.row_end) {
                 if constexpr (VEC) {
@@ -396,12 +423,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
         return kt1;
     };
     const int ktiles_per_split = (p.k_tiles + p.splits - 1) / p.splits;
+    // phase-2 (SCREEN) / VEC-at-fixed-potentials key tile sequence
+    auto first_kt = [&](int unit, int kt0, int kt1) {
+        if constexpr (SCREEN) return next_live(kt0, kt0, kt1);
+        return (VEC && p.live_in) ? live_in_next(p, unit, kt0, kt1) : kt0;
+    };
+    auto next_kt = [&](int unit, int kt, int kt0, int kt1) {
+        if constexpr (SCREEN) return next_live(kt + 1, kt0, kt1);
+        return (VEC && p.live_in) ? live_in_next(p, unit, kt + 1, kt1) : kt + 1;
+    };
 
     if (warp == 0) {
         if (lane == 0) {
             int it = 0;
             for (int item = blockIdx.x, lu = 0; item < p.items; item += gridDim.x, ++lu) {
-                const int split = item % p.splits;
+                const int unit = item / p.splits, split = item % p.splits;
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
                 if constexpr (SCREEN) {
@@ -416,8 +452,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                     mbar_wait(screen_done, lu & 1);
                 }
                 int nlive = 0;
-                for (int kt = SCREEN ? next_live(kt0, kt0, kt1) : kt0; kt < kt1;
-                     kt = SCREEN ? next_live(kt + 1, kt0, kt1) : kt + 1, ++it, ++nlive) {
+                for (int kt = first_kt(unit, kt0, kt1); kt < kt1;
+                     kt = next_kt(unit, kt, kt0, kt1), ++it, ++nlive) {
                     const int s = it % TQ_STAGES;
                     mbar_wait(kempty(s), ((it / TQ_STAGES) & 1) ^ 1);
                     mbar_expect_tx(kfull(s), KSTAGE);
@@ -468,8 +504,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                     for (int kt = kt0; kt < kt1; ++kt) tile_mmas(kt, true);
                     mbar_wait(screen_done, lu & 1);
                 }
-                for (int kt = SCREEN ? next_live(kt0, kt0, kt1) : kt0; kt < kt1;
-                     kt = SCREEN ? next_live(kt + 1, kt0, kt1) : kt + 1)
+                for (int kt = first_kt(unit, kt0, kt1); kt < kt1; kt = next_kt(unit, kt, kt0, kt1))
                     tile_mmas(kt, false);
                 if constexpr (SCREEN) mbar_arrive(bits_free);
                 umma_commit(qfree);
@@ -579,8 +614,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                     for (int w = threadIdx.x - 64; w < p.kwords; w += 256)
                         p.live_global[size_t(item) * p.kwords + w] = live_bits[w];
             }
-            for (int kt = SCREEN ? next_live(kt0, kt0, kt1) : kt0; kt < kt1;
-                 kt = SCREEN ? next_live(kt + 1, kt0, kt1) : kt + 1) {
+            for (int kt = first_kt(unit, kt0, kt1); kt < kt1; kt = next_kt(unit, kt, kt0, kt1)) {
                 if (t >= nq) continue;
                 mbar_wait(accfull(t), acc_n & 1);
                 fence_after();
@@ -594,7 +628,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 __syncwarp();
                 if (lane == 0) mbar_arrive(accempty(t));
                 ++acc_n;
-                k1_tile_update<VEC>(v, int64_t(kt) * TILE, p, M, S, nlh, nll, vb, lane);
+                const bool hit = k1_tile_update<VEC>(v, int64_t(kt) * TILE, p, M, S, nlh, nll, vb,
+                                                     lane);
+                if (!VEC && !SCREEN && hit && p.live_global && lane == 0)
+                    atomicOr(&p.live_global[size_t(item) * p.kwords + ((kt - kt0) >> 5)],
+                             1u << ((kt - kt0) & 31));
             }
             if constexpr (SCREEN) {
                 mbar_wait(bits_free, lu & 1);
@@ -961,7 +999,24 @@ struct TcApplyGenParams {
     const float* l2h;
     const float* l2l;
     float* part_o;          // [splits][R][vc * 64]
+    // live key tiles of the LSE pass at the same potentials (nullable); query tile
+    // u belongs to that pass's unit u / 2
+    const uint32_t* live_in;
+    int in_splits, in_kps, in_kwords;
 };
+
+__device__ __forceinline__ int gen_next_live(const TcApplyGenParams& p, int u, int kt, int kt1) {
+    if (!p.live_in) return kt;
+    while (kt < kt1) {
+        const int ls = kt / p.in_kps, rel = kt - ls * p.in_kps;
+        const uint32_t w = __ldg(p.live_in + (size_t(u >> 1) * p.in_splits + ls) * p.in_kwords +
+                                 (rel >> 5)) >> (rel & 31);
+        if (w) return kt + __ffs(w) - 1;
+        kt += 32 - (rel & 31);
+        if (rel + 32 - (rel & 31) > p.in_kps) kt = (ls + 1) * p.in_kps;
+    }
+    return kt1;
+}
 
 // 12 MMAs of one 64-feature chunk of W = A B^T into one accumulator (no bias):
 // cross terms first, then hi x hi.
@@ -1042,7 +1097,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
                 const int qt = p.q_tile_begin + unit;
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
-                for (int kt = kt0; kt < kt1; ++kt, ++vt) {
+                for (int kt = gen_next_live(p, unit, kt0, kt1); kt < kt1;
+                     kt = gen_next_live(p, unit, kt + 1, kt1), ++vt) {
                     const int bb = vt & 1;
                     mbar_wait(bempty(bb), ((vt >> 1) & 1) ^ 1);
                     mbar_expect_tx(bfull(bb), BIAS);
@@ -1072,12 +1128,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
         if (lane == 0) {
             int sq = 0, vt = 0, lu = 0;
             for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++lu) {
-                const int split = item % p.splits;
+                const int unit = item / p.splits, split = item % p.splits;
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
                 mbar_wait(oempty, (lu & 1) ^ 1);
                 fence_after();
-                for (int kt = kt0; kt < kt1; ++kt, ++vt) {
+                bool o_first = true;
+                for (int kt = gen_next_live(p, unit, kt0, kt1); kt < kt1;
+                     kt = gen_next_live(p, unit, kt + 1, kt1), ++vt) {
                     const int bb = vt & 1;
                     mbar_wait(bfull(bb), (vt >> 1) & 1);
                     for (int c = 0; c < C; ++c) {
@@ -1108,12 +1166,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
                             const uint32_t ph = tmem + uint32_t((kk >> 2) * 64 + (kk & 3) * 8);
                             const uint64_t vh = umma_desc(vst + kk * 2048, 1024, 2, 8192);
                             const uint64_t vl = umma_desc(vst + CHUNK + kk * 2048, 1024, 2, 8192);
-                            umma_ts(o, ph, vh, IDESC_PV, (kt > kt0 || kk > 0) ? 1u : 0u);
+                            umma_ts(o, ph, vh, IDESC_PV, (!o_first || kk > 0) ? 1u : 0u);
                             umma_ts(o, ph + 32, vh, IDESC_PV, 1u);
                             umma_ts(o, ph, vl, IDESC_PV, 1u);
                         }
                     }
                     umma_commit(vempty);
+                    o_first = false;
                 }
                 umma_commit(ofull);
             }
@@ -1132,7 +1191,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
             const bool live = row < p.R;
             const float nlh = live ? -p.l2h[row] : -3.0e38f;
             const float c2 = live ? kPScaleLog2 - p.l2l[row] : 0.0f;
-            for (int kt = kt0; kt < kt1; ++kt, ++vt) {
+            bool any_tile = false;
+            for (int kt = gen_next_live(p, unit, kt0, kt1); kt < kt1;
+                 kt = gen_next_live(p, unit, kt + 1, kt1), ++vt) {
+                any_tile = true;
                 mbar_wait(sfull, vt & 1);
                 fence_after();
                 const uint32_t taddr = tmem + lane_addr + uint32_t(half * 64);
@@ -1211,6 +1273,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(oempty);
+            if (!any_tile) {  // no live key tile in this split range: O = 0
+#pragma unroll
+                for (int c = 0; c < 64; ++c) o[c] = 0u;
+            }
             if (row >= p.row_begin && row < p.row_end) {
                 float* dst = p.part_o + (size_t(split) * p.R + row) * width + half * per_half;
 #pragma unroll
@@ -1492,6 +1558,7 @@ struct TcHalfStep::Impl {
     bool live_valid[2] = {false, false};
     int live_splits[2] = {1, 1}, live_kps[2] = {1, 1}, live_kwords[2] = {1, 1};
     int64_t live_row_begin[2] = {0, 0}, live_row_end[2] = {0, 0};
+    const float* live_kpot[2] = {nullptr, nullptr};  // potentials the live set belongs to
     ~Impl() {
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
@@ -1677,17 +1744,31 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         p.live_count = I.live_count.get() + side;
         if (!I.pending[side])
             FSKB_CUDA(cudaMemsetAsync(p.live_count, 0, sizeof(unsigned long long), P.s));
+    }
+    if (!vec) {
+        // every LSE pass records the key tiles it did not prove negligible (the
+        // screen's phase-1 set, or the tiles the epilogue did not skip); transport
+        // passes at the same potentials then score only those
         p.kwords = (kps + 31) / 32;
         const size_t words = size_t(p.items) * size_t(p.kwords);
         if (I.live_glob[side].size() < words) I.live_glob[side].alloc(words, P.s);
         p.live_global = I.live_glob[side].get();
+        if (!screen)
+            FSKB_CUDA(cudaMemsetAsync(p.live_global, 0, words * sizeof(uint32_t), P.s));
+        I.live_valid[side] = true;
+        I.live_kpot[side] = kpot;
         I.live_splits[side] = p.splits;
         I.live_kps[side] = kps;
         I.live_kwords[side] = p.kwords;
         I.live_row_begin[side] = row_begin;
         I.live_row_end[side] = row_end;
+    } else if (I.live_valid[side] && I.live_kpot[side] == kpot && I.live_row_begin[side] == 0 &&
+               I.live_row_end[side] == p.R && row_begin == 0 && row_end == p.R) {
+        p.live_in = I.live_glob[side].get();
+        p.in_splits = I.live_splits[side];
+        p.in_kps = I.live_kps[side];
+        p.in_kwords = I.live_kwords[side];
     }
-    if (!vec) I.live_valid[side] = screen;
     if (I.chunks == 1) {
         if (vec)
             tc_lse_tq_kernel<true, false><<<grid, NUM_THREADS, TQ_SMEM_BYTES, P.s>>>(p);
@@ -1812,6 +1893,13 @@ void TcHalfStep::apply_mat(DevProblem<float>& P, int side, const float* kpot, fl
     g.acc_scale = std::ldexp(1.0f, E);
     g.l2h = l2h;
     g.l2l = l2l;
+    if (I.live_valid[side] && I.live_kpot[side] == kpot && I.live_row_begin[side] == 0 &&
+        I.live_row_end[side] == R) {
+        g.live_in = I.live_glob[side].get();
+        g.in_splits = I.live_splits[side];
+        g.in_kps = I.live_kps[side];
+        g.in_kwords = I.live_kwords[side];
+    }
     const int vc_max = A ? 1 : 2;
     DevBuf<float> part(size_t(g.splits) * size_t(R) * vc_max * DPAD, P.s);
     g.part_o = part.get();
@@ -1907,7 +1995,7 @@ void TcHalfStep::grad(DevProblem<float>& P, int side, const float* kpot, const f
     p.acc_scale = std::ldexp(1.0f, I.eq[qc] + I.ek[side]);
     p.l2h = L2h;
     p.l2l = L2l;
-    if (I.live_valid[side] && I.live_row_begin[side] == row_begin &&
+    if (I.live_valid[side] && I.live_kpot[side] == kpot && I.live_row_begin[side] == row_begin &&
         I.live_row_end[side] == row_end) {
         // the LSE pass above was screened: stream only its live key tiles
         p.live_global = I.live_glob[side].get();
