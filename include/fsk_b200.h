@@ -306,6 +306,10 @@ int fsk_engine_transport_hadamard(fsk_engine* e, const float* a_dev, const float
  * every row's max by the 5-MMA hi x hi screen (diagnostics for the bench line).
  * Screening is adaptive (on while the live fraction stays below 0.45). */
 uint64_t fsk_engine_screen_live_tiles(const fsk_engine* e);
+/* Fraction of (query tile pair, key tile) blocks in the live-tile set recorded by
+ * the last LSE pass of `side` (reused by transport passes at the same potentials);
+ * -1 when none. Synchronizes the device (diagnostics). */
+double fsk_engine_live_set_fraction(const fsk_engine* e, int side);
 /* (query tile pair, key tile) blocks covered by those screened passes. */
 uint64_t fsk_engine_screen_blocks(const fsk_engine* e);
 /* Launch counter of this engine's kernels (for bench accounting). */

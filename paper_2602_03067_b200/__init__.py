@@ -104,6 +104,7 @@ def lib() -> C.CDLL:
         L.fsk_engine_kernel_launches.restype = C.c_int64
         L.fsk_engine_screen_live_tiles.restype = C.c_uint64
         L.fsk_engine_screen_blocks.restype = C.c_uint64
+        L.fsk_engine_live_set_fraction.restype = C.c_double
         for name in ("fsk_io_count_f_update", "fsk_io_count_g_update",
                      "fsk_io_count_symmetric_update", "fsk_io_count_apply_plan",
                      "fsk_io_count_apply_plan_adjoint", "fsk_io_count_apply_hadamard",
@@ -479,6 +480,10 @@ class Engine:
     def live_tiles(self) -> int:
         """Blocks scored in full by screened LSE passes so far."""
         return int(lib().fsk_engine_screen_live_tiles(self.h))
+
+    def live_set_fraction(self, side: int) -> float:
+        """Live-tile fraction recorded by the last LSE pass of `side` (-1: none)."""
+        return float(lib().fsk_engine_live_set_fraction(self.h, C.c_int(side)))
 
     def screened_blocks(self) -> int:
         """Blocks covered by screened LSE passes so far."""

@@ -354,6 +354,10 @@ uint64_t fsk_engine_screen_live_tiles(const fsk_engine* e) {
     return e && e->P.tc ? uint64_t(e->P.tc->live_tiles()) : 0;
 }
 
+double fsk_engine_live_set_fraction(const fsk_engine* e, int side) {
+    return e && e->P.tc ? e->P.tc->live_set_fraction(side) : -1.0;
+}
+
 uint64_t fsk_engine_screen_blocks(const fsk_engine* e) {
     if (!e || !e->P.tc) return 0;
     e->P.tc->live_tiles();  // drains the pending read-backs

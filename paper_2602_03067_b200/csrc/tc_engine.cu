@@ -60,6 +60,13 @@ constexpr uint32_t C_OFF_BAR = C_OFF_ONES + BIAS;              // 204 KB
 constexpr uint32_t C_SMEM_BYTES = C_OFF_BAR + 256 + VBUF + 1024;
 constexpr float kSkipLog2 = 64.0f;  // LSE tiles entirely 2^-64 below the running max are skipped
 
+// order-preserving float <-> int for atomicMax / atomicMin on floats
+__device__ __forceinline__ int fenc(float f) {
+    const int i = __float_as_int(f);
+    return i >= 0 ? i : i ^ 0x7FFFFFFF;
+}
+__device__ __forceinline__ float fdec(int k) { return __int_as_float(k >= 0 ? k : k ^ 0x7FFFFFFF); }
+
 struct TcParams {
     const uint8_t* qimg;    // query tile images (hi+lo per 128-row tile)
     const uint8_t* kimg;    // key tile images (hi+lo per 128-key tile)
@@ -91,6 +98,11 @@ struct TcParams {
     // (unit u of this pass = unit u of the LSE pass; item index u * in_splits + kt / in_kps)
     const uint32_t* live_in;
     int in_splits, in_kps, in_kwords;
+    // warm bounds (LSE, d <= 64): gap[u][kt] = max over the unit's rows of
+    // (tile max - running row max), ordered-int atomicMax; part_arg[split][row] =
+    // key tile of the row's running max in that split
+    int* gap;
+    int* part_arg;
 };
 
 // next key tile >= kt (< kt1) in the live set `live_in` of LSE-pass unit u
@@ -113,7 +125,7 @@ __device__ __forceinline__ int live_in_next(const TcParams& p, int u, int kt, in
 template <bool VEC>
 __device__ __forceinline__ bool k1_tile_update(uint32_t (&v)[128], int64_t kbase, const TcParams& p,
                                                float& M, double& S, float nlh, float nll,
-                                               float* vb, int lane) {
+                                               float* vb, int lane, float& umax_out) {
     if (kbase + TILE > p.key_valid) {
 #pragma unroll
         for (int j = 0; j < 128; ++j)
@@ -129,6 +141,7 @@ __device__ __forceinline__ bool k1_tile_update(uint32_t (&v)[128], int64_t kbase
         mx3 = fmaxf(mx3, __uint_as_float(v[j + 3]));
     }
     const float umax = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * p.acc_scale;
+    umax_out = umax;
     if constexpr (VEC) {
         // P~ = 2^(t - L) <= 1; a tile whose P~ are all < 2^-64 for the warp's rows
         // adds < m 2^-64 max|v| - below the fp32 result's rounding
@@ -324,8 +337,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
                 __syncwarp();
                 if (lane == 0) mbar_arrive(accempty);
                 if (t >= nq) continue;
+                float umax;
                 const bool hit = k1_tile_update<VEC>(v, int64_t(kt) * TILE, p, M, S, nlh, nll, vb,
-                                                     lane);
+                                                     lane, umax);
                 if (!VEC && hit && p.live_global && lane == 0)
                     atomicOr(&p.live_global[size_t(item) * p.kwords + ((kt - kt0) >> 5)],
                              1u << ((kt - kt0) & 31));
@@ -426,11 +440,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
     // phase-2 (SCREEN) / VEC-at-fixed-potentials key tile sequence
     auto first_kt = [&](int unit, int kt0, int kt1) {
         if constexpr (SCREEN) return next_live(kt0, kt0, kt1);
-        return (VEC && p.live_in) ? live_in_next(p, unit, kt0, kt1) : kt0;
+        return p.live_in ? live_in_next(p, unit, kt0, kt1) : kt0;
     };
     auto next_kt = [&](int unit, int kt, int kt0, int kt1) {
         if constexpr (SCREEN) return next_live(kt + 1, kt0, kt1);
-        return (VEC && p.live_in) ? live_in_next(p, unit, kt + 1, kt1) : kt + 1;
+        return p.live_in ? live_in_next(p, unit, kt + 1, kt1) : kt + 1;
     };
 
     if (warp == 0) {
@@ -560,6 +574,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
 
             float M = -INFINITY;
             double S = 0.0;
+            int best_kt = -1;
             float nlh = 0.0f, nll = 0.0f;
             if constexpr (VEC) {
                 const bool live = t < nq && row < p.R;
@@ -628,11 +643,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 __syncwarp();
                 if (lane == 0) mbar_arrive(accempty(t));
                 ++acc_n;
+                const float M_old = M;
+                float umax;
                 const bool hit = k1_tile_update<VEC>(v, int64_t(kt) * TILE, p, M, S, nlh, nll, vb,
-                                                     lane);
+                                                     lane, umax);
                 if (!VEC && !SCREEN && hit && p.live_global && lane == 0)
                     atomicOr(&p.live_global[size_t(item) * p.kwords + ((kt - kt0) >> 5)],
                              1u << ((kt - kt0) & 31));
+                if constexpr (!VEC) {
+                    if (M > M_old) best_kt = kt;
+                    if (p.gap) {
+                        float gv = row < p.R ? umax - M : -INFINITY;
+                        for (int off = 16; off >= 1; off >>= 1)
+                            gv = fmaxf(gv, __shfl_xor_sync(0xffffffffu, gv, off));
+                        if (lane == 0)
+                            atomicMax(&p.gap[size_t(unit) * p.k_tiles + kt], fenc(gv));
+                    }
+                }
             }
             if constexpr (SCREEN) {
                 mbar_wait(bits_free, lu & 1);
@@ -646,6 +673,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 } else {
                     p.part_m[size_t(split) * p.R + row] = double(M) * 0.69314718055994530942;
                     p.part_s[size_t(split) * p.R + row] = S;
+                    if (p.part_arg) p.part_arg[size_t(split) * p.R + row] = best_kt;
                 }
             }
         }
@@ -1355,12 +1383,19 @@ __global__ void tc_grad_finalize_kernel(const float* __restrict__ part_o, int sp
 
 __global__ void tc_finalize_kernel(const double* __restrict__ pm, const double* __restrict__ ps,
                                    int splits, int64_t R, int64_t row_begin, int64_t row_end,
-                                   FinalizeArgs<float> a) {
+                                   FinalizeArgs<float> a, const int* __restrict__ part_arg,
+                                   int* __restrict__ argtile) {
     const int64_t i = row_begin + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     double vsum = 0.0;
     if (i < row_end) {
         double M = -INFINITY;
-        for (int k = 0; k < splits; ++k) M = fmax(M, pm[size_t(k) * R + i]);
+        int kbest = 0;
+        for (int k = 0; k < splits; ++k)
+            if (pm[size_t(k) * R + i] > M) {
+                M = pm[size_t(k) * R + i];
+                kbest = k;
+            }
+        if (argtile) argtile[i] = part_arg[size_t(kbest) * R + i];
         double S = 0.0;
         for (int k = 0; k < splits; ++k) {
             const double mk = pm[size_t(k) * R + i];
@@ -1427,17 +1462,24 @@ __global__ void build_split_image(const float* __restrict__ pts, int64_t R, int6
 }
 
 // bias chunk: b_j 2^-E = 2048 p0 + p1 + p2 / 2048, b_j = log2(e) (pot_j / eps + log w_j)
+// bias chunk: b_j 2^-E = 2048 p0 + p1 + p2 / 2048, b_j = log2(e) (pot_j / eps + log w_j).
+// Warm-bound bookkeeping (all nullable): bcur[j] = b_j (log2 units) and, against
+// bprev (the previous LSE pass's bias of this side), the per-key-tile max / min of
+// b_j - bprev_j (tile_dmax / tile_dmin, ordered-int encoded). 256 threads = 2 tiles.
 __global__ void build_bias(const float* __restrict__ pot, const float* __restrict__ logw,
                            int64_t C, int64_t rows_padded, double eps, double inv_scale,
-                           uint8_t* __restrict__ img, int* flags) {
+                           uint8_t* __restrict__ img, int* flags, float* __restrict__ bcur,
+                           const float* __restrict__ bprev, int* __restrict__ tile_dmax,
+                           int* __restrict__ tile_dmin) {
+    __shared__ float smax[8], smin[8];
     const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (j >= rows_padded) return;
     __align__(16) __half pc[16];
 #pragma unroll
     for (int e = 0; e < 16; ++e) pc[e] = __float2half_rn(0.0f);
+    float dmax = -INFINITY, dmin = INFINITY;
     if (j < C) {
-        const double b =
-            1.4426950408889634074 * (double(pot[j]) / eps + double(logw[j])) * inv_scale;
+        const double bl = 1.4426950408889634074 * (double(pot[j]) / eps + double(logw[j]));
+        const double b = bl * inv_scale;
         const double p0 = double(__half2float(__double2half(b / 2048.0)));
         const double r1 = b - 2048.0 * p0;
         const double p1 = double(__half2float(__double2half(r1)));
@@ -1446,13 +1488,104 @@ __global__ void build_bias(const float* __restrict__ pot, const float* __restric
         pc[1] = __double2half(p1);
         pc[2] = __double2half(r2);
         if (!isfinite(b) || fabs(b) > 1.3e8) atomicOr(flags, kFlagNonFinitePotential);
+        if (bcur) bcur[j] = float(bl);
+        if (bprev) {
+            // float rounding of the two stored values: widen by their ulps
+            const float dl = float(bl - double(bprev[j]));
+            const float slack = 1e-6f * (fabsf(float(bl)) + fabsf(bprev[j])) + 1e-6f;
+            dmax = dl + slack;
+            dmin = dl - slack;
+        }
     }
-    const int64_t tile = j / TILE;
-    const int r = int(j % TILE);
-    uint8_t* dst = img + size_t(tile) * BIAS + size_t(r) * 32;
-    const int x = (r >> 2) & 1;
-    *reinterpret_cast<uint4*>(dst + ((0 ^ x) << 4)) = *reinterpret_cast<const uint4*>(pc);
-    *reinterpret_cast<uint4*>(dst + ((1 ^ x) << 4)) = *reinterpret_cast<const uint4*>(pc + 8);
+    if (j < rows_padded) {
+        const int64_t tile = j / TILE;
+        const int r = int(j % TILE);
+        uint8_t* dst = img + size_t(tile) * BIAS + size_t(r) * 32;
+        const int x = (r >> 2) & 1;
+        *reinterpret_cast<uint4*>(dst + ((0 ^ x) << 4)) = *reinterpret_cast<const uint4*>(pc);
+        *reinterpret_cast<uint4*>(dst + ((1 ^ x) << 4)) = *reinterpret_cast<const uint4*>(pc + 8);
+    }
+    if (bprev) {
+        for (int off = 16; off >= 1; off >>= 1) {
+            dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, off));
+            dmin = fminf(dmin, __shfl_xor_sync(0xffffffffu, dmin, off));
+        }
+        const int w = threadIdx.x >> 5;
+        if ((threadIdx.x & 31) == 0) {
+            smax[w] = dmax;
+            smin[w] = dmin;
+        }
+        __syncthreads();
+        if (threadIdx.x < 2) {  // tile (threadIdx.x) of this block: warps 4t .. 4t+3
+            const int64_t tile = (int64_t(blockIdx.x) * blockDim.x) / TILE + threadIdx.x;
+            if (tile * TILE < rows_padded) {
+                float mx = -INFINITY, mn = INFINITY;
+                for (int k = 0; k < 4; ++k) {
+                    mx = fmaxf(mx, smax[4 * threadIdx.x + k]);
+                    mn = fminf(mn, smin[4 * threadIdx.x + k]);
+                }
+                tile_dmax[tile] = fenc(mx);
+                tile_dmin[tile] = fenc(mn);
+            }
+        }
+    }
+}
+
+// lambda_u = min over the rows of unit u (2 query tiles) of the smallest bias change
+// in the key tile that held the row's max in the previous pass: M_i^new >=
+// M_i^old + lambda_u (the old argmax key is still there, shifted by its bias change)
+__global__ void warm_lambda_kernel(const int* __restrict__ argtile, const int* __restrict__ tile_dmin,
+                                   int64_t row_begin, int64_t row_end, int q_tile_begin,
+                                   int* __restrict__ lam) {
+    const int64_t i = row_begin + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= row_end) return;
+    const int a = argtile[i];
+    const float v = a >= 0 ? fdec(tile_dmin[a]) : -INFINITY;
+    const int u = int(i / TILE - q_tile_begin) >> 1;
+    atomicMin(&lam[u], fenc(v));
+}
+
+__global__ void fill_int_kernel(int* __restrict__ p, int64_t n, int v) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+
+// Propagate the per-(unit, key tile) gap bounds E = max_i (tilemax_i - M_i) to the
+// new bias: E' = E + max_tile(db) - lambda_u. Blocks with E' < -(64 + 1) are
+// provably below 2^-64 of every row's max and stay out of the live set (E <- E');
+// live blocks get E <- -inf for the pass to re-measure. One thread per bitmask
+// word (u, split, w) of the pass's live_in layout.
+__global__ void warm_prepass_kernel(int* __restrict__ gap, const int* __restrict__ tile_dmax,
+                                    const int* __restrict__ lam, int units, int k_tiles, int splits,
+                                    int kps, int kwords, uint32_t* __restrict__ live,
+                                    unsigned long long* __restrict__ live_count) {
+    const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t total = int64_t(units) * splits * kwords;
+    if (gid >= total) return;
+    const int w = int(gid % kwords);
+    const int s = int((gid / kwords) % splits);
+    const int u = int(gid / (int64_t(kwords) * splits));
+    const float lu = fdec(lam[u]);
+    const int kt_end = min(k_tiles, (s + 1) * kps);
+    uint32_t bits = 0;
+    int nlive = 0;
+    for (int b = 0; b < 32; ++b) {
+        const int kt = s * kps + w * 32 + b;
+        if (w * 32 + b >= kps || kt >= kt_end) break;
+        int* g = gap + size_t(u) * k_tiles + kt;
+        const float e = fdec(*g) + fdec(tile_dmax[kt]) - lu;
+        const bool dead = e < -(kSkipLog2 + 1.0f);   // NaN -> live
+        if (dead) {
+            *g = fenc(e);
+        } else {
+            *g = fenc(-INFINITY);
+            bits |= 1u << b;
+            ++nlive;
+        }
+    }
+    live[gid] = bits;
+    if (live_count && nlive) atomicAdd(live_count, (unsigned long long)nlive);
 }
 
 __global__ void absmax_kernel(const float* __restrict__ x, int64_t n, unsigned int* out) {
@@ -1559,6 +1692,17 @@ struct TcHalfStep::Impl {
     int live_splits[2] = {1, 1}, live_kps[2] = {1, 1}, live_kwords[2] = {1, 1};
     int64_t live_row_begin[2] = {0, 0}, live_row_end[2] = {0, 0};
     const float* live_kpot[2] = {nullptr, nullptr};  // potentials the live set belongs to
+    // warm bounds across LSE passes (d <= 64), per side: the bias of the last pass
+    // (double-buffered), per-key-tile bias-change range, gap bounds per (unit, key
+    // tile), the key tile of each row's max
+    DevBuf<float> bval[2][2];
+    int bcur[2] = {0, 0};
+    bool b_valid[2] = {false, false};
+    DevBuf<int> tdmax[2], tdmin[2], gap[2], argtile[2], part_arg[2], lam[2];
+    DevBuf<uint32_t> warm_live[2];
+    bool warm_ok[2] = {false, false}, last_warm_track[2] = {false, false};
+    int64_t warm_rb[2] = {0, 0}, warm_re[2] = {0, 0};
+    unsigned long long warm_blocks = 0;
     ~Impl() {
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
@@ -1584,6 +1728,22 @@ unsigned long long TcHalfStep::live_tiles() const {
 }
 
 unsigned long long TcHalfStep::screened_blocks() const { return impl_->screened_blocks; }
+
+double TcHalfStep::live_set_fraction(int side) const {
+    const Impl& I = *impl_;
+    if (!I.live_valid[side]) return -1.0;
+    const int kc = side == 0 ? 1 : 0, qc = 1 - kc;
+    const int k_tiles = int(I.rows_pad[kc] / TILE);
+    const int64_t q_tiles = (I.live_row_end[side] + TILE - 1) / TILE - I.live_row_begin[side] / TILE;
+    const int64_t units = (q_tiles + 1) / 2;
+    std::vector<uint32_t> h(size_t(units * I.live_splits[side] * I.live_kwords[side]));
+    FSKB_CUDA(cudaDeviceSynchronize());
+    FSKB_CUDA(cudaMemcpy(h.data(), I.live_glob[side].get(), h.size() * 4, cudaMemcpyDeviceToHost));
+    uint64_t bits = 0;
+    for (uint32_t w : h) bits += uint64_t(__builtin_popcount(w));
+    (void)qc;
+    return double(bits) / (double(units) * double(k_tiles));
+}
 
 void TcHalfStep::poll_screen(int side) {
     Impl& I = *impl_;
@@ -1641,6 +1801,7 @@ TcHalfStep::~TcHalfStep() { delete impl_; }
 
 void TcHalfStep::set_eps(DevProblem<float>& P, double eps) {
     impl_->eps = eps;
+    for (int side = 0; side < 2; ++side) impl_->warm_ok[side] = impl_->b_valid[side] = false;
     const double c = 2.0 * P.fscale / eps * 1.4426950408889634074;
     // screening threshold: |t - t~| <= delta = 2^-10 (1 + 2^-11) ||x|| ||c y|| (the
     // dropped cross terms, Cauchy-Schwarz) -> thr = 64 + 2 delta + 8 (fp32 slack)
@@ -1688,10 +1849,26 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
     const DevSide<float>& ks = side == 0 ? P.tgt : P.src;
     const int E = I.eq[qc] + I.ek[side];
     const int k_tiles = int(I.rows_pad[kc] / TILE);
+    // warm bounds: LSE passes of the d <= 64 kernel (FSK_WARM=0 disables)
+    const char* wenv = std::getenv("FSK_WARM");
+    const bool warm_track =
+        !vec && I.chunks == 1 && !break_lse_flag() && !(wenv && wenv[0] == '0');
+    I.last_warm_track[side] = warm_track;
+    const int n_ktiles = int(I.rows_pad[kc] / TILE);
+    if (warm_track) {
+        for (auto& b : I.bval[side])
+            if (b.size() < size_t(I.rows_pad[kc])) b.alloc(size_t(I.rows_pad[kc]), P.s);
+        if (I.tdmax[side].size() < size_t(n_ktiles)) {
+            I.tdmax[side].alloc(size_t(n_ktiles), P.s);
+            I.tdmin[side].alloc(size_t(n_ktiles), P.s);
+        }
+    }
     // per-pass bias chunk (bit-identical scores for the same potentials)
     build_bias<<<unsigned((I.rows_pad[kc] + 255) / 256), 256, 0, P.s>>>(
         kpot, ks.logw.get(), ks.n, I.rows_pad[kc], double(eps), std::ldexp(1.0, -E),
-        I.kbias[side].get(), flags);
+        I.kbias[side].get(), flags, warm_track ? I.bval[side][I.bcur[side]].get() : nullptr,
+        warm_track && I.b_valid[side] ? I.bval[side][I.bcur[side] ^ 1].get() : nullptr,
+        warm_track ? I.tdmax[side].get() : nullptr, warm_track ? I.tdmin[side].get() : nullptr);
     FSKB_CUDA(cudaGetLastError());
     count_launch();
 
@@ -1731,6 +1908,50 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
     p.screen_thr = I.screen_thr[side];
     bool screen = !vec && I.chunks == 1 && p.screen_thr > 0.0f && kps <= kMaxScreenTiles &&
                   !p.break_lse;
+    if (warm_track) {
+        // warm bounds replace the 5-MMA screen: the previous pass's gaps, moved by the
+        // bias change, decide the live blocks without any extra GEMM
+        screen = false;
+        const int kw = (kps + 31) / 32;
+        const size_t gsz = size_t(units) * size_t(n_ktiles);
+        if (I.gap[side].size() < gsz) I.gap[side].alloc(gsz, P.s);
+        if (I.argtile[side].size() < size_t(p.R)) I.argtile[side].alloc(size_t(p.R), P.s);
+        if (I.part_arg[side].size() < size_t(p.splits) * size_t(p.R))
+            I.part_arg[side].alloc(size_t(p.splits) * size_t(p.R), P.s);
+        const bool warm = I.warm_ok[side] && I.b_valid[side] && I.warm_rb[side] == row_begin &&
+                          I.warm_re[side] == row_end;
+        if (warm) {
+            if (I.lam[side].size() < size_t(units)) I.lam[side].alloc(size_t(units), P.s);
+            fill_int_kernel<<<64, 256, 0, P.s>>>(I.lam[side].get(), units, 0x7F800000);
+            warm_lambda_kernel<<<unsigned((row_end - row_begin + 255) / 256), 256, 0, P.s>>>(
+                I.argtile[side].get(), I.tdmin[side].get(), row_begin, row_end, p.q_tile_begin,
+                I.lam[side].get());
+            const size_t words = size_t(units) * p.splits * kw;
+            if (I.warm_live[side].size() < words) I.warm_live[side].alloc(words, P.s);
+            if (!I.live_count.get()) {
+                I.live_count.alloc(2, P.s);
+                I.live_count.zero();
+            }
+            warm_prepass_kernel<<<unsigned((words + 255) / 256), 256, 0, P.s>>>(
+                I.gap[side].get(), I.tdmax[side].get(), I.lam[side].get(), units, n_ktiles,
+                p.splits, kps, kw, I.warm_live[side].get(), nullptr);
+            FSKB_CUDA(cudaGetLastError());
+            count_launch(3);
+            p.live_in = I.warm_live[side].get();
+            p.in_splits = p.splits;
+            p.in_kps = kps;
+            p.in_kwords = kw;
+            I.warm_blocks += 1;
+        } else {
+            // cold pass: every block is scored and re-measured
+            fill_int_kernel<<<256, 256, 0, P.s>>>(I.gap[side].get(), int64_t(gsz),
+                                                  int(0x807FFFFF));  // fenc(-inf)
+            FSKB_CUDA(cudaGetLastError());
+            count_launch();
+        }
+        p.gap = I.gap[side].get();
+        p.part_arg = I.part_arg[side].get();
+    }
     if (screen) {
         poll_screen(side);
         if (I.pending[side]) {
@@ -1804,10 +2025,20 @@ void TcHalfStep::run(DevProblem<float>& P, int side, const float* kpot, float ep
     const int64_t R = side == 0 ? P.src.n : P.tgt.n;
     FinalizeArgs<float> fb = fa;
     fb.break_lse = break_lse_flag() ? 1 : 0;
+    Impl& I = *impl_;
+    const bool warm = I.last_warm_track[side];
     tc_finalize_kernel<<<unsigned((rows + 255) / 256), 256, 0, P.s>>>(
-        pm.get(), ps.get(), splits, R, row_begin, row_end, fb);
+        pm.get(), ps.get(), splits, R, row_begin, row_end, fb,
+        warm ? I.part_arg[side].get() : nullptr, warm ? I.argtile[side].get() : nullptr);
     FSKB_CUDA(cudaGetLastError());
     count_launch();
+    if (warm) {
+        I.warm_ok[side] = true;
+        I.warm_rb[side] = row_begin;
+        I.warm_re[side] = row_end;
+        I.b_valid[side] = true;
+        I.bcur[side] ^= 1;
+    }
 }
 
 void TcHalfStep::vec(DevProblem<float>& P, int side, const float* kpot, float eps,
@@ -1837,7 +2068,7 @@ void TcHalfStep::apply_mat(DevProblem<float>& P, int side, const float* kpot, fl
     const int k_tiles = int(I.rows_pad[kc] / TILE);
     build_bias<<<unsigned((I.rows_pad[kc] + 255) / 256), 256, 0, P.s>>>(
         kpot, ks.logw.get(), ks.n, I.rows_pad[kc], double(eps), std::ldexp(1.0, -E),
-        I.kbias[side].get(), flags);
+        I.kbias[side].get(), flags, nullptr, nullptr, nullptr, nullptr);
     FSKB_CUDA(cudaGetLastError());
     count_launch();
     // V's own split image, [key tile][64-column chunk][hi | lo], scaled by 2^-ev

@@ -31,6 +31,9 @@ public:
     // phase 2 of screened passes, and blocks those passes covered.
     unsigned long long live_tiles() const;
     unsigned long long screened_blocks() const;
+    // Fraction of (query tile pair, key tile) blocks in the live set of the last
+    // LSE pass of `side` (-1 when none is recorded); synchronizes the device.
+    double live_set_fraction(int side) const;
 
     // (Re)builds the scaled key images for this eps (O((n+m) d) work).
     void set_eps(DevProblem<float>& P, double eps);

@@ -284,6 +284,45 @@ def test_single_precision_hvp_matches_fp64(fsk, port, tensor_mode, d):
     assert led.transport_vector_applies == 2 * i32["cg_iters"] + 3
 
 
+def test_warm_bounds_match_cold_passes(fsk):
+    """Warm bounds (gap bounds carried across LSE passes and moved by the bias
+    change) only drop blocks provably < 2^-64 of every row's max: 10 iterations +
+    gradient agree with FSK_WARM=0 / FSK_SCREEN=0 to fp32 rounding."""
+    torch = pytest.importorskip("torch")
+    n = m = 1 << 18
+    d, eps = 64, 0.05
+    z = fsk.rng_normal(1001, (n + m) * d)
+    X, Y = z[: n * d].reshape(n, d), z[n * d:].reshape(m, d)
+    a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+    out = {}
+    for warm in ("1", "0"):
+        os.environ["FSK_WARM"] = warm
+        os.environ["FSK_SCREEN"] = "0"
+        try:
+            eng = fsk.Engine(0, X, a, Y, b, mode="tensor")
+            eng.set_eps(eps)
+            f = torch.empty(n, dtype=torch.float32, device="cuda")
+            g = torch.empty(m, dtype=torch.float32, device="cuda")
+            eng.bind(f.data_ptr(), g.data_ptr())
+            eng.init_potentials()
+            for _ in range(10):
+                eng.half_step(0, 0, n)
+                eng.half_step(1, 0, m)
+            G = torch.empty((n, d), dtype=torch.float32, device="cuda")
+            eng.grad(0, n, G.data_ptr())
+            torch.cuda.synchronize()
+            out[warm] = (f.cpu().numpy(), g.cpu().numpy(), G.cpu().numpy())
+            eng.close()
+        finally:
+            os.environ.pop("FSK_WARM", None)
+            os.environ.pop("FSK_SCREEN", None)
+    fw, gw, Gw = out["1"]
+    fc, gc, Gc = out["0"]
+    assert np.abs(fw - fc).max() <= 1e-6 * max(1.0, np.abs(fc).max())
+    assert np.abs(gw - gc).max() <= 1e-6 * max(1.0, np.abs(gc).max())
+    assert np.abs(Gw - Gc).max() <= 1e-5 * np.abs(Gc).max()
+
+
 def test_screened_lse_matches_unscreened(fsk):
     """The 5-MMA screen only drops tiles whose terms are all < 2^-64 of the row max:
     screened and unscreened f/g updates agree to fp32 rounding. n = m = 2^18 at
@@ -297,6 +336,7 @@ def test_screened_lse_matches_unscreened(fsk):
     out = {}
     for flag in ("1", "0"):
         os.environ["FSK_SCREEN"] = flag  # adaptive screening vs the plain kernel
+        os.environ["FSK_WARM"] = "0"     # (warm bounds replace the screen when on)
         try:
             eng = fsk.Engine(0, X, a, Y, b, mode="tensor")
             eng.set_eps(eps)
@@ -316,6 +356,7 @@ def test_screened_lse_matches_unscreened(fsk):
         out[flag] = (f.cpu().numpy(), g.cpu().numpy(), eng.live_tiles(), eng.screened_blocks(),
                      G.cpu().numpy())
         eng.close()
+        os.environ.pop("FSK_WARM", None)
     fs, gs, live, blocks, Gs = out["1"]
     fu, gu, live_u, blocks_u, Gu = out["0"]
     assert np.abs(Gs - Gu).max() <= 1e-5 * np.abs(Gu).max()
