@@ -513,11 +513,12 @@ def run_b200(args, cfgname):
         "e2e": e2e,
     }
     if tensor and chunks == 1:
-        # adaptive screening: of the (query tile pair, key tile) blocks of the screened
-        # LSE passes, the fraction scored in full after the 5-MMA hi x hi screen (the
-        # rest are provably < 2^-64 of every row's max)
-        line["screen"] = {"screened_blocks": sblk, "live_blocks": live,
-                          "live_fraction": live / sblk if sblk else None}
+        # block skipping in the LSE passes (warm bounds across passes, or the 5-MMA
+        # screen): of the (query tile pair, key tile) blocks of the passes whose live
+        # count was read back, the fraction scored in full; the rest are provably
+        # < 2^-64 of every row's max
+        line["block_skipping"] = {"tracked_blocks": sblk, "live_blocks": live,
+                                  "live_fraction": live / sblk if sblk else None}
     if world == 1 and args.cpu_baseline:
         try:
             cb = reference_sample(cfgname)

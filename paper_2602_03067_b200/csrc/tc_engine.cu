@@ -1715,6 +1715,10 @@ struct TcHalfStep::Impl {
 // cfg2 65536^2: 99.9% live, 2.24 vs 1.42 ms. Passes with a high measured live
 // fraction run unscreened and re-probe after an exponentially growing backoff.
 constexpr double kScreenMaxLive = 0.45;
+// Warm bounds cost a gap atomic per (warp, block) and a prepass; they pay while a
+// clear minority of blocks stays live (cfg3: ~11% live, 129 vs 264 ms per
+// half-step; cfg2: ~100% live, 1.82 vs 1.53 ms) - same async probe / backoff.
+constexpr double kWarmMaxLive = 0.7;
 
 bool TcHalfStep::supported(int64_t d) { return d >= 1 && d <= 64 * 64; }
 int TcHalfStep::chunks() const { return impl_->chunks; }
@@ -1722,8 +1726,8 @@ int TcHalfStep::chunks() const { return impl_->chunks; }
 unsigned long long TcHalfStep::live_tiles() const {
     for (int side = 0; side < 2; ++side)
         if (impl_->pending[side]) FSKB_CUDA(cudaEventSynchronize(impl_->ev[side]));
-    const_cast<TcHalfStep*>(this)->poll_screen(0);
-    const_cast<TcHalfStep*>(this)->poll_screen(1);
+    const_cast<TcHalfStep*>(this)->poll_screen(0, kScreenMaxLive);
+    const_cast<TcHalfStep*>(this)->poll_screen(1, kScreenMaxLive);
     return impl_->live_total;
 }
 
@@ -1745,7 +1749,7 @@ double TcHalfStep::live_set_fraction(int side) const {
     return double(bits) / (double(units) * double(k_tiles));
 }
 
-void TcHalfStep::poll_screen(int side) {
+void TcHalfStep::poll_screen(int side, double max_live) {
     Impl& I = *impl_;
     if (!I.pending[side] || cudaEventQuery(I.ev[side]) != cudaSuccess) return;
     const double live = double(I.h_live[side]);
@@ -1753,7 +1757,7 @@ void TcHalfStep::poll_screen(int side) {
     I.screened_blocks += (unsigned long long)I.pending_blocks[side];
     I.live_est[side] = live / std::max(1.0, I.pending_blocks[side]);
     I.pending[side] = false;
-    if (I.live_est[side] >= kScreenMaxLive) {
+    if (I.live_est[side] >= max_live) {
         I.skip_left[side] = I.backoff[side];
         I.backoff[side] = std::min(I.backoff[side] * 2, 1 << 12);
     } else {
@@ -1851,8 +1855,13 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
     const int k_tiles = int(I.rows_pad[kc] / TILE);
     // warm bounds: LSE passes of the d <= 64 kernel (FSK_WARM=0 disables)
     const char* wenv = std::getenv("FSK_WARM");
-    const bool warm_track =
-        !vec && I.chunks == 1 && !break_lse_flag() && !(wenv && wenv[0] == '0');
+    bool warm_track = !vec && I.chunks == 1 && !break_lse_flag() && !(wenv && wenv[0] == '0');
+    if (warm_track && I.live_count.get()) {
+        poll_screen(side, kWarmMaxLive);
+        if (!I.pending[side] && I.live_est[side] >= kWarmMaxLive && I.skip_left[side]-- > 0)
+            warm_track = false;  // mostly live: plain passes until the next probe
+    }
+    if (!warm_track) I.warm_ok[side] = false;
     I.last_warm_track[side] = warm_track;
     const int n_ktiles = int(I.rows_pad[kc] / TILE);
     if (warm_track) {
@@ -1928,15 +1937,21 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
                 I.lam[side].get());
             const size_t words = size_t(units) * p.splits * kw;
             if (I.warm_live[side].size() < words) I.warm_live[side].alloc(words, P.s);
-            if (!I.live_count.get()) {
-                I.live_count.alloc(2, P.s);
-                I.live_count.zero();
-            }
+            const bool track = !I.pending[side];
+            unsigned long long* cnt = track ? I.live_count.get() + side : nullptr;
+            if (track) FSKB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), P.s));
             warm_prepass_kernel<<<unsigned((words + 255) / 256), 256, 0, P.s>>>(
                 I.gap[side].get(), I.tdmax[side].get(), I.lam[side].get(), units, n_ktiles,
-                p.splits, kps, kw, I.warm_live[side].get(), nullptr);
+                p.splits, kps, kw, I.warm_live[side].get(), cnt);
             FSKB_CUDA(cudaGetLastError());
             count_launch(3);
+            if (track) {  // live fraction of this pass, read back without a host sync
+                FSKB_CUDA(cudaMemcpyAsync(I.h_live + side, cnt, sizeof(unsigned long long),
+                                          cudaMemcpyDeviceToHost, P.s));
+                FSKB_CUDA(cudaEventRecord(I.ev[side], P.s));
+                I.pending[side] = true;
+                I.pending_blocks[side] = double(units) * double(n_ktiles);
+            }
             p.live_in = I.warm_live[side].get();
             p.in_splits = p.splits;
             p.in_kps = kps;
@@ -1953,7 +1968,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         p.part_arg = I.part_arg[side].get();
     }
     if (screen) {
-        poll_screen(side);
+        poll_screen(side, kScreenMaxLive);
         if (I.pending[side]) {
             screen = I.live_est[side] < kScreenMaxLive;  // last estimate still in flight
         } else if (I.live_est[side] >= kScreenMaxLive) {

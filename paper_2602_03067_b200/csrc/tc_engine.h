@@ -73,7 +73,7 @@ public:
                    float* out, int* flags, const float* A = nullptr);
 
 private:
-    void poll_screen(int side);
+    void poll_screen(int side, double max_live);
     int pass(DevProblem<float>& P, int side, const float* kpot, float eps, int64_t row_begin,
              int64_t row_end, const float* const* vec, int* flags, DevBuf<double>& pm,
              DevBuf<double>& ps);
