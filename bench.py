@@ -409,8 +409,12 @@ def run_b200(args, cfgname):
     e2e = None
     if args.e2e:
         if world == 1:
-            t0 = time.perf_counter()
             want_grad = STEP_TAIL[cfgname] == "grad"
+            # one untimed call first (lazy module loading, allocator warm-up), as the
+            # device-resident arm gets its warmup steps
+            fsk.sinkhorn_solve(X, a, Y, b, eps=eps, max_iters=iters, precision="single",
+                               grad=want_grad)
+            t0 = time.perf_counter()
             out = fsk.sinkhorn_solve(X, a, Y, b, eps=eps, max_iters=iters, precision="single",
                                      grad=want_grad)
             if STEP_TAIL[cfgname] == "hvp":

@@ -1858,8 +1858,12 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
     bool warm_track = !vec && I.chunks == 1 && !break_lse_flag() && !(wenv && wenv[0] == '0');
     if (warm_track && I.live_count.get()) {
         poll_screen(side, kWarmMaxLive);
-        if (!I.pending[side] && I.live_est[side] >= kWarmMaxLive && I.skip_left[side]-- > 0)
-            warm_track = false;  // mostly live: plain passes until the next probe
+        // mostly live at the last measurement (possibly still in flight for a newer
+        // pass): plain passes until the backoff expires, then a probe
+        if (I.live_est[side] >= kWarmMaxLive && I.skip_left[side] > 0) {
+            --I.skip_left[side];
+            warm_track = false;
+        }
     }
     if (!warm_track) I.warm_ok[side] = false;
     I.last_warm_track[side] = warm_track;
