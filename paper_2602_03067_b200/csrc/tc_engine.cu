@@ -1856,10 +1856,15 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
     // warm bounds: LSE passes of the d <= 64 kernel (FSK_WARM=0 disables)
     const char* wenv = std::getenv("FSK_WARM");
     bool warm_track = !vec && I.chunks == 1 && !break_lse_flag() && !(wenv && wenv[0] == '0');
+    // small problems: the bookkeeping would not pay (and the probe read-back waits)
+    const int64_t q_units = ((row_end + TILE - 1) / TILE - row_begin / TILE + 1) / 2;
+    if (q_units * int64_t(n_ktiles) < (int64_t(1) << 16)) warm_track = false;
     if (warm_track && I.live_count.get()) {
+        // the probe of the previous tracked pass: wait for it (one pass of host/device
+        // pipeline, ~0.1% at these sizes) so the decision is never stale
+        if (I.pending[side]) FSKB_CUDA(cudaEventSynchronize(I.ev[side]));
         poll_screen(side, kWarmMaxLive);
-        // mostly live at the last measurement (possibly still in flight for a newer
-        // pass): plain passes until the backoff expires, then a probe
+        // mostly live: plain passes until the backoff expires, then a probe
         if (I.live_est[side] >= kWarmMaxLive && I.skip_left[side] > 0) {
             --I.skip_left[side];
             warm_track = false;
