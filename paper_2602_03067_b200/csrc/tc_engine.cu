@@ -1858,7 +1858,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
     bool warm_track = !vec && I.chunks == 1 && !break_lse_flag() && !(wenv && wenv[0] == '0');
     // small problems: the bookkeeping would not pay (and the probe read-back waits)
     const int64_t q_units = ((row_end + TILE - 1) / TILE - row_begin / TILE + 1) / 2;
-    if (q_units * int64_t(n_ktiles) < (int64_t(1) << 16)) warm_track = false;
+    if (q_units * (I.rows_pad[kc] / TILE) < (int64_t(1) << 16)) warm_track = false;
     if (warm_track && I.live_count.get()) {
         // the probe of the previous tracked pass: wait for it (one pass of host/device
         // pipeline, ~0.1% at these sizes) so the decision is never stale
