@@ -1715,10 +1715,12 @@ struct TcHalfStep::Impl {
 // cfg2 65536^2: 99.9% live, 2.24 vs 1.42 ms. Passes with a high measured live
 // fraction run unscreened and re-probe after an exponentially growing backoff.
 constexpr double kScreenMaxLive = 0.45;
-// Warm bounds cost a gap atomic per (warp, block) and a prepass; they pay while a
-// clear minority of blocks stays live (cfg3: ~11% live, 129 vs 264 ms per
-// half-step; cfg2: ~100% live, 1.82 vs 1.53 ms) - same async probe / backoff.
-constexpr double kWarmMaxLive = 0.7;
+// Warm bounds cost a gap atomic per (warp, block) and a prepass (~15% of a pass
+// when nothing can be skipped: cfg2, 99.8% live, 1.79 vs 1.53 ms) and pay off
+// steeply as blocks die (cfg3: the first passes after a restart are 60-90% live,
+// later ones ~10%; 127 vs 333 ms per half-step). Only a pass that finds nearly
+// everything live backs off (async probe, exponential backoff).
+constexpr double kWarmMaxLive = 0.95;
 
 bool TcHalfStep::supported(int64_t d) { return d >= 1 && d <= 64 * 64; }
 int TcHalfStep::chunks() const { return impl_->chunks; }
