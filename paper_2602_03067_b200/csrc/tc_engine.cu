@@ -1684,7 +1684,7 @@ struct TcHalfStep::Impl {
     bool pending[2] = {false, false};
     double pending_blocks[2] = {0.0, 0.0};
     double live_est[2] = {0.0, 0.0};         // 0 -> screen the first pass (probe)
-    int skip_left[2] = {0, 0}, backoff[2] = {8, 8};
+    int skip_left[2] = {0, 0}, backoff[2] = {8, 8}, high_run[2] = {0, 0};
     unsigned long long live_total = 0, screened_blocks = 0;
     // live set of the last LSE pass per side (valid when that pass was screened)
     DevBuf<uint32_t> live_glob[2];
@@ -1759,10 +1759,16 @@ void TcHalfStep::poll_screen(int side, double max_live) {
     I.screened_blocks += (unsigned long long)I.pending_blocks[side];
     I.live_est[side] = live / std::max(1.0, I.pending_blocks[side]);
     I.pending[side] = false;
+    // back off only after 3 consecutive mostly-live probes: the passes right after a
+    // restart (fresh potentials) are mostly live even when the plan concentrates
     if (I.live_est[side] >= max_live) {
-        I.skip_left[side] = I.backoff[side];
-        I.backoff[side] = std::min(I.backoff[side] * 2, 1 << 12);
+        if (++I.high_run[side] >= 3) {
+            I.high_run[side] = 0;
+            I.skip_left[side] = I.backoff[side];
+            I.backoff[side] = std::min(I.backoff[side] * 2, 1 << 12);
+        }
     } else {
+        I.high_run[side] = 0;
         I.backoff[side] = 8;
     }
 }
@@ -1867,7 +1873,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         if (I.pending[side]) FSKB_CUDA(cudaEventSynchronize(I.ev[side]));
         poll_screen(side, kWarmMaxLive);
         // mostly live: plain passes until the backoff expires, then a probe
-        if (I.live_est[side] >= kWarmMaxLive && I.skip_left[side] > 0) {
+        if (I.skip_left[side] > 0) {
             --I.skip_left[side];
             warm_track = false;
         }
