@@ -469,10 +469,19 @@ def run_b200(args, cfgname):
     hs = sorted(half_ms)
     med_half = hs[len(hs) // 2] / 1e3
     w_dot = 2.0 * rows0 * m * d
-    achieved = w_dot / med_half / 1e12
     sm_clk = (clocks or {}).get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)
     tensor = eng.path.startswith("tcgen05")
     chunks = -(-d // 64)
+    # block skipping (warm bounds / screen): the kernel scores only the blocks it
+    # cannot prove negligible. Executed fraction over the timed LSE passes: the
+    # live blocks of the passes whose live count was read back, plus every block
+    # of the untracked (cold / plain) passes.
+    passes = args.steps * (2 * iters + (1 if STEP_TAIL[cfgname] == "grad" else 0))
+    blocks_pass = -(-rows0 // 256) * -(-m // 128)
+    total_blocks = passes * blocks_pass
+    executed = min(1.0, (live + max(0, total_blocks - sblk)) / total_blocks) if total_blocks \
+        else 1.0
+    achieved = executed * w_dot / med_half / 1e12
     if tensor:
         mode_factor = (12 * chunks + 1) / (4.0 * chunks) * (64.0 * chunks / d)
         peak_raw = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
@@ -508,7 +517,9 @@ def run_b200(args, cfgname):
                      "kernel": kernel + " (+bias/finalize; CUDA events around each f half-step "
                                "on the launching stream)",
                      "algorithmic": f"W_dot = 2 n m d per half-step (n_rows={rows0}, m={m}, "
-                                    f"d={d})",
+                                    f"d={d}) x executed block fraction {executed:.3f}",
+                     "executed_fraction": executed,
+                     "effective_tflops": w_dot / med_half / 1e12,
                      "peak_source": peak_src,
                      "exp_floor_ms": exp_floor * 1e3,
                      "mode_floor_ms": w_dot / (peak * 1e12) * 1e3},
