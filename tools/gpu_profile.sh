@@ -15,7 +15,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_l
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_apply -c 1 \
   -o "$OUT/k3" python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline \
   > "$OUT/ncu_k3.log" 2>&1; echo "k3 rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_lse_kernel -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_lse_chunked -c 1 \
   -o "$OUT/k1c" python bench.py --config cfg4 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline \
   > "$OUT/ncu_k1c.log" 2>&1; echo "k1c rc=$?"
 ls -la "$OUT"
