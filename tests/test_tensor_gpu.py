@@ -490,3 +490,26 @@ def test_engine_iterate_graph_matches_loop(fsk):
         eng.close()
     for fr, gr in res[1:]:
         assert np.array_equal(fr, res[0][0]) and np.array_equal(gr, res[0][1])
+
+
+@pytest.mark.parametrize("n,m,d", [(1, 1, 64), (1, 300, 64), (300, 1, 64), (2, 3, 100), (1, 1, 1024),
+                                   (127, 129, 65)])
+def test_tensor_degenerate_shapes(fsk, port, tensor_mode, n, m, d):
+    """Single-point measures and tile-boundary sizes through the tensor kernels
+    (half-steps both ways and the gradient) against the fp64 oracle."""
+    rng = np.random.default_rng(n * 1000 + m + d)
+    X = rng.normal(size=(n, d)) * 0.5
+    Y = rng.normal(size=(m, d)) * 0.5
+    a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+    g = -(Y ** 2).sum(1)
+    eps = 0.5
+    want = port.update_f_hat(X, a, Y, b, g, eps)
+    got = fsk.update_f_hat_f32(X, a, Y, b, g, eps)
+    assert contract(got, want) <= 1e-5
+    wg = port.update_g_hat(X, a, Y, b, want, eps)
+    gg = fsk.update_g_hat_f32(X, a, Y, b, want, eps)
+    assert contract(gg, wg) <= 1e-5
+    s = fsk.sinkhorn_solve(X, a, Y, b, eps=eps, max_iters=3, precision="single", grad=True)
+    r = port.sinkhorn_solve(X, a, Y, b, eps=eps, max_iters=3, precision="double")
+    assert abs(s["dual_cost"] - r["dual_cost"]) <= 1e-5 * max(1.0, abs(r["dual_cost"]))
+    assert np.all(np.isfinite(s["grad"]))
