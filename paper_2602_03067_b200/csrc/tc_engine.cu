@@ -995,16 +995,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_kernel(const TcApplyP
 // TMEM accumulator pair, bit-identical to the chunked K1 so P~ = 2^(t - L + 12)
 // normalises exactly against that pass's L. P~ is split hi/lo into fp16 over the
 // big accumulator and a second GEMM O += P~ V reads it from TMEM (A operand)
-// against VC <= 2 64-column chunks of V's own split image. p > 128 takes several
-// passes (the score is recomputed per pass; P~ never leaves TMEM).
+// against up to VC = 4 64-column chunks of V's own split image, streamed through
+// the same slot ring after the score chunks. p > 256 takes several passes (the
+// score is recomputed per pass; P~ never leaves TMEM).
 // Hadamard mode ((P (.) A B^T) V, apply_hadamard_plan stream.cpp:359-375): a
 // third split GEMM accumulates W = A B^T per tile in TMEM (B = the key image)
-// and the epilogue splits P~ W 2^-wexp instead of P~; VC = 1 then.
+// and the epilogue splits P~ W 2^-wexp instead of P~; VC <= 2 then.
 // 1 query tile per work item; the epilogue is the 4 lane quarters x 2 column
 // halves of tc_apply_kernel.
-constexpr int G_SLOTS_MAX = 5;
-constexpr uint32_t G_OFF_V_END = 192 * 1024;                    // V region ends here
-constexpr uint32_t G_OFF_BIAS = G_OFF_V_END;                    // 2 x 4 KB bias ring
+constexpr int G_SLOTS_MAX = 6;
+constexpr uint32_t G_OFF_BIAS = G_SLOTS_MAX * QTILE;            // 192 KB: 2 x 4 KB bias ring
 constexpr uint32_t G_OFF_ONES = G_OFF_BIAS + 2 * BIAS;          // 200 KB
 constexpr uint32_t G_OFF_BAR = G_OFF_ONES + BIAS;               // 204 KB
 constexpr uint32_t G_SMEM_BYTES = G_OFF_BAR + 256 + 1024;
@@ -1068,21 +1068,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t* sbase = smem_raw + (base - raw);
     const bool had = p.aimg != nullptr;
-    const int ops = had ? 3 : 2;                     // slots per chunk step
-    const int NS = had ? 5 : 4;                      // ring slots
-    const uint32_t off_v = G_OFF_V_END - uint32_t(had ? 1 : 2) * QTILE;
+    const int ops = had ? 3 : 2;                     // slots per score chunk step
+    const int NS = G_SLOTS_MAX;                      // ring slots (score chunks, then V)
 
     const uint32_t bar0 = base + G_OFF_BAR;
     auto sfull_ = [&](int s) { return bar0 + 8u * s; };
     auto sempty_ = [&](int s) { return bar0 + 8u * (G_SLOTS_MAX + s); };
-    const uint32_t vfull = bar0 + 8u * (2 * G_SLOTS_MAX);
-    const uint32_t vempty = vfull + 8u;
-    auto bfull = [&](int b) { return vfull + 16u + 8u * b; };
-    auto bempty = [&](int b) { return vfull + 32u + 8u * b; };
-    const uint32_t sfull = vfull + 48u;
-    const uint32_t pready = vfull + 56u;
-    const uint32_t ofull = vfull + 64u;
-    const uint32_t oempty = vfull + 72u;
+    const uint32_t bar1 = bar0 + 8u * (2 * G_SLOTS_MAX);
+    auto bfull = [&](int b) { return bar1 + 8u * b; };
+    auto bempty = [&](int b) { return bar1 + 16u + 8u * b; };
+    const uint32_t sfull = bar1 + 32u;
+    const uint32_t pready = bar1 + 40u;
+    const uint32_t ofull = bar1 + 48u;
+    const uint32_t oempty = bar1 + 56u;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + G_OFF_BAR + 192);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1093,8 +1091,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
             mbar_init(sfull_(s), 1);
             mbar_init(sempty_(s), 1);
         }
-        mbar_init(vfull, 1);
-        mbar_init(vempty, 1);
         for (int b = 0; b < 2; ++b) {
             mbar_init(bfull(b), 1);
             mbar_init(bempty(b), 1);
@@ -1144,11 +1140,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
                             bulk_g2s(base + s * QTILE, src[o], QTILE, sfull_(s));
                         }
                     }
-                    mbar_wait(vempty, (vt & 1) ^ 1);
-                    mbar_expect_tx(vfull, p.vc * QTILE);
-                    bulk_g2s(base + off_v,
-                             p.vimg + (size_t(kt) * p.v_chunks + p.v_chunk0) * QTILE,
-                             p.vc * QTILE, vfull);
+                    for (int j = 0; j < p.vc; ++j, ++sq) {
+                        const int s = sq % NS;
+                        mbar_wait(sempty_(s), ((sq / NS) & 1) ^ 1);
+                        mbar_expect_tx(sfull_(s), QTILE);
+                        bulk_g2s(base + s * QTILE,
+                                 p.vimg + (size_t(kt) * p.v_chunks + p.v_chunk0 + j) * QTILE, QTILE,
+                                 sfull_(s));
+                    }
                 }
             }
         }
@@ -1184,10 +1183,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
                     umma_commit(bempty(bb));
                     umma_commit(sfull);
                     mbar_wait(pready, vt & 1);
-                    mbar_wait(vfull, vt & 1);
                     fence_after();
-                    for (int j = 0; j < p.vc; ++j) {
-                        const uint32_t vst = base + off_v + j * QTILE;
+                    for (int j = 0; j < p.vc; ++j, ++sq) {
+                        const int s = sq % NS;
+                        mbar_wait(sfull_(s), (sq / NS) & 1);
+                        fence_after();
+                        const uint32_t vst = base + s * QTILE;
                         const uint32_t o = tmem + G_OCOL + uint32_t(j * DPAD);
 #pragma unroll
                         for (int kk = 0; kk < TILE / 16; ++kk) {
@@ -1198,8 +1199,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
                             umma_ts(o, ph + 32, vh, IDESC_PV, 1u);
                             umma_ts(o, ph, vl, IDESC_PV, 1u);
                         }
+                        umma_commit(sempty_(s));
                     }
-                    umma_commit(vempty);
                     o_first = false;
                 }
                 umma_commit(ofull);
@@ -1291,30 +1292,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
             }
             mbar_wait(ofull, lu & 1);
             fence_after();
-            const int width = p.vc * DPAD;          // 64 or 128 output columns
-            const int per_half = width / 2;         // 32 or 64
-            uint32_t o[64];
-            const uint32_t oaddr = tmem + lane_addr + G_OCOL + uint32_t(half * per_half);
-            FSKB_TMEM_LD32(oaddr, o);
-            if (per_half == 64) FSKB_TMEM_LD32(oaddr + 32, (o + 32));
-            tmem_ld_wait();
+            const int width = p.vc * DPAD;          // 64 .. 256 output columns
+            const int per_half = width / 2;         // 32 .. 128
+            const bool write = row >= p.row_begin && row < p.row_end;
+            float* dst = p.part_o + (size_t(split) * p.R + row) * width + half * per_half;
+            for (int c0 = 0; c0 < per_half; c0 += 32) {
+                uint32_t o[32];
+                FSKB_TMEM_LD32(tmem + lane_addr + G_OCOL + uint32_t(half * per_half + c0), o);
+                tmem_ld_wait();
+                if (!any_tile) {  // no live key tile in this split range: O = 0
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) o[c] = 0u;
+                }
+                if (write) {
+#pragma unroll
+                    for (int c = 0; c < 32; c += 4)
+                        *reinterpret_cast<float4*>(dst + c0 + c) =
+                            make_float4(__uint_as_float(o[c]), __uint_as_float(o[c + 1]),
+                                        __uint_as_float(o[c + 2]), __uint_as_float(o[c + 3]));
+                }
+            }
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(oempty);
-            if (!any_tile) {  // no live key tile in this split range: O = 0
-#pragma unroll
-                for (int c = 0; c < 64; ++c) o[c] = 0u;
-            }
-            if (row >= p.row_begin && row < p.row_end) {
-                float* dst = p.part_o + (size_t(split) * p.R + row) * width + half * per_half;
-#pragma unroll
-                for (int c = 0; c < 64; c += 4) {
-                    if (c >= per_half) break;
-                    *reinterpret_cast<float4*>(dst + c) =
-                        make_float4(__uint_as_float(o[c]), __uint_as_float(o[c + 1]),
-                                    __uint_as_float(o[c + 2]), __uint_as_float(o[c + 3]));
-                }
-            }
         }
     }
     fence_before();
@@ -2163,7 +2163,7 @@ void TcHalfStep::apply_mat(DevProblem<float>& P, int side, const float* kpot, fl
         g.in_kps = I.live_kps[side];
         g.in_kwords = I.live_kwords[side];
     }
-    const int vc_max = A ? 1 : 2;
+    const int vc_max = A ? 2 : 4;
     DevBuf<float> part(size_t(g.splits) * size_t(R) * vc_max * DPAD, P.s);
     g.part_o = part.get();
     for (int v0 = 0; v0 < VC; v0 += vc_max) {
