@@ -24,6 +24,16 @@ using namespace fskb;
 
 namespace {
 
+// host doubles -> device floats without a host conversion pass
+DevBuf<float> narrow_on_device(const double* h, int64_t n, cudaStream_t s) {
+    DevBuf<double> tmp(size_t(n), s);
+    tmp.upload(h, size_t(n));
+    DevBuf<float> out(size_t(n), s);
+    launch_f64_to_f32(tmp.get(), out.get(), n, s);
+    FSKB_CUDA(cudaStreamSynchronize(s));
+    return out;
+}
+
 template <typename T>
 std::vector<T> to_t(const double* p, int64_t n) {
     return std::vector<T>(p, p + n);
@@ -66,28 +76,21 @@ struct HvpCtx {
             // Hadamard: the tensor kernel needs B = the key cloud (true in the HVP)
             const bool had_ok = A && side == 0 && B == tgt.points && r == src.d;
             if (P.tc && ((!A && p > 1) || had_ok)) {
-                DevBuf<float> vd(size_t(cols * p), C.s);
-                const std::vector<float> vf(V.begin(), V.end());
-                vd.upload(vf.data(), size_t(cols * p));
+                // ship the host doubles as they are, narrow / widen on the device
+                DevBuf<float> vd = narrow_on_device(V.data(), cols * p, C.s);
                 DevBuf<float> ad;
-                if (A) {
-                    const std::vector<float> af = to_t<float>(A, src.n * r);
-                    ad.alloc(size_t(src.n * r), C.s);
-                    ad.upload(af.data(), af.size());
-                }
+                if (A) ad = narrow_on_device(A, src.n * r, C.s);
                 DevBuf<float> out(size_t(rows * p), C.s);
                 P.s = C.s;
                 P.tc->apply_mat(P, side, kpot, float(eps), l2h[side], l2l[side], marg[side],
                                 vd.get(), p, out.get(), C.flags, ad.get());
-                std::vector<float> hf((size_t)(rows * p));
-                out.download(hf.data(), hf.size());
+                DevBuf<double> wide(size_t(rows * p), C.s);
+                launch_f32_to_f64(out.get(), wide.get(), rows * p, C.s);
+                wide.download(h.data(), h.size());
                 FSKB_CUDA(cudaStreamSynchronize(C.s));
-                h.assign(hf.begin(), hf.end());
                 done = true;
             } else if (P.tc && !A && p == 1) {
-                DevBuf<float> vd(size_t(cols), C.s);
-                const std::vector<float> vf(V.begin(), V.end());
-                vd.upload(vf.data(), size_t(cols));
+                DevBuf<float> vd = narrow_on_device(V.data(), cols, C.s);
                 DevBuf<double> out(size_t(rows), C.s);
                 P.s = C.s;
                 P.tc->vec(P, side, kpot, float(eps), l2h[side], l2l[side], marg[side], vd.get(),
