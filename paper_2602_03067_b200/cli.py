@@ -105,10 +105,10 @@ def _device_pool_peak_reset():
         import torch
         if not torch.cuda.is_available():
             return None
-        from cuda.bindings import runtime as rt  # cuda-python
+        from cuda.bindings import driver, runtime as rt  # cuda-python
         err, pool = rt.cudaDeviceGetDefaultMemPool(torch.cuda.current_device())
         rt.cudaMemPoolSetAttribute(pool, rt.cudaMemPoolAttr.cudaMemPoolAttrReservedMemHigh,
-                                   rt.cuuint64_t(0))
+                                   driver.cuuint64_t(0))
         return pool
     except Exception:
         return None
