@@ -165,7 +165,8 @@ __device__ __forceinline__ bool k1_tile_update(uint32_t (&v)[128], int64_t kbase
             s0 = fmaf(ex2(fmaf(__uint_as_float(v[j]), p.acc_scale, nlh) + nll), w.x, s0);
             s1 = fmaf(ex2(fmaf(__uint_as_float(v[j + 1]), p.acc_scale, nlh) + nll), w.y, s1);
             s2 = fmaf(ex2(fmaf(__uint_as_float(v[j + 2]), p.acc_scale, nlh) + nll), w.z, s2);
-            s3 = fmaf(ex2(fmaf(__uint_as_float(v[j + 3]), p.acc_scale, nlh) + nll), w.w, s3);
+            const float x3 = fmaf(__uint_as_float(v[j + 3]), p.acc_scale, nlh) + nll;
+            s3 = fmaf(((j >> 2) & 3) != 3 ? ex2_poly(x3) : ex2(x3), w.w, s3);
         }
         S += double((s0 + s1) + (s2 + s3));
         __syncwarp();
@@ -186,7 +187,10 @@ __device__ __forceinline__ bool k1_tile_update(uint32_t (&v)[128], int64_t kbase
             s0 += ex2(fmaf(__uint_as_float(v[j]), p.acc_scale, nm));
             s1 += ex2(fmaf(__uint_as_float(v[j + 1]), p.acc_scale, nm));
             s2 += ex2(fmaf(__uint_as_float(v[j + 2]), p.acc_scale, nm));
-            s3 += ex2(fmaf(__uint_as_float(v[j + 3]), p.acc_scale, nm));
+            // 3 of every 16 exponentials on the FMA pipe: MUFU (16/clk/SM) and the
+            // split-precision MMAs then bound a fully live tile about equally
+            const float x3 = fmaf(__uint_as_float(v[j + 3]), p.acc_scale, nm);
+            s3 += ((j >> 2) & 3) != 3 ? ex2_poly(x3) : ex2(x3);
         }
         S += double((s0 + s1) + (s2 + s3));
         return true;

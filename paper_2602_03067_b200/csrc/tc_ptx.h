@@ -145,6 +145,26 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
+// 2^x on the FMA / ALU pipes (the MUFU unit is the bottleneck of the LSE epilogue
+// when few tiles can be skipped): x = n + f, n = rint(x) by the 1.5 * 2^23 magic
+// add, f in [-1/2, 1/2], degree-6 minimax polynomial (max relative error 9.6e-8
+// with fp32 Horner, vs ~2^-22 for ex2.approx), 2^n added into the exponent field.
+// x is clamped at -125 (2^-125 is far below anything an fp32 sum can register).
+__device__ __forceinline__ float ex2_poly(float x) {
+    x = fmaxf(x, -125.0f);
+    const float t = x + 12582912.0f;
+    const float n = t - 12582912.0f;
+    const float f = x - n;
+    float p = 1.5394332876894623e-4f;
+    p = fmaf(p, f, 1.3388522202149034e-3f);
+    p = fmaf(p, f, 9.618211537599564e-3f);
+    p = fmaf(p, f, 5.550358444452286e-2f);
+    p = fmaf(p, f, 2.4022650718688965e-1f);
+    p = fmaf(p, f, 6.931471824645996e-1f);
+    p = fmaf(p, f, 1.0f);
+    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 // Constant "ones" chunk of the query operand, [2048, 1, 1/2048, 0...] per row
 // (SW32 K-major): multiplies the 3-piece key bias chunk into the score GEMM.
 __device__ __forceinline__ void fill_ones_chunk(uint8_t* dst, int tid, int nthreads) {
