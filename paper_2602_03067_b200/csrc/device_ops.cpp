@@ -1,3 +1,4 @@
+#include <atomic>
 #include "device_ops.h"
 
 #include <climits>
@@ -28,12 +29,29 @@ int num_sms() {
     return n;
 }
 
+// Every DevBuf is a stream-ordered allocation from the device's default pool. Its
+// default release threshold (0) hands freed memory back to the driver at every
+// synchronization, so the next pass re-maps its partial buffers (and a solve its
+// operand images): keep what the pool holds instead. Once per device.
+void configure_device_pool(int device) {
+    static std::atomic<uint64_t> done_mask{0};
+    if (device < 0 || device >= 64 || (done_mask.load() >> device) & 1u) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t keep = ~uint64_t(0);
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done_mask.fetch_or(uint64_t(1) << device);
+}
+
 ExecCtx& exec_ctx() {
     thread_local ExecCtx c;
     if (!c.s) {
         int count = 0;
         if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
             throw CudaFailure("no CUDA device available (the B200 engine has no CPU fallback)");
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess) configure_device_pool(dev);
         FSKB_CUDA(cudaStreamCreateWithFlags(&c.s, cudaStreamNonBlocking));
         FSKB_CUDA(cudaMalloc(reinterpret_cast<void**>(&c.flags), 2 * sizeof(int)));
         c.bad_iter = c.flags + 1;

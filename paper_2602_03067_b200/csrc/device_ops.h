@@ -21,6 +21,9 @@ struct ExecCtx {
     int* bad_iter = nullptr;
 };
 ExecCtx& exec_ctx();
+// Keep freed stream-ordered allocations in the device's default pool (release
+// threshold = max) instead of returning them to the driver at every sync.
+void configure_device_pool(int device);
 int read_and_clear_flags(ExecCtx& c);
 void throw_for_flags(int flags, const std::string& suffix = "");
 

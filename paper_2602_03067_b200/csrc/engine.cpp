@@ -75,6 +75,7 @@ int fsk_engine_create(int device, const double* X, const double* a, int64_t n, c
         fsk_measure src{X, a, nullptr, n, d}, tgt{Y, b, nullptr, m, d};
         validate_problem_raw(src, tgt, nullptr);
         FSKB_CUDA(cudaSetDevice(device));
+        configure_device_pool(device);
         auto* e = new fsk_engine();
         e->device = device;
         FSKB_CUDA(cudaStreamCreateWithFlags(&e->own, cudaStreamNonBlocking));
