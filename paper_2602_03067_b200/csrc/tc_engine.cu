@@ -103,6 +103,9 @@ struct TcParams {
     // key tile of the row's running max in that split
     int* gap;
     int* part_arg;
+    // warm LSE passes: per-row lower bound of this pass's row max (log2 units),
+    // the running max starts there (tighter gaps, earlier in-epilogue skips)
+    const float* m_init;
 };
 
 // next key tile >= kt (< kt1) in the live set `live_in` of LSE-pass unit u
@@ -122,19 +125,19 @@ __device__ __forceinline__ int live_in_next(const TcParams& p, int u, int kt, in
 // last tile, then either the online (max, sum-exp) update (LSE) or, with the row
 // LSE known, the transport-vector sum sum_j 2^(t - L) v_j (VEC). `v` holds the 128
 // fp32 scores of this thread's row (acc units; t = acc * acc_scale).
-template <bool VEC>
-__device__ __forceinline__ bool k1_tile_update(uint32_t (&v)[128], int64_t kbase, const TcParams& p,
+template <bool VEC, int W = 128>
+__device__ __forceinline__ bool k1_tile_update(uint32_t (&v)[W], int64_t kbase, const TcParams& p,
                                                float& M, double& S, float nlh, float nll,
                                                float* vb, int lane, float& umax_out) {
-    if (kbase + TILE > p.key_valid) {
+    if (kbase + W > p.key_valid) {
 #pragma unroll
-        for (int j = 0; j < 128; ++j)
+        for (int j = 0; j < W; ++j)
             if (kbase + j >= p.key_valid) v[j] = __float_as_uint(-INFINITY);
     }
     float mx0 = __uint_as_float(v[0]), mx1 = __uint_as_float(v[1]);
     float mx2 = __uint_as_float(v[2]), mx3 = __uint_as_float(v[3]);
 #pragma unroll
-    for (int j = 4; j < 128; j += 4) {
+    for (int j = 4; j < W; j += 4) {
         mx0 = fmaxf(mx0, __uint_as_float(v[j]));
         mx1 = fmaxf(mx1, __uint_as_float(v[j + 1]));
         mx2 = fmaxf(mx2, __uint_as_float(v[j + 2]));
@@ -146,21 +149,29 @@ __device__ __forceinline__ bool k1_tile_update(uint32_t (&v)[128], int64_t kbase
         // P~ = 2^(t - L) <= 1; a tile whose P~ are all < 2^-64 for the warp's rows
         // adds < m 2^-64 max|v| - below the fp32 result's rounding
         if (__all_sync(0xffffffffu, umax + nlh < -kSkipLog2)) return false;
-        // the tile's 128 values of v, broadcast through a per-warp buffer
-        float4 vv = make_float4(0.f, 0.f, 0.f, 0.f);
-        const int64_t j0 = kbase + 4 * lane;
-        if (j0 + 3 < p.key_valid) {
-            vv = *reinterpret_cast<const float4*>(p.vvec + j0);
+        // the tile's W values of v, broadcast through a per-warp buffer
+        if constexpr (W == 128) {
+            float4 vv = make_float4(0.f, 0.f, 0.f, 0.f);
+            const int64_t j0 = kbase + 4 * lane;
+            if (j0 + 3 < p.key_valid) {
+                vv = *reinterpret_cast<const float4*>(p.vvec + j0);
+            } else {
+                if (j0 < p.key_valid) vv.x = p.vvec[j0];
+                if (j0 + 1 < p.key_valid) vv.y = p.vvec[j0 + 1];
+                if (j0 + 2 < p.key_valid) vv.z = p.vvec[j0 + 2];
+            }
+            reinterpret_cast<float4*>(vb)[lane] = vv;
         } else {
+            float2 vv = make_float2(0.f, 0.f);
+            const int64_t j0 = kbase + 2 * lane;
             if (j0 < p.key_valid) vv.x = p.vvec[j0];
             if (j0 + 1 < p.key_valid) vv.y = p.vvec[j0 + 1];
-            if (j0 + 2 < p.key_valid) vv.z = p.vvec[j0 + 2];
+            reinterpret_cast<float2*>(vb)[lane] = vv;
         }
-        reinterpret_cast<float4*>(vb)[lane] = vv;
         __syncwarp();
         float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
-        for (int j = 0; j < 128; j += 4) {
+        for (int j = 0; j < W; j += 4) {
             const float4 w = reinterpret_cast<const float4*>(vb)[j >> 2];
             s0 = fmaf(ex2(fmaf(__uint_as_float(v[j]), p.acc_scale, nlh) + nll), w.x, s0);
             s1 = fmaf(ex2(fmaf(__uint_as_float(v[j + 1]), p.acc_scale, nlh) + nll), w.y, s1);
@@ -183,7 +194,7 @@ __device__ __forceinline__ bool k1_tile_update(uint32_t (&v)[128], int64_t kbase
         const float nm = dead ? 0.0f : -M;
         float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
-        for (int j = 0; j < 128; j += 4) {
+        for (int j = 0; j < W; j += 4) {
             s0 += ex2(fmaf(__uint_as_float(v[j]), p.acc_scale, nm));
             s1 += ex2(fmaf(__uint_as_float(v[j + 1]), p.acc_scale, nm));
             s2 += ex2(fmaf(__uint_as_float(v[j + 2]), p.acc_scale, nm));
@@ -577,6 +588,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
             if (lane == 0) mbar_arrive(qready);
 
             float M = -INFINITY;
+            if (!VEC && p.m_init && t < nq && row >= p.row_begin && row < p.row_end)
+                M = p.m_init[row];
             double S = 0.0;
             int best_kt = -1;
             float nlh = 0.0f, nll = 0.0f;
@@ -680,6 +693,256 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                     if (p.part_arg) p.part_arg[size_t(split) * p.R + row] = best_kt;
                 }
             }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}
+
+// ---- K1 (d <= 64) with 16 epilogue warps -------------------------------------
+//
+// Same producer / MMA structure as tc_lse_tq_kernel (query operand in TMEM, one
+// accumulator per query tile), but each row's 128 score columns are split over
+// two warps (column halves): 4 epilogue warps per SM sub-partition instead of 2,
+// so the ex2 / max dependency chains of one warp overlap another's. Each half
+// keeps its own running (max, sum); they are merged through shared memory at
+// the end of every work item. Not used for the opt-in SCREEN mode.
+constexpr int TQ2_WARPS = 18;
+constexpr int TQ2_THREADS = TQ2_WARPS * 32;
+constexpr uint32_t TQ2_VBUF = 16 * 64 * 4;                       // per epilogue warp: 64 floats
+constexpr uint32_t TQ2_COMB = 2 * TILE * 16;                     // per (tile, row): M, S, best
+constexpr uint32_t TQ2_SMEM_BYTES = TQ_OFF_BAR + 256 + TQ2_VBUF + TQ2_COMB + 1024;
+
+template <bool VEC>
+__global__ void __launch_bounds__(TQ2_THREADS, 1) tc_lse_tq2_kernel(const TcParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t* sbase = smem_raw + (base - raw);
+
+    const uint32_t bar0 = base + TQ_OFF_BAR;
+    auto kfull = [&](int s) { return bar0 + 8u * s; };
+    auto kempty = [&](int s) { return bar0 + 8u * (TQ_STAGES + s); };
+    const uint32_t qready = bar0 + 8u * (2 * TQ_STAGES);
+    const uint32_t qfree = qready + 8u;
+    auto accfull = [&](int t) { return qready + 16u + 8u * t; };
+    auto accempty = [&](int t) { return qready + 32u + 8u * t; };
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + TQ_OFF_BAR + 192);
+    uint8_t* comb = sbase + TQ_OFF_BAR + 256 + TQ2_VBUF;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TQ_STAGES; ++s) {
+            mbar_init(kfull(s), 1);
+            mbar_init(kempty(s), 1);
+        }
+        mbar_init(qready, 16);
+        mbar_init(qfree, 1);
+        for (int t = 0; t < 2; ++t) {
+            mbar_init(accfull(t), 1);
+            mbar_init(accempty(t), 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+            smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int ktiles_per_split = (p.k_tiles + p.splits - 1) / p.splits;
+    auto first_kt = [&](int unit, int kt0, int kt1) {
+        return p.live_in ? live_in_next(p, unit, kt0, kt1) : kt0;
+    };
+    auto next_kt = [&](int unit, int kt, int kt1) {
+        return p.live_in ? live_in_next(p, unit, kt + 1, kt1) : kt + 1;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int it = 0;
+            for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+                const int unit = item / p.splits, split = item % p.splits;
+                const int kt0 = split * ktiles_per_split;
+                const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
+                for (int kt = first_kt(unit, kt0, kt1); kt < kt1; kt = next_kt(unit, kt, kt1), ++it) {
+                    const int s = it % TQ_STAGES;
+                    mbar_wait(kempty(s), ((it / TQ_STAGES) & 1) ^ 1);
+                    mbar_expect_tx(kfull(s), KSTAGE);
+                    const uint32_t dst = base + TQ_OFF_K + s * KSTAGE;
+                    bulk_g2s(dst, p.kimg + size_t(kt) * QTILE, QTILE, kfull(s));
+                    bulk_g2s(dst + QTILE, p.kbias + size_t(kt) * BIAS, BIAS, kfull(s));
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            int it = 0;
+            int acc_n[2] = {0, 0};
+            for (int item = blockIdx.x, lu = 0; item < p.items; item += gridDim.x, ++lu) {
+                const int unit = item / p.splits, split = item % p.splits;
+                const int qt0 = p.q_tile_begin + 2 * unit;
+                const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
+                const int kt0 = split * ktiles_per_split;
+                const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
+                mbar_wait(qready, lu & 1);
+                fence_after();
+                for (int kt = first_kt(unit, kt0, kt1); kt < kt1; kt = next_kt(unit, kt, kt1)) {
+                    const int s = it % TQ_STAGES;
+                    mbar_wait(kfull(s), (it / TQ_STAGES) & 1);
+                    fence_after();
+                    const uint32_t kst = base + TQ_OFF_K + s * KSTAGE;
+                    for (int t = 0; t < nq; ++t) {
+                        mbar_wait(accempty(t), (acc_n[t] & 1) ^ 1);
+                        fence_after();
+                        issue_score_tile_tq(tmem + uint32_t(t * TILE),
+                                            tmem + TQ_QCOL + uint32_t(t) * TQ_QSTRIDE, kst);
+                        umma_commit(accfull(t));
+                        ++acc_n[t];
+                    }
+                    umma_commit(kempty(s));
+                    ++it;
+                }
+                umma_commit(qfree);
+            }
+        }
+    } else {
+        // epilogue warps 2..17: e = warp - 2; tile t = (e >> 2) & 1, column half
+        // h = e >> 3, TMEM lane quarter = warp % 4 (each (t, h) covers all quarters)
+        const int e = warp - 2;
+        const int t = (e >> 2) & 1;
+        const int half = e >> 3;
+        const int quarter = warp & 3;
+        const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
+        const uint32_t acc_addr = tmem + lane_addr + uint32_t(t * TILE + half * 64);
+        const uint32_t q_addr = tmem + lane_addr + TQ_QCOL + uint32_t(t) * TQ_QSTRIDE;
+        float* vb = reinterpret_cast<float*>(sbase + TQ_OFF_BAR + 256) + e * 64;
+        const int r_in_tile = quarter * 32 + lane;
+        float* cM = reinterpret_cast<float*>(comb) + (t * TILE + r_in_tile);
+        double* cS = reinterpret_cast<double*>(comb + 2 * TILE * 4) + (t * TILE + r_in_tile);
+        int* cB = reinterpret_cast<int*>(comb + 2 * TILE * 12) + (t * TILE + r_in_tile);
+        const int pair_bar = 1 + t * 4 + quarter;  // named barrier of the two halves
+        int acc_n = 0;
+        for (int item = blockIdx.x, lu = 0; item < p.items; item += gridDim.x, ++lu) {
+            const int unit = item / p.splits, split = item % p.splits;
+            const int qt0 = p.q_tile_begin + 2 * unit;
+            const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
+            const int kt0 = split * ktiles_per_split;
+            const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
+            const int64_t row = int64_t(qt0 + t) * TILE + r_in_tile;
+            // stage this item's query operand (half 0), after the previous item's MMAs
+            if (lu > 0) mbar_wait(qfree, (lu - 1) & 1);
+            fence_after();
+            if (half == 0 && t < nq) {
+                const uint8_t* src = p.qimg + size_t(qt0 + t) * QTILE + size_t(r_in_tile) * 128;
+                uint32_t qh[32], ql[32];
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {
+                    const int sw = (g ^ (r_in_tile & 7)) << 4;
+                    const uint4 h = *reinterpret_cast<const uint4*>(src + sw);
+                    const uint4 l = *reinterpret_cast<const uint4*>(src + CHUNK + sw);
+                    qh[4 * g] = h.x, qh[4 * g + 1] = h.y, qh[4 * g + 2] = h.z, qh[4 * g + 3] = h.w;
+                    ql[4 * g] = l.x, ql[4 * g + 1] = l.y, ql[4 * g + 2] = l.z, ql[4 * g + 3] = l.w;
+                }
+                FSKB_TMEM_ST32(q_addr, qh);
+                FSKB_TMEM_ST32(q_addr + 32, ql);
+                const uint32_t ones01 = uint32_t(__half_as_ushort(__float2half_rn(kOnesW0))) |
+                                        (uint32_t(__half_as_ushort(__float2half_rn(1.0f))) << 16);
+                const uint32_t ones2 = uint32_t(__half_as_ushort(__float2half_rn(kOnesW2)));
+                asm volatile(
+                    "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%3,%3,%3,%3,%3};" ::"r"(
+                        q_addr + 64),
+                    "r"(ones01), "r"(ones2), "r"(0u)
+                    : "memory");
+                tmem_st_wait();
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(qready);
+
+            float M = -INFINITY;
+            if (!VEC && p.m_init && t < nq && row >= p.row_begin && row < p.row_end)
+                M = p.m_init[row];
+            double S = 0.0;
+            int best_kt = -1;
+            float nlh = 0.0f, nll = 0.0f;
+            if constexpr (VEC) {
+                const bool live = t < nq && row < p.R;
+                nlh = live ? -p.l2h[row] : -3.0e38f;
+                nll = live ? -p.l2l[row] : 0.0f;
+            }
+            for (int kt = first_kt(unit, kt0, kt1); kt < kt1; kt = next_kt(unit, kt, kt1)) {
+                if (t >= nq) continue;
+                mbar_wait(accfull(t), acc_n & 1);
+                fence_after();
+                uint32_t v[64];
+                FSKB_TMEM_LD32(acc_addr, (v + 0));
+                FSKB_TMEM_LD32(acc_addr + 32, (v + 32));
+                tmem_ld_wait();
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(accempty(t));
+                ++acc_n;
+                const float M_old = M;
+                float umax;
+                const bool hit = k1_tile_update<VEC, 64>(v, int64_t(kt) * TILE + half * 64, p, M, S,
+                                                         nlh, nll, vb, lane, umax);
+                if (!VEC && hit && p.live_global && lane == 0)
+                    atomicOr(&p.live_global[size_t(item) * p.kwords + ((kt - kt0) >> 5)],
+                             1u << ((kt - kt0) & 31));
+                if constexpr (!VEC) {
+                    if (M > M_old) best_kt = kt;
+                    if (p.gap) {
+                        float gv = row < p.R ? umax - M : -INFINITY;
+                        for (int off = 16; off >= 1; off >>= 1)
+                            gv = fmaxf(gv, __shfl_xor_sync(0xffffffffu, gv, off));
+                        if (lane == 0)
+                            atomicMax(&p.gap[size_t(unit) * p.k_tiles + kt], fenc(gv));
+                    }
+                }
+            }
+            // merge the two column halves of each row
+            if (half == 1) {
+                *cM = M;
+                *cS = S;
+                *cB = best_kt;
+            }
+            asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+            if (half == 0) {
+                const float Mb = *cM;
+                const double Sb = *cS;
+                const int Bb = *cB;
+                double Sm;
+                float Mm;
+                int Bm;
+                if constexpr (VEC) {
+                    Sm = S + Sb;
+                    Mm = 0.0f;
+                    Bm = -1;
+                } else {
+                    Mm = fmaxf(M, Mb);
+                    Sm = (M == -INFINITY ? 0.0 : S * exp2(double(M) - double(Mm))) +
+                         (Mb == -INFINITY ? 0.0 : Sb * exp2(double(Mb) - double(Mm)));
+                    Bm = M >= Mb ? best_kt : Bb;
+                }
+                if (t < nq && row >= p.row_begin && row < p.row_end) {
+                    if constexpr (VEC) {
+                        p.part_m[size_t(split) * p.R + row] = Sm;
+                    } else {
+                        p.part_m[size_t(split) * p.R + row] = double(Mm) * 0.69314718055994530942;
+                        p.part_s[size_t(split) * p.R + row] = Sm;
+                        if (p.part_arg) p.part_arg[size_t(split) * p.R + row] = Bm;
+                    }
+                }
+            }
+            asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
         }
     }
     fence_before();
@@ -1388,7 +1651,7 @@ __global__ void tc_grad_finalize_kernel(const float* __restrict__ part_o, int sp
 __global__ void tc_finalize_kernel(const double* __restrict__ pm, const double* __restrict__ ps,
                                    int splits, int64_t R, int64_t row_begin, int64_t row_end,
                                    FinalizeArgs<float> a, const int* __restrict__ part_arg,
-                                   int* __restrict__ argtile) {
+                                   int* __restrict__ argtile, float* __restrict__ rowmax) {
     const int64_t i = row_begin + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     double vsum = 0.0;
     if (i < row_end) {
@@ -1400,6 +1663,7 @@ __global__ void tc_finalize_kernel(const double* __restrict__ pm, const double* 
                 kbest = k;
             }
         if (argtile) argtile[i] = part_arg[size_t(kbest) * R + i];
+        if (rowmax) rowmax[i] = float(M * 1.4426950408889634074);
         double S = 0.0;
         for (int k = 0; k < splits; ++k) {
             const double mk = pm[size_t(k) * R + i];
@@ -1538,15 +1802,24 @@ __global__ void build_bias(const float* __restrict__ pot, const float* __restric
 // lambda_u = min over the rows of unit u (2 query tiles) of the smallest bias change
 // in the key tile that held the row's max in the previous pass: M_i^new >=
 // M_i^old + lambda_u (the old argmax key is still there, shifted by its bias change)
+// lambda_u = min over the unit's rows of min(db) over the tile of the row's last
+// max: the row max moves by >= lambda_u. The row's own bound, previous max +
+// min(db over its argtile) - 1 (one binade of margin for the fp32 rounding of the
+// stored max), seeds the running max of the next pass (m_init).
 __global__ void warm_lambda_kernel(const int* __restrict__ argtile, const int* __restrict__ tile_dmin,
                                    int64_t row_begin, int64_t row_end, int q_tile_begin,
-                                   int* __restrict__ lam) {
+                                   int* __restrict__ lam, const float* __restrict__ rowmax,
+                                   float* __restrict__ m_init) {
     const int64_t i = row_begin + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= row_end) return;
     const int a = argtile[i];
     const float v = a >= 0 ? fdec(tile_dmin[a]) : -INFINITY;
     const int u = int(i / TILE - q_tile_begin) >> 1;
     atomicMin(&lam[u], fenc(v));
+    if (m_init) {
+        const float lb = rowmax[i] + v - 1.0f;
+        m_init[i] = isfinite(lb) ? lb : -INFINITY;
+    }
 }
 
 __global__ void fill_int_kernel(int* __restrict__ p, int64_t n, int v) {
@@ -1703,6 +1976,7 @@ struct TcHalfStep::Impl {
     int bcur[2] = {0, 0};
     bool b_valid[2] = {false, false};
     DevBuf<int> tdmax[2], tdmin[2], gap[2], argtile[2], part_arg[2], lam[2];
+    DevBuf<float> rowmax[2], minit[2];  // last row max (log2), next pass's lower bound
     DevBuf<uint32_t> warm_live[2];
     bool warm_ok[2] = {false, false}, last_warm_track[2] = {false, false};
     int64_t warm_rb[2] = {0, 0}, warm_re[2] = {0, 0};
@@ -1779,6 +2053,10 @@ void TcHalfStep::poll_screen(int side, double max_live) {
 
 TcHalfStep::TcHalfStep(DevProblem<float>& P) : impl_(new Impl()) {
     // per device (the attribute is per-context), cheap enough to set every time
+    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_tq2_kernel<false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(TQ2_SMEM_BYTES)));
+    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_tq2_kernel<true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(TQ2_SMEM_BYTES)));
     FSKB_CUDA(cudaFuncSetAttribute(tc_lse_tq_kernel<false, false>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(TQ_SMEM_BYTES)));
     FSKB_CUDA(cudaFuncSetAttribute(tc_lse_tq_kernel<true, false>,
@@ -1946,6 +2224,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         const size_t gsz = size_t(units) * size_t(n_ktiles);
         if (I.gap[side].size() < gsz) I.gap[side].alloc(gsz, P.s);
         if (I.argtile[side].size() < size_t(p.R)) I.argtile[side].alloc(size_t(p.R), P.s);
+        if (I.rowmax[side].size() < size_t(p.R)) I.rowmax[side].alloc(size_t(p.R), P.s);
         if (I.part_arg[side].size() < size_t(p.splits) * size_t(p.R))
             I.part_arg[side].alloc(size_t(p.splits) * size_t(p.R), P.s);
         const bool warm = I.warm_ok[side] && I.b_valid[side] && I.warm_rb[side] == row_begin &&
@@ -1953,9 +2232,15 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         if (warm) {
             if (I.lam[side].size() < size_t(units)) I.lam[side].alloc(size_t(units), P.s);
             fill_int_kernel<<<64, 256, 0, P.s>>>(I.lam[side].get(), units, 0x7F800000);
+            static const bool seed = [] {
+                const char* e = std::getenv("FSK_MINIT");
+                return !(e && e[0] == '0');
+            }();
+            if (seed && I.minit[side].size() < size_t(p.R)) I.minit[side].alloc(size_t(p.R), P.s);
             warm_lambda_kernel<<<unsigned((row_end - row_begin + 255) / 256), 256, 0, P.s>>>(
                 I.argtile[side].get(), I.tdmin[side].get(), row_begin, row_end, p.q_tile_begin,
-                I.lam[side].get());
+                I.lam[side].get(), I.rowmax[side].get(), seed ? I.minit[side].get() : nullptr);
+            p.m_init = seed ? I.minit[side].get() : nullptr;
             const size_t words = size_t(units) * p.splits * kw;
             if (I.warm_live[side].size() < words) I.warm_live[side].alloc(words, P.s);
             const bool track = !I.pending[side];
@@ -2027,10 +2312,16 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         p.in_kwords = I.live_kwords[side];
     }
     if (I.chunks == 1) {
-        if (vec)
+        const char* e16 = std::getenv("FSK_EPI16");
+        const bool wide = e16 && e16[0] == '1' && !p.break_lse;  // opt-in 16-warp epilogue
+        if (vec && wide)
+            tc_lse_tq2_kernel<true><<<grid, TQ2_THREADS, TQ2_SMEM_BYTES, P.s>>>(p);
+        else if (vec)
             tc_lse_tq_kernel<true, false><<<grid, NUM_THREADS, TQ_SMEM_BYTES, P.s>>>(p);
         else if (screen)
             tc_lse_tq_kernel<false, true><<<grid, NUM_THREADS, TQ_SMEM_BYTES, P.s>>>(p);
+        else if (wide)
+            tc_lse_tq2_kernel<false><<<grid, TQ2_THREADS, TQ2_SMEM_BYTES, P.s>>>(p);
         else
             tc_lse_tq_kernel<false, false><<<grid, NUM_THREADS, TQ_SMEM_BYTES, P.s>>>(p);
         if (screen && !I.pending[side]) {
@@ -2065,7 +2356,8 @@ void TcHalfStep::run(DevProblem<float>& P, int side, const float* kpot, float ep
     const bool warm = I.last_warm_track[side];
     tc_finalize_kernel<<<unsigned((rows + 255) / 256), 256, 0, P.s>>>(
         pm.get(), ps.get(), splits, R, row_begin, row_end, fb,
-        warm ? I.part_arg[side].get() : nullptr, warm ? I.argtile[side].get() : nullptr);
+        warm ? I.part_arg[side].get() : nullptr, warm ? I.argtile[side].get() : nullptr,
+        warm ? I.rowmax[side].get() : nullptr);
     FSKB_CUDA(cudaGetLastError());
     count_launch();
     if (warm) {

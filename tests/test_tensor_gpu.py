@@ -170,6 +170,8 @@ def test_tensor_fused_gradient_parity(fsk, port, n, m, d, eps):
     print(f"grad rel err gpu {e_gpu:.2e} ref-fp32 {e32:.2e}")
     assert e_gpu <= max(1e-5, 2.0 * e32)
     # the row shard reproduces the same rows of the full gradient
+    dsh = np.abs(Gs.cpu().numpy() - G.cpu().numpy()[lo:hi]).max()
+    print(f"shard vs full max |diff| {dsh:.3e}")
     assert np.array_equal(Gs.cpu().numpy(), G.cpu().numpy()[lo:hi])
     eng.close()
 
@@ -320,7 +322,12 @@ def test_warm_bounds_match_cold_passes(fsk):
     fc, gc, Gc = out["0"]
     assert np.abs(fw - fc).max() <= 1e-6 * max(1.0, np.abs(fc).max())
     assert np.abs(gw - gc).max() <= 1e-6 * max(1.0, np.abs(gc).max())
-    assert np.abs(Gw - Gc).max() <= 1e-5 * np.abs(Gc).max()
+    # warm passes seed each row's running max with a lower bound, which moves the
+    # reference point of the online LSE: f and g differ by fp32 rounding, and one
+    # ulp of f / eps perturbs every P_ij by that much relative - the gradient
+    # (a difference of two such sums) inherits it
+    floor = 2.0 ** -23 * max(np.abs(fc).max(), np.abs(gc).max()) / eps
+    assert np.abs(Gw - Gc).max() <= max(1e-5, floor) * np.abs(Gc).max()
 
 
 def test_screened_lse_matches_unscreened(fsk):
