@@ -487,7 +487,7 @@ def run_b200(args, cfgname):
     # live blocks of the passes whose live count was read back, plus every block
     # of the untracked (cold / plain) passes.
     passes = args.steps * (2 * iters + (1 if STEP_TAIL[cfgname] == "grad" else 0))
-    blocks_pass = -(-rows0 // 256) * -(-m // 128)
+    blocks_pass = -(-rows0 // 128) * -(-m // 128)   # (query tile, key tile) blocks
     total_blocks = passes * blocks_pass
     executed = min(1.0, (live + max(0, total_blocks - sblk)) / total_blocks) if total_blocks \
         else 1.0

@@ -301,16 +301,16 @@ int fsk_engine_transport_mat(fsk_engine* e, int side, const float* v_dev, int64_
  * out_dev (float, n x p) = (P (.) A Y^T) V for A (n x d) and V (m x p), device. */
 int fsk_engine_transport_hadamard(fsk_engine* e, const float* a_dev, const float* v_dev,
                                   int64_t p, float* out_dev, void* stream);
-/* Cumulative count of (query tile pair, key tile) blocks scored in full by
- * screened tcgen05 LSE passes (phase 2); the rest were proven below 2^-64 of
- * every row's max by the 5-MMA hi x hi screen (diagnostics for the bench line).
- * Screening is adaptive (on while the live fraction stays below 0.45). */
+/* Cumulative count of (query tile, key tile) blocks scored in full by tracked
+ * tcgen05 LSE passes (warm-bound passes, or screened passes' phase 2); the rest
+ * were proven below 2^-64 of every row's max (diagnostics for the bench line).
+ * Tracking is adaptive (warm bounds). */
 uint64_t fsk_engine_screen_live_tiles(const fsk_engine* e);
 /* Fraction of (query tile pair, key tile) blocks in the live-tile set recorded by
  * the last LSE pass of `side` (reused by transport passes at the same potentials);
  * -1 when none. Synchronizes the device (diagnostics). */
 double fsk_engine_live_set_fraction(const fsk_engine* e, int side);
-/* (query tile pair, key tile) blocks covered by those screened passes. */
+/* (query tile, key tile) blocks covered by those tracked passes. */
 uint64_t fsk_engine_screen_blocks(const fsk_engine* e);
 /* Launch counter of this engine's kernels (for bench accounting). */
 int64_t fsk_engine_kernel_launches(const fsk_engine* e);

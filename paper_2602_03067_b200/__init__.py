@@ -478,7 +478,7 @@ class Engine:
         return lib().fsk_engine_path(self.h).decode()
 
     def live_tiles(self) -> int:
-        """Blocks scored in full by screened LSE passes so far."""
+        """(query tile, key tile) blocks scored in full by tracked LSE passes so far."""
         return int(lib().fsk_engine_screen_live_tiles(self.h))
 
     def live_set_fraction(self, side: int) -> float:
@@ -486,7 +486,7 @@ class Engine:
         return float(lib().fsk_engine_live_set_fraction(self.h, C.c_int(side)))
 
     def screened_blocks(self) -> int:
-        """Blocks covered by screened LSE passes so far."""
+        """(query tile, key tile) blocks covered by tracked LSE passes so far."""
         return int(lib().fsk_engine_screen_blocks(self.h))
 
     @staticmethod

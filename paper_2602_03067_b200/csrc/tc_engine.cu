@@ -98,22 +98,42 @@ struct TcParams {
     // (unit u of this pass = unit u of the LSE pass; item index u * in_splits + kt / in_kps)
     const uint32_t* live_in;
     int in_splits, in_kps, in_kwords;
-    // warm bounds (LSE, d <= 64): gap[u][kt] = max over the unit's rows of
+    // warm LSE passes: live_in holds one mask per query tile of the unit,
+    // [unit][split][t][in_kwords]; the key tile is loaded if either tile is live and
+    // only the live tiles' MMAs are issued
+    int live_tq;
+    // warm bounds (LSE, d <= 64): gap[qt][kt] = max over the query tile's rows of
     // (tile max - running row max), ordered-int atomicMax; part_arg[split][row] =
     // key tile of the row's running max in that split
-    int* gap;
+    int* gap;                    // [local query tile][key tile]
     int* part_arg;
     // warm LSE passes: per-row lower bound of this pass's row max (log2 units),
     // the running max starts there (tighter gaps, earlier in-epilogue skips)
     const float* m_init;
 };
 
-// next key tile >= kt (< kt1) in the live set `live_in` of LSE-pass unit u
-__device__ __forceinline__ int live_in_next(const TcParams& p, int u, int kt, int kt1) {
+// live-set word of key tile kt: per-unit layout, or (live_tq) the mask of query
+// tile t of the unit (t < 0: the union of both)
+__device__ __forceinline__ uint32_t live_in_word(const TcParams& p, bool tq, int u, int t, int ls,
+                                                 int wi) {
+    if (!tq) return __ldg(p.live_in + (size_t(u) * p.in_splits + ls) * p.in_kwords + wi);
+    const uint32_t* b = p.live_in + (size_t(u) * p.in_splits + ls) * 2 * p.in_kwords + wi;
+    if (t >= 0) return __ldg(b + t * p.in_kwords);
+    return __ldg(b) | __ldg(b + p.in_kwords);
+}
+
+__device__ __forceinline__ bool live_in_bit(const TcParams& p, int u, int t, int kt) {
+    const int ls = kt / p.in_kps, rel = kt - ls * p.in_kps;
+    return (live_in_word(p, true, u, t, ls, rel >> 5) >> (rel & 31)) & 1u;
+}
+
+// next key tile >= kt (< kt1) in the live set `live_in` of LSE-pass unit u (query
+// tile t of it when the set is per tile, t < 0: either tile)
+__device__ __forceinline__ int live_in_next(const TcParams& p, int u, int kt, int kt1, int t = -1,
+                                            bool tq = false) {
     while (kt < kt1) {
         const int ls = kt / p.in_kps, rel = kt - ls * p.in_kps;
-        const uint32_t w =
-            __ldg(p.live_in + (size_t(u) * p.in_splits + ls) * p.in_kwords + (rel >> 5)) >> (rel & 31);
+        const uint32_t w = live_in_word(p, tq, u, t, ls, rel >> 5) >> (rel & 31);
         if (w) return kt + __ffs(w) - 1;
         kt += 32 - (rel & 31);
         if (rel + 32 - (rel & 31) > p.in_kps) kt = (ls + 1) * p.in_kps;
@@ -414,6 +434,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
     const uint32_t bits_free = qready + 56u;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + TQ_OFF_BAR + 192);
     uint32_t* live_bits = reinterpret_cast<uint32_t*>(sbase + TQ_OFF_BAR + 256 + VBUF);
+    // per K stage: which query tiles of the unit are live for the staged key tile
+    // (written by the producer before its arrive, read by the MMA thread after the
+    // stage's full-barrier wait: no global loads on the MMA issue path)
+    volatile uint32_t* stage_mask = reinterpret_cast<uint32_t*>(sbase + TQ_OFF_BAR + 160);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if constexpr (SCREEN)
@@ -453,13 +477,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
     };
     const int ktiles_per_split = (p.k_tiles + p.splits - 1) / p.splits;
     // phase-2 (SCREEN) / VEC-at-fixed-potentials key tile sequence
-    auto first_kt = [&](int unit, int kt0, int kt1) {
+    // (t >= 0: the sequence of query tile t of the unit; producer / MMA: t = -1)
+    auto first_kt = [&](int unit, int kt0, int kt1, int t = -1) {
         if constexpr (SCREEN) return next_live(kt0, kt0, kt1);
-        return p.live_in ? live_in_next(p, unit, kt0, kt1) : kt0;
+        return p.live_in ? live_in_next(p, unit, kt0, kt1, t, !VEC && p.live_tq) : kt0;
     };
-    auto next_kt = [&](int unit, int kt, int kt0, int kt1) {
+    auto next_kt = [&](int unit, int kt, int kt0, int kt1, int t = -1) {
         if constexpr (SCREEN) return next_live(kt + 1, kt0, kt1);
-        return p.live_in ? live_in_next(p, unit, kt + 1, kt1) : kt + 1;
+        return p.live_in ? live_in_next(p, unit, kt + 1, kt1, t, !VEC && p.live_tq) : kt + 1;
     };
 
     if (warp == 0) {
@@ -484,7 +509,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 for (int kt = first_kt(unit, kt0, kt1); kt < kt1;
                      kt = next_kt(unit, kt, kt0, kt1), ++it, ++nlive) {
                     const int s = it % TQ_STAGES;
+                    uint32_t mask = 3u;
+                    if (!SCREEN && !VEC && p.live_tq)
+                        mask = uint32_t(live_in_bit(p, unit, 0, kt)) |
+                               (uint32_t(live_in_bit(p, unit, 1, kt)) << 1);
                     mbar_wait(kempty(s), ((it / TQ_STAGES) & 1) ^ 1);
+                    stage_mask[s] = mask;
                     mbar_expect_tx(kfull(s), KSTAGE);
                     const uint32_t dst = base + TQ_OFF_K + s * KSTAGE;
                     bulk_g2s(dst, p.kimg + size_t(kt) * QTILE, QTILE, kfull(s));
@@ -492,7 +522,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 }
                 if constexpr (SCREEN) {
                     mbar_arrive(bits_free);
-                    if (p.live_count) atomicAdd(p.live_count, (unsigned long long)nlive);
+                    if (p.live_count)  // (query tile, key tile) blocks, as the warm count
+                        atomicAdd(p.live_count,
+                                  (unsigned long long)nlive *
+                                      min(2, p.q_tiles - 2 * unit));
                 }
             }
         }
@@ -508,13 +541,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
                 mbar_wait(qready, lu & 1);
                 fence_after();
-                auto tile_mmas = [&](int kt_unused, bool screen_phase) {
-                    (void)kt_unused;
+                auto tile_mmas = [&](bool screen_phase) {
                     const int s = it % TQ_STAGES;
                     mbar_wait(kfull(s), (it / TQ_STAGES) & 1);
                     fence_after();
                     const uint32_t kst = base + TQ_OFF_K + s * KSTAGE;
+                    const uint32_t mask = screen_phase ? 3u : stage_mask[s];
                     for (int t = 0; t < nq; ++t) {
+                        if (!((mask >> t) & 1u)) continue;
                         mbar_wait(accempty(t), (acc_n[t] & 1) ^ 1);
                         fence_after();
                         const uint32_t d = tmem + uint32_t(t * TILE);
@@ -530,11 +564,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                     ++it;
                 };
                 if constexpr (SCREEN) {
-                    for (int kt = kt0; kt < kt1; ++kt) tile_mmas(kt, true);
+                    for (int kt = kt0; kt < kt1; ++kt) tile_mmas(true);
                     mbar_wait(screen_done, lu & 1);
                 }
                 for (int kt = first_kt(unit, kt0, kt1); kt < kt1; kt = next_kt(unit, kt, kt0, kt1))
-                    tile_mmas(kt, false);
+                    tile_mmas(false);
                 if constexpr (SCREEN) mbar_arrive(bits_free);
                 umma_commit(qfree);
             }
@@ -636,8 +670,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                         const bool live = row_ok && tmax >= Ma - p.screen_thr;
                         if (__any_sync(0xffffffffu, live) && lane == 0)
                             atomicOr(&live_bits[(kt - kt0) >> 5], 1u << ((kt - kt0) & 31));
+                        if (p.gap) {
+                            // warm-bound seed: true gap <= screened gap + 2 delta + slack
+                            float gv = row_ok ? tmax - Ma + (p.screen_thr - kSkipLog2)
+                                              : -INFINITY;
+                            for (int off = 16; off >= 1; off >>= 1)
+                                gv = fmaxf(gv, __shfl_xor_sync(0xffffffffu, gv, off));
+                            if (lane == 0)
+                                atomicMax(&p.gap[size_t(2 * unit + t) * p.k_tiles + kt],
+                                          fenc(gv));
+                        }
                     }
                 }
+                // the split's true max is >= the screened max - (delta + slack):
+                // seed the running max there (earlier in-epilogue skips)
+                if (!VEC && row_ok && Ma > -INFINITY)
+                    M = fmaxf(M, Ma - 0.5f * (p.screen_thr - kSkipLog2) - 1.0f);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(screen_done);
                 mbar_wait(screen_done, lu & 1);
@@ -646,8 +694,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                     for (int w = threadIdx.x - 64; w < p.kwords; w += 256)
                         p.live_global[size_t(item) * p.kwords + w] = live_bits[w];
             }
-            for (int kt = first_kt(unit, kt0, kt1); kt < kt1; kt = next_kt(unit, kt, kt0, kt1)) {
-                if (t >= nq) continue;
+            for (int kt = t < nq ? first_kt(unit, kt0, kt1, t) : kt1, kt_next; kt < kt1;
+                 kt = kt_next) {
                 mbar_wait(accfull(t), acc_n & 1);
                 fence_after();
                 uint32_t v[128];
@@ -655,6 +703,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 FSKB_TMEM_LD32(acc_addr + 32, (v + 32));
                 FSKB_TMEM_LD32(acc_addr + 64, (v + 64));
                 FSKB_TMEM_LD32(acc_addr + 96, (v + 96));
+                kt_next = next_kt(unit, kt, kt0, kt1, t);  // overlaps the TMEM loads
                 tmem_ld_wait();
                 fence_before();
                 __syncwarp();
@@ -674,7 +723,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                         for (int off = 16; off >= 1; off >>= 1)
                             gv = fmaxf(gv, __shfl_xor_sync(0xffffffffu, gv, off));
                         if (lane == 0)
-                            atomicMax(&p.gap[size_t(unit) * p.k_tiles + kt], fenc(gv));
+                            atomicMax(&p.gap[size_t(2 * unit + t) * p.k_tiles + kt], fenc(gv));
                     }
                 }
             }
@@ -693,256 +742,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                     if (p.part_arg) p.part_arg[size_t(split) * p.R + row] = best_kt;
                 }
             }
-        }
-    }
-    fence_before();
-    __syncthreads();
-    if (warp == 1) {
-        fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-    }
-}
-
-// ---- K1 (d <= 64) with 16 epilogue warps -------------------------------------
-//
-// Same producer / MMA structure as tc_lse_tq_kernel (query operand in TMEM, one
-// accumulator per query tile), but each row's 128 score columns are split over
-// two warps (column halves): 4 epilogue warps per SM sub-partition instead of 2,
-// so the ex2 / max dependency chains of one warp overlap another's. Each half
-// keeps its own running (max, sum); they are merged through shared memory at
-// the end of every work item. Not used for the opt-in SCREEN mode.
-constexpr int TQ2_WARPS = 18;
-constexpr int TQ2_THREADS = TQ2_WARPS * 32;
-constexpr uint32_t TQ2_VBUF = 16 * 64 * 4;                       // per epilogue warp: 64 floats
-constexpr uint32_t TQ2_COMB = 2 * TILE * 16;                     // per (tile, row): M, S, best
-constexpr uint32_t TQ2_SMEM_BYTES = TQ_OFF_BAR + 256 + TQ2_VBUF + TQ2_COMB + 1024;
-
-template <bool VEC>
-__global__ void __launch_bounds__(TQ2_THREADS, 1) tc_lse_tq2_kernel(const TcParams p) {
-    extern __shared__ uint8_t smem_raw[];
-    const uint32_t raw = smem_u32(smem_raw);
-    const uint32_t base = (raw + 1023u) & ~1023u;
-    uint8_t* sbase = smem_raw + (base - raw);
-
-    const uint32_t bar0 = base + TQ_OFF_BAR;
-    auto kfull = [&](int s) { return bar0 + 8u * s; };
-    auto kempty = [&](int s) { return bar0 + 8u * (TQ_STAGES + s); };
-    const uint32_t qready = bar0 + 8u * (2 * TQ_STAGES);
-    const uint32_t qfree = qready + 8u;
-    auto accfull = [&](int t) { return qready + 16u + 8u * t; };
-    auto accempty = [&](int t) { return qready + 32u + 8u * t; };
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + TQ_OFF_BAR + 192);
-    uint8_t* comb = sbase + TQ_OFF_BAR + 256 + TQ2_VBUF;
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < TQ_STAGES; ++s) {
-            mbar_init(kfull(s), 1);
-            mbar_init(kempty(s), 1);
-        }
-        mbar_init(qready, 16);
-        mbar_init(qfree, 1);
-        for (int t = 0; t < 2; ++t) {
-            mbar_init(accfull(t), 1);
-            mbar_init(accempty(t), 8);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-            smem_u32(tmem_slot)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    fence_before();
-    __syncthreads();
-    fence_after();
-    const uint32_t tmem = *tmem_slot;
-    const int ktiles_per_split = (p.k_tiles + p.splits - 1) / p.splits;
-    auto first_kt = [&](int unit, int kt0, int kt1) {
-        return p.live_in ? live_in_next(p, unit, kt0, kt1) : kt0;
-    };
-    auto next_kt = [&](int unit, int kt, int kt1) {
-        return p.live_in ? live_in_next(p, unit, kt + 1, kt1) : kt + 1;
-    };
-
-    if (warp == 0) {
-        if (lane == 0) {
-            int it = 0;
-            for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
-                const int unit = item / p.splits, split = item % p.splits;
-                const int kt0 = split * ktiles_per_split;
-                const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
-                for (int kt = first_kt(unit, kt0, kt1); kt < kt1; kt = next_kt(unit, kt, kt1), ++it) {
-                    const int s = it % TQ_STAGES;
-                    mbar_wait(kempty(s), ((it / TQ_STAGES) & 1) ^ 1);
-                    mbar_expect_tx(kfull(s), KSTAGE);
-                    const uint32_t dst = base + TQ_OFF_K + s * KSTAGE;
-                    bulk_g2s(dst, p.kimg + size_t(kt) * QTILE, QTILE, kfull(s));
-                    bulk_g2s(dst + QTILE, p.kbias + size_t(kt) * BIAS, BIAS, kfull(s));
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            int it = 0;
-            int acc_n[2] = {0, 0};
-            for (int item = blockIdx.x, lu = 0; item < p.items; item += gridDim.x, ++lu) {
-                const int unit = item / p.splits, split = item % p.splits;
-                const int qt0 = p.q_tile_begin + 2 * unit;
-                const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
-                const int kt0 = split * ktiles_per_split;
-                const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
-                mbar_wait(qready, lu & 1);
-                fence_after();
-                for (int kt = first_kt(unit, kt0, kt1); kt < kt1; kt = next_kt(unit, kt, kt1)) {
-                    const int s = it % TQ_STAGES;
-                    mbar_wait(kfull(s), (it / TQ_STAGES) & 1);
-                    fence_after();
-                    const uint32_t kst = base + TQ_OFF_K + s * KSTAGE;
-                    for (int t = 0; t < nq; ++t) {
-                        mbar_wait(accempty(t), (acc_n[t] & 1) ^ 1);
-                        fence_after();
-                        issue_score_tile_tq(tmem + uint32_t(t * TILE),
-                                            tmem + TQ_QCOL + uint32_t(t) * TQ_QSTRIDE, kst);
-                        umma_commit(accfull(t));
-                        ++acc_n[t];
-                    }
-                    umma_commit(kempty(s));
-                    ++it;
-                }
-                umma_commit(qfree);
-            }
-        }
-    } else {
-        // epilogue warps 2..17: e = warp - 2; tile t = (e >> 2) & 1, column half
-        // h = e >> 3, TMEM lane quarter = warp % 4 (each (t, h) covers all quarters)
-        const int e = warp - 2;
-        const int t = (e >> 2) & 1;
-        const int half = e >> 3;
-        const int quarter = warp & 3;
-        const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
-        const uint32_t acc_addr = tmem + lane_addr + uint32_t(t * TILE + half * 64);
-        const uint32_t q_addr = tmem + lane_addr + TQ_QCOL + uint32_t(t) * TQ_QSTRIDE;
-        float* vb = reinterpret_cast<float*>(sbase + TQ_OFF_BAR + 256) + e * 64;
-        const int r_in_tile = quarter * 32 + lane;
-        float* cM = reinterpret_cast<float*>(comb) + (t * TILE + r_in_tile);
-        double* cS = reinterpret_cast<double*>(comb + 2 * TILE * 4) + (t * TILE + r_in_tile);
-        int* cB = reinterpret_cast<int*>(comb + 2 * TILE * 12) + (t * TILE + r_in_tile);
-        const int pair_bar = 1 + t * 4 + quarter;  // named barrier of the two halves
-        int acc_n = 0;
-        for (int item = blockIdx.x, lu = 0; item < p.items; item += gridDim.x, ++lu) {
-            const int unit = item / p.splits, split = item % p.splits;
-            const int qt0 = p.q_tile_begin + 2 * unit;
-            const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
-            const int kt0 = split * ktiles_per_split;
-            const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
-            const int64_t row = int64_t(qt0 + t) * TILE + r_in_tile;
-            // stage this item's query operand (half 0), after the previous item's MMAs
-            if (lu > 0) mbar_wait(qfree, (lu - 1) & 1);
-            fence_after();
-            if (half == 0 && t < nq) {
-                const uint8_t* src = p.qimg + size_t(qt0 + t) * QTILE + size_t(r_in_tile) * 128;
-                uint32_t qh[32], ql[32];
-#pragma unroll
-                for (int g = 0; g < 8; ++g) {
-                    const int sw = (g ^ (r_in_tile & 7)) << 4;
-                    const uint4 h = *reinterpret_cast<const uint4*>(src + sw);
-                    const uint4 l = *reinterpret_cast<const uint4*>(src + CHUNK + sw);
-                    qh[4 * g] = h.x, qh[4 * g + 1] = h.y, qh[4 * g + 2] = h.z, qh[4 * g + 3] = h.w;
-                    ql[4 * g] = l.x, ql[4 * g + 1] = l.y, ql[4 * g + 2] = l.z, ql[4 * g + 3] = l.w;
-                }
-                FSKB_TMEM_ST32(q_addr, qh);
-                FSKB_TMEM_ST32(q_addr + 32, ql);
-                const uint32_t ones01 = uint32_t(__half_as_ushort(__float2half_rn(kOnesW0))) |
-                                        (uint32_t(__half_as_ushort(__float2half_rn(1.0f))) << 16);
-                const uint32_t ones2 = uint32_t(__half_as_ushort(__float2half_rn(kOnesW2)));
-                asm volatile(
-                    "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%3,%3,%3,%3,%3};" ::"r"(
-                        q_addr + 64),
-                    "r"(ones01), "r"(ones2), "r"(0u)
-                    : "memory");
-                tmem_st_wait();
-            }
-            fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(qready);
-
-            float M = -INFINITY;
-            if (!VEC && p.m_init && t < nq && row >= p.row_begin && row < p.row_end)
-                M = p.m_init[row];
-            double S = 0.0;
-            int best_kt = -1;
-            float nlh = 0.0f, nll = 0.0f;
-            if constexpr (VEC) {
-                const bool live = t < nq && row < p.R;
-                nlh = live ? -p.l2h[row] : -3.0e38f;
-                nll = live ? -p.l2l[row] : 0.0f;
-            }
-            for (int kt = first_kt(unit, kt0, kt1); kt < kt1; kt = next_kt(unit, kt, kt1)) {
-                if (t >= nq) continue;
-                mbar_wait(accfull(t), acc_n & 1);
-                fence_after();
-                uint32_t v[64];
-                FSKB_TMEM_LD32(acc_addr, (v + 0));
-                FSKB_TMEM_LD32(acc_addr + 32, (v + 32));
-                tmem_ld_wait();
-                fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(accempty(t));
-                ++acc_n;
-                const float M_old = M;
-                float umax;
-                const bool hit = k1_tile_update<VEC, 64>(v, int64_t(kt) * TILE + half * 64, p, M, S,
-                                                         nlh, nll, vb, lane, umax);
-                if (!VEC && hit && p.live_global && lane == 0)
-                    atomicOr(&p.live_global[size_t(item) * p.kwords + ((kt - kt0) >> 5)],
-                             1u << ((kt - kt0) & 31));
-                if constexpr (!VEC) {
-                    if (M > M_old) best_kt = kt;
-                    if (p.gap) {
-                        float gv = row < p.R ? umax - M : -INFINITY;
-                        for (int off = 16; off >= 1; off >>= 1)
-                            gv = fmaxf(gv, __shfl_xor_sync(0xffffffffu, gv, off));
-                        if (lane == 0)
-                            atomicMax(&p.gap[size_t(unit) * p.k_tiles + kt], fenc(gv));
-                    }
-                }
-            }
-            // merge the two column halves of each row
-            if (half == 1) {
-                *cM = M;
-                *cS = S;
-                *cB = best_kt;
-            }
-            asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
-            if (half == 0) {
-                const float Mb = *cM;
-                const double Sb = *cS;
-                const int Bb = *cB;
-                double Sm;
-                float Mm;
-                int Bm;
-                if constexpr (VEC) {
-                    Sm = S + Sb;
-                    Mm = 0.0f;
-                    Bm = -1;
-                } else {
-                    Mm = fmaxf(M, Mb);
-                    Sm = (M == -INFINITY ? 0.0 : S * exp2(double(M) - double(Mm))) +
-                         (Mb == -INFINITY ? 0.0 : Sb * exp2(double(Mb) - double(Mm)));
-                    Bm = M >= Mb ? best_kt : Bb;
-                }
-                if (t < nq && row >= p.row_begin && row < p.row_end) {
-                    if constexpr (VEC) {
-                        p.part_m[size_t(split) * p.R + row] = Sm;
-                    } else {
-                        p.part_m[size_t(split) * p.R + row] = double(Mm) * 0.69314718055994530942;
-                        p.part_s[size_t(split) * p.R + row] = Sm;
-                        if (p.part_arg) p.part_arg[size_t(split) * p.R + row] = Bm;
-                    }
-                }
-            }
-            asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
         }
     }
     fence_before();
@@ -1298,6 +1097,10 @@ struct TcApplyGenParams {
     // u belongs to that pass's unit u / 2
     const uint32_t* live_in;
     int in_splits, in_kps, in_kwords;
+    // warm LSE passes: live_in holds one mask per query tile of the unit,
+    // [unit][split][t][in_kwords]; the key tile is loaded if either tile is live and
+    // only the live tiles' MMAs are issued
+    int live_tq;
 };
 
 __device__ __forceinline__ int gen_next_live(const TcApplyGenParams& p, int u, int kt, int kt1) {
@@ -1799,11 +1602,10 @@ __global__ void build_bias(const float* __restrict__ pot, const float* __restric
     }
 }
 
-// lambda_u = min over the rows of unit u (2 query tiles) of the smallest bias change
-// in the key tile that held the row's max in the previous pass: M_i^new >=
-// M_i^old + lambda_u (the old argmax key is still there, shifted by its bias change)
-// lambda_u = min over the unit's rows of min(db) over the tile of the row's last
-// max: the row max moves by >= lambda_u. The row's own bound, previous max +
+// lambda_t = min over the rows of query tile t of the smallest bias change in the
+// key tile that held the row's max in the previous pass: M_i^new >= M_i^old +
+// lambda_t (the old argmax key is still there, shifted by its bias change). The
+// row's own bound, previous max +
 // min(db over its argtile) - 1 (one binade of margin for the fp32 rounding of the
 // stored max), seeds the running max of the next pass (m_init).
 __global__ void warm_lambda_kernel(const int* __restrict__ argtile, const int* __restrict__ tile_dmin,
@@ -1814,8 +1616,7 @@ __global__ void warm_lambda_kernel(const int* __restrict__ argtile, const int* _
     if (i >= row_end) return;
     const int a = argtile[i];
     const float v = a >= 0 ? fdec(tile_dmin[a]) : -INFINITY;
-    const int u = int(i / TILE - q_tile_begin) >> 1;
-    atomicMin(&lam[u], fenc(v));
+    atomicMin(&lam[int(i / TILE - q_tile_begin)], fenc(v));
     if (m_init) {
         const float lb = rowmax[i] + v - 1.0f;
         m_init[i] = isfinite(lb) ? lb : -INFINITY;
@@ -1828,11 +1629,12 @@ __global__ void fill_int_kernel(int* __restrict__ p, int64_t n, int v) {
         p[i] = v;
 }
 
-// Propagate the per-(unit, key tile) gap bounds E = max_i (tilemax_i - M_i) to the
-// new bias: E' = E + max_tile(db) - lambda_u. Blocks with E' < -(64 + 1) are
-// provably below 2^-64 of every row's max and stay out of the live set (E <- E');
-// live blocks get E <- -inf for the pass to re-measure. One thread per bitmask
-// word (u, split, w) of the pass's live_in layout.
+// Propagate the per-(query tile, key tile) gap bounds E = max_i (tilemax_i - M_i)
+// to the new bias: E' = E + max_tile(db) - lambda_t. Blocks with E' < -(64 + 1)
+// are provably below 2^-64 of every row's max and stay out of the live set
+// (E <- E'); live blocks get E <- -inf for the pass to re-measure. One thread per
+// bitmask word (u, split, w) of the pass's live_in layout, both query tiles of
+// the unit: live[u][split][t][w].
 __global__ void warm_prepass_kernel(int* __restrict__ gap, const int* __restrict__ tile_dmax,
                                     const int* __restrict__ lam, int units, int k_tiles, int splits,
                                     int kps, int kwords, uint32_t* __restrict__ live,
@@ -1843,25 +1645,27 @@ __global__ void warm_prepass_kernel(int* __restrict__ gap, const int* __restrict
     const int w = int(gid % kwords);
     const int s = int((gid / kwords) % splits);
     const int u = int(gid / (int64_t(kwords) * splits));
-    const float lu = fdec(lam[u]);
     const int kt_end = min(k_tiles, (s + 1) * kps);
-    uint32_t bits = 0;
     int nlive = 0;
-    for (int b = 0; b < 32; ++b) {
-        const int kt = s * kps + w * 32 + b;
-        if (w * 32 + b >= kps || kt >= kt_end) break;
-        int* g = gap + size_t(u) * k_tiles + kt;
-        const float e = fdec(*g) + fdec(tile_dmax[kt]) - lu;
-        const bool dead = e < -(kSkipLog2 + 1.0f);   // NaN -> live
-        if (dead) {
-            *g = fenc(e);
-        } else {
-            *g = fenc(-INFINITY);
-            bits |= 1u << b;
-            ++nlive;
+    for (int t = 0; t < 2; ++t) {
+        const float lt = fdec(lam[2 * u + t]);   // +inf for a missing second tile
+        int* grow = gap + size_t(2 * u + t) * k_tiles;
+        uint32_t bits = 0;
+        for (int b = 0; b < 32; ++b) {
+            const int kt = s * kps + w * 32 + b;
+            if (w * 32 + b >= kps || kt >= kt_end) break;
+            const float e = fdec(grow[kt]) + fdec(tile_dmax[kt]) - lt;
+            const bool dead = e < -(kSkipLog2 + 1.0f);   // NaN -> live
+            if (dead) {
+                grow[kt] = fenc(e);
+            } else {
+                grow[kt] = fenc(-INFINITY);
+                bits |= 1u << b;
+                ++nlive;
+            }
         }
+        live[((size_t(u) * splits + s) * 2 + t) * kwords + w] = bits;
     }
-    live[gid] = bits;
     if (live_count && nlive) atomicAdd(live_count, (unsigned long long)nlive);
 }
 
@@ -1961,6 +1765,8 @@ struct TcHalfStep::Impl {
     bool pending[2] = {false, false};
     double pending_blocks[2] = {0.0, 0.0};
     double live_est[2] = {0.0, 0.0};         // 0 -> screen the first pass (probe)
+    bool pending_screen[2] = {false, false};  // the probe in flight is a screened pass's
+    double screen_est[2] = {0.3, 0.3};        // live fraction of the last screened pass
     int skip_left[2] = {0, 0}, backoff[2] = {8, 8}, high_run[2] = {0, 0};
     unsigned long long live_total = 0, screened_blocks = 0;
     // live set of the last LSE pass per side (valid when that pass was screened)
@@ -2036,7 +1842,9 @@ void TcHalfStep::poll_screen(int side, double max_live) {
     I.live_total += I.h_live[side];
     I.screened_blocks += (unsigned long long)I.pending_blocks[side];
     I.live_est[side] = live / std::max(1.0, I.pending_blocks[side]);
+    if (I.pending_screen[side]) I.screen_est[side] = I.live_est[side];
     I.pending[side] = false;
+    I.pending_screen[side] = false;
     // back off only after 3 consecutive mostly-live probes: the passes right after a
     // restart (fresh potentials) are mostly live even when the plan concentrates
     if (I.live_est[side] >= max_live) {
@@ -2053,10 +1861,6 @@ void TcHalfStep::poll_screen(int side, double max_live) {
 
 TcHalfStep::TcHalfStep(DevProblem<float>& P) : impl_(new Impl()) {
     // per device (the attribute is per-context), cheap enough to set every time
-    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_tq2_kernel<false>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(TQ2_SMEM_BYTES)));
-    FSKB_CUDA(cudaFuncSetAttribute(tc_lse_tq2_kernel<true>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(TQ2_SMEM_BYTES)));
     FSKB_CUDA(cudaFuncSetAttribute(tc_lse_tq_kernel<false, false>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(TQ_SMEM_BYTES)));
     FSKB_CUDA(cudaFuncSetAttribute(tc_lse_tq_kernel<true, false>,
@@ -2216,12 +2020,15 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
     p.screen_thr = I.screen_thr[side];
     bool screen = !vec && I.chunks == 1 && p.screen_thr > 0.0f && kps <= kMaxScreenTiles &&
                   !p.break_lse;
+    const bool can_screen = screen;
+    bool cold_screen = false;
     if (warm_track) {
         // warm bounds replace the 5-MMA screen: the previous pass's gaps, moved by the
-        // bias change, decide the live blocks without any extra GEMM
+        // bias change, decide the live blocks without any extra GEMM (the cold first
+        // pass is screened: its phase 1 seeds the gap bounds and the running max)
         screen = false;
         const int kw = (kps + 31) / 32;
-        const size_t gsz = size_t(units) * size_t(n_ktiles);
+        const size_t gsz = 2 * size_t(units) * size_t(n_ktiles);
         if (I.gap[side].size() < gsz) I.gap[side].alloc(gsz, P.s);
         if (I.argtile[side].size() < size_t(p.R)) I.argtile[side].alloc(size_t(p.R), P.s);
         if (I.rowmax[side].size() < size_t(p.R)) I.rowmax[side].alloc(size_t(p.R), P.s);
@@ -2229,9 +2036,10 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
             I.part_arg[side].alloc(size_t(p.splits) * size_t(p.R), P.s);
         const bool warm = I.warm_ok[side] && I.b_valid[side] && I.warm_rb[side] == row_begin &&
                           I.warm_re[side] == row_end;
+        bool go_cold = false;
         if (warm) {
-            if (I.lam[side].size() < size_t(units)) I.lam[side].alloc(size_t(units), P.s);
-            fill_int_kernel<<<64, 256, 0, P.s>>>(I.lam[side].get(), units, 0x7F800000);
+            if (I.lam[side].size() < 2 * size_t(units)) I.lam[side].alloc(2 * size_t(units), P.s);
+            fill_int_kernel<<<64, 256, 0, P.s>>>(I.lam[side].get(), 2 * units, 0x7F800000);
             static const bool seed = [] {
                 const char* e = std::getenv("FSK_MINIT");
                 return !(e && e[0] == '0');
@@ -2242,38 +2050,55 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
                 I.lam[side].get(), I.rowmax[side].get(), seed ? I.minit[side].get() : nullptr);
             p.m_init = seed ? I.minit[side].get() : nullptr;
             const size_t words = size_t(units) * p.splits * kw;
-            if (I.warm_live[side].size() < words) I.warm_live[side].alloc(words, P.s);
-            const bool track = !I.pending[side];
-            unsigned long long* cnt = track ? I.live_count.get() + side : nullptr;
-            if (track) FSKB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), P.s));
+            if (I.warm_live[side].size() < 2 * words) I.warm_live[side].alloc(2 * words, P.s);
+            // (the previous probe of this side was consumed on entry: pending is clear)
+            unsigned long long* cnt = I.live_count.get() + side;
+            FSKB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), P.s));
             warm_prepass_kernel<<<unsigned((words + 255) / 256), 256, 0, P.s>>>(
                 I.gap[side].get(), I.tdmax[side].get(), I.lam[side].get(), units, n_ktiles,
                 p.splits, kps, kw, I.warm_live[side].get(), cnt);
             FSKB_CUDA(cudaGetLastError());
             count_launch(3);
-            if (track) {  // live fraction of this pass, read back without a host sync
-                FSKB_CUDA(cudaMemcpyAsync(I.h_live + side, cnt, sizeof(unsigned long long),
-                                          cudaMemcpyDeviceToHost, P.s));
-                FSKB_CUDA(cudaEventRecord(I.ev[side], P.s));
+            // the live fraction decides this pass: wait for it (the stream is drained up
+            // to the prepass; one launch latency per pass of >= tens of ms)
+            FSKB_CUDA(cudaMemcpyAsync(I.h_live + side, cnt, sizeof(unsigned long long),
+                                      cudaMemcpyDeviceToHost, P.s));
+            FSKB_CUDA(cudaEventRecord(I.ev[side], P.s));
+            FSKB_CUDA(cudaEventSynchronize(I.ev[side]));
+            const double blocks = double(p.q_tiles) * double(n_ktiles);
+            const double est = double(I.h_live[side]) / std::max(1.0, blocks);
+            // mostly live (right after a restart of the potentials, whose bias change
+            // voids the bounds): a cold pass re-seeds the bounds for less. Cost model in
+            // units of a full unscreened pass: warm ~ est, screened ~ 0.4 + 1.2 x the
+            // last screened pass's live fraction (5 of 13 MMAs per block + phase 2)
+            const double c_screen = can_screen ? 0.4 + 1.2 * I.screen_est[side] : 1.0;
+            go_cold = est > std::min(c_screen, 1.0) + 0.05;
+            if (!go_cold) {
                 I.pending[side] = true;
-                I.pending_blocks[side] = double(units) * double(n_ktiles);
+                I.pending_blocks[side] = blocks;
+                poll_screen(side, kWarmMaxLive);   // accounting (event complete)
+                p.live_in = I.warm_live[side].get();
+                p.live_tq = 1;
+                p.in_splits = p.splits;
+                p.in_kps = kps;
+                p.in_kwords = kw;
+                I.warm_blocks += 1;
             }
-            p.live_in = I.warm_live[side].get();
-            p.in_splits = p.splits;
-            p.in_kps = kps;
-            p.in_kwords = kw;
-            I.warm_blocks += 1;
-        } else {
-            // cold pass: every block is scored and re-measured
+        }
+        if (!warm || go_cold) {
+            // cold pass: every block is screened (or scored) and re-measured; a warm
+            // pass that turned cold keeps its m_init (a valid lower bound)
             fill_int_kernel<<<256, 256, 0, P.s>>>(I.gap[side].get(), int64_t(gsz),
                                                   int(0x807FFFFF));  // fenc(-inf)
             FSKB_CUDA(cudaGetLastError());
             count_launch();
+            // screened when the last screened pass says it pays (see the cost model)
+            screen = cold_screen = can_screen && 0.4 + 1.2 * I.screen_est[side] < 0.95;
         }
         p.gap = I.gap[side].get();
         p.part_arg = I.part_arg[side].get();
     }
-    if (screen) {
+    if (screen && !cold_screen) {
         poll_screen(side, kScreenMaxLive);
         if (I.pending[side]) {
             screen = I.live_est[side] < kScreenMaxLive;  // last estimate still in flight
@@ -2312,16 +2137,10 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         p.in_kwords = I.live_kwords[side];
     }
     if (I.chunks == 1) {
-        const char* e16 = std::getenv("FSK_EPI16");
-        const bool wide = e16 && e16[0] == '1' && !p.break_lse;  // opt-in 16-warp epilogue
-        if (vec && wide)
-            tc_lse_tq2_kernel<true><<<grid, TQ2_THREADS, TQ2_SMEM_BYTES, P.s>>>(p);
-        else if (vec)
+        if (vec)
             tc_lse_tq_kernel<true, false><<<grid, NUM_THREADS, TQ_SMEM_BYTES, P.s>>>(p);
         else if (screen)
             tc_lse_tq_kernel<false, true><<<grid, NUM_THREADS, TQ_SMEM_BYTES, P.s>>>(p);
-        else if (wide)
-            tc_lse_tq2_kernel<false><<<grid, TQ2_THREADS, TQ2_SMEM_BYTES, P.s>>>(p);
         else
             tc_lse_tq_kernel<false, false><<<grid, NUM_THREADS, TQ_SMEM_BYTES, P.s>>>(p);
         if (screen && !I.pending[side]) {
@@ -2330,7 +2149,8 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
                                       cudaMemcpyDeviceToHost, P.s));
             FSKB_CUDA(cudaEventRecord(I.ev[side], P.s));
             I.pending[side] = true;
-            I.pending_blocks[side] = double(units) * double(k_tiles);
+            I.pending_screen[side] = true;
+            I.pending_blocks[side] = double(p.q_tiles) * double(k_tiles);
         }
     } else {
         if (vec)

@@ -169,10 +169,12 @@ def test_tensor_fused_gradient_parity(fsk, port, n, m, d, eps):
     e_gpu, e32, want = grad_errors(port, X, a, Y, b, fh, gh, eps, G.cpu().numpy())
     print(f"grad rel err gpu {e_gpu:.2e} ref-fp32 {e32:.2e}")
     assert e_gpu <= max(1e-5, 2.0 * e32)
-    # the row shard reproduces the same rows of the full gradient
+    # the row shard reproduces the same rows of the full gradient (to rounding: a
+    # ragged shard pairs its query tiles into different units, so the screened
+    # live sets and running-max seeds of those rows can differ)
     dsh = np.abs(Gs.cpu().numpy() - G.cpu().numpy()[lo:hi]).max()
     print(f"shard vs full max |diff| {dsh:.3e}")
-    assert np.array_equal(Gs.cpu().numpy(), G.cpu().numpy()[lo:hi])
+    assert dsh <= 1e-6 * np.abs(G.cpu().numpy()).max()
     eng.close()
 
 
@@ -286,10 +288,13 @@ def test_single_precision_hvp_matches_fp64(fsk, port, tensor_mode, d):
     assert led.transport_vector_applies == 2 * i32["cg_iters"] + 3
 
 
-def test_warm_bounds_match_cold_passes(fsk):
+@pytest.mark.parametrize("cold_screen", ["0", "1"])
+def test_warm_bounds_match_cold_passes(fsk, cold_screen):
     """Warm bounds (gap bounds carried across LSE passes and moved by the bias
     change) only drop blocks provably < 2^-64 of every row's max: 10 iterations +
-    gradient agree with FSK_WARM=0 / FSK_SCREEN=0 to fp32 rounding."""
+    gradient agree with FSK_WARM=0 / FSK_SCREEN=0 to fp32 rounding. With
+    cold_screen the first pass of each side is screened and its phase 1 seeds the
+    gap bounds."""
     torch = pytest.importorskip("torch")
     n = m = 1 << 18
     d, eps = 64, 0.05
@@ -299,7 +304,7 @@ def test_warm_bounds_match_cold_passes(fsk):
     out = {}
     for warm in ("1", "0"):
         os.environ["FSK_WARM"] = warm
-        os.environ["FSK_SCREEN"] = "0"
+        os.environ["FSK_SCREEN"] = cold_screen if warm == "1" else "0"
         try:
             eng = fsk.Engine(0, X, a, Y, b, mode="tensor")
             eng.set_eps(eps)
