@@ -112,6 +112,15 @@ struct TcParams {
     const float* m_init;
 };
 
+// Work items run split-major: the CTAs running at the same time share one key
+// range (small enough to stay L2-resident when the splits are sized for it).
+// Partial outputs and live sets keep the unit-major slot unit * splits + split.
+__device__ __forceinline__ void item_coords(int items, int splits, int item, int& unit, int& split) {
+    const int units = items / splits;
+    split = item / units;
+    unit = item - split * units;
+}
+
 // live-set word of key tile kt: per-unit layout, or (live_tq) the mask of query
 // tile t of the unit (t < 0: the union of both)
 __device__ __forceinline__ uint32_t live_in_word(const TcParams& p, bool tq, int u, int t, int ls,
@@ -279,7 +288,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
         if (lane == 0) {
             int it = 0;
             for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
-                const int unit = item / p.splits, split = item % p.splits;
+                int unit, split;
+                item_coords(p.items, p.splits, item, unit, split);
                 const int qt0 = p.q_tile_begin + 2 * unit;
                 const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
                 const int kt0 = split * ktiles_per_split;
@@ -304,7 +314,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
         if (lane == 0) {
             int it = 0, acc_it = 0;
             for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
-                const int unit = item / p.splits, split = item % p.splits;
+                int unit, split;
+                item_coords(p.items, p.splits, item, unit, split);
                 const int qt0 = p.q_tile_begin + 2 * unit;
                 const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
                 const int kt0 = split * ktiles_per_split;
@@ -336,7 +347,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
         float* vb = reinterpret_cast<float*>(sbase + C_OFF_BAR + 256) + (warp - 2) * TILE;
         int acc_it = 0;
         for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
-            const int unit = item / p.splits, split = item % p.splits;
+            int unit, split;
+                item_coords(p.items, p.splits, item, unit, split);
             const int qt0 = p.q_tile_begin + 2 * unit;
             const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
             const int kt0 = split * ktiles_per_split;
@@ -376,7 +388,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
                 const bool hit = k1_tile_update<VEC>(v, int64_t(kt) * TILE, p, M, S, nlh, nll, vb,
                                                      lane, umax);
                 if (!VEC && hit && p.live_global && lane == 0)
-                    atomicOr(&p.live_global[size_t(item) * p.kwords + ((kt - kt0) >> 5)],
+                    atomicOr(&p.live_global[(size_t(unit) * p.splits + split) * p.kwords + ((kt - kt0) >> 5)],
                              1u << ((kt - kt0) & 31));
             }
             if (t < nq && row >= p.row_begin && row < p.row_end) {
@@ -491,7 +503,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
         if (lane == 0) {
             int it = 0;
             for (int item = blockIdx.x, lu = 0; item < p.items; item += gridDim.x, ++lu) {
-                const int unit = item / p.splits, split = item % p.splits;
+                int unit, split;
+                item_coords(p.items, p.splits, item, unit, split);
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
                 if constexpr (SCREEN) {
@@ -534,7 +547,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
             int it = 0;
             int acc_n[2] = {0, 0};
             for (int item = blockIdx.x, lu = 0; item < p.items; item += gridDim.x, ++lu) {
-                const int unit = item / p.splits, split = item % p.splits;
+                int unit, split;
+                item_coords(p.items, p.splits, item, unit, split);
                 const int qt0 = p.q_tile_begin + 2 * unit;
                 const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
                 const int kt0 = split * ktiles_per_split;
@@ -583,7 +597,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
         float* vb = reinterpret_cast<float*>(sbase + TQ_OFF_BAR + 256) + (warp - 2) * TILE;
         int acc_n = 0;
         for (int item = blockIdx.x, lu = 0; item < p.items; item += gridDim.x, ++lu) {
-            const int unit = item / p.splits, split = item % p.splits;
+            int unit, split;
+                item_coords(p.items, p.splits, item, unit, split);
             const int qt0 = p.q_tile_begin + 2 * unit;
             const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
             const int kt0 = split * ktiles_per_split;
@@ -633,7 +648,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 nll = live ? -p.l2l[row] : 0.0f;
             }
             if constexpr (SCREEN) {
-                float Ma = -INFINITY;
+                // screened running max; a seeded row (m_init <= true max) starts at
+                // m_init - (delta + slack), a lower bound of its screened max
+                float Ma = M > -INFINITY ? M - 0.5f * (p.screen_thr - kSkipLog2) : -INFINITY;
                 const bool row_ok = t < nq && row < p.R;
                 for (int kt = kt0; kt < kt1; ++kt) {
                     float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
@@ -692,7 +709,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 // publish the live set for the gradient's transport pass (K3)
                 if (p.live_global)
                     for (int w = threadIdx.x - 64; w < p.kwords; w += 256)
-                        p.live_global[size_t(item) * p.kwords + w] = live_bits[w];
+                        p.live_global[(size_t(unit) * p.splits + split) * p.kwords + w] = live_bits[w];
             }
             for (int kt = t < nq ? first_kt(unit, kt0, kt1, t) : kt1, kt_next; kt < kt1;
                  kt = kt_next) {
@@ -714,7 +731,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 const bool hit = k1_tile_update<VEC>(v, int64_t(kt) * TILE, p, M, S, nlh, nll, vb,
                                                      lane, umax);
                 if (!VEC && !SCREEN && hit && p.live_global && lane == 0)
-                    atomicOr(&p.live_global[size_t(item) * p.kwords + ((kt - kt0) >> 5)],
+                    atomicOr(&p.live_global[(size_t(unit) * p.splits + split) * p.kwords + ((kt - kt0) >> 5)],
                              1u << ((kt - kt0) & 31));
                 if constexpr (!VEC) {
                     if (M > M_old) best_kt = kt;
@@ -873,7 +890,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_kernel(const TcApplyP
         if (lane == 0) {
             int it = 0, lu = 0;
             for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++lu) {
-                const int unit = item / p.splits, split = item % p.splits;
+                int unit, split;
+                item_coords(p.items, p.splits, item, unit, split);
                 const int qt = p.q_tile_begin + unit;
                 mbar_wait(qempty, (lu & 1) ^ 1);
                 mbar_expect_tx(qfull, QTILE);
@@ -896,7 +914,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_kernel(const TcApplyP
         if (lane == 0) {
             int it0 = 0, sq0 = 0, lu = 0;
             for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++lu) {
-                const int unit = item / p.splits, split = item % p.splits;
+                int unit, split;
+                item_coords(p.items, p.splits, item, unit, split);
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
                 const int K = apply_count_live(p, unit, kt0, kt1);
@@ -960,7 +979,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_kernel(const TcApplyP
         const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
         int sq = 0, lu = 0;
         for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++lu) {
-            const int unit = item / p.splits, split = item % p.splits;
+            int unit, split;
+                item_coords(p.items, p.splits, item, unit, split);
             const int qt = p.q_tile_begin + unit;
             const int kt0 = split * ktiles_per_split;
             const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
@@ -1187,7 +1207,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
         if (lane == 0) {
             int sq = 0, vt = 0;
             for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
-                const int unit = item / p.splits, split = item % p.splits;
+                int unit, split;
+                item_coords(p.items, p.splits, item, unit, split);
                 const int qt = p.q_tile_begin + unit;
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
@@ -1225,7 +1246,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
         if (lane == 0) {
             int sq = 0, vt = 0, lu = 0;
             for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++lu) {
-                const int unit = item / p.splits, split = item % p.splits;
+                int unit, split;
+                item_coords(p.items, p.splits, item, unit, split);
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
                 mbar_wait(oempty, (lu & 1) ^ 1);
@@ -1282,7 +1304,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
         const uint32_t lane_addr = uint32_t(quarter * 32) << 16;
         int vt = 0, lu = 0;
         for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++lu) {
-            const int unit = item / p.splits, split = item % p.splits;
+            int unit, split;
+                item_coords(p.items, p.splits, item, unit, split);
             const int qt = p.q_tile_begin + unit;
             const int kt0 = split * ktiles_per_split;
             const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
@@ -1997,7 +2020,19 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
     // chunked: keep the query chunks of the concurrently running work items
     // L2-resident (~48 MB) by letting several CTAs share a query tile pair
     const double q_bytes = 2.0 * I.chunks * QTILE;
-    const int min_s = I.chunks > 1 ? int(std::ceil(sms * q_bytes / (48.0 * (1 << 20)))) : 1;
+    const int base_min_s = I.chunks > 1 ? int(std::ceil(sms * q_bytes / (48.0 * (1 << 20)))) : 1;
+    int min_s = base_min_s;
+    // warm passes skip most key tiles, so the CTAs drift apart in the key sequence
+    // and every live block would be an HBM read: split the keys into ranges that
+    // stay L2-resident (~40 MB; items run split-major, item_coords)
+    const bool warm = warm_track && I.warm_ok[side] && I.b_valid[side] &&
+                      I.warm_rb[side] == row_begin && I.warm_re[side] == row_end;
+    static const bool range_split = [] {
+        const char* e = std::getenv("FSK_WARM_SPLIT");
+        return !(e && e[0] == '0');
+    }();
+    if (warm && range_split)
+        min_s = std::max(min_s, int(std::ceil(double(k_tiles) * KSTAGE / (40.0 * (1 << 20)))));
     p.splits = pick_splits(units, k_tiles, sms, min_s);
     p.items = units * p.splits;
     p.row_begin = row_begin;
@@ -2015,12 +2050,12 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
     if (!vec) ps.alloc(size_t(p.splits) * size_t(p.R), P.s);
     p.part_m = pm.get();
     p.part_s = ps.get();
-    const int grid = std::min(p.items, sms);
-    const int kps = (k_tiles + p.splits - 1) / p.splits;
+    int grid = std::min(p.items, sms);
+    int kps = (k_tiles + p.splits - 1) / p.splits;
     p.screen_thr = I.screen_thr[side];
     bool screen = !vec && I.chunks == 1 && p.screen_thr > 0.0f && kps <= kMaxScreenTiles &&
                   !p.break_lse;
-    const bool can_screen = screen;
+    bool can_screen = screen;
     bool cold_screen = false;
     if (warm_track) {
         // warm bounds replace the 5-MMA screen: the previous pass's gaps, moved by the
@@ -2034,8 +2069,6 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         if (I.rowmax[side].size() < size_t(p.R)) I.rowmax[side].alloc(size_t(p.R), P.s);
         if (I.part_arg[side].size() < size_t(p.splits) * size_t(p.R))
             I.part_arg[side].alloc(size_t(p.splits) * size_t(p.R), P.s);
-        const bool warm = I.warm_ok[side] && I.b_valid[side] && I.warm_rb[side] == row_begin &&
-                          I.warm_re[side] == row_end;
         bool go_cold = false;
         if (warm) {
             if (I.lam[side].size() < 2 * size_t(units)) I.lam[side].alloc(2 * size_t(units), P.s);
@@ -2084,6 +2117,16 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
                 p.in_kwords = kw;
                 I.warm_blocks += 1;
             }
+        }
+        if (go_cold && p.splits != pick_splits(units, k_tiles, sms, base_min_s)) {
+            // the key-range splits serve the warm live sets; a screened pass keeps one
+            // running max over the whole key range (a split-local screened max would
+            // admit far more tiles when the row has no good seed)
+            p.splits = pick_splits(units, k_tiles, sms, base_min_s);
+            p.items = units * p.splits;
+            grid = std::min(p.items, sms);
+            kps = (k_tiles + p.splits - 1) / p.splits;
+            can_screen = can_screen && kps <= kMaxScreenTiles;
         }
         if (!warm || go_cold) {
             // cold pass: every block is screened (or scored) and re-measured; a warm
