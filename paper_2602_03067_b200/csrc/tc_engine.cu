@@ -51,7 +51,8 @@ constexpr int NUM_WARPS = 10;
 constexpr int NUM_THREADS = NUM_WARPS * 32;
 constexpr uint32_t VBUF = 8 * TILE * 4;                        // per epilogue warp: 128 floats
 constexpr uint32_t SBITS = 4096;                               // screened: live-tile bitmask
-constexpr int kMaxScreenTiles = int(SBITS * 8);
+constexpr int kMaxScreenTiles = int(SBITS * 4);  // one mask per query tile of the unit
+constexpr int SWORDS = int(SBITS / 8);             // words per query tile's mask
 // chunked layout (d > 64): stage = Q chunk of 2 query tiles + key chunk + bias
 constexpr int CSTAGES = 2;
 constexpr uint32_t CSTAGE = 3 * QTILE + BIAS;                  // 100 KB
@@ -66,6 +67,31 @@ __device__ __forceinline__ int fenc(float f) {
     return i >= 0 ? i : i ^ 0x7FFFFFFF;
 }
 __device__ __forceinline__ float fdec(int k) { return __int_as_float(k >= 0 ? k : k ^ 0x7FFFFFFF); }
+
+// three-input max (FMNMX3 on sm_100)
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+// max over the W accumulator words of a row (4 independent FMNMX3 chains)
+template <int W>
+__device__ __forceinline__ float row_max(const uint32_t (&v)[W]) {
+    float m0 = __uint_as_float(v[0]), m1 = __uint_as_float(v[1]);
+    float m2 = __uint_as_float(v[2]), m3 = __uint_as_float(v[3]);
+#pragma unroll
+    for (int j = 4; j + 8 <= W; j += 8) {
+        m0 = fmax3(m0, __uint_as_float(v[j]), __uint_as_float(v[j + 1]));
+        m1 = fmax3(m1, __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+        m2 = fmax3(m2, __uint_as_float(v[j + 4]), __uint_as_float(v[j + 5]));
+        m3 = fmax3(m3, __uint_as_float(v[j + 6]), __uint_as_float(v[j + 7]));
+    }
+    // W = 4 (mod 8): the last four words
+    m0 = fmax3(m0, __uint_as_float(v[W - 4]), __uint_as_float(v[W - 3]));
+    m1 = fmax3(m1, __uint_as_float(v[W - 2]), __uint_as_float(v[W - 1]));
+    return fmax3(m0, m1, fmaxf(m2, m3));
+}
 
 struct TcParams {
     const uint8_t* qimg;    // query tile images (hi+lo per 128-row tile)
@@ -163,16 +189,7 @@ __device__ __forceinline__ bool k1_tile_update(uint32_t (&v)[W], int64_t kbase, 
         for (int j = 0; j < W; ++j)
             if (kbase + j >= p.key_valid) v[j] = __float_as_uint(-INFINITY);
     }
-    float mx0 = __uint_as_float(v[0]), mx1 = __uint_as_float(v[1]);
-    float mx2 = __uint_as_float(v[2]), mx3 = __uint_as_float(v[3]);
-#pragma unroll
-    for (int j = 4; j < W; j += 4) {
-        mx0 = fmaxf(mx0, __uint_as_float(v[j]));
-        mx1 = fmaxf(mx1, __uint_as_float(v[j + 1]));
-        mx2 = fmaxf(mx2, __uint_as_float(v[j + 2]));
-        mx3 = fmaxf(mx3, __uint_as_float(v[j + 3]));
-    }
-    const float umax = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * p.acc_scale;
+    const float umax = row_max<W>(v) * p.acc_scale;
     umax_out = umax;
     if constexpr (VEC) {
         // P~ = 2^(t - L) <= 1; a tile whose P~ are all < 2^-64 for the warp's rows
@@ -478,10 +495,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
     __syncthreads();
     fence_after();
     const uint32_t tmem = *tmem_slot;
-    auto next_live = [&](int kt, int kt0, int kt1) {
+    // screened live sets: mask t at live_bits[t * SWORDS], t < 0: the union
+    auto live_word = [&](int t, int wi) -> uint32_t {
+        if (t >= 0) return live_bits[t * SWORDS + wi];
+        return live_bits[wi] | live_bits[SWORDS + wi];
+    };
+    auto next_live = [&](int kt, int kt0, int kt1, int t) {
         while (kt < kt1) {
             const int rel = kt - kt0;
-            const uint32_t w = live_bits[rel >> 5] >> (rel & 31);
+            const uint32_t w = live_word(t, rel >> 5) >> (rel & 31);
             if (w) return kt + __ffs(w) - 1;
             kt += 32 - (rel & 31);
         }
@@ -491,11 +513,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
     // phase-2 (SCREEN) / VEC-at-fixed-potentials key tile sequence
     // (t >= 0: the sequence of query tile t of the unit; producer / MMA: t = -1)
     auto first_kt = [&](int unit, int kt0, int kt1, int t = -1) {
-        if constexpr (SCREEN) return next_live(kt0, kt0, kt1);
+        if constexpr (SCREEN) return next_live(kt0, kt0, kt1, t);
         return p.live_in ? live_in_next(p, unit, kt0, kt1, t, !VEC && p.live_tq) : kt0;
     };
     auto next_kt = [&](int unit, int kt, int kt0, int kt1, int t = -1) {
-        if constexpr (SCREEN) return next_live(kt + 1, kt0, kt1);
+        if constexpr (SCREEN) return next_live(kt + 1, kt0, kt1, t);
         return p.live_in ? live_in_next(p, unit, kt + 1, kt1, t, !VEC && p.live_tq) : kt + 1;
     };
 
@@ -520,12 +542,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 }
                 int nlive = 0;
                 for (int kt = first_kt(unit, kt0, kt1); kt < kt1;
-                     kt = next_kt(unit, kt, kt0, kt1), ++it, ++nlive) {
+                     kt = next_kt(unit, kt, kt0, kt1), ++it) {
                     const int s = it % TQ_STAGES;
                     uint32_t mask = 3u;
-                    if (!SCREEN && !VEC && p.live_tq)
+                    if constexpr (SCREEN) {
+                        const int rel = kt - kt0;
+                        mask = ((live_bits[rel >> 5] >> (rel & 31)) & 1u) |
+                               (((live_bits[SWORDS + (rel >> 5)] >> (rel & 31)) & 1u) << 1);
+                    } else if (!VEC && p.live_tq) {
                         mask = uint32_t(live_in_bit(p, unit, 0, kt)) |
                                (uint32_t(live_in_bit(p, unit, 1, kt)) << 1);
+                    }
+                    nlive += __popc(mask);
                     mbar_wait(kempty(s), ((it / TQ_STAGES) & 1) ^ 1);
                     stage_mask[s] = mask;
                     mbar_expect_tx(kfull(s), KSTAGE);
@@ -536,14 +564,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 if constexpr (SCREEN) {
                     mbar_arrive(bits_free);
                     if (p.live_count)  // (query tile, key tile) blocks, as the warm count
-                        atomicAdd(p.live_count,
-                                  (unsigned long long)nlive *
-                                      min(2, p.q_tiles - 2 * unit));
+                        atomicAdd(p.live_count, (unsigned long long)nlive);
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        // the whole warp runs the issue loop converged; one elected lane issues each
+        // tcgen05 op (uniform operands: no per-instruction divergence handling)
+        const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+        {
             int it = 0;
             int acc_n[2] = {0, 0};
             for (int item = blockIdx.x, lu = 0; item < p.items; item += gridDim.x, ++lu) {
@@ -565,16 +594,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                         if (!((mask >> t) & 1u)) continue;
                         mbar_wait(accempty(t), (acc_n[t] & 1) ^ 1);
                         fence_after();
-                        const uint32_t d = tmem + uint32_t(t * TILE);
-                        const uint32_t q = tmem + TQ_QCOL + uint32_t(t) * TQ_QSTRIDE;
+                        const uint32_t d = tm + uint32_t(t * TILE);
+                        const uint32_t q = tm + TQ_QCOL + uint32_t(t) * TQ_QSTRIDE;
                         if (screen_phase)
-                            issue_screen_tile_tq(d, q, kst);
+                            issue_screen_tile_tq<true>(d, q, kst);
                         else
-                            issue_score_tile_tq(d, q, kst);
-                        umma_commit(accfull(t));
+                            issue_score_tile_tq<true>(d, q, kst);
+                        umma_commit<true>(accfull(t));
                         ++acc_n[t];
                     }
-                    umma_commit(kempty(s));
+                    umma_commit<true>(kempty(s));
                     ++it;
                 };
                 if constexpr (SCREEN) {
@@ -583,8 +612,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 }
                 for (int kt = first_kt(unit, kt0, kt1); kt < kt1; kt = next_kt(unit, kt, kt0, kt1))
                     tile_mmas(false);
-                if constexpr (SCREEN) mbar_arrive(bits_free);
-                umma_commit(qfree);
+                if constexpr (SCREEN) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(bits_free);
+                }
+                umma_commit<true>(qfree);
             }
         }
     } else {
@@ -653,7 +685,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 float Ma = M > -INFINITY ? M - 0.5f * (p.screen_thr - kSkipLog2) : -INFINITY;
                 const bool row_ok = t < nq && row < p.R;
                 for (int kt = kt0; kt < kt1; ++kt) {
-                    float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
                     if (t < nq) {
                         mbar_wait(accfull(t), acc_n & 1);
                         fence_after();
@@ -670,32 +701,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                             for (int j = 0; j < 128; ++j)
                                 if (kbase + j >= p.key_valid) v[j] = __float_as_uint(-INFINITY);
                         }
-#pragma unroll
-                        for (int j = 0; j < 128; j += 4) {
-                            mx0 = fmaxf(mx0, __uint_as_float(v[j]));
-                            mx1 = fmaxf(mx1, __uint_as_float(v[j + 1]));
-                            mx2 = fmaxf(mx2, __uint_as_float(v[j + 2]));
-                            mx3 = fmaxf(mx3, __uint_as_float(v[j + 3]));
-                        }
+                        const float tmax = row_max<128>(v) * p.acc_scale;
                         fence_before();
                         __syncwarp();
                         if (lane == 0) mbar_arrive(accempty(t));
                         ++acc_n;
-                        const float tmax =
-                            fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * p.acc_scale;
                         Ma = fmaxf(Ma, tmax);
                         const bool live = row_ok && tmax >= Ma - p.screen_thr;
                         if (__any_sync(0xffffffffu, live) && lane == 0)
-                            atomicOr(&live_bits[(kt - kt0) >> 5], 1u << ((kt - kt0) & 31));
+                            atomicOr(&live_bits[t * SWORDS + ((kt - kt0) >> 5)],
+                                     1u << ((kt - kt0) & 31));
                         if (p.gap) {
                             // warm-bound seed: true gap <= screened gap + 2 delta + slack
-                            float gv = row_ok ? tmax - Ma + (p.screen_thr - kSkipLog2)
-                                              : -INFINITY;
-                            for (int off = 16; off >= 1; off >>= 1)
-                                gv = fmaxf(gv, __shfl_xor_sync(0xffffffffu, gv, off));
+                            const float gv = row_ok ? tmax - Ma + (p.screen_thr - kSkipLog2)
+                                                    : -INFINITY;
+                            const int gmax = __reduce_max_sync(0xffffffffu, fenc(gv));
                             if (lane == 0)
-                                atomicMax(&p.gap[size_t(2 * unit + t) * p.k_tiles + kt],
-                                          fenc(gv));
+                                atomicMax(&p.gap[size_t(2 * unit + t) * p.k_tiles + kt], gmax);
                         }
                     }
                 }
@@ -709,7 +731,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 // publish the live set for the gradient's transport pass (K3)
                 if (p.live_global)
                     for (int w = threadIdx.x - 64; w < p.kwords; w += 256)
-                        p.live_global[(size_t(unit) * p.splits + split) * p.kwords + w] = live_bits[w];
+                        p.live_global[(size_t(unit) * p.splits + split) * p.kwords + w] =
+                            live_word(-1, w);
             }
             for (int kt = t < nq ? first_kt(unit, kt0, kt1, t) : kt1, kt_next; kt < kt1;
                  kt = kt_next) {
@@ -736,11 +759,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 if constexpr (!VEC) {
                     if (M > M_old) best_kt = kt;
                     if (p.gap) {
-                        float gv = row < p.R ? umax - M : -INFINITY;
-                        for (int off = 16; off >= 1; off >>= 1)
-                            gv = fmaxf(gv, __shfl_xor_sync(0xffffffffu, gv, off));
+                        const float gv = row < p.R ? umax - M : -INFINITY;
+                        const int gmax = __reduce_max_sync(0xffffffffu, fenc(gv));
                         if (lane == 0)
-                            atomicMax(&p.gap[size_t(2 * unit + t) * p.k_tiles + kt], fenc(gv));
+                            atomicMax(&p.gap[size_t(2 * unit + t) * p.k_tiles + kt], gmax);
                     }
                 }
             }

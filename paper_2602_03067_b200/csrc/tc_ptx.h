@@ -79,33 +79,66 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t sbo, uint
     return d;
 }
 
-// D[tmem] (+)= A[smem] B[smem]
+// D[tmem] (+)= A[smem] B[smem]. ELECT: called by a converged warp, one elected lane
+// issues (no per-instruction divergence handling around the uniform operands)
+template <bool ELECT = false>
 __device__ __forceinline__ void umma_ss(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
                                         uint32_t acc) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-        "}\n" ::"r"(d_tmem),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+    if constexpr (ELECT)
+        asm volatile(
+            "{\n"
+            ".reg .pred p, e;\n"
+            "setp.ne.b32 p, %4, 0;\n"
+            "elect.sync _|e, 0xffffffff;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+            "}\n" ::"r"(d_tmem),
+            "l"(a), "l"(b), "r"(idesc), "r"(acc));
+    else
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "setp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+            "}\n" ::"r"(d_tmem),
+            "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 // D[tmem] (+)= A[tmem] B[smem]
+template <bool ELECT = false>
 __device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
                                         uint32_t idesc, uint32_t acc) {
     const uint32_t z = 0;
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%5, %5, %5, %5}, p;\n"
-        "}\n" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc), "r"(z));
+    if constexpr (ELECT)
+        asm volatile(
+            "{\n"
+            ".reg .pred p, e;\n"
+            "setp.ne.b32 p, %4, 0;\n"
+            "elect.sync _|e, 0xffffffff;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%5, %5, %5, %5}, p;\n"
+            "}\n" ::"r"(d_tmem),
+            "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc), "r"(z));
+    else
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "setp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%5, %5, %5, %5}, p;\n"
+            "}\n" ::"r"(d_tmem),
+            "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc), "r"(z));
 }
+template <bool ELECT = false>
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
-    asm volatile(
-        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-        : "memory");
+    if constexpr (ELECT)
+        asm volatile(
+            "{\n"
+            ".reg .pred e;\n"
+            "elect.sync _|e, 0xffffffff;\n"
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+            "}\n" ::"r"(bar)
+            : "memory");
+    else
+        asm volatile(
+            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+            : "memory");
 }
 
 #define FSKB_TMEM_LD32(addr, r)                                                                  \
@@ -201,23 +234,25 @@ __device__ __forceinline__ void issue_score_tile(uint32_t d_tmem, uint32_t qa, u
 
 // Score tile with the query operand in TMEM (A from TMEM at column q: hi at +0,
 // lo at +32, ones at +64; 8 columns per K16 slice), same 13-MMA order as above.
+template <bool ELECT = false>
 __device__ __forceinline__ void issue_score_tile_tq(uint32_t d_tmem, uint32_t q, uint32_t kst) {
 #pragma unroll
     for (int kk = 0; kk < DPAD / 16; ++kk) {
-        umma_ts(d_tmem, q + 32 + kk * 8, umma_desc(kst + kk * 32, 1024, 2), IDESC_QK,
+        umma_ts<ELECT>(d_tmem, q + 32 + kk * 8, umma_desc(kst + kk * 32, 1024, 2), IDESC_QK,
                 kk > 0 ? 1u : 0u);
-        umma_ts(d_tmem, q + kk * 8, umma_desc(kst + CHUNK + kk * 32, 1024, 2), IDESC_QK, 1u);
+        umma_ts<ELECT>(d_tmem, q + kk * 8, umma_desc(kst + CHUNK + kk * 32, 1024, 2), IDESC_QK, 1u);
     }
-    umma_ts(d_tmem, q + 64, umma_desc(kst + QTILE, 256, 6), IDESC_QK, 1u);
+    umma_ts<ELECT>(d_tmem, q + 64, umma_desc(kst + QTILE, 256, 6), IDESC_QK, 1u);
 #pragma unroll
     for (int kk = 0; kk < DPAD / 16; ++kk)
-        umma_ts(d_tmem, q + kk * 8, umma_desc(kst + kk * 32, 1024, 2), IDESC_QK, 1u);
+        umma_ts<ELECT>(d_tmem, q + kk * 8, umma_desc(kst + kk * 32, 1024, 2), IDESC_QK, 1u);
 }
+template <bool ELECT = false>
 __device__ __forceinline__ void issue_screen_tile_tq(uint32_t d_tmem, uint32_t q, uint32_t kst) {
-    umma_ts(d_tmem, q + 64, umma_desc(kst + QTILE, 256, 6), IDESC_QK, 0u);
+    umma_ts<ELECT>(d_tmem, q + 64, umma_desc(kst + QTILE, 256, 6), IDESC_QK, 0u);
 #pragma unroll
     for (int kk = 0; kk < DPAD / 16; ++kk)
-        umma_ts(d_tmem, q + kk * 8, umma_desc(kst + kk * 32, 1024, 2), IDESC_QK, 1u);
+        umma_ts<ELECT>(d_tmem, q + kk * 8, umma_desc(kst + kk * 32, 1024, 2), IDESC_QK, 1u);
 }
 
 // Screening approximation t~ = bias + hi x hi (5 MMAs): only the hi chunk and the
