@@ -146,6 +146,12 @@ __device__ __forceinline__ void item_coords(int items, int splits, int item, int
     split = item / units;
     unit = item - split * units;
 }
+// unit-major order (d > 64 kernels: CTAs running together share one query unit's
+// chunks, the L2-resident operand there)
+__device__ __forceinline__ void item_coords_um(int splits, int item, int& unit, int& split) {
+    unit = item / splits;
+    split = item - unit * splits;
+}
 
 // live-set word of key tile kt: per-unit layout, or (live_tq) the mask of query
 // tile t of the unit (t < 0: the union of both)
@@ -306,7 +312,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
             int it = 0;
             for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
                 int unit, split;
-                item_coords(p.items, p.splits, item, unit, split);
+                item_coords_um(p.splits, item, unit, split);
                 const int qt0 = p.q_tile_begin + 2 * unit;
                 const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
                 const int kt0 = split * ktiles_per_split;
@@ -328,11 +334,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        // converged issue warp, elected tcgen05 ops (see tc_lse_tq_kernel)
+        const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+        {
             int it = 0, acc_it = 0;
             for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
                 int unit, split;
-                item_coords(p.items, p.splits, item, unit, split);
+                item_coords_um(p.splits, item, unit, split);
                 const int qt0 = p.q_tile_begin + 2 * unit;
                 const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
                 const int kt0 = split * ktiles_per_split;
@@ -346,13 +354,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
                         fence_after();
                         const uint32_t st = base + s * CSTAGE;
                         for (int t = 0; t < nq; ++t)
-                            issue_score_chunk(tmem + uint32_t(t * 2 * TILE),
-                                              tmem + uint32_t((t * 2 + 1) * TILE), st + t * QTILE,
+                            issue_score_chunk<true>(tm + uint32_t(t * 2 * TILE),
+                                              tm + uint32_t((t * 2 + 1) * TILE), st + t * QTILE,
                                               st + 2 * QTILE, base + C_OFF_ONES, st + 3 * QTILE,
                                               c == 0, c == C - 1);
-                        umma_commit(kempty(s));
+                        umma_commit<true>(kempty(s));
                     }
-                    umma_commit(accfull);
+                    umma_commit<true>(accfull);
                 }
             }
         }
@@ -365,7 +373,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
         int acc_it = 0;
         for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
             int unit, split;
-                item_coords(p.items, p.splits, item, unit, split);
+                item_coords_um(p.splits, item, unit, split);
             const int qt0 = p.q_tile_begin + 2 * unit;
             const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
             const int kt0 = split * ktiles_per_split;
@@ -933,7 +941,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_kernel(const TcApplyP
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        // converged issue warp, elected tcgen05 ops (see tc_lse_tq_kernel)
+        const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+        {
             int it0 = 0, sq0 = 0, lu = 0;
             for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++lu) {
                 int unit, split;
@@ -949,15 +959,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_kernel(const TcApplyP
                     mbar_wait(kfull(s), ((it0 + i) / ASTAGES) & 1);
                     fence_after();
                     const int buf = (sq0 + i) % NSBUF;
-                    issue_score_tile(tmem + uint32_t(buf * TILE), base + A_OFF_Q,
+                    issue_score_tile<true>(tm + uint32_t(buf * TILE), base + A_OFF_Q,
                                      base + A_OFF_ONES, base + A_OFF_K + s * KSTAGE);
-                    umma_commit(sfull(buf));
+                    umma_commit<true>(sfull(buf));
                 };
                 if (K > 0) issue_s(0);
                 if (K > 1) issue_s(1);
                 mbar_wait(oempty(ob), ((lu >> 1) & 1) ^ 1);
                 fence_after();
-                const uint32_t o_tmem = tmem + O_COL0 + uint32_t(ob * DPAD);
+                const uint32_t o_tmem = tm + O_COL0 + uint32_t(ob * DPAD);
                 bool o_started = false;
                 for (int i = 0; i < K; ++i) {
                     // the next score tile goes first: its buffer's P~ was consumed by
@@ -973,7 +983,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_kernel(const TcApplyP
                     const bool live = i == 0 || live_tag[buf] == sq0 + i;
                     if (live) {
                         const uint32_t kst = base + A_OFF_K + s * KSTAGE;
-                        const uint32_t pcol = tmem + uint32_t(buf * TILE);
+                        const uint32_t pcol = tm + uint32_t(buf * TILE);
 #pragma unroll
                         for (int kk = 0; kk < TILE / 16; ++kk) {
                             // keys [16 kk, 16 kk + 16): column half kk / 4 of the P~ buffer,
@@ -981,16 +991,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_kernel(const TcApplyP
                             const uint32_t ph = pcol + uint32_t((kk >> 2) * 64 + (kk & 3) * 8);
                             const uint64_t vh = umma_desc(kst + kk * 2048, 1024, 2, 8192);
                             const uint64_t vl = umma_desc(kst + CHUNK + kk * 2048, 1024, 2, 8192);
-                            umma_ts(o_tmem, ph, vh, IDESC_PV, (o_started || kk > 0) ? 1u : 0u);
-                            umma_ts(o_tmem, ph + 32, vh, IDESC_PV, 1u);
-                            umma_ts(o_tmem, ph, vl, IDESC_PV, 1u);
+                            umma_ts<true>(o_tmem, ph, vh, IDESC_PV, (o_started || kk > 0) ? 1u : 0u);
+                            umma_ts<true>(o_tmem, ph + 32, vh, IDESC_PV, 1u);
+                            umma_ts<true>(o_tmem, ph, vl, IDESC_PV, 1u);
                         }
                         o_started = true;
                     }
-                    umma_commit(kempty(s));
+                    umma_commit<true>(kempty(s));
                 }
-                umma_commit(ofull(ob));
-                umma_commit(qempty);
+                umma_commit<true>(ofull(ob));
+                umma_commit<true>(qempty);
                 it0 += K;
                 sq0 += K;
             }
@@ -1160,17 +1170,18 @@ __device__ __forceinline__ int gen_next_live(const TcApplyGenParams& p, int u, i
 
 // 12 MMAs of one 64-feature chunk of W = A B^T into one accumulator (no bias):
 // cross terms first, then hi x hi.
+template <bool ELECT = false>
 __device__ __forceinline__ void issue_w_chunk(uint32_t d, uint32_t aa, uint32_t ka, bool first) {
 #pragma unroll
     for (int kk = 0; kk < DPAD / 16; ++kk) {
-        umma_ss(d, umma_desc(aa + CHUNK + kk * 32, 1024, 2), umma_desc(ka + kk * 32, 1024, 2),
+        umma_ss<ELECT>(d, umma_desc(aa + CHUNK + kk * 32, 1024, 2), umma_desc(ka + kk * 32, 1024, 2),
                 IDESC_QK, (first && kk == 0) ? 0u : 1u);
-        umma_ss(d, umma_desc(aa + kk * 32, 1024, 2), umma_desc(ka + CHUNK + kk * 32, 1024, 2),
+        umma_ss<ELECT>(d, umma_desc(aa + kk * 32, 1024, 2), umma_desc(ka + CHUNK + kk * 32, 1024, 2),
                 IDESC_QK, 1u);
     }
 #pragma unroll
     for (int kk = 0; kk < DPAD / 16; ++kk)
-        umma_ss(d, umma_desc(aa + kk * 32, 1024, 2), umma_desc(ka + kk * 32, 1024, 2), IDESC_QK,
+        umma_ss<ELECT>(d, umma_desc(aa + kk * 32, 1024, 2), umma_desc(ka + kk * 32, 1024, 2), IDESC_QK,
                 1u);
 }
 
@@ -1230,7 +1241,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
             int sq = 0, vt = 0;
             for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
                 int unit, split;
-                item_coords(p.items, p.splits, item, unit, split);
+                item_coords_um(p.splits, item, unit, split);
                 const int qt = p.q_tile_begin + unit;
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
@@ -1265,11 +1276,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        // converged issue warp, elected tcgen05 ops (see tc_lse_tq_kernel)
+        const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+        {
             int sq = 0, vt = 0, lu = 0;
             for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++lu) {
                 int unit, split;
-                item_coords(p.items, p.splits, item, unit, split);
+                item_coords_um(p.splits, item, unit, split);
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
                 mbar_wait(oempty, (lu & 1) ^ 1);
@@ -1288,14 +1301,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
                             addr[o] = base + slot[o] * QTILE;
                         }
                         fence_after();
-                        issue_score_chunk(tmem, tmem + TILE, addr[0], addr[1], base + G_OFF_ONES,
+                        issue_score_chunk<true>(tm, tm + TILE, addr[0], addr[1], base + G_OFF_ONES,
                                           base + G_OFF_BIAS + bb * BIAS, c == 0, c == C - 1);
-                        if (had) issue_w_chunk(tmem + G_WCOL, addr[2], addr[1], c == 0);
-                        for (int o = 0; o < ops; ++o) umma_commit(sempty_(slot[o]));
+                        if (had) issue_w_chunk<true>(tm + G_WCOL, addr[2], addr[1], c == 0);
+                        for (int o = 0; o < ops; ++o) umma_commit<true>(sempty_(slot[o]));
                         sq += ops;
                     }
-                    umma_commit(bempty(bb));
-                    umma_commit(sfull);
+                    umma_commit<true>(bempty(bb));
+                    umma_commit<true>(sfull);
                     mbar_wait(pready, vt & 1);
                     fence_after();
                     for (int j = 0; j < p.vc; ++j, ++sq) {
@@ -1303,21 +1316,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
                         mbar_wait(sfull_(s), (sq / NS) & 1);
                         fence_after();
                         const uint32_t vst = base + s * QTILE;
-                        const uint32_t o = tmem + G_OCOL + uint32_t(j * DPAD);
+                        const uint32_t o = tm + G_OCOL + uint32_t(j * DPAD);
 #pragma unroll
                         for (int kk = 0; kk < TILE / 16; ++kk) {
-                            const uint32_t ph = tmem + uint32_t((kk >> 2) * 64 + (kk & 3) * 8);
+                            const uint32_t ph = tm + uint32_t((kk >> 2) * 64 + (kk & 3) * 8);
                             const uint64_t vh = umma_desc(vst + kk * 2048, 1024, 2, 8192);
                             const uint64_t vl = umma_desc(vst + CHUNK + kk * 2048, 1024, 2, 8192);
-                            umma_ts(o, ph, vh, IDESC_PV, (!o_first || kk > 0) ? 1u : 0u);
-                            umma_ts(o, ph + 32, vh, IDESC_PV, 1u);
-                            umma_ts(o, ph, vl, IDESC_PV, 1u);
+                            umma_ts<true>(o, ph, vh, IDESC_PV, (!o_first || kk > 0) ? 1u : 0u);
+                            umma_ts<true>(o, ph + 32, vh, IDESC_PV, 1u);
+                            umma_ts<true>(o, ph, vl, IDESC_PV, 1u);
                         }
-                        umma_commit(sempty_(s));
+                        umma_commit<true>(sempty_(s));
                     }
                     o_first = false;
                 }
-                umma_commit(ofull);
+                umma_commit<true>(ofull);
             }
         }
     } else {
@@ -1327,7 +1340,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
         int vt = 0, lu = 0;
         for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++lu) {
             int unit, split;
-                item_coords(p.items, p.splits, item, unit, split);
+                item_coords_um(p.splits, item, unit, split);
             const int qt = p.q_tile_begin + unit;
             const int kt0 = split * ktiles_per_split;
             const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);

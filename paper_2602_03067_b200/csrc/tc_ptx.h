@@ -214,6 +214,7 @@ __device__ __forceinline__ void fill_ones_chunk(uint8_t* dst, int tid, int nthre
 // accumulator's rounding: the 8 small cross terms (2^-11 of the score) first,
 // then the bias, then the 4 hi x hi slices, so only 5 additions round at the
 // score's full magnitude and the bias partially cancels the dot product early.
+template <bool ELECT = false>
 __device__ __forceinline__ void issue_score_tile(uint32_t d_tmem, uint32_t qa, uint32_t ones,
                                                  uint32_t kst) {
 #pragma unroll
@@ -222,13 +223,13 @@ __device__ __forceinline__ void issue_score_tile(uint32_t d_tmem, uint32_t qa, u
         const uint64_t al = umma_desc(qa + CHUNK + kk * 32, 1024, 2);
         const uint64_t bh = umma_desc(kst + kk * 32, 1024, 2);
         const uint64_t bl = umma_desc(kst + CHUNK + kk * 32, 1024, 2);
-        umma_ss(d_tmem, al, bh, IDESC_QK, kk > 0 ? 1u : 0u);
-        umma_ss(d_tmem, ah, bl, IDESC_QK, 1u);
+        umma_ss<ELECT>(d_tmem, al, bh, IDESC_QK, kk > 0 ? 1u : 0u);
+        umma_ss<ELECT>(d_tmem, ah, bl, IDESC_QK, 1u);
     }
-    umma_ss(d_tmem, umma_desc(ones, 256, 6), umma_desc(kst + QTILE, 256, 6), IDESC_QK, 1u);
+    umma_ss<ELECT>(d_tmem, umma_desc(ones, 256, 6), umma_desc(kst + QTILE, 256, 6), IDESC_QK, 1u);
 #pragma unroll
     for (int kk = 0; kk < DPAD / 16; ++kk)
-        umma_ss(d_tmem, umma_desc(qa + kk * 32, 1024, 2), umma_desc(kst + kk * 32, 1024, 2),
+        umma_ss<ELECT>(d_tmem, umma_desc(qa + kk * 32, 1024, 2), umma_desc(kst + kk * 32, 1024, 2),
                 IDESC_QK, 1u);
 }
 
@@ -257,12 +258,13 @@ __device__ __forceinline__ void issue_screen_tile_tq(uint32_t d_tmem, uint32_t q
 
 // Screening approximation t~ = bias + hi x hi (5 MMAs): only the hi chunk and the
 // bias chunk of the key stage are read.
+template <bool ELECT = false>
 __device__ __forceinline__ void issue_screen_tile(uint32_t d_tmem, uint32_t qa, uint32_t ones,
                                                   uint32_t kst) {
-    umma_ss(d_tmem, umma_desc(ones, 256, 6), umma_desc(kst + QTILE, 256, 6), IDESC_QK, 0u);
+    umma_ss<ELECT>(d_tmem, umma_desc(ones, 256, 6), umma_desc(kst + QTILE, 256, 6), IDESC_QK, 0u);
 #pragma unroll
     for (int kk = 0; kk < DPAD / 16; ++kk)
-        umma_ss(d_tmem, umma_desc(qa + kk * 32, 1024, 2), umma_desc(kst + kk * 32, 1024, 2),
+        umma_ss<ELECT>(d_tmem, umma_desc(qa + kk * 32, 1024, 2), umma_desc(kst + kk * 32, 1024, 2),
                 IDESC_QK, 1u);
 }
 
@@ -273,21 +275,22 @@ __device__ __forceinline__ void issue_screen_tile(uint32_t d_tmem, uint32_t qa, 
 // it last keeps the 4 C roundings of the dot product at the dot product's own
 // magnitude); d_small = the 8 cross terms per chunk (2^-11 of the score),
 // summed by the epilogue.
+template <bool ELECT = false>
 __device__ __forceinline__ void issue_score_chunk(uint32_t d_big, uint32_t d_small, uint32_t qa,
                                                   uint32_t ka, uint32_t ones, uint32_t bias,
                                                   bool first, bool last) {
 #pragma unroll
     for (int kk = 0; kk < DPAD / 16; ++kk) {
-        umma_ss(d_small, umma_desc(qa + CHUNK + kk * 32, 1024, 2), umma_desc(ka + kk * 32, 1024, 2),
+        umma_ss<ELECT>(d_small, umma_desc(qa + CHUNK + kk * 32, 1024, 2), umma_desc(ka + kk * 32, 1024, 2),
                 IDESC_QK, (first && kk == 0) ? 0u : 1u);
-        umma_ss(d_small, umma_desc(qa + kk * 32, 1024, 2), umma_desc(ka + CHUNK + kk * 32, 1024, 2),
+        umma_ss<ELECT>(d_small, umma_desc(qa + kk * 32, 1024, 2), umma_desc(ka + CHUNK + kk * 32, 1024, 2),
                 IDESC_QK, 1u);
     }
 #pragma unroll
     for (int kk = 0; kk < DPAD / 16; ++kk)
-        umma_ss(d_big, umma_desc(qa + kk * 32, 1024, 2), umma_desc(ka + kk * 32, 1024, 2),
+        umma_ss<ELECT>(d_big, umma_desc(qa + kk * 32, 1024, 2), umma_desc(ka + kk * 32, 1024, 2),
                 IDESC_QK, (first && kk == 0) ? 0u : 1u);
-    if (last) umma_ss(d_big, umma_desc(ones, 256, 6), umma_desc(bias, 256, 6), IDESC_QK, 1u);
+    if (last) umma_ss<ELECT>(d_big, umma_desc(ones, 256, 6), umma_desc(bias, 256, 6), IDESC_QK, 1u);
 }
 
 }  // namespace tc
