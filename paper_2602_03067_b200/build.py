@@ -27,7 +27,8 @@ LIB = OUT / "libfsk_b200.so"
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++20", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=default",
-          "--expt-relaxed-constexpr", "-I", str(ROOT / "include"), "-I", str(CSRC)]
+          "--expt-relaxed-constexpr", "-I", str(ROOT / "include"), "-I", str(CSRC),
+          *os.environ.get("FSK_NVCC_EXTRA", "").split()]
 
 
 def sources() -> list[Path]:

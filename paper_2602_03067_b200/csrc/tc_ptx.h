@@ -40,6 +40,23 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+#ifdef FSKB_HANG_DEBUG
+    // debug builds: report the barrier a warp is stuck on, then trap
+    for (long long i = 0;; ++i) {
+        uint32_t ok;
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (i == (1ll << 21) && (threadIdx.x & 31) == 0)
+            printf("[hang] block %d thread %d bar 0x%x parity %u\n", int(blockIdx.x),
+                   int(threadIdx.x), bar, parity);
+        if (i == (1ll << 23)) asm volatile("trap;");
+    }
+#endif
     asm volatile(
         "{\n"
         ".reg .pred p;\n"

@@ -7,9 +7,9 @@ OUT=gpurun_out/$TAG
 mkdir -p "$OUT"
 i=0
 for setting in "$@"; do
-  env $setting timeout 900 python -m pytest tests/test_tensor_gpu.py -x -q -s > "$OUT/pytest_$i.log" 2>&1; echo "rc=$? [$setting]" >> "$OUT/pytest_$i.log"
+  env $setting timeout 400 python -m pytest tests/test_tensor_gpu.py -x -q -s > "$OUT/pytest_$i.log" 2>&1; echo "rc=$? [$setting]" >> "$OUT/pytest_$i.log"
   for c in $CFGS; do
-    env $setting timeout 900 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > "$OUT/bench_${c}_$i.log" 2>&1
+    env $setting timeout 300 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > "$OUT/bench_${c}_$i.log" 2>&1
     echo "[$setting]" >> "$OUT/bench_${c}_$i.log"
   done
   i=$((i+1))
