@@ -7,9 +7,9 @@ TAG=${1:-r01}
 OUT=gpurun_out/$TAG
 mkdir -p "$OUT"
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu,power.draw --format=csv > "$OUT/smi.txt" 2>&1
-timeout 900 python -m pytest tests -m gpu -x -q > "$OUT/pytest_gpu.log" 2>&1; echo "pytest rc=$?" >> "$OUT/pytest_gpu.log"
+timeout 600 python -m pytest tests -m gpu -x -q > "$OUT/pytest_gpu.log" 2>&1; echo "pytest rc=$?" >> "$OUT/pytest_gpu.log"
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.log" 2>&1; echo "smoke rc=$?" >> "$OUT/smoke.log"
-timeout 900 python bench.py --steps 3 --warmup 3 > "$OUT/bench.log" 2>&1; echo "bench rc=$?" >> "$OUT/bench.log"
+timeout 400 python bench.py --steps 3 --warmup 3 > "$OUT/bench.log" 2>&1; echo "bench rc=$?" >> "$OUT/bench.log"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file "$OUT/launches.csv" python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline \
   > "$OUT/ncu_launch.log" 2>&1; echo "ncu launches rc=$?" >> "$OUT/ncu_launch.log"
