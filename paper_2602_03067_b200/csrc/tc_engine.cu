@@ -93,6 +93,20 @@ __device__ __forceinline__ float row_max(const uint32_t (&v)[W]) {
     return fmax3(m0, m1, fmaxf(m2, m3));
 }
 
+// max over the 32 accumulator words [32 c, 32 c + 32) of a row (2 FMNMX3 chains)
+template <int W>
+__device__ __forceinline__ float group_max32(const uint32_t (&v)[W], int c) {
+    const int b = 32 * c;
+    float m0 = fmax3(__uint_as_float(v[b]), __uint_as_float(v[b + 1]), __uint_as_float(v[b + 2]));
+    float m1 = fmax3(__uint_as_float(v[b + 3]), __uint_as_float(v[b + 4]), __uint_as_float(v[b + 5]));
+#pragma unroll
+    for (int j = 6; j + 4 <= 30; j += 4) {
+        m0 = fmax3(m0, __uint_as_float(v[b + j]), __uint_as_float(v[b + j + 1]));
+        m1 = fmax3(m1, __uint_as_float(v[b + j + 2]), __uint_as_float(v[b + j + 3]));
+    }
+    return fmax3(m0, m1, fmaxf(__uint_as_float(v[b + 30]), __uint_as_float(v[b + 31])));
+}
+
 struct TcParams {
     const uint8_t* qimg;    // query tile images (hi+lo per 128-row tile)
     const uint8_t* kimg;    // key tile images (hi+lo per 128-key tile)
@@ -195,7 +209,16 @@ __device__ __forceinline__ bool k1_tile_update(uint32_t (&v)[W], int64_t kbase, 
         for (int j = 0; j < W; ++j)
             if (kbase + j >= p.key_valid) v[j] = __float_as_uint(-INFINITY);
     }
-    const float umax = row_max<W>(v) * p.acc_scale;
+    // per 32-column group maxima: a group whose terms are all < 2^-64 of the
+    // reference for every row of the warp skips its exponentials (same bound as
+    // the whole-tile skip); live blocks of a warm pass mostly hold a few near keys
+    constexpr int G = W / 32;
+    float gmax[G];
+#pragma unroll
+    for (int c = 0; c < G; ++c) gmax[c] = group_max32<W>(v, c) * p.acc_scale;
+    float umax = gmax[0];
+#pragma unroll
+    for (int c = 1; c < G; ++c) umax = fmaxf(umax, gmax[c]);
     umax_out = umax;
     if constexpr (VEC) {
         // P~ = 2^(t - L) <= 1; a tile whose P~ are all < 2^-64 for the warp's rows
@@ -223,13 +246,17 @@ __device__ __forceinline__ bool k1_tile_update(uint32_t (&v)[W], int64_t kbase, 
         __syncwarp();
         float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
-        for (int j = 0; j < W; j += 4) {
-            const float4 w = reinterpret_cast<const float4*>(vb)[j >> 2];
-            s0 = fmaf(ex2(fmaf(__uint_as_float(v[j]), p.acc_scale, nlh) + nll), w.x, s0);
-            s1 = fmaf(ex2(fmaf(__uint_as_float(v[j + 1]), p.acc_scale, nlh) + nll), w.y, s1);
-            s2 = fmaf(ex2(fmaf(__uint_as_float(v[j + 2]), p.acc_scale, nlh) + nll), w.z, s2);
-            const float x3 = fmaf(__uint_as_float(v[j + 3]), p.acc_scale, nlh) + nll;
-            s3 = fmaf(((j >> 2) & 3) != 3 ? ex2_poly(x3) : ex2(x3), w.w, s3);
+        for (int c = 0; c < G; ++c) {
+            if (__all_sync(0xffffffffu, gmax[c] + nlh < -kSkipLog2)) continue;
+#pragma unroll
+            for (int j = 32 * c; j < 32 * c + 32; j += 4) {
+                const float4 w = reinterpret_cast<const float4*>(vb)[j >> 2];
+                s0 = fmaf(ex2(fmaf(__uint_as_float(v[j]), p.acc_scale, nlh) + nll), w.x, s0);
+                s1 = fmaf(ex2(fmaf(__uint_as_float(v[j + 1]), p.acc_scale, nlh) + nll), w.y, s1);
+                s2 = fmaf(ex2(fmaf(__uint_as_float(v[j + 2]), p.acc_scale, nlh) + nll), w.z, s2);
+                const float x3 = fmaf(__uint_as_float(v[j + 3]), p.acc_scale, nlh) + nll;
+                s3 = fmaf(((j >> 2) & 3) != 3 ? ex2_poly(x3) : ex2(x3), w.w, s3);
+            }
         }
         S += double((s0 + s1) + (s2 + s3));
         __syncwarp();
@@ -246,14 +273,19 @@ __device__ __forceinline__ bool k1_tile_update(uint32_t (&v)[W], int64_t kbase, 
         const float nm = dead ? 0.0f : -M;
         float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
-        for (int j = 0; j < W; j += 4) {
-            s0 += ex2(fmaf(__uint_as_float(v[j]), p.acc_scale, nm));
-            s1 += ex2(fmaf(__uint_as_float(v[j + 1]), p.acc_scale, nm));
-            s2 += ex2(fmaf(__uint_as_float(v[j + 2]), p.acc_scale, nm));
-            // 3 of every 16 exponentials on the FMA pipe: MUFU (16/clk/SM) and the
-            // split-precision MMAs then bound a fully live tile about equally
-            const float x3 = fmaf(__uint_as_float(v[j + 3]), p.acc_scale, nm);
-            s3 += ((j >> 2) & 3) != 3 ? ex2_poly(x3) : ex2(x3);
+        for (int c = 0; c < G; ++c) {
+            if (!p.break_lse && __all_sync(0xffffffffu, dead || gmax[c] < M - kSkipLog2))
+                continue;
+#pragma unroll
+            for (int j = 32 * c; j < 32 * c + 32; j += 4) {
+                s0 += ex2(fmaf(__uint_as_float(v[j]), p.acc_scale, nm));
+                s1 += ex2(fmaf(__uint_as_float(v[j + 1]), p.acc_scale, nm));
+                s2 += ex2(fmaf(__uint_as_float(v[j + 2]), p.acc_scale, nm));
+                // 3 of every 16 exponentials on the FMA pipe: MUFU (16/clk/SM) and the
+                // split-precision MMAs then bound a fully live tile about equally
+                const float x3 = fmaf(__uint_as_float(v[j + 3]), p.acc_scale, nm);
+                s3 += ((j >> 2) & 3) != 3 ? ex2_poly(x3) : ex2(x3);
+            }
         }
         S += double((s0 + s1) + (s2 + s3));
         return true;
