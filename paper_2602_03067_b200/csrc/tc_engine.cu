@@ -478,6 +478,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
 // overlaps the epilogue of the other), query operand of tile t at 256 + 72 t:
 // hi (32 columns of fp16 pairs), lo (32), ones (8). The epilogue warps stage the
 // query operand themselves (tcgen05.st from the pre-split image) per work item.
+constexpr uint32_t kStageLast = 4u;  // stage_mask flag: last stage of the work item
 constexpr int TQ_STAGES = 6;
 constexpr uint32_t TQ_OFF_K = 0;
 constexpr uint32_t TQ_OFF_BAR = TQ_OFF_K + TQ_STAGES * KSTAGE;   // 216 KB
@@ -581,9 +582,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                     mbar_wait(screen_done, lu & 1);
                 }
                 int nlive = 0;
-                for (int kt = first_kt(unit, kt0, kt1); kt < kt1;
-                     kt = next_kt(unit, kt, kt0, kt1), ++it) {
+                int kt = first_kt(unit, kt0, kt1);
+                if (kt >= kt1) {
+                    // nothing live: one empty stage carrying only the end-of-item flag
                     const int s = it % TQ_STAGES;
+                    mbar_wait(kempty(s), ((it / TQ_STAGES) & 1) ^ 1);
+                    stage_mask[s] = kStageLast;
+                    mbar_arrive(kfull(s));
+                    ++it;
+                }
+                for (int kn; kt < kt1; kt = kn, ++it) {
+                    const int s = it % TQ_STAGES;
+                    kn = next_kt(unit, kt, kt0, kt1);
                     uint32_t mask = 3u;
                     if constexpr (SCREEN) {
                         const int rel = kt - kt0;
@@ -595,7 +605,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                     }
                     nlive += __popc(mask);
                     mbar_wait(kempty(s), ((it / TQ_STAGES) & 1) ^ 1);
-                    stage_mask[s] = mask;
+                    stage_mask[s] = mask | (kn >= kt1 ? kStageLast : 0u);
                     mbar_expect_tx(kfull(s), KSTAGE);
                     const uint32_t dst = base + TQ_OFF_K + s * KSTAGE;
                     bulk_g2s(dst, p.kimg + size_t(kt) * QTILE, QTILE, kfull(s));
@@ -624,7 +634,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
                 mbar_wait(qready, lu & 1);
                 fence_after();
-                auto tile_mmas = [&](bool screen_phase) {
+                auto tile_mmas = [&](bool screen_phase) -> uint32_t {
                     const int s = it % TQ_STAGES;
                     mbar_wait(kfull(s), (it / TQ_STAGES) & 1);
                     fence_after();
@@ -645,13 +655,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                     }
                     umma_commit<true>(kempty(s));
                     ++it;
+                    return mask;
                 };
                 if constexpr (SCREEN) {
                     for (int kt = kt0; kt < kt1; ++kt) tile_mmas(true);
                     mbar_wait(screen_done, lu & 1);
                 }
-                for (int kt = first_kt(unit, kt0, kt1); kt < kt1; kt = next_kt(unit, kt, kt0, kt1))
-                    tile_mmas(false);
+                // the producer walks the live sequence and flags its last stage: no
+                // global loads or divisions on the issue path
+                while (!(tile_mmas(false) & kStageLast)) {
+                }
                 if constexpr (SCREEN) {
                     __syncwarp();
                     if (lane == 0) mbar_arrive(bits_free);
