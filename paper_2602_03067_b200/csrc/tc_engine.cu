@@ -2488,7 +2488,15 @@ void TcHalfStep::grad(DevProblem<float>& P, int side, const float* kpot, const f
     p.q_tiles = int((row_end + TILE - 1) / TILE) - p.q_tile_begin;
     p.k_tiles = int(I.rows_pad[kc] / TILE);
     const int sms = num_sms();
-    p.splits = pick_splits(p.q_tiles, p.k_tiles, sms);
+    const bool sparse = I.live_valid[side] && I.live_kpot[side] == kpot &&
+                        I.live_row_begin[side] == row_begin && I.live_row_end[side] == row_end;
+    // a sparse live set desynchronizes the CTAs' key streams: L2-sized key ranges
+    // (split-major items), as in the warm LSE passes
+    const char* wsplit = std::getenv("FSK_WARM_SPLIT");
+    const int min_s = sparse && !(wsplit && wsplit[0] == '0')
+                          ? int(std::ceil(double(p.k_tiles) * KSTAGE / (40.0 * (1 << 20))))
+                          : 1;
+    p.splits = pick_splits(p.q_tiles, p.k_tiles, sms, min_s);
     p.items = p.q_tiles * p.splits;
     p.row_begin = row_begin;
     p.row_end = row_end;
@@ -2497,8 +2505,7 @@ void TcHalfStep::grad(DevProblem<float>& P, int side, const float* kpot, const f
     p.acc_scale = std::ldexp(1.0f, I.eq[qc] + I.ek[side]);
     p.l2h = L2h;
     p.l2l = L2l;
-    if (I.live_valid[side] && I.live_kpot[side] == kpot && I.live_row_begin[side] == row_begin &&
-        I.live_row_end[side] == row_end) {
+    if (sparse) {
         // the LSE pass above was screened: stream only its live key tiles
         p.live_global = I.live_glob[side].get();
         p.lse_splits = I.live_splits[side];
