@@ -498,7 +498,7 @@ def run_b200(args, cfgname):
         peak = peak_raw / mode_factor
         peak_src = (f"{pk_kind} bf16_tflops_sustained {peak_raw} / split-fp16 mode factor "
                     f"{mode_factor:.3f}")
-        kernel = "tc_lse_kernel<" + ("true" if chunks > 1 else "false") + ">"
+        kernel = "tc_lse_chunked_kernel<false>" if chunks > 1 else "tc_lse_tq_kernel<false, *>"
     else:
         mode_factor = 1.0
         peak = 2.0 * 128 * 148 * sm_clk * 1e6 / 1e12   # FP32 FMA at the sampled clock

@@ -735,6 +735,7 @@ int fsk_sinkhorn_divergence_batch(const fsk_measure* mus, const fsk_measure* nus
                                   const fsk_tiles* tiles, fsk_ledger* ledger, double* out) {
     return guarded([&] {
         validate_config_raw(*cfg);
+        UploadCacheScope uploads;   // each distinct cloud crosses the host link once
         for (int64_t k = 0; k < pairs; ++k) {
             common_checks(&mus[k], &nus[k], cost, tiles);
             const double cross = solve_dual(mus[k], nus[k], cost, *cfg, *tiles, ledger);

@@ -1,3 +1,6 @@
+#include <memory>
+#include <utility>
+#include <vector>
 #include <atomic>
 #include "device_ops.h"
 
@@ -90,8 +93,69 @@ void throw_for_flags(int flags, const std::string& suffix) {
 
 namespace {
 
+// Batch-scoped cache of uploaded measures, keyed by the caller's host buffers
+// (read-only for the duration of the call): a batch of solves over a few
+// distinct clouds ships each cloud over the host link once; later uses are
+// device-to-device copies.
+struct UploadKey {
+    const double* pts;
+    const double* w;
+    const int32_t* lab;
+    int64_t n, d;
+    bool labels;
+    bool operator==(const UploadKey& o) const {
+        return pts == o.pts && w == o.w && lab == o.lab && n == o.n && d == o.d &&
+               labels == o.labels;
+    }
+};
+template <typename T>
+using UploadCacheT = std::vector<std::pair<UploadKey, std::unique_ptr<DevSide<T>>>>;
+struct UploadCache {
+    UploadCacheT<float> f;
+    UploadCacheT<double> d;
+    template <typename T>
+    UploadCacheT<T>& get() {
+        if constexpr (std::is_same_v<T, float>) return f;
+        else return d;
+    }
+};
+thread_local UploadCache* t_upload_cache = nullptr;
+
+template <typename T>
+void copy_side(DevSide<T>& dst, const DevSide<T>& src, cudaStream_t s) {
+    dst.n = src.n;
+    dst.d = src.d;
+    auto cp = [&](auto& to, const auto& from) {
+        using E = std::remove_pointer_t<decltype(from.get())>;
+        if (!from.get()) return;
+        to.alloc(from.size(), s);
+        FSKB_CUDA(cudaMemcpyAsync(to.get(), from.get(), from.size() * sizeof(E),
+                                  cudaMemcpyDeviceToDevice, s));
+    };
+    cp(dst.pts, src.pts);
+    cp(dst.w, src.w);
+    cp(dst.logw, src.logw);
+    cp(dst.lab, src.lab);
+}
+
+template <typename T>
+void upload_side_host(DevSide<T>& side, const fsk_measure& m, bool want_labels, cudaStream_t s);
+
 template <typename T>
 void upload_side(DevSide<T>& side, const fsk_measure& m, bool want_labels, cudaStream_t s) {
+    if (!t_upload_cache) return upload_side_host(side, m, want_labels, s);
+    const UploadKey key{m.points, m.weights, m.labels, m.n, m.d, want_labels && m.labels};
+    auto& cache = t_upload_cache->get<T>();
+    for (auto& [k, v] : cache)
+        if (k == key) return copy_side(side, *v, s);
+    upload_side_host(side, m, want_labels, s);
+    auto keep = std::make_unique<DevSide<T>>();
+    copy_side(*keep, side, s);
+    cache.emplace_back(key, std::move(keep));
+}
+
+template <typename T>
+void upload_side_host(DevSide<T>& side, const fsk_measure& m, bool want_labels, cudaStream_t s) {
     side.n = m.n;
     side.d = m.d;
     side.pts.alloc(size_t(m.n * m.d), s);
@@ -118,6 +182,12 @@ void upload_side(DevSide<T>& side, const fsk_measure& m, bool want_labels, cudaS
 }
 
 }  // namespace
+
+UploadCacheScope::UploadCacheScope() : prev_(t_upload_cache) { t_upload_cache = new UploadCache; }
+UploadCacheScope::~UploadCacheScope() {
+    delete t_upload_cache;
+    t_upload_cache = static_cast<UploadCache*>(prev_);
+}
 
 template <typename T>
 void DevProblem<T>::upload(const fsk_measure& a, const fsk_measure& b, const fsk_cost* cost,

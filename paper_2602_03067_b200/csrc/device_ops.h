@@ -34,6 +34,18 @@ struct DevSide {
     int64_t n = 0, d = 0;
 };
 
+// While alive (one per host thread), DevProblem::upload ships each distinct
+// caller measure once and serves repeats from device copies (batch entry points).
+struct UploadCacheScope {
+    UploadCacheScope();
+    ~UploadCacheScope();
+    UploadCacheScope(const UploadCacheScope&) = delete;
+    UploadCacheScope& operator=(const UploadCacheScope&) = delete;
+
+  private:
+    void* prev_;
+};
+
 template <typename T>
 struct DevProblem {
     DevSide<T> src, tgt;

@@ -525,3 +525,21 @@ def test_tensor_degenerate_shapes(fsk, port, tensor_mode, n, m, d):
     r = port.sinkhorn_solve(X, a, Y, b, eps=eps, max_iters=3, precision="double")
     assert abs(s["dual_cost"] - r["dual_cost"]) <= 1e-5 * max(1.0, abs(r["dual_cost"]))
     assert np.all(np.isfinite(s["grad"]))
+
+
+@pytest.mark.parametrize("precision", ["single", "double"])
+def test_divergence_batch_matches_single_calls(fsk, precision):
+    """fsk_sinkhorn_divergence_batch (uploads each distinct cloud once per call and
+    serves repeats from device copies) returns exactly what per-pair
+    sinkhorn_divergence calls return; pairs reuse clouds in both roles."""
+    rng = np.random.default_rng(11)
+    d = 100 if precision == "single" else 8
+    clouds = [rng.normal(size=(300 + 37 * i, d)) * (1.0 + 0.1 * i) for i in range(3)]
+    ws = [np.full(len(c), 1.0 / len(c)) for c in clouds]
+    idx = [(0, 1), (1, 2), (2, 0), (0, 1), (1, 1)]
+    pairs = [(clouds[i], ws[i], clouds[j], ws[j]) for i, j in idx]
+    got = fsk.sinkhorn_divergence_batch(pairs, eps=0.5, max_iters=8, precision=precision)
+    want = [fsk.sinkhorn_divergence(X, a, Y, b, eps=0.5, max_iters=8, precision=precision)
+            for X, a, Y, b in pairs]
+    assert np.array_equal(got, np.array(want)), (got, want)
+    assert got[0] == got[3]

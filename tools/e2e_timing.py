@@ -2,7 +2,7 @@ import os, sys, time
 sys.path.insert(0, os.getcwd())
 import numpy as np
 import bench, paper_2602_03067_b200 as fsk
-n, m, d, eps, iters = bench.CONFIGS["cfg3"]
+n, m, d, eps, iters = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "cfg3"]
 X, Y = bench.make_inputs(n, m, d)
 a, b = bench.uniform_weights(n), bench.uniform_weights(m)
 for rep in range(2):
