@@ -55,7 +55,41 @@ namespace {
 
 // |x_i|^2 (core.cpp:83-96 squared_norms; same per-row summation order), rows
 // split across host threads for the large clouds.
+// Batch-scoped memo of per-measure host work (validation scans, squared norms),
+// keyed by the caller's buffers, which are read-only for the duration of a call.
+struct BatchMemo {
+    struct Key {
+        const double* pts;
+        const double* w;
+        int64_t n, d;
+        bool operator==(const Key& o) const {
+            return pts == o.pts && w == o.w && n == o.n && d == o.d;
+        }
+    };
+    std::vector<Key> validated;
+    std::vector<std::pair<std::pair<Key, double>, std::vector<double>>> sqnorms;
+};
+thread_local BatchMemo* t_batch_memo = nullptr;
+
+struct BatchMemoScope {
+    BatchMemo memo;
+    BatchMemo* prev;
+    BatchMemoScope() : prev(t_batch_memo) { t_batch_memo = &memo; }
+    ~BatchMemoScope() { t_batch_memo = prev; }
+};
+
+std::vector<double> host_sqnorm_compute(const fsk_measure& m, double scale);
+
 std::vector<double> host_sqnorm(const fsk_measure& m, double scale) {
+    if (!t_batch_memo) return host_sqnorm_compute(m, scale);
+    const BatchMemo::Key k{m.points, m.weights, m.n, m.d};
+    for (auto& [key, v] : t_batch_memo->sqnorms)
+        if (key.first == k && key.second == scale) return v;
+    t_batch_memo->sqnorms.push_back({{k, scale}, host_sqnorm_compute(m, scale)});
+    return t_batch_memo->sqnorms.back().second;
+}
+
+std::vector<double> host_sqnorm_compute(const fsk_measure& m, double scale) {
     std::vector<double> out((size_t)(m.n));
     auto rows = [&](int64_t i0, int64_t i1) {
         for (int64_t i = i0; i < i1; ++i) {
@@ -122,7 +156,21 @@ int bad_iteration(ExecCtx& C) {
 void common_checks(const fsk_measure* src, const fsk_measure* tgt, const fsk_cost* cost,
                    const fsk_tiles* tiles) {
     if (!src || !tgt) throw ValidationFailure("null measure");
-    validate_problem_raw(*src, *tgt, cost);
+    if (t_batch_memo) {
+        // scan each distinct measure of a batch once (same checks, same order)
+        for (const fsk_measure* m : {src, tgt}) {
+            const BatchMemo::Key k{m->points, m->weights, m->n, m->d};
+            bool seen = false;
+            for (auto& v : t_batch_memo->validated) seen = seen || v == k;
+            if (!seen) {
+                validate_measure_raw(*m);
+                if (m->labels == nullptr) t_batch_memo->validated.push_back(k);
+            }
+        }
+        validate_problem_raw(*src, *tgt, cost, /*measures_checked=*/true);
+    } else {
+        validate_problem_raw(*src, *tgt, cost);
+    }
     validate_tiles_raw(tiles);
 }
 
@@ -736,6 +784,7 @@ int fsk_sinkhorn_divergence_batch(const fsk_measure* mus, const fsk_measure* nus
     return guarded([&] {
         validate_config_raw(*cfg);
         UploadCacheScope uploads;   // each distinct cloud crosses the host link once
+        BatchMemoScope memo;        // and is scanned / normed on the host once
         for (int64_t k = 0; k < pairs; ++k) {
             common_checks(&mus[k], &nus[k], cost, tiles);
             const double cross = solve_dual(mus[k], nus[k], cost, *cfg, *tiles, ledger);

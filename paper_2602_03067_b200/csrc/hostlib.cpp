@@ -36,9 +36,12 @@ void validate_measure_raw(const fsk_measure& m) {
     }
 }
 
-void validate_problem_raw(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* cost) {
-    validate_measure_raw(src);
-    validate_measure_raw(tgt);
+void validate_problem_raw(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* cost,
+                          bool measures_checked) {
+    if (!measures_checked) {
+        validate_measure_raw(src);
+        validate_measure_raw(tgt);
+    }
     if (src.d != tgt.d)
         throw ValidationFailure("source dimension " + std::to_string(src.d) +
                                 " != target dimension " + std::to_string(tgt.d));

@@ -13,7 +13,9 @@ namespace fskb {
 
 // ---- validation (proj/src/core.cpp:18-81, stream.cpp:253-259) -------------
 void validate_measure_raw(const fsk_measure& m);
-void validate_problem_raw(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* cost);
+// measures_checked: validate_measure_raw already ran on both (batch entry points)
+void validate_problem_raw(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* cost,
+                          bool measures_checked = false);
 void validate_config_raw(const fsk_config& cfg);
 void validate_tiles_raw(const fsk_tiles* tiles);
 bool all_finite(const double* p, int64_t n);

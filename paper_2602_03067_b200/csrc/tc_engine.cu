@@ -27,6 +27,9 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <mutex>
+#include <utility>
+#include <vector>
 #include <climits>
 #include <cstdlib>
 #include <cmath>
@@ -1847,6 +1850,39 @@ int pick_splits(int units, int k_tiles, int sms, int min_splits = 1) {
     return best;
 }
 
+// Pinned probe words and their events, pooled per device: a solve creates and
+// drops a TcHalfStep, and cudaFreeHost synchronizes the whole device.
+struct ProbeBufs {
+    unsigned long long* h;
+    cudaEvent_t ev[2];
+};
+std::mutex g_probe_mu;
+std::vector<std::pair<int, ProbeBufs>> g_probe_pool;
+
+void acquire_probe_bufs(int dev, unsigned long long*& h, cudaEvent_t (&ev)[2]) {
+    {
+        std::lock_guard<std::mutex> lk(g_probe_mu);
+        for (size_t i = 0; i < g_probe_pool.size(); ++i)
+            if (g_probe_pool[i].first == dev) {
+                h = g_probe_pool[i].second.h;
+                ev[0] = g_probe_pool[i].second.ev[0];
+                ev[1] = g_probe_pool[i].second.ev[1];
+                g_probe_pool.erase(g_probe_pool.begin() + long(i));
+                return;
+            }
+    }
+    FSKB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h), 2 * sizeof(unsigned long long),
+                            cudaHostAllocDefault));
+    for (auto& e : ev) FSKB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
+
+void release_probe_bufs(int dev, unsigned long long* h, const cudaEvent_t (&ev)[2]) {
+    // a probe still in flight must land before the words are handed out again
+    for (auto e : ev) cudaEventSynchronize(e);
+    std::lock_guard<std::mutex> lk(g_probe_mu);
+    g_probe_pool.push_back({dev, ProbeBufs{h, {ev[0], ev[1]}}});
+}
+
 struct TcHalfStep::Impl {
     int64_t rows_pad[2] = {0, 0};   // padded rows of each side's cloud (0: X, 1: Y)
     int64_t npts[2] = {0, 0};
@@ -1890,10 +1926,9 @@ struct TcHalfStep::Impl {
     bool warm_ok[2] = {false, false}, last_warm_track[2] = {false, false};
     int64_t warm_rb[2] = {0, 0}, warm_re[2] = {0, 0};
     unsigned long long warm_blocks = 0;
+    int probe_dev = -1;
     ~Impl() {
-        for (auto& e : ev)
-            if (e) cudaEventDestroy(e);
-        if (h_live) cudaFreeHost(h_live);
+        if (h_live) release_probe_bufs(probe_dev, h_live, ev);
     }
 };
 
@@ -2017,9 +2052,8 @@ void TcHalfStep::set_eps(DevProblem<float>& P, double eps) {
     if (!impl_->live_count.get()) {
         impl_->live_count.alloc(2, P.s);
         impl_->live_count.zero();
-        FSKB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&impl_->h_live),
-                                2 * sizeof(unsigned long long), cudaHostAllocDefault));
-        for (auto& e : impl_->ev) FSKB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        FSKB_CUDA(cudaGetDevice(&impl_->probe_dev));
+        acquire_probe_bufs(impl_->probe_dev, impl_->h_live, impl_->ev);
     }
     // side 0 (f-update): keys = Y (cloud 1); side 1 (g-update): keys = X (cloud 0)
     for (int side = 0; side < 2; ++side) {
