@@ -73,7 +73,17 @@ class ClockSampler:
         self.rows = []
         self.proc = None
 
-    def start(self):
+    def start(self, wait_first=True):
+        """Starts sampling every 200 ms; waits (<= 3 s) for the first sample so that a
+        short timed region still sees one."""
+        self._start()
+        if wait_first and self.proc is not None:
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 3.0:
+                time.sleep(0.01)
+        self.n0 = len(self.rows)
+
+    def _start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -93,6 +103,11 @@ class ClockSampler:
     def stop(self):
         if self.proc is None:
             return None
+        # a region shorter than the sampling period: take the next sample as well
+        t0 = time.time()
+        while len(self.rows) <= getattr(self, "n0", 0) and time.time() - t0 < 1.0:
+            time.sleep(0.01)
+        self.rows = self.rows[max(0, getattr(self, "n0", 0) - 1):]
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
