@@ -38,6 +38,11 @@ enum : int {
     kFlagNonFiniteColMarginal = 16,
 };
 
+// Large caller-buffer copies through pooled pinned staging (hostcopy.cpp);
+// synchronous with respect to the host buffer (it may be reused on return).
+void copy_host_to_device(void* dst, const void* src, std::size_t bytes, cudaStream_t s);
+void copy_device_to_host(void* dst, const void* src, std::size_t bytes, cudaStream_t s);
+
 // Plain owning device buffer (stream-ordered allocation).
 template <typename T>
 class DevBuf {
@@ -73,10 +78,11 @@ public:
     T* get() const { return p_; }
     std::size_t size() const { return n_; }
     void upload(const T* host, std::size_t n) {
-        if (n) FSKB_CUDA(cudaMemcpyAsync(p_, host, n * sizeof(T), cudaMemcpyHostToDevice, s_));
+        if (n) copy_host_to_device(p_, host, n * sizeof(T), s_);
     }
+    // completes before returning for large copies (staged), else stream-ordered
     void download(T* host, std::size_t n) const {
-        if (n) FSKB_CUDA(cudaMemcpyAsync(host, p_, n * sizeof(T), cudaMemcpyDeviceToHost, s_));
+        if (n) copy_device_to_host(host, p_, n * sizeof(T), s_);
     }
     void zero() {
         if (n_) FSKB_CUDA(cudaMemsetAsync(p_, 0, n_ * sizeof(T), s_));
