@@ -1,6 +1,10 @@
 #include "hostlib.h"
 
+#include <algorithm>
 #include <cmath>
+#include <cstdint>
+#include <thread>
+#include <vector>
 #include <limits>
 
 #include "../../include/fsk/rng.hpp"
@@ -12,9 +16,32 @@ namespace {
 std::string num(double v) { return std::to_string(v); }
 }  // namespace
 
+namespace {
+// non-finite <=> all exponent bits set: a branch-free integer scan (vectorizes)
+bool finite_range(const double* p, int64_t n) {
+    const uint64_t* b = reinterpret_cast<const uint64_t*>(p);
+    uint64_t bad = 0;
+    for (int64_t i = 0; i < n; ++i) bad |= uint64_t((b[i] & 0x7FF0000000000000ull) == 0x7FF0000000000000ull);
+    return bad == 0;
+}
+}  // namespace
+
 bool all_finite(const double* p, int64_t n) {
-    for (int64_t i = 0; i < n; ++i)
-        if (!std::isfinite(p[i])) return false;
+    const int64_t per = int64_t(1) << 22;
+    if (n < 2 * per) return finite_range(p, n);
+    // the cloud scan runs on every validated call: split it over host threads
+    const int T = int(std::min<int64_t>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())),
+                                        n / per));
+    std::vector<char> ok(size_t(T), 1);
+    std::vector<std::thread> th;
+    for (int t = 0; t < T; ++t)
+        th.emplace_back([&, t] {
+            const int64_t lo = n * t / T, hi = n * (t + 1) / T;
+            ok[size_t(t)] = finite_range(p + lo, hi - lo) ? 1 : 0;
+        });
+    for (auto& x : th) x.join();
+    for (char v : ok)
+        if (!v) return false;
     return true;
 }
 
