@@ -200,6 +200,15 @@ void hvp_run(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat
         fb.out_l2h = l2h_g.get();
         fb.out_l2l = l2l_g.get();
         half_step<T>(P, 1, f.get(), T(eps), fb);
+        if constexpr (kSingle) {
+            // every transport pass below runs at these potentials: seed exact row maxima
+            // so the recorded live sets hold only blocks within 2^-64 of a row max
+            if (P.tc) {
+                P.s = C.s;
+                P.tc->tighten_live(P, 0, g.get(), float(eps), mx_f.get(), C.flags);
+                P.tc->tighten_live(P, 1, f.get(), float(eps), mx_g.get(), C.flags);
+            }
+        }
         ledger_marginals(ledger, n, m, d, *tiles, cost);
         std::vector<double> r((size_t)(n)), c((size_t)(m));
         {

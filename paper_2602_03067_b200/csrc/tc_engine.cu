@@ -415,6 +415,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
             const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
             const int64_t row = int64_t(qt0 + t) * TILE + quarter * 32 + lane;
             float M = -INFINITY;
+            if (!VEC && p.m_init && t < nq && row >= p.row_begin && row < p.row_end)
+                M = p.m_init[row];
             double S = 0.0;
             float nlh = 0.0f, nll = 0.0f;
             if constexpr (VEC) {
@@ -2078,7 +2080,7 @@ void TcHalfStep::set_eps(DevProblem<float>& P, double eps) {
 // transport-vector partials (vec = {l2h, l2l, v}) into pm (and ps), per key split.
 int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float eps,
                      int64_t row_begin, int64_t row_end, const float* const* vec, int* flags,
-                     DevBuf<double>& pm, DevBuf<double>& ps) {
+                     DevBuf<double>& pm, DevBuf<double>& ps, const float* m_init) {
     Impl& I = *impl_;
     const int qc = side == 0 ? 0 : 1, kc = side == 0 ? 1 : 0;
     const DevSide<float>& ks = side == 0 ? P.tgt : P.src;
@@ -2293,6 +2295,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         p.in_kps = I.live_kps[side];
         p.in_kwords = I.live_kwords[side];
     }
+    if (m_init && !vec) p.m_init = m_init;
     if (I.chunks == 1) {
         if (vec)
             tc_lse_tq_kernel<true, false><<<grid, NUM_THREADS, TQ_SMEM_BYTES, P.s>>>(p);
@@ -2344,6 +2347,27 @@ void TcHalfStep::run(DevProblem<float>& P, int side, const float* kpot, float ep
         I.b_valid[side] = true;
         I.bcur[side] ^= 1;
     }
+}
+
+__global__ void seed_from_max_kernel(const float* __restrict__ mx_nat, int64_t n,
+                                     float* __restrict__ m_init) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    // natural-log row max of a pass at the same potentials -> kernel log2 units, one
+    // binade of margin for its fp32 rounding: a valid lower bound of the row max
+    const float v = mx_nat[i] * 1.4426950408889634f - 1.0f;
+    m_init[i] = isfinite(v) ? v : -INFINITY;
+}
+
+void TcHalfStep::tighten_live(DevProblem<float>& P, int side, const float* kpot, float eps,
+                              const float* mx_nat, int* flags) {
+    const int64_t R = side == 0 ? P.src.n : P.tgt.n;
+    DevBuf<float> seed(size_t(R), P.s);
+    seed_from_max_kernel<<<unsigned((R + 255) / 256), 256, 0, P.s>>>(mx_nat, R, seed.get());
+    FSKB_CUDA(cudaGetLastError());
+    count_launch();
+    DevBuf<double> pm, ps;
+    pass(P, side, kpot, eps, 0, R, nullptr, flags, pm, ps, seed.get());
 }
 
 void TcHalfStep::vec(DevProblem<float>& P, int side, const float* kpot, float eps,

@@ -55,6 +55,14 @@ public:
               const float* pre_l2h = nullptr, const float* pre_l2l = nullptr,
               const float* pre_r = nullptr);
 
+    // Re-records the live key-tile set of `side` at fixed potentials with every
+    // row's running max seeded just below its true max (mx_nat: the natural-log row
+    // max of a pass at the same potentials): only tiles holding terms within 2^-64
+    // of a row's max stay live, so the transport passes that follow (HVP/CG) skip
+    // the rest. One extra LSE pass.
+    void tighten_live(DevProblem<float>& P, int side, const float* kpot, float eps,
+                      const float* mx_nat, int* flags);
+
     // Transport-vector application with fixed potentials: out_i = marg_i sum_j
     // 2^(t_ij - L_i) v_j = (P v)_i (side 0) or (P^T v)_j (side 1), given the row
     // LSE of that orientation in log2 units (l2h + l2l) and its induced marginal
@@ -76,7 +84,7 @@ private:
     void poll_screen(int side, double max_live);
     int pass(DevProblem<float>& P, int side, const float* kpot, float eps, int64_t row_begin,
              int64_t row_end, const float* const* vec, int* flags, DevBuf<double>& pm,
-             DevBuf<double>& ps);
+             DevBuf<double>& ps, const float* m_init = nullptr);
     struct Impl;
     Impl* impl_;
 };
