@@ -426,6 +426,20 @@ void launch_neg_sqnorm(const T* P, int64_t n, int64_t d, T scale, T* out, cudaSt
     count_launch();
 }
 
+__global__ void scale_rows_kernel(const float* __restrict__ Y, const double* __restrict__ w,
+                                  int64_t m, int64_t d, float* __restrict__ out) {
+    for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < m * d;
+         k += int64_t(gridDim.x) * blockDim.x)
+        out[k] = float(w[k / d] * double(Y[k]));
+}
+void launch_scale_rows(const float* Y, const double* w, int64_t m, int64_t d, float* out,
+                       cudaStream_t s) {
+    if (!m || !d) return;
+    scale_rows_kernel<<<blocks_for(m * d), 256, 0, s>>>(Y, w, m, d, out);
+    FSKB_CUDA(cudaGetLastError());
+    count_launch();
+}
+
 void launch_f64_to_f32(const double* in, float* out, int64_t n, cudaStream_t s) {
     if (!n) return;
     f64_to_f32_kernel<<<blocks_for(n), 256, 0, s>>>(in, out, n);

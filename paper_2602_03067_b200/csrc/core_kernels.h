@@ -87,6 +87,9 @@ void launch_log(const T* in, T* out, int64_t n, cudaStream_t s);
 template <typename T>
 void launch_neg_sqnorm(const T* P, int64_t n, int64_t d, T scale, T* out, cudaStream_t s);
 void launch_f64_to_f32(const double* in, float* out, int64_t n, cudaStream_t s);
+// out (m x d) = diag(w) Y, rounded to float
+void launch_scale_rows(const float* Y, const double* w, int64_t m, int64_t d, float* out,
+                       cudaStream_t s);
 void launch_f32_to_f64(const float* in, double* out, int64_t n, cudaStream_t s);
 // G_i = 2 (r_i X_i - O_i) with r_i = w_i exp(pot_i/eps + lse_i)
 template <typename T>

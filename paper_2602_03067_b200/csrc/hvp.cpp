@@ -67,6 +67,29 @@ struct HvpCtx {
     // side 0: out (n x p) = P V ; side 1: out (m x p) = P^T V
     std::vector<double> apply(int side, const std::vector<double>& V, int64_t p,
                               const double* A = nullptr, const double* B = nullptr, int64_t r = 0) {
+        return apply(side, V.data(), p, A, B, r);
+    }
+    // tensor path, V already on the device (float, cols x p): out (host doubles)
+    std::vector<double> apply_dev(int side, const float* vd, int64_t p) {
+        const int64_t rows = side == 0 ? src.n : tgt.n;
+        const T* kpot = side == 0 ? gd : fd;
+        std::vector<double> h((size_t)(rows * p));
+        if constexpr (std::is_same_v<T, float>) {
+            DevBuf<float> out(size_t(rows * p), C.s);
+            P.s = C.s;
+            P.tc->apply_mat(P, side, kpot, float(eps), l2h[side], l2l[side], marg[side], vd, p,
+                            out.get(), C.flags, nullptr);
+            DevBuf<double> wide(size_t(rows * p), C.s);
+            launch_f32_to_f64(out.get(), wide.get(), rows * p, C.s);
+            wide.download(h.data(), h.size());
+            FSKB_CUDA(cudaStreamSynchronize(C.s));
+        }
+        ledger_apply(ledger, src.n, tgt.n, src.d, p, tiles, cost, side == 1);
+        return h;
+    }
+    // V: the caller's (cols x p) row-major doubles, read in place
+    std::vector<double> apply(int side, const double* V, int64_t p, const double* A = nullptr,
+                              const double* B = nullptr, int64_t r = 0) {
         const int64_t rows = side == 0 ? src.n : tgt.n, cols = side == 0 ? tgt.n : src.n;
         const T* kpot = side == 0 ? gd : fd;
         const T* pot = side == 0 ? fd : gd;
@@ -77,7 +100,7 @@ struct HvpCtx {
             const bool had_ok = A && side == 0 && B == tgt.points && r == src.d;
             if (P.tc && ((!A && p > 1) || had_ok)) {
                 // ship the host doubles as they are, narrow / widen on the device
-                DevBuf<float> vd = narrow_on_device(V.data(), cols * p, C.s);
+                DevBuf<float> vd = narrow_on_device(V, cols * p, C.s);
                 DevBuf<float> ad;
                 if (A) ad = narrow_on_device(A, src.n * r, C.s);
                 DevBuf<float> out(size_t(rows * p), C.s);
@@ -90,7 +113,7 @@ struct HvpCtx {
                 FSKB_CUDA(cudaStreamSynchronize(C.s));
                 done = true;
             } else if (P.tc && !A && p == 1) {
-                DevBuf<float> vd = narrow_on_device(V.data(), cols, C.s);
+                DevBuf<float> vd = narrow_on_device(V, cols, C.s);
                 DevBuf<double> out(size_t(rows), C.s);
                 P.s = C.s;
                 P.tc->vec(P, side, kpot, float(eps), l2h[side], l2l[side], marg[side], vd.get(),
@@ -102,7 +125,7 @@ struct HvpCtx {
         }
         if (!done) {
             DevBuf<T> Vd(size_t(cols * p), C.s), out(size_t(rows * p), C.s);
-            const std::vector<T> Vt(V.begin(), V.end());
+            const std::vector<T> Vt(V, V + cols * p);
             Vd.upload(Vt.data(), size_t(cols * p));
             DevBuf<T> Ad, Bd;
             if (A) {
@@ -232,10 +255,15 @@ void hvp_run(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat
         H.l2l[1] = l2l_g.get();
         H.marg[0] = r_d.get();
         H.marg[1] = c_d.get();
-        const std::vector<double> X(src->points, src->points + n * d);
-        const std::vector<double> Y(tgt->points, tgt->points + m * d);
-        const std::vector<double> Av(A, A + n * d);
-        const std::vector<double> PY = H.apply(0, Y, d);  // cached transport-matrix product
+        // the caller's clouds and direction, read in place (no host copies of n x d)
+        const double* X = src->points;
+        const double* Y = tgt->points;
+        const double* Av = A;
+        // cached transport-matrix product; on the tensor path V = Y is the resident cloud
+        const bool tc_mat = kSingle && P.tc && d > 1;
+        const std::vector<double> PY =
+            tc_mat ? H.apply_dev(0, reinterpret_cast<const float*>(P.tgt.pts.get()), d)
+                   : H.apply(0, Y, d);
         timer.mark("hvp P Y");
 
         // build_rhs
@@ -309,10 +337,22 @@ void hvp_run(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat
         const std::vector<double> Pw2 = H.apply(0, w2, 1);
         std::vector<double> w1((size_t)(n));
         for (int64_t i = 0; i < n; ++i) w1[size_t(i)] = (r1[size_t(i)] - Pw2[size_t(i)]) / r[size_t(i)];
-        std::vector<double> w2Y((size_t)(m * d));
-        for (int64_t j = 0; j < m; ++j)
-            for (int64_t t = 0; t < d; ++t) w2Y[size_t(j * d + t)] = w2[size_t(j)] * Y[size_t(j * d + t)];
-        const std::vector<double> Pw2Y = H.apply(0, w2Y, d);
+        std::vector<double> Pw2Y;
+        if (tc_mat) {
+            // V = diag(w2) Y built on the device from the resident cloud
+            DevBuf<double> w2d(size_t(m), C.s);
+            w2d.upload(w2.data(), size_t(m));
+            DevBuf<float> w2Yd(size_t(m * d), C.s);
+            launch_scale_rows(reinterpret_cast<const float*>(P.tgt.pts.get()), w2d.get(), m, d,
+                              w2Yd.get(), C.s);
+            Pw2Y = H.apply_dev(0, w2Yd.get(), d);
+        } else {
+            std::vector<double> w2Y((size_t)(m * d));
+            for (int64_t j = 0; j < m; ++j)
+                for (int64_t t = 0; t < d; ++t)
+                    w2Y[size_t(j * d + t)] = w2[size_t(j)] * Y[size_t(j * d + t)];
+            Pw2Y = H.apply(0, w2Y, d);
+        }
         // explicit term: B5 = (P (.) A Y^T) Y
         timer.mark("hvp P w2, P (w2 Y)");
         const std::vector<double> B5 = H.apply(0, Y, d, A, tgt->points, d);
