@@ -5,7 +5,9 @@
 // Operation count per call: 2 K_CG + 3 transport-vector, 3 transport-matrix
 // (PY, P^T A, P(diag(w2) Y)) and 1 Hadamard-weighted transport.
 #include <cmath>
+#include <algorithm>
 #include <cstring>
+#include <thread>
 #include <type_traits>
 #include <vector>
 
@@ -32,6 +34,26 @@ DevBuf<float> narrow_on_device(const double* h, int64_t n, cudaStream_t s) {
     launch_f64_to_f32(tmp.get(), out.get(), n, s);
     FSKB_CUDA(cudaStreamSynchronize(s));
     return out;
+}
+
+// Rows are independent (each row's sums run in order): split the host n x d
+// loops of the HVP assembly over host threads, bit-identical to the serial loop.
+template <typename F>
+void parallel_rows(int64_t rows, int64_t per_row, F&& f) {
+    const int64_t work = rows * per_row;
+    const int T = work < (int64_t(1) << 22)
+                      ? 1
+                      : int(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+    if (T == 1) {
+        for (int64_t i = 0; i < rows; ++i) f(i);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int t = 0; t < T; ++t)
+        th.emplace_back([&, t] {
+            for (int64_t i = rows * t / T; i < rows * (t + 1) / T; ++i) f(i);
+        });
+    for (auto& x : th) x.join();
 }
 
 template <typename T>
@@ -268,7 +290,7 @@ void hvp_run(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat
 
         // build_rhs
         std::vector<double> u((size_t)(n)), uP((size_t)(n)), r1((size_t)(n));
-        for (int64_t i = 0; i < n; ++i) {
+        parallel_rows(n, d, [&](int64_t i) {
             double su = 0.0, sp = 0.0;
             for (int64_t t = 0; t < d; ++t) {
                 su += X[size_t(i * d + t)] * Av[size_t(i * d + t)];
@@ -277,15 +299,15 @@ void hvp_run(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat
             u[size_t(i)] = su;
             uP[size_t(i)] = sp;
             r1[size_t(i)] = 2.0 * (r[size_t(i)] * su - sp);
-        }
+        });
         const std::vector<double> Ptu = H.apply(1, u, 1);
         const std::vector<double> PtA = H.apply(1, Av, d);
         std::vector<double> r2((size_t)(m));
-        for (int64_t j = 0; j < m; ++j) {
+        parallel_rows(m, d, [&](int64_t j) {
             double s = 0.0;
             for (int64_t t = 0; t < d; ++t) s += PtA[size_t(j * d + t)] * Y[size_t(j * d + t)];
             r2[size_t(j)] = 2.0 * (Ptu[size_t(j)] - s);
-        }
+        });
         // Schur right-hand side r2 - P^T diag(r)^-1 r1
         std::vector<double> tmp((size_t)(n));
         for (int64_t i = 0; i < n; ++i) tmp[size_t(i)] = r1[size_t(i)] / r[size_t(i)];
@@ -357,7 +379,7 @@ void hvp_run(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat
         timer.mark("hvp P w2, P (w2 Y)");
         const std::vector<double> B5 = H.apply(0, Y, d, A, tgt->points, d);
         timer.mark("hvp Hadamard");
-        for (int64_t i = 0; i < n; ++i) {
+        parallel_rows(n, d, [&](int64_t i) {
             const double ri = r[size_t(i)], ui = u[size_t(i)], upi = uP[size_t(i)];
             for (int64_t t = 0; t < d; ++t) {
                 const size_t k = size_t(i * d + t);
@@ -367,7 +389,7 @@ void hvp_run(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat
                                   (4.0 / eps) * (ri * ui * X[k] - ui * PY[k] - upi * X[k] + B5[k]);
                 out[k] = rtw / eps + ea;
             }
-        }
+        });
         timer.mark("hvp assemble");
         throw_for_flags(read_and_clear_flags(C) & ~kFlagNonFinitePotential);
         if (hrep) {
