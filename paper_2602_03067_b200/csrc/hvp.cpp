@@ -252,6 +252,10 @@ void hvp_run(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat
                 P.s = C.s;
                 P.tc->tighten_live(P, 0, g.get(), float(eps), mx_f.get(), C.flags);
                 P.tc->tighten_live(P, 1, f.get(), float(eps), mx_g.get(), C.flags);
+                // the ~100 transport-vector passes of the CG then sweep the live blocks
+                // of the plan kept in HBM instead of recomputing their scores
+                P.tc->build_plan(P, g.get(), f.get(), float(eps), l2h_f.get(), l2l_f.get(),
+                                 r_d.get(), C.flags);
             }
         }
         ledger_marginals(ledger, n, m, d, *tiles, cost);

@@ -153,6 +153,11 @@ struct TcParams {
     // warm LSE passes: per-row lower bound of this pass's row max (log2 units),
     // the running max starts there (tighter gaps, earlier in-epilogue skips)
     const float* m_init;
+    // VEC passes (chunked kernel): also store each visited block's row-normalized
+    // plan entries 2^(t - L) to plan_out[plan_slot[unit * k_tiles + kt]] (256 x 128
+    // fp32, row-major; slot < 0: not stored)
+    float* plan_out;
+    const int* plan_slot;
 };
 
 // Work items run split-major: the CTAs running at the same time share one key
@@ -446,6 +451,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
                 __syncwarp();
                 if (lane == 0) mbar_arrive(accempty);
                 if (t >= nq) continue;
+                if (VEC && p.plan_out) {
+                    const int slot = p.plan_slot[size_t(unit) * p.k_tiles + kt];
+                    if (slot >= 0) {
+                        float4* dst = reinterpret_cast<float4*>(
+                            p.plan_out + (size_t(slot) * 2 * TILE + size_t(t * TILE + quarter * 32 + lane)) * TILE);
+                        const int64_t kb = int64_t(kt) * TILE;
+#pragma unroll
+                        for (int j = 0; j < TILE; j += 4) {
+                            float e[4];
+#pragma unroll
+                            for (int c = 0; c < 4; ++c)
+                                e[c] = kb + j + c < p.key_valid
+                                           ? ex2(fmaf(__uint_as_float(v[j + c]), p.acc_scale, nlh) + nll)
+                                           : 0.0f;
+                            dst[j >> 2] = make_float4(e[0], e[1], e[2], e[3]);
+                        }
+                    }
+                }
                 float umax;
                 const bool hit = k1_tile_update<VEC>(v, int64_t(kt) * TILE, p, M, S, nlh, nll, vb,
                                                      lane, umax);
@@ -1925,6 +1948,13 @@ struct TcHalfStep::Impl {
     DevBuf<int> tdmax[2], tdmin[2], gap[2], argtile[2], part_arg[2], lam[2];
     DevBuf<float> rowmax[2], minit[2];  // last row max (log2), next pass's lower bound
     DevBuf<uint32_t> warm_live[2];
+    // HBM-resident plan blocks (build_plan)
+    DevBuf<float> plan;
+    DevBuf<int> plan_slot, plan_uptr, plan_ukt, plan_uslot, plan_kptr, plan_kunit, plan_kslot;
+    bool plan_valid = false;
+    const float* plan_kpot[2] = {nullptr, nullptr};
+    const float* plan_r = nullptr;
+    int plan_units = 0, plan_k_tiles = 0, plan_blocks = 0;
     bool warm_ok[2] = {false, false}, last_warm_track[2] = {false, false};
     int64_t warm_rb[2] = {0, 0}, warm_re[2] = {0, 0};
     unsigned long long warm_blocks = 0;
@@ -2080,7 +2110,8 @@ void TcHalfStep::set_eps(DevProblem<float>& P, double eps) {
 // transport-vector partials (vec = {l2h, l2l, v}) into pm (and ps), per key split.
 int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float eps,
                      int64_t row_begin, int64_t row_end, const float* const* vec, int* flags,
-                     DevBuf<double>& pm, DevBuf<double>& ps, const float* m_init) {
+                     DevBuf<double>& pm, DevBuf<double>& ps, const PassExtras* ex) {
+    const float* m_init = ex ? ex->m_init : nullptr;
     Impl& I = *impl_;
     const int qc = side == 0 ? 0 : 1, kc = side == 0 ? 1 : 0;
     const DevSide<float>& ks = side == 0 ? P.tgt : P.src;
@@ -2296,6 +2327,17 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         p.in_kwords = I.live_kwords[side];
     }
     if (m_init && !vec) p.m_init = m_init;
+    if (ex && ex->live_in) {   // caller-supplied live set (plan materialization)
+        p.live_in = ex->live_in;
+        p.in_splits = ex->in_splits;
+        p.in_kps = ex->in_kps;
+        p.in_kwords = ex->in_kwords;
+        p.live_tq = 0;
+    }
+    if (ex && vec) {
+        p.plan_out = ex->plan_out;
+        p.plan_slot = ex->plan_slot;
+    }
     if (I.chunks == 1) {
         if (vec)
             tc_lse_tq_kernel<true, false><<<grid, NUM_THREADS, TQ_SMEM_BYTES, P.s>>>(p);
@@ -2367,7 +2409,220 @@ void TcHalfStep::tighten_live(DevProblem<float>& P, int side, const float* kpot,
     FSKB_CUDA(cudaGetLastError());
     count_launch();
     DevBuf<double> pm, ps;
-    pass(P, side, kpot, eps, 0, R, nullptr, flags, pm, ps, seed.get());
+    PassExtras ex{};
+    ex.m_init = seed.get();
+    pass(P, side, kpot, eps, 0, R, nullptr, flags, pm, ps, &ex);
+}
+
+// ---- HBM-resident transport plan (live blocks only) ---------------------------
+//
+// At fixed potentials (the HVP's CG) every transport-vector pass recomputes the
+// same scores. The plan cache keeps the row-normalized entries 2^(t - L_i) of the
+// live (query tile pair, key tile) blocks of the side-0 orientation (the union of
+// both orientations' live sets) as 256 x 128 fp32 blocks; P v and P^T u then are
+// memory-bound sweeps over it. Unit-major (CSR) and key-tile-major (CSC) block
+// lists index the same blocks.
+__global__ void plan_pv_kernel(const float* __restrict__ plan, const int* __restrict__ uptr,
+                               const int* __restrict__ ukt, const int* __restrict__ uslot,
+                               const float* __restrict__ v, int64_t key_valid,
+                               const float* __restrict__ marg, int64_t R, double* __restrict__ out) {
+    __shared__ float vs[TILE];
+    const int unit = blockIdx.x;
+    const int64_t row = int64_t(unit) * 2 * TILE + threadIdx.x;
+    double acc = 0.0;
+    for (int b = uptr[unit]; b < uptr[unit + 1]; ++b) {
+        const int kt = ukt[b];
+        __syncthreads();
+        if (threadIdx.x < TILE) {
+            const int64_t j = int64_t(kt) * TILE + threadIdx.x;
+            vs[threadIdx.x] = j < key_valid ? v[j] : 0.0f;
+        }
+        __syncthreads();
+        const float4* rp =
+            reinterpret_cast<const float4*>(plan + (size_t(uslot[b]) * 2 * TILE + threadIdx.x) * TILE);
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll 8
+        for (int c = 0; c < TILE / 4; ++c) {
+            const float4 q = __ldg(rp + c);
+            s0 = fmaf(q.x, vs[4 * c], s0);
+            s1 = fmaf(q.y, vs[4 * c + 1], s1);
+            s2 = fmaf(q.z, vs[4 * c + 2], s2);
+            s3 = fmaf(q.w, vs[4 * c + 3], s3);
+        }
+        acc += double((s0 + s1) + (s2 + s3));
+    }
+    if (row < R) out[row] = double(marg[row]) * acc;
+}
+
+__global__ void plan_ptu_kernel(const float* __restrict__ plan, const int* __restrict__ kptr,
+                                const int* __restrict__ kunit, const int* __restrict__ kslot,
+                                const float* __restrict__ u, const float* __restrict__ r,
+                                int64_t R, int64_t key_valid, double* __restrict__ out) {
+    __shared__ double red[8][TILE];
+    const int kt = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int b = kptr[kt]; b < kptr[kt + 1]; ++b) {
+        const int unit = kunit[b];
+        const float4* bp = reinterpret_cast<const float4*>(plan + size_t(kslot[b]) * 2 * TILE * TILE);
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll 4
+        for (int rr = warp; rr < 2 * TILE; rr += 8) {
+            const int64_t i = int64_t(unit) * 2 * TILE + rr;
+            const float coef = i < R ? r[i] * u[i] : 0.0f;
+            const float4 q = __ldg(bp + rr * (TILE / 4) + lane);
+            s0 = fmaf(coef, q.x, s0);
+            s1 = fmaf(coef, q.y, s1);
+            s2 = fmaf(coef, q.z, s2);
+            s3 = fmaf(coef, q.w, s3);
+        }
+        a0 += s0, a1 += s1, a2 += s2, a3 += s3;
+    }
+    red[warp][4 * lane] = a0;
+    red[warp][4 * lane + 1] = a1;
+    red[warp][4 * lane + 2] = a2;
+    red[warp][4 * lane + 3] = a3;
+    __syncthreads();
+    if (threadIdx.x < TILE) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[w][threadIdx.x];
+        const int64_t j = int64_t(kt) * TILE + threadIdx.x;
+        if (j < key_valid) out[j] = t;
+    }
+}
+
+bool TcHalfStep::build_plan(DevProblem<float>& P, const float* g, const float* f, float eps,
+                            const float* l2h0, const float* l2l0, const float* r, int* flags) {
+    Impl& I = *impl_;
+    drop_plan();
+    const char* env = std::getenv("FSK_PLAN_CACHE");
+    const bool enabled = !(env && env[0] == '0');
+    if (!enabled || I.chunks == 1) return false;   // the d <= 64 kernels do not store blocks
+    if (!(I.live_valid[0] && I.live_kpot[0] == g && I.live_valid[1] && I.live_kpot[1] == f))
+        return false;
+    const int64_t n = P.src.n, m = P.tgt.n;
+    const int q_tiles = int((n + TILE - 1) / TILE), units = (q_tiles + 1) / 2;
+    const int k_tiles = int(I.rows_pad[1] / TILE);   // key tiles of side 0 (Y)
+    const int kx_tiles = int(I.rows_pad[0] / TILE);  // key tiles of side 1 (X)
+    // union of both orientations' live sets in side-0 block space
+    auto fetch = [&](int side) {
+        const int64_t u = side == 0 ? units : (int64_t((m + TILE - 1) / TILE) + 1) / 2;
+        std::vector<uint32_t> h(size_t(u) * I.live_splits[side] * I.live_kwords[side]);
+        FSKB_CUDA(cudaMemcpyAsync(h.data(), I.live_glob[side].get(), h.size() * 4,
+                                  cudaMemcpyDeviceToHost, P.s));
+        return h;
+    };
+    const std::vector<uint32_t> s0 = fetch(0), s1 = fetch(1);
+    FSKB_CUDA(cudaStreamSynchronize(P.s));
+    std::vector<uint8_t> live(size_t(units) * k_tiles, 0);
+    auto walk = [&](int side, const std::vector<uint32_t>& bits, auto&& mark) {
+        const int sp = I.live_splits[side], kps = I.live_kps[side], kw = I.live_kwords[side];
+        const size_t u_n = bits.size() / size_t(sp * kw);
+        const int kmax = side == 0 ? k_tiles : kx_tiles;
+        for (size_t u = 0; u < u_n; ++u)
+            for (int ls = 0; ls < sp; ++ls)
+                for (int w = 0; w < kw; ++w) {
+                    uint32_t word = bits[(u * sp + ls) * kw + w];
+                    while (word) {
+                        const int b = __builtin_ctz(word);
+                        word &= word - 1;
+                        const int kt = ls * kps + w * 32 + b;
+                        if (w * 32 + b < kps && kt < kmax) mark(int(u), kt);
+                    }
+                }
+    };
+    walk(0, s0, [&](int u, int kt) { live[size_t(u) * k_tiles + kt] = 1; });
+    // side 1: unit of Y tiles (2 ug, 2 ug + 1) x X tile kx -> side-0 block (kx / 2, Y tile)
+    walk(1, s1, [&](int ug, int kx) {
+        for (int yt = 2 * ug; yt < 2 * ug + 2 && yt < k_tiles; ++yt)
+            live[size_t(kx / 2) * k_tiles + yt] = 1;
+    });
+    std::vector<int> slot(live.size(), -1), uptr(size_t(units) + 1, 0), ukt, uslot;
+    std::vector<int> kcount(size_t(k_tiles) + 1, 0);
+    int nb = 0;
+    for (int u = 0; u < units; ++u) {
+        for (int kt = 0; kt < k_tiles; ++kt)
+            if (live[size_t(u) * k_tiles + kt]) {
+                slot[size_t(u) * k_tiles + kt] = nb;
+                ukt.push_back(kt);
+                uslot.push_back(nb);
+                ++kcount[size_t(kt) + 1];
+                ++nb;
+            }
+        uptr[size_t(u) + 1] = nb;
+    }
+    if (nb == 0) return false;
+    const size_t bytes = size_t(nb) * 2 * TILE * TILE * sizeof(float);
+    size_t free_b = 0, total_b = 0;
+    FSKB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    if (bytes > free_b / 2) return false;            // keep room for everything else
+    std::vector<int> kptr(size_t(k_tiles) + 1, 0);
+    std::vector<int> kunit(static_cast<size_t>(nb), 0), kslot(static_cast<size_t>(nb), 0);
+    for (int kt = 0; kt < k_tiles; ++kt) kptr[size_t(kt) + 1] = kptr[size_t(kt)] + kcount[size_t(kt) + 1];
+    {
+        std::vector<int> fill(kptr.begin(), kptr.end() - 1);
+        for (int u = 0; u < units; ++u)
+            for (int b = uptr[size_t(u)]; b < uptr[size_t(u) + 1]; ++b) {
+                const int kt = ukt[size_t(b)];
+                kunit[size_t(fill[size_t(kt)])] = u;
+                kslot[size_t(fill[size_t(kt)]++)] = uslot[size_t(b)];
+            }
+    }
+    auto up = [&](DevBuf<int>& d, const std::vector<int>& h) {
+        d.alloc(h.size(), P.s);
+        FSKB_CUDA(cudaMemcpyAsync(d.get(), h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice,
+                                  P.s));
+    };
+    up(I.plan_slot, slot);
+    up(I.plan_uptr, uptr);
+    up(I.plan_ukt, ukt);
+    up(I.plan_uslot, uslot);
+    up(I.plan_kptr, kptr);
+    up(I.plan_kunit, kunit);
+    up(I.plan_kslot, kslot);
+    // the union as a live_in set: one split, every key tile
+    const int kw = (k_tiles + 31) / 32;
+    std::vector<uint32_t> uni(size_t(units) * kw, 0u);
+    for (int u = 0; u < units; ++u)
+        for (int kt = 0; kt < k_tiles; ++kt)
+            if (live[size_t(u) * k_tiles + kt]) uni[size_t(u) * kw + kt / 32] |= 1u << (kt & 31);
+    DevBuf<uint32_t> uni_d(uni.size(), P.s);
+    FSKB_CUDA(cudaMemcpyAsync(uni_d.get(), uni.data(), uni.size() * 4, cudaMemcpyHostToDevice, P.s));
+    I.plan.alloc(bytes / sizeof(float), P.s);
+    // materialize: one VEC pass over the union storing each block (v = 0)
+    DevBuf<float> vz(size_t(m), P.s);
+    vz.zero();
+    PassExtras ex{};
+    ex.live_in = uni_d.get();
+    ex.in_splits = 1;
+    ex.in_kps = k_tiles;
+    ex.in_kwords = kw;
+    ex.plan_out = I.plan.get();
+    ex.plan_slot = I.plan_slot.get();
+    DevBuf<double> pm, ps;
+    const float* args[3] = {l2h0, l2l0, vz.get()};
+    pass(P, 0, g, eps, 0, n, args, flags, pm, ps, &ex);
+    FSKB_CUDA(cudaStreamSynchronize(P.s));
+    I.plan_valid = true;
+    I.plan_kpot[0] = g;
+    I.plan_kpot[1] = f;
+    I.plan_r = r;
+    I.plan_units = units;
+    I.plan_k_tiles = k_tiles;
+    I.plan_blocks = nb;
+    return true;
+}
+
+void TcHalfStep::drop_plan() {
+    Impl& I = *impl_;
+    I.plan_valid = false;
+    I.plan.release();
+}
+
+double TcHalfStep::plan_fraction() const {
+    const Impl& I = *impl_;
+    if (!I.plan_valid) return -1.0;
+    return double(I.plan_blocks) / (double(I.plan_units) * double(I.plan_k_tiles));
 }
 
 void TcHalfStep::vec(DevProblem<float>& P, int side, const float* kpot, float eps,
@@ -2375,6 +2630,20 @@ void TcHalfStep::vec(DevProblem<float>& P, int side, const float* kpot, float ep
                      double* out, int* flags) {
     const int64_t R = side == 0 ? P.src.n : P.tgt.n;
     if (R == 0) return;
+    Impl& I = *impl_;
+    if (I.plan_valid && I.plan_kpot[side] == kpot) {
+        if (side == 0)
+            plan_pv_kernel<<<unsigned(I.plan_units), 2 * TILE, 0, P.s>>>(
+                I.plan.get(), I.plan_uptr.get(), I.plan_ukt.get(), I.plan_uslot.get(), v, P.tgt.n,
+                marg, R, out);
+        else
+            plan_ptu_kernel<<<unsigned(I.plan_k_tiles), 256, 0, P.s>>>(
+                I.plan.get(), I.plan_kptr.get(), I.plan_kunit.get(), I.plan_kslot.get(), v, I.plan_r,
+                P.src.n, R, out);
+        FSKB_CUDA(cudaGetLastError());
+        count_launch();
+        return;
+    }
     DevBuf<double> pm, ps;
     const float* args[3] = {l2h, l2l, v};
     const int splits = pass(P, side, kpot, eps, 0, R, args, flags, pm, ps);

@@ -55,6 +55,16 @@ public:
               const float* pre_l2h = nullptr, const float* pre_l2l = nullptr,
               const float* pre_r = nullptr);
 
+    // Keeps the live blocks of the transport plan at potentials (f, g) in HBM
+    // (row-normalized fp32, union of both orientations' live sets; needs both sides'
+    // live sets recorded at these potentials and l2h0/l2l0/r of side 0); while it
+    // is valid, vec() at those potentials sweeps it instead of recomputing scores.
+    // Returns false (nothing cached) for d <= 64 or when it would not fit.
+    bool build_plan(DevProblem<float>& P, const float* g, const float* f, float eps,
+                    const float* l2h0, const float* l2l0, const float* r, int* flags);
+    void drop_plan();
+    double plan_fraction() const;   // cached blocks / all blocks, -1 when none
+
     // Re-records the live key-tile set of `side` at fixed potentials with every
     // row's running max seeded just below its true max (mx_nat: the natural-log row
     // max of a pass at the same potentials): only tiles holding terms within 2^-64
@@ -82,9 +92,16 @@ public:
 
 private:
     void poll_screen(int side, double max_live);
+    struct PassExtras {
+        const float* m_init;        // running-max seeds (LSE passes)
+        const uint32_t* live_in;    // caller-supplied live set
+        int in_splits, in_kps, in_kwords;
+        float* plan_out;            // VEC passes: store the visited plan blocks
+        const int* plan_slot;
+    };
     int pass(DevProblem<float>& P, int side, const float* kpot, float eps, int64_t row_begin,
              int64_t row_end, const float* const* vec, int* flags, DevBuf<double>& pm,
-             DevBuf<double>& ps, const float* m_init = nullptr);
+             DevBuf<double>& ps, const PassExtras* ex = nullptr);
     struct Impl;
     Impl* impl_;
 };

@@ -543,3 +543,28 @@ def test_divergence_batch_matches_single_calls(fsk, precision):
             for X, a, Y, b in pairs]
     assert np.array_equal(got, np.array(want)), (got, want)
     assert got[0] == got[3]
+
+
+def test_hvp_plan_cache_matches_recomputed_scores(fsk, port):
+    """d > 64: the HVP's transport-vector passes sweep the live plan blocks kept in
+    HBM (build_plan); with FSK_PLAN_CACHE=0 they recompute the scores. Both runs use
+    the same fp32 plan entries, so they agree to accumulation-order rounding."""
+    rng = np.random.default_rng(3)
+    n, m, d = 700, 650, 100
+    X = rng.normal(size=(n, d)) * 0.3
+    Y = rng.normal(size=(m, d)) * 0.3 + 0.05
+    a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+    eps = 0.5
+    s = port.sinkhorn_solve(X, a, Y, b, eps=eps, max_iters=100)
+    A = rng.normal(size=X.shape)
+    out = {}
+    for flag in ("1", "0"):
+        os.environ["FSK_PLAN_CACHE"] = flag
+        try:
+            out[flag], _ = fsk.hvp_apply(X, a, Y, b, s["f_hat"], s["g_hat"], eps, A, tau=1e-5,
+                                         cg_tol=1e-30, cg_max_iters=30, precision="single")
+        finally:
+            os.environ.pop("FSK_PLAN_CACHE", None)
+    rel = np.linalg.norm(out["1"] - out["0"]) / np.linalg.norm(out["0"])
+    print(f"plan cache vs recomputed: rel Frobenius {rel:.2e}")
+    assert rel <= 1e-5
