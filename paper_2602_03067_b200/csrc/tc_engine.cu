@@ -1772,32 +1772,35 @@ __global__ void warm_prepass_kernel(int* __restrict__ gap, const int* __restrict
                                     unsigned long long* __restrict__ live_count) {
     const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t total = int64_t(units) * splits * kwords;
-    if (gid >= total) return;
-    const int w = int(gid % kwords);
-    const int s = int((gid / kwords) % splits);
-    const int u = int(gid / (int64_t(kwords) * splits));
-    const int kt_end = min(k_tiles, (s + 1) * kps);
     int nlive = 0;
-    for (int t = 0; t < 2; ++t) {
-        const float lt = fdec(lam[2 * u + t]);   // +inf for a missing second tile
-        int* grow = gap + size_t(2 * u + t) * k_tiles;
-        uint32_t bits = 0;
-        for (int b = 0; b < 32; ++b) {
-            const int kt = s * kps + w * 32 + b;
-            if (w * 32 + b >= kps || kt >= kt_end) break;
-            const float e = fdec(grow[kt]) + fdec(tile_dmax[kt]) - lt;
-            const bool dead = e < -(kSkipLog2 + 1.0f);   // NaN -> live
-            if (dead) {
-                grow[kt] = fenc(e);
-            } else {
-                grow[kt] = fenc(-INFINITY);
-                bits |= 1u << b;
-                ++nlive;
+    if (gid < total) {
+        const int w = int(gid % kwords);
+        const int s = int((gid / kwords) % splits);
+        const int u = int(gid / (int64_t(kwords) * splits));
+        const int kt_end = min(k_tiles, (s + 1) * kps);
+        for (int t = 0; t < 2; ++t) {
+            const float lt = fdec(lam[2 * u + t]);   // +inf for a missing second tile
+            int* grow = gap + size_t(2 * u + t) * k_tiles;
+            uint32_t bits = 0;
+            for (int b = 0; b < 32; ++b) {
+                const int kt = s * kps + w * 32 + b;
+                if (w * 32 + b >= kps || kt >= kt_end) break;
+                const float e = fdec(grow[kt]) + fdec(tile_dmax[kt]) - lt;
+                const bool dead = e < -(kSkipLog2 + 1.0f);   // NaN -> live
+                if (dead) {
+                    grow[kt] = fenc(e);
+                } else {
+                    grow[kt] = fenc(-INFINITY);
+                    bits |= 1u << b;
+                    ++nlive;
+                }
             }
+            live[((size_t(u) * splits + s) * 2 + t) * kwords + w] = bits;
         }
-        live[((size_t(u) * splits + s) * 2 + t) * kwords + w] = bits;
     }
-    if (live_count && nlive) atomicAdd(live_count, (unsigned long long)nlive);
+    // one counter update per warp (a per-thread atomic on one word serialized ~1 ms)
+    const unsigned wl = __reduce_add_sync(0xffffffffu, unsigned(nlive));
+    if (live_count && (threadIdx.x & 31) == 0 && wl) atomicAdd(live_count, (unsigned long long)wl);
 }
 
 __global__ void absmax_kernel(const float* __restrict__ x, int64_t n, unsigned int* out) {
