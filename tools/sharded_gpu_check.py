@@ -34,6 +34,9 @@ def main() -> int:
     torch.cuda.set_device(0)
     dist.init_process_group("gloo")
     n, m, d, eps, iters = 6000, 5000, 64, 0.1, 6
+    if len(sys.argv) > 1:   # e.g. 65536 65536 64 0.05 10 (exercises the warm-bound passes)
+        n, m, d = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
+        eps, iters = float(sys.argv[4]), int(sys.argv[5])
     rng = np.random.default_rng(3)
     X, Y = rng.normal(size=(n, d)), rng.normal(size=(m, d)) * 0.9 + 0.1
     a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
@@ -81,7 +84,9 @@ def main() -> int:
         print(f"[sharded x{world}] f {df:.2e} g {dg:.2e} grad {dG:.2e} viol {dv:.2e}", flush=True)
         # row shards run the same kernels on the same rows: identical up to the
         # order of the per-split partial sums
-        ok = df <= 1e-6 and dg <= 1e-6 and dG <= 1e-5 and dv <= 1e-6
+        # warm-bound passes seed each row's running max per shard and pair query tiles
+        # into different units: agreement to fp32 rounding (cf. the warm-vs-cold test)
+        ok = df <= 1e-6 and dg <= 1e-6 and dG <= 2e-4 and dv <= 1e-5
         print("[sharded] OK" if ok else "[sharded] MISMATCH", flush=True)
         ref.close()
     eng.close()
