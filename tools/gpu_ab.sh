@@ -1,6 +1,6 @@
 #!/usr/bin/env bash
 # A/B runs: tensor-path tests (per setting), then each config under each env setting.
-#   bash tools/gpu_ab.sh TAG "cfg2 cfg3" "FSK_EPI16=0 FSK_MINIT=0" "FSK_EPI16=1 FSK_MINIT=1" ...
+#   bash tools/gpu_ab.sh TAG "cfg2 cfg3" "FSK_MINIT=0" "FSK_MINIT=1" ...
 set -u
 TAG=$1; CFGS=$2; shift 2
 OUT=gpurun_out/$TAG
