@@ -108,7 +108,8 @@ struct PhaseTimer {
     bool on;
     cudaStream_t s;
     std::chrono::steady_clock::time_point t0;
-    explicit PhaseTimer(cudaStream_t st) : on(std::getenv("FSK_TIMING") != nullptr), s(st) {
+    explicit PhaseTimer(cudaStream_t st)
+        : on(std::getenv("FSK_TIMING") && std::getenv("FSK_TIMING")[0] != '0'), s(st) {
         t0 = std::chrono::steady_clock::now();
     }
     void mark(const char* what) {
