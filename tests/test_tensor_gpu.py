@@ -92,6 +92,27 @@ def test_tensor_solver_matches_fp64(fsk, port, tensor_mode):
     assert abs(s["dual_cost"] - r["dual_cost"]) <= 1e-5 * abs(r["dual_cost"])
 
 
+def test_tensor_solver_eps_scaling(fsk, port, tensor_mode):
+    """eps-scaling on the tensor path (operand images and bias rebuilt at every
+    eps of the schedule, warm state reset): same eps history as the reference,
+    potentials and loss within the fp32 solve contract."""
+    rng = np.random.default_rng(8)
+    n, m, d = 600, 520, 64
+    X, Y = rng.normal(size=(n, d)), rng.normal(size=(m, d)) * 0.9
+    a, b = np.full(n, 1 / n), np.full(m, 1 / m)
+    kw = dict(eps=0.3, max_iters=40, eps_scaling_factor=0.7, extra_iters_at_final_eps=5)
+    s = fsk.sinkhorn_solve(X, a, Y, b, precision="single", **kw)
+    r = port.sinkhorn_solve(X, a, Y, b, precision="double", **kw)
+    r32 = port.sinkhorn_solve(X, a, Y, b, precision="single", **kw)
+    assert np.array_equal(np.asarray(s["eps_history"]), np.asarray(r["eps_history"]))
+    assert s["iterations"] == r["iterations"]
+    err = contract(s["f_hat"], r["f_hat"])
+    err32 = contract(r32["f_hat"], r["f_hat"])
+    print(f"eps-scaled solve: tensor {err:.2e}, reference fp32 {err32:.2e}")
+    assert err <= max(1e-5, 2 * err32)
+    assert abs(s["dual_cost"] - r["dual_cost"]) <= 1e-5 * abs(r["dual_cost"])
+
+
 def test_engine_row_shards_reproduce_full_half_step(fsk, port):
     torch = pytest.importorskip("torch")
     rng = np.random.default_rng(11)
