@@ -113,6 +113,24 @@ def test_tensor_solver_eps_scaling(fsk, port, tensor_mode):
     assert abs(s["dual_cost"] - r["dual_cost"]) <= 1e-5 * abs(r["dual_cost"])
 
 
+def test_tensor_solver_symmetric_schedule(fsk, port, tensor_mode):
+    """Symmetric (Jacobi) schedule on the tensor path: both half-steps from the old
+    pair, averaged in the finalize; fp32 solve contract against the reference."""
+    rng = np.random.default_rng(9)
+    n, m, d = 640, 580, 64
+    X, Y = rng.normal(size=(n, d)), rng.normal(size=(m, d)) + 0.1
+    a, b = np.full(n, 1 / n), np.full(m, 1 / m)
+    kw = dict(eps=0.4, max_iters=25, schedule="symmetric")
+    s = fsk.sinkhorn_solve(X, a, Y, b, precision="single", **kw)
+    r = port.sinkhorn_solve(X, a, Y, b, precision="double", **kw)
+    r32 = port.sinkhorn_solve(X, a, Y, b, precision="single", **kw)
+    err = contract(s["f_hat"], r["f_hat"])
+    err32 = contract(r32["f_hat"], r["f_hat"])
+    print(f"symmetric solve: tensor {err:.2e}, reference fp32 {err32:.2e}")
+    assert err <= max(1e-5, 2 * err32)
+    assert abs(s["dual_cost"] - r["dual_cost"]) <= 1e-5 * abs(r["dual_cost"])
+
+
 def test_engine_row_shards_reproduce_full_half_step(fsk, port):
     torch = pytest.importorskip("torch")
     rng = np.random.default_rng(11)
