@@ -2429,32 +2429,41 @@ __global__ void plan_pv_kernel(const float* __restrict__ plan, const int* __rest
                                const int* __restrict__ ukt, const int* __restrict__ uslot,
                                const float* __restrict__ v, int64_t key_valid,
                                const float* __restrict__ marg, int64_t R, double* __restrict__ out) {
-    __shared__ float vs[TILE];
+    // warp w owns rows [32 w, 32 w + 32) of the unit; per block its lanes read each
+    // row's 128 entries as one coalesced 512 B line (lane = 4 columns) and keep one
+    // partial per row, reduced across lanes once per unit
     const int unit = blockIdx.x;
-    const int64_t row = int64_t(unit) * 2 * TILE + threadIdx.x;
-    double acc = 0.0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double acc[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) acc[r] = 0.0;
     for (int b = uptr[unit]; b < uptr[unit + 1]; ++b) {
-        const int kt = ukt[b];
-        __syncthreads();
-        if (threadIdx.x < TILE) {
-            const int64_t j = int64_t(kt) * TILE + threadIdx.x;
-            vs[threadIdx.x] = j < key_valid ? v[j] : 0.0f;
+        const int64_t j = int64_t(ukt[b]) * TILE + 4 * lane;
+        float4 vv = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (j + 3 < key_valid) {
+            vv = *reinterpret_cast<const float4*>(v + j);
+        } else {
+            if (j < key_valid) vv.x = v[j];
+            if (j + 1 < key_valid) vv.y = v[j + 1];
+            if (j + 2 < key_valid) vv.z = v[j + 2];
         }
-        __syncthreads();
-        const float4* rp =
-            reinterpret_cast<const float4*>(plan + (size_t(uslot[b]) * 2 * TILE + threadIdx.x) * TILE);
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-#pragma unroll 8
-        for (int c = 0; c < TILE / 4; ++c) {
-            const float4 q = __ldg(rp + c);
-            s0 = fmaf(q.x, vs[4 * c], s0);
-            s1 = fmaf(q.y, vs[4 * c + 1], s1);
-            s2 = fmaf(q.z, vs[4 * c + 2], s2);
-            s3 = fmaf(q.w, vs[4 * c + 3], s3);
+        const float4* bp = reinterpret_cast<const float4*>(plan + size_t(uslot[b]) * 2 * TILE * TILE) +
+                           size_t(warp) * 32 * (TILE / 4) + lane;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+            const float4 q = __ldg(bp + r * (TILE / 4));
+            acc[r] += double(fmaf(q.x, vv.x, fmaf(q.y, vv.y, fmaf(q.z, vv.z, q.w * vv.w))));
         }
-        acc += double((s0 + s1) + (s2 + s3));
     }
-    if (row < R) out[row] = double(marg[row]) * acc;
+    double mine = 0.0;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+        double t = acc[r];
+        for (int off = 16; off >= 1; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+        if (lane == r) mine = t;
+    }
+    const int64_t row = int64_t(unit) * 2 * TILE + warp * 32 + lane;
+    if (row < R) out[row] = double(marg[row]) * mine;
 }
 
 __global__ void plan_ptu_kernel(const float* __restrict__ plan, const int* __restrict__ kptr,
