@@ -1862,6 +1862,16 @@ int scale_exponent(double maxabs) {
 }  // namespace
 
 // Key split that best fills a persistent grid of `sms` CTAs with units x splits items.
+// key-range size of the L2-local splits (warm passes, sparse K3); FSK_WARM_RANGE_MB
+double warm_range_bytes() {
+    static const double b = [] {
+        const char* e = std::getenv("FSK_WARM_RANGE_MB");
+        const double mb = e ? std::atof(e) : 40.0;
+        return (mb > 1.0 ? mb : 40.0) * double(1 << 20);
+    }();
+    return b;
+}
+
 int pick_splits(int units, int k_tiles, int sms, int min_splits = 1) {
     const int max_s = std::max(1, std::min(32, k_tiles / 4));
     min_splits = std::min(std::max(1, min_splits), max_s);
@@ -2182,7 +2192,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         return !(e && e[0] == '0');
     }();
     if (warm && range_split)
-        min_s = std::max(min_s, int(std::ceil(double(k_tiles) * KSTAGE / (40.0 * (1 << 20)))));
+        min_s = std::max(min_s, int(std::ceil(double(k_tiles) * KSTAGE / warm_range_bytes())));
     p.splits = pick_splits(units, k_tiles, sms, min_s);
     p.items = units * p.splits;
     p.row_begin = row_begin;
@@ -2833,7 +2843,7 @@ void TcHalfStep::grad(DevProblem<float>& P, int side, const float* kpot, const f
     // (split-major items), as in the warm LSE passes
     const char* wsplit = std::getenv("FSK_WARM_SPLIT");
     const int min_s = sparse && !(wsplit && wsplit[0] == '0')
-                          ? int(std::ceil(double(p.k_tiles) * KSTAGE / (40.0 * (1 << 20))))
+                          ? int(std::ceil(double(p.k_tiles) * KSTAGE / warm_range_bytes()))
                           : 1;
     p.splits = pick_splits(p.q_tiles, p.k_tiles, sms, min_s);
     p.items = p.q_tiles * p.splits;
