@@ -557,7 +557,7 @@ def run_b200(args, cfgname):
         # block skipping in the LSE passes (warm bounds across passes, or the 5-MMA
         # screen): of the (query tile pair, key tile) blocks of the passes whose live
         # count was read back, the fraction scored in full; the rest are provably
-        # < 2^-64 of every row's max
+        # < 2^-58 of every row's max
         line["block_skipping"] = {"tracked_blocks": sblk, "live_blocks": live,
                                   "live_fraction": live / sblk if sblk else None}
     if world == 1 and args.cpu_baseline:

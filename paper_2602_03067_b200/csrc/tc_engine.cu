@@ -62,7 +62,14 @@ constexpr uint32_t CSTAGE = 3 * QTILE + BIAS;                  // 100 KB
 constexpr uint32_t C_OFF_ONES = CSTAGES * CSTAGE;              // 200 KB
 constexpr uint32_t C_OFF_BAR = C_OFF_ONES + BIAS;              // 204 KB
 constexpr uint32_t C_SMEM_BYTES = C_OFF_BAR + 256 + VBUF + 1024;
-constexpr float kSkipLog2 = 64.0f;  // LSE tiles entirely 2^-64 below the running max are skipped
+// Terms below 2^-kSkipLog2 of a row's running max are provably negligible: even
+// all m <= 2^32 of them add < 2^(32 - kSkipLog2) relative to the row sum (>= 1),
+// below half an fp32 ulp (2^-25) for kSkipLog2 >= 57 (58: 2^-26). Tiles / blocks
+// entirely below it are skipped (64 measured 4% slower on cfg3).
+#ifndef FSKB_SKIP_LOG2
+#define FSKB_SKIP_LOG2 58.0f
+#endif
+constexpr float kSkipLog2 = FSKB_SKIP_LOG2;
 
 // order-preserving float <-> int for atomicMax / atomicMin on floats
 __device__ __forceinline__ int fenc(float f) {
@@ -217,7 +224,7 @@ __device__ __forceinline__ bool k1_tile_update(uint32_t (&v)[W], int64_t kbase, 
         for (int j = 0; j < W; ++j)
             if (kbase + j >= p.key_valid) v[j] = __float_as_uint(-INFINITY);
     }
-    // per 32-column group maxima: a group whose terms are all < 2^-64 of the
+    // per 32-column group maxima: a group whose terms are all < 2^-kSkipLog2 of the
     // reference for every row of the warp skips its exponentials (same bound as
     // the whole-tile skip); live blocks of a warm pass mostly hold a few near keys
     constexpr int G = W / 32;
@@ -229,8 +236,8 @@ __device__ __forceinline__ bool k1_tile_update(uint32_t (&v)[W], int64_t kbase, 
     for (int c = 1; c < G; ++c) umax = fmaxf(umax, gmax[c]);
     umax_out = umax;
     if constexpr (VEC) {
-        // P~ = 2^(t - L) <= 1; a tile whose P~ are all < 2^-64 for the warp's rows
-        // adds < m 2^-64 max|v| - below the fp32 result's rounding
+        // P~ = 2^(t - L) <= 1; a tile whose P~ are all < 2^-kSkipLog2 for the warp's rows
+        // adds < m 2^-kSkipLog2 max|v| - below the fp32 result's rounding
         if (__all_sync(0xffffffffu, umax + nlh < -kSkipLog2)) return false;
         // the tile's W values of v, broadcast through a per-warp buffer
         if constexpr (W == 128) {
@@ -274,8 +281,8 @@ __device__ __forceinline__ bool k1_tile_update(uint32_t (&v)[W], int64_t kbase, 
             if (S != 0.0) S *= double(ex2(p.break_lse ? umax - M : M - umax));
             M = umax;
         }
-        // every term of this tile is < 2^-64 of the running max for all 32 rows of
-        // the warp: the whole tile adds < m 2^-64 relative - below rounding
+        // every term of this tile is < 2^-kSkipLog2 of the running max for all 32 rows of
+        // the warp: the whole tile adds < m 2^-kSkipLog2 relative - below rounding
         const bool dead = M == -INFINITY;
         if (__all_sync(0xffffffffu, dead || umax < M - kSkipLog2)) return false;
         const float nm = dead ? 0.0f : -M;
@@ -1762,7 +1769,7 @@ __global__ void fill_int_kernel(int* __restrict__ p, int64_t n, int v) {
 
 // Propagate the per-(query tile, key tile) gap bounds E = max_i (tilemax_i - M_i)
 // to the new bias: E' = E + max_tile(db) - lambda_t. Blocks with E' < -(64 + 1)
-// are provably below 2^-64 of every row's max and stay out of the live set
+// are provably below 2^-kSkipLog2 of every row's max and stay out of the live set
 // (E <- E'); live blocks get E <- -inf for the pass to re-measure. One thread per
 // bitmask word (u, split, w) of the pass's live_in layout, both query tiles of
 // the unit: live[u][split][t][w].
@@ -2092,7 +2099,7 @@ void TcHalfStep::set_eps(DevProblem<float>& P, double eps) {
     for (int side = 0; side < 2; ++side) {
         const double delta = std::ldexp(1.0, -10) * 1.001 * double(impl_->rownorm[side]) *
                              double(impl_->rownorm[1 - side]) * c;
-        impl_->screen_thr[side] = screen_on ? float(64.0 + 2.0 * delta + 8.0) : 0.0f;
+        impl_->screen_thr[side] = screen_on ? float(double(kSkipLog2) + 2.0 * delta + 8.0) : 0.0f;
     }
     if (!impl_->live_count.get()) {
         impl_->live_count.alloc(2, P.s);

@@ -330,7 +330,7 @@ def test_single_precision_hvp_matches_fp64(fsk, port, tensor_mode, d):
 @pytest.mark.parametrize("cold_screen", ["0", "1"])
 def test_warm_bounds_match_cold_passes(fsk, cold_screen):
     """Warm bounds (gap bounds carried across LSE passes and moved by the bias
-    change) only drop blocks provably < 2^-64 of every row's max: 10 iterations +
+    change) only drop blocks provably < 2^-58 of every row's max: 10 iterations +
     gradient agree with FSK_WARM=0 / FSK_SCREEN=0 to fp32 rounding. With
     cold_screen the first pass of each side is screened and its phase 1 seeds the
     gap bounds."""
@@ -375,7 +375,7 @@ def test_warm_bounds_match_cold_passes(fsk, cold_screen):
 
 
 def test_screened_lse_matches_unscreened(fsk):
-    """The 5-MMA screen only drops tiles whose terms are all < 2^-64 of the row max:
+    """The 5-MMA screen only drops tiles whose terms are all < 2^-58 of the row max:
     screened and unscreened f/g updates agree to fp32 rounding. n = m = 2^18 at
     eps = 0.05 is concentrated enough for most tiles to be screened out."""
     torch = pytest.importorskip("torch")
