@@ -2092,14 +2092,21 @@ void TcHalfStep::set_eps(DevProblem<float>& P, double eps) {
     for (int side = 0; side < 2; ++side) impl_->warm_ok[side] = impl_->b_valid[side] = false;
     const double c = 2.0 * P.fscale / eps * 1.4426950408889634074;
     // screening threshold: |t - t~| <= delta = 2^-10 (1 + 2^-11) ||x|| ||c y|| (the
-    // dropped cross terms, Cauchy-Schwarz) -> thr = 64 + 2 delta + 8 (fp32 slack)
+    // dropped cross terms, Cauchy-Schwarz) -> thr = kSkipLog2 + 2 delta + slack; the
+    // fp32 accumulation of the 5 exact fp16 products rounds by < 5 ulp(|t|) ~ 2^-8
+    // log2 units at the score magnitudes here, so a slack of 2 is ample
+    // (FSK_SCREEN_SLACK overrides, default 2)
     // adaptive (kScreenMaxLive), FSK_SCREEN=0 disables it
     const char* env = std::getenv("FSK_SCREEN");
     const bool screen_on = !(env && env[0] == '0') && impl_->chunks == 1;
     for (int side = 0; side < 2; ++side) {
         const double delta = std::ldexp(1.0, -10) * 1.001 * double(impl_->rownorm[side]) *
                              double(impl_->rownorm[1 - side]) * c;
-        impl_->screen_thr[side] = screen_on ? float(double(kSkipLog2) + 2.0 * delta + 8.0) : 0.0f;
+        static const double slack = [] {
+            const char* e = std::getenv("FSK_SCREEN_SLACK");
+            return e ? std::atof(e) : 2.0;
+        }();
+        impl_->screen_thr[side] = screen_on ? float(double(kSkipLog2) + 2.0 * delta + slack) : 0.0f;
     }
     if (!impl_->live_count.get()) {
         impl_->live_count.alloc(2, P.s);
