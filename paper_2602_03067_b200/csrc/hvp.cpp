@@ -287,9 +287,10 @@ void hvp_run(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat
         const double* Av = A;
         // cached transport-matrix product; on the tensor path V = Y is the resident cloud
         const bool tc_mat = kSingle && P.tc && d > 1;
-        const std::vector<double> PY =
-            tc_mat ? H.apply_dev(0, reinterpret_cast<const float*>(P.tgt.pts.get()), d)
-                   : H.apply(0, Y, d);
+        // the resident key cloud as float (the tensor path's problems are float)
+        const float* y_dev = nullptr;
+        if constexpr (kSingle) y_dev = P.tgt.pts.get();
+        const std::vector<double> PY = tc_mat ? H.apply_dev(0, y_dev, d) : H.apply(0, Y, d);
         timer.mark("hvp P Y");
 
         // build_rhs
@@ -369,8 +370,7 @@ void hvp_run(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat
             DevBuf<double> w2d(size_t(m), C.s);
             w2d.upload(w2.data(), size_t(m));
             DevBuf<float> w2Yd(size_t(m * d), C.s);
-            launch_scale_rows(reinterpret_cast<const float*>(P.tgt.pts.get()), w2d.get(), m, d,
-                              w2Yd.get(), C.s);
+            launch_scale_rows(y_dev, w2d.get(), m, d, w2Yd.get(), C.s);
             Pw2Y = H.apply_dev(0, w2Yd.get(), d);
         } else {
             std::vector<double> w2Y((size_t)(m * d));
