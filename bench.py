@@ -295,8 +295,49 @@ def workload_config(cfgname):
     return {"workload": f"{cfgname}: point-cloud EOT n=m={n}, d={d}, eps={eps}, "
                         f"{iters} alternating iterations{tail} per step",
             "n": n, "m": m, "d": d, "eps": eps, "iterations_per_step": iters,
-            "precision": "fp32 contract (tcgen05 split-fp16 scores, fp32 accumulate)",
-            "l2": "inputs larger than L2 (operand images 2 x 288 MB per side)"}
+            "precision": "fp32 contract (SURVEY §8d: potentials / loss within 1e-5)",
+            "l2": "inputs larger than L2 (no flush needed)"}
+
+
+# ------------------------------------------------------------- parity check --
+
+def parity_sample(cfgname, X, a, Y, b, f_dev, g_dev, grad_dev, grad_lo, rows=512, grad_rows=64):
+    """Sampled parity of the last timed step against the oracle, after the timed
+    region (the oracle is the checker here, never the thing timed): `rows` random
+    rows of the step's final g half-step (update_g_hat on the final f, through the
+    C port, oracle/rows.py) and `grad_rows` random gradient rows (SPEC grad_source,
+    fp64) against the device results. Contracts: SURVEY §8d (i) and the stated
+    tensor-mode gradient bound max(1e-5, 2 e32)."""
+    import torch
+
+    from oracle import Oracle
+    from oracle import rows as orows
+
+    n, m, d, eps, iters = CONFIGS[cfgname]
+    port = Oracle("port")
+    f = f_dev[:n].double().cpu().numpy()
+    g = g_dev[:m].double().cpu().numpy()
+    rng = np.random.default_rng(2024)
+    sel = np.sort(rng.choice(m, min(rows, m), replace=False))
+    t0 = time.perf_counter()
+    want = orows.half_step_rows(port, 1, X, a, Y, b, f, eps, sel)
+    err = float(np.abs(g[sel] - want).max() / max(1.0, np.abs(want).max()))
+    out = {"half_step": "final g-update of the last timed step", "rows": int(len(sel)),
+           "max_rel_err": err, "bound": 1e-5,
+           "norm": "||g_gpu - g_64||_inf / max(1, ||g_64||_inf) over the sampled rows"}
+    if grad_dev is not None:
+        R = grad_dev.shape[0]
+        gsel = np.sort(rng.choice(R, min(grad_rows, R), replace=False))
+        Gs = grad_dev[torch.as_tensor(gsel, device=grad_dev.device)].double().cpu().numpy()
+        rows_x = gsel + grad_lo
+        G64, r64, _ = orows.grad_rows(port, X, a, Y, b, f, g, eps, rows_x)
+        e32 = orows.grad_rows_fp32_error(port, X, a, Y, b, f, g, eps, rows_x, G64, r64)
+        gerr = float(np.abs(Gs - G64).max() / np.abs(G64).max())
+        out.update(grad_rows=int(len(gsel)), grad_max_rel_err=gerr, grad_ref_fp32_err=e32,
+                   grad_bound=max(1e-5, 2.0 * e32))
+    out["ok"] = bool(err <= 1e-5 and out.get("grad_max_rel_err", 0.0) <= out.get("grad_bound", 1.0))
+    out["check_s"] = time.perf_counter() - t0
+    return out
 
 
 # --------------------------------------------------------------- B200 arm -----
@@ -531,9 +572,11 @@ def run_b200(args, cfgname):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (fsk::Rng(1000) Gaussian clouds, uniform weights)",
-        "config": dict(workload_config(cfgname), parallelism=f"row-shard x{world} + NCCL "
-                       "all-gather of potentials" if world > 1 else "1 GPU",
-                       path=eng.path),
+        "config": workload_config(cfgname),
+        "parallelism": (f"row-shard x{world} + NCCL all-gather of potentials" if world > 1
+                        else "1 GPU"),
+        "path": eng.path + (" (split-fp16 scores on tcgen05, fp32 accumulate)"
+                            if eng.path.startswith("tcgen05") else ""),
         "half_step_ms": med_half * 1e3,
         "half_step_mean_ms": mean_half * 1e3,
         ("hvp_ms" if STEP_TAIL[cfgname] == "hvp" else "grad_ms"):
@@ -560,6 +603,12 @@ def run_b200(args, cfgname):
         # < 2^-58 of every row's max
         line["block_skipping"] = {"tracked_blocks": sblk, "live_blocks": live,
                                   "live_fraction": live / sblk if sblk else None}
+    if args.parity:
+        try:
+            line["parity"] = parity_sample(cfgname, X, a, Y, b, solver.f, solver.g,
+                                           grad if STEP_TAIL[cfgname] == "grad" else None, lo)
+        except Exception as exc:  # oracle library absent on this host
+            line["parity"] = {"ok": None, "unavailable": str(exc)}
     if world == 1 and args.cpu_baseline:
         try:
             cb = reference_sample(cfgname)
@@ -590,8 +639,8 @@ def run_b200_divergence(args, cfgname):
     n, m, d, eps, iters = CONFIGS[cfgname]
     if int(os.environ.get("RANK", "0")) != 0:
         return 0
-    rng = np.random.default_rng(1000)
-    clouds = [rng.standard_normal((n, d)) for _ in range(16)]
+    # 16 distinct clouds, cloud k = fsk::Rng(1000 + k).normal() (SURVEY §8d seeds)
+    clouds = [fsk.rng_normal(1000 + k, n * d).reshape(n, d) for k in range(16)]
     w = uniform_weights(n)
     pairs = [(clouds[k % 16], w, clouds[(k * 7 + 3) % 16], w) for k in range(CFG5_PAIRS)]
     os.environ.setdefault("FSK_TENSOR_MODE", args.mode)
@@ -612,14 +661,33 @@ def run_b200_divergence(args, cfgname):
     its = CFG5_PAIRS * 3 * iters
     value = its / step_s
     h2d = sum(2 * (X.nbytes + a.nbytes + Y.nbytes + b.nbytes) for (X, a, Y, b) in pairs)
+    # roofline (dominant kernel tc_lse_chunked_kernel, d = 784 -> 13 feature chunks):
+    # algorithmic W_dot = 2 n m d per half-step x 2 iters per solve x 3 solves x 64
+    # pairs over the whole step time (uploads, dual costs and the 2 marginal passes per
+    # solve included in the time, not in the work: a lower bound on the kernel's rate)
+    pk, pk_kind = peaks()
+    chunks = -(-d // 64)
+    mode_factor = (12 * chunks + 1) / (4.0 * chunks) * (64.0 * chunks / d)
+    peak_raw = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    w_dot = 2.0 * n * m * d * 2 * iters * 3 * CFG5_PAIRS
+    achieved = w_dot / step_s / 1e12
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_raw / mode_factor,
+                "unit": "TFLOP/s", "frac": achieved / (peak_raw / mode_factor), "traffic": None,
+                "kernel": "tc_lse_chunked_kernel<false> (whole C ABI step time, incl. uploads)",
+                "algorithmic": f"W_dot = 2 n m d x {2 * iters} half-steps x 3 solves x "
+                               f"{CFG5_PAIRS} pairs (n=m={n}, d={d})",
+                "peak_source": f"{pk_kind} bf16_tflops_sustained {peak_raw} / split-fp16 mode "
+                               f"factor {mode_factor:.3f}"}
     line = {
         "metric": metric_name(cfgname), "value": value, "unit": "iterations/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (16 Gaussian clouds, 64 pairs), uniform weights",
-        "config": dict(workload_config(cfgname), parallelism="1 GPU, pairs sequential",
-                       api="fsk_sinkhorn_divergence_batch (C ABI, host buffers)"),
+        "config": workload_config(cfgname),
+        "parallelism": "1 GPU, pairs sequential",
+        "api": "fsk_sinkhorn_divergence_batch (C ABI, host buffers)",
         "pairs_per_s": CFG5_PAIRS / step_s, "divergence_mean": float(np.mean(out)),
+        "roofline": roofline,
         "gpu_launches": launches, "clocks": clocks,
         "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(out.nbytes),
@@ -644,6 +712,7 @@ def main():
     ap.add_argument("--mode", default="auto", choices=["auto", "tensor", "fma"])
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--no-parity", dest="parity", action="store_false")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args, args.config)

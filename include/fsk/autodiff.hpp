@@ -1,7 +1,7 @@
-// fsk::autodiff - SPEC.md "autodiff" module (SPEC.md:239-291), specified by
+// fsk::autodiff - SPEC.md "autodiff" module (SPEC.md:378-430), specified by
 // the reference but never implemented there (SURVEY.md finding 5). Provided by
 // the B200 library as fused streaming kernels (one LSE pass + one transport
-// pass, no n x m buffer). Induced-marginal form throughout (SPEC.md:277).
+// pass, no n x m buffer). Induced-marginal form throughout (SPEC.md:396, :416).
 #pragma once
 
 #include "fsk/core.hpp"

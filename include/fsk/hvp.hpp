@@ -1,8 +1,10 @@
-// fsk::hvp - SPEC.md "hvp" module (SPEC.md:293-403; PAPER.md Thm. 3.5),
+// fsk::hvp - SPEC.md "hvp" module (SPEC.md:432-542; PAPER.md Thm. 3.5),
 // specified by the reference but never implemented there. Streaming
 // Hessian-vector product of OT_eps w.r.t. the source points: explicit term via
 // one Hadamard-weighted transport, implicit term via damped Schur-complement CG
-// over transport-vector products. O((n + m) d) memory, never n x m.
+// over transport-vector products. O((n + m) d) memory, never n x m (the opt-in
+// FSK_PLAN_CACHE=1 plan-block cache of the single-precision path trades that
+// contract for speed; it is off by default).
 #pragma once
 
 #include "fsk/core.hpp"

@@ -96,7 +96,7 @@ typedef struct fsk_report {
     double eps;
 } fsk_report;
 
-/* HvpConfig (SPEC.md:298-301): damping tau, CG tolerance eta, CG cap. */
+/* HvpConfig (SPEC.md:437-441): damping tau, CG tolerance eta, CG cap. */
 typedef struct fsk_hvp_config {
     double tau;
     double cg_tol;
@@ -214,17 +214,17 @@ int fsk_sinkhorn_divergence_batch(const fsk_measure* mus, const fsk_measure* nus
 
 /* ---- SPEC modules the reference specifies but never implemented ----------- */
 
-/* autodiff.grad_source (SPEC.md:254-262): G = 2 (diag(r) X - P Y), n x d. */
+/* autodiff.grad_source (SPEC.md:393-401): G = 2 (diag(r) X - P Y), n x d. */
 int fsk_grad_source(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat,
                     const double* g_hat, double eps, const fsk_cost* cost, const fsk_tiles* tiles,
                     fsk_ledger* ledger, double* out_grad);
 
-/* autodiff.grad_target (SPEC.md:264-270): G = 2 (diag(c) Y - P^T X), m x d. */
+/* autodiff.grad_target (SPEC.md:403-410): G = 2 (diag(c) Y - P^T X), m x d. */
 int fsk_grad_target(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat,
                     const double* g_hat, double eps, const fsk_cost* cost, const fsk_tiles* tiles,
                     fsk_ledger* ledger, double* out_grad);
 
-/* autodiff.barycentric_projection (SPEC.md:244-252): T = diag(r)^-1 P Y. */
+/* autodiff.barycentric_projection (SPEC.md:383-391): T = diag(r)^-1 P Y. */
 int fsk_barycentric_projection(const fsk_measure* src, const fsk_measure* tgt,
                                const double* f_hat, const double* g_hat, double eps,
                                const fsk_cost* cost, const fsk_tiles* tiles, fsk_ledger* ledger,
@@ -236,7 +236,7 @@ int fsk_sinkhorn_solve_grad(const fsk_measure* src, const fsk_measure* tgt, cons
                             const fsk_config* cfg, const fsk_tiles* tiles, fsk_ledger* ledger,
                             fsk_report* report, double* out_grad);
 
-/* hvp.hvp_apply (SPEC.md:349-357; PAPER.md Thm. 3.5): HVP of OT_eps w.r.t. X
+/* hvp.hvp_apply (SPEC.md:488-496; PAPER.md Thm. 3.5): HVP of OT_eps w.r.t. X
  * along A (n x d) at the given potentials, damped Schur-complement CG. */
 int fsk_hvp_apply(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat,
                   const double* g_hat, double eps, const fsk_cost* cost, const double* A,
@@ -258,7 +258,8 @@ int fsk_hvp_apply_single(const fsk_measure* src, const fsk_measure* tgt, const d
  * (float, length n / m) so a collective library can all-gather them in place. */
 typedef struct fsk_engine fsk_engine;
 
-/* mode: 0 = auto (split-fp16 tensor cores when 32 <= d <= 64, else FMA),
+/* mode: 0 = auto (split-fp16 tensor cores when d >= 32, up to d = 4096; CUDA-core
+ *       FMA below d = 32),
  *       1 = force CUDA-core FMA fp32, 2 = force tensor (split-fp16). */
 int fsk_engine_create(int device, const double* X, const double* a, int64_t n, const double* Y,
                       const double* b, int64_t m, int64_t d, int mode, fsk_engine** out);
@@ -323,6 +324,12 @@ void fsk_rng_normal_fill(uint64_t seed, double* out, int64_t count);
 /* Library build/version string and device check. */
 const char* fsk_version(void);
 int fsk_device_count(void);
+
+/* High-water mark (bytes) of the device's default memory pool, which holds every
+ * allocation the library makes; reset != 0 restarts it at the current usage.
+ * The HVP memory contract (peak <= c (n + m) d scalars, never n m)
+ * is asserted through this. */
+int64_t fsk_device_peak_bytes(int device, int reset);
 
 #ifdef __cplusplus
 }

@@ -16,7 +16,7 @@ import numpy as np
 
 
 class Workspace:
-    """HvpWorkspace (SPEC.md:303-306): cached P Y and induced marginals."""
+    """HvpWorkspace (SPEC.md:442-446): cached P Y and induced marginals."""
 
     def __init__(self, ops, X, a, Y, b, f_hat, g_hat, eps, tiles=(64, 64)):
         self.ops, self.X, self.a, self.Y, self.b = ops, X, a, Y, b
@@ -44,22 +44,22 @@ class Workspace:
 
 
 def barycentric_projection(ws: Workspace):
-    """T = diag(r)^-1 P Y (SPEC.md:244-252)."""
+    """T = diag(r)^-1 P Y (SPEC.md:383-391)."""
     return ws.PY / ws.r[:, None]
 
 
 def grad_source(ws: Workspace):
-    """G = 2 (diag(r) X - P Y) (SPEC.md:254-262)."""
+    """G = 2 (diag(r) X - P Y) (SPEC.md:393-401)."""
     return 2.0 * (ws.r[:, None] * ws.X - ws.PY)
 
 
 def grad_target(ws: Workspace):
-    """G = 2 (diag(c) Y - P^T X) (SPEC.md:264-270)."""
+    """G = 2 (diag(c) Y - P^T X) (SPEC.md:403-410)."""
     return 2.0 * (ws.c[:, None] * ws.Y - ws.Pt(ws.X))
 
 
 def explicit_term(ws: Workspace, A):
-    """E.A = B1 - (4/eps)(B2 - B3 - B4 + B5) (SPEC.md:309-317)."""
+    """E.A = B1 - (4/eps)(B2 - B3 - B4 + B5) (SPEC.md:448-456)."""
     X, PY, r, eps = ws.X, ws.PY, ws.r, ws.eps
     u = (X * A).sum(1)
     uP = (PY * A).sum(1)
@@ -71,7 +71,7 @@ def explicit_term(ws: Workspace, A):
 
 
 def build_rhs(ws: Workspace, A):
-    """r1 = 2 (r u - u_P), r2 = 2 (P^T u - <P^T A, Y>_row) (SPEC.md:319-327)."""
+    """r1 = 2 (r u - u_P), r2 = 2 (P^T u - <P^T A, Y>_row) (SPEC.md:458-466)."""
     u = (ws.X * A).sum(1)
     uP = (ws.PY * A).sum(1)
     r1 = 2.0 * (ws.r * u - uP)
@@ -80,12 +80,12 @@ def build_rhs(ws: Workspace, A):
 
 
 def schur_apply(ws: Workspace, v, tau):
-    """S_tau v = c v - P^T diag(r)^-1 P v + tau v (SPEC.md:329-337)."""
+    """S_tau v = c v - P^T diag(r)^-1 P v + tau v (SPEC.md:468-476)."""
     return ws.c * v - ws.Pt(ws.P(v) / ws.r) + tau * v
 
 
 def cg_solve(apply, rhs, tol=1e-6, max_iters=50):
-    """Unpreconditioned CG from 0 (SPEC.md:339-347). Returns (x, iters, rel_residual)."""
+    """Unpreconditioned CG from 0 (SPEC.md:478-486). Returns (x, iters, rel_residual)."""
     x = np.zeros_like(rhs)
     rnorm0 = np.linalg.norm(rhs)
     if rnorm0 == 0.0:
@@ -109,7 +109,7 @@ def cg_solve(apply, rhs, tol=1e-6, max_iters=50):
 
 
 def hvp_apply(ws: Workspace, A, tau=1e-5, tol=1e-6, max_iters=50):
-    """G = (1/eps) R^T w + E.A (SPEC.md:349-357, Thm. 3.5)."""
+    """G = (1/eps) R^T w + E.A (SPEC.md:488-496, Thm. 3.5)."""
     A = np.asarray(A, dtype=np.float64)
     r1, r2 = build_rhs(ws, A)
     rhs = r2 - ws.Pt(r1 / ws.r)

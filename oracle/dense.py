@@ -117,3 +117,42 @@ def dense_primal_objective(X, a, Y, b, P, eps, cost=None, la=None, lb=None):
     with np.errstate(divide="ignore", invalid="ignore"):
         kl = np.where(P > 0, P * np.log(P / ab) - P + ab, ab)
     return float((C * P).sum() + eps * kl.sum())
+
+
+class DenseOps:
+    """The stream-op interface of ``oracle.Oracle`` (apply_plan, apply_plan_adjoint,
+    apply_hadamard_plan, induced_marginals) over the materialised fp64 plan
+    P_ij = a_i b_j exp((f_i + g_j + 2 <x_i, y_j>)/eps) (shifted potentials,
+    stream.cpp:140-207 / :377-404 evaluated densely), so ``compose.Workspace`` /
+    ``compose.hvp_apply`` run at d = 1024 in seconds where the streaming port's
+    per-column transport (stream.cpp:182-186) would take hours. Pinned against the
+    port in tests/test_oracle.py. Squared-Euclidean cost only."""
+
+    def _plan(self, X, a, Y, b, f_hat, g_hat, eps):
+        X = np.asarray(X, dtype=np.float64)
+        Y = np.asarray(Y, dtype=np.float64)
+        key = (id(X), id(Y), id(f_hat), id(g_hat), float(eps))
+        if getattr(self, "_key", None) != key:
+            S = (2.0 / eps) * (X @ Y.T)
+            S += (np.asarray(f_hat, dtype=np.float64) / eps + np.log(a))[:, None]
+            S += (np.asarray(g_hat, dtype=np.float64) / eps + np.log(b))[None, :]
+            self._P = np.exp(S)
+            if not np.all(np.isfinite(self._P)):
+                raise FloatingPointError("dense plan overflow, potentials are not stabilized")
+            self._key = key
+            self._refs = (X, Y, f_hat, g_hat)   # keep the ids alive while cached
+        return self._P
+
+    def apply_plan(self, X, a, Y, b, f_hat, g_hat, eps, V, tiles=None):
+        return self._plan(X, a, Y, b, f_hat, g_hat, eps) @ np.asarray(V, dtype=np.float64)
+
+    def apply_plan_adjoint(self, X, a, Y, b, f_hat, g_hat, eps, U, tiles=None):
+        return self._plan(X, a, Y, b, f_hat, g_hat, eps).T @ np.asarray(U, dtype=np.float64)
+
+    def apply_hadamard_plan(self, X, a, Y, b, f_hat, g_hat, eps, A, B, V, tiles=None):
+        P = self._plan(X, a, Y, b, f_hat, g_hat, eps)
+        return (P * (np.asarray(A) @ np.asarray(B).T)) @ np.asarray(V, dtype=np.float64)
+
+    def induced_marginals(self, X, a, Y, b, f_hat, g_hat, eps, tiles=None):
+        P = self._plan(X, a, Y, b, f_hat, g_hat, eps)
+        return P.sum(1), P.sum(0)

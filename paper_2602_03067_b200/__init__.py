@@ -105,6 +105,7 @@ def lib() -> C.CDLL:
         L.fsk_engine_screen_live_tiles.restype = C.c_uint64
         L.fsk_engine_screen_blocks.restype = C.c_uint64
         L.fsk_engine_live_set_fraction.restype = C.c_double
+        L.fsk_device_peak_bytes.restype = C.c_int64
         for name in ("fsk_io_count_f_update", "fsk_io_count_g_update",
                      "fsk_io_count_symmetric_update", "fsk_io_count_apply_plan",
                      "fsk_io_count_apply_plan_adjoint", "fsk_io_count_apply_hadamard",
@@ -263,10 +264,25 @@ def induced_marginals(X, a, Y, b, f_hat, g_hat, eps, tiles=(64, 64), cost=None, 
     return r, c
 
 
+def _check_clouds(X, a, Y, b, pots=()):
+    """Shape checks a raw-pointer entry cannot make itself (d is passed once for both
+    clouds): 2-D clouds of equal width, weights and potentials of matching length."""
+    if X.ndim != 2 or Y.ndim != 2:
+        raise ValidationError("point clouds must be 2-D (n x d) arrays")
+    if X.shape[1] != Y.shape[1]:
+        raise ValidationError(f"source and target dimensions differ ({X.shape[1]} vs {Y.shape[1]})")
+    if a.shape != (X.shape[0],) or b.shape != (Y.shape[0],):
+        raise ValidationError("weight vector length does not match the number of points")
+    for v, want, name in pots:
+        if v.shape != (want,):
+            raise ValidationError(f"{name} length {v.shape[0] if v.ndim else 0} != {want}")
+
+
 def update_f_hat_f32(X, a, Y, b, g_hat, eps, tiles=(64, 64), ledger=None):
     k = _Keep()
     X, a, Y, b = (k.arr(v, np.float32) for v in (X, a, Y, b))
     g = k.arr(g_hat, np.float32)
+    _check_clouds(X, a, Y, b, [(g, Y.shape[0], "g_hat")])
     out = np.empty(X.shape[0], dtype=np.float32)
     _check(lib().fsk_update_f_hat_f32(
         C.c_void_p(X.ctypes.data), C.c_void_p(a.ctypes.data), C.c_int64(X.shape[0]),
@@ -280,6 +296,7 @@ def update_g_hat_f32(X, a, Y, b, f_hat, eps, tiles=(64, 64), ledger=None):
     k = _Keep()
     X, a, Y, b = (k.arr(v, np.float32) for v in (X, a, Y, b))
     f = k.arr(f_hat, np.float32)
+    _check_clouds(X, a, Y, b, [(f, X.shape[0], "f_hat")])
     out = np.empty(Y.shape[0], dtype=np.float32)
     _check(lib().fsk_update_g_hat_f32(
         C.c_void_p(X.ctypes.data), C.c_void_p(a.ctypes.data), C.c_int64(X.shape[0]),
@@ -437,6 +454,12 @@ def rng_normal(seed: int, count: int) -> np.ndarray:
     return out
 
 
+def device_peak_bytes(device: int = 0, reset: bool = False) -> int:
+    """High-water mark of the device memory pool every library allocation comes from
+    (fsk_device_peak_bytes); reset=True restarts it at the current usage."""
+    return int(lib().fsk_device_peak_bytes(C.c_int(device), C.c_int(1 if reset else 0)))
+
+
 def version() -> str:
     return lib().fsk_version().decode()
 
@@ -453,6 +476,7 @@ class Engine:
     def __init__(self, device, X, a, Y, b, mode="auto"):
         k = _Keep()
         X, a, Y, b = k.arr(X), k.arr(a), k.arr(Y), k.arr(b)
+        _check_clouds(X, a, Y, b)
         h = C.c_void_p()
         _check(lib().fsk_engine_create(C.c_int(device), C.c_void_p(X.ctypes.data),
                                        C.c_void_p(a.ctypes.data), C.c_int64(X.shape[0]),

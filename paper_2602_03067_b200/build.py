@@ -10,6 +10,7 @@ the GPU box inside the repo snapshot; nothing is installed into site-packages.
 """
 from __future__ import annotations
 
+import hashlib
 import os
 import shutil
 import subprocess
@@ -39,15 +40,21 @@ def _compile(src: Path) -> Path:
     rel = src.relative_to(CSRC)
     obj = OBJ / (str(rel).replace("/", "_") + ".o")
     deps = [src, *CSRC.glob("*.h"), *CSRC.glob("api/*.h"), *(ROOT / "include").rglob("*.h*")]
-    if obj.exists() and obj.stat().st_mtime >= max(p.stat().st_mtime for p in deps):
-        return obj
     cmd = [NVCC, *ARCH, *COMMON, "-c", str(src), "-o", str(obj)]
     if src.suffix == ".cu":
         cmd += ["-Xptxas", "-v"] if os.environ.get("FSK_PTXAS_VERBOSE") else []
+    # the full command line (FSK_NVCC_EXTRA flags change numerics / add traps) is
+    # part of the object's identity, not just the source mtimes
+    stamp = obj.with_suffix(".cmd")
+    digest = hashlib.sha256("\0".join(cmd).encode()).hexdigest()
+    if (obj.exists() and stamp.exists() and stamp.read_text() == digest
+            and obj.stat().st_mtime >= max(p.stat().st_mtime for p in deps)):
+        return obj
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError(f"nvcc failed on {src}")
+    stamp.write_text(digest)
     if r.stderr.strip() and os.environ.get("FSK_PTXAS_VERBOSE"):
         sys.stderr.write(r.stderr)
     return obj

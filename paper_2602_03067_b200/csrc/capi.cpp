@@ -882,4 +882,16 @@ int fsk_device_count(void) {
     return c;
 }
 
+int64_t fsk_device_peak_bytes(int device, int reset) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return -1;
+    if (reset) {
+        unsigned long long zero = 0;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &zero);
+    }
+    unsigned long long v = 0;
+    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &v) != cudaSuccess) return -1;
+    return int64_t(v);
+}
+
 }  // extern "C"

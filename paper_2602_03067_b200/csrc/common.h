@@ -43,7 +43,22 @@ enum : int {
 void copy_host_to_device(void* dst, const void* src, std::size_t bytes, cudaStream_t s);
 void copy_device_to_host(void* dst, const void* src, std::size_t bytes, cudaStream_t s);
 
-// Plain owning device buffer (stream-ordered allocation).
+// Owner teardown after a full device synchronize: the buffers may have been
+// allocated on caller streams that no longer exist, so frees inside the scope go
+// to the legacy default stream.
+struct DevBufTeardown {
+    bool prev;
+    DevBufTeardown() : prev(active()) { active() = true; }
+    ~DevBufTeardown() { active() = prev; }
+    static bool& active() {
+        thread_local bool a = false;
+        return a;
+    }
+};
+
+// Plain owning device buffer (stream-ordered allocation). A regrow frees the old
+// block on the stream of the regrowing call: callers that switch streams order
+// the new stream after the old one first (the engine's stream fence).
 template <typename T>
 class DevBuf {
 public:
@@ -65,13 +80,14 @@ public:
         return *this;
     }
     void alloc(std::size_t n, cudaStream_t s) {
-        release();
+        release(s);
         s_ = s;
         n_ = n;
         if (n) FSKB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), s));
     }
-    void release() {
-        if (p_) cudaFreeAsync(p_, s_);
+    void release() { release(s_); }
+    void release(cudaStream_t s) {
+        if (p_) cudaFreeAsync(p_, DevBufTeardown::active() ? cudaStream_t(nullptr) : s);
         p_ = nullptr;
         n_ = 0;
     }

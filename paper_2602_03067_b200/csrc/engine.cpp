@@ -27,6 +27,8 @@ struct fsk_engine {
     int graph_iters = 0;
     cudaStream_t graph_stream = nullptr;
     const float* graph_f = nullptr;
+    const float* graph_g = nullptr;
+    double graph_eps = 0.0;
     int device = 0;
     DevProblem<float> P;
     float* f = nullptr;
@@ -35,6 +37,12 @@ struct fsk_engine {
     cudaStream_t own = nullptr;
     int* flags = nullptr;
     int64_t launches_at_create = 0;
+    // stream fence: the engine's persistent buffers are used (and regrown) on
+    // whatever stream each call passes; a call on a new stream first waits for
+    // the last call's work
+    cudaEvent_t fence = nullptr;
+    cudaStream_t last = nullptr;
+    bool fenced = false;
 };
 
 namespace {
@@ -61,8 +69,26 @@ int eguard(F&& f) {
 // torch and its NCCL collectives - runs on that stream. The engine's private
 // stream is only used by create/set_eps, which synchronize before returning.
 cudaStream_t pick(fsk_engine* e, void* stream) {
-    (void)e;
-    return static_cast<cudaStream_t>(stream);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (e->fenced && s != e->last) FSKB_CUDA(cudaStreamWaitEvent(s, e->fence, 0));
+    return s;
+}
+
+// records the fence after a call's work on `s` (RAII at the top of each call)
+struct Fence {
+    fsk_engine* e;
+    cudaStream_t s;
+    ~Fence() {
+        if (cudaEventRecord(e->fence, s) == cudaSuccess) {
+            e->last = s;
+            e->fenced = true;
+        }
+    }
+};
+
+void drop_graph(fsk_engine* e) {
+    if (e->graph) cudaGraphExecDestroy(e->graph);
+    e->graph = nullptr;
 }
 
 }  // namespace
@@ -79,6 +105,7 @@ int fsk_engine_create(int device, const double* X, const double* a, int64_t n, c
         auto* e = new fsk_engine();
         e->device = device;
         FSKB_CUDA(cudaStreamCreateWithFlags(&e->own, cudaStreamNonBlocking));
+        FSKB_CUDA(cudaEventCreateWithFlags(&e->fence, cudaEventDisableTiming));
         FSKB_CUDA(cudaMalloc(reinterpret_cast<void**>(&e->flags), 2 * sizeof(int)));
         FSKB_CUDA(cudaMemset(e->flags, 0, 2 * sizeof(int)));
         e->P.upload(src, tgt, nullptr, e->own);
@@ -92,12 +119,18 @@ void fsk_engine_destroy(fsk_engine* e) {
     if (!e) return;
     cudaSetDevice(e->device);
     if (e->graph) cudaGraphExecDestroy(e->graph);
-    cudaStreamSynchronize(e->own);
-    e->P.tc.reset();
-    e->P.src = DevSide<float>();
-    e->P.tgt = DevSide<float>();
-    cudaStreamSynchronize(e->own);
+    // the buffers may sit on caller streams that are gone by now: drain the device,
+    // then free on the legacy stream
+    cudaDeviceSynchronize();
+    {
+        DevBufTeardown td;
+        e->P.tc.reset();
+        e->P.src = DevSide<float>();
+        e->P.tgt = DevSide<float>();
+    }
+    cudaDeviceSynchronize();
     cudaFree(e->flags);
+    cudaEventDestroy(e->fence);
     cudaStreamDestroy(e->own);
     delete e;
 }
@@ -105,14 +138,19 @@ void fsk_engine_destroy(fsk_engine* e) {
 int fsk_engine_set_eps(fsk_engine* e, double eps) {
     return eguard([&] {
         if (!(eps > 0.0)) throw ValidationFailure("eps must be positive");
+        // the captured iterate graph bakes eps (2/eps key scale, finalize eps) into
+        // its launches: a new eps needs a new capture
+        if (eps != e->eps) drop_graph(e);
         e->eps = eps;
-        e->P.s = e->own;
+        e->P.s = pick(e, e->own);
+        Fence fence_{e, e->own};
         if (e->P.tc) e->P.tc->set_eps(e->P, eps);
         FSKB_CUDA(cudaStreamSynchronize(e->own));
     });
 }
 
 int fsk_engine_bind_potentials(fsk_engine* e, float* f_dev, float* g_dev) {
+    if (f_dev != e->f || g_dev != e->g) drop_graph(e);
     e->f = f_dev;
     e->g = g_dev;
     return FSK_OK;
@@ -121,6 +159,7 @@ int fsk_engine_bind_potentials(fsk_engine* e, float* f_dev, float* g_dev) {
 int fsk_engine_init_potentials(fsk_engine* e, void* stream) {
     return eguard([&] {
         cudaStream_t s = pick(e, stream);
+        Fence fence_{e, s};
         launch_neg_sqnorm<float>(e->P.src.pts.get(), e->P.src.n, e->P.src.d, 1.0f, e->f, s);
         launch_neg_sqnorm<float>(e->P.tgt.pts.get(), e->P.tgt.n, e->P.tgt.d, 1.0f, e->g, s);
     });
@@ -135,6 +174,7 @@ int fsk_engine_half_step(fsk_engine* e, int side, int64_t row_begin, int64_t row
         if (row_begin < 0 || row_end > R || row_begin > row_end)
             throw ValidationFailure("engine row range out of bounds");
         e->P.s = pick(e, stream);
+        Fence fence_{e, e->P.s};
         const float eps = float(e->eps);
         float* pot = side == 0 ? e->f : e->g;
         const float* kpot = side == 0 ? e->g : e->f;
@@ -158,6 +198,7 @@ int fsk_engine_iterate(fsk_engine* e, int iters, void* stream) {
         if (!(e->eps > 0.0)) throw ValidationFailure("engine eps not set");
         if (iters < 1) throw ValidationFailure("iters must be positive");
         cudaStream_t s = pick(e, stream);
+        Fence fence_{e, s};
         e->P.s = s;
         const float eps = float(e->eps);
         auto body = [&] {
@@ -179,9 +220,9 @@ int fsk_engine_iterate(fsk_engine* e, int iters, void* stream) {
             body();
             return;
         }
-        if (!e->graph || e->graph_iters != iters || e->graph_stream != s || e->graph_f != e->f) {
-            if (e->graph) cudaGraphExecDestroy(e->graph);
-            e->graph = nullptr;
+        if (!e->graph || e->graph_iters != iters || e->graph_stream != s || e->graph_f != e->f ||
+            e->graph_g != e->g || e->graph_eps != e->eps) {
+            drop_graph(e);
             cudaGraph_t g = nullptr;
             FSKB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
             try {
@@ -197,6 +238,8 @@ int fsk_engine_iterate(fsk_engine* e, int iters, void* stream) {
             e->graph_iters = iters;
             e->graph_stream = s;
             e->graph_f = e->f;
+            e->graph_g = e->g;
+            e->graph_eps = e->eps;
         } else {
             count_launch(4 * iters);  // the captured launches (host-side counter)
         }
@@ -214,6 +257,7 @@ int fsk_engine_grad(fsk_engine* e, int64_t row_begin, int64_t row_end, float* gr
         const int64_t R = row_end - row_begin;
         if (R == 0) return;
         cudaStream_t s = pick(e, stream);
+        Fence fence_{e, s};
         e->P.s = s;
         const float eps = float(e->eps);
         if (e->P.tc) {
@@ -276,6 +320,7 @@ int fsk_engine_transport_mat(fsk_engine* e, int side, const float* v_dev, int64_
         if (side != 0 && side != 1) throw ValidationFailure("side must be 0 or 1");
         if (p < 1) throw ValidationFailure("p must be positive");
         cudaStream_t s = pick(e, stream);
+        Fence fence_{e, s};
         e->P.s = s;
         const float eps = float(e->eps);
         const float* kpot = side == 0 ? e->g : e->f;
@@ -297,6 +342,7 @@ int fsk_engine_transport_hadamard(fsk_engine* e, const float* a_dev, const float
         if (!e->f || !e->g) throw ValidationFailure("engine potentials not bound");
         if (p < 1) throw ValidationFailure("p must be positive");
         cudaStream_t s = pick(e, stream);
+        Fence fence_{e, s};
         e->P.s = s;
         const float eps = float(e->eps);
         SideLse L = side_lse(e, 0, s);
@@ -316,6 +362,7 @@ int fsk_engine_transport_vec(fsk_engine* e, int side, const float* v_dev, double
         if (!e->f || !e->g) throw ValidationFailure("engine potentials not bound");
         if (side != 0 && side != 1) throw ValidationFailure("side must be 0 or 1");
         cudaStream_t s = pick(e, stream);
+        Fence fence_{e, s};
         e->P.s = s;
         const float eps = float(e->eps);
         const int64_t R = side == 0 ? e->P.src.n : e->P.tgt.n;

@@ -1,7 +1,9 @@
 // Streaming Hessian-vector product (Thm. 3.5 and
 // Appendix F). Every P / P^T application is one CUDA apply pass over the
 // cached per-orientation LSE (the potentials are fixed, so the LSE passes run
-// once per call); the O(n + m) CG vector algebra stays on the host in double.
+// once per call). On the tensor path the CG iterate, residual and direction stay
+// on the device (cg_device.h, one scalar read-back per iteration); the fp64
+// engine keeps the O(n + m) CG algebra on the host in double.
 // Operation count per call: 2 K_CG + 3 transport-vector, 3 transport-matrix
 // (PY, P^T A, P(diag(w2) Y)) and 1 Hadamard-weighted transport.
 #include <cmath>
@@ -12,6 +14,7 @@
 #include <vector>
 
 #include "../../include/fsk_b200.h"
+#include "cg_device.h"
 #include "common.h"
 #include "core_kernels.h"
 #include "device_ops.h"
@@ -293,7 +296,7 @@ void hvp_run(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat
         const std::vector<double> PY = tc_mat ? H.apply_dev(0, y_dev, d) : H.apply(0, Y, d);
         timer.mark("hvp P Y");
 
-        // build_rhs (SPEC.md:319-327)
+        // build_rhs (SPEC.md:458-466)
         std::vector<double> u((size_t)(n)), uP((size_t)(n)), r1((size_t)(n));
         parallel_rows(n, d, [&](int64_t i) {
             double su = 0.0, sp = 0.0;
@@ -320,7 +323,7 @@ void hvp_run(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat
         for (int64_t j = 0; j < m; ++j) rhs[size_t(j)] = r2[size_t(j)] - rhs[size_t(j)];
 
         timer.mark("hvp rhs (P^T u, P^T A, P^T r1/r)");
-        // CG on S_tau = diag(c) - P^T diag(r)^-1 P + tau I (SPEC.md:329-347)
+        // CG on S_tau = diag(c) - P^T diag(r)^-1 P + tau I (SPEC.md:468-486)
         auto schur = [&](const std::vector<double>& v) {
             std::vector<double> pv = H.apply(0, v, 1);
             for (int64_t i = 0; i < n; ++i) pv[size_t(i)] /= r[size_t(i)];
@@ -334,7 +337,44 @@ void hvp_run(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat
         int iters = 0;
         double relres = 0.0;
         bool converged = true;
-        if (rn0 > 0.0) {
+        bool device_cg = false;
+        if constexpr (kSingle) device_cg = P.tc != nullptr && rn0 > 0.0;
+        if (device_cg) {
+            // tensor path: the CG lives on the device; each iteration is two
+            // transport-vector passes (P p, then P^T (P p / r)) plus four small
+            // vector kernels, and one scalar read-back for the stopping test
+            if constexpr (kSingle) {
+                DeviceCg cg(m, C.s);
+                DevBuf<double> rhs_d(size_t(m), C.s), pv(size_t(n), C.s), ptq(size_t(m), C.s);
+                DevBuf<float> tmpf(size_t(n), C.s);
+                rhs_d.upload(rhs.data(), size_t(m));
+                double rs = cg.init(rhs_d.get());
+                converged = false;
+                P.s = C.s;
+                while (iters < hcfg->cg_max_iters) {
+                    P.tc->vec(P, 0, g.get(), float(eps), l2h_f.get(), l2l_f.get(), r_d.get(),
+                              cg.pf.get(), pv.get(), C.flags);
+                    ledger_apply(ledger, n, m, d, 1, *tiles, cost, false);
+                    cg.div_rows(pv.get(), r_d.get(), n, tmpf.get());
+                    P.tc->vec(P, 1, f.get(), float(eps), l2h_g.get(), l2l_g.get(), c_d.get(),
+                              tmpf.get(), ptq.get(), C.flags);
+                    ledger_apply(ledger, n, m, d, 1, *tiles, cost, true);
+                    const double rs_new = cg.step(c_d.get(), ptq.get(), hcfg->tau);
+                    ++iters;
+                    if (!std::isfinite(rs_new)) throw NumericalFailure("hvp: non-finite CG iterate");
+                    if (std::sqrt(rs_new) <= hcfg->cg_tol * rn0) {
+                        converged = true;
+                        rs = rs_new;
+                        break;
+                    }
+                    cg.direction();
+                    rs = rs_new;
+                }
+                relres = std::sqrt(rs) / rn0;
+                cg.w2.download(w2.data(), size_t(m));
+                FSKB_CUDA(cudaStreamSynchronize(C.s));
+            }
+        } else if (rn0 > 0.0) {
             std::vector<double> res = rhs, pdir = rhs;
             double rs = dotv(res, res);
             converged = false;
@@ -360,7 +400,7 @@ void hvp_run(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat
             relres = std::sqrt(rs) / rn0;
         }
         timer.mark("hvp CG");
-        // w1 = diag(r)^-1 (r1 - P w2) ; R^T w (SPEC.md:349-357)
+        // w1 = diag(r)^-1 (r1 - P w2) ; R^T w (SPEC.md:488-496)
         const std::vector<double> Pw2 = H.apply(0, w2, 1);
         std::vector<double> w1((size_t)(n));
         for (int64_t i = 0; i < n; ++i) w1[size_t(i)] = (r1[size_t(i)] - Pw2[size_t(i)]) / r[size_t(i)];
@@ -379,7 +419,7 @@ void hvp_run(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat
                     w2Y[size_t(j * d + t)] = w2[size_t(j)] * Y[size_t(j * d + t)];
             Pw2Y = H.apply(0, w2Y, d);
         }
-        // explicit term (SPEC.md:309-317): B5 = (P (.) A Y^T) Y
+        // explicit term (SPEC.md:448-456): B5 = (P (.) A Y^T) Y
         timer.mark("hvp P w2, P (w2 Y)");
         const std::vector<double> B5 = H.apply(0, Y, d, A, tgt->points, d);
         timer.mark("hvp Hadamard");

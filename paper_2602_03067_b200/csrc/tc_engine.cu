@@ -2531,8 +2531,11 @@ bool TcHalfStep::build_plan(DevProblem<float>& P, const float* g, const float* f
                             const float* l2h0, const float* l2l0, const float* r, int* flags) {
     Impl& I = *impl_;
     drop_plan();
+    // opt-in (FSK_PLAN_CACHE=1): the cache holds n x m-scaled plan blocks in HBM,
+    // outside the HVP's O((n + m) d) memory contract; by default
+    // every transport-vector pass streams its scores instead
     const char* env = std::getenv("FSK_PLAN_CACHE");
-    const bool enabled = !(env && env[0] == '0');
+    const bool enabled = env && env[0] == '1';
     if (!enabled || I.chunks == 1) return false;   // the d <= 64 kernels do not store blocks
     if (!(I.live_valid[0] && I.live_kpot[0] == g && I.live_valid[1] && I.live_kpot[1] == f))
         return false;

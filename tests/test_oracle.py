@@ -137,3 +137,64 @@ def test_dense_and_streaming_hvp_compositions_agree(port):
     assert np.linalg.norm(H - Hd) <= 1e-9 * np.linalg.norm(Hd)
     # operation accounting of Thm. 3.5: 2K+3 vector, 3 matrix, 1 Hadamard
     assert ws.counts == dict(vector=2 * iters + 3, matrix=3, hadamard=1)
+
+
+def test_row_slice_restatements_match_full_port(port):
+    """oracle/rows.py (the checker behind the benchmark-size parity tests): sliced
+    half-steps are bit-identical to the same rows of a full port call; the numpy
+    transport rows and SPEC gradient rows match the port's apply_plan composition
+    to fp64 rounding."""
+    from oracle import compose, rows as orows
+    rng = np.random.default_rng(5)
+    n, m, d, eps = 300, 260, 7, 0.2
+    X, Y = rng.normal(size=(n, d)), rng.normal(size=(m, d))
+    a = orows.slice_weights(n)
+    b = rng.random(m) + 0.5
+    b /= b.sum()
+    b[-1] = 1.0 - np.cumsum(b[:-1])[-1]
+    g = -(Y ** 2).sum(1) + 0.1 * rng.normal(size=m)
+    f = port.update_f_hat(X, a, Y, b, g, eps)
+    g = port.update_g_hat(X, a, Y, b, f, eps)
+    sel = np.sort(rng.choice(n, 70, replace=False))
+    assert np.array_equal(orows.half_step_rows(port, 0, X, a, Y, b, g, eps, sel),
+                          port.update_f_hat(X, a, Y, b, g, eps)[sel])
+    selg = np.sort(rng.choice(m, 50, replace=False))
+    assert np.array_equal(orows.half_step_rows(port, 1, X, a, Y, b, f, eps, selg),
+                          port.update_g_hat(X, a, Y, b, f, eps)[selg])
+    PY = port.apply_plan(X, a, Y, b, f, g, eps, Y)
+    got = orows.transport_rows(X[sel], a[sel], f[sel], Y, b, g, eps, Y, chunk=97)
+    assert np.abs(got - PY[sel]).max() <= 1e-12 * np.abs(PY).max()
+    ws = compose.Workspace(port, X, a, Y, b, f, g, eps)
+    G = compose.grad_source(ws)
+    Gr, r, _ = orows.grad_rows(port, X, a, Y, b, f, g, eps, sel)
+    assert np.abs(Gr - G[sel]).max() <= 1e-11 * np.abs(G).max()
+    e32 = orows.grad_rows_fp32_error(port, X, a, Y, b, f, g, eps, sel, Gr, r)
+    assert 0.0 < e32 < 1e-3
+
+
+def test_dense_ops_match_port_stream_ops(port):
+    """oracle.dense.DenseOps (the checker of the d = 1024 single-precision HVP) agrees
+    with the port's streaming transport / marginals and gives the same SPEC HVP."""
+    from oracle import compose
+    from oracle.dense import DenseOps
+    rng = np.random.default_rng(8)
+    n, m, d, eps = 90, 70, 6, 0.4
+    X, Y = rng.normal(size=(n, d)), rng.normal(size=(m, d)) + 0.2
+    a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+    s = port.sinkhorn_solve(X, a, Y, b, eps=eps, max_iters=60)
+    f, g = s["f_hat"], s["g_hat"]
+    D = DenseOps()
+    V, U, A = rng.normal(size=(m, 3)), rng.normal(size=(n, 2)), rng.normal(size=(n, d))
+    want = port.apply_plan(X, a, Y, b, f, g, eps, V)
+    assert np.abs(D.apply_plan(X, a, Y, b, f, g, eps, V) - want).max() <= 1e-12 * np.abs(want).max()
+    want = port.apply_plan_adjoint(X, a, Y, b, f, g, eps, U)
+    assert np.abs(D.apply_plan_adjoint(X, a, Y, b, f, g, eps, U) - want).max() <= 1e-12 * np.abs(want).max()
+    want = port.apply_hadamard_plan(X, a, Y, b, f, g, eps, A, Y, Y)
+    got = D.apply_hadamard_plan(X, a, Y, b, f, g, eps, A, Y, Y)
+    assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
+    r, c = port.induced_marginals(X, a, Y, b, f, g, eps)
+    rd, cd = D.induced_marginals(X, a, Y, b, f, g, eps)
+    assert np.abs(rd - r).max() <= 1e-13 and np.abs(cd - c).max() <= 1e-13
+    H1 = compose.hvp_apply(compose.Workspace(port, X, a, Y, b, f, g, eps), A, max_iters=40)[0]
+    H2 = compose.hvp_apply(compose.Workspace(D, X, a, Y, b, f, g, eps), A, max_iters=40)[0]
+    assert np.linalg.norm(H1 - H2) <= 1e-9 * np.linalg.norm(H1)

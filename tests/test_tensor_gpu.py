@@ -543,6 +543,47 @@ def test_engine_iterate_graph_matches_loop(fsk):
         assert np.array_equal(fr, res[0][0]) and np.array_equal(gr, res[0][1])
 
 
+def test_engine_iterate_graph_follows_eps_and_rebinding(fsk):
+    """An eps-annealing loop (set_eps(e_k); iterate(k)) and a rebinding of g must not
+    replay a graph captured for the old eps / old buffer: every iterate() equals the
+    per-call half-step loop at the current eps and buffers."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(22)
+    n, m, d = 800, 700, 3
+    X, Y = rng.normal(size=(n, d)), rng.normal(size=(m, d))
+    a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+    s = torch.cuda.Stream()
+
+    def run(use_iterate):
+        eng = fsk.Engine(0, X, a, Y, b, mode="fma")
+        f = torch.empty(n, dtype=torch.float32, device="cuda")
+        g = torch.empty(m, dtype=torch.float32, device="cuda")
+        g2 = torch.empty(m, dtype=torch.float32, device="cuda")
+        eng.bind(f.data_ptr(), g.data_ptr())
+        eng.set_eps(1.0)
+        eng.init_potentials(s.cuda_stream)
+        out = []
+        for eps, gbuf in ((1.0, g), (0.5, g), (0.25, g), (0.25, g2)):
+            if gbuf is g2:
+                g2.copy_(g)
+                eng.bind(f.data_ptr(), g2.data_ptr())
+            eng.set_eps(eps)
+            if use_iterate:
+                eng.iterate(3, s.cuda_stream)
+            else:
+                for _ in range(3):
+                    eng.half_step(0, 0, n, 0, s.cuda_stream)
+                    eng.half_step(1, 0, m, 0, s.cuda_stream)
+            s.synchronize()
+            out.append((f.cpu().numpy().copy(), gbuf.cpu().numpy().copy()))
+        eng.close()
+        return out
+
+    want, got = run(False), run(True)
+    for (fw, gw), (fg, gg) in zip(want, got):
+        assert np.array_equal(fw, fg) and np.array_equal(gw, gg)
+
+
 @pytest.mark.parametrize("n,m,d", [(1, 1, 64), (1, 300, 64), (300, 1, 64), (2, 3, 100), (1, 1, 1024),
                                    (127, 129, 65)])
 def test_tensor_degenerate_shapes(fsk, port, tensor_mode, n, m, d):
