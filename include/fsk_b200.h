@@ -194,6 +194,16 @@ int fsk_sinkhorn_solve(const fsk_measure* src, const fsk_measure* tgt, const fsk
                        const fsk_config* cfg, const fsk_tiles* tiles, fsk_ledger* ledger,
                        fsk_report* report);
 
+/* Warm-started solve (the downstream re-solve loops of SPEC.md:656):
+ * sinkhorn_solve from the caller's shifted potentials (f_init n, g_init m) instead
+ * of the reference init f_hat = -alpha, g_hat = -beta (solver.cpp:27-32); same
+ * schedule, stopping rule and report. out_grad (n x d, nullable) as in
+ * fsk_sinkhorn_solve_grad. */
+int fsk_sinkhorn_solve_warm(const fsk_measure* src, const fsk_measure* tgt, const fsk_cost* cost,
+                            const fsk_config* cfg, const fsk_tiles* tiles, fsk_ledger* ledger,
+                            const double* f_init, const double* g_init, fsk_report* report,
+                            double* out_grad);
+
 /* fsk::solver::dual_cost (solver.hpp:23-25, solver.cpp:131-143) */
 int fsk_dual_cost(const fsk_measure* src, const fsk_measure* tgt, const double* f_hat,
                   const double* g_hat, double eps, const fsk_cost* cost, const fsk_tiles* tiles,
@@ -314,6 +324,10 @@ double fsk_engine_live_set_fraction(const fsk_engine* e, int side);
 /* (query tile, key tile) blocks covered by those tracked passes. */
 uint64_t fsk_engine_screen_blocks(const fsk_engine* e);
 /* Launch counter of this engine's kernels (for bench accounting). */
+/* LSE passes the tensor path ran so far, by kind: out[0] screened cold passes
+ * (5-MMA phase 1 + live blocks), out[1] warm-bound passes, out[2] plain passes. */
+void fsk_engine_pass_counts(const fsk_engine* e, uint64_t out[3]);
+
 int64_t fsk_engine_kernel_launches(const fsk_engine* e);
 /* Name of the kernel path the engine uses for half-steps ("tcgen05-split3" / "fma-f32"). */
 const char* fsk_engine_path(const fsk_engine* e);

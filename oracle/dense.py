@@ -128,14 +128,30 @@ class DenseOps:
     per-column transport (stream.cpp:182-186) would take hours. Pinned against the
     port in tests/test_oracle.py. Squared-Euclidean cost only."""
 
+    def __init__(self, fp32_scores: bool = False):
+        # fp32_scores: S_ij = <x_i, y_j (2/eps)> + (g_j + eps log b_j)/eps evaluated in
+        # fp32 as the reference's single-precision path does (make_ctx_f32,
+        # stream.cpp:421-434: float clouds, keys pre-scaled by 2/eps, float bias), the
+        # rest in fp64. The HVP computed on that plan measures what fp32-grade score
+        # arithmetic alone does to the result (the "e32" of the tensor-mode bounds).
+        self.fp32_scores = fp32_scores
+
     def _plan(self, X, a, Y, b, f_hat, g_hat, eps):
         X = np.asarray(X, dtype=np.float64)
         Y = np.asarray(Y, dtype=np.float64)
         key = (id(X), id(Y), id(f_hat), id(g_hat), float(eps))
         if getattr(self, "_key", None) != key:
-            S = (2.0 / eps) * (X @ Y.T)
-            S += (np.asarray(f_hat, dtype=np.float64) / eps + np.log(a))[:, None]
-            S += (np.asarray(g_hat, dtype=np.float64) / eps + np.log(b))[None, :]
+            if self.fp32_scores:
+                k32 = Y.astype(np.float32) * np.float32(2.0 / eps)
+                bias32 = ((np.asarray(g_hat).astype(np.float32) +
+                           np.float32(eps) * np.log(np.asarray(b).astype(np.float32))) /
+                          np.float32(eps)).astype(np.float32)
+                S = ((X.astype(np.float32) @ k32.T) + bias32[None, :]).astype(np.float64)
+                S += (np.asarray(f_hat, dtype=np.float64) / eps + np.log(a))[:, None]
+            else:
+                S = (2.0 / eps) * (X @ Y.T)
+                S += (np.asarray(f_hat, dtype=np.float64) / eps + np.log(a))[:, None]
+                S += (np.asarray(g_hat, dtype=np.float64) / eps + np.log(b))[None, :]
             self._P = np.exp(S)
             if not np.all(np.isfinite(self._P)):
                 raise FloatingPointError("dense plan overflow, potentials are not stabilized")

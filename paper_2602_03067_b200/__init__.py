@@ -333,8 +333,10 @@ def _config(eps, schedule, max_iters, marginal_tol, eps_scaling_factor, extra_it
 
 def sinkhorn_solve(X, a, Y, b, eps=0.1, schedule="alternating", max_iters=100, marginal_tol=0.0,
                    eps_scaling_factor=1.0, extra_iters_at_final_eps=0, precision="double",
-                   tiles=(64, 64), cost=None, la=None, lb=None, ledger=None, grad=False):
-    """fsk::solver::sinkhorn_solve; with grad=True also returns grad_X (fwd+grad)."""
+                   tiles=(64, 64), cost=None, la=None, lb=None, ledger=None, grad=False,
+                   f_init=None, g_init=None):
+    """fsk::solver::sinkhorn_solve; with grad=True also returns grad_X (fwd+grad).
+    f_init / g_init (shifted potentials): warm start (fsk_sinkhorn_solve_warm)."""
     k = _Keep()
     src, tgt = k.measure(X, a, la), k.measure(Y, b, lb)
     cfg = _config(eps, schedule, max_iters, marginal_tol, eps_scaling_factor,
@@ -342,7 +344,19 @@ def sinkhorn_solve(X, a, Y, b, eps=0.1, schedule="alternating", max_iters=100, m
     f, g = np.empty(src.n), np.empty(tgt.n)
     hist = np.zeros(max(max_iters, 1))
     rep = _Report(f.ctypes.data, g.ctypes.data, hist.ctypes.data, len(hist), 0, 0.0, 0.0, 0.0)
-    if grad:
+    if f_init is not None or g_init is not None:
+        if f_init is None or g_init is None:
+            raise ValidationError("warm start needs both f_init and g_init")
+        fi, gi = k.arr(f_init), k.arr(g_init)
+        if fi.shape != (src.n,) or gi.shape != (tgt.n,):
+            raise ValidationError("warm-start potentials do not match the measures")
+        G = np.empty((src.n, src.d)) if grad else None
+        _check(lib().fsk_sinkhorn_solve_warm(
+            C.byref(src), C.byref(tgt), C.byref(k.cost(cost)), C.byref(cfg),
+            C.byref(_tiles(tiles)), _lp(ledger), C.c_void_p(fi.ctypes.data),
+            C.c_void_p(gi.ctypes.data), C.byref(rep),
+            C.c_void_p(G.ctypes.data) if grad else None))
+    elif grad:
         G = np.empty((src.n, src.d))
         _check(lib().fsk_sinkhorn_solve_grad(C.byref(src), C.byref(tgt), C.byref(k.cost(cost)),
                                              C.byref(cfg), C.byref(_tiles(tiles)), _lp(ledger),
@@ -512,6 +526,12 @@ class Engine:
     def screened_blocks(self) -> int:
         """(query tile, key tile) blocks covered by tracked LSE passes so far."""
         return int(lib().fsk_engine_screen_blocks(self.h))
+
+    def pass_counts(self) -> dict:
+        """LSE passes of the tensor path so far by kind (screened / warm / plain)."""
+        out = (C.c_uint64 * 3)()
+        lib().fsk_engine_pass_counts(self.h, out)
+        return {"screened": int(out[0]), "warm": int(out[1]), "plain": int(out[2])}
 
     @staticmethod
     def launches() -> int:

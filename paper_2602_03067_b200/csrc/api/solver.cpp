@@ -44,6 +44,36 @@ SolveReport sinkhorn_solve(const DiscreteMeasure& src, const DiscreteMeasure& tg
     return rep;
 }
 
+SolveReport sinkhorn_solve_warm(const DiscreteMeasure& src, const DiscreteMeasure& tgt,
+                                const CostSpec& spec, const SinkhornConfig& cfg,
+                                const TileConfig& tiles, IoLedger& ledger,
+                                const ShiftedPotentials& init) {
+    validate_problem(src, tgt, spec);
+    validate_sinkhorn_config(cfg);
+    validate_tiles(tiles);
+    check_pots(init, src.size(), tgt.size());
+    const fsk_measure a = bridge::view(src), b = bridge::view(tgt);
+    const fsk_cost c = bridge::view(spec);
+    const fsk_tiles t = bridge::view(tiles);
+    const fsk_config k = bridge::view(cfg);
+    bridge::LedgerScope led(ledger);
+    SolveReport rep;
+    rep.potentials.f_hat.resize(src.size());
+    rep.potentials.g_hat.resize(tgt.size());
+    std::vector<double> hist(std::size_t(cfg.max_iters));
+    fsk_report r{rep.potentials.f_hat.data(), rep.potentials.g_hat.data(), hist.data(),
+                 int64_t(hist.size()), 0, 0.0, 0.0, 0.0};
+    bridge::check(fsk_sinkhorn_solve_warm(&a, &b, &c, &k, &t, led.get(), init.f_hat.data(),
+                                          init.g_hat.data(), &r, nullptr));
+    rep.iterations = r.iterations;
+    rep.marginal_violation = r.marginal_violation;
+    rep.dual_cost = r.dual_cost;
+    rep.potentials.eps = r.eps;
+    hist.resize(std::size_t(r.iterations));
+    rep.eps_history = std::move(hist);
+    return rep;
+}
+
 double dual_cost(const DiscreteMeasure& src, const DiscreteMeasure& tgt,
                  const ShiftedPotentials& p, const CostSpec& spec, const TileConfig& tiles,
                  IoLedger& ledger) {

@@ -248,7 +248,8 @@ HostMarginals marginals_to_host(DevProblem<T>& P, const T* f, const T* g, T eps,
 template <typename T>
 void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* cost,
                 const fsk_config& cfg, const fsk_tiles& tiles, fsk_ledger* ledger,
-                fsk_report* rep, double* grad_out) {
+                fsk_report* rep, double* grad_out, const double* f_init = nullptr,
+                const double* g_init = nullptr) {
     constexpr bool kSingle = std::is_same_v<T, float>;
     const int64_t n = src.n, m = tgt.n, d = src.d;
     auto& C = exec_ctx();
@@ -262,8 +263,10 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
     const double fs = feature_scale(cost);
     const std::vector<double> alpha = host_sqnorm(src, fs), beta = host_sqnorm(tgt, fs);
     std::vector<double> f0((size_t)(n)), g0((size_t)(m));
-    for (int64_t i = 0; i < n; ++i) f0[size_t(i)] = -alpha[size_t(i)];
-    for (int64_t j = 0; j < m; ++j) g0[size_t(j)] = -beta[size_t(j)];
+    // reference init f = g = 0, i.e. f_hat = -alpha, g_hat = -beta (solver.cpp:27-32);
+    // a warm start (fsk_sinkhorn_solve_warm) starts from the caller's shifted pair
+    for (int64_t i = 0; i < n; ++i) f0[size_t(i)] = f_init ? f_init[i] : -alpha[size_t(i)];
+    for (int64_t j = 0; j < m; ++j) g0[size_t(j)] = g_init ? g_init[j] : -beta[size_t(j)];
     DevBuf<T> f = dev_from<T>(f0.data(), n, C.s), g = dev_from<T>(g0.data(), m, C.s);
     DevBuf<T> f2, g2;
     if (cfg.schedule == 1) {
@@ -282,6 +285,21 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
     bool stopped = false;
     std::vector<double> hist;
     double cur_tc_eps = -1.0;
+    // Fused convergence check (alternating schedule, fp64, marginal_tol > 0; SURVEY
+    // §8a): the violation of iterate k needs f+ = the f-update of iteration k + 1,
+    // so that f-update emits r_i = a_i exp((f_k - f_{k+1})/eps) and sum |r - a| as a
+    // by-product (c = b exactly: g_k is the g-update of f_k). Stopping returns
+    // iterate k and drops f_{k+1}: the reference's result (solver.cpp:51-60) for one
+    // extra pass at the stop instead of two marginal passes every iteration.
+    const bool fused_check = !kSingle && cfg.marginal_tol > 0.0 && cfg.schedule == 0;
+    DevBuf<T> f_next, r_dev;
+    DevBuf<double> viol_dev;
+    bool check_pending = false;   // iterate `iters` awaits its violation
+    if (fused_check) {
+        f_next.alloc(size_t(n), C.s);
+        r_dev.alloc(size_t(n), C.s);
+        viol_dev.alloc(1, C.s);
+    }
     for (double eps_d : schedule) {
         const T eps = T(eps_d);
         final_eps = eps_d;
@@ -296,7 +314,45 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
         fa.flags = C.flags;
         fa.bad_iter = C.bad_iter;
         fa.iter = iters + 1;
-        if (cfg.schedule == 0) {
+        if (cfg.schedule == 0 && check_pending) {
+            // f_{k+1} with the lagged violation of iterate k fused into its epilogue
+            FinalizeArgs<T> fv = fa;
+            fv.out_pot = f_next.get();
+            fv.old_pot = f.get();
+            fv.w = P.src.w.get();
+            fv.out_marg = r_dev.get();
+            fv.marg_flag = kFlagNonFiniteRowMarginal;
+            fv.viol = viol_dev.get();
+            viol_dev.zero();
+            half_step<T>(P, 0, g.get(), eps, fv);
+            double hv = 0.0;
+            FSKB_CUDA(cudaMemcpyAsync(&hv, viol_dev.get(), sizeof(double), cudaMemcpyDeviceToHost,
+                                      C.s));
+            FSKB_CUDA(cudaStreamSynchronize(C.s));
+            // the reference's induced_marginals + violation of iterate k
+            ledger_marginals(ledger, n, m, d, tiles, cost);
+            check_pending = false;
+            viol = hv;
+            if (viol <= cfg.marginal_tol) {
+                const int fl = read_and_clear_flags(C);
+                if (fl) throw_for_flags(fl, " at iteration " + std::to_string(iters));
+                HostMarginals hm;
+                hm.r.resize(size_t(n));
+                dev_to<T>(r_dev, hm.r.data(), n, C.s);
+                std::vector<double> fh((size_t)(n)), gh((size_t)(m));
+                dev_to<T>(f, fh.data(), n, C.s);
+                dev_to<T>(g, gh.data(), m, C.s);
+                ledger_marginals(ledger, n, m, d, tiles, cost);
+                dual = dual_value(src, tgt, fh.data(), gh.data(), alpha, beta, hm.r, final_eps);
+                stopped = true;
+                break;
+            }
+            std::swap(f, f_next);
+            fa.out_pot = g.get();
+            half_step<T>(P, 1, f.get(), eps, fa);
+            ledger_update_f(ledger, n, m, d, tiles, cost);
+            ledger_update_g(ledger, n, m, d, tiles, cost);
+        } else if (cfg.schedule == 0) {
             fa.out_pot = f.get();
             half_step<T>(P, 0, g.get(), eps, fa);
             fa.out_pot = g.get();
@@ -329,7 +385,9 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
         hist.push_back(eps_d);
         // early stopping is checked at the final eps only; the reference's
         // single-precision loop ignores it (solver.cpp:87-108)
-        if (!kSingle && cfg.marginal_tol > 0.0 && eps_d == cfg.eps) {
+        if (fused_check && eps_d == cfg.eps) {
+            check_pending = true;   // decided by the next iteration's f-update
+        } else if (!kSingle && !fused_check && cfg.marginal_tol > 0.0 && eps_d == cfg.eps) {
             const int fl = read_and_clear_flags(C);
             if (fl) throw_for_flags(fl, " at iteration " + std::to_string(iters));
             HostMarginals hm = marginals_to_host<T>(P, f.get(), g.get(), eps, C);
@@ -377,6 +435,9 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
         sync_and_check(C);
         ledger_marginals(ledger, n, m, d, tiles, cost);
         viol = violation(hm, src, tgt);
+        // the last iterate's own tolerance check (fused path: never run in the loop);
+        // the reference charges it unless that check stopped the solve
+        if (check_pending && !(viol <= cfg.marginal_tol)) ledger_marginals(ledger, n, m, d, tiles, cost);
         ledger_marginals(ledger, n, m, d, tiles, cost);
         dual = dual_value(src, tgt, fh.data(), gh.data(), alpha, beta, hm.r, pot_eps);
     }
@@ -722,6 +783,28 @@ int fsk_sinkhorn_solve_grad(const fsk_measure* src, const fsk_measure* tgt, cons
             solve_impl<float>(*src, *tgt, cost, *cfg, *tiles, ledger, report, out_grad);
         } else {
             solve_impl<double>(*src, *tgt, cost, *cfg, *tiles, ledger, report, out_grad);
+        }
+    });
+}
+
+int fsk_sinkhorn_solve_warm(const fsk_measure* src, const fsk_measure* tgt, const fsk_cost* cost,
+                            const fsk_config* cfg, const fsk_tiles* tiles, fsk_ledger* ledger,
+                            const double* f_init, const double* g_init, fsk_report* report,
+                            double* out_grad) {
+    return guarded([&] {
+        common_checks(src, tgt, cost, tiles);
+        validate_config_raw(*cfg);
+        if (!f_init || !g_init) throw ValidationFailure("warm start needs both potentials");
+        check_potentials_raw(f_init, src->n, g_init, tgt->n, cfg->eps);
+        if (cfg->precision == 0) {
+            if (labeled_cost(cost))
+                throw ValidationFailure(
+                    "single-precision solve supports the squared-Euclidean cost only");
+            solve_impl<float>(*src, *tgt, cost, *cfg, *tiles, ledger, report, out_grad, f_init,
+                              g_init);
+        } else {
+            solve_impl<double>(*src, *tgt, cost, *cfg, *tiles, ledger, report, out_grad, f_init,
+                               g_init);
         }
     });
 }

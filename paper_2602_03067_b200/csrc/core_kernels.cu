@@ -183,10 +183,21 @@ __global__ void lse_finalize_kernel(const T* __restrict__ part_m, const T* __res
         }
         if (a.out_pot) a.out_pot[i] = a.sym_old ? T(0.5) * a.sym_old[i] + T(0.5) * pot : pot;
     }
-    if (a.viol) {
-        for (int off = 16; off >= 1; off >>= 1) vsum += __shfl_xor_sync(0xffffffffu, vsum, off);
-        if ((threadIdx.x & 31) == 0 && vsum != 0.0) atomicAdd(a.viol, vsum);
+    if (a.viol) viol_block_partial(vsum, a.viol_part);
+}
+
+__global__ void viol_accumulate_kernel(const double* __restrict__ part, int nb,
+                                       double* __restrict__ viol) {
+    __shared__ double sh[256];
+    double v = 0.0;
+    for (int i = threadIdx.x; i < nb; i += 256) v += part[i];
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
     }
+    if (threadIdx.x == 0) *viol += sh[0];
 }
 
 template <typename T, bool LAB, bool HAD>
@@ -366,7 +377,20 @@ void launch_lse_finalize(const T* part_m, const T* part_s, int splits, int64_t R
                          const FinalizeArgs<T>& a, cudaStream_t s) {
     FinalizeArgs<T> fa = a;
     fa.break_lse = break_lse_flag() ? 1 : 0;
-    lse_finalize_kernel<T><<<blocks_for(R), 256, 0, s>>>(part_m, part_s, splits, R, fa);
+    const unsigned nb = blocks_for(R);
+    DevBuf<double> vpart;
+    if (fa.viol) {
+        vpart.alloc(nb, s);
+        fa.viol_part = vpart.get();
+    }
+    lse_finalize_kernel<T><<<nb, 256, 0, s>>>(part_m, part_s, splits, R, fa);
+    FSKB_CUDA(cudaGetLastError());
+    count_launch();
+    if (fa.viol) launch_viol_accumulate(vpart.get(), int(nb), fa.viol, s);
+}
+
+void launch_viol_accumulate(const double* part, int nb, double* viol, cudaStream_t s) {
+    viol_accumulate_kernel<<<1, 256, 0, s>>>(part, nb, viol);
     FSKB_CUDA(cudaGetLastError());
     count_launch();
 }

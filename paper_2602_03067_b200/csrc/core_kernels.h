@@ -51,7 +51,8 @@ struct FinalizeArgs {
     const T* old_pot;    // for marginals: r_i = w_i exp((old_pot_i - pot_i) / eps)
     const T* w;
     T* out_marg;
-    double* viol;        // += sum_i |r_i - w_i|
+    double* viol;        // += sum_i |r_i - w_i| (fixed-order: per-block partials in
+                         // viol_part, summed by launch_viol_accumulate)
     int marg_flag;       // which flag bit a non-finite marginal raises
     int* flags;
     int* bad_iter;       // nullable: atomicMin(iter) on a non-finite potential
@@ -59,7 +60,27 @@ struct FinalizeArgs {
     int break_lse;       // negative control (set by the launchers)
     float* out_l2h = nullptr;  // tcgen05 path only: log2(e) LSE split hi + lo (float pair)
     float* out_l2l = nullptr;
+    double* viol_part = nullptr;  // set by the launchers when viol != null
 };
+
+// *viol += sum of part[0 .. nb) in index order (one block): the marginal
+// violation is bit-identical run to run.
+void launch_viol_accumulate(const double* part, int nb, double* viol, cudaStream_t s);
+
+#ifdef __CUDACC__
+// Block-level partial of the violation, in a fixed order (256-thread blocks).
+__device__ __forceinline__ void viol_block_partial(double v, double* part) {
+    __shared__ double wsum[8];
+    for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) t += wsum[w];
+        part[blockIdx.x] = t;
+    }
+}
+#endif
 
 // Number of column splits used for R rows (fills the machine when R is small).
 int lse_splits(int64_t R, int64_t C);

@@ -412,6 +412,15 @@ uint64_t fsk_engine_screen_blocks(const fsk_engine* e) {
     return uint64_t(e->P.tc->screened_blocks());
 }
 
+void fsk_engine_pass_counts(const fsk_engine* e, uint64_t out[3]) {
+    unsigned long long c[3] = {0, 0, 0};
+    if (e && e->P.tc) {
+        e->P.tc->live_tiles();   // drains the pending read-backs
+        e->P.tc->pass_counts(c);
+    }
+    for (int k = 0; k < 3; ++k) out[k] = uint64_t(c[k]);
+}
+
 int64_t fsk_engine_kernel_launches(const fsk_engine* e) {
     (void)e;
     return launch_counter();

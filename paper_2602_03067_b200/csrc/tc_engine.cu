@@ -1635,10 +1635,7 @@ __global__ void tc_finalize_kernel(const double* __restrict__ pm, const double* 
         }
         if (a.out_pot) a.out_pot[i] = a.sym_old ? 0.5f * a.sym_old[i] + 0.5f * pot : pot;
     }
-    if (a.viol) {
-        for (int off = 16; off >= 1; off >>= 1) vsum += __shfl_xor_sync(0xffffffffu, vsum, off);
-        if ((threadIdx.x & 31) == 0 && vsum != 0.0) atomicAdd(a.viol, vsum);
-    }
+    if (a.viol) viol_block_partial(vsum, a.viol_part);
 }
 
 // ---- operand images ------------------------------------------------------------
@@ -1978,6 +1975,8 @@ struct TcHalfStep::Impl {
     bool warm_ok[2] = {false, false}, last_warm_track[2] = {false, false};
     int64_t warm_rb[2] = {0, 0}, warm_re[2] = {0, 0};
     unsigned long long warm_blocks = 0;
+    // LSE passes by kind: screened cold, warm-bound, plain (unscreened, untracked)
+    unsigned long long n_pass[3] = {0, 0, 0};
     int probe_dev = -1;
     ~Impl() {
         if (h_live) release_probe_bufs(probe_dev, h_live, ev);
@@ -2008,6 +2007,10 @@ unsigned long long TcHalfStep::live_tiles() const {
 }
 
 unsigned long long TcHalfStep::screened_blocks() const { return impl_->screened_blocks; }
+
+void TcHalfStep::pass_counts(unsigned long long out[3]) const {
+    for (int k = 0; k < 3; ++k) out[k] = impl_->n_pass[k];
+}
 
 double TcHalfStep::live_set_fraction(int side) const {
     const Impl& I = *impl_;
@@ -2316,10 +2319,12 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         p.part_arg = I.part_arg[side].get();
     }
     if (screen && !cold_screen) {
+        // wait for the previous probe of this side (one pass of pipeline): the decision
+        // must not depend on whether an asynchronous read-back has landed, or results
+        // would differ run to run at rounding level
+        if (I.pending[side]) FSKB_CUDA(cudaEventSynchronize(I.ev[side]));
         poll_screen(side, kScreenMaxLive);
-        if (I.pending[side]) {
-            screen = I.live_est[side] < kScreenMaxLive;  // last estimate still in flight
-        } else if (I.live_est[side] >= kScreenMaxLive) {
+        if (I.live_est[side] >= kScreenMaxLive) {
             screen = I.skip_left[side] <= 0;               // re-probe after the backoff
             --I.skip_left[side];
         }
@@ -2365,6 +2370,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         p.plan_out = ex->plan_out;
         p.plan_slot = ex->plan_slot;
     }
+    if (!vec) ++I.n_pass[screen ? 0 : (p.live_in && p.live_tq) ? 1 : 2];
     if (I.chunks == 1) {
         if (vec)
             tc_lse_tq_kernel<true, false><<<grid, NUM_THREADS, TQ_SMEM_BYTES, P.s>>>(p);
@@ -2403,12 +2409,19 @@ void TcHalfStep::run(DevProblem<float>& P, int side, const float* kpot, float ep
     fb.break_lse = break_lse_flag() ? 1 : 0;
     Impl& I = *impl_;
     const bool warm = I.last_warm_track[side];
-    tc_finalize_kernel<<<unsigned((rows + 255) / 256), 256, 0, P.s>>>(
+    const unsigned nb = unsigned((rows + 255) / 256);
+    DevBuf<double> vpart;
+    if (fb.viol) {
+        vpart.alloc(nb, P.s);
+        fb.viol_part = vpart.get();
+    }
+    tc_finalize_kernel<<<nb, 256, 0, P.s>>>(
         pm.get(), ps.get(), splits, R, row_begin, row_end, fb,
         warm ? I.part_arg[side].get() : nullptr, warm ? I.argtile[side].get() : nullptr,
         warm ? I.rowmax[side].get() : nullptr);
     FSKB_CUDA(cudaGetLastError());
     count_launch();
+    if (fb.viol) launch_viol_accumulate(vpart.get(), int(nb), fb.viol, P.s);
     if (warm) {
         I.warm_ok[side] = true;
         I.warm_rb[side] = row_begin;

@@ -31,6 +31,8 @@ public:
     // phase 2 of screened passes, and blocks those passes covered.
     unsigned long long live_tiles() const;
     unsigned long long screened_blocks() const;
+    // LSE passes run so far: [screened cold, warm-bound, plain]
+    void pass_counts(unsigned long long out[3]) const;
     // Fraction of (query tile pair, key tile) blocks in the live set of the last
     // LSE pass of `side` (-1 when none is recorded); synchronizes the device.
     double live_set_fraction(int side) const;

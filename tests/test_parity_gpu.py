@@ -93,6 +93,9 @@ def test_solver_tolerance_and_scaling_golden(fsk, golden):
     s = fsk.sinkhorn_solve(X, a, Y, b, eps=0.2, max_iters=2000, marginal_tol=1e-9)
     assert abs(s["iterations"] - int(G["sv_tol_s"][0])) <= 1
     assert abs(s["dual_cost"] - G["sv_tol_s"][2]) < 1e-9
+    if s["iterations"] == int(G["sv_tol_s"][0]):
+        # the fused lagged check reports the reference's violation of the same iterate
+        assert abs(s["marginal_violation"] - G["sv_tol_s"][1]) <= 1e-6 * G["sv_tol_s"][1]
     s = fsk.sinkhorn_solve(X, a, Y, b, eps=0.2, max_iters=300, eps_scaling_factor=0.8,
                            extra_iters_at_final_eps=20)
     assert np.array_equal(s["eps_history"], G["sv_sc_hist"])
@@ -243,3 +246,33 @@ def test_break_lse_negative_control(fsk, port):
     finally:
         fsk.debug_break_lse(False)
     assert np.abs(fsk.update_f_hat(X, a, Y, b, g, 0.1) - good).max() < 1e-12
+
+
+@pytest.mark.parametrize("tol", [1e-3, 1e-6, 1e-9])
+def test_fused_convergence_matches_reference_stop(fsk, port, tol):
+    """N1: the drop-in fp64 solver's early stop runs the reference's check
+    (solver.cpp:51-60) as a by-product of the next f-update (one extra pass at the
+    stop instead of two marginal passes per iteration): same stopping iterate, the
+    same violation to 1e-6 relative, the same dual cost, and the reference ledger."""
+    rng = np.random.default_rng(31)
+    n, m, d = 300, 260, 5
+    X, Y = rng.normal(size=(n, d)), rng.normal(size=(m, d)) * 0.8 + 0.1
+    a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+    led = fsk.Ledger()
+    s = fsk.sinkhorn_solve(X, a, Y, b, eps=0.3, max_iters=500, marginal_tol=tol, ledger=led)
+    r = port.sinkhorn_solve(X, a, Y, b, eps=0.3, max_iters=500, marginal_tol=tol)
+    assert abs(s["iterations"] - r["iterations"]) <= 1
+    if s["iterations"] == r["iterations"]:
+        assert abs(s["marginal_violation"] - r["marginal_violation"]) <= \
+            1e-6 * r["marginal_violation"]
+        assert rel(s["f_hat"], r["f_hat"]) < 1e-10
+        assert abs(s["dual_cost"] - r["dual_cost"]) <= 1e-10 * abs(r["dual_cost"])
+    assert s["marginal_violation"] <= tol or s["iterations"] == 500
+    # ledger (closed forms, solver.cpp:36-66): every iteration at the final eps runs
+    # the reference's check (induced_marginals), plus dual_cost's marginals at the stop
+    # (or the final marginals + dual_cost when the cap is hit)
+    K = s["iterations"]
+    stopped = s["marginal_violation"] <= tol
+    expect = K * (fsk.io_count("f_update", n, m, d) + fsk.io_count("g_update", n, m, d)) + \
+        (K + (1 if stopped else 2)) * fsk.io_count("induced_marginals", n, m, d)
+    assert led.total_scalars() == expect

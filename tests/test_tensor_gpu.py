@@ -648,3 +648,72 @@ def test_hvp_plan_cache_matches_recomputed_scores(fsk, port):
     rel = np.linalg.norm(out["1"] - out["0"]) / np.linalg.norm(out["0"])
     print(f"plan cache vs recomputed: rel Frobenius {rel:.2e}")
     assert rel <= 1e-5
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+def test_warm_start_continues_the_solve(fsk, precision):
+    """f3: fsk_sinkhorn_solve_warm from the potentials of a 10-iteration solve, run
+    10 more iterations, is the 20-iteration solve (bit-identical in fp64: same
+    kernels, same inputs; single precision to rounding of the skip decisions)."""
+    rng = np.random.default_rng(5)
+    n, m, d = 3000, 2600, 64
+    X, Y = rng.normal(size=(n, d)), rng.normal(size=(m, d)) + 0.1
+    a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+    s10 = fsk.sinkhorn_solve(X, a, Y, b, eps=0.1, max_iters=10, precision=precision)
+    s20 = fsk.sinkhorn_solve(X, a, Y, b, eps=0.1, max_iters=20, precision=precision, grad=True)
+    w = fsk.sinkhorn_solve(X, a, Y, b, eps=0.1, max_iters=10, precision=precision, grad=True,
+                           f_init=s10["f_hat"], g_init=s10["g_hat"])
+    if precision == "double":
+        assert np.array_equal(w["f_hat"], s20["f_hat"]) and np.array_equal(w["g_hat"], s20["g_hat"])
+        assert w["dual_cost"] == s20["dual_cost"]
+    else:
+        assert contract(w["f_hat"], s20["f_hat"]) <= 1e-6
+        assert abs(w["dual_cost"] - s20["dual_cost"]) <= 1e-7 * abs(s20["dual_cost"])
+    assert np.abs(w["grad"] - s20["grad"]).max() <= 1e-5 * np.abs(s20["grad"]).max()
+    with pytest.raises(fsk.ValidationError):
+        fsk.sinkhorn_solve(X, a, Y, b, eps=0.1, max_iters=3, f_init=s10["f_hat"])
+
+
+def test_engine_warm_resolve_runs_no_screened_pass(fsk):
+    """f3 on the device engine: continuing a solve from its own potentials (a warm
+    re-solve) keeps every LSE pass on the warm bounds - zero screened cold passes -
+    while the cold start needed them."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(6)
+    n = m = 1 << 17
+    d = 64
+    X, Y = rng.normal(size=(n, d)), rng.normal(size=(m, d))
+    a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+    eng = fsk.Engine(0, X, a, Y, b)
+    eng.set_eps(0.05)
+    f = torch.empty(n, dtype=torch.float32, device="cuda")
+    g = torch.empty(m, dtype=torch.float32, device="cuda")
+    eng.bind(f.data_ptr(), g.data_ptr())
+    eng.init_potentials()
+    eng.iterate(10)
+    c0 = eng.pass_counts()
+    eng.iterate(10)   # warm re-solve: continue from the current potentials
+    c1 = eng.pass_counts()
+    torch.cuda.synchronize()
+    print(f"cold solve passes {c0}, warm re-solve adds "
+          f"{ {k: c1[k] - c0[k] for k in c1} }")
+    assert c0["screened"] >= 1
+    assert c1["screened"] == c0["screened"]
+    assert c1["warm"] - c0["warm"] >= 18
+    eng.close()
+
+
+@pytest.mark.parametrize("n,m", [(20000, 18000), (65536, 65536)])
+def test_run_to_run_bit_identical(fsk, n, m):
+    """SPEC.md:300 (bit-exact regardless of parallelism): two independent solves +
+    gradients of the same problem on the tensor path (screen / warm-bound decisions,
+    split partials, fixed-order violation reductions) return identical bits."""
+    rng = np.random.default_rng(n)
+    X, Y = rng.normal(size=(n, 64)), rng.normal(size=(m, 64))
+    a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+    outs = [fsk.sinkhorn_solve(X, a, Y, b, eps=0.05, max_iters=10, precision="single",
+                               grad=True) for _ in range(2)]
+    for key in ("f_hat", "g_hat", "grad"):
+        assert np.array_equal(outs[0][key], outs[1][key]), key
+    assert outs[0]["dual_cost"] == outs[1]["dual_cost"]
+    assert outs[0]["marginal_violation"] == outs[1]["marginal_violation"]
