@@ -128,12 +128,14 @@ class DenseOps:
     per-column transport (stream.cpp:182-186) would take hours. Pinned against the
     port in tests/test_oracle.py. Squared-Euclidean cost only."""
 
-    def __init__(self, fp32_scores: bool = False):
-        # fp32_scores: S_ij = <x_i, y_j (2/eps)> + (g_j + eps log b_j)/eps evaluated in
-        # fp32 as the reference's single-precision path does (make_ctx_f32,
-        # stream.cpp:421-434: float clouds, keys pre-scaled by 2/eps, float bias), the
-        # rest in fp64. The HVP computed on that plan measures what fp32-grade score
-        # arithmetic alone does to the result (the "e32" of the tensor-mode bounds).
+    def __init__(self, fp32_scores=False):
+        # fp32_scores="reference": S_ij evaluated in the reference's single-precision
+        # arithmetic and order (make_ctx_f32 stream.cpp:421-434 + score_tile
+        # stream.cpp:61-79 over float: keys x (2.0f/eps), bias (g + eps logf(w))/eps
+        # first, then += x_t * k_t sequentially in t, each product and sum rounded to
+        # fp32, no FMA), the rest in fp64. The HVP on that plan is what the reference's
+        # own fp32 arithmetic does to the result: the "e32" of the tensor-mode bounds.
+        # fp32_scores=True: the same in fp32 BLAS order (sgemm), a milder variant.
         self.fp32_scores = fp32_scores
 
     def _plan(self, X, a, Y, b, f_hat, g_hat, eps):
@@ -141,7 +143,21 @@ class DenseOps:
         Y = np.asarray(Y, dtype=np.float64)
         key = (id(X), id(Y), id(f_hat), id(g_hat), float(eps))
         if getattr(self, "_key", None) != key:
-            if self.fp32_scores:
+            if self.fp32_scores == "reference":
+                e32 = np.float32(eps)
+                k32 = Y.astype(np.float32) * (np.float32(2.0) / e32)
+                bias32 = (np.asarray(g_hat).astype(np.float32) +
+                          e32 * np.log(np.asarray(b).astype(np.float32))) / e32
+                S32 = np.empty((X.shape[0], Y.shape[0]), dtype=np.float32)
+                S32[:] = bias32[None, :]
+                X32 = X.astype(np.float32)
+                prod = np.empty_like(S32)
+                for t in range(X.shape[1]):
+                    np.multiply.outer(X32[:, t], k32[:, t], out=prod)
+                    S32 += prod
+                S = S32.astype(np.float64)
+                S += (np.asarray(f_hat, dtype=np.float64) / eps + np.log(a))[:, None]
+            elif self.fp32_scores:
                 k32 = Y.astype(np.float32) * np.float32(2.0 / eps)
                 bias32 = ((np.asarray(g_hat).astype(np.float32) +
                            np.float32(eps) * np.log(np.asarray(b).astype(np.float32))) /

@@ -16,6 +16,7 @@
 #include "core_kernels.h"
 #include "device_ops.h"
 #include "hostlib.h"
+#include "small_solve.h"
 #include "tc_engine.h"
 
 namespace fskb {
@@ -300,7 +301,46 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
         r_dev.alloc(size_t(n), C.s);
         viol_dev.alloc(1, C.s);
     }
+    bool persistent_done = false;
+    if constexpr (kSingle) {
+        // small fp32 CUDA-core problems: the whole alternating loop (the f32 path has no
+        // early stop, solver.cpp:87-108) is one persistent kernel (small_solve.cu)
+        const char* penv = std::getenv("FSK_PERSIST");
+        if (!P.tc && !P.labeled && cfg.schedule == 0 && !schedule.empty() &&
+            !(penv && penv[0] == '0') && small_solve_fits(n, m, d)) {
+            const std::vector<float> es(schedule.begin(), schedule.end());
+            DevBuf<float> es_d(es.size(), C.s);
+            FSKB_CUDA(cudaMemcpyAsync(es_d.get(), es.data(), es.size() * sizeof(float),
+                                      cudaMemcpyHostToDevice, C.s));
+            SmallSolveParams sp{};
+            sp.X = P.src.pts.get();
+            sp.Y = P.tgt.pts.get();
+            sp.logw_x = P.src.logw.get();
+            sp.logw_y = P.tgt.logw.get();
+            sp.f = f.get();
+            sp.g = g.get();
+            sp.eps_sched = es_d.get();
+            sp.iters = int(es.size());
+            sp.n = n;
+            sp.m = m;
+            sp.d = int(d);
+            sp.fscale = float(P.fscale);
+            sp.flags = C.flags;
+            sp.bad_iter = C.bad_iter;
+            launch_small_solve(sp, C.s);
+            FSKB_CUDA(cudaStreamSynchronize(C.s));
+            for (double eps_d : schedule) {
+                ledger_update_f32(ledger, n, m, d, tiles.block_rows, tiles.block_cols);
+                ledger_update_f32(ledger, m, n, d, tiles.block_cols, tiles.block_rows);
+                hist.push_back(eps_d);
+                final_eps = eps_d;
+                ++iters;
+            }
+            persistent_done = true;
+        }
+    }
     for (double eps_d : schedule) {
+        if (persistent_done) break;
         const T eps = T(eps_d);
         final_eps = eps_d;
         if constexpr (kSingle) {

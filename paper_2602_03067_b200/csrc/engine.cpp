@@ -13,6 +13,7 @@
 #include "core_kernels.h"
 #include "device_ops.h"
 #include "hostlib.h"
+#include "small_solve.h"
 #include "tc_engine.h"
 
 namespace fskb {
@@ -43,6 +44,8 @@ struct fsk_engine {
     cudaEvent_t fence = nullptr;
     cudaStream_t last = nullptr;
     bool fenced = false;
+    DevBuf<float> eps_sched;   // persistent small-problem loop: eps per iteration
+    double eps_sched_val = 0.0;
 };
 
 namespace {
@@ -127,6 +130,7 @@ void fsk_engine_destroy(fsk_engine* e) {
         e->P.tc.reset();
         e->P.src = DevSide<float>();
         e->P.tgt = DevSide<float>();
+        e->eps_sched.release();
     }
     cudaDeviceSynchronize();
     cudaFree(e->flags);
@@ -212,6 +216,36 @@ int fsk_engine_iterate(fsk_engine* e, int iters, void* stream) {
                 half_step_rows<float>(e->P, 1, e->f, eps, fa, 0, e->P.tgt.n);
             }
         };
+        // small CUDA-core problems (keys fit in shared memory, d <= 16): the whole
+        // loop is one persistent cooperative kernel (small_solve.cu)
+        const char* penv = std::getenv("FSK_PERSIST");
+        if (!e->P.tc && !e->P.labeled && !(penv && penv[0] == '0') &&
+            small_solve_fits(e->P.src.n, e->P.tgt.n, e->P.src.d)) {
+            if (e->eps_sched.size() < size_t(iters) || e->eps_sched_val != e->eps) {
+                const std::vector<float> h(size_t(iters), float(e->eps));
+                e->eps_sched.alloc(size_t(iters), s);
+                FSKB_CUDA(cudaMemcpyAsync(e->eps_sched.get(), h.data(), h.size() * sizeof(float),
+                                          cudaMemcpyHostToDevice, s));
+                FSKB_CUDA(cudaStreamSynchronize(s));
+                e->eps_sched_val = e->eps;
+            }
+            SmallSolveParams sp{};
+            sp.X = e->P.src.pts.get();
+            sp.Y = e->P.tgt.pts.get();
+            sp.logw_x = e->P.src.logw.get();
+            sp.logw_y = e->P.tgt.logw.get();
+            sp.f = e->f;
+            sp.g = e->g;
+            sp.eps_sched = e->eps_sched.get();
+            sp.iters = iters;
+            sp.n = e->P.src.n;
+            sp.m = e->P.tgt.n;
+            sp.d = int(e->P.src.d);
+            sp.fscale = float(e->P.fscale);
+            sp.flags = e->flags;
+            launch_small_solve(sp, s);
+            return;
+        }
         // the tensor path decides screening per pass on the host: run it eagerly;
         // the CUDA-core path (small / low-d problems, launch-bound) replays a graph
         const char* env = std::getenv("FSK_GRAPH");

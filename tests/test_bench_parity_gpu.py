@@ -142,9 +142,10 @@ def test_cfg4_single_precision_hvp_against_oracle(fsk, plan_cache):
     same fixed K_CG = 50 (cg_tol 1e-30, the bench setting), tau = 1e-5.
     Bound (stated tensor-mode HVP bound, like the gradient's): relative Frobenius
     error <= max(1e-5, 2 e32), e32 = the error of the same composition on the plan
-    whose scores are evaluated in the reference's fp32 arithmetic (DenseOps
-    fp32_scores). At d = 1024, eps = 0.1 the scores reach ~2e3 nats, so fp32-grade
-    score arithmetic alone moves plan entries by ~1e-4 relative."""
+    whose scores are evaluated in the reference's own fp32 arithmetic and order
+    (DenseOps fp32_scores="reference", stream.cpp:61-79 / :421-434). At d = 1024,
+    eps = 0.1 the score terms reach ~1.4e4 log2 units and cancel to a few hundred, so
+    fp32 arithmetic alone moves plan entries by ~1e-3 relative."""
     from oracle import compose
     from oracle.dense import DenseOps
     bench = _bench()
@@ -163,7 +164,7 @@ def test_cfg4_single_precision_hvp_against_oracle(fsk, plan_cache):
         os.environ.pop("FSK_PLAN_CACHE", None)
     ws = compose.Workspace(DenseOps(), X, a, Y, b, f, g, eps)
     H64, it64, _ = compose.hvp_apply(ws, A, tau=1e-5, tol=1e-30, max_iters=50)
-    ws32 = compose.Workspace(DenseOps(fp32_scores=True), X, a, Y, b, f, g, eps)
+    ws32 = compose.Workspace(DenseOps(fp32_scores="reference"), X, a, Y, b, f, g, eps)
     H32 = compose.hvp_apply(ws32, A, tau=1e-5, tol=1e-30, max_iters=50)[0]
     rel = np.linalg.norm(H - H64) / np.linalg.norm(H64)
     e32 = np.linalg.norm(H32 - H64) / np.linalg.norm(H64)

@@ -198,3 +198,21 @@ def test_dense_ops_match_port_stream_ops(port):
     H1 = compose.hvp_apply(compose.Workspace(port, X, a, Y, b, f, g, eps), A, max_iters=40)[0]
     H2 = compose.hvp_apply(compose.Workspace(D, X, a, Y, b, f, g, eps), A, max_iters=40)[0]
     assert np.linalg.norm(H1 - H2) <= 1e-9 * np.linalg.norm(H1)
+
+
+def test_dense_ops_reference_fp32_scores_match_port_f32_half_step(port):
+    """DenseOps(fp32_scores="reference") forms the scores in the reference's fp32
+    order (stream.cpp:61-79, :421-434): the fp64 LSE over those scores reproduces
+    the port's update_f_hat_f32 up to its fp32 LSE accumulation."""
+    from oracle.dense import DenseOps
+    rng = np.random.default_rng(3)
+    n, m, d, eps = 64, 70, 33, 0.3
+    X, Y = rng.standard_normal((n, d)), rng.standard_normal((m, d))
+    b = np.full(m, 1.0 / m)
+    g = -(Y ** 2).sum(1)
+    P = DenseOps("reference")._plan(X, np.ones(n), Y, b, np.zeros(n), g, eps)
+    f = -eps * np.log(P.sum(1))
+    f32 = port.update_f_hat_f32(X.astype(np.float32), np.full(n, 1 / n, np.float32),
+                                Y.astype(np.float32), b.astype(np.float32),
+                                g.astype(np.float32), eps)
+    assert np.abs(f - f32).max() <= 4e-7 * np.abs(f32).max()

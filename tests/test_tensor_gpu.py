@@ -512,7 +512,16 @@ def test_tensor_transport_hadamard_parity(fsk, port, n, m, d, p):
     eng.close()
 
 
-def test_engine_iterate_graph_matches_loop(fsk):
+@pytest.fixture()
+def graph_path():
+    """fsk_engine_iterate on the CUDA graph of per-half-step launches (the persistent
+    small-problem kernel disabled)."""
+    os.environ["FSK_PERSIST"] = "0"
+    yield
+    os.environ.pop("FSK_PERSIST", None)
+
+
+def test_engine_iterate_graph_matches_loop(fsk, graph_path):
     """fsk_engine_iterate (CUDA graph on the CUDA-core path) reproduces the per-call
     half-step loop bit for bit, on first capture and on replay."""
     torch = pytest.importorskip("torch")
@@ -543,7 +552,7 @@ def test_engine_iterate_graph_matches_loop(fsk):
         assert np.array_equal(fr, res[0][0]) and np.array_equal(gr, res[0][1])
 
 
-def test_engine_iterate_graph_follows_eps_and_rebinding(fsk):
+def test_engine_iterate_graph_follows_eps_and_rebinding(fsk, graph_path):
     """An eps-annealing loop (set_eps(e_k); iterate(k)) and a rebinding of g must not
     replay a graph captured for the old eps / old buffer: every iterate() equals the
     per-call half-step loop at the current eps and buffers."""
@@ -717,3 +726,46 @@ def test_run_to_run_bit_identical(fsk, n, m):
         assert np.array_equal(outs[0][key], outs[1][key]), key
     assert outs[0]["dual_cost"] == outs[1]["dual_cost"]
     assert outs[0]["marginal_violation"] == outs[1]["marginal_violation"]
+
+
+def test_persistent_small_solve(fsk, port, golden):
+    """cfg1-class problems (keys fit in shared memory, d <= 16): the whole iteration
+    loop is one cooperative kernel (small_solve.cu). Engine iterate and the drop-in
+    single-precision solve against the fp64 oracle / the reference golden cfg1
+    (fp32 contract), eps changes and rebinding honoured, and the same iterate as
+    the per-launch path to fp32 rounding."""
+    torch = pytest.importorskip("torch")
+    G = golden
+    X, Y = G["cfg1_X"], G["cfg1_Y"]
+    n, m = len(X), len(Y)
+    u = np.full(n, 1.0 / n)
+    s = fsk.sinkhorn_solve(X, u, Y, u, eps=0.1, max_iters=100, precision="single", grad=True)
+    assert contract(s["f_hat"], G["cfg1_f"]) <= 1e-5
+    assert abs(s["dual_cost"] - G["cfg1_s"][2]) <= 1e-5 * abs(G["cfg1_s"][2])
+    eng = fsk.Engine(0, X, u, Y, u, mode="fma")
+    f = torch.empty(n, dtype=torch.float32, device="cuda")
+    g = torch.empty(m, dtype=torch.float32, device="cuda")
+    eng.bind(f.data_ptr(), g.data_ptr())
+    ref_f, ref_g = -(X ** 2).sum(1), -(Y ** 2).sum(1)
+    eng.init_potentials()
+    for eps, its in ((0.5, 4), (0.1, 6)):
+        eng.set_eps(eps)
+        eng.iterate(its)
+        for _ in range(its):
+            ref_f = port.update_f_hat(X, u, Y, u, ref_g, eps)
+            ref_g = port.update_g_hat(X, u, Y, u, ref_f, eps)
+        torch.cuda.synchronize()
+        assert contract(f.cpu().numpy(), ref_f) <= 1e-5
+        assert contract(g.cpu().numpy(), ref_g) <= 1e-5
+    # the per-launch path from the same state agrees to fp32 rounding
+    f2, g2 = f.clone(), g.clone()
+    eng.iterate(5)
+    eng.bind(f2.data_ptr(), g2.data_ptr())
+    os.environ["FSK_PERSIST"] = "0"
+    try:
+        eng.iterate(5)
+    finally:
+        os.environ.pop("FSK_PERSIST", None)
+    torch.cuda.synchronize()
+    assert contract(f2.cpu().numpy(), f.cpu().numpy().astype(np.float64)) <= 1e-6
+    eng.close()
