@@ -268,8 +268,9 @@ int fsk_hvp_apply_single(const fsk_measure* src, const fsk_measure* tgt, const d
  * (float, length n / m) so a collective library can all-gather them in place. */
 typedef struct fsk_engine fsk_engine;
 
-/* mode: 0 = auto (split-fp16 tensor cores when d >= 32, up to d = 4096; CUDA-core
- *       FMA below d = 32),
+/* mode: 0 = auto (split-fp16 tensor cores for 1 <= d <= 4096, except small d < 32
+ *       problems whose keys fit in shared memory, which run the persistent CUDA-core
+ *       loop; measured in profiles/r02_dsweep.md),
  *       1 = force CUDA-core FMA fp32, 2 = force tensor (split-fp16). */
 int fsk_engine_create(int device, const double* X, const double* a, int64_t n, const double* Y,
                       const double* b, int64_t m, int64_t d, int mode, fsk_engine** out);

@@ -508,6 +508,21 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
                 done = true;
             }
         }
+        if constexpr (kSingle) {
+            if (!done) {
+                // CUDA-core fp32 problem: the gradient pass in fp64 (grad_rows_fp64)
+                DevBuf<double> G64(size_t(n * d), C.s);
+                grad_rows_fp64(P, f.get(), g.get(), pot_eps, 0, n, G64.get(), C.flags, C.s);
+                G64.download(grad_out, size_t(n * d));
+                done = true;
+                sync_and_check(C);
+                if (ledger) {
+                    ledger_marginals(ledger, n, m, d, tiles, cost);
+                    ledger_apply(ledger, n, m, d, d, tiles, cost, false);
+                }
+                return;
+            }
+        }
         if (!done) {
             if (stopped) {
                 FinalizeArgs<T> fa{};

@@ -315,6 +315,47 @@ void transport(DevProblem<T>& P, int side, const T* kpot, const T* pot, T eps, c
 
 template struct DevProblem<float>;
 template struct DevProblem<double>;
+void grad_rows_fp64(const DevProblem<float>& P, const float* f, const float* g, double eps,
+                    int64_t row_begin, int64_t row_end, double* out_dev, int* flags,
+                    cudaStream_t s) {
+    const int64_t n = P.src.n, m = P.tgt.n, d = P.src.d, R = row_end - row_begin;
+    if (R <= 0) return;
+    DevProblem<double> Pd;
+    Pd.s = s;
+    Pd.fscale = P.fscale;
+    auto widen = [&](DevSide<double>& o, const DevSide<float>& i) {
+        o.n = i.n;
+        o.d = i.d;
+        o.pts.alloc(size_t(i.n * i.d), s);
+        o.w.alloc(size_t(i.n), s);
+        o.logw.alloc(size_t(i.n), s);
+        launch_f32_to_f64(i.pts.get(), o.pts.get(), i.n * i.d, s);
+        launch_f32_to_f64(i.w.get(), o.w.get(), i.n, s);
+        launch_log<double>(o.w.get(), o.logw.get(), i.n, s);
+    };
+    widen(Pd.src, P.src);
+    widen(Pd.tgt, P.tgt);
+    DevBuf<double> fd(size_t(n), s), gd(size_t(m), s), lse(size_t(n), s), mx(size_t(n), s);
+    launch_f32_to_f64(f, fd.get(), n, s);
+    launch_f32_to_f64(g, gd.get(), m, s);
+    FinalizeArgs<double> fa{};
+    fa.eps = eps;
+    fa.flags = flags;
+    fa.out_lse = lse.get();
+    fa.out_max = mx.get();
+    half_step_rows<double>(Pd, 0, gd.get(), eps, fa, row_begin, row_end);
+    ScoreParams<double> sp = Pd.params(0, gd.get(), eps);
+    sp.Q += row_begin * d;
+    sp.R = R;
+    DevBuf<double> O(size_t(R * d), s);
+    launch_apply<double>(sp, lse.get() + row_begin, Pd.tgt.pts.get(), d, nullptr, nullptr, 0,
+                         O.get(), s);
+    launch_grad_epilogue<double>(Pd.src.pts.get() + row_begin * d, O.get(),
+                                 Pd.src.w.get() + row_begin, fd.get() + row_begin,
+                                 lse.get() + row_begin, R, d, eps, out_dev, flags, s);
+    FSKB_CUDA(cudaStreamSynchronize(s));
+}
+
 template void half_step<float>(DevProblem<float>&, int, const float*, float,
                                const FinalizeArgs<float>&);
 template void half_step<double>(DevProblem<double>&, int, const double*, double,

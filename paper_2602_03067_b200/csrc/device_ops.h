@@ -85,6 +85,14 @@ void transport(DevProblem<T>& P, int side, const T* kpot, const T* pot, T eps, c
                const T* mx, const T* V, int64_t p, const T* A, const T* B, int64_t r, T* out,
                int* flags);
 
+// CUDA-core fp32 problems: gradient rows [row_begin, row_end) of G = 2 (diag(r) X -
+// P Y) evaluated in fp64 (scores, LSE, transport) from the float clouds and
+// potentials; out_dev is (row_end - row_begin) x d doubles. fp32 score arithmetic
+// alone moves plan entries by |S| 2^-24 (~1e-5 at cfg1), above the gradient contract.
+void grad_rows_fp64(const DevProblem<float>& P, const float* f, const float* g, double eps,
+                    int64_t row_begin, int64_t row_end, double* out_dev, int* flags,
+                    cudaStream_t s);
+
 // Enables the tcgen05 path for a float problem when the shape allows it.
 // mode: 0 auto, 1 force FMA, 2 force tensor. Returns true when enabled.
 bool enable_tensor_path(DevProblem<float>& P, int mode);

@@ -298,20 +298,11 @@ int fsk_engine_grad(fsk_engine* e, int64_t row_begin, int64_t row_end, float* gr
             e->P.tc->grad(e->P, 0, e->g, e->f, eps, row_begin, row_end, grad_dev, e->flags);
             return;
         }
-        DevBuf<float> lse(size_t(n), s), O(size_t(R * d), s);
-        FinalizeArgs<float> fa{};
-        fa.eps = eps;
-        fa.flags = e->flags;
-        fa.out_lse = lse.get();
-        half_step_rows<float>(e->P, 0, e->g, eps, fa, row_begin, row_end);
-        ScoreParams<float> sp = e->P.params(0, e->g, eps);
-        sp.Q += row_begin * d;
-        sp.R = R;
-        launch_apply<float>(sp, lse.get() + row_begin, e->P.tgt.pts.get(), d, nullptr, nullptr, 0,
-                            O.get(), s);
-        launch_grad_epilogue<float>(e->P.src.pts.get() + row_begin * d, O.get(),
-                                    e->P.src.w.get() + row_begin, e->f + row_begin,
-                                    lse.get() + row_begin, R, d, eps, grad_dev, e->flags, s);
+        // CUDA-core path: the gradient pass in fp64 (grad_rows_fp64)
+        (void)eps;
+        DevBuf<double> G64(size_t(R * d), s);
+        grad_rows_fp64(e->P, e->f, e->g, e->eps, row_begin, row_end, G64.get(), e->flags, s);
+        launch_f64_to_f32(G64.get(), grad_dev, R * d, s);
     });
 }
 

@@ -6,13 +6,14 @@
 // gaps. Here every half-step is
 //   stage:  all keys of the side (pre-scaled by 2/eps, SoA) + their bias
 //           (pot_j + eps log w_j)/eps into shared memory (<= 192 KB)
-//   rows:   one warp per query row, lanes stride the keys; pass 1 row max,
-//           pass 2 sum of exp(s - max) (one exp per score, no online rescale),
-//           warp reductions; f_i = -eps (max + log sum)
+//   rows:   one warp per query row (32 warps per CTA), lanes stride groups of 4
+//           keys (float4 shared loads), online (max, sum) in log2 units with one
+//           rescale per group at most and one ex2 per score, warp reduction;
+//           f_i = -eps ln2 (max + log2 sum)
 //   sync:   grid-wide barrier, then the other side reads the new potential.
-// Scores are formed exactly as the FP32 tile kernel does (fma over features in
-// order, then + bias), so the result differs from the per-launch path only in
-// the LSE summation order (fp32 contract of SURVEY §8d).
+// Scores are formed as the FP32 tile kernel does (fma over features in order onto
+// the bias), with keys and bias pre-scaled to log2 units at staging, so the
+// result differs from the per-launch path at fp32 rounding (contract of SURVEY §8d).
 #include <cooperative_groups.h>
 
 #include "common.h"
@@ -23,15 +24,22 @@ namespace cg = cooperative_groups;
 namespace fskb {
 namespace {
 
-constexpr int kWarps = 8;
+constexpr int kWarps = 32;
 constexpr int kThreads = 32 * kWarps;
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1) small_solve_kernel(const SmallSolveParams p) {
     extern __shared__ __align__(16) float sm[];
     cg::grid_group grid = cg::this_grid();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t cpad = p.cpad;
+    const int64_t cpad = p.cpad;   // multiple of 128: every lane's float4 group is in range
+    constexpr float kLog2e = 1.4426950408889634f;
     for (int it = 0; it < p.iters; ++it) {
         const float eps = p.eps_sched[it];
         const float kscale = 2.0f * p.fscale / eps;
@@ -43,40 +51,62 @@ __global__ void __launch_bounds__(kThreads, 1) small_solve_kernel(const SmallSol
             float* out = side == 0 ? p.f : p.g;
             const int64_t R = side == 0 ? p.n : p.m;
             const int64_t C = side == 0 ? p.m : p.n;
-            // stage the keys (SoA, x 2/eps) and their bias
-            for (int64_t j = threadIdx.x; j < C; j += kThreads) {
+            // stage the keys (SoA, x 2 s / eps, in log2 units) and their bias; padded
+            // keys get a -inf bias
+            for (int64_t j = threadIdx.x; j < cpad; j += kThreads) {
+                if (j < C) {
 #pragma unroll
-                for (int t = 0; t < D; ++t) sm[t * cpad + j] = K[j * D + t] * kscale;
-                sm[D * cpad + j] = (kpot[j] + eps * klogw[j]) / eps;
+                    for (int t = 0; t < D; ++t)
+                        sm[t * cpad + j] = (K[j * D + t] * kscale) * kLog2e;
+                    sm[D * cpad + j] = ((kpot[j] + eps * klogw[j]) / eps) * kLog2e;
+                } else {
+#pragma unroll
+                    for (int t = 0; t < D; ++t) sm[t * cpad + j] = 0.0f;
+                    sm[D * cpad + j] = -INFINITY;
+                }
             }
             __syncthreads();
+            const float4* s4 = reinterpret_cast<const float4*>(sm);
+            const int64_t c4 = cpad / 4;
             for (int64_t r = int64_t(blockIdx.x) * kWarps + warp; r < R;
                  r += int64_t(gridDim.x) * kWarps) {
                 float q[D];
 #pragma unroll
                 for (int t = 0; t < D; ++t) q[t] = Q[r * D + t];
-                float mx = -INFINITY;
-                for (int64_t j = lane; j < C; j += 32) {
-                    float acc = 0.0f;
+                // online (max, sum) per lane over groups of 4 keys: one rescale per
+                // group at most, one ex2 per score
+                float mx = -INFINITY, sum = 0.0f;
+                for (int64_t g = lane; g < c4; g += 32) {
+                    float4 acc = s4[D * c4 + g];
 #pragma unroll
-                    for (int t = 0; t < D; ++t) acc = fmaf(q[t], sm[t * cpad + j], acc);
-                    mx = fmaxf(mx, acc + sm[D * cpad + j]);
+                    for (int t = 0; t < D; ++t) {
+                        const float4 k = s4[t * c4 + g];
+                        acc.x = fmaf(q[t], k.x, acc.x);
+                        acc.y = fmaf(q[t], k.y, acc.y);
+                        acc.z = fmaf(q[t], k.z, acc.z);
+                        acc.w = fmaf(q[t], k.w, acc.w);
+                    }
+                    const float gm = fmaxf(fmaxf(acc.x, acc.y), fmaxf(acc.z, acc.w));
+                    if (gm > mx) {
+                        sum *= ex2(mx - gm);
+                        mx = gm;
+                    }
+                    if (mx > -INFINITY)   // (a lane whose groups are all padding stays empty)
+                        sum += ex2(acc.x - mx) + ex2(acc.y - mx) + ex2(acc.z - mx) +
+                               ex2(acc.w - mx);
                 }
 #pragma unroll
-                for (int off = 16; off >= 1; off >>= 1)
-                    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-                float sum = 0.0f;
-                for (int64_t j = lane; j < C; j += 32) {
-                    float acc = 0.0f;
-#pragma unroll
-                    for (int t = 0; t < D; ++t) acc = fmaf(q[t], sm[t * cpad + j], acc);
-                    sum += __expf(acc + sm[D * cpad + j] - mx);
+                for (int off = 16; off >= 1; off >>= 1) {
+                    const float mo = __shfl_xor_sync(0xffffffffu, mx, off);
+                    const float so = __shfl_xor_sync(0xffffffffu, sum, off);
+                    const float M = fmaxf(mx, mo);
+                    sum = (mx > -INFINITY ? sum * ex2(mx - M) : 0.0f) +
+                          (mo > -INFINITY ? so * ex2(mo - M) : 0.0f);
+                    mx = M;
                 }
-#pragma unroll
-                for (int off = 16; off >= 1; off >>= 1)
-                    sum += __shfl_xor_sync(0xffffffffu, sum, off);
                 if (lane == 0) {
-                    const float pot = -eps * (mx + logf(sum));
+                    // f = -eps ln 2 (max + log2 sum)
+                    const float pot = -eps * 0.6931471805599453f * (mx + __log2f(sum));
                     if (!isfinite(pot)) {
                         atomicOr(p.flags, kFlagNonFinitePotential);
                         if (p.bad_iter) atomicMin(p.bad_iter, p.iter0 + it + 1);
@@ -110,7 +140,7 @@ void launch_d(const SmallSolveParams& p, int grid, size_t smem, cudaStream_t s) 
 bool small_solve_fits(int64_t n, int64_t m, int64_t d) {
     if (d < 1 || d > kSmallSolveMaxD || n < 1 || m < 1) return false;
     const int64_t cmax = n > m ? n : m;
-    const int64_t cpad = (cmax + 3) / 4 * 4;
+    const int64_t cpad = (cmax + 127) / 128 * 128;
     return size_t(cpad) * size_t(d + 1) * sizeof(float) <= kSmallSolveSmem;
 }
 
@@ -118,7 +148,7 @@ void launch_small_solve(const SmallSolveParams& p0, cudaStream_t s) {
     if (p0.iters < 1) return;
     SmallSolveParams p = p0;
     const int64_t cmax = p.n > p.m ? p.n : p.m;
-    p.cpad = (cmax + 3) / 4 * 4;
+    p.cpad = (cmax + 127) / 128 * 128;
     const size_t smem = size_t(p.cpad) * size_t(p.d + 1) * sizeof(float);
     // one CTA per SM (co-residency is what the grid barrier needs)
     const int grid = num_sms();

@@ -39,6 +39,7 @@
 #include "common.h"
 #include "device_ops.h"
 #include "tc_engine.h"
+#include "small_solve.h"
 #include "tc_ptx.h"
 
 namespace fskb {
@@ -2911,9 +2912,16 @@ bool enable_tensor_path(DevProblem<float>& P, int mode) {
     const int64_t d = P.src.d;
     const bool shape_ok = TcHalfStep::supported(d);
     if (mode == 2 && !shape_ok) throw ValidationFailure("tensor path supports 1 <= d <= 4096");
-    // auto: the contraction is a real GEMM only from d >= 32 (north star: small-d
-    // point clouds stay on CUDA-core FMA)
-    if (mode == 0 && !(shape_ok && d >= 32)) return false;
+    // auto (N2, measured: profiles/r02_dsweep.md): on large problems the tcgen05
+    // kernel wins at EVERY d - a dense half-step at n = m = 65536 is 1.8 vs 9.4 ms at
+    // d = 3 and 1.55 vs 23 ms at d = 64 - because the bound is the exp / online-LSE
+    // epilogue, not the contraction: the CUDA-core kernel is issue-bound (72% issue
+    // slots, XU 17%) where the tensor kernel's epilogue runs ex2 on MUFU + FMA (XU
+    // 49%). Small low-d problems whose keys fit in shared memory (cfg1) are launch-
+    // bound instead: they stay on the CUDA cores, where the whole loop is one
+    // persistent kernel (small_solve.cu).
+    if (mode == 0 && (!shape_ok || (d < 32 && small_solve_fits(P.src.n, P.tgt.n, d))))
+        return false;
     P.tc = std::make_shared<TcHalfStep>(P);
     return true;
 }

@@ -43,13 +43,16 @@ def main() -> int:
             for side, rows_ in ((0, n), (1, m)):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 l0, b0 = eng.live_tiles(), eng.screened_blocks()
+                c0 = eng.pass_counts()
                 e0.record(stream)
                 eng.half_step(side, 0, rows_, 0, sp)
                 e1.record(stream)
                 torch.cuda.synchronize()
                 l1, b1 = eng.live_tiles(), eng.screened_blocks()
+                c1 = eng.pass_counts()
+                kind = [k for k in c1 if c1[k] != c0[k]]
                 rows.append((it, side, e0.elapsed_time(e1), (l1 - l0) / max(1, b1 - b0),
-                             eng.live_set_fraction(side)))
+                             eng.live_set_fraction(side), kind[0] if kind else "?"))
         G = torch.empty((n, d), dtype=torch.float32, device="cuda")
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -58,8 +61,9 @@ def main() -> int:
         torch.cuda.synchronize()
         tot = sum(r[2] for r in rows)
         print(f"rep {rep}: half-steps {tot:.1f} ms, grad {e0.elapsed_time(e1):.1f} ms")
-        for it, side, ms, lf, lset in rows:
-            print(f"  it {it:2d} side {side} {ms:8.2f} ms  probe-live {lf:.3f}  live-set {lset:.3f}")
+        for it, side, ms, lf, lset, kind in rows:
+            print(f"  it {it:2d} side {side} {kind:8s} {ms:8.2f} ms  probe-live {lf:.3f}  "
+                  f"live-set {lset:.3f}")
     eng.close()
     return 0
 
