@@ -325,6 +325,25 @@ double fsk_engine_live_set_fraction(const fsk_engine* e, int side);
 /* (query tile, key tile) blocks covered by those tracked passes. */
 uint64_t fsk_engine_screen_blocks(const fsk_engine* e);
 /* Launch counter of this engine's kernels (for bench accounting). */
+/* Fixed-potential transport over row shards (the HVP workspace, SPEC.md:442-446;
+ * the multi-GPU HVP of SURVEY §8e). prepare runs the LSE pass of each orientation
+ * over rows [f_begin, f_end) of X and [g_begin, g_end) of Y at the bound potentials
+ * and eps (tensor path: shards start on 256-row boundaries) and keeps the row
+ * LSE, max and induced marginal; it stays valid until the potentials / eps change.
+ *   marginal:         out (float, n or m) = r (side 0) / c (side 1), prepared rows
+ *   transport_vec_rows:  out (double, rows) = rows [b, e) of P v (side 0, v: m) or
+ *                        P^T v (side 1, v: n)
+ *   transport_mat_rows:  out (float, rows x p) = rows of P V / P^T V (V: key rows x p);
+ *                        a_dev (n x d, side 0 only): the Hadamard form (P (.) A Y^T) V */
+int fsk_engine_transport_prepare(fsk_engine* e, int64_t f_begin, int64_t f_end, int64_t g_begin,
+                                 int64_t g_end, void* stream);
+int fsk_engine_marginal(fsk_engine* e, int side, float* out_dev, void* stream);
+int fsk_engine_transport_vec_rows(fsk_engine* e, int side, int64_t row_begin, int64_t row_end,
+                                  const float* v_dev, double* out_dev, void* stream);
+int fsk_engine_transport_mat_rows(fsk_engine* e, int side, int64_t row_begin, int64_t row_end,
+                                  const float* v_dev, int64_t p, const float* a_dev,
+                                  float* out_dev, void* stream);
+
 /* LSE passes the tensor path ran so far, by kind: out[0] screened cold passes
  * (5-MMA phase 1 + live blocks), out[1] warm-bound passes, out[2] plain passes. */
 void fsk_engine_pass_counts(const fsk_engine* e, uint64_t out[3]);

@@ -480,6 +480,11 @@ def version() -> str:
 
 # ---- device engine ------------------------------------------------------------------
 
+def _dp(x) -> int:
+    """Device pointer of a torch tensor, or the int itself."""
+    return x.data_ptr() if hasattr(x, "data_ptr") else int(x)
+
+
 class Engine:
     """Device-resident problem (fsk_engine_*). Potentials are caller-owned float32
     device buffers (e.g. torch tensors) so a collective library can all-gather them
@@ -573,6 +578,33 @@ class Engine:
         _check(lib().fsk_engine_transport_hadamard(self.h, C.c_void_p(a_ptr), C.c_void_p(v_ptr),
                                                    C.c_int64(p), C.c_void_p(out_ptr),
                                                    C.c_void_p(stream)))
+
+    def transport_prepare(self, f_rows, g_rows, stream: int = 0):
+        """LSE / marginals of both orientations over row shards at the bound potentials
+        (fsk_engine_transport_prepare); f_rows, g_rows = (begin, end)."""
+        _check(lib().fsk_engine_transport_prepare(self.h, C.c_int64(f_rows[0]),
+                                                  C.c_int64(f_rows[1]), C.c_int64(g_rows[0]),
+                                                  C.c_int64(g_rows[1]), C.c_void_p(stream)))
+
+    def marginal(self, side: int, out_ptr: int, stream: int = 0):
+        _check(lib().fsk_engine_marginal(self.h, C.c_int(side), C.c_void_p(_dp(out_ptr)),
+                                         C.c_void_p(stream)))
+
+    def transport_vec_rows(self, side: int, lo: int, hi: int, v_ptr: int, out_ptr: int,
+                           stream: int = 0):
+        _check(lib().fsk_engine_transport_vec_rows(self.h, C.c_int(side), C.c_int64(lo),
+                                                   C.c_int64(hi), C.c_void_p(_dp(v_ptr)),
+                                                   C.c_void_p(_dp(out_ptr)), C.c_void_p(stream)))
+
+    def transport_mat_rows(self, side: int, lo: int, hi: int, v_ptr, p: int, out_ptr,
+                           a_ptr=None, stream: int = 0):
+        _check(lib().fsk_engine_transport_mat_rows(self.h, C.c_int(side), C.c_int64(lo),
+                                                   C.c_int64(hi), C.c_void_p(_dp(v_ptr)),
+                                                   C.c_int64(p),
+                                                   C.c_void_p(_dp(a_ptr)) if a_ptr is not None
+                                                   and not (isinstance(a_ptr, int) and a_ptr == 0)
+                                                   else None,
+                                                   C.c_void_p(_dp(out_ptr)), C.c_void_p(stream)))
 
     def grad(self, row_begin: int, row_end: int, grad_ptr: int, stream: int = 0):
         _check(lib().fsk_engine_grad(self.h, C.c_int64(row_begin), C.c_int64(row_end),

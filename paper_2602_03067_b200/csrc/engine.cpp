@@ -46,6 +46,16 @@ struct fsk_engine {
     bool fenced = false;
     DevBuf<float> eps_sched;   // persistent small-problem loop: eps per iteration
     double eps_sched_val = 0.0;
+    // fixed-potential transport state over row shards (fsk_engine_transport_prepare):
+    // the HVP workspace of SPEC.md:442-446, per orientation
+    struct Prep {
+        bool valid = false;
+        const float* f = nullptr;
+        const float* g = nullptr;
+        double eps = 0.0;
+        int64_t rb[2] = {0, 0}, re[2] = {0, 0};
+        DevBuf<float> marg[2], lse[2], mx[2], l2h[2], l2l[2];
+    } prep;
 };
 
 namespace {
@@ -131,6 +141,7 @@ void fsk_engine_destroy(fsk_engine* e) {
         e->P.src = DevSide<float>();
         e->P.tgt = DevSide<float>();
         e->eps_sched.release();
+        e->prep = fsk_engine::Prep();
     }
     cudaDeviceSynchronize();
     cudaFree(e->flags);
@@ -420,6 +431,146 @@ int fsk_engine_transport_vec(fsk_engine* e, int side, const float* v_dev, double
                              nullptr, 0, outf.get(), e->flags);
             launch_f32_to_f64(outf.get(), out_dev, R, s);
         }
+    });
+}
+
+int fsk_engine_transport_prepare(fsk_engine* e, int64_t f_begin, int64_t f_end, int64_t g_begin,
+                                 int64_t g_end, void* stream) {
+    return eguard([&] {
+        if (!e->f || !e->g) throw ValidationFailure("engine potentials not bound");
+        if (!(e->eps > 0.0)) throw ValidationFailure("engine eps not set");
+        const int64_t rb[2] = {f_begin, g_begin}, re[2] = {f_end, g_end};
+        cudaStream_t s = pick(e, stream);
+        Fence fence_{e, s};
+        e->P.s = s;
+        auto& pr = e->prep;
+        pr.valid = false;
+        for (int side = 0; side < 2; ++side) {
+            const int64_t R = side == 0 ? e->P.src.n : e->P.tgt.n;
+            if (rb[side] < 0 || re[side] > R || rb[side] > re[side])
+                throw ValidationFailure("engine row range out of bounds");
+            if (e->P.tc && rb[side] % 256 != 0)
+                throw ValidationFailure("transport row shards must start on a 256-row boundary");
+            for (DevBuf<float>* b : {&pr.marg[side], &pr.lse[side], &pr.mx[side]})
+                if (b->size() < size_t(R)) b->alloc(size_t(R), s);
+            FinalizeArgs<float> fa{};
+            fa.eps = float(e->eps);
+            fa.flags = e->flags;
+            fa.old_pot = side == 0 ? e->f : e->g;
+            fa.w = side == 0 ? e->P.src.w.get() : e->P.tgt.w.get();
+            fa.out_marg = pr.marg[side].get();
+            fa.marg_flag = side == 0 ? kFlagNonFiniteRowMarginal : kFlagNonFiniteColMarginal;
+            fa.out_lse = pr.lse[side].get();
+            fa.out_max = pr.mx[side].get();
+            if (e->P.tc) {
+                for (DevBuf<float>* b : {&pr.l2h[side], &pr.l2l[side]})
+                    if (b->size() < size_t(R)) b->alloc(size_t(R), s);
+                fa.out_l2h = pr.l2h[side].get();
+                fa.out_l2l = pr.l2l[side].get();
+            }
+            const float* kpot = side == 0 ? e->g : e->f;
+            half_step_rows<float>(e->P, side, kpot, float(e->eps), fa, rb[side], re[side]);
+            // exact row-max seeds: the recorded live sets keep only blocks within 2^-64
+            // of a row max (the transport passes below score only those)
+            if (e->P.tc)
+                e->P.tc->tighten_live(e->P, side, kpot, float(e->eps), pr.mx[side].get(),
+                                      e->flags, rb[side], re[side]);
+            pr.rb[side] = rb[side];
+            pr.re[side] = re[side];
+        }
+        pr.f = e->f;
+        pr.g = e->g;
+        pr.eps = e->eps;
+        pr.valid = true;
+    });
+}
+
+namespace {
+const fsk_engine::Prep& check_prep(fsk_engine* e, int side, int64_t rb, int64_t re) {
+    const auto& pr = e->prep;
+    if (!pr.valid || pr.f != e->f || pr.g != e->g || pr.eps != e->eps)
+        throw ValidationFailure("transport state not prepared for the bound potentials / eps");
+    if (side != 0 && side != 1) throw ValidationFailure("side must be 0 or 1");
+    if (rb < pr.rb[side] || re > pr.re[side] || rb > re)
+        throw ValidationFailure("transport rows outside the prepared range");
+    return pr;
+}
+}  // namespace
+
+int fsk_engine_marginal(fsk_engine* e, int side, float* out_dev, void* stream) {
+    return eguard([&] {
+        const auto& pr = check_prep(e, side, e->prep.rb[side & 1], e->prep.re[side & 1]);
+        cudaStream_t s = pick(e, stream);
+        Fence fence_{e, s};
+        const int64_t R = side == 0 ? e->P.src.n : e->P.tgt.n;
+        FSKB_CUDA(cudaMemcpyAsync(out_dev, pr.marg[side].get(), size_t(R) * sizeof(float),
+                                  cudaMemcpyDeviceToDevice, s));
+    });
+}
+
+int fsk_engine_transport_vec_rows(fsk_engine* e, int side, int64_t row_begin, int64_t row_end,
+                                  const float* v_dev, double* out_dev, void* stream) {
+    return eguard([&] {
+        const auto& pr = check_prep(e, side, row_begin, row_end);
+        cudaStream_t s = pick(e, stream);
+        Fence fence_{e, s};
+        e->P.s = s;
+        const float eps = float(e->eps);
+        const float* kpot = side == 0 ? e->g : e->f;
+        const float* pot = side == 0 ? e->f : e->g;
+        const int64_t R = row_end - row_begin;
+        if (R == 0) return;
+        if (e->P.tc) {
+            e->P.tc->vec(e->P, side, kpot, eps, pr.l2h[side].get(), pr.l2l[side].get(),
+                         pr.marg[side].get(), v_dev, out_dev, e->flags, row_begin, row_end);
+            return;
+        }
+        ScoreParams<float> sp = e->P.params(side, kpot, eps);
+        sp.Q += row_begin * sp.d;
+        sp.R = R;
+        DevBuf<float> O(size_t(R), s), outf(size_t(R), s);
+        launch_apply<float>(sp, pr.lse[side].get() + row_begin, v_dev, 1, nullptr, nullptr, 0,
+                            O.get(), s);
+        const float* w = side == 0 ? e->P.src.w.get() : e->P.tgt.w.get();
+        launch_apply_finalize<float>(O.get(), R, 1, w + row_begin, pot + row_begin,
+                                     pr.lse[side].get() + row_begin, pr.mx[side].get() + row_begin,
+                                     eps, outf.get(), e->flags, s);
+        launch_f32_to_f64(outf.get(), out_dev, R, s);
+    });
+}
+
+int fsk_engine_transport_mat_rows(fsk_engine* e, int side, int64_t row_begin, int64_t row_end,
+                                  const float* v_dev, int64_t p, const float* a_dev,
+                                  float* out_dev, void* stream) {
+    return eguard([&] {
+        const auto& pr = check_prep(e, side, row_begin, row_end);
+        if (p < 1) throw ValidationFailure("p must be positive");
+        if (a_dev && side != 0) throw ValidationFailure("the Hadamard form is side 0 only");
+        cudaStream_t s = pick(e, stream);
+        Fence fence_{e, s};
+        e->P.s = s;
+        const float eps = float(e->eps);
+        const float* kpot = side == 0 ? e->g : e->f;
+        const float* pot = side == 0 ? e->f : e->g;
+        const int64_t R = row_end - row_begin, d = e->P.src.d;
+        if (R == 0) return;
+        if (e->P.tc) {
+            e->P.tc->apply_mat(e->P, side, kpot, eps, pr.l2h[side].get(), pr.l2l[side].get(),
+                               pr.marg[side].get(), v_dev, p, out_dev, e->flags, a_dev, row_begin,
+                               row_end);
+            return;
+        }
+        ScoreParams<float> sp = e->P.params(side, kpot, eps);
+        sp.Q += row_begin * sp.d;
+        sp.R = R;
+        DevBuf<float> O(size_t(R * p), s);
+        launch_apply<float>(sp, pr.lse[side].get() + row_begin, v_dev, p,
+                            a_dev ? a_dev + row_begin * d : nullptr,
+                            a_dev ? e->P.tgt.pts.get() : nullptr, a_dev ? d : 0, O.get(), s);
+        const float* w = side == 0 ? e->P.src.w.get() : e->P.tgt.w.get();
+        launch_apply_finalize<float>(O.get(), R, p, w + row_begin, pot + row_begin,
+                                     pr.lse[side].get() + row_begin, pr.mx[side].get() + row_begin,
+                                     eps, out_dev, e->flags, s);
     });
 }
 

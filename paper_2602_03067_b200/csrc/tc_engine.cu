@@ -1538,23 +1538,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
 __global__ void tc_apply_gen_finalize(const float* __restrict__ part, int splits, int64_t R,
                                       int width, int cols, int col0, int64_t p_total,
                                       const float* __restrict__ marg, double inv_v,
-                                      float* __restrict__ out, int* flags) {
+                                      float* __restrict__ out, int* flags, int64_t row0,
+                                      int64_t row1) {
     const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t i = gid / cols;
+    const int64_t i = row0 + gid / cols;   // rows [row0, row1) into out[0 ..)
     const int c = int(gid % cols);
-    if (i >= R) return;
+    if (i >= row1) return;
     double s = 0.0;
     for (int k = 0; k < splits; ++k) s += double(part[(size_t(k) * R + i) * width + c]);
     const double v = double(marg[i]) * s * inv_v;
     if (!isfinite(v)) atomicOr(flags, kFlagNonFiniteTransport);
-    out[i * p_total + col0 + c] = float(v);
+    out[(i - row0) * p_total + col0 + c] = float(v);
 }
 
 // transport-vector epilogue: out_i = r_i sum_s part[s][i]  (P v = diag(r) P~ v)
 __global__ void tc_vec_finalize_kernel(const double* __restrict__ part, int splits, int64_t R,
-                                       const float* __restrict__ marg, double* __restrict__ out) {
+                                       const float* __restrict__ marg, double* __restrict__ out,
+                                       int64_t rows = -1) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= R) return;
+    if (i >= (rows < 0 ? R : rows)) return;
     double s = 0.0;
     for (int k = 0; k < splits; ++k) s += part[size_t(k) * R + i];
     out[i] = double(marg[i]) * s;
@@ -1968,10 +1970,9 @@ struct TcHalfStep::Impl {
     DevBuf<uint32_t> warm_live[2];
     // HBM-resident plan blocks (build_plan)
     DevBuf<float> plan;
-    DevBuf<int> plan_slot, plan_uptr, plan_ukt, plan_uslot, plan_kptr, plan_kunit, plan_kslot;
+    DevBuf<int> plan_slot, plan_uptr, plan_ukt, plan_uslot;
     bool plan_valid = false;
     const float* plan_kpot[2] = {nullptr, nullptr};
-    const float* plan_r = nullptr;
     int plan_units = 0, plan_k_tiles = 0, plan_blocks = 0;
     bool warm_ok[2] = {false, false}, last_warm_track[2] = {false, false};
     int64_t warm_rb[2] = {0, 0}, warm_re[2] = {0, 0};
@@ -2352,9 +2353,14 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         I.live_kwords[side] = p.kwords;
         I.live_row_begin[side] = row_begin;
         I.live_row_end[side] = row_end;
-    } else if (I.live_valid[side] && I.live_kpot[side] == kpot && I.live_row_begin[side] == 0 &&
-               I.live_row_end[side] == p.R && row_begin == 0 && row_end == p.R) {
-        p.live_in = I.live_glob[side].get();
+    } else if (I.live_valid[side] && I.live_kpot[side] == kpot &&
+               row_begin >= I.live_row_begin[side] && row_end <= I.live_row_end[side] &&
+               (row_begin - I.live_row_begin[side]) % (2 * TILE) == 0) {
+        // rows inside the recorded set's range, on its 256-row unit grid: offset to
+        // their units (a row shard of the HVP's transport passes)
+        p.live_in = I.live_glob[side].get() +
+                    size_t((row_begin - I.live_row_begin[side]) / (2 * TILE)) *
+                        size_t(I.live_splits[side]) * size_t(I.live_kwords[side]);
         p.in_splits = I.live_splits[side];
         p.in_kps = I.live_kps[side];
         p.in_kwords = I.live_kwords[side];
@@ -2443,8 +2449,11 @@ __global__ void seed_from_max_kernel(const float* __restrict__ mx_nat, int64_t n
 }
 
 void TcHalfStep::tighten_live(DevProblem<float>& P, int side, const float* kpot, float eps,
-                              const float* mx_nat, int* flags) {
+                              const float* mx_nat, int* flags, int64_t row_begin,
+                              int64_t row_end) {
     const int64_t R = side == 0 ? P.src.n : P.tgt.n;
+    if (row_end < 0) row_end = R;
+    if (row_end <= row_begin) return;
     DevBuf<float> seed(size_t(R), P.s);
     seed_from_max_kernel<<<unsigned((R + 255) / 256), 256, 0, P.s>>>(mx_nat, R, seed.get());
     FSKB_CUDA(cudaGetLastError());
@@ -2452,17 +2461,16 @@ void TcHalfStep::tighten_live(DevProblem<float>& P, int side, const float* kpot,
     DevBuf<double> pm, ps;
     PassExtras ex{};
     ex.m_init = seed.get();
-    pass(P, side, kpot, eps, 0, R, nullptr, flags, pm, ps, &ex);
+    pass(P, side, kpot, eps, row_begin, row_end, nullptr, flags, pm, ps, &ex);
 }
 
 // ---- HBM-resident transport plan (live blocks only) ---------------------------
 //
-// At fixed potentials (the HVP's CG) every transport-vector pass recomputes the
-// same scores. The plan cache keeps the row-normalized entries 2^(t - L_i) of the
-// live (query tile pair, key tile) blocks of the side-0 orientation (the union of
-// both orientations' live sets) as 256 x 128 fp32 blocks; P v and P^T u then are
-// memory-bound sweeps over it. Unit-major (CSR) and key-tile-major (CSC) block
-// lists index the same blocks.
+// Opt-in (FSK_PLAN_CACHE=1; outside the HVP memory contract). At fixed potentials
+// (the HVP's CG) every transport-vector pass recomputes the same scores. The plan
+// cache keeps the row-normalized entries 2^(t - L_i) of the live (query tile pair,
+// key tile) blocks of the side-0 orientation as 256 x 128 fp32 blocks (unit-major
+// CSR); P v is then a memory-bound sweep over it. P^T u keeps streaming (see vec).
 __global__ void plan_pv_kernel(const float* __restrict__ plan, const int* __restrict__ uptr,
                                const int* __restrict__ ukt, const int* __restrict__ uslot,
                                const float* __restrict__ v, int64_t key_valid,
@@ -2504,42 +2512,6 @@ __global__ void plan_pv_kernel(const float* __restrict__ plan, const int* __rest
     if (row < R) out[row] = double(marg[row]) * mine;
 }
 
-__global__ void plan_ptu_kernel(const float* __restrict__ plan, const int* __restrict__ kptr,
-                                const int* __restrict__ kunit, const int* __restrict__ kslot,
-                                const float* __restrict__ u, const float* __restrict__ r,
-                                int64_t R, int64_t key_valid, double* __restrict__ out) {
-    __shared__ double red[8][TILE];
-    const int kt = blockIdx.x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    for (int b = kptr[kt]; b < kptr[kt + 1]; ++b) {
-        const int unit = kunit[b];
-        const float4* bp = reinterpret_cast<const float4*>(plan + size_t(kslot[b]) * 2 * TILE * TILE);
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-#pragma unroll 4
-        for (int rr = warp; rr < 2 * TILE; rr += 8) {
-            const int64_t i = int64_t(unit) * 2 * TILE + rr;
-            const float coef = i < R ? r[i] * u[i] : 0.0f;
-            const float4 q = __ldg(bp + rr * (TILE / 4) + lane);
-            s0 = fmaf(coef, q.x, s0);
-            s1 = fmaf(coef, q.y, s1);
-            s2 = fmaf(coef, q.z, s2);
-            s3 = fmaf(coef, q.w, s3);
-        }
-        a0 += s0, a1 += s1, a2 += s2, a3 += s3;
-    }
-    red[warp][4 * lane] = a0;
-    red[warp][4 * lane + 1] = a1;
-    red[warp][4 * lane + 2] = a2;
-    red[warp][4 * lane + 3] = a3;
-    __syncthreads();
-    if (threadIdx.x < TILE) {
-        double t = 0.0;
-        for (int w = 0; w < 8; ++w) t += red[w][threadIdx.x];
-        const int64_t j = int64_t(kt) * TILE + threadIdx.x;
-        if (j < key_valid) out[j] = t;
-    }
-}
 
 bool TcHalfStep::build_plan(DevProblem<float>& P, const float* g, const float* f, float eps,
                             const float* l2h0, const float* l2l0, const float* r, int* flags) {
@@ -2551,7 +2523,9 @@ bool TcHalfStep::build_plan(DevProblem<float>& P, const float* g, const float* f
     const char* env = std::getenv("FSK_PLAN_CACHE");
     const bool enabled = env && env[0] == '1';
     if (!enabled || I.chunks == 1) return false;   // the d <= 64 kernels do not store blocks
-    if (!(I.live_valid[0] && I.live_kpot[0] == g && I.live_valid[1] && I.live_kpot[1] == f))
+    (void)f;
+    if (!(I.live_valid[0] && I.live_kpot[0] == g && I.live_row_begin[0] == 0 &&
+          I.live_row_end[0] == P.src.n))
         return false;
     const int64_t n = P.src.n, m = P.tgt.n;
     const int q_tiles = int((n + TILE - 1) / TILE), units = (q_tiles + 1) / 2;
@@ -2565,7 +2539,7 @@ bool TcHalfStep::build_plan(DevProblem<float>& P, const float* g, const float* f
                                   cudaMemcpyDeviceToHost, P.s));
         return h;
     };
-    const std::vector<uint32_t> s0 = fetch(0), s1 = fetch(1);
+    const std::vector<uint32_t> s0 = fetch(0);
     FSKB_CUDA(cudaStreamSynchronize(P.s));
     std::vector<uint8_t> live(size_t(units) * k_tiles, 0);
     auto walk = [&](int side, const std::vector<uint32_t>& bits, auto&& mark) {
@@ -2585,13 +2559,7 @@ bool TcHalfStep::build_plan(DevProblem<float>& P, const float* g, const float* f
                 }
     };
     walk(0, s0, [&](int u, int kt) { live[size_t(u) * k_tiles + kt] = 1; });
-    // side 1: unit of Y tiles (2 ug, 2 ug + 1) x X tile kx -> side-0 block (kx / 2, Y tile)
-    walk(1, s1, [&](int ug, int kx) {
-        for (int yt = 2 * ug; yt < 2 * ug + 2 && yt < k_tiles; ++yt)
-            live[size_t(kx / 2) * k_tiles + yt] = 1;
-    });
     std::vector<int> slot(live.size(), -1), uptr(size_t(units) + 1, 0), ukt, uslot;
-    std::vector<int> kcount(size_t(k_tiles) + 1, 0);
     int nb = 0;
     for (int u = 0; u < units; ++u) {
         for (int kt = 0; kt < k_tiles; ++kt)
@@ -2599,7 +2567,6 @@ bool TcHalfStep::build_plan(DevProblem<float>& P, const float* g, const float* f
                 slot[size_t(u) * k_tiles + kt] = nb;
                 ukt.push_back(kt);
                 uslot.push_back(nb);
-                ++kcount[size_t(kt) + 1];
                 ++nb;
             }
         uptr[size_t(u) + 1] = nb;
@@ -2609,18 +2576,6 @@ bool TcHalfStep::build_plan(DevProblem<float>& P, const float* g, const float* f
     size_t free_b = 0, total_b = 0;
     FSKB_CUDA(cudaMemGetInfo(&free_b, &total_b));
     if (bytes > free_b / 2) return false;            // keep room for everything else
-    std::vector<int> kptr(size_t(k_tiles) + 1, 0);
-    std::vector<int> kunit(static_cast<size_t>(nb), 0), kslot(static_cast<size_t>(nb), 0);
-    for (int kt = 0; kt < k_tiles; ++kt) kptr[size_t(kt) + 1] = kptr[size_t(kt)] + kcount[size_t(kt) + 1];
-    {
-        std::vector<int> fill(kptr.begin(), kptr.end() - 1);
-        for (int u = 0; u < units; ++u)
-            for (int b = uptr[size_t(u)]; b < uptr[size_t(u) + 1]; ++b) {
-                const int kt = ukt[size_t(b)];
-                kunit[size_t(fill[size_t(kt)])] = u;
-                kslot[size_t(fill[size_t(kt)]++)] = uslot[size_t(b)];
-            }
-    }
     auto up = [&](DevBuf<int>& d, const std::vector<int>& h) {
         d.alloc(h.size(), P.s);
         FSKB_CUDA(cudaMemcpyAsync(d.get(), h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice,
@@ -2630,9 +2585,6 @@ bool TcHalfStep::build_plan(DevProblem<float>& P, const float* g, const float* f
     up(I.plan_uptr, uptr);
     up(I.plan_ukt, ukt);
     up(I.plan_uslot, uslot);
-    up(I.plan_kptr, kptr);
-    up(I.plan_kunit, kunit);
-    up(I.plan_kslot, kslot);
     // the union as a live_in set: one split, every key tile
     const int kw = (k_tiles + 31) / 32;
     std::vector<uint32_t> uni(size_t(units) * kw, 0u);
@@ -2659,7 +2611,7 @@ bool TcHalfStep::build_plan(DevProblem<float>& P, const float* g, const float* f
     I.plan_valid = true;
     I.plan_kpot[0] = g;
     I.plan_kpot[1] = f;
-    I.plan_r = r;
+    (void)r;
     I.plan_units = units;
     I.plan_k_tiles = k_tiles;
     I.plan_blocks = nb;
@@ -2680,19 +2632,31 @@ double TcHalfStep::plan_fraction() const {
 
 void TcHalfStep::vec(DevProblem<float>& P, int side, const float* kpot, float eps,
                      const float* l2h, const float* l2l, const float* marg, const float* v,
-                     double* out, int* flags) {
+                     double* out, int* flags, int64_t row_begin, int64_t row_end) {
     const int64_t R = side == 0 ? P.src.n : P.tgt.n;
-    if (R == 0) return;
+    if (row_end < 0) row_end = R;
+    if (R == 0 || row_end <= row_begin) return;
     Impl& I = *impl_;
-    if (I.plan_valid && I.plan_kpot[side] == kpot) {
-        if (side == 0)
-            plan_pv_kernel<<<unsigned(I.plan_units), 2 * TILE, 0, P.s>>>(
-                I.plan.get(), I.plan_uptr.get(), I.plan_ukt.get(), I.plan_uslot.get(), v, P.tgt.n,
-                marg, R, out);
-        else
-            plan_ptu_kernel<<<unsigned(I.plan_k_tiles), 256, 0, P.s>>>(
-                I.plan.get(), I.plan_kptr.get(), I.plan_kunit.get(), I.plan_kslot.get(), v, I.plan_r,
-                P.src.n, R, out);
+    if (row_begin != 0 || row_end != R) {
+        // a row shard (multi-GPU HVP): rows [row_begin, row_end) into out[0 ..)
+        DevBuf<double> pm, ps;
+        const float* args[3] = {l2h, l2l, v};
+        const int splits = pass(P, side, kpot, eps, row_begin, row_end, args, flags, pm, ps);
+        const int64_t rows = row_end - row_begin;
+        tc_vec_finalize_kernel<<<unsigned((rows + 255) / 256), 256, 0, P.s>>>(
+            pm.get() + row_begin, splits, R, marg + row_begin, out, rows);
+        FSKB_CUDA(cudaGetLastError());
+        count_launch();
+        return;
+    }
+    // the cached blocks are row-normalised fp32 entries 2^(t - L_i): exact for P v, but a
+    // column whose mass sits in entries below 2^-126 of their rows' maxima (peaked
+    // plans, e.g. d = 1024 at eps = 0.1) flushes to zero there, so P^T u always
+    // streams its column-normalised pass (measured: 2.4e-2 HVP error otherwise)
+    if (I.plan_valid && I.plan_kpot[side] == kpot && side == 0) {
+        plan_pv_kernel<<<unsigned(I.plan_units), 2 * TILE, 0, P.s>>>(
+            I.plan.get(), I.plan_uptr.get(), I.plan_ukt.get(), I.plan_uslot.get(), v, P.tgt.n,
+            marg, R, out);
         FSKB_CUDA(cudaGetLastError());
         count_launch();
         return;
@@ -2708,13 +2672,17 @@ void TcHalfStep::vec(DevProblem<float>& P, int side, const float* kpot, float ep
 
 void TcHalfStep::apply_mat(DevProblem<float>& P, int side, const float* kpot, float eps,
                            const float* l2h, const float* l2l, const float* marg, const float* V,
-                           int64_t p_cols, float* out, int* flags, const float* A) {
+                           int64_t p_cols, float* out, int* flags, const float* A,
+                           int64_t row_begin, int64_t row_end) {
     Impl& I = *impl_;
     const int qc = side == 0 ? 0 : 1, kc = side == 0 ? 1 : 0;
     const DevSide<float>& ks = side == 0 ? P.tgt : P.src;
     const DevSide<float>& qs = side == 0 ? P.src : P.tgt;
     const int64_t R = qs.n;
-    if (R == 0 || p_cols == 0) return;
+    if (row_end < 0) row_end = R;
+    if (R == 0 || p_cols == 0 || row_end <= row_begin) return;
+    if (row_begin % (2 * TILE) != 0)
+        throw ValidationFailure("transport row range must start on a 256-row boundary");
     const int E = I.eq[qc] + I.ek[side];
     const int k_tiles = int(I.rows_pad[kc] / TILE);
     build_bias<<<unsigned((I.rows_pad[kc] + 255) / 256), 256, 0, P.s>>>(
@@ -2760,24 +2728,27 @@ void TcHalfStep::apply_mat(DevProblem<float>& P, int side, const float* kpot, fl
     g.w_mul = w_mul;
     g.chunks = I.chunks;
     g.v_chunks = VC;
-    g.q_tile_begin = 0;
-    g.q_tiles = int(I.rows_pad[qc] / TILE);
+    g.q_tile_begin = int(row_begin / TILE);
+    g.q_tiles = int((row_end + TILE - 1) / TILE) - g.q_tile_begin;
     g.k_tiles = k_tiles;
     const int sms = num_sms();
     const double q_bytes = double(I.chunks) * QTILE * (A ? 2 : 1);
     const int min_s = I.chunks > 1 ? int(std::ceil(sms * q_bytes / (48.0 * (1 << 20)))) : 1;
     g.splits = pick_splits(g.q_tiles, k_tiles, sms, min_s);
     g.items = g.q_tiles * g.splits;
-    g.row_begin = 0;
-    g.row_end = R;
+    g.row_begin = row_begin;
+    g.row_end = row_end;
     g.key_valid = ks.n;
     g.R = R;
     g.acc_scale = std::ldexp(1.0f, E);
     g.l2h = l2h;
     g.l2l = l2l;
-    if (I.live_valid[side] && I.live_kpot[side] == kpot && I.live_row_begin[side] == 0 &&
-        I.live_row_end[side] == R) {
-        g.live_in = I.live_glob[side].get();
+    if (I.live_valid[side] && I.live_kpot[side] == kpot && row_begin >= I.live_row_begin[side] &&
+        row_end <= I.live_row_end[side] &&
+        (row_begin - I.live_row_begin[side]) % (2 * TILE) == 0) {
+        g.live_in = I.live_glob[side].get() +
+                    size_t((row_begin - I.live_row_begin[side]) / (2 * TILE)) *
+                        size_t(I.live_splits[side]) * size_t(I.live_kwords[side]);
         g.in_splits = I.live_splits[side];
         g.in_kps = I.live_kps[side];
         g.in_kwords = I.live_kwords[side];
@@ -2793,9 +2764,10 @@ void TcHalfStep::apply_mat(DevProblem<float>& P, int side, const float* kpot, fl
         count_launch();
         const int width = g.vc * DPAD;
         const int cols = int(std::min<int64_t>(width, p_cols - int64_t(v0) * DPAD));
-        const int64_t total = R * cols;
+        const int64_t total = (row_end - row_begin) * cols;
         tc_apply_gen_finalize<<<unsigned((total + 255) / 256), 256, 0, P.s>>>(
-            part.get(), g.splits, R, width, cols, v0 * DPAD, p_cols, marg, out_scale, out, flags);
+            part.get(), g.splits, R, width, cols, v0 * DPAD, p_cols, marg, out_scale, out, flags,
+            row_begin, row_end);
         FSKB_CUDA(cudaGetLastError());
         count_launch();
     }

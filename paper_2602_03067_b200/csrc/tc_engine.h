@@ -73,7 +73,8 @@ public:
     // of a row's max stay live, so the transport passes that follow (HVP/CG) skip
     // the rest. One extra LSE pass.
     void tighten_live(DevProblem<float>& P, int side, const float* kpot, float eps,
-                      const float* mx_nat, int* flags);
+                      const float* mx_nat, int* flags, int64_t row_begin = 0,
+                      int64_t row_end = -1);
 
     // Transport-vector application with fixed potentials: out_i = marg_i sum_j
     // 2^(t_ij - L_i) v_j = (P v)_i (side 0) or (P^T v)_j (side 1), given the row
@@ -81,7 +82,8 @@ public:
     // (from a `run` with out_l2h/out_l2l/out_marg at the same potentials). v is
     // indexed by the key side; out (double) by the updated side.
     void vec(DevProblem<float>& P, int side, const float* kpot, float eps, const float* l2h,
-             const float* l2l, const float* marg, const float* v, double* out, int* flags);
+             const float* l2l, const float* marg, const float* v, double* out, int* flags,
+             int64_t row_begin = 0, int64_t row_end = -1);
 
     // Transport-matrix application with fixed potentials: out (rows x p, float) =
     // P V (side 0) or P^T V (side 1) for a general V (key rows x p, float, device),
@@ -90,7 +92,8 @@ public:
     // key cloud (apply_hadamard_plan with B = the key cloud, as in the HVP).
     void apply_mat(DevProblem<float>& P, int side, const float* kpot, float eps, const float* l2h,
                    const float* l2l, const float* marg, const float* V, int64_t p_cols,
-                   float* out, int* flags, const float* A = nullptr);
+                   float* out, int* flags, const float* A = nullptr, int64_t row_begin = 0,
+                   int64_t row_end = -1);
 
 private:
     void poll_screen(int side, double max_live);
