@@ -373,6 +373,17 @@ def run_b200(args, cfgname):
     hvp_dir = np.random.default_rng(7).standard_normal((n, d)) if STEP_TAIL[cfgname] == "hvp" \
         else None
     sptr = stream.cuda_stream
+    hvp = None
+    if STEP_TAIL[cfgname] == "hvp":
+        # the HVP on the engine's resident potentials, rows sharded over the ranks (2
+        # all-gathers per CG iteration, paper_2602_03067_b200.sharded.ShardedHvp);
+        # X, Y, A replicated fp64 on the device (row-local assembly)
+        from paper_2602_03067_b200.sharded import ShardedHvp
+        dev = torch.device("cuda", local)
+        hvp = ShardedHvp(eng, plan, dev, dist if world > 1 else None)
+        Xd = torch.tensor(X, dtype=torch.float64, device=dev)
+        Yd = torch.tensor(Y, dtype=torch.float64, device=dev)
+        Ad = torch.tensor(hvp_dir, dtype=torch.float64, device=dev)
 
     # the engine launches on its own stream unless given one: pass torch's
     def half(side, lo_, hi_):
@@ -412,15 +423,11 @@ def run_b200(args, cfgname):
                 events[-1].record(stream)
             solver._gather(solver.g, plan.g_per)
         if STEP_TAIL[cfgname] == "hvp":
-            # SPEC hvp_apply at the step's potentials through the public C ABI
-            # (fsk_hvp_apply_single: tcgen05 transport-vector applies)
+            # SPEC hvp_apply at the step's potentials: K_CG = 50 fixed
             if events is not None:
                 gev.append(torch.cuda.Event(enable_timing=True))
                 gev[-1].record(stream)
-            fh = solver.f[:n].double().cpu().numpy()
-            gh = solver.g[:m].double().cpu().numpy()
-            fsk.hvp_apply(X, a, Y, b, fh, gh, eps, hvp_dir, tau=1e-5, cg_tol=1e-30,
-                          cg_max_iters=HVP_CG_ITERS, precision="single")
+            hvp.apply(Xd, Yd, Ad, eps, tau=1e-5, cg_tol=1e-30, cg_max_iters=HVP_CG_ITERS)
             if events is not None:
                 gev.append(torch.cuda.Event(enable_timing=True))
                 gev[-1].record(stream)

@@ -24,8 +24,10 @@ from dataclasses import dataclass
 
 
 def all_gather_shards(dist, group, buf, per, rank, world):
-    """In-place all-gather of `buf` (world * per), rank k owning [k per, (k+1) per)."""
-    if dist is None or world == 1:
+    """In-place all-gather of `buf` (world * per), rank k owning [k per, (k+1) per).
+    (A world-size-1 group still runs the collective: that is how the NCCL branch is
+    exercised on a single device.)"""
+    if dist is None:
         return
     if dist.get_backend(group) == "nccl":
         # in place: rank k's slice is the send buffer (NVLink / NVSwitch)
@@ -100,7 +102,7 @@ class ShardedSinkhorn:
         one collective per half-step; returns the summed violation (fp64)."""
         torch = self.torch
         k, world = self.plan.rank, self.plan.world
-        if self.dist is None or world == 1:
+        if self.dist is None:
             return float(viol_partial.item())
         stride = per + 2
         pay = self._pay if getattr(self, "_pay", None) is not None and \
