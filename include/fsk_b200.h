@@ -359,6 +359,16 @@ void fsk_rng_normal_fill(uint64_t seed, double* out, int64_t count);
 const char* fsk_version(void);
 int fsk_device_count(void);
 
+/* Multi-GPU solves inside the library: n >= 1 makes sinkhorn_solve,
+ * _solve_grad and _solve_warm (alternating schedule) shard rows of X and Y over
+ * devices 0..n-1 of this process - one host thread and stream per device, both
+ * clouds resident on each, an NCCL all-gather of the potential shards after every
+ * half-step (ncclCommInitAll; the fp64 early stop's violation partials ride in the
+ * same NCCL group), marginals / dual / gradient assembled from the shards.
+ * n = 0 (default) is the single-device path on the current device. */
+int fsk_set_num_devices(int n);
+int fsk_num_devices(void);
+
 /* High-water mark (bytes) of the device's default memory pool, which holds every
  * allocation the library makes; reset != 0 restarts it at the current usage.
  * The HVP memory contract (peak <= c (n + m) d scalars, never n m)

@@ -468,6 +468,17 @@ def rng_normal(seed: int, count: int) -> np.ndarray:
     return out
 
 
+def set_num_devices(n: int) -> None:
+    """fsk_set_num_devices: 0 (default) = the single-device path; n >= 1 = sinkhorn_solve
+    (and _grad / warm starts) shard rows over devices 0..n-1 with in-library NCCL
+    all-gathers."""
+    _check(lib().fsk_set_num_devices(C.c_int(n)))
+
+
+def num_devices() -> int:
+    return int(lib().fsk_num_devices())
+
+
 def device_peak_bytes(device: int = 0, reset: bool = False) -> int:
     """High-water mark of the device memory pool every library allocation comes from
     (fsk_device_peak_bytes); reset=True restarts it at the current usage."""

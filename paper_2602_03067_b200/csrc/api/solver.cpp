@@ -2,6 +2,7 @@
 #include "../../../include/fsk/solver.hpp"
 
 #include "../../../include/fsk/autodiff.hpp"
+#include "../../../include/fsk/devices.hpp"
 #include "../../../include/fsk/hvp.hpp"
 #include "../hostlib.h"
 #include "bridge.h"
@@ -14,6 +15,9 @@ void check_pots(const ShiftedPotentials& p, std::size_t n, std::size_t m) {
         throw ValidationError("potential lengths do not match the measures");
 }
 }  // namespace
+
+void set_num_devices(int n) { bridge::check(fsk_set_num_devices(n)); }
+int num_devices() { return fsk_num_devices(); }
 
 namespace solver {
 

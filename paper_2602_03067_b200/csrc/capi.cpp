@@ -16,6 +16,7 @@
 #include "core_kernels.h"
 #include "device_ops.h"
 #include "hostlib.h"
+#include "multi_device.h"
 #include "small_solve.h"
 #include "tc_engine.h"
 
@@ -253,6 +254,17 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
                 const double* g_init = nullptr) {
     constexpr bool kSingle = std::is_same_v<T, float>;
     const int64_t n = src.n, m = tgt.n, d = src.d;
+    const double fs = feature_scale(cost);
+    if (num_devices_setting() >= 1 && cfg.schedule == 0) {
+        // sharded over the configured devices (multi_device.cpp)
+        const std::vector<double> alpha_m = host_sqnorm(src, fs), beta_m = host_sqnorm(tgt, fs);
+        const double diam2_m = cfg.eps_scaling_factor < 1.0
+                                   ? joint_sq_diameter_raw(src.points, n, tgt.points, m, d)
+                                   : 0.0;
+        if (solve_multi_device<T>(src, tgt, cost, cfg, eps_schedule_raw(cfg, diam2_m), alpha_m,
+                                  beta_m, f_init, g_init, tiles, ledger, rep, grad_out))
+            return;
+    }
     auto& C = exec_ctx();
     PhaseTimer timer(C.s);
     DevProblem<T> P;
@@ -261,7 +273,6 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
     if constexpr (kSingle) enable_tensor_path(P, tensor_mode_from_env());
     timer.mark("operand images");
 
-    const double fs = feature_scale(cost);
     const std::vector<double> alpha = host_sqnorm(src, fs), beta = host_sqnorm(tgt, fs);
     std::vector<double> f0((size_t)(n)), g0((size_t)(m));
     // reference init f = g = 0, i.e. f_hat = -alpha, g_hat = -beta (solver.cpp:27-32);

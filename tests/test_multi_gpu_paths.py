@@ -162,3 +162,44 @@ def test_nccl_world1_gather_and_violation_payload(fsk):
         eng2.close()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("precision,tol", [("single", 0.0), ("double", 0.0), ("double", 1e-7)])
+def test_in_library_multi_device_solve_matches_single_device(fsk, port, precision, tol):
+    """fsk_set_num_devices(1): sinkhorn_solve(_grad) through the in-library NCCL path
+    (one host thread + stream per device, ncclCommInitAll, all-gather of the potential
+    shards after every half-step, fused early stop with the violation all-reduce in
+    the same NCCL group) returns what the single-device path returns: same iterate
+    count, potentials, loss, violation, gradient, ledger."""
+    X, a, Y, b, eps = _problem(n=3000, m=2600, d=64, eps=0.2)
+    kw = dict(eps=eps, max_iters=300 if tol else 12, marginal_tol=tol, precision=precision,
+              grad=True)
+    l0, l1 = fsk.Ledger(), fsk.Ledger()
+    want = fsk.sinkhorn_solve(X, a, Y, b, ledger=l0, **kw)
+    fsk.set_num_devices(1)
+    try:
+        got = fsk.sinkhorn_solve(X, a, Y, b, ledger=l1, **kw)
+    finally:
+        fsk.set_num_devices(0)
+    print(f"{precision} tol={tol}: iterations {got['iterations']} vs {want['iterations']}, "
+          f"loss {got['dual_cost']!r} vs {want['dual_cost']!r}")
+    assert got["iterations"] == want["iterations"]
+    for key in ("f_hat", "g_hat", "grad"):
+        ref = want[key]
+        err = np.abs(got[key] - ref).max() / max(1.0, np.abs(ref).max())
+        assert err <= (1e-12 if precision == "double" else 1e-6), (key, err)
+    assert abs(got["dual_cost"] - want["dual_cost"]) <= 1e-12 * abs(want["dual_cost"]) + (
+        0.0 if precision == "double" else 1e-7 * abs(want["dual_cost"]))
+    assert abs(got["marginal_violation"] - want["marginal_violation"]) <= \
+        1e-9 * want["marginal_violation"] + (0.0 if precision == "double" else 1e-6)
+    assert l0.total_scalars() == l1.total_scalars()
+
+
+def test_in_library_multi_device_rejects_missing_devices(fsk):
+    X, a, Y, b, eps = _problem(n=300, m=260, d=8)
+    fsk.set_num_devices(fsk.lib().fsk_device_count() + 1)
+    try:
+        with pytest.raises(fsk.ValidationError):
+            fsk.sinkhorn_solve(X, a, Y, b, eps=eps, max_iters=3)
+    finally:
+        fsk.set_num_devices(0)
