@@ -534,8 +534,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
     auto kempty = [&](int s) { return bar0 + 8u * (TQ_STAGES + s); };
     const uint32_t qready = bar0 + 8u * (2 * TQ_STAGES);          // epilogue -> MMA
     const uint32_t qfree = qready + 8u;                            // MMA -> epilogue
-    auto accfull = [&](int t) { return qready + 16u + 8u * t; };
-    auto accempty = [&](int t) { return qready + 32u + 8u * t; };
+    // half h (keys [64 h, 64 h + 64) of the key tile) of query tile t's accumulator:
+    // h = 0 next to qready, h = 1 past the TMEM slot word
+    auto accfull = [&](int t, int h) { return h == 0 ? qready + 16u + 8u * t : bar0 + 200u + 8u * t; };
+    auto accempty = [&](int t, int h) {
+        return h == 0 ? qready + 32u + 8u * t : bar0 + 216u + 8u * t;
+    };
     const uint32_t screen_done = qready + 48u;
     const uint32_t bits_free = qready + 56u;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + TQ_OFF_BAR + 192);
@@ -555,10 +559,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
         }
         mbar_init(qready, 8);
         mbar_init(qfree, 1);
-        for (int t = 0; t < 2; ++t) {
-            mbar_init(accfull(t), 1);
-            mbar_init(accempty(t), 4);
-        }
+        for (int t = 0; t < 2; ++t)
+            for (int h = 0; h < 2; ++h) {
+                mbar_init(accfull(t, h), 1);
+                mbar_init(accempty(t, h), 4);
+            }
         mbar_init(screen_done, 8);
         mbar_init(bits_free, 2);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -678,15 +683,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                     const uint32_t mask = screen_phase ? 3u : stage_mask[s];
                     for (int t = 0; t < nq; ++t) {
                         if (!((mask >> t) & 1u)) continue;
-                        mbar_wait(accempty(t), (acc_n[t] & 1) ^ 1);
-                        fence_after();
-                        const uint32_t d = tm + uint32_t(t * TILE);
                         const uint32_t q = tm + TQ_QCOL + uint32_t(t) * TQ_QSTRIDE;
-                        if (screen_phase)
-                            issue_screen_tile_tq<true>(d, q, kst);
-                        else
-                            issue_score_tile_tq<true>(d, q, kst);
-                        umma_commit<true>(accfull(t));
+                        // two N = 64 halves: the epilogue drains half 0 while half 1
+                        // computes, and half 0 of the next key tile overlaps half 1
+                        for (int h = 0; h < 2; ++h) {
+                            mbar_wait(accempty(t, h), (acc_n[t] & 1) ^ 1);
+                            fence_after();
+                            const uint32_t d = tm + uint32_t(t * TILE + h * 64);
+                            if (screen_phase)
+                                issue_screen_half_tq<true>(d, q, kst, h);
+                            else
+                                issue_score_half_tq<true>(d, q, kst, h);
+                            umma_commit<true>(accfull(t, h));
+                        }
                         ++acc_n[t];
                     }
                     umma_commit<true>(kempty(s));
@@ -775,25 +784,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 const bool row_ok = t < nq && row < p.R;
                 for (int kt = kt0; kt < kt1; ++kt) {
                     if (t < nq) {
-                        mbar_wait(accfull(t), acc_n & 1);
-                        fence_after();
-                        const int64_t kbase = int64_t(kt) * TILE;
-                        // all four 32-column loads in flight before one wait
-                        uint32_t v[128];
-                        FSKB_TMEM_LD32(acc_addr + 0, (v + 0));
-                        FSKB_TMEM_LD32(acc_addr + 32, (v + 32));
-                        FSKB_TMEM_LD32(acc_addr + 64, (v + 64));
-                        FSKB_TMEM_LD32(acc_addr + 96, (v + 96));
-                        tmem_ld_wait();
-                        if (kbase + TILE > p.key_valid) {
+                        float tmax = -INFINITY;
 #pragma unroll
-                            for (int j = 0; j < 128; ++j)
-                                if (kbase + j >= p.key_valid) v[j] = __float_as_uint(-INFINITY);
+                        for (int h = 0; h < 2; ++h) {
+                            mbar_wait(accfull(t, h), acc_n & 1);
+                            fence_after();
+                            const int64_t kbase = int64_t(kt) * TILE + 64 * h;
+                            uint32_t v[64];
+                            FSKB_TMEM_LD32(acc_addr + 64 * h, (v + 0));
+                            FSKB_TMEM_LD32(acc_addr + 64 * h + 32, (v + 32));
+                            tmem_ld_wait();
+                            fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(accempty(t, h));
+                            if (kbase + 64 > p.key_valid) {
+#pragma unroll
+                                for (int j = 0; j < 64; ++j)
+                                    if (kbase + j >= p.key_valid) v[j] = __float_as_uint(-INFINITY);
+                            }
+                            tmax = fmaxf(tmax, row_max<64>(v) * p.acc_scale);
                         }
-                        const float tmax = row_max<128>(v) * p.acc_scale;
-                        fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(accempty(t));
                         ++acc_n;
                         Ma = fmaxf(Ma, tmax);
                         const bool live = row_ok && tmax >= Ma - p.screen_thr;
@@ -825,23 +835,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
             }
             for (int kt = t < nq ? first_kt(unit, kt0, kt1, t) : kt1, kt_next; kt < kt1;
                  kt = kt_next) {
-                mbar_wait(accfull(t), acc_n & 1);
-                fence_after();
-                uint32_t v[128];
-                FSKB_TMEM_LD32(acc_addr + 0, (v + 0));
-                FSKB_TMEM_LD32(acc_addr + 32, (v + 32));
-                FSKB_TMEM_LD32(acc_addr + 64, (v + 64));
-                FSKB_TMEM_LD32(acc_addr + 96, (v + 96));
-                kt_next = next_kt(unit, kt, kt0, kt1, t);  // overlaps the TMEM loads
-                tmem_ld_wait();
-                fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(accempty(t));
-                ++acc_n;
                 const float M_old = M;
-                float umax;
-                const bool hit = k1_tile_update<VEC>(v, int64_t(kt) * TILE, p, M, S, nlh, nll, vb,
-                                                     lane, umax);
+                float umax = -INFINITY;
+                bool hit = false;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    mbar_wait(accfull(t, h), acc_n & 1);
+                    fence_after();
+                    uint32_t v[64];
+                    FSKB_TMEM_LD32(acc_addr + 64 * h, (v + 0));
+                    FSKB_TMEM_LD32(acc_addr + 64 * h + 32, (v + 32));
+                    if (h == 0) kt_next = next_kt(unit, kt, kt0, kt1, t);  // overlaps the loads
+                    tmem_ld_wait();
+                    fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(accempty(t, h));
+                    float uh;
+                    hit |= k1_tile_update<VEC, 64>(v, int64_t(kt) * TILE + 64 * h, p, M, S, nlh,
+                                                   nll, vb, lane, uh);
+                    umax = fmaxf(umax, uh);
+                }
+                ++acc_n;
                 if (!VEC && !SCREEN && hit && p.live_global && lane == 0)
                     atomicOr(&p.live_global[(size_t(unit) * p.splits + split) * p.kwords + ((kt - kt0) >> 5)],
                              1u << ((kt - kt0) & 31));

@@ -265,6 +265,41 @@ __device__ __forceinline__ void issue_score_tile_tq(uint32_t d_tmem, uint32_t q,
     for (int kk = 0; kk < DPAD / 16; ++kk)
         umma_ts<ELECT>(d_tmem, q + kk * 8, umma_desc(kst + kk * 32, 1024, 2), IDESC_QK, 1u);
 }
+// Half-width (N = 64) forms: keys [64 h, 64 h + 64) of the staged key tile into a
+// 64-column accumulator. A query tile then owns two half accumulators, so the MMAs
+// of one half overlap the epilogue of the other even when only one query tile of
+// the pair is live (the common case of a warm pass).
+constexpr uint32_t IDESC_QK64 = (1u << 4) | (uint32_t(64 >> 3) << 17) | (uint32_t(TILE >> 4) << 24);
+constexpr uint32_t kHalfK = 64 * 128;   // 64 key rows of a SW128 hi / lo chunk
+constexpr uint32_t kHalfB = 64 * 32;    // 64 key rows of the SW32 bias chunk
+template <bool ELECT = false>
+__device__ __forceinline__ void issue_score_half_tq(uint32_t d_tmem, uint32_t q, uint32_t kst,
+                                                    int h) {
+    const uint32_t kh = kst + uint32_t(h) * kHalfK;
+#pragma unroll
+    for (int kk = 0; kk < DPAD / 16; ++kk) {
+        umma_ts<ELECT>(d_tmem, q + 32 + kk * 8, umma_desc(kh + kk * 32, 1024, 2), IDESC_QK64,
+                       kk > 0 ? 1u : 0u);
+        umma_ts<ELECT>(d_tmem, q + kk * 8, umma_desc(kh + CHUNK + kk * 32, 1024, 2), IDESC_QK64,
+                       1u);
+    }
+    umma_ts<ELECT>(d_tmem, q + 64, umma_desc(kst + QTILE + uint32_t(h) * kHalfB, 256, 6),
+                   IDESC_QK64, 1u);
+#pragma unroll
+    for (int kk = 0; kk < DPAD / 16; ++kk)
+        umma_ts<ELECT>(d_tmem, q + kk * 8, umma_desc(kh + kk * 32, 1024, 2), IDESC_QK64, 1u);
+}
+template <bool ELECT = false>
+__device__ __forceinline__ void issue_screen_half_tq(uint32_t d_tmem, uint32_t q, uint32_t kst,
+                                                     int h) {
+    const uint32_t kh = kst + uint32_t(h) * kHalfK;
+    umma_ts<ELECT>(d_tmem, q + 64, umma_desc(kst + QTILE + uint32_t(h) * kHalfB, 256, 6),
+                   IDESC_QK64, 0u);
+#pragma unroll
+    for (int kk = 0; kk < DPAD / 16; ++kk)
+        umma_ts<ELECT>(d_tmem, q + kk * 8, umma_desc(kh + kk * 32, 1024, 2), IDESC_QK64, 1u);
+}
+
 template <bool ELECT = false>
 __device__ __forceinline__ void issue_screen_tile_tq(uint32_t d_tmem, uint32_t q, uint32_t kst) {
     umma_ts<ELECT>(d_tmem, q + 64, umma_desc(kst + QTILE, 256, 6), IDESC_QK, 0u);
