@@ -542,6 +542,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
     };
     const uint32_t screen_done = qready + 48u;
     const uint32_t bits_free = qready + 56u;
+    // warm passes: the item's live words (both query tiles) are staged in shared
+    // memory by the producer warp, double-buffered by item parity; ready: producer ->
+    // epilogue, free: epilogue -> producer (SCREEN kernels use the first pair above)
+    auto wbits_ready = [&](int b) { return b == 0 ? screen_done : bar0 + 232u; };
+    auto wbits_free = [&](int b) { return b == 0 ? bits_free : bar0 + 240u; };
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + TQ_OFF_BAR + 192);
     uint32_t* live_bits = reinterpret_cast<uint32_t*>(sbase + TQ_OFF_BAR + 256 + VBUF);
     // per K stage: which query tiles of the unit are live for the staged key tile
@@ -564,8 +569,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 mbar_init(accfull(t, h), 1);
                 mbar_init(accempty(t, h), 4);
             }
-        mbar_init(screen_done, 8);
-        mbar_init(bits_free, 2);
+        if constexpr (SCREEN) {
+            mbar_init(screen_done, 8);
+            mbar_init(bits_free, 2);
+        } else {
+            for (int b = 0; b < 2; ++b) {
+                mbar_init(wbits_ready(b), 1);
+                mbar_init(wbits_free(b), 8);
+            }
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -592,23 +604,59 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
         return kt1;
     };
     const int ktiles_per_split = (p.k_tiles + p.splits - 1) / p.splits;
+    // warm pass with per-tile live sets whose split matches the pass's: stage the
+    // item's words in shared memory (the walk otherwise waits an L1/L2 round trip per
+    // key tile, on the producer and on every epilogue warp)
+    constexpr int kStageW = SWORDS / 2;   // words per query tile and buffer
+    const bool staged = !VEC && !SCREEN && p.live_in && p.live_tq &&
+                        p.in_splits == p.splits && p.in_kps == ktiles_per_split &&
+                        p.in_kwords <= kStageW;
+    auto staged_words = [&](int lu, int t) { return live_bits + ((lu & 1) * 2 + t) * kStageW; };
+    auto next_staged = [&](int kt, int kt0, int kt1, int lu, int t) {
+        const uint32_t* w0 = staged_words(lu, t < 0 ? 0 : t);
+        const uint32_t* w1 = staged_words(lu, 1);
+        while (kt < kt1) {
+            const int rel = kt - kt0;
+            const uint32_t w = (t < 0 ? (w0[rel >> 5] | w1[rel >> 5]) : w0[rel >> 5]) >> (rel & 31);
+            if (w) return kt + __ffs(w) - 1;
+            kt += 32 - (rel & 31);
+        }
+        return kt1;
+    };
     // phase-2 (SCREEN) / VEC-at-fixed-potentials key tile sequence
     // (t >= 0: the sequence of query tile t of the unit; producer / MMA: t = -1)
-    auto first_kt = [&](int unit, int kt0, int kt1, int t = -1) {
+    auto first_kt = [&](int unit, int kt0, int kt1, int t = -1, int lu = 0) {
         if constexpr (SCREEN) return next_live(kt0, kt0, kt1, t);
+        if (staged) return next_staged(kt0, kt0, kt1, lu, t);
         return p.live_in ? live_in_next(p, unit, kt0, kt1, t, !VEC && p.live_tq) : kt0;
     };
-    auto next_kt = [&](int unit, int kt, int kt0, int kt1, int t = -1) {
+    auto next_kt = [&](int unit, int kt, int kt0, int kt1, int t = -1, int lu = 0) {
         if constexpr (SCREEN) return next_live(kt + 1, kt0, kt1, t);
+        if (staged) return next_staged(kt + 1, kt0, kt1, lu, t);
         return p.live_in ? live_in_next(p, unit, kt + 1, kt1, t, !VEC && p.live_tq) : kt + 1;
     };
 
     if (warp == 0) {
-        if (lane == 0) {
-            int it = 0;
-            for (int item = blockIdx.x, lu = 0; item < p.items; item += gridDim.x, ++lu) {
-                int unit, split;
-                item_coords(p.items, p.splits, item, unit, split);
+        int it = 0;   // (lane 0's stage counter)
+        for (int item = blockIdx.x, lu = 0; item < p.items; item += gridDim.x, ++lu) {
+            int unit, split;
+            item_coords(p.items, p.splits, item, unit, split);
+            if (staged) {
+                // the whole warp copies both query tiles' words of this item
+                const int b = lu & 1;
+                mbar_wait(wbits_free(b), ((lu >> 1) & 1) ^ 1);
+                const uint32_t* src =
+                    p.live_in + (size_t(unit) * p.in_splits + split) * 2 * p.in_kwords;
+                uint32_t* d0 = staged_words(lu, 0);
+                uint32_t* d1 = staged_words(lu, 1);
+                for (int w = lane; w < p.in_kwords; w += 32) {
+                    d0[w] = __ldg(src + w);
+                    d1[w] = __ldg(src + p.in_kwords + w);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(wbits_ready(b));
+            }
+            if (lane == 0) {
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
                 if constexpr (SCREEN) {
@@ -623,7 +671,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                     mbar_wait(screen_done, lu & 1);
                 }
                 int nlive = 0;
-                int kt = first_kt(unit, kt0, kt1);
+                int kt = first_kt(unit, kt0, kt1, -1, lu);
                 if (kt >= kt1) {
                     // nothing live: one empty stage carrying only the end-of-item flag
                     const int s = it % TQ_STAGES;
@@ -634,12 +682,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 }
                 for (int kn; kt < kt1; kt = kn, ++it) {
                     const int s = it % TQ_STAGES;
-                    kn = next_kt(unit, kt, kt0, kt1);
+                    kn = next_kt(unit, kt, kt0, kt1, -1, lu);
                     uint32_t mask = 3u;
                     if constexpr (SCREEN) {
                         const int rel = kt - kt0;
                         mask = ((live_bits[rel >> 5] >> (rel & 31)) & 1u) |
                                (((live_bits[SWORDS + (rel >> 5)] >> (rel & 31)) & 1u) << 1);
+                    } else if (staged) {
+                        const int rel = kt - kt0;
+                        mask = ((staged_words(lu, 0)[rel >> 5] >> (rel & 31)) & 1u) |
+                               (((staged_words(lu, 1)[rel >> 5] >> (rel & 31)) & 1u) << 1);
                     } else if (!VEC && p.live_tq) {
                         mask = uint32_t(live_in_bit(p, unit, 0, kt)) |
                                (uint32_t(live_in_bit(p, unit, 1, kt)) << 1);
@@ -658,6 +710,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                         atomicAdd(p.live_count, (unsigned long long)nlive);
                 }
             }
+            __syncwarp();
         }
     } else if (warp == 1) {
         // the whole warp runs the issue loop converged; one elected lane issues each
@@ -833,7 +886,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                         p.live_global[(size_t(unit) * p.splits + split) * p.kwords + w] =
                             live_word(-1, w);
             }
-            for (int kt = t < nq ? first_kt(unit, kt0, kt1, t) : kt1, kt_next; kt < kt1;
+            if (staged) mbar_wait(wbits_ready(lu & 1), (lu >> 1) & 1);
+            for (int kt = t < nq ? first_kt(unit, kt0, kt1, t, lu) : kt1, kt_next; kt < kt1;
                  kt = kt_next) {
                 const float M_old = M;
                 float umax = -INFINITY;
@@ -845,7 +899,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                     uint32_t v[64];
                     FSKB_TMEM_LD32(acc_addr + 64 * h, (v + 0));
                     FSKB_TMEM_LD32(acc_addr + 64 * h + 32, (v + 32));
-                    if (h == 0) kt_next = next_kt(unit, kt, kt0, kt1, t);  // overlaps the loads
+                    if (h == 0) kt_next = next_kt(unit, kt, kt0, kt1, t, lu);  // overlaps the loads
                     tmem_ld_wait();
                     fence_before();
                     __syncwarp();
@@ -868,6 +922,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                             atomicMax(&p.gap[size_t(2 * unit + t) * p.k_tiles + kt], gmax);
                     }
                 }
+            }
+            if (staged) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(wbits_free(lu & 1));
             }
             if constexpr (SCREEN) {
                 mbar_wait(bits_free, lu & 1);
