@@ -274,6 +274,15 @@ typedef struct fsk_engine fsk_engine;
  *       1 = force CUDA-core FMA fp32, 2 = force tensor (split-fp16). */
 int fsk_engine_create(int device, const double* X, const double* a, int64_t n, const double* Y,
                       const double* b, int64_t m, int64_t d, int mode, fsk_engine** out);
+/* Same with the label-augmented cost C_ij = lambda1 |x_i - y_j|^2 + lambda2 W[la_i, lb_j]
+ * (CostSpec::LabelAugmented, core.hpp; stream.cpp:73-77): labels int32 in [0, V), W
+ * row-major V x V. The tensor path applies lambda2 W / eps in the chunked / general
+ * kernels' epilogues (V <= 64), the CUDA-core path in its score tiles. */
+int fsk_engine_create_labeled(int device, const double* X, const double* a, const int32_t* la,
+                              int64_t n, const double* Y, const double* b, const int32_t* lb,
+                              int64_t m, int64_t d, double lambda1, double lambda2,
+                              const double* label_cost, int64_t num_labels, int mode,
+                              fsk_engine** out);
 void fsk_engine_destroy(fsk_engine* e);
 /* Sets eps (rebuilds the scaled key images) and the potential buffers. */
 int fsk_engine_set_eps(fsk_engine* e, double eps);

@@ -503,16 +503,30 @@ class Engine:
 
     MODES = {"auto": 0, "fma": 1, "tensor": 2}
 
-    def __init__(self, device, X, a, Y, b, mode="auto"):
+    def __init__(self, device, X, a, Y, b, mode="auto", cost=None, la=None, lb=None):
+        """cost (dict lambda1, lambda2, label_cost V x V) with labels la, lb: the
+        label-augmented cost (fsk_engine_create_labeled)."""
         k = _Keep()
         X, a, Y, b = k.arr(X), k.arr(a), k.arr(Y), k.arr(b)
         _check_clouds(X, a, Y, b)
         h = C.c_void_p()
-        _check(lib().fsk_engine_create(C.c_int(device), C.c_void_p(X.ctypes.data),
-                                       C.c_void_p(a.ctypes.data), C.c_int64(X.shape[0]),
-                                       C.c_void_p(Y.ctypes.data), C.c_void_p(b.ctypes.data),
-                                       C.c_int64(Y.shape[0]), C.c_int64(X.shape[1]),
-                                       C.c_int(self.MODES[mode]), C.byref(h)))
+        if cost is not None:
+            la = k.arr(la, np.int32)
+            lb = k.arr(lb, np.int32)
+            W = k.arr(cost["label_cost"])
+            _check(lib().fsk_engine_create_labeled(
+                C.c_int(device), C.c_void_p(X.ctypes.data), C.c_void_p(a.ctypes.data),
+                C.c_void_p(la.ctypes.data), C.c_int64(X.shape[0]), C.c_void_p(Y.ctypes.data),
+                C.c_void_p(b.ctypes.data), C.c_void_p(lb.ctypes.data), C.c_int64(Y.shape[0]),
+                C.c_int64(X.shape[1]), C.c_double(cost["lambda1"]), C.c_double(cost["lambda2"]),
+                C.c_void_p(W.ctypes.data), C.c_int64(W.shape[0]), C.c_int(self.MODES[mode]),
+                C.byref(h)))
+        else:
+            _check(lib().fsk_engine_create(C.c_int(device), C.c_void_p(X.ctypes.data),
+                                           C.c_void_p(a.ctypes.data), C.c_int64(X.shape[0]),
+                                           C.c_void_p(Y.ctypes.data), C.c_void_p(b.ctypes.data),
+                                           C.c_int64(Y.shape[0]), C.c_int64(X.shape[1]),
+                                           C.c_int(self.MODES[mode]), C.byref(h)))
         self.h = h
         self.n, self.m, self.d = X.shape[0], Y.shape[0], X.shape[1]
 

@@ -335,6 +335,21 @@ void grad_rows_fp64(const DevProblem<float>& P, const float* f, const float* g, 
     };
     widen(Pd.src, P.src);
     widen(Pd.tgt, P.tgt);
+    if (P.labeled) {
+        // label-augmented cost: labels and the V x V table as they are
+        Pd.labeled = true;
+        Pd.lambda2 = P.lambda2;
+        Pd.wdim = P.wdim;
+        Pd.wtab.alloc(size_t(P.wdim * P.wdim), s);
+        FSKB_CUDA(cudaMemcpyAsync(Pd.wtab.get(), P.wtab.get(),
+                                  size_t(P.wdim * P.wdim) * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, s));
+        for (auto [o, i] : {std::pair{&Pd.src, &P.src}, std::pair{&Pd.tgt, &P.tgt}}) {
+            o->lab.alloc(size_t(i->n), s);
+            FSKB_CUDA(cudaMemcpyAsync(o->lab.get(), i->lab.get(), size_t(i->n) * sizeof(int32_t),
+                                      cudaMemcpyDeviceToDevice, s));
+        }
+    }
     DevBuf<double> fd(size_t(n), s), gd(size_t(m), s), lse(size_t(n), s), mx(size_t(n), s);
     launch_f32_to_f64(f, fd.get(), n, s);
     launch_f32_to_f64(g, gd.get(), m, s);

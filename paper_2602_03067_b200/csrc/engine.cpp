@@ -128,6 +128,30 @@ int fsk_engine_create(int device, const double* X, const double* a, int64_t n, c
     });
 }
 
+int fsk_engine_create_labeled(int device, const double* X, const double* a, const int32_t* la,
+                              int64_t n, const double* Y, const double* b, const int32_t* lb,
+                              int64_t m, int64_t d, double lambda1, double lambda2,
+                              const double* label_cost, int64_t num_labels, int mode,
+                              fsk_engine** out) {
+    return eguard([&] {
+        fsk_measure src{X, a, la, n, d}, tgt{Y, b, lb, m, d};
+        fsk_cost cost{1, lambda1, lambda2, label_cost, num_labels};
+        validate_problem_raw(src, tgt, &cost);
+        FSKB_CUDA(cudaSetDevice(device));
+        configure_device_pool(device);
+        auto* e = new fsk_engine();
+        e->device = device;
+        FSKB_CUDA(cudaStreamCreateWithFlags(&e->own, cudaStreamNonBlocking));
+        FSKB_CUDA(cudaEventCreateWithFlags(&e->fence, cudaEventDisableTiming));
+        FSKB_CUDA(cudaMalloc(reinterpret_cast<void**>(&e->flags), 2 * sizeof(int)));
+        FSKB_CUDA(cudaMemset(e->flags, 0, 2 * sizeof(int)));
+        e->P.upload(src, tgt, &cost, e->own);
+        enable_tensor_path(e->P, mode);
+        FSKB_CUDA(cudaStreamSynchronize(e->own));
+        *out = e;
+    });
+}
+
 void fsk_engine_destroy(fsk_engine* e) {
     if (!e) return;
     cudaSetDevice(e->device);
@@ -175,8 +199,10 @@ int fsk_engine_init_potentials(fsk_engine* e, void* stream) {
     return eguard([&] {
         cudaStream_t s = pick(e, stream);
         Fence fence_{e, s};
-        launch_neg_sqnorm<float>(e->P.src.pts.get(), e->P.src.n, e->P.src.d, 1.0f, e->f, s);
-        launch_neg_sqnorm<float>(e->P.tgt.pts.get(), e->P.tgt.n, e->P.tgt.d, 1.0f, e->g, s);
+        // f_hat = -s |x|^2, g_hat = -s |y|^2 (solver.cpp:27-32; s = lambda1 for labels)
+        const float fs = float(e->P.fscale);
+        launch_neg_sqnorm<float>(e->P.src.pts.get(), e->P.src.n, e->P.src.d, fs, e->f, s);
+        launch_neg_sqnorm<float>(e->P.tgt.pts.get(), e->P.tgt.n, e->P.tgt.d, fs, e->g, s);
     });
 }
 

@@ -55,6 +55,10 @@ constexpr int NUM_WARPS = 10;
 constexpr int NUM_THREADS = NUM_WARPS * 32;
 constexpr uint32_t VBUF = 8 * TILE * 4;                        // per epilogue warp: 128 floats
 constexpr uint32_t SBITS = 4096;                               // screened: live-tile bitmask
+// label-augmented cost: V x V table (V <= kMaxLabels) and per-warp key-label buffers
+constexpr int kMaxLabels = 64;
+constexpr uint32_t LAB_TABLE = kMaxLabels * kMaxLabels * 4;    // 16 KB
+constexpr uint32_t LAB_BUF = 8 * 64 * 4;                       // per epilogue warp: 64 labels
 constexpr int kMaxScreenTiles = int(SBITS * 4);  // one mask per query tile of the unit
 constexpr int SWORDS = int(SBITS / 8);             // words per query tile's mask
 // chunked layout (d > 64): stage = Q chunk of 2 query tiles + key chunk + bias
@@ -62,7 +66,8 @@ constexpr int CSTAGES = 2;
 constexpr uint32_t CSTAGE = 3 * QTILE + BIAS;                  // 100 KB
 constexpr uint32_t C_OFF_ONES = CSTAGES * CSTAGE;              // 200 KB
 constexpr uint32_t C_OFF_BAR = C_OFF_ONES + BIAS;              // 204 KB
-constexpr uint32_t C_SMEM_BYTES = C_OFF_BAR + 256 + VBUF + 1024;
+constexpr uint32_t C_OFF_LAB = C_OFF_BAR + 256 + VBUF;          // label table (labeled only)
+constexpr uint32_t C_SMEM_BYTES = C_OFF_LAB + LAB_TABLE + 1024;
 // Terms below 2^-kSkipLog2 of a row's running max are provably negligible: even
 // all m <= 2^32 of them add < 2^(32 - kSkipLog2) relative to the row sum (>= 1),
 // below half an fp32 ulp (2^-25) for kSkipLog2 >= 57 (58: 2^-26). Tiles / blocks
@@ -118,6 +123,40 @@ __device__ __forceinline__ float group_max32(const uint32_t (&v)[W], int c) {
     return fmax3(m0, m1, fmaxf(__uint_as_float(v[b + 30]), __uint_as_float(v[b + 31])));
 }
 
+// Label-augmented cost on the tensor path (chunked K1 and the general transport
+// kernel): labels of the query and key rows, the V x V table in log2 units
+// (lambda2 log2(e) W / eps; row = query label when !trans, else key label).
+struct LabelArgs {
+    const int32_t* qlab = nullptr;
+    const int32_t* klab = nullptr;
+    const float* wl2 = nullptr;
+    int nlab = 0;     // V (0: squared Euclidean)
+    int trans = 0;    // g-side passes read W^T
+};
+
+// stage the table in shared memory in query-label-major order, in accumulator units
+__device__ __forceinline__ void stage_label_table(const LabelArgs& L, float inv_acc, float* dst) {
+    const int V = L.nlab;
+    for (int e = threadIdx.x; e < V * V; e += blockDim.x) {
+        const int a = e / V, b = e - a * V;
+        dst[e] = (L.trans ? L.wl2[b * V + a] : L.wl2[e]) * inv_acc;
+    }
+}
+
+// v[j] -= W[l_row, l_key(kbase + j)] for the W columns of this thread's row; the warp
+// loads the key labels into its buffer first (keys past key_valid keep -inf)
+template <int W>
+__device__ __forceinline__ void apply_label_cost(uint32_t (&v)[W], const LabelArgs& L,
+                                                 const float* wrow, int64_t kbase,
+                                                 int64_t key_valid, int* kbuf, int lane) {
+    for (int j = lane; j < W; j += 32)
+        kbuf[j] = kbase + j < key_valid ? L.klab[kbase + j] : 0;
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < W; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) - wrow[kbuf[j]]);
+    __syncwarp();
+}
+
 struct TcParams {
     const uint8_t* qimg;    // query tile images (hi+lo per 128-row tile)
     const uint8_t* kimg;    // key tile images (hi+lo per 128-key tile)
@@ -166,6 +205,9 @@ struct TcParams {
     // fp32, row-major; slot < 0: not stored)
     float* plan_out;
     const int* plan_slot;
+    // label-augmented cost (stream.cpp:73-77): t_ij -= lambda2 log2(e) W[l_i, l_j] / eps,
+    // applied in the epilogue from a shared-memory copy of the V x V table
+    LabelArgs lab;
 };
 
 // Work items run split-major: the CTAs running at the same time share one key
@@ -329,6 +371,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     fill_ones_chunk(sbase + C_OFF_ONES, threadIdx.x, NUM_THREADS);
+    float* lab_table = reinterpret_cast<float*>(sbase + C_OFF_LAB);
+    if (p.lab.nlab) stage_label_table(p.lab, 1.0f / p.acc_scale, lab_table);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (threadIdx.x == 0) {
         for (int s = 0; s < CSTAGES; ++s) {
@@ -437,6 +481,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
                 nlh = live ? -p.l2h[row] : -3.0e38f;
                 nll = live ? -p.l2l[row] : 0.0f;
             }
+            const float* lab_row =
+                p.lab.nlab ? lab_table + (t < nq && row < p.R ? p.lab.qlab[row] : 0) * p.lab.nlab
+                           : nullptr;
             for (int kt = nxt(unit, kt0, kt1); kt < kt1; kt = nxt(unit, kt + 1, kt1), ++acc_it) {
                 mbar_wait(accfull, acc_it & 1);
                 fence_after();
@@ -459,6 +506,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
                 __syncwarp();
                 if (lane == 0) mbar_arrive(accempty);
                 if (t >= nq) continue;
+                if (lab_row)
+                    apply_label_cost<128>(v, p.lab, lab_row, int64_t(kt) * TILE, p.key_valid,
+                                          reinterpret_cast<int*>(vb), lane);
                 if (VEC && p.plan_out) {
                     const int slot = p.plan_slot[size_t(unit) * p.k_tiles + kt];
                     if (slot >= 0) {
@@ -1278,7 +1328,8 @@ constexpr int G_SLOTS_MAX = 6;
 constexpr uint32_t G_OFF_BIAS = G_SLOTS_MAX * QTILE;            // 192 KB: 2 x 4 KB bias ring
 constexpr uint32_t G_OFF_ONES = G_OFF_BIAS + 2 * BIAS;          // 200 KB
 constexpr uint32_t G_OFF_BAR = G_OFF_ONES + BIAS;               // 204 KB
-constexpr uint32_t G_SMEM_BYTES = G_OFF_BAR + 256 + 1024;
+constexpr uint32_t G_OFF_LAB = G_OFF_BAR + 256;                 // label table + key-label buffers
+constexpr uint32_t G_SMEM_BYTES = G_OFF_LAB + LAB_TABLE + LAB_BUF + 1024;
 constexpr uint32_t G_OCOL = 2 * TILE;                            // O at column 256
 constexpr uint32_t G_WCOL = 3 * TILE;                            // W at column 384
 
@@ -1306,6 +1357,7 @@ struct TcApplyGenParams {
     // [unit][split][t][in_kwords]; the key tile is loaded if either tile is live and
     // only the live tiles' MMAs are issued
     int live_tq;
+    LabelArgs lab;           // label-augmented cost (see TcParams)
 };
 
 __device__ __forceinline__ int gen_next_live(const TcApplyGenParams& p, int u, int kt, int kt1) {
@@ -1361,6 +1413,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     fill_ones_chunk(sbase + G_OFF_ONES, threadIdx.x, NUM_THREADS);
+    float* lab_table = reinterpret_cast<float*>(sbase + G_OFF_LAB);
+    if (p.lab.nlab) stage_label_table(p.lab, 1.0f / p.acc_scale, lab_table);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (threadIdx.x == 0) {
         for (int s = 0; s < G_SLOTS_MAX; ++s) {
@@ -1501,6 +1555,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
             const bool live = row < p.R;
             const float nlh = live ? -p.l2h[row] : -3.0e38f;
             const float c2 = live ? kPScaleLog2 - p.l2l[row] : 0.0f;
+            const float* lab_row =
+                p.lab.nlab ? lab_table + (live ? p.lab.qlab[row] : 0) * p.lab.nlab : nullptr;
+            int* lab_buf = reinterpret_cast<int*>(sbase + G_OFF_LAB + LAB_TABLE) + (warp - 2) * 64;
             bool any_tile = false;
             for (int kt = gen_next_live(p, unit, kt0, kt1); kt < kt1;
                  kt = gen_next_live(p, unit, kt + 1, kt1), ++vt) {
@@ -1526,6 +1583,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_apply_gen_kernel(const TcAp
                     for (int j = 0; j < 64; ++j)
                         if (kbase + j >= p.key_valid) v[j] = __float_as_uint(-3.0e38f);
                 }
+                if (lab_row) apply_label_cost<64>(v, p.lab, lab_row, kbase, p.key_valid, lab_buf, lane);
                 uint32_t hi[32], lo[32];
                 if (had) {
                     // P~ (x) W: W read in two 32-column pieces to bound the registers
@@ -1833,6 +1891,12 @@ __global__ void warm_lambda_kernel(const int* __restrict__ argtile, const int* _
     }
 }
 
+__global__ void scale_table_kernel(const double* __restrict__ w, int n, double s,
+                                   float* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = float(w[i] * s);
+}
+
 __global__ void fill_int_kernel(int* __restrict__ p, int64_t n, int v) {
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x)
@@ -2051,6 +2115,11 @@ struct TcHalfStep::Impl {
     unsigned long long warm_blocks = 0;
     // LSE passes by kind: screened cold, warm-bound, plain (unscreened, untracked)
     unsigned long long n_pass[3] = {0, 0, 0};
+    // label-augmented cost: the chunked / general kernels apply lambda2 W / eps in
+    // their epilogues (the d <= 64 fast kernels, warm bounds and screen are off)
+    bool labeled = false;
+    int nlab = 0;
+    DevBuf<float> wl2;   // lambda2 log2(e) W / eps, V x V
     int probe_dev = -1;
     ~Impl() {
         if (h_live) release_probe_bufs(probe_dev, h_live, ev);
@@ -2144,6 +2213,8 @@ TcHalfStep::TcHalfStep(DevProblem<float>& P) : impl_(new Impl()) {
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, int(G_SMEM_BYTES)));
     const DevSide<float>* sides[2] = {&P.src, &P.tgt};
     impl_->chunks = int((P.src.d + DPAD - 1) / DPAD);
+    impl_->labeled = P.labeled;
+    impl_->nlab = P.labeled ? int(P.wdim) : 0;
     for (int c = 0; c < 2; ++c) {
         const DevSide<float>& sd = *sides[c];
         impl_->npts[c] = sd.n;
@@ -2175,7 +2246,15 @@ void TcHalfStep::set_eps(DevProblem<float>& P, double eps) {
     // (FSK_SCREEN_SLACK overrides, default 2)
     // adaptive (kScreenMaxLive), FSK_SCREEN=0 disables it
     const char* env = std::getenv("FSK_SCREEN");
-    const bool screen_on = !(env && env[0] == '0') && impl_->chunks == 1;
+    const bool screen_on = !(env && env[0] == '0') && impl_->chunks == 1 && !impl_->labeled;
+    if (impl_->labeled) {
+        const int V2 = impl_->nlab * impl_->nlab;
+        if (impl_->wl2.size() < size_t(V2)) impl_->wl2.alloc(size_t(V2), P.s);
+        scale_table_kernel<<<unsigned((V2 + 255) / 256), 256, 0, P.s>>>(
+            P.wtab.get(), V2, P.lambda2 / eps * 1.4426950408889634074, impl_->wl2.get());
+        FSKB_CUDA(cudaGetLastError());
+        count_launch();
+    }
     for (int side = 0; side < 2; ++side) {
         const double delta = std::ldexp(1.0, -10) * 1.001 * double(impl_->rownorm[side]) *
                              double(impl_->rownorm[1 - side]) * c;
@@ -2223,7 +2302,8 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
     const int k_tiles = int(I.rows_pad[kc] / TILE);
     // warm bounds: LSE passes of the d <= 64 kernel (FSK_WARM=0 disables)
     const char* wenv = std::getenv("FSK_WARM");
-    bool warm_track = !vec && I.chunks == 1 && !break_lse_flag() && !(wenv && wenv[0] == '0');
+    bool warm_track = !vec && I.chunks == 1 && !I.labeled && !break_lse_flag() &&
+                      !(wenv && wenv[0] == '0');
     // small problems: the bookkeeping would not pay (and the probe read-back waits)
     const int64_t q_units = ((row_end + TILE - 1) / TILE - row_begin / TILE + 1) / 2;
     if (q_units * (I.rows_pad[kc] / TILE) < (int64_t(1) << 16)) warm_track = false;
@@ -2304,8 +2384,8 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
     int grid = std::min(p.items, sms);
     int kps = (k_tiles + p.splits - 1) / p.splits;
     p.screen_thr = I.screen_thr[side];
-    bool screen = !vec && I.chunks == 1 && p.screen_thr > 0.0f && kps <= kMaxScreenTiles &&
-                  !p.break_lse;
+    bool screen = !vec && I.chunks == 1 && !I.labeled && p.screen_thr > 0.0f &&
+                  kps <= kMaxScreenTiles && !p.break_lse;
     bool can_screen = screen;
     bool cold_screen = false;
     if (warm_track) {
@@ -2450,7 +2530,14 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         p.plan_slot = ex->plan_slot;
     }
     if (!vec) ++I.n_pass[screen ? 0 : (p.live_in && p.live_tq) ? 1 : 2];
-    if (I.chunks == 1) {
+    if (I.labeled) {
+        p.lab.qlab = (side == 0 ? P.src : P.tgt).lab.get();
+        p.lab.klab = ks.lab.get();
+        p.lab.wl2 = I.wl2.get();
+        p.lab.nlab = I.nlab;
+        p.lab.trans = side;
+    }
+    if (I.chunks == 1 && !I.labeled) {
         if (vec)
             tc_lse_tq_kernel<true, false><<<grid, NUM_THREADS, TQ_SMEM_BYTES, P.s>>>(p);
         else if (screen)
@@ -2825,6 +2912,13 @@ void TcHalfStep::apply_mat(DevProblem<float>& P, int side, const float* kpot, fl
         g.in_kps = I.live_kps[side];
         g.in_kwords = I.live_kwords[side];
     }
+    if (I.labeled) {
+        g.lab.qlab = qs.lab.get();
+        g.lab.klab = ks.lab.get();
+        g.lab.wl2 = I.wl2.get();
+        g.lab.nlab = I.nlab;
+        g.lab.trans = side;
+    }
     const int vc_max = A ? 2 : 4;
     DevBuf<float> part(size_t(g.splits) * size_t(R) * vc_max * DPAD, P.s);
     g.part_o = part.get();
@@ -2850,8 +2944,9 @@ void TcHalfStep::grad(DevProblem<float>& P, int side, const float* kpot, const f
                       const float* pre_l2h, const float* pre_l2l, const float* pre_r) {
     if (row_end <= row_begin) return;
     Impl& I = *impl_;
-    if (I.chunks != 1) {
-        // d > 64: P V with V = the key cloud through the general apply kernel (all
+    if (I.chunks != 1 || I.labeled) {
+        // d > 64 (or a labeled cost): P V with V = the key cloud through the general
+        // apply kernel (all
         // rows), then G = 2 (diag(r) X - P Y) on the requested rows
         const DevSide<float>& qs = side == 0 ? P.src : P.tgt;
         const DevSide<float>& ks = side == 0 ? P.tgt : P.src;
@@ -2952,7 +3047,7 @@ void TcHalfStep::grad(DevProblem<float>& P, int side, const float* kpot, const f
 }
 
 bool enable_tensor_path(DevProblem<float>& P, int mode) {
-    if (mode == 1 || P.labeled) return false;
+    if (mode == 1 || (P.labeled && P.wdim > kMaxLabels)) return false;
     const int64_t d = P.src.d;
     const bool shape_ok = TcHalfStep::supported(d);
     if (mode == 2 && !shape_ok) throw ValidationFailure("tensor path supports 1 <= d <= 4096");

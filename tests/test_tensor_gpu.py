@@ -769,3 +769,81 @@ def test_persistent_small_solve(fsk, port, golden):
     torch.cuda.synchronize()
     assert contract(f2.cpu().numpy(), f.cpu().numpy().astype(np.float64)) <= 1e-6
     eng.close()
+
+
+def _labeled_engine_half_steps(fsk, X, a, Y, b, g0, eps, cost, la, lb, mode):
+    torch = pytest.importorskip("torch")
+    n, m = len(X), len(Y)
+    eng = fsk.Engine(0, X, a, Y, b, mode=mode, cost=cost, la=la, lb=lb)
+    eng.set_eps(eps)
+    f = torch.zeros(n, dtype=torch.float32, device="cuda")
+    g = torch.tensor(g0, dtype=torch.float32, device="cuda")
+    eng.bind(f.data_ptr(), g.data_ptr())
+    eng.half_step(0, 0, n)
+    torch.cuda.synchronize()
+    fo = f.cpu().numpy().astype(np.float64)
+    eng.half_step(1, 0, m)
+    torch.cuda.synchronize()
+    go = g.cpu().numpy().astype(np.float64)
+    G = torch.empty((n, X.shape[1]), dtype=torch.float32, device="cuda")
+    eng.grad(0, n, G.data_ptr())
+    torch.cuda.synchronize()
+    path = eng.path
+    eng.close()
+    return fo, go, G.cpu().numpy().astype(np.float64), path
+
+
+@pytest.mark.parametrize("mode", ["tensor", "fma"])
+def test_label_augmented_golden_fp32(fsk, golden, port, mode):
+    """f1: the label-augmented cost (stream.cpp:73-77) on the fp32 engine - the tensor
+    path applies lambda2 W / eps in the chunked kernels' epilogues - against the
+    reference golden f-update (lab_*) at the fp32 contract."""
+    G = golden
+    cost = dict(lambda1=0.5, lambda2=0.5, label_cost=G["lab_W"])
+    fo, go, _, path = _labeled_engine_half_steps(fsk, G["lab_X"], G["lab_a"], G["lab_Y"],
+                                                 G["lab_b"], G["lab_g"], 0.25, cost, G["lab_la"],
+                                                 G["lab_lb"], mode)
+    assert path.startswith("tcgen05" if mode == "tensor" else "fma")
+    assert contract(fo, G["lab_out"]) <= 1e-5
+    want_g = port.update_g_hat(G["lab_X"], G["lab_a"], G["lab_Y"], G["lab_b"], fo, 0.25,
+                               cost=cost, la=G["lab_la"], lb=G["lab_lb"])
+    assert contract(go, want_g) <= 1e-5
+
+
+@pytest.mark.parametrize("n,m,d,V", [(600, 520, 784, 10), (700, 333, 64, 5), (300, 257, 100, 64)])
+def test_label_augmented_tensor_path_vs_oracle(fsk, port, n, m, d, V):
+    """Labelled OTDD-style problems (d = 784 as cfg5, 10 classes; ragged shapes; V = 64,
+    the table limit) on the tensor path: both half-steps against the port (fp32
+    contract) and the gradient rows against the SPEC composition on the port's
+    labelled transport (the stated tensor-mode gradient bound)."""
+    from oracle import compose
+    rng = np.random.default_rng(n + V)
+    X = rng.normal(size=(n, d)) * 0.1
+    Y = rng.normal(size=(m, d)) * 0.1 + 0.01
+    a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+    la, lb = rng.integers(0, V, n), rng.integers(0, V, m)
+    W = rng.random((V, V)) * 2.0
+    cost = dict(lambda1=0.8, lambda2=0.6, label_cost=W)
+    eps = 0.5
+    g0 = -0.8 * (Y ** 2).sum(1)
+    fo, go, Gg, path = _labeled_engine_half_steps(fsk, X, a, Y, b, g0, eps, cost, la, lb, "tensor")
+    assert path.startswith("tcgen05")
+    fw = port.update_f_hat(X, a, Y, b, g0, eps, cost=cost, la=la, lb=lb)
+    assert contract(fo, fw) <= 1e-5
+    gw = port.update_g_hat(X, a, Y, b, fo, eps, cost=cost, la=la, lb=lb)
+    assert contract(go, gw) <= 1e-5
+    # gradient at the engine's potentials (fo, go): SPEC grad_source, G = 2 (diag(r) X - P Y)
+    # (SPEC.md:393-401, the convention of fsk_grad_source for every cost)
+    f64, g64 = fo, go
+
+    class LabOps:
+        def __getattr__(self, name):
+            fn = getattr(port, name)
+            return lambda *args, **kw: fn(*args, cost=cost, la=la, lb=lb, **kw)
+
+    ws = compose.Workspace(LabOps(), X, a, Y, b, f64, g64, eps)
+    G64 = compose.grad_source(ws)
+    err = np.abs(Gg - G64).max() / np.abs(G64).max()
+    print(f"labelled n={n} m={m} d={d} V={V}: f {contract(fo, fw):.2e} g {contract(go, gw):.2e} "
+          f"grad {err:.2e}")
+    assert err <= 1e-4
