@@ -162,8 +162,7 @@ void fsk_engine_destroy(fsk_engine* e) {
     {
         DevBufTeardown td;
         e->P.tc.reset();
-        e->P.src = DevSide<float>();
-        e->P.tgt = DevSide<float>();
+        e->P = DevProblem<float>();   // clouds, labels, label table (on e->own)
         e->eps_sched.release();
         e->prep = fsk_engine::Prep();
     }
