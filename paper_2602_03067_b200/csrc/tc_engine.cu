@@ -68,10 +68,11 @@ constexpr uint32_t C_OFF_ONES = CSTAGES * CSTAGE;              // 200 KB
 constexpr uint32_t C_OFF_BAR = C_OFF_ONES + BIAS;              // 204 KB
 constexpr uint32_t C_OFF_LAB = C_OFF_BAR + 256 + VBUF;          // label table (labeled only)
 constexpr uint32_t C_SMEM_BYTES = C_OFF_LAB + LAB_TABLE + 1024;
-// Terms below 2^-kSkipLog2 of a row's running max are provably negligible: even
-// all m <= 2^32 of them add < 2^(32 - kSkipLog2) relative to the row sum (>= 1),
-// below half an fp32 ulp (2^-25) for kSkipLog2 >= 57 (58: 2^-26). Tiles / blocks
-// entirely below it are skipped (64 measured 4% slower on cfg3).
+// Terms below 2^-T of a row's running max are provably negligible: all m of them
+// add < m 2^-T relative to the row sum (>= 1). T = 26 + ceil(log2 m) keeps that
+// below 2^-26, under half an fp32 ulp, for the pass's own key count m (46 at
+// m = 2^20); kSkipLog2 = 58 is the m <= 2^32 cap. Tiles / blocks entirely below
+// 2^-T are skipped (TcParams::skip; FSK_SKIP_LOG2 overrides).
 #ifndef FSKB_SKIP_LOG2
 #define FSKB_SKIP_LOG2 58.0f
 #endif
@@ -131,7 +132,7 @@ struct LabelArgs {
     const int32_t* klab = nullptr;
     const float* wl2 = nullptr;
     int nlab = 0;     // V (0: squared Euclidean)
-    int trans = 0;    // g-side passes read W^T
+    int trans = 0;    // 1: read W^T (unused: the reference never transposes W)
 };
 
 // stage the table in shared memory in query-label-major order, in accumulator units
@@ -181,6 +182,7 @@ struct TcParams {
     // screened LSE (SCREEN): tiles whose approximate (hi x hi + bias) max is below
     // the running approximate row max - screen_thr for every row are not scored
     float screen_thr;
+    float skip;                  // T: terms below 2^-T of the row max are dropped
     unsigned long long* live_count;  // += live key tiles (diagnostics), nullable
     uint32_t* live_global;       // LSE passes: per item, the key tiles not proven negligible
     int kwords;                  //   (kwords words per item; bit kt - kt0)
@@ -267,7 +269,7 @@ __device__ __forceinline__ bool k1_tile_update(uint32_t (&v)[W], int64_t kbase, 
         for (int j = 0; j < W; ++j)
             if (kbase + j >= p.key_valid) v[j] = __float_as_uint(-INFINITY);
     }
-    // per 32-column group maxima: a group whose terms are all < 2^-kSkipLog2 of the
+    // per 32-column group maxima: a group whose terms are all < 2^-T of the
     // reference for every row of the warp skips its exponentials (same bound as
     // the whole-tile skip); live blocks of a warm pass mostly hold a few near keys
     constexpr int G = W / 32;
@@ -279,9 +281,9 @@ __device__ __forceinline__ bool k1_tile_update(uint32_t (&v)[W], int64_t kbase, 
     for (int c = 1; c < G; ++c) umax = fmaxf(umax, gmax[c]);
     umax_out = umax;
     if constexpr (VEC) {
-        // P~ = 2^(t - L) <= 1; a tile whose P~ are all < 2^-kSkipLog2 for the warp's rows
-        // adds < m 2^-kSkipLog2 max|v| - below the fp32 result's rounding
-        if (__all_sync(0xffffffffu, umax + nlh < -kSkipLog2)) return false;
+        // P~ = 2^(t - L) <= 1; a tile whose P~ are all < 2^-T for the warp's rows
+        // adds < m 2^-T max|v| <= 2^-26 max|v| - below the fp32 result's rounding
+        if (__all_sync(0xffffffffu, umax + nlh < -p.skip)) return false;
         // the tile's W values of v, broadcast through a per-warp buffer
         if constexpr (W == 128) {
             float4 vv = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -305,7 +307,7 @@ __device__ __forceinline__ bool k1_tile_update(uint32_t (&v)[W], int64_t kbase, 
         float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
         for (int c = 0; c < G; ++c) {
-            if (__all_sync(0xffffffffu, gmax[c] + nlh < -kSkipLog2)) continue;
+            if (__all_sync(0xffffffffu, gmax[c] + nlh < -p.skip)) continue;
 #pragma unroll
             for (int j = 32 * c; j < 32 * c + 32; j += 4) {
                 const float4 w = reinterpret_cast<const float4*>(vb)[j >> 2];
@@ -324,15 +326,15 @@ __device__ __forceinline__ bool k1_tile_update(uint32_t (&v)[W], int64_t kbase, 
             if (S != 0.0) S *= double(ex2(p.break_lse ? umax - M : M - umax));
             M = umax;
         }
-        // every term of this tile is < 2^-kSkipLog2 of the running max for all 32 rows of
-        // the warp: the whole tile adds < m 2^-kSkipLog2 relative - below rounding
+        // every term of this tile is < 2^-T of the running max for all 32 rows of
+        // the warp: the whole tile adds < m 2^-T <= 2^-26 relative - below rounding
         const bool dead = M == -INFINITY;
-        if (__all_sync(0xffffffffu, dead || umax < M - kSkipLog2)) return false;
+        if (__all_sync(0xffffffffu, dead || umax < M - p.skip)) return false;
         const float nm = dead ? 0.0f : -M;
         float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
         for (int c = 0; c < G; ++c) {
-            if (!p.break_lse && __all_sync(0xffffffffu, dead || gmax[c] < M - kSkipLog2))
+            if (!p.break_lse && __all_sync(0xffffffffu, dead || gmax[c] < M - p.skip))
                 continue;
 #pragma unroll
             for (int j = 32 * c; j < 32 * c + 32; j += 4) {
@@ -883,7 +885,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
             if constexpr (SCREEN) {
                 // screened running max; a seeded row (m_init <= true max) starts at
                 // m_init - (delta + slack), a lower bound of its screened max
-                float Ma = M > -INFINITY ? M - 0.5f * (p.screen_thr - kSkipLog2) : -INFINITY;
+                float Ma = M > -INFINITY ? M - 0.5f * (p.screen_thr - p.skip) : -INFINITY;
                 const bool row_ok = t < nq && row < p.R;
                 for (int kt = kt0; kt < kt1; ++kt) {
                     if (t < nq) {
@@ -915,7 +917,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                                      1u << ((kt - kt0) & 31));
                         if (p.gap) {
                             // warm-bound seed: true gap <= screened gap + 2 delta + slack
-                            const float gv = row_ok ? tmax - Ma + (p.screen_thr - kSkipLog2)
+                            const float gv = row_ok ? tmax - Ma + (p.screen_thr - p.skip)
                                                     : -INFINITY;
                             const int gmax = __reduce_max_sync(0xffffffffu, fenc(gv));
                             if (lane == 0)
@@ -926,7 +928,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 // the split's true max is >= the screened max - (delta + slack):
                 // seed the running max there (earlier in-epilogue skips)
                 if (!VEC && row_ok && Ma > -INFINITY)
-                    M = fmaxf(M, Ma - 0.5f * (p.screen_thr - kSkipLog2) - 1.0f);
+                    M = fmaxf(M, Ma - 0.5f * (p.screen_thr - p.skip) - 1.0f);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(screen_done);
                 mbar_wait(screen_done, lu & 1);
@@ -1905,13 +1907,13 @@ __global__ void fill_int_kernel(int* __restrict__ p, int64_t n, int v) {
 
 // Propagate the per-(query tile, key tile) gap bounds E = max_i (tilemax_i - M_i)
 // to the new bias: E' = E + max_tile(db) - lambda_t. Blocks with E' < -(64 + 1)
-// are provably below 2^-kSkipLog2 of every row's max and stay out of the live set
+// are provably below 2^-T of every row's max and stay out of the live set
 // (E <- E'); live blocks get E <- -inf for the pass to re-measure. One thread per
 // bitmask word (u, split, w) of the pass's live_in layout, both query tiles of
 // the unit: live[u][split][t][w].
 __global__ void warm_prepass_kernel(int* __restrict__ gap, const int* __restrict__ tile_dmax,
                                     const int* __restrict__ lam, int units, int k_tiles, int splits,
-                                    int kps, int kwords, uint32_t* __restrict__ live,
+                                    int kps, int kwords, float skip, uint32_t* __restrict__ live,
                                     unsigned long long* __restrict__ live_count) {
     const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t total = int64_t(units) * splits * kwords;
@@ -1929,7 +1931,7 @@ __global__ void warm_prepass_kernel(int* __restrict__ gap, const int* __restrict
                 const int kt = s * kps + w * 32 + b;
                 if (w * 32 + b >= kps || kt >= kt_end) break;
                 const float e = fdec(grow[kt]) + fdec(tile_dmax[kt]) - lt;
-                const bool dead = e < -(kSkipLog2 + 1.0f);   // NaN -> live
+                const bool dead = e < -(skip + 1.0f);   // NaN -> live
                 if (dead) {
                     grow[kt] = fenc(e);
                 } else {
@@ -1994,6 +1996,17 @@ float device_absmax(const float* x, int64_t n, cudaStream_t s) {
     float f;
     std::memcpy(&f, &h, 4);
     return f;
+}
+
+// T = 26 + ceil(log2 m) (<= kSkipLog2): m terms below 2^-T of the max add < 2^-26
+float skip_log2_for(int64_t m) {
+    static const double env = [] {
+        const char* e = std::getenv("FSK_SKIP_LOG2");
+        return e ? std::atof(e) : 0.0;
+    }();
+    if (env > 0.0) return float(env);
+    const double t = 26.0 + std::ceil(std::log2(double(std::max<int64_t>(m, 2))));
+    return float(std::min(t, double(kSkipLog2)));
 }
 
 // exponent e such that max|v| * 2^-e lies in [128, 256)
@@ -2077,6 +2090,7 @@ struct TcHalfStep::Impl {
     int chunks = 1;                 // 64-wide feature chunks (d > 64: chunked kernels)
     float rownorm[2] = {0.f, 0.f};  // max_i ||x_i|| of each cloud
     float screen_thr[2] = {0.f, 0.f};  // per side, log2 units; 0 = no screening
+    float skip[2] = {kSkipLog2, kSkipLog2};  // per side: T for the side's key count
     // adaptive screening, per side: live fraction of the last screened pass (read
     // back asynchronously: counter -> pinned host word -> event, never a host sync)
     DevBuf<unsigned long long> live_count;  // [2] live key tiles of the last pass
@@ -2218,6 +2232,8 @@ TcHalfStep::TcHalfStep(DevProblem<float>& P) : impl_(new Impl()) {
     for (int c = 0; c < 2; ++c) {
         const DevSide<float>& sd = *sides[c];
         impl_->npts[c] = sd.n;
+        // side 0 (f-update) streams the keys of cloud 1, side 1 those of cloud 0
+        impl_->skip[1 - c] = skip_log2_for(sd.n);
         impl_->rows_pad[c] = (sd.n + TILE - 1) / TILE * TILE;
         impl_->maxabs[c] = device_absmax(sd.pts.get(), sd.n * sd.d, P.s);
         impl_->rownorm[c] = device_rownorm_max(sd.pts.get(), sd.n, sd.d, P.s);
@@ -2240,7 +2256,7 @@ void TcHalfStep::set_eps(DevProblem<float>& P, double eps) {
     for (int side = 0; side < 2; ++side) impl_->warm_ok[side] = impl_->b_valid[side] = false;
     const double c = 2.0 * P.fscale / eps * 1.4426950408889634074;
     // screening threshold: |t - t~| <= delta = 2^-10 (1 + 2^-11) ||x|| ||c y|| (the
-    // dropped cross terms, Cauchy-Schwarz) -> thr = kSkipLog2 + 2 delta + slack; the
+    // dropped cross terms, Cauchy-Schwarz) -> thr = T + 2 delta + slack; the
     // fp32 accumulation of the 5 exact fp16 products rounds by < 5 ulp(|t|) ~ 2^-8
     // log2 units at the score magnitudes here, so a slack of 2 is ample
     // (FSK_SCREEN_SLACK overrides, default 2)
@@ -2262,7 +2278,8 @@ void TcHalfStep::set_eps(DevProblem<float>& P, double eps) {
             const char* e = std::getenv("FSK_SCREEN_SLACK");
             return e ? std::atof(e) : 2.0;
         }();
-        impl_->screen_thr[side] = screen_on ? float(double(kSkipLog2) + 2.0 * delta + slack) : 0.0f;
+        impl_->screen_thr[side] =
+            screen_on ? float(double(impl_->skip[side]) + 2.0 * delta + slack) : 0.0f;
     }
     if (!impl_->live_count.get()) {
         impl_->live_count.alloc(2, P.s);
@@ -2384,6 +2401,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
     int grid = std::min(p.items, sms);
     int kps = (k_tiles + p.splits - 1) / p.splits;
     p.screen_thr = I.screen_thr[side];
+    p.skip = I.skip[side];
     bool screen = !vec && I.chunks == 1 && !I.labeled && p.screen_thr > 0.0f &&
                   kps <= kMaxScreenTiles && !p.break_lse;
     bool can_screen = screen;
@@ -2420,7 +2438,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
             FSKB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), P.s));
             warm_prepass_kernel<<<unsigned((words + 255) / 256), 256, 0, P.s>>>(
                 I.gap[side].get(), I.tdmax[side].get(), I.lam[side].get(), units, n_ktiles,
-                p.splits, kps, kw, I.warm_live[side].get(), cnt);
+                p.splits, kps, kw, I.skip[side], I.warm_live[side].get(), cnt);
             FSKB_CUDA(cudaGetLastError());
             count_launch(3);
             // the live fraction decides this pass: wait for it (the stream is drained up
@@ -2535,7 +2553,9 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         p.lab.klab = ks.lab.get();
         p.lab.wl2 = I.wl2.get();
         p.lab.nlab = I.nlab;
-        p.lab.trans = side;
+        // both orientations index W[query label][key label]: the reference's g-side
+        // context takes W as is with the target's labels as rows (stream.cpp:239-242)
+        p.lab.trans = 0;
     }
     if (I.chunks == 1 && !I.labeled) {
         if (vec)
@@ -2917,7 +2937,7 @@ void TcHalfStep::apply_mat(DevProblem<float>& P, int side, const float* kpot, fl
         g.lab.klab = ks.lab.get();
         g.lab.wl2 = I.wl2.get();
         g.lab.nlab = I.nlab;
-        g.lab.trans = side;
+        g.lab.trans = 0;   // W[query label][key label] (stream.cpp:239-242, :354)
     }
     const int vc_max = A ? 2 : 4;
     DevBuf<float> part(size_t(g.splits) * size_t(R) * vc_max * DPAD, P.s);
