@@ -183,6 +183,14 @@ struct TcParams {
     // the running approximate row max - screen_thr for every row are not scored
     float screen_thr;
     float skip;                  // T: terms below 2^-T of the row max are dropped
+    // screen-only launch (SCREEN, cold passes of large problems): phase 1 alone; the
+    // live masks go to live_out in the warm live_in layout of the phase-2 launch
+    // ([unit][out_split][t][out_kwords], out_kps key tiles per split), each row's
+    // seeded running max to minit_out; phase 2 is a warm-pass launch over them
+    int screen_only;
+    uint32_t* live_out;
+    int out_splits, out_kps, out_kwords;
+    float* minit_out;
     unsigned long long* live_count;  // += live key tiles (diagnostics), nullable
     uint32_t* live_global;       // LSE passes: per item, the key tiles not proven negligible
     int kwords;                  //   (kwords words per item; bit kt - kt0)
@@ -708,7 +716,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 __syncwarp();
                 if (lane == 0) mbar_arrive(wbits_ready(b));
             }
-            if (lane == 0) {
+            if (lane == 0) do {   // (do-while: the screen-only exit breaks to the syncwarp)
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
                 if constexpr (SCREEN) {
@@ -721,6 +729,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                         bulk_g2s(dst + QTILE, p.kbias + size_t(kt) * BIAS, BIAS, kfull(s));
                     }
                     mbar_wait(screen_done, lu & 1);
+                    if (p.screen_only) {
+                        mbar_arrive(bits_free);
+                        break;
+                    }
                 }
                 int nlive = 0;
                 int kt = first_kt(unit, kt0, kt1, -1, lu);
@@ -761,7 +773,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                     if (p.live_count)  // (query tile, key tile) blocks, as the warm count
                         atomicAdd(p.live_count, (unsigned long long)nlive);
                 }
-            }
+            } while (0);
             __syncwarp();
         }
     } else if (warp == 1) {
@@ -807,14 +819,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                     ++it;
                     return mask;
                 };
+                bool phase2 = true;
                 if constexpr (SCREEN) {
                     for (int kt = kt0; kt < kt1; ++kt) tile_mmas(true);
                     mbar_wait(screen_done, lu & 1);
+                    phase2 = !p.screen_only;
                 }
                 // the producer walks the live sequence and flags its last stage: no
                 // global loads or divisions on the issue path
-                while (!(tile_mmas(false) & kStageLast)) {
-                }
+                if (phase2)
+                    while (!(tile_mmas(false) & kStageLast)) {
+                    }
                 if constexpr (SCREEN) {
                     __syncwarp();
                     if (lane == 0) mbar_arrive(bits_free);
@@ -937,9 +952,39 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                     for (int w = threadIdx.x - 64; w < p.kwords; w += 256)
                         p.live_global[(size_t(unit) * p.splits + split) * p.kwords + w] =
                             live_word(-1, w);
+                if (p.screen_only) {
+                    // per-tile masks re-cut into the phase-2 launch's key-range splits
+                    // (this launch runs one split: bit kt = key tile kt), live count
+                    const int nw = 2 * p.out_splits * p.out_kwords;
+                    unsigned nl = 0;
+                    for (int e = threadIdx.x - 64; e < nw; e += 256) {
+                        const int tt = e / (p.out_splits * p.out_kwords);
+                        const int r = e - tt * p.out_splits * p.out_kwords;
+                        const int s2 = r / p.out_kwords, w = r - s2 * p.out_kwords;
+                        const int b0 = s2 * p.out_kps + 32 * w;            // first key tile
+                        const int nb = min(32, min(p.out_kps - 32 * w, p.k_tiles - b0));
+                        uint32_t bits = 0;
+                        if (nb > 0 && tt < nq) {
+                            const int wi = b0 >> 5, sh = b0 & 31;
+                            bits = live_bits[tt * SWORDS + wi] >> sh;
+                            if (sh && wi + 1 < SWORDS)
+                                bits |= live_bits[tt * SWORDS + wi + 1] << (32 - sh);
+                            if (nb < 32) bits &= (1u << nb) - 1u;
+                        }
+                        p.live_out[((size_t(unit) * p.out_splits + s2) * 2 + tt) * p.out_kwords +
+                                   w] = bits;
+                        nl += __popc(bits);
+                    }
+                    const unsigned wl = __reduce_add_sync(0xffffffffu, nl);
+                    if (p.live_count && lane == 0 && wl)
+                        atomicAdd(p.live_count, (unsigned long long)wl);
+                    if (t < nq && row >= p.row_begin && row < p.row_end && p.minit_out)
+                        p.minit_out[row] = M;
+                }
             }
             if (staged) mbar_wait(wbits_ready(lu & 1), (lu >> 1) & 1);
-            for (int kt = t < nq ? first_kt(unit, kt0, kt1, t, lu) : kt1, kt_next; kt < kt1;
+            const bool run2 = !SCREEN || !p.screen_only;
+            for (int kt = t < nq && run2 ? first_kt(unit, kt0, kt1, t, lu) : kt1, kt_next; kt < kt1;
                  kt = kt_next) {
                 const float M_old = M;
                 float umax = -INFINITY;
@@ -985,7 +1030,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 for (int i = threadIdx.x - 64; i < int(SBITS / 4); i += 256) live_bits[i] = 0u;
                 asm volatile("bar.sync 1, 256;" ::: "memory");
             }
-            if (t < nq && row >= p.row_begin && row < p.row_end) {
+            if (t < nq && row >= p.row_begin && row < p.row_end && run2) {
                 if constexpr (VEC) {
                     p.part_m[size_t(split) * p.R + row] = S;
                 } else {
@@ -2490,6 +2535,66 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         p.gap = I.gap[side].get();
         p.part_arg = I.part_arg[side].get();
     }
+    // Large cold passes run the screen as two launches: phase 1 alone over the whole
+    // key range (the CTAs stream the key tiles in lockstep, L2-resident), then phase 2
+    // as a warm-pass launch over its per-tile live masks in L2-sized key-range splits
+    // (one launch scattered the phase-2 reads of ~20% live blocks over the whole key
+    // image: ~230 GB of HBM traffic per pass at cfg3)
+    bool two_phase = false;
+    if (cold_screen && screen && !vec && range_split && p.splits == 1 && !(m_init && ex)) {
+        const int s2 = pick_splits(units, k_tiles, sms,
+                                   std::max(base_min_s, int(std::ceil(double(k_tiles) * KSTAGE /
+                                                                       warm_range_bytes()))));
+        const int kps2 = (k_tiles + s2 - 1) / s2;
+        const int kw2 = (kps2 + 31) / 32;
+        two_phase = s2 > 1 && kw2 <= int(SWORDS / 2) && k_tiles <= kMaxScreenTiles;
+        if (two_phase) {
+            const size_t words = size_t(units) * s2 * 2 * kw2;
+            if (I.warm_live[side].size() < words) I.warm_live[side].alloc(words, P.s);
+            if (I.minit[side].size() < size_t(p.R)) I.minit[side].alloc(size_t(p.R), P.s);
+            TcParams p1 = p;
+            p1.screen_only = 1;
+            p1.live_out = I.warm_live[side].get();
+            p1.out_splits = s2;
+            p1.out_kps = kps2;
+            p1.out_kwords = kw2;
+            p1.minit_out = I.minit[side].get();
+            p1.live_global = nullptr;
+            p1.live_count = I.live_count.get() + side;
+            if (I.pending[side]) FSKB_CUDA(cudaEventSynchronize(I.ev[side]));
+            poll_screen(side, kScreenMaxLive);
+            FSKB_CUDA(cudaMemsetAsync(p1.live_count, 0, sizeof(unsigned long long), P.s));
+            tc_lse_tq_kernel<false, true><<<grid, NUM_THREADS, TQ_SMEM_BYTES, P.s>>>(p1);
+            FSKB_CUDA(cudaGetLastError());
+            count_launch();
+            FSKB_CUDA(cudaMemcpyAsync(I.h_live + side, p1.live_count, sizeof(unsigned long long),
+                                      cudaMemcpyDeviceToHost, P.s));
+            FSKB_CUDA(cudaEventRecord(I.ev[side], P.s));
+            I.pending[side] = true;
+            I.pending_screen[side] = true;
+            I.pending_blocks[side] = double(p.q_tiles) * double(k_tiles);
+            // phase 2: a warm pass over the screened masks, seeded with phase 1's maxima
+            screen = false;
+            p.splits = s2;
+            p.items = units * s2;
+            grid = std::min(p.items, sms);
+            kps = kps2;
+            p.live_in = I.warm_live[side].get();
+            p.live_tq = 1;
+            p.in_splits = s2;
+            p.in_kps = kps2;
+            p.in_kwords = kw2;
+            p.m_init = I.minit[side].get();
+            p.live_count = nullptr;
+            pm.alloc(size_t(p.splits) * size_t(p.R), P.s);
+            ps.alloc(size_t(p.splits) * size_t(p.R), P.s);
+            p.part_m = pm.get();
+            p.part_s = ps.get();
+            if (I.part_arg[side].size() < size_t(p.splits) * size_t(p.R))
+                I.part_arg[side].alloc(size_t(p.splits) * size_t(p.R), P.s);
+            p.part_arg = I.part_arg[side].get();
+        }
+    }
     if (screen && !cold_screen) {
         // wait for the previous probe of this side (one pass of pipeline): the decision
         // must not depend on whether an asynchronous read-back has landed, or results
@@ -2535,7 +2640,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         p.in_kps = I.live_kps[side];
         p.in_kwords = I.live_kwords[side];
     }
-    if (m_init && !vec) p.m_init = m_init;
+    if (m_init && !vec && !two_phase) p.m_init = m_init;
     if (ex && ex->live_in) {   // caller-supplied live set (plan materialization)
         p.live_in = ex->live_in;
         p.in_splits = ex->in_splits;
@@ -2547,7 +2652,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         p.plan_out = ex->plan_out;
         p.plan_slot = ex->plan_slot;
     }
-    if (!vec) ++I.n_pass[screen ? 0 : (p.live_in && p.live_tq) ? 1 : 2];
+    if (!vec) ++I.n_pass[screen || two_phase ? 0 : (p.live_in && p.live_tq) ? 1 : 2];
     if (I.labeled) {
         p.lab.qlab = (side == 0 ? P.src : P.tgt).lab.get();
         p.lab.klab = ks.lab.get();
