@@ -546,11 +546,14 @@ def run_b200(args, cfgname):
     tensor = eng.path.startswith("tcgen05")
     chunks = -(-d // 64)
     # block skipping (warm bounds / screen): the kernel scores only the blocks it
-    # cannot prove negligible. Executed fraction over the timed LSE passes: the
-    # live blocks of the passes whose live count was read back, plus every block
-    # of the untracked (cold / plain) passes.
+    # cannot prove negligible, in units of (query tile, 64-key half) - the MMA and
+    # epilogue unit of the d <= 64 kernel. Executed fraction over the timed LSE
+    # passes: the live halves of the passes whose live count was read back, plus
+    # every half of the untracked (plain) passes.
     passes = args.steps * (2 * iters + (1 if STEP_TAIL[cfgname] == "grad" else 0))
     blocks_pass = -(-rows0 // 128) * -(-m // 128)   # (query tile, key tile) blocks
+    if tensor and chunks == 1:
+        blocks_pass *= 2   # 64-key halves
     total_blocks = passes * blocks_pass
     executed = min(1.0, (live + max(0, total_blocks - sblk)) / total_blocks) if total_blocks \
         else 1.0
@@ -593,7 +596,8 @@ def run_b200(args, cfgname):
                      "kernel": kernel + " (+bias/finalize; CUDA events around every f and g "
                                "half-step on the launching stream, mean)",
                      "algorithmic": f"W_dot = 2 n m d per half-step (n_rows={rows0}, m={m}, "
-                                    f"d={d}) x executed block fraction {executed:.3f}",
+                                    f"d={d}) x executed (query tile, 64-key half) block "
+                                    f"fraction {executed:.3f} (screen phase-1 MMAs not counted)",
                      "executed_fraction": executed,
                      "effective_tflops": w_dot / mean_half / 1e12,
                      "peak_source": peak_src,
@@ -605,10 +609,11 @@ def run_b200(args, cfgname):
     }
     if tensor and chunks == 1:
         # block skipping in the LSE passes (warm bounds across passes, or the 5-MMA
-        # screen): of the (query tile pair, key tile) blocks of the passes whose live
+        # screen): of the (query tile, 64-key half) blocks of the passes whose live
         # count was read back, the fraction scored in full; the rest are provably
-        # < 2^-58 of every row's max
-        line["block_skipping"] = {"tracked_blocks": sblk, "live_blocks": live,
+        # < 2^-T of every row's max (T = 26 + ceil(log2 m))
+        line["block_skipping"] = {"unit": "(query tile, 64-key half) blocks",
+                                  "tracked_blocks": sblk, "live_blocks": live,
                                   "live_fraction": live / sblk if sblk else None}
     if args.parity:
         try:

@@ -61,6 +61,9 @@ constexpr uint32_t LAB_TABLE = kMaxLabels * kMaxLabels * 4;    // 16 KB
 constexpr uint32_t LAB_BUF = 8 * 64 * 4;                       // per epilogue warp: 64 labels
 constexpr int kMaxScreenTiles = int(SBITS * 4);  // one mask per query tile of the unit
 constexpr int SWORDS = int(SBITS / 8);             // words per query tile's mask
+// warm live sets (one bit per 64-key half) are staged per item in shared memory:
+// SWORDS / 2 words per query tile and buffer -> at most this many key tiles per split
+constexpr int kMaxWarmKps = int(SWORDS / 2) * 32 / 2;
 // chunked layout (d > 64): stage = Q chunk of 2 query tiles + key chunk + bias
 constexpr int CSTAGES = 2;
 constexpr uint32_t CSTAGE = 3 * QTILE + BIAS;                  // 100 KB
@@ -574,7 +577,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
 // overlaps the epilogue of the other), query operand of tile t at 256 + 72 t:
 // hi (32 columns of fp16 pairs), lo (32), ones (8). The epilogue warps stage the
 // query operand themselves (tcgen05.st from the pre-split image) per work item.
-constexpr uint32_t kStageLast = 4u;  // stage_mask flag: last stage of the work item
+// stage_mask: bit 2 t + h = half h (keys [64 h, 64 h + 64)) of query tile t is live;
+// kStageLast flags the last stage of the work item
+constexpr uint32_t kStageLast = 16u;
 constexpr int TQ_STAGES = 6;
 constexpr uint32_t TQ_OFF_K = 0;
 constexpr uint32_t TQ_OFF_BAR = TQ_OFF_K + TQ_STAGES * KSTAGE;   // 216 KB
@@ -671,17 +676,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
     const bool staged = !VEC && !SCREEN && p.live_in && p.live_tq &&
                         p.in_splits == p.splits && p.in_kps == ktiles_per_split &&
                         p.in_kwords <= kStageW;
+    // Warm live sets (live_tq) hold one bit per 64-key half of a key tile: bit
+    // 2 (kt - kt0) + h of query tile t's words. Only live halves are multiplied and
+    // read back (a live (query tile, key tile) block has ~1.01 live halves at cfg3).
+    if (!VEC && !SCREEN && p.live_in && p.live_tq && !staged) __trap();   // host contract
     auto staged_words = [&](int lu, int t) { return live_bits + ((lu & 1) * 2 + t) * kStageW; };
-    auto next_staged = [&](int kt, int kt0, int kt1, int lu, int t) {
+    // next live half index >= q (< q1), relative to the item's first key tile
+    auto next_sub = [&](int q, int q1, int lu, int t) {
         const uint32_t* w0 = staged_words(lu, t < 0 ? 0 : t);
         const uint32_t* w1 = staged_words(lu, 1);
-        while (kt < kt1) {
-            const int rel = kt - kt0;
-            const uint32_t w = (t < 0 ? (w0[rel >> 5] | w1[rel >> 5]) : w0[rel >> 5]) >> (rel & 31);
-            if (w) return kt + __ffs(w) - 1;
-            kt += 32 - (rel & 31);
+        while (q < q1) {
+            const uint32_t w = (t < 0 ? (w0[q >> 5] | w1[q >> 5]) : w0[q >> 5]) >> (q & 31);
+            if (w) return q + __ffs(w) - 1;
+            q += 32 - (q & 31);
         }
-        return kt1;
+        return q1;
+    };
+    auto next_staged = [&](int kt, int kt0, int kt1, int lu, int t) {
+        return kt0 + (next_sub(2 * (kt - kt0), 2 * (kt1 - kt0), lu, t) >> 1);
     };
     // phase-2 (SCREEN) / VEC-at-fixed-potentials key tile sequence
     // (t >= 0: the sequence of query tile t of the unit; producer / MMA: t = -1)
@@ -747,18 +759,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 for (int kn; kt < kt1; kt = kn, ++it) {
                     const int s = it % TQ_STAGES;
                     kn = next_kt(unit, kt, kt0, kt1, -1, lu);
-                    uint32_t mask = 3u;
+                    uint32_t mask = 15u;
                     if constexpr (SCREEN) {
                         const int rel = kt - kt0;
-                        mask = ((live_bits[rel >> 5] >> (rel & 31)) & 1u) |
-                               (((live_bits[SWORDS + (rel >> 5)] >> (rel & 31)) & 1u) << 1);
+                        mask = (((live_bits[rel >> 5] >> (rel & 31)) & 1u) ? 3u : 0u) |
+                               (((live_bits[SWORDS + (rel >> 5)] >> (rel & 31)) & 1u) ? 12u : 0u);
                     } else if (staged) {
-                        const int rel = kt - kt0;
-                        mask = ((staged_words(lu, 0)[rel >> 5] >> (rel & 31)) & 1u) |
-                               (((staged_words(lu, 1)[rel >> 5] >> (rel & 31)) & 1u) << 1);
-                    } else if (!VEC && p.live_tq) {
-                        mask = uint32_t(live_in_bit(p, unit, 0, kt)) |
-                               (uint32_t(live_in_bit(p, unit, 1, kt)) << 1);
+                        const int r2 = 2 * (kt - kt0);   // even: both halves in one word
+                        mask = ((staged_words(lu, 0)[r2 >> 5] >> (r2 & 31)) & 3u) |
+                               (((staged_words(lu, 1)[r2 >> 5] >> (r2 & 31)) & 3u) << 2);
                     }
                     nlive += __popc(mask);
                     mbar_wait(kempty(s), ((it / TQ_STAGES) & 1) ^ 1);
@@ -782,7 +791,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
         const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
         {
             int it = 0;
-            int acc_n[2] = {0, 0};
+            int acc_n[2][2] = {{0, 0}, {0, 0}};   // per (query tile, half) accumulator uses
             for (int item = blockIdx.x, lu = 0; item < p.items; item += gridDim.x, ++lu) {
                 int unit, split;
                 item_coords(p.items, p.splits, item, unit, split);
@@ -797,14 +806,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                     mbar_wait(kfull(s), (it / TQ_STAGES) & 1);
                     fence_after();
                     const uint32_t kst = base + TQ_OFF_K + s * KSTAGE;
-                    const uint32_t mask = screen_phase ? 3u : stage_mask[s];
+                    const uint32_t mask = screen_phase ? 15u : stage_mask[s];
                     for (int t = 0; t < nq; ++t) {
-                        if (!((mask >> t) & 1u)) continue;
                         const uint32_t q = tm + TQ_QCOL + uint32_t(t) * TQ_QSTRIDE;
-                        // two N = 64 halves: the epilogue drains half 0 while half 1
-                        // computes, and half 0 of the next key tile overlaps half 1
+                        // N = 64 halves, each with its own accumulator: the epilogue
+                        // drains one while the other computes; dead halves are skipped
                         for (int h = 0; h < 2; ++h) {
-                            mbar_wait(accempty(t, h), (acc_n[t] & 1) ^ 1);
+                            if (!((mask >> (2 * t + h)) & 1u)) continue;
+                            mbar_wait(accempty(t, h), (acc_n[t][h] & 1) ^ 1);
                             fence_after();
                             const uint32_t d = tm + uint32_t(t * TILE + h * 64);
                             if (screen_phase)
@@ -812,8 +821,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                             else
                                 issue_score_half_tq<true>(d, q, kst, h);
                             umma_commit<true>(accfull(t, h));
+                            ++acc_n[t][h];
                         }
-                        ++acc_n[t];
                     }
                     umma_commit<true>(kempty(s));
                     ++it;
@@ -845,10 +854,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
         const uint32_t acc_addr = tmem + lane_addr + uint32_t(t * TILE);
         const uint32_t q_addr = tmem + lane_addr + TQ_QCOL + uint32_t(t) * TQ_QSTRIDE;
         float* vb = reinterpret_cast<float*>(sbase + TQ_OFF_BAR + 256) + (warp - 2) * TILE;
-        int acc_n = 0;
+        int acc_h[2] = {0, 0};   // uses of this tile's two half accumulators
+        const size_t nsub_all = 2 * size_t(p.k_tiles);   // gap row length (halves)
         for (int item = blockIdx.x, lu = 0; item < p.items; item += gridDim.x, ++lu) {
             int unit, split;
-                item_coords(p.items, p.splits, item, unit, split);
+            item_coords(p.items, p.splits, item, unit, split);
             const int qt0 = p.q_tile_begin + 2 * unit;
             const int nq = min(2, p.q_tile_begin + p.q_tiles - qt0);
             const int kt0 = split * ktiles_per_split;
@@ -890,7 +900,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
             if (!VEC && p.m_init && t < nq && row >= p.row_begin && row < p.row_end)
                 M = p.m_init[row];
             double S = 0.0;
-            int best_kt = -1;
+            int best_sub = -1;   // half index 2 kt + h holding the running max
             float nlh = 0.0f, nll = 0.0f;
             if constexpr (VEC) {
                 const bool live = t < nq && row < p.R;
@@ -902,12 +912,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 // m_init - (delta + slack), a lower bound of its screened max
                 float Ma = M > -INFINITY ? M - 0.5f * (p.screen_thr - p.skip) : -INFINITY;
                 const bool row_ok = t < nq && row < p.R;
+                unsigned nl = 0;   // screen-only: halves newly marked live by this warp
                 for (int kt = kt0; kt < kt1; ++kt) {
                     if (t < nq) {
-                        float tmax = -INFINITY;
+                        float tmax = -INFINITY, th[2];
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
-                            mbar_wait(accfull(t, h), acc_n & 1);
+                            mbar_wait(accfull(t, h), acc_h[h] & 1);
                             fence_after();
                             const int64_t kbase = int64_t(kt) * TILE + 64 * h;
                             uint32_t v[64];
@@ -922,24 +933,45 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                                 for (int j = 0; j < 64; ++j)
                                     if (kbase + j >= p.key_valid) v[j] = __float_as_uint(-INFINITY);
                             }
-                            tmax = fmaxf(tmax, row_max<64>(v) * p.acc_scale);
+                            th[h] = row_max<64>(v) * p.acc_scale;
+                            tmax = fmaxf(tmax, th[h]);
                         }
-                        ++acc_n;
+                        ++acc_h[0];
+                        ++acc_h[1];
                         Ma = fmaxf(Ma, tmax);
                         const bool live = row_ok && tmax >= Ma - p.screen_thr;
                         if (__any_sync(0xffffffffu, live) && lane == 0)
                             atomicOr(&live_bits[t * SWORDS + ((kt - kt0) >> 5)],
                                      1u << ((kt - kt0) & 31));
-                        if (p.gap) {
-                            // warm-bound seed: true gap <= screened gap + 2 delta + slack
-                            const float gv = row_ok ? tmax - Ma + (p.screen_thr - p.skip)
-                                                    : -INFINITY;
-                            const int gmax = __reduce_max_sync(0xffffffffu, fenc(gv));
-                            if (lane == 0)
-                                atomicMax(&p.gap[size_t(2 * unit + t) * p.k_tiles + kt], gmax);
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            if (p.gap) {
+                                // warm-bound seed: true gap <= screened gap + 2 delta + slack
+                                const float gv = row_ok ? th[h] - Ma + (p.screen_thr - p.skip)
+                                                        : -INFINITY;
+                                const int gmax = __reduce_max_sync(0xffffffffu, fenc(gv));
+                                if (lane == 0)
+                                    atomicMax(&p.gap[size_t(2 * unit + t) * nsub_all + 2 * kt + h],
+                                              gmax);
+                            }
+                            if (p.screen_only &&
+                                __any_sync(0xffffffffu, row_ok && th[h] >= Ma - p.screen_thr) &&
+                                lane == 0) {
+                                // the half's bit in the phase-2 launch's live set (this
+                                // launch runs one split, kt0 = 0)
+                                const int s2 = kt / p.out_kps;
+                                const int q = 2 * (kt - s2 * p.out_kps) + h;
+                                const uint32_t bit = 1u << (q & 31);
+                                const uint32_t old = atomicOr(
+                                    &p.live_out[((size_t(unit) * p.out_splits + s2) * 2 + t) *
+                                                    p.out_kwords + (q >> 5)], bit);
+                                nl += (old & bit) ? 0u : 1u;
+                            }
                         }
                     }
                 }
+                if (p.screen_only && p.live_count && lane == 0 && nl)
+                    atomicAdd(p.live_count, (unsigned long long)nl);
                 // the split's true max is >= the screened max - (delta + slack):
                 // seed the running max there (earlier in-epilogue skips)
                 if (!VEC && row_ok && Ma > -INFINITY)
@@ -952,71 +984,50 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                     for (int w = threadIdx.x - 64; w < p.kwords; w += 256)
                         p.live_global[(size_t(unit) * p.splits + split) * p.kwords + w] =
                             live_word(-1, w);
-                if (p.screen_only) {
-                    // per-tile masks re-cut into the phase-2 launch's key-range splits
-                    // (this launch runs one split: bit kt = key tile kt), live count
-                    const int nw = 2 * p.out_splits * p.out_kwords;
-                    unsigned nl = 0;
-                    for (int e = threadIdx.x - 64; e < nw; e += 256) {
-                        const int tt = e / (p.out_splits * p.out_kwords);
-                        const int r = e - tt * p.out_splits * p.out_kwords;
-                        const int s2 = r / p.out_kwords, w = r - s2 * p.out_kwords;
-                        const int b0 = s2 * p.out_kps + 32 * w;            // first key tile
-                        const int nb = min(32, min(p.out_kps - 32 * w, p.k_tiles - b0));
-                        uint32_t bits = 0;
-                        if (nb > 0 && tt < nq) {
-                            const int wi = b0 >> 5, sh = b0 & 31;
-                            bits = live_bits[tt * SWORDS + wi] >> sh;
-                            if (sh && wi + 1 < SWORDS)
-                                bits |= live_bits[tt * SWORDS + wi + 1] << (32 - sh);
-                            if (nb < 32) bits &= (1u << nb) - 1u;
-                        }
-                        p.live_out[((size_t(unit) * p.out_splits + s2) * 2 + tt) * p.out_kwords +
-                                   w] = bits;
-                        nl += __popc(bits);
-                    }
-                    const unsigned wl = __reduce_add_sync(0xffffffffu, nl);
-                    if (p.live_count && lane == 0 && wl)
-                        atomicAdd(p.live_count, (unsigned long long)wl);
-                    if (t < nq && row >= p.row_begin && row < p.row_end && p.minit_out)
-                        p.minit_out[row] = M;
-                }
+                if (p.screen_only && t < nq && row >= p.row_begin && row < p.row_end &&
+                    p.minit_out)
+                    p.minit_out[row] = M;
             }
             if (staged) mbar_wait(wbits_ready(lu & 1), (lu >> 1) & 1);
             const bool run2 = !SCREEN || !p.screen_only;
-            for (int kt = t < nq && run2 ? first_kt(unit, kt0, kt1, t, lu) : kt1, kt_next; kt < kt1;
-                 kt = kt_next) {
+            // the item's live halves of this query tile in key order: every half of a
+            // live key tile (tile-granular sets), or the set halves of a warm live set
+            const int qend = 2 * (kt1 - kt0);
+            auto next_half = [&](int q) -> int {   // next after q (q < 0: the first)
+                if (staged) return next_sub(q + 1, qend, lu, t);
+                if (q >= 0 && !(q & 1)) return q + 1;
+                const int kt = q < 0 ? first_kt(unit, kt0, kt1, t, lu)
+                                     : next_kt(unit, kt0 + (q >> 1), kt0, kt1, t, lu);
+                return kt < kt1 ? 2 * (kt - kt0) : qend;
+            };
+            for (int q = t < nq && run2 ? next_half(-1) : qend, q_next; q < qend; q = q_next) {
+                const int kt = kt0 + (q >> 1), h = q & 1;
                 const float M_old = M;
-                float umax = -INFINITY;
-                bool hit = false;
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    mbar_wait(accfull(t, h), acc_n & 1);
-                    fence_after();
-                    uint32_t v[64];
-                    FSKB_TMEM_LD32(acc_addr + 64 * h, (v + 0));
-                    FSKB_TMEM_LD32(acc_addr + 64 * h + 32, (v + 32));
-                    if (h == 0) kt_next = next_kt(unit, kt, kt0, kt1, t, lu);  // overlaps the loads
-                    tmem_ld_wait();
-                    fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(accempty(t, h));
-                    float uh;
-                    hit |= k1_tile_update<VEC, 64>(v, int64_t(kt) * TILE + 64 * h, p, M, S, nlh,
-                                                   nll, vb, lane, uh);
-                    umax = fmaxf(umax, uh);
-                }
-                ++acc_n;
+                mbar_wait(accfull(t, h), acc_h[h] & 1);
+                fence_after();
+                uint32_t v[64];
+                FSKB_TMEM_LD32(acc_addr + 64 * h, (v + 0));
+                FSKB_TMEM_LD32(acc_addr + 64 * h + 32, (v + 32));
+                q_next = next_half(q);   // overlaps the loads
+                tmem_ld_wait();
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(accempty(t, h));
+                ++acc_h[h];
+                float uh;
+                const bool hit = k1_tile_update<VEC, 64>(v, int64_t(kt) * TILE + 64 * h, p, M, S,
+                                                         nlh, nll, vb, lane, uh);
                 if (!VEC && !SCREEN && hit && p.live_global && lane == 0)
-                    atomicOr(&p.live_global[(size_t(unit) * p.splits + split) * p.kwords + ((kt - kt0) >> 5)],
+                    atomicOr(&p.live_global[(size_t(unit) * p.splits + split) * p.kwords +
+                                            ((kt - kt0) >> 5)],
                              1u << ((kt - kt0) & 31));
                 if constexpr (!VEC) {
-                    if (M > M_old) best_kt = kt;
+                    if (M > M_old) best_sub = 2 * kt + h;
                     if (p.gap) {
-                        const float gv = row < p.R ? umax - M : -INFINITY;
+                        const float gv = row < p.R ? uh - M : -INFINITY;
                         const int gmax = __reduce_max_sync(0xffffffffu, fenc(gv));
                         if (lane == 0)
-                            atomicMax(&p.gap[size_t(2 * unit + t) * p.k_tiles + kt], gmax);
+                            atomicMax(&p.gap[size_t(2 * unit + t) * nsub_all + 2 * kt + h], gmax);
                     }
                 }
             }
@@ -1036,7 +1047,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 } else {
                     p.part_m[size_t(split) * p.R + row] = double(M) * 0.69314718055994530942;
                     p.part_s[size_t(split) * p.R + row] = S;
-                    if (p.part_arg) p.part_arg[size_t(split) * p.R + row] = best_kt;
+                    if (p.part_arg) p.part_arg[size_t(split) * p.R + row] = best_sub;
                 }
             }
         }
@@ -1851,7 +1862,8 @@ __global__ void build_split_image(const float* __restrict__ pts, int64_t R, int6
 // bias chunk: b_j 2^-E = 2048 p0 + p1 + p2 / 2048, b_j = log2(e) (pot_j / eps + log w_j).
 // Warm-bound bookkeeping (all nullable): bcur[j] = b_j (log2 units) and, against
 // bprev (the previous LSE pass's bias of this side), the per-key-tile max / min of
-// b_j - bprev_j (tile_dmax / tile_dmin, ordered-int encoded). 256 threads = 2 tiles.
+// b_j - bprev_j per 64-key half of a key tile (tile_dmax / tile_dmin, ordered-int
+// encoded, indexed 2 kt + h). 256 threads = 2 tiles.
 __global__ void build_bias(const float* __restrict__ pot, const float* __restrict__ logw,
                            int64_t C, int64_t rows_padded, double eps, double inv_scale,
                            uint8_t* __restrict__ img, int* flags, float* __restrict__ bcur,
@@ -1902,16 +1914,11 @@ __global__ void build_bias(const float* __restrict__ pot, const float* __restric
             smin[w] = dmin;
         }
         __syncthreads();
-        if (threadIdx.x < 2) {  // tile (threadIdx.x) of this block: warps 4t .. 4t+3
-            const int64_t tile = (int64_t(blockIdx.x) * blockDim.x) / TILE + threadIdx.x;
-            if (tile * TILE < rows_padded) {
-                float mx = -INFINITY, mn = INFINITY;
-                for (int k = 0; k < 4; ++k) {
-                    mx = fmaxf(mx, smax[4 * threadIdx.x + k]);
-                    mn = fminf(mn, smin[4 * threadIdx.x + k]);
-                }
-                tile_dmax[tile] = fenc(mx);
-                tile_dmin[tile] = fenc(mn);
+        if (threadIdx.x < 4) {  // 64-key half (threadIdx.x) of this block: warps 2h, 2h+1
+            const int64_t half = (int64_t(blockIdx.x) * blockDim.x) / 64 + threadIdx.x;
+            if (half * 64 < rows_padded) {
+                tile_dmax[half] = fenc(fmaxf(smax[2 * threadIdx.x], smax[2 * threadIdx.x + 1]));
+                tile_dmin[half] = fenc(fminf(smin[2 * threadIdx.x], smin[2 * threadIdx.x + 1]));
             }
         }
     }
@@ -1950,12 +1957,12 @@ __global__ void fill_int_kernel(int* __restrict__ p, int64_t n, int v) {
         p[i] = v;
 }
 
-// Propagate the per-(query tile, key tile) gap bounds E = max_i (tilemax_i - M_i)
-// to the new bias: E' = E + max_tile(db) - lambda_t. Blocks with E' < -(64 + 1)
+// Propagate the per-(query tile, 64-key half) gap bounds E = max_i (halfmax_i - M_i)
+// to the new bias: E' = E + max_half(db) - lambda_t. Halves with E' < -(T + 1)
 // are provably below 2^-T of every row's max and stay out of the live set
-// (E <- E'); live blocks get E <- -inf for the pass to re-measure. One thread per
+// (E <- E'); live halves get E <- -inf for the pass to re-measure. One thread per
 // bitmask word (u, split, w) of the pass's live_in layout, both query tiles of
-// the unit: live[u][split][t][w].
+// the unit: live[u][split][t][w], bit 2 (kt - split kps) + h.
 __global__ void warm_prepass_kernel(int* __restrict__ gap, const int* __restrict__ tile_dmax,
                                     const int* __restrict__ lam, int units, int k_tiles, int splits,
                                     int kps, int kwords, float skip, uint32_t* __restrict__ live,
@@ -1967,20 +1974,21 @@ __global__ void warm_prepass_kernel(int* __restrict__ gap, const int* __restrict
         const int w = int(gid % kwords);
         const int s = int((gid / kwords) % splits);
         const int u = int(gid / (int64_t(kwords) * splits));
-        const int kt_end = min(k_tiles, (s + 1) * kps);
+        const int q_end = 2 * (min(k_tiles, (s + 1) * kps) - s * kps);   // halves of the split
         for (int t = 0; t < 2; ++t) {
             const float lt = fdec(lam[2 * u + t]);   // +inf for a missing second tile
-            int* grow = gap + size_t(2 * u + t) * k_tiles;
+            int* grow = gap + size_t(2 * u + t) * 2 * k_tiles;
             uint32_t bits = 0;
             for (int b = 0; b < 32; ++b) {
-                const int kt = s * kps + w * 32 + b;
-                if (w * 32 + b >= kps || kt >= kt_end) break;
-                const float e = fdec(grow[kt]) + fdec(tile_dmax[kt]) - lt;
+                const int q = w * 32 + b;
+                if (q >= q_end) break;
+                const int hq = 2 * s * kps + q;   // absolute half index
+                const float e = fdec(grow[hq]) + fdec(tile_dmax[hq]) - lt;
                 const bool dead = e < -(skip + 1.0f);   // NaN -> live
                 if (dead) {
-                    grow[kt] = fenc(e);
+                    grow[hq] = fenc(e);
                 } else {
-                    grow[kt] = fenc(-INFINITY);
+                    grow[hq] = fenc(-INFINITY);
                     bits |= 1u << b;
                     ++nlive;
                 }
@@ -2386,9 +2394,9 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
     if (warm_track) {
         for (auto& b : I.bval[side])
             if (b.size() < size_t(I.rows_pad[kc])) b.alloc(size_t(I.rows_pad[kc]), P.s);
-        if (I.tdmax[side].size() < size_t(n_ktiles)) {
-            I.tdmax[side].alloc(size_t(n_ktiles), P.s);
-            I.tdmin[side].alloc(size_t(n_ktiles), P.s);
+        if (I.tdmax[side].size() < 2 * size_t(n_ktiles)) {   // per 64-key half
+            I.tdmax[side].alloc(2 * size_t(n_ktiles), P.s);
+            I.tdmin[side].alloc(2 * size_t(n_ktiles), P.s);
         }
     }
     // per-pass bias chunk (bit-identical scores for the same potentials)
@@ -2426,6 +2434,8 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
     }();
     if (warm && range_split)
         min_s = std::max(min_s, int(std::ceil(double(k_tiles) * KSTAGE / warm_range_bytes())));
+    // warm live sets are staged in shared memory: <= kMaxWarmKps key tiles per split
+    if (warm) min_s = std::max(min_s, (k_tiles + kMaxWarmKps - 1) / kMaxWarmKps);
     p.splits = pick_splits(units, k_tiles, sms, min_s);
     p.items = units * p.splits;
     p.row_begin = row_begin;
@@ -2456,8 +2466,8 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         // bias change, decide the live blocks without any extra GEMM (the cold first
         // pass is screened: its phase 1 seeds the gap bounds and the running max)
         screen = false;
-        const int kw = (kps + 31) / 32;
-        const size_t gsz = 2 * size_t(units) * size_t(n_ktiles);
+        const int kw = (2 * kps + 31) / 32;   // one bit per 64-key half
+        const size_t gsz = 2 * size_t(units) * 2 * size_t(n_ktiles);
         if (I.gap[side].size() < gsz) I.gap[side].alloc(gsz, P.s);
         if (I.argtile[side].size() < size_t(p.R)) I.argtile[side].alloc(size_t(p.R), P.s);
         if (I.rowmax[side].size() < size_t(p.R)) I.rowmax[side].alloc(size_t(p.R), P.s);
@@ -2492,7 +2502,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
                                       cudaMemcpyDeviceToHost, P.s));
             FSKB_CUDA(cudaEventRecord(I.ev[side], P.s));
             FSKB_CUDA(cudaEventSynchronize(I.ev[side]));
-            const double blocks = double(p.q_tiles) * double(n_ktiles);
+            const double blocks = double(p.q_tiles) * 2.0 * double(n_ktiles);   // halves
             const double est = double(I.h_live[side]) / std::max(1.0, blocks);
             // mostly live (right after a restart of the potentials, whose bias change
             // voids the bounds): a cold pass re-seeds the bounds for less. Cost model in
@@ -2542,15 +2552,18 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
     // image: ~230 GB of HBM traffic per pass at cfg3)
     bool two_phase = false;
     if (cold_screen && screen && !vec && range_split && p.splits == 1 && !(m_init && ex)) {
-        const int s2 = pick_splits(units, k_tiles, sms,
-                                   std::max(base_min_s, int(std::ceil(double(k_tiles) * KSTAGE /
-                                                                       warm_range_bytes()))));
+        const int s2 = pick_splits(
+            units, k_tiles, sms,
+            std::max({base_min_s, int(std::ceil(double(k_tiles) * KSTAGE / warm_range_bytes())),
+                      (k_tiles + kMaxWarmKps - 1) / kMaxWarmKps}));
         const int kps2 = (k_tiles + s2 - 1) / s2;
-        const int kw2 = (kps2 + 31) / 32;
-        two_phase = s2 > 1 && kw2 <= int(SWORDS / 2) && k_tiles <= kMaxScreenTiles;
+        const int kw2 = (2 * kps2 + 31) / 32;   // one bit per 64-key half
+        two_phase = s2 > 1 && kps2 <= kMaxWarmKps && k_tiles <= kMaxScreenTiles;
         if (two_phase) {
             const size_t words = size_t(units) * s2 * 2 * kw2;
             if (I.warm_live[side].size() < words) I.warm_live[side].alloc(words, P.s);
+            // phase 1 sets the live halves' bits
+            FSKB_CUDA(cudaMemsetAsync(I.warm_live[side].get(), 0, words * sizeof(uint32_t), P.s));
             if (I.minit[side].size() < size_t(p.R)) I.minit[side].alloc(size_t(p.R), P.s);
             TcParams p1 = p;
             p1.screen_only = 1;
@@ -2572,7 +2585,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
             FSKB_CUDA(cudaEventRecord(I.ev[side], P.s));
             I.pending[side] = true;
             I.pending_screen[side] = true;
-            I.pending_blocks[side] = double(p.q_tiles) * double(k_tiles);
+            I.pending_blocks[side] = double(p.q_tiles) * 2.0 * double(k_tiles);   // halves
             // phase 2: a warm pass over the screened masks, seeded with phase 1's maxima
             screen = false;
             p.splits = s2;
@@ -2676,7 +2689,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
             FSKB_CUDA(cudaEventRecord(I.ev[side], P.s));
             I.pending[side] = true;
             I.pending_screen[side] = true;
-            I.pending_blocks[side] = double(p.q_tiles) * double(k_tiles);
+            I.pending_blocks[side] = double(p.q_tiles) * 2.0 * double(k_tiles);   // halves
         }
     } else {
         if (vec)
