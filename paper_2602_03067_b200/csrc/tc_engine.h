@@ -39,6 +39,10 @@ public:
 
     // (Re)builds the scaled key images for this eps (O((n+m) d) work).
     void set_eps(DevProblem<float>& P, double eps);
+    // Forget the skip state carried from earlier passes (warm bounds, pass-kind
+    // history): a solve restarted from fresh potentials then runs exactly like the
+    // first solve of the problem, whatever ran before (history-independent bits).
+    void reset_history();
 
     // One half-step for rows [row_begin, row_end) of `side` (0: f from g over
     // keys Y, 1: g from f over keys X). FinalizeArgs pointers address full-length

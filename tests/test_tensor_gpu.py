@@ -728,6 +728,37 @@ def test_run_to_run_bit_identical(fsk, n, m):
     assert outs[0]["marginal_violation"] == outs[1]["marginal_violation"]
 
 
+def test_engine_solves_history_independent(fsk):
+    """A solve restarted on the same engine (init_potentials) forgets the warm
+    bounds and pass-kind history of the previous solve: the second solve, after a
+    different one in between, returns the first one's bits (skip decisions are a
+    function of the problem and the pass, not of what ran before)."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(77)
+    n = m = 1 << 17
+    X, Y = rng.normal(size=(n, 64)), rng.normal(size=(m, 64))
+    u = np.full(n, 1.0 / n)
+    eng = fsk.Engine(0, X, u, Y, u, mode="tensor")
+    f = torch.empty(n, dtype=torch.float32, device="cuda")
+    g = torch.empty(m, dtype=torch.float32, device="cuda")
+    eng.bind(f.data_ptr(), g.data_ptr())
+    outs = []
+    for eps in (0.05, 0.07, 0.05):
+        eng.set_eps(eps)
+        eng.init_potentials()
+        for _ in range(6):
+            eng.half_step(0, 0, n)
+            eng.half_step(1, 0, m)
+        G = torch.empty((n, 64), dtype=torch.float32, device="cuda")
+        eng.grad(0, n, G.data_ptr())
+        torch.cuda.synchronize()
+        outs.append((f.cpu().numpy().copy(), g.cpu().numpy().copy(), G.cpu().numpy()))
+    assert eng.pass_counts()["warm"] > 0
+    for a_, b_ in zip(outs[0], outs[2]):
+        assert np.array_equal(a_, b_)
+    eng.close()
+
+
 def test_persistent_small_solve(fsk, port, golden):
     """cfg1-class problems (keys fit in shared memory, d <= 16): the whole iteration
     loop is one cooperative kernel (small_solve.cu). Engine iterate and the drop-in
