@@ -1967,38 +1967,39 @@ __global__ void warm_prepass_kernel(int* __restrict__ gap, const int* __restrict
                                     const int* __restrict__ lam, int units, int k_tiles, int splits,
                                     int kps, int kwords, float skip, uint32_t* __restrict__ live,
                                     unsigned long long* __restrict__ live_count) {
-    const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t total = int64_t(units) * splits * kwords;
-    int nlive = 0;
-    if (gid < total) {
-        const int w = int(gid % kwords);
-        const int s = int((gid / kwords) % splits);
-        const int u = int(gid / (int64_t(kwords) * splits));
+    // one warp per live-set word (u, split, t, w), one lane per half: coalesced gap
+    // and bias-change reads, the word by ballot; one counter update per block
+    const int64_t words = int64_t(units) * splits * 2 * kwords;
+    const int lane = threadIdx.x & 31;
+    unsigned nlive = 0;
+    for (int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; wid < words;
+         wid += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+        const int w = int(wid % kwords);
+        const int t = int((wid / kwords) & 1);
+        const int s = int((wid / (2 * kwords)) % splits);
+        const int u = int(wid / (int64_t(2) * kwords * splits));
         const int q_end = 2 * (min(k_tiles, (s + 1) * kps) - s * kps);   // halves of the split
-        for (int t = 0; t < 2; ++t) {
+        const int q = w * 32 + lane;
+        bool is_live = false;
+        if (q < q_end) {
             const float lt = fdec(lam[2 * u + t]);   // +inf for a missing second tile
-            int* grow = gap + size_t(2 * u + t) * 2 * k_tiles;
-            uint32_t bits = 0;
-            for (int b = 0; b < 32; ++b) {
-                const int q = w * 32 + b;
-                if (q >= q_end) break;
-                const int hq = 2 * s * kps + q;   // absolute half index
-                const float e = fdec(grow[hq]) + fdec(tile_dmax[hq]) - lt;
-                const bool dead = e < -(skip + 1.0f);   // NaN -> live
-                if (dead) {
-                    grow[hq] = fenc(e);
-                } else {
-                    grow[hq] = fenc(-INFINITY);
-                    bits |= 1u << b;
-                    ++nlive;
-                }
-            }
-            live[((size_t(u) * splits + s) * 2 + t) * kwords + w] = bits;
+            int* g = gap + size_t(2 * u + t) * 2 * k_tiles + 2 * size_t(s) * kps + q;
+            const float e = fdec(*g) + fdec(tile_dmax[2 * size_t(s) * kps + q]) - lt;
+            is_live = !(e < -(skip + 1.0f));   // NaN -> live
+            *g = is_live ? fenc(-INFINITY) : fenc(e);
+        }
+        const uint32_t bits = __ballot_sync(0xffffffffu, is_live);
+        if (lane == 0) {
+            live[wid] = bits;   // [u][split][t][w]
+            nlive += __popc(bits);
         }
     }
-    // one counter update per warp (a per-thread atomic on one word serialized ~1 ms)
-    const unsigned wl = __reduce_add_sync(0xffffffffu, unsigned(nlive));
-    if (live_count && (threadIdx.x & 31) == 0 && wl) atomicAdd(live_count, (unsigned long long)wl);
+    __shared__ unsigned blk;
+    if (threadIdx.x == 0) blk = 0;
+    __syncthreads();
+    if (lane == 0 && nlive) atomicAdd(&blk, nlive);
+    __syncthreads();
+    if (live_count && threadIdx.x == 0 && blk) atomicAdd(live_count, (unsigned long long)blk);
 }
 
 __global__ void absmax_kernel(const float* __restrict__ x, int64_t n, unsigned int* out) {
@@ -2304,6 +2305,19 @@ TcHalfStep::TcHalfStep(DevProblem<float>& P) : impl_(new Impl()) {
 
 TcHalfStep::~TcHalfStep() { delete impl_; }
 
+void TcHalfStep::reset_history() {
+    Impl& I = *impl_;
+    for (int side = 0; side < 2; ++side) {
+        if (I.pending[side]) FSKB_CUDA(cudaEventSynchronize(I.ev[side]));
+        poll_screen(side, kScreenMaxLive);   // (accounting of the last probe)
+        I.warm_ok[side] = I.b_valid[side] = false;
+        I.live_est[side] = 0.0;
+        I.screen_est[side] = 0.3;
+        I.skip_left[side] = I.high_run[side] = 0;
+        I.backoff[side] = 8;
+    }
+}
+
 void TcHalfStep::set_eps(DevProblem<float>& P, double eps) {
     impl_->eps = eps;
     for (int side = 0; side < 2; ++side) impl_->warm_ok[side] = impl_->b_valid[side] = false;
@@ -2491,7 +2505,8 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
             // (the previous probe of this side was consumed on entry: pending is clear)
             unsigned long long* cnt = I.live_count.get() + side;
             FSKB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), P.s));
-            warm_prepass_kernel<<<unsigned((words + 255) / 256), 256, 0, P.s>>>(
+            warm_prepass_kernel<<<unsigned(std::min<size_t>(4 * size_t(sms), (2 * words + 7) / 8)),
+                                  256, 0, P.s>>>(
                 I.gap[side].get(), I.tdmax[side].get(), I.lam[side].get(), units, n_ktiles,
                 p.splits, kps, kw, I.skip[side], I.warm_live[side].get(), cnt);
             FSKB_CUDA(cudaGetLastError());
@@ -2510,6 +2525,10 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
             // last screened pass's live fraction (5 of 13 MMAs per block + phase 2)
             const double c_screen = can_screen ? 0.4 + 1.2 * I.screen_est[side] : 1.0;
             go_cold = est > std::min(c_screen, 1.0) + 0.05;
+            static const bool dbg = std::getenv("FSK_DEBUG_PASS") != nullptr;
+            if (dbg)
+                std::fprintf(stderr, "[fsk pass] side %d warm-bound live %.4f screened cost %.3f -> %s\n",
+                             side, est, c_screen, go_cold ? "cold" : "warm");
             if (!go_cold) {
                 I.pending[side] = true;
                 I.pending_blocks[side] = blocks;
