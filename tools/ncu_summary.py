@@ -72,31 +72,47 @@ def summarise_report(rep: str, title: str | None) -> str:
 
 
 def summarise_launches(path: str) -> str:
+    """Per-kernel launch count, time and share; DRAM bytes per launch when the list
+    also carries dram__bytes_read/write.sum (several metrics per launch)."""
     text = open(path).read()
     start = text.find('"ID"')
     rows = list(csv.reader(io.StringIO(text[start:])))
     hdr = rows[0]
     ik, iv, iu = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    im = hdr.index("Metric Name") if "Metric Name" in hdr else None
     tot = collections.defaultdict(float)
+    dram = collections.defaultdict(float)
     cnt = collections.Counter()
     unit = ""
+    scales = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "nsecond": 1e-6, "ms": 1.0,
+              "msecond": 1.0}
+    bscale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
     for r in rows[1:]:
         if len(r) <= iv or not r[iv]:
             continue
         v = float(r[iv].replace(",", ""))
-        unit = r[iu]
         name = r[ik].split("(")[0]
-        tot[name] += v
+        metric = r[im] if im is not None else "gpu__time_duration.sum"
+        if metric.startswith("dram__bytes"):
+            dram[name] += v * bscale.get(r[iu], 1.0)
+            continue
+        if metric != "gpu__time_duration.sum":
+            continue
+        tot[name] += v * scales.get(r[iu], 1.0)
         cnt[name] += 1
-    scale = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "nsecond": 1e-6, "ms": 1.0,
-             "msecond": 1.0}.get(unit, 1.0)
     grand = sum(tot.values())
-    lines = [f"Launch list `{path}` (`ncu --metrics gpu__time_duration.sum --clock-control none`,"
-             " serialised, cold cache)\n", "| kernel | launches | total ms | mean ms | share |",
-             "|---|---|---|---|---|"]
+    has_dram = bool(dram)
+    lines = [f"Launch list `{path}` (`ncu --metrics gpu__time_duration.sum"
+             f"{',dram__bytes_read.sum,dram__bytes_write.sum' if has_dram else ''}"
+             " --clock-control none`, serialised, cold cache)\n",
+             "| kernel | launches | total ms | mean ms | share |" +
+             (" DRAM GB / launch |" if has_dram else ""),
+             "|---|---|---|---|---|" + ("---|" if has_dram else "")]
     for name, t in sorted(tot.items(), key=lambda kv: -kv[1]):
-        lines.append(f"| `{name}` | {cnt[name]} | {t * scale:.3f} | {t * scale / cnt[name]:.3f} |"
-                     f" {t / grand:.1%} |")
+        row = f"| `{name}` | {cnt[name]} | {t:.3f} | {t / cnt[name]:.3f} | {t / grand:.1%} |"
+        if has_dram:
+            row += f" {dram[name] / cnt[name] / 1e9:.2f} |"
+        lines.append(row)
     return "\n".join(lines) + "\n"
 
 
