@@ -203,7 +203,7 @@ int fsk_engine_init_potentials(fsk_engine* e, void* stream) {
         launch_neg_sqnorm<float>(e->P.src.pts.get(), e->P.src.n, e->P.src.d, fs, e->f, s);
         launch_neg_sqnorm<float>(e->P.tgt.pts.get(), e->P.tgt.n, e->P.tgt.d, fs, e->g, s);
         // a new solve: the skip decisions start from scratch (same bits as a fresh engine)
-        if (e->P.tc) e->P.tc->reset_history();
+        if (e->P.tc) e->P.tc->reset_history(s);
     });
 }
 

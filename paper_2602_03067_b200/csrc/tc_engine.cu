@@ -191,6 +191,7 @@ struct TcParams {
     // ([unit][out_split][t][out_kwords], out_kps key tiles per split), each row's
     // seeded running max to minit_out; phase 2 is a warm-pass launch over them
     int screen_only;
+    const int* run_flag;         // non-null: run only if *run_flag != 0 (device-decided cold pass)
     uint32_t* live_out;
     int out_splits, out_kps, out_kwords;
     float* minit_out;
@@ -589,6 +590,7 @@ constexpr uint32_t TQ_QSTRIDE = 72;
 
 template <bool VEC, bool SCREEN>
 __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParams p) {
+    if (p.run_flag && *p.run_flag == 0) return;   // the device decided this pass is warm
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -2002,6 +2004,58 @@ __global__ void warm_prepass_kernel(int* __restrict__ gap, const int* __restrict
     if (live_count && threadIdx.x == 0 && blk) atomicAdd(live_count, (unsigned long long)blk);
 }
 
+// Device-side warm/cold decision of a warm-tracked pass (no host read-back): the
+// prepass live count against the screened-pass cost model (see TcHalfStep::pass).
+// acc[side]: 0 live halves of tracked passes, 1 tracked halves, 2 screened passes,
+// 3 warm passes, 4 phase-1 live halves of the last cold pass, 5 prepass count.
+struct DecideState {
+    unsigned long long acc[8];
+    float screen_est;   // live fraction of the last screened pass
+    int cold;           // the decision of the current pass
+};
+__global__ void decide_kernel(DecideState* st, double blocks, int can_screen, int side) {
+    if (threadIdx.x != 0) return;
+    DecideState& d = st[side];
+    const double est = double(d.acc[5]) / (blocks > 1.0 ? blocks : 1.0);
+    const double c_screen = can_screen ? 0.4 + 1.2 * double(d.screen_est) : 1.0;
+    const int cold = est > fmin(c_screen, 1.0) + 0.05;
+    d.cold = cold;
+    d.acc[1] += (unsigned long long)blocks;
+    if (cold) {
+        d.acc[2] += 1;
+        d.acc[4] = 0;
+    } else {
+        d.acc[3] += 1;
+        d.acc[0] += d.acc[5];
+    }
+}
+// after a device-decided cold pass's phase 1: its live count feeds the accounting
+// and the cost model of later passes
+__global__ void account_screen_kernel(DecideState* st, double blocks, int side) {
+    if (threadIdx.x != 0) return;
+    DecideState& d = st[side];
+    if (!d.cold) return;
+    d.acc[0] += d.acc[4];
+    d.screen_est = float(double(d.acc[4]) / (blocks > 1.0 ? blocks : 1.0));
+}
+__global__ void fill_int_if_kernel(int* __restrict__ p, int64_t n, int v, const int* flag) {
+    if (*flag == 0) return;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+__global__ void init_decide_kernel(DecideState* st) {
+    const int side = threadIdx.x;
+    if (side < 2) {
+        for (int k = 0; k < 8; ++k) st[side].acc[k] = 0;
+        st[side].screen_est = 0.3f;
+        st[side].cold = 0;
+    }
+}
+__global__ void reset_decide_kernel(DecideState* st) {
+    if (threadIdx.x < 2) st[threadIdx.x].screen_est = 0.3f;
+}
+
 __global__ void absmax_kernel(const float* __restrict__ x, int64_t n, unsigned int* out) {
     float m = 0.0f;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -2171,6 +2225,17 @@ struct TcHalfStep::Impl {
     bool b_valid[2] = {false, false};
     DevBuf<int> tdmax[2], tdmin[2], gap[2], argtile[2], part_arg[2], lam[2];
     DevBuf<float> rowmax[2], minit[2];  // last row max (log2), next pass's lower bound
+    DevBuf<uint8_t> decide;             // DecideState[2] (device-decided warm passes)
+    DecideState* dstate() { return reinterpret_cast<DecideState*>(decide.get()); }
+    // device accounting read back (synchronizing) by the diagnostics getters
+    void read_decide(DecideState (&h)[2]) const {
+        if (!decide.get()) {
+            std::memset(h, 0, sizeof(h));
+            return;
+        }
+        FSKB_CUDA(cudaDeviceSynchronize());
+        FSKB_CUDA(cudaMemcpy(h, decide.get(), sizeof(h), cudaMemcpyDeviceToHost));
+    }
     DevBuf<uint32_t> warm_live[2];
     // HBM-resident plan blocks (build_plan)
     DevBuf<float> plan;
@@ -2214,13 +2279,23 @@ unsigned long long TcHalfStep::live_tiles() const {
         if (impl_->pending[side]) FSKB_CUDA(cudaEventSynchronize(impl_->ev[side]));
     const_cast<TcHalfStep*>(this)->poll_screen(0, kScreenMaxLive);
     const_cast<TcHalfStep*>(this)->poll_screen(1, kScreenMaxLive);
-    return impl_->live_total;
+    DecideState d[2];
+    impl_->read_decide(d);
+    return impl_->live_total + d[0].acc[0] + d[1].acc[0];
 }
 
-unsigned long long TcHalfStep::screened_blocks() const { return impl_->screened_blocks; }
+unsigned long long TcHalfStep::screened_blocks() const {
+    DecideState d[2];
+    impl_->read_decide(d);
+    return impl_->screened_blocks + d[0].acc[1] + d[1].acc[1];
+}
 
 void TcHalfStep::pass_counts(unsigned long long out[3]) const {
+    DecideState d[2];
+    impl_->read_decide(d);
     for (int k = 0; k < 3; ++k) out[k] = impl_->n_pass[k];
+    out[0] += d[0].acc[2] + d[1].acc[2];   // device-decided screened
+    out[1] += d[0].acc[3] + d[1].acc[3];   // device-decided warm
 }
 
 double TcHalfStep::live_set_fraction(int side) const {
@@ -2305,8 +2380,13 @@ TcHalfStep::TcHalfStep(DevProblem<float>& P) : impl_(new Impl()) {
 
 TcHalfStep::~TcHalfStep() { delete impl_; }
 
-void TcHalfStep::reset_history() {
+void TcHalfStep::reset_history(cudaStream_t s) {
     Impl& I = *impl_;
+    if (I.decide.get()) {
+        reset_decide_kernel<<<1, 32, 0, s>>>(I.dstate());
+        FSKB_CUDA(cudaGetLastError());
+        count_launch();
+    }
     for (int side = 0; side < 2; ++side) {
         if (I.pending[side]) FSKB_CUDA(cudaEventSynchronize(I.ev[side]));
         poll_screen(side, kScreenMaxLive);   // (accounting of the last probe)
@@ -2347,6 +2427,12 @@ void TcHalfStep::set_eps(DevProblem<float>& P, double eps) {
         }();
         impl_->screen_thr[side] =
             screen_on ? float(double(impl_->skip[side]) + 2.0 * delta + slack) : 0.0f;
+    }
+    if (!impl_->decide.get()) {
+        impl_->decide.alloc(2 * sizeof(DecideState), P.s);
+        init_decide_kernel<<<1, 32, 0, P.s>>>(impl_->dstate());
+        FSKB_CUDA(cudaGetLastError());
+        count_launch();
     }
     if (!impl_->live_count.get()) {
         impl_->live_count.alloc(2, P.s);
@@ -2475,6 +2561,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
                   kps <= kMaxScreenTiles && !p.break_lse;
     bool can_screen = screen;
     bool cold_screen = false;
+    bool dev_decided = false;
     if (warm_track) {
         // warm bounds replace the 5-MMA screen: the previous pass's gaps, moved by the
         // bias change, decide the live blocks without any extra GEMM (the cold first
@@ -2502,8 +2589,60 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
             p.m_init = seed ? I.minit[side].get() : nullptr;
             const size_t words = size_t(units) * p.splits * kw;
             if (I.warm_live[side].size() < 2 * words) I.warm_live[side].alloc(2 * words, P.s);
+            // Device-decided passes (large problems whose cold pass is the two-launch
+            // screen): the prepass count, the cost model and the cold path's launches
+            // all stay on the stream - no host read-back, the host runs ahead
+            static const bool dev_decide_on = [] {
+                const char* e = std::getenv("FSK_DEVICE_DECIDE");
+                return !(e && e[0] == '0');
+            }();
+            const bool dd = dev_decide_on && can_screen && range_split && seed &&
+                            pick_splits(units, k_tiles, sms, base_min_s) == 1 && !(m_init && ex) &&
+                            k_tiles <= kMaxScreenTiles && kps <= kMaxWarmKps && I.decide.get();
+            if (dd) {
+                DecideState* st = I.dstate();
+                const double blocks = double(p.q_tiles) * 2.0 * double(n_ktiles);   // halves
+                FSKB_CUDA(cudaMemsetAsync(&st[side].acc[5], 0, sizeof(unsigned long long), P.s));
+                warm_prepass_kernel<<<unsigned(std::min<size_t>(4 * size_t(sms), (2 * words + 7) / 8)),
+                                      256, 0, P.s>>>(
+                    I.gap[side].get(), I.tdmax[side].get(), I.lam[side].get(), units, n_ktiles,
+                    p.splits, kps, kw, I.skip[side], I.warm_live[side].get(), &st[side].acc[5]);
+                decide_kernel<<<1, 32, 0, P.s>>>(st, blocks, can_screen ? 1 : 0, side);
+                const int* cold = &st[side].cold;
+                // cold: bounds re-measured from scratch, live set rebuilt by phase 1
+                fill_int_if_kernel<<<256, 256, 0, P.s>>>(I.gap[side].get(), int64_t(gsz),
+                                                         int(0x807FFFFF), cold);
+                fill_int_if_kernel<<<64, 256, 0, P.s>>>(
+                    reinterpret_cast<int*>(I.warm_live[side].get()), int64_t(2 * words), 0, cold);
+                TcParams p1 = p;
+                p1.splits = 1;
+                p1.items = units;
+                p1.screen_only = 1;
+                p1.run_flag = cold;
+                p1.live_out = I.warm_live[side].get();
+                p1.out_splits = p.splits;
+                p1.out_kps = kps;
+                p1.out_kwords = kw;
+                p1.minit_out = I.minit[side].get();
+                p1.live_global = nullptr;
+                p1.live_count = &st[side].acc[4];
+                p1.gap = I.gap[side].get();
+                tc_lse_tq_kernel<false, true>
+                    <<<std::min(units, sms), NUM_THREADS, TQ_SMEM_BYTES, P.s>>>(p1);
+                account_screen_kernel<<<1, 32, 0, P.s>>>(st, blocks, side);
+                FSKB_CUDA(cudaGetLastError());
+                count_launch(7);
+                p.live_in = I.warm_live[side].get();
+                p.live_tq = 1;
+                p.in_splits = p.splits;
+                p.in_kps = kps;
+                p.in_kwords = kw;
+                I.warm_blocks += 1;
+                dev_decided = true;
+            }
             // (the previous probe of this side was consumed on entry: pending is clear)
             unsigned long long* cnt = I.live_count.get() + side;
+            if (!dd) {
             FSKB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), P.s));
             warm_prepass_kernel<<<unsigned(std::min<size_t>(4 * size_t(sms), (2 * words + 7) / 8)),
                                   256, 0, P.s>>>(
@@ -2540,6 +2679,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
                 p.in_kwords = kw;
                 I.warm_blocks += 1;
             }
+            }   // !dd
         }
         if (go_cold && p.splits != pick_splits(units, k_tiles, sms, base_min_s)) {
             // the key-range splits serve the warm live sets; a screened pass keeps one
@@ -2684,7 +2824,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         p.plan_out = ex->plan_out;
         p.plan_slot = ex->plan_slot;
     }
-    if (!vec) ++I.n_pass[screen || two_phase ? 0 : (p.live_in && p.live_tq) ? 1 : 2];
+    if (!vec && !dev_decided) ++I.n_pass[screen || two_phase ? 0 : (p.live_in && p.live_tq) ? 1 : 2];
     if (I.labeled) {
         p.lab.qlab = (side == 0 ? P.src : P.tgt).lab.get();
         p.lab.klab = ks.lab.get();

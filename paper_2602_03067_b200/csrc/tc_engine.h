@@ -42,7 +42,7 @@ public:
     // Forget the skip state carried from earlier passes (warm bounds, pass-kind
     // history): a solve restarted from fresh potentials then runs exactly like the
     // first solve of the problem, whatever ran before (history-independent bits).
-    void reset_history();
+    void reset_history(cudaStream_t s);
 
     // One half-step for rows [row_begin, row_end) of `side` (0: f from g over
     // keys Y, 1: g from f over keys X). FinalizeArgs pointers address full-length
