@@ -270,6 +270,9 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
     DevProblem<T> P;
     P.upload(src, tgt, cost, C.s);
     timer.mark("upload");
+    // the gradient's host pages are faulted in while the device iterates
+    HostPrefault prefault;
+    if (grad_out) prefault.start(grad_out, sizeof(double) * size_t(n) * size_t(d));
     if constexpr (kSingle) enable_tensor_path(P, tensor_mode_from_env());
     timer.mark("operand images");
 
@@ -524,6 +527,7 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
                 // CUDA-core fp32 problem: the gradient pass in fp64 (grad_rows_fp64)
                 DevBuf<double> G64(size_t(n * d), C.s);
                 grad_rows_fp64(P, f.get(), g.get(), pot_eps, 0, n, G64.get(), C.flags, C.s);
+                prefault.join();
                 G64.download(grad_out, size_t(n * d));
                 done = true;
                 sync_and_check(C);
@@ -549,8 +553,11 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
             launch_grad_epilogue<T>(P.src.pts.get(), O.get(), P.src.w.get(), f.get(),
                                     lse_f.get(), n, d, eps, G.get(), C.flags, C.s);
         }
+        timer.mark("gradient");
+        prefault.join();
+        timer.mark("output page faults (join)");
         dev_to<T>(G, grad_out, n * d, C.s);
-        timer.mark("gradient + download");
+        timer.mark("gradient download");
         sync_and_check(C);
         if (ledger) {
             ledger_marginals(ledger, n, m, d, tiles, cost);
@@ -840,8 +847,10 @@ int fsk_sinkhorn_solve_grad(const fsk_measure* src, const fsk_measure* tgt, cons
                             const fsk_config* cfg, const fsk_tiles* tiles, fsk_ledger* ledger,
                             fsk_report* report, double* out_grad) {
     return guarded([&] {
+        PhaseTimer timer(nullptr);
         common_checks(src, tgt, cost, tiles);
         validate_config_raw(*cfg);
+        timer.mark("validation");
         if (cfg->precision == 0) {
             if (labeled_cost(cost))
                 throw ValidationFailure(
@@ -850,6 +859,7 @@ int fsk_sinkhorn_solve_grad(const fsk_measure* src, const fsk_measure* tgt, cons
         } else {
             solve_impl<double>(*src, *tgt, cost, *cfg, *tiles, ledger, report, out_grad);
         }
+        timer.mark("solve incl. teardown");
     });
 }
 

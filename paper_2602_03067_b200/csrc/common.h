@@ -6,6 +6,8 @@
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
+#include <thread>
+#include <vector>
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
@@ -42,6 +44,21 @@ enum : int {
 // synchronous with respect to the host buffer (it may be reused on return).
 void copy_host_to_device(void* dst, const void* src, std::size_t bytes, cudaStream_t s);
 void copy_device_to_host(void* dst, const void* src, std::size_t bytes, cudaStream_t s);
+
+// Page-faults a caller's output buffer (>= 64 MB) from background host threads
+// (hostcopy.cpp); join() before the buffer is written for real.
+class HostPrefault {
+public:
+    HostPrefault() = default;
+    HostPrefault(const HostPrefault&) = delete;
+    HostPrefault& operator=(const HostPrefault&) = delete;
+    ~HostPrefault() { join(); }
+    void start(void* p, std::size_t bytes);
+    void join();
+
+private:
+    std::vector<std::thread> th_;
+};
 
 // Owner teardown after a full device synchronize: the buffers may have been
 // allocated on caller streams that no longer exist, so frees inside the scope go
@@ -108,6 +125,27 @@ private:
     T* p_ = nullptr;
     std::size_t n_ = 0;
     cudaStream_t s_ = nullptr;
+};
+
+// Grow-only device scratch per host thread and device for the large per-call
+// partial buffers of the transport kernels (GBs at cfg3): a fresh stream-ordered
+// allocation of that size can make the pool map new memory (measured 0-400 ms per
+// call through the C ABI). Uses on different streams are ordered by an event.
+class Scratch {
+public:
+    // pointer to >= bytes of device memory, ordered after the previous use
+    void* get(std::size_t bytes, cudaStream_t s);
+    // marks the end of this use (enqueued work on s that reads or writes it)
+    void done(cudaStream_t s);
+    static Scratch& local();   // this thread's scratch on the current device
+    ~Scratch();
+
+private:
+    void* p_ = nullptr;
+    std::size_t n_ = 0;
+    int dev_ = -1;
+    cudaEvent_t ev_ = nullptr;
+    bool pending_ = false;
 };
 
 // Global launch counter (the bench reports how many of our kernels ran).

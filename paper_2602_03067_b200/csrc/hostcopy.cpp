@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -165,6 +166,69 @@ void copy_device_to_host(void* dst, const void* src, size_t bytes, cudaStream_t 
         parallel_copy(pieces);
     }
     release(st);
+}
+
+// A fresh output buffer of the caller (e.g. a just-allocated numpy array) is mapped
+// page by page on first touch; when that happens inside the final download, the
+// fault cost (0.1-0.5 s for 0.5 GB, varying with the host's memory state) lands on
+// the critical path. Touching one byte per page from a few host threads while the
+// device iterates moves it off.
+void HostPrefault::start(void* p, std::size_t bytes) {
+    join();
+    if (!p || bytes < (std::size_t(64) << 20)) return;
+    const int nt = int(std::max(1u, std::min(4u, std::thread::hardware_concurrency())));
+    char* c = static_cast<char*>(p);
+    const std::size_t page = 4096, per = (bytes / page + nt - 1) / nt * page;
+    for (int t = 0; t < nt; ++t)
+        th_.emplace_back([c, bytes, page, per, t] {
+            const std::size_t lo = std::size_t(t) * per, hi = std::min(bytes, lo + per);
+            for (std::size_t o = lo; o < hi; o += page) reinterpret_cast<volatile char*>(c)[o] = 0;
+        });
+}
+
+void HostPrefault::join() {
+    for (auto& t : th_) t.join();
+    th_.clear();
+}
+
+Scratch& Scratch::local() {
+    int dev = 0;
+    FSKB_CUDA(cudaGetDevice(&dev));
+    thread_local std::vector<std::unique_ptr<Scratch>> per_dev;
+    if (per_dev.size() <= size_t(dev)) per_dev.resize(size_t(dev) + 1);
+    if (!per_dev[size_t(dev)]) {
+        per_dev[size_t(dev)] = std::make_unique<Scratch>();
+        per_dev[size_t(dev)]->dev_ = dev;
+    }
+    return *per_dev[size_t(dev)];
+}
+
+void* Scratch::get(std::size_t bytes, cudaStream_t s) {
+    if (!ev_) FSKB_CUDA(cudaEventCreateWithFlags(&ev_, cudaEventDisableTiming));
+    if (pending_) FSKB_CUDA(cudaStreamWaitEvent(s, ev_, 0));
+    if (bytes > n_) {
+        if (p_) FSKB_CUDA(cudaFreeAsync(p_, s));
+        p_ = nullptr;
+        n_ = 0;
+        FSKB_CUDA(cudaMallocAsync(&p_, bytes, s));
+        n_ = bytes;
+    }
+    return p_;
+}
+
+void Scratch::done(cudaStream_t s) {
+    FSKB_CUDA(cudaEventRecord(ev_, s));
+    pending_ = true;
+}
+
+Scratch::~Scratch() {
+    // thread exit: the device may already be torn down; best effort
+    if (p_) {
+        cudaSetDevice(dev_);
+        cudaDeviceSynchronize();
+        cudaFree(p_);
+    }
+    if (ev_) cudaEventDestroy(ev_);
 }
 
 }  // namespace fskb

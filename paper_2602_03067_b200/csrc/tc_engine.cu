@@ -194,7 +194,8 @@ struct TcParams {
     const int* run_flag;         // non-null: run only if *run_flag != 0 (device-decided cold pass)
     uint32_t* live_out;
     int out_splits, out_kps, out_kwords;
-    float* minit_out;
+    float* minit_out;            // [row], or [split][minit_stride] when several key splits
+    int64_t minit_stride;
     unsigned long long* live_count;  // += live key tiles (diagnostics), nullable
     uint32_t* live_global;       // LSE passes: per item, the key tiles not proven negligible
     int kwords;                  //   (kwords words per item; bit kt - kt0)
@@ -988,7 +989,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                             live_word(-1, w);
                 if (p.screen_only && t < nq && row >= p.row_begin && row < p.row_end &&
                     p.minit_out)
-                    p.minit_out[row] = M;
+                    p.minit_out[size_t(split) * size_t(p.minit_stride) + row] = M;
             }
             if (staged) mbar_wait(wbits_ready(lu & 1), (lu >> 1) & 1);
             const bool run2 = !SCREEN || !p.screen_only;
@@ -2038,6 +2039,18 @@ __global__ void account_screen_kernel(DecideState* st, double blocks, int side) 
     d.acc[0] += d.acc[4];
     d.screen_est = float(double(d.acc[4]) / (blocks > 1.0 ? blocks : 1.0));
 }
+// a screen-only launch over several key splits leaves one seed per (split, row): the
+// row's seed is the largest (each is a lower bound of the row's true max)
+__global__ void minit_reduce_kernel(const float* __restrict__ parts, int splits, int64_t R,
+                                    int64_t row_begin, int64_t row_end, float* __restrict__ out,
+                                    const int* flag) {
+    if (flag && *flag == 0) return;
+    const int64_t i = row_begin + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= row_end) return;
+    float m = parts[i];
+    for (int s = 1; s < splits; ++s) m = fmaxf(m, parts[size_t(s) * R + i]);
+    out[i] = m;
+}
 __global__ void fill_int_if_kernel(int* __restrict__ p, int64_t n, int v, const int* flag) {
     if (*flag == 0) return;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -2124,6 +2137,16 @@ int scale_exponent(double maxabs) {
 }
 
 }  // namespace
+
+// Largest key-split count of a two-launch screened cold pass (phase 1 over several
+// key splits leaves split-local screened maxima: looser live sets; FSK_TP_SPLITS)
+int two_phase_max_splits() {
+    static const int v = [] {
+        const char* e = std::getenv("FSK_TP_SPLITS");
+        return e ? std::max(1, std::atoi(e)) : 1;
+    }();
+    return v;
+}
 
 // Key split that best fills a persistent grid of `sms` CTAs with units x splits items.
 // key-range size of the L2-local splits (warm passes, sparse K3); FSK_WARM_RANGE_MB
@@ -2225,6 +2248,7 @@ struct TcHalfStep::Impl {
     bool b_valid[2] = {false, false};
     DevBuf<int> tdmax[2], tdmin[2], gap[2], argtile[2], part_arg[2], lam[2];
     DevBuf<float> rowmax[2], minit[2];  // last row max (log2), next pass's lower bound
+    DevBuf<float> minit_parts[2];       // per-split seeds of a multi-split screen-only launch
     DevBuf<uint8_t> decide;             // DecideState[2] (device-decided warm passes)
     DecideState* dstate() { return reinterpret_cast<DecideState*>(decide.get()); }
     // device accounting read back (synchronizing) by the diagnostics getters
@@ -2596,9 +2620,11 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
                 const char* e = std::getenv("FSK_DEVICE_DECIDE");
                 return !(e && e[0] == '0');
             }();
-            const bool dd = dev_decide_on && can_screen && range_split && seed &&
-                            pick_splits(units, k_tiles, sms, base_min_s) == 1 && !(m_init && ex) &&
-                            k_tiles <= kMaxScreenTiles && kps <= kMaxWarmKps && I.decide.get();
+            const int base_s = pick_splits(units, k_tiles, sms, base_min_s);
+            const bool dd = dev_decide_on && can_screen && range_split && seed && !(m_init && ex) &&
+                            base_s <= two_phase_max_splits() &&
+                            (k_tiles + base_s - 1) / base_s <= kMaxScreenTiles &&
+                            kps <= kMaxWarmKps && I.decide.get();
             if (dd) {
                 DecideState* st = I.dstate();
                 const double blocks = double(p.q_tiles) * 2.0 * double(n_ktiles);   // halves
@@ -2615,8 +2641,8 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
                 fill_int_if_kernel<<<64, 256, 0, P.s>>>(
                     reinterpret_cast<int*>(I.warm_live[side].get()), int64_t(2 * words), 0, cold);
                 TcParams p1 = p;
-                p1.splits = 1;
-                p1.items = units;
+                p1.splits = base_s;
+                p1.items = units * base_s;
                 p1.screen_only = 1;
                 p1.run_flag = cold;
                 p1.live_out = I.warm_live[side].get();
@@ -2624,14 +2650,24 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
                 p1.out_kps = kps;
                 p1.out_kwords = kw;
                 p1.minit_out = I.minit[side].get();
+                p1.minit_stride = 0;
+                if (base_s > 1) {
+                    const size_t np = size_t(base_s) * size_t(p.R);
+                    if (I.minit_parts[side].size() < np) I.minit_parts[side].alloc(np, P.s);
+                    p1.minit_out = I.minit_parts[side].get();
+                    p1.minit_stride = p.R;
+                }
                 p1.live_global = nullptr;
                 p1.live_count = &st[side].acc[4];
                 p1.gap = I.gap[side].get();
                 tc_lse_tq_kernel<false, true>
-                    <<<std::min(units, sms), NUM_THREADS, TQ_SMEM_BYTES, P.s>>>(p1);
+                    <<<std::min(p1.items, sms), NUM_THREADS, TQ_SMEM_BYTES, P.s>>>(p1);
+                if (base_s > 1)
+                    minit_reduce_kernel<<<unsigned((row_end - row_begin + 255) / 256), 256, 0, P.s>>>(
+                        p1.minit_out, base_s, p.R, row_begin, row_end, I.minit[side].get(), cold);
                 account_screen_kernel<<<1, 32, 0, P.s>>>(st, blocks, side);
                 FSKB_CUDA(cudaGetLastError());
-                count_launch(7);
+                count_launch(8);
                 p.live_in = I.warm_live[side].get();
                 p.live_tq = 1;
                 p.in_splits = p.splits;
@@ -2710,7 +2746,8 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
     // (one launch scattered the phase-2 reads of ~20% live blocks over the whole key
     // image: ~230 GB of HBM traffic per pass at cfg3)
     bool two_phase = false;
-    if (cold_screen && screen && !vec && range_split && p.splits == 1 && !(m_init && ex)) {
+    if (cold_screen && screen && !vec && range_split && !(m_init && ex) &&
+        p.splits <= two_phase_max_splits()) {
         const int s2 = pick_splits(
             units, k_tiles, sms,
             std::max({base_min_s, int(std::ceil(double(k_tiles) * KSTAGE / warm_range_bytes())),
@@ -2731,6 +2768,13 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
             p1.out_kps = kps2;
             p1.out_kwords = kw2;
             p1.minit_out = I.minit[side].get();
+            p1.minit_stride = 0;
+            if (p.splits > 1) {   // one seed per (key split, row), reduced after the launch
+                const size_t np = size_t(p.splits) * size_t(p.R);
+                if (I.minit_parts[side].size() < np) I.minit_parts[side].alloc(np, P.s);
+                p1.minit_out = I.minit_parts[side].get();
+                p1.minit_stride = p.R;
+            }
             p1.live_global = nullptr;
             p1.live_count = I.live_count.get() + side;
             if (I.pending[side]) FSKB_CUDA(cudaEventSynchronize(I.ev[side]));
@@ -2739,6 +2783,12 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
             tc_lse_tq_kernel<false, true><<<grid, NUM_THREADS, TQ_SMEM_BYTES, P.s>>>(p1);
             FSKB_CUDA(cudaGetLastError());
             count_launch();
+            if (p.splits > 1) {
+                minit_reduce_kernel<<<unsigned((row_end - row_begin + 255) / 256), 256, 0, P.s>>>(
+                    p1.minit_out, p.splits, p.R, row_begin, row_end, I.minit[side].get(), nullptr);
+                FSKB_CUDA(cudaGetLastError());
+                count_launch();
+            }
             FSKB_CUDA(cudaMemcpyAsync(I.h_live + side, p1.live_count, sizeof(unsigned long long),
                                       cudaMemcpyDeviceToHost, P.s));
             FSKB_CUDA(cudaEventRecord(I.ev[side], P.s));
@@ -3217,8 +3267,9 @@ void TcHalfStep::apply_mat(DevProblem<float>& P, int side, const float* kpot, fl
         g.lab.trans = 0;   // W[query label][key label] (stream.cpp:239-242, :354)
     }
     const int vc_max = A ? 2 : 4;
-    DevBuf<float> part(size_t(g.splits) * size_t(R) * vc_max * DPAD, P.s);
-    g.part_o = part.get();
+    Scratch& part = Scratch::local();
+    g.part_o = static_cast<float*>(
+        part.get(sizeof(float) * size_t(g.splits) * size_t(R) * vc_max * DPAD, P.s));
     for (int v0 = 0; v0 < VC; v0 += vc_max) {
         g.v_chunk0 = v0;
         g.vc = std::min(vc_max, VC - v0);
@@ -3229,11 +3280,12 @@ void TcHalfStep::apply_mat(DevProblem<float>& P, int side, const float* kpot, fl
         const int cols = int(std::min<int64_t>(width, p_cols - int64_t(v0) * DPAD));
         const int64_t total = (row_end - row_begin) * cols;
         tc_apply_gen_finalize<<<unsigned((total + 255) / 256), 256, 0, P.s>>>(
-            part.get(), g.splits, R, width, cols, v0 * DPAD, p_cols, marg, out_scale, out, flags,
+            g.part_o, g.splits, R, width, cols, v0 * DPAD, p_cols, marg, out_scale, out, flags,
             row_begin, row_end);
         FSKB_CUDA(cudaGetLastError());
         count_launch();
     }
+    part.done(P.s);
 }
 
 void TcHalfStep::grad(DevProblem<float>& P, int side, const float* kpot, const float* pot,
@@ -3328,8 +3380,8 @@ void TcHalfStep::grad(DevProblem<float>& P, int side, const float* kpot, const f
         p.lse_kps = I.live_kps[side];
         p.lse_kwords = I.live_kwords[side];
     }
-    DevBuf<float> part(size_t(p.splits) * size_t(R) * DPAD, P.s);
-    p.part_o = part.get();
+    Scratch& part = Scratch::local();
+    p.part_o = static_cast<float*>(part.get(sizeof(float) * size_t(p.splits) * size_t(R) * DPAD, P.s));
     tc_apply_kernel<<<std::min(p.items, sms), NUM_THREADS, A_SMEM_BYTES, P.s>>>(p);
     FSKB_CUDA(cudaGetLastError());
     count_launch();
@@ -3338,9 +3390,10 @@ void TcHalfStep::grad(DevProblem<float>& P, int side, const float* kpot, const f
     const double inv_v = std::ldexp(1.0, I.ek[side] - int(kPScaleLog2)) / c;
     const int64_t total = (row_end - row_begin) * d;
     tc_grad_finalize_kernel<<<unsigned((total + 255) / 256), 256, 0, P.s>>>(
-        part.get(), p.splits, R, row_begin, row_end, d, qs.pts.get(), Rm, inv_v, G, flags);
+        p.part_o, p.splits, R, row_begin, row_end, d, qs.pts.get(), Rm, inv_v, G, flags);
     FSKB_CUDA(cudaGetLastError());
     count_launch();
+    part.done(P.s);
 }
 
 bool enable_tensor_path(DevProblem<float>& P, int mode) {
