@@ -2143,7 +2143,7 @@ int scale_exponent(double maxabs) {
 int two_phase_max_splits() {
     static const int v = [] {
         const char* e = std::getenv("FSK_TP_SPLITS");
-        return e ? std::max(1, std::atoi(e)) : 1;
+        return e ? std::max(1, std::atoi(e)) : 2;   // 2: 8-GPU row shards of cfg3
     }();
     return v;
 }
