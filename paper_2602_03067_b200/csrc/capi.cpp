@@ -555,8 +555,24 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
         }
         timer.mark("gradient");
         prefault.join();
-        timer.mark("output page faults (join)");
-        dev_to<T>(G, grad_out, n * d, C.s);
+        timer.mark("output page faults + lock (join)");
+        if (prefault.pinned()) {
+            // one DMA into the page-locked caller buffer (widened on the device)
+            if constexpr (std::is_same_v<T, double>) {
+                FSKB_CUDA(cudaMemcpyAsync(grad_out, G.get(), sizeof(double) * size_t(n * d),
+                                          cudaMemcpyDeviceToHost, C.s));
+                FSKB_CUDA(cudaStreamSynchronize(C.s));
+            } else {
+                DevBuf<double> wide(size_t(n * d), C.s);
+                launch_f32_to_f64(G.get(), wide.get(), n * d, C.s);
+                FSKB_CUDA(cudaMemcpyAsync(grad_out, wide.get(), sizeof(double) * size_t(n * d),
+                                          cudaMemcpyDeviceToHost, C.s));
+                FSKB_CUDA(cudaStreamSynchronize(C.s));
+            }
+        } else {
+            dev_to<T>(G, grad_out, n * d, C.s);
+        }
+        prefault.release();
         timer.mark("gradient download");
         sync_and_check(C);
         if (ledger) {

@@ -45,19 +45,25 @@ enum : int {
 void copy_host_to_device(void* dst, const void* src, std::size_t bytes, cudaStream_t s);
 void copy_device_to_host(void* dst, const void* src, std::size_t bytes, cudaStream_t s);
 
-// Page-faults a caller's output buffer (>= 64 MB) from background host threads
-// (hostcopy.cpp); join() before the buffer is written for real.
+// Faults in and page-locks a caller's output buffer (>= 64 MB) from a background
+// host thread (hostcopy.cpp). join() before writing it; pinned() then says whether a
+// plain cudaMemcpyAsync may DMA into it; release() (also in the destructor) unlocks.
 class HostPrefault {
 public:
     HostPrefault() = default;
     HostPrefault(const HostPrefault&) = delete;
     HostPrefault& operator=(const HostPrefault&) = delete;
-    ~HostPrefault() { join(); }
+    ~HostPrefault() { release(); }
     void start(void* p, std::size_t bytes);
     void join();
+    bool pinned() const { return pinned_; }
+    void release();
 
 private:
-    std::vector<std::thread> th_;
+    std::thread th_;
+    void* p_ = nullptr;
+    std::size_t bytes_ = 0;
+    bool pinned_ = false;
 };
 
 // Owner teardown after a full device synchronize: the buffers may have been

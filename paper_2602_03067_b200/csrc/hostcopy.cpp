@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -169,26 +170,52 @@ void copy_device_to_host(void* dst, const void* src, size_t bytes, cudaStream_t 
 }
 
 // A fresh output buffer of the caller (e.g. a just-allocated numpy array) is mapped
-// page by page on first touch; when that happens inside the final download, the
-// fault cost (0.1-0.5 s for 0.5 GB, varying with the host's memory state) lands on
-// the critical path. Touching one byte per page from a few host threads while the
-// device iterates moves it off.
+// page by page on first touch, and a staged download then costs a host memcpy of
+// the whole buffer: both land on the critical path and both vary with the host's
+// load (0.02-0.5 s for 0.5 GB measured). A background thread faults the pages in
+// (with helpers) while the device iterates; with FSK_PIN_OUTPUT=1 it also page-locks
+// the buffer so the download is one DMA straight into it (see pinned()).
 void HostPrefault::start(void* p, std::size_t bytes) {
     join();
     if (!p || bytes < (std::size_t(64) << 20)) return;
-    const int nt = int(std::max(1u, std::min(4u, std::thread::hardware_concurrency())));
-    char* c = static_cast<char*>(p);
-    const std::size_t page = 4096, per = (bytes / page + nt - 1) / nt * page;
-    for (int t = 0; t < nt; ++t)
-        th_.emplace_back([c, bytes, page, per, t] {
-            const std::size_t lo = std::size_t(t) * per, hi = std::min(bytes, lo + per);
-            for (std::size_t o = lo; o < hi; o += page) reinterpret_cast<volatile char*>(c)[o] = 0;
-        });
+    p_ = p;
+    bytes_ = bytes;
+    pinned_ = false;
+    int dev = 0;
+    FSKB_CUDA(cudaGetDevice(&dev));
+    th_ = std::thread([this, dev] {
+        const int nt = int(std::max(1u, std::min(4u, std::thread::hardware_concurrency())));
+        char* c = static_cast<char*>(p_);
+        const std::size_t page = 4096, per = (bytes_ / page + nt - 1) / nt * page;
+        std::vector<std::thread> helpers;
+        for (int t = 0; t < nt; ++t)
+            helpers.emplace_back([c, page, per, t, this] {
+                const std::size_t lo = std::size_t(t) * per, hi = std::min(bytes_, lo + per);
+                for (std::size_t o = lo; o < hi; o += page) reinterpret_cast<volatile char*>(c)[o] = 0;
+            });
+        for (auto& h : helpers) h.join();
+        // page-locking the buffer for a direct DMA measured slower end to end (the
+        // register / unregister of 0.5 GB outweighs the staged copy): off by default
+        static const bool lock = [] {
+            const char* e = std::getenv("FSK_PIN_OUTPUT");
+            return e && e[0] == '1';
+        }();
+        if (lock && cudaSetDevice(dev) == cudaSuccess &&
+            cudaHostRegister(p_, bytes_, cudaHostRegisterDefault) == cudaSuccess)
+            pinned_ = true;
+        else
+            cudaGetLastError();   // (not fatal: the staged download is the fallback)
+    });
 }
 
 void HostPrefault::join() {
-    for (auto& t : th_) t.join();
-    th_.clear();
+    if (th_.joinable()) th_.join();
+}
+
+void HostPrefault::release() {
+    join();
+    if (pinned_) cudaHostUnregister(p_);
+    pinned_ = false;
 }
 
 Scratch& Scratch::local() {

@@ -198,6 +198,7 @@ struct TcParams {
     int64_t minit_stride;
     unsigned long long* live_count;  // += live key tiles (diagnostics), nullable
     uint32_t* live_global;       // LSE passes: per item, the key tiles not proven negligible
+    uint32_t* live_pt;           //   and per query tile of the item ([item][t][kwords], d <= 64)
     int kwords;                  //   (kwords words per item; bit kt - kt0)
     // VEC passes at the same potentials: only key tiles of that live set are scored
     // (unit u of this pass = unit u of the LSE pass; item index u * in_splits + kt / in_kps)
@@ -1024,6 +1025,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                     atomicOr(&p.live_global[(size_t(unit) * p.splits + split) * p.kwords +
                                             ((kt - kt0) >> 5)],
                              1u << ((kt - kt0) & 31));
+                if (!VEC && hit && p.live_pt && lane == 0)
+                    atomicOr(&p.live_pt[((size_t(unit) * p.splits + split) * 2 + t) * p.kwords +
+                                        ((kt - kt0) >> 5)],
+                             1u << ((kt - kt0) & 31));
                 if constexpr (!VEC) {
                     if (M > M_old) best_sub = 2 * kt + h;
                     if (p.gap) {
@@ -1100,9 +1105,9 @@ struct TcApplyParams {
     const float* l2h;   // [R] log2-domain row LSE, hi
     const float* l2l;   // [R] lo
     float* part_o;      // [splits][R][64] partial O (V units x 2^12)
-    // live key tiles from the screened LSE pass over the same rows and potentials
-    // (nullable): query tile u uses the bitmask of the pass's work item
-    // (u / 2) * lse_splits + kt / lse_kps, bit kt % lse_kps
+    // live key tiles of query tile u from the LSE pass over the same rows and
+    // potentials (nullable; the pass's per-tile record live_pt): the words of the
+    // pass's work item (u / 2) * lse_splits + kt / lse_kps, tile u % 2, bit kt % lse_kps
     const uint32_t* live_global;
     int lse_splits, lse_kps, lse_kwords;
 };
@@ -1112,7 +1117,8 @@ __device__ __forceinline__ int apply_next_live(const TcApplyParams& p, int u, in
     if (!p.live_global) return kt;
     while (kt < kt1) {
         const int ls = kt / p.lse_kps, rel = kt - ls * p.lse_kps;
-        const uint32_t w = __ldg(p.live_global + (size_t(u >> 1) * p.lse_splits + ls) * p.lse_kwords +
+        const uint32_t w = __ldg(p.live_global + ((size_t(u >> 1) * p.lse_splits + ls) * 2 + (u & 1)) *
+                                                     p.lse_kwords +
                                  (rel >> 5)) >> (rel & 31);
         if (w) return kt + __ffs(w) - 1;
         kt += 32 - (rel & 31);
@@ -2236,6 +2242,7 @@ struct TcHalfStep::Impl {
     unsigned long long live_total = 0, screened_blocks = 0;
     // live set of the last LSE pass per side (valid when that pass was screened)
     DevBuf<uint32_t> live_glob[2];
+    DevBuf<uint32_t> live_pt[2];        // the same, per query tile of the item (K3)
     bool live_valid[2] = {false, false};
     int live_splits[2] = {1, 1}, live_kps[2] = {1, 1}, live_kwords[2] = {1, 1};
     int64_t live_row_begin[2] = {0, 0}, live_row_end[2] = {0, 0};
@@ -2843,6 +2850,11 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         p.live_global = I.live_glob[side].get();
         if (!screen)
             FSKB_CUDA(cudaMemsetAsync(p.live_global, 0, words * sizeof(uint32_t), P.s));
+        if (I.chunks == 1 && !I.labeled) {
+            if (I.live_pt[side].size() < 2 * words) I.live_pt[side].alloc(2 * words, P.s);
+            p.live_pt = I.live_pt[side].get();
+            FSKB_CUDA(cudaMemsetAsync(p.live_pt, 0, 2 * words * sizeof(uint32_t), P.s));
+        }
         I.live_valid[side] = true;
         I.live_kpot[side] = kpot;
         I.live_splits[side] = p.splits;
@@ -3375,7 +3387,7 @@ void TcHalfStep::grad(DevProblem<float>& P, int side, const float* kpot, const f
     p.l2l = L2l;
     if (sparse) {
         // the LSE pass above was screened: stream only its live key tiles
-        p.live_global = I.live_glob[side].get();
+        p.live_global = I.live_pt[side].get();
         p.lse_splits = I.live_splits[side];
         p.lse_kps = I.live_kps[side];
         p.lse_kwords = I.live_kwords[side];
