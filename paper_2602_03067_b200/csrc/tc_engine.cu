@@ -410,9 +410,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
     const uint32_t tmem = *tmem_slot;
     const int ktiles_per_split = (p.k_tiles + p.splits - 1) / p.splits;
     const int C = p.chunks;
-    // VEC at fixed potentials: only the key tiles of the LSE pass's live set
+    // VEC at fixed potentials: only the key tiles of the LSE pass's live set (the
+    // union of both query tiles'; with per-tile sets (live_tq) a tile that is not live
+    // for a key tile is neither loaded, multiplied nor read back)
     auto nxt = [&](int unit, int kt, int kt1) {
-        return (VEC && p.live_in) ? live_in_next(p, unit, kt, kt1) : kt;
+        return (VEC && p.live_in) ? live_in_next(p, unit, kt, kt1, -1, p.live_tq != 0) : kt;
+    };
+    auto tiles_of = [&](int unit, int kt, int nq) -> uint32_t {
+        const uint32_t all = nq > 1 ? 3u : 1u;
+        if (!(VEC && p.live_in && p.live_tq)) return all;
+        return (uint32_t(live_in_bit(p, unit, 0, kt)) | (uint32_t(live_in_bit(p, unit, 1, kt)) << 1)) &
+               all;
     };
 
     if (warp == 0) {
@@ -426,14 +434,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
                 for (int kt = nxt(unit, kt0, kt1); kt < kt1; kt = nxt(unit, kt + 1, kt1)) {
+                    const uint32_t tm = tiles_of(unit, kt, nq);
                     for (int c = 0; c < C; ++c, ++it) {
                         const int s = it % CSTAGES;
                         mbar_wait(kempty(s), ((it / CSTAGES) & 1) ^ 1);
-                        mbar_expect_tx(kfull(s), (nq + 1) * QTILE + BIAS);
+                        mbar_expect_tx(kfull(s), (__popc(tm) + 1) * QTILE + BIAS);
                         const uint32_t dst = base + s * CSTAGE;
                         for (int t = 0; t < nq; ++t)
-                            bulk_g2s(dst + t * QTILE, p.qimg + (size_t(qt0 + t) * C + c) * QTILE,
-                                     QTILE, kfull(s));
+                            if ((tm >> t) & 1u)
+                                bulk_g2s(dst + t * QTILE, p.qimg + (size_t(qt0 + t) * C + c) * QTILE,
+                                         QTILE, kfull(s));
                         bulk_g2s(dst + 2 * QTILE, p.kimg + (size_t(kt) * C + c) * QTILE, QTILE,
                                  kfull(s));
                         bulk_g2s(dst + 3 * QTILE, p.kbias + size_t(kt) * BIAS, BIAS, kfull(s));
@@ -454,6 +464,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
                 const int kt0 = split * ktiles_per_split;
                 const int kt1 = min(p.k_tiles, kt0 + ktiles_per_split);
                 for (int kt = nxt(unit, kt0, kt1); kt < kt1; kt = nxt(unit, kt + 1, kt1), ++acc_it) {
+                    const uint32_t tmk = tiles_of(unit, kt, nq);
                     mbar_wait(accempty, (acc_it & 1) ^ 1);
                     fence_after();
                     for (int c = 0; c < C; ++c, ++it) {
@@ -462,6 +473,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
                         fence_after();
                         const uint32_t st = base + s * CSTAGE;
                         for (int t = 0; t < nq; ++t)
+                            if ((tmk >> t) & 1u)
                             issue_score_chunk<true>(tm + uint32_t(t * 2 * TILE),
                                               tm + uint32_t((t * 2 + 1) * TILE), st + t * QTILE,
                                               st + 2 * QTILE, base + C_OFF_ONES, st + 3 * QTILE,
@@ -501,10 +513,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
                 p.lab.nlab ? lab_table + (t < nq && row < p.R ? p.lab.qlab[row] : 0) * p.lab.nlab
                            : nullptr;
             for (int kt = nxt(unit, kt0, kt1); kt < kt1; kt = nxt(unit, kt + 1, kt1), ++acc_it) {
+                const bool mine = (tiles_of(unit, kt, nq) >> t) & 1u;
                 mbar_wait(accfull, acc_it & 1);
                 fence_after();
                 uint32_t v[128];
-                if (t < nq) {
+                if (mine) {
                     // score = big + small accumulator
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
@@ -521,7 +534,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
                 fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(accempty);
-                if (t >= nq) continue;
+                if (!mine) continue;
                 if (lab_row)
                     apply_label_cost<128>(v, p.lab, lab_row, int64_t(kt) * TILE, p.key_valid,
                                           reinterpret_cast<int*>(vb), lane);
@@ -548,6 +561,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
                                                      lane, umax);
                 if (!VEC && hit && p.live_global && lane == 0)
                     atomicOr(&p.live_global[(size_t(unit) * p.splits + split) * p.kwords + ((kt - kt0) >> 5)],
+                             1u << ((kt - kt0) & 31));
+                if (!VEC && hit && p.live_pt && lane == 0)
+                    atomicOr(&p.live_pt[((size_t(unit) * p.splits + split) * 2 + t) * p.kwords +
+                                        ((kt - kt0) >> 5)],
                              1u << ((kt - kt0) & 31));
             }
             if (t < nq && row >= p.row_begin && row < p.row_end) {
@@ -1431,7 +1448,8 @@ __device__ __forceinline__ int gen_next_live(const TcApplyGenParams& p, int u, i
     if (!p.live_in) return kt;
     while (kt < kt1) {
         const int ls = kt / p.in_kps, rel = kt - ls * p.in_kps;
-        const uint32_t w = __ldg(p.live_in + (size_t(u >> 1) * p.in_splits + ls) * p.in_kwords +
+        const uint32_t w = __ldg(p.live_in + ((size_t(u >> 1) * p.in_splits + ls) * 2 + (u & 1)) *
+                                                 p.in_kwords +
                                  (rel >> 5)) >> (rel & 31);
         if (w) return kt + __ffs(w) - 1;
         kt += 32 - (rel & 31);
@@ -2850,11 +2868,9 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         p.live_global = I.live_glob[side].get();
         if (!screen)
             FSKB_CUDA(cudaMemsetAsync(p.live_global, 0, words * sizeof(uint32_t), P.s));
-        if (I.chunks == 1 && !I.labeled) {
-            if (I.live_pt[side].size() < 2 * words) I.live_pt[side].alloc(2 * words, P.s);
-            p.live_pt = I.live_pt[side].get();
-            FSKB_CUDA(cudaMemsetAsync(p.live_pt, 0, 2 * words * sizeof(uint32_t), P.s));
-        }
+        if (I.live_pt[side].size() < 2 * words) I.live_pt[side].alloc(2 * words, P.s);
+        p.live_pt = I.live_pt[side].get();
+        FSKB_CUDA(cudaMemsetAsync(p.live_pt, 0, 2 * words * sizeof(uint32_t), P.s));
         I.live_valid[side] = true;
         I.live_kpot[side] = kpot;
         I.live_splits[side] = p.splits;
@@ -2867,9 +2883,16 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
                (row_begin - I.live_row_begin[side]) % (2 * TILE) == 0) {
         // rows inside the recorded set's range, on its 256-row unit grid: offset to
         // their units (a row shard of the HVP's transport passes)
-        p.live_in = I.live_glob[side].get() +
-                    size_t((row_begin - I.live_row_begin[side]) / (2 * TILE)) *
-                        size_t(I.live_splits[side]) * size_t(I.live_kwords[side]);
+        const size_t u0 = size_t((row_begin - I.live_row_begin[side]) / (2 * TILE)) *
+                          size_t(I.live_splits[side]) * size_t(I.live_kwords[side]);
+        if (I.chunks > 1) {
+            // d > 64: per-query-tile sets (the chunked kernel skips a dead tile's loads,
+            // MMAs and epilogue per key tile)
+            p.live_in = I.live_pt[side].get() + 2 * u0;
+            p.live_tq = 1;
+        } else {
+            p.live_in = I.live_glob[side].get() + u0;
+        }
         p.in_splits = I.live_splits[side];
         p.in_kps = I.live_kps[side];
         p.in_kwords = I.live_kwords[side];
@@ -3264,8 +3287,9 @@ void TcHalfStep::apply_mat(DevProblem<float>& P, int side, const float* kpot, fl
     if (I.live_valid[side] && I.live_kpot[side] == kpot && row_begin >= I.live_row_begin[side] &&
         row_end <= I.live_row_end[side] &&
         (row_begin - I.live_row_begin[side]) % (2 * TILE) == 0) {
-        g.live_in = I.live_glob[side].get() +
-                    size_t((row_begin - I.live_row_begin[side]) / (2 * TILE)) *
+        // per query tile (the kernel's work item is one query tile)
+        g.live_in = I.live_pt[side].get() +
+                    2 * size_t((row_begin - I.live_row_begin[side]) / (2 * TILE)) *
                         size_t(I.live_splits[side]) * size_t(I.live_kwords[side]);
         g.in_splits = I.live_splits[side];
         g.in_kps = I.live_kps[side];
