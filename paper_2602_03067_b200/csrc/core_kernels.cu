@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(NT) apply_kernel(ScoreParams<T> P, const T* __
                                                    const T* __restrict__ V, int64_t p,
                                                    const T* __restrict__ A,
                                                    const T* __restrict__ B, int64_t r,
-                                                   T* __restrict__ O) {
+                                                   T* __restrict__ O, int64_t per) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* Qs = reinterpret_cast<T*>(smem_raw);
     T* Ks = Qs + DK * (BM + 1);
@@ -228,9 +228,12 @@ __global__ void __launch_bounds__(NT) apply_kernel(ScoreParams<T> P, const T* __
     for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) o[ii][cc] = T(0);
-    for (int64_t J0 = 0; J0 < P.C; J0 += BN) {
+    // key split blockIdx.z: keys [z per, z per + per); partial O at O + z R p
+    const int64_t Jb = int64_t(blockIdx.z) * per, Je = min(P.C, Jb + per);
+    O += int64_t(blockIdx.z) * P.R * p;
+    for (int64_t J0 = Jb; J0 < Je; J0 += BN) {
         T sc[4][4];
-        score_tile<T, LAB>(P, I0, J0, P.C, sc, Qs, Ks);
+        score_tile<T, LAB>(P, I0, J0, Je, sc, Qs, Ks);
 #pragma unroll
         for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
@@ -397,10 +400,33 @@ void launch_viol_accumulate(const double* part, int nb, double* viol, cudaStream
     count_launch();
 }
 
+// O = sum over the key splits' partials, in split order (deterministic)
+template <typename T>
+__global__ void sum_splits_kernel(const T* __restrict__ part, int splits, int64_t n,
+                                  T* __restrict__ out) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    T v = part[i];
+    for (int k = 1; k < splits; ++k) v += part[size_t(k) * n + i];
+    out[i] = v;
+}
+
 template <typename T>
 void launch_apply(const ScoreParams<T>& P, const T* lse, const T* V, int64_t p, const T* A,
                   const T* B, int64_t r, T* O, cudaStream_t s) {
-    dim3 grid(unsigned((P.R + BM - 1) / BM), unsigned((p + PC - 1) / PC));
+    // small row counts fill the GPU with key splits (partials summed in split order)
+    const int64_t tiles = ((P.R + BM - 1) / BM) * ((p + PC - 1) / PC);
+    int64_t splits = (2 * int64_t(num_sms()) + tiles - 1) / tiles;
+    splits = std::max<int64_t>(1, std::min<int64_t>({splits, (P.C + BN - 1) / BN, 16}));
+    const int64_t per = ((P.C + splits - 1) / splits + BN - 1) / BN * BN;
+    splits = (P.C + per - 1) / per;
+    DevBuf<T> part;
+    T* dst = O;
+    if (splits > 1) {
+        part.alloc(size_t(splits) * size_t(P.R) * size_t(p), s);
+        dst = part.get();
+    }
+    dim3 grid(unsigned((P.R + BM - 1) / BM), unsigned((p + PC - 1) / PC), unsigned(splits));
     const std::size_t sm = apply_smem<T>();
     static bool configured = false;
     if (!configured) {
@@ -416,15 +442,21 @@ void launch_apply(const ScoreParams<T>& P, const T* lse, const T* V, int64_t p, 
     }
     const bool lab = P.qlab != nullptr, had = A != nullptr;
     if (lab && had)
-        apply_kernel<T, true, true><<<grid, NT, sm, s>>>(P, lse, V, p, A, B, r, O);
+        apply_kernel<T, true, true><<<grid, NT, sm, s>>>(P, lse, V, p, A, B, r, dst, per);
     else if (lab)
-        apply_kernel<T, true, false><<<grid, NT, sm, s>>>(P, lse, V, p, A, B, r, O);
+        apply_kernel<T, true, false><<<grid, NT, sm, s>>>(P, lse, V, p, A, B, r, dst, per);
     else if (had)
-        apply_kernel<T, false, true><<<grid, NT, sm, s>>>(P, lse, V, p, A, B, r, O);
+        apply_kernel<T, false, true><<<grid, NT, sm, s>>>(P, lse, V, p, A, B, r, dst, per);
     else
-        apply_kernel<T, false, false><<<grid, NT, sm, s>>>(P, lse, V, p, A, B, r, O);
+        apply_kernel<T, false, false><<<grid, NT, sm, s>>>(P, lse, V, p, A, B, r, dst, per);
     FSKB_CUDA(cudaGetLastError());
     count_launch();
+    if (splits > 1) {
+        const int64_t n = P.R * p;
+        sum_splits_kernel<T><<<blocks_for(n), 256, 0, s>>>(part.get(), int(splits), n, O);
+        FSKB_CUDA(cudaGetLastError());
+        count_launch();
+    }
 }
 
 template <typename T>

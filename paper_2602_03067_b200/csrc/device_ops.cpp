@@ -368,7 +368,6 @@ void grad_rows_fp64(const DevProblem<float>& P, const float* f, const float* g, 
     launch_grad_epilogue<double>(Pd.src.pts.get() + row_begin * d, O.get(),
                                  Pd.src.w.get() + row_begin, fd.get() + row_begin,
                                  lse.get() + row_begin, R, d, eps, out_dev, flags, s);
-    FSKB_CUDA(cudaStreamSynchronize(s));
 }
 
 template void half_step<float>(DevProblem<float>&, int, const float*, float,
