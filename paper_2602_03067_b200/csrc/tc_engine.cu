@@ -2641,10 +2641,8 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
             // Device-decided passes (large problems whose cold pass is the two-launch
             // screen): the prepass count, the cost model and the cold path's launches
             // all stay on the stream - no host read-back, the host runs ahead
-            static const bool dev_decide_on = [] {
-                const char* e = std::getenv("FSK_DEVICE_DECIDE");
-                return !(e && e[0] == '0');
-            }();
+            const char* dde = std::getenv("FSK_DEVICE_DECIDE");   // (read per pass: tests flip it)
+            const bool dev_decide_on = !(dde && dde[0] == '0');
             const int base_s = pick_splits(units, k_tiles, sms, base_min_s);
             const bool dd = dev_decide_on && can_screen && range_split && seed && !(m_init && ex) &&
                             base_s <= two_phase_max_splits() &&

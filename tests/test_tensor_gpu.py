@@ -759,6 +759,41 @@ def test_engine_solves_history_independent(fsk):
     eng.close()
 
 
+def test_device_decided_passes_match_host_decided(fsk):
+    """Large problems decide warm vs cold on the device (no host read-back): the
+    same decisions and bits as the host-decided path (FSK_DEVICE_DECIDE=0), and the
+    same pass-kind counts."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(404)
+    n = m = 1 << 18
+    X, Y = rng.normal(size=(n, 64)), rng.normal(size=(m, 64))
+    u = np.full(n, 1.0 / n)
+    out = {}
+    for flag in ("1", "0"):
+        os.environ["FSK_DEVICE_DECIDE"] = flag
+        try:
+            eng = fsk.Engine(0, X, u, Y, u, mode="tensor")
+            eng.set_eps(0.05)
+            f = torch.empty(n, dtype=torch.float32, device="cuda")
+            g = torch.empty(m, dtype=torch.float32, device="cuda")
+            eng.bind(f.data_ptr(), g.data_ptr())
+            eng.init_potentials()
+            for _ in range(8):
+                eng.half_step(0, 0, n)
+                eng.half_step(1, 0, m)
+            G = torch.empty((n, 64), dtype=torch.float32, device="cuda")
+            eng.grad(0, n, G.data_ptr())
+            torch.cuda.synchronize()
+            out[flag] = (f.cpu().numpy(), g.cpu().numpy(), G.cpu().numpy(), eng.pass_counts())
+            eng.close()
+        finally:
+            os.environ.pop("FSK_DEVICE_DECIDE", None)
+    for a_, b_ in zip(out["1"][:3], out["0"][:3]):
+        assert np.array_equal(a_, b_)
+    assert out["1"][3] == out["0"][3]
+    assert out["1"][3]["warm"] > 0 and out["1"][3]["screened"] > 0
+
+
 def test_persistent_small_solve(fsk, port, golden):
     """cfg1-class problems (keys fit in shared memory, d <= 16): the whole iteration
     loop is one cooperative kernel (small_solve.cu). Engine iterate and the drop-in
