@@ -270,6 +270,28 @@ __device__ __forceinline__ int live_in_next(const TcParams& p, int u, int kt, in
     return kt1;
 }
 
+// Warm live sets of the d > 64 kernel (half-granular, per query tile, bit
+// 2 (kt - split kps) + h of [unit][split][t][in_kwords]): the query tiles of unit u
+// with a live half in key tile kt, and the next key tile >= kt with any
+__device__ __forceinline__ uint32_t warm_tiles(const TcParams& p, int u, int kt) {
+    const int ls = kt / p.in_kps, q = 2 * (kt - ls * p.in_kps);
+    const uint32_t* b = p.live_in + (size_t(u) * p.in_splits + ls) * 2 * p.in_kwords + (q >> 5);
+    const uint32_t m0 = (__ldg(b) >> (q & 31)) & 3u, m1 = (__ldg(b + p.in_kwords) >> (q & 31)) & 3u;
+    return (m0 ? 1u : 0u) | (m1 ? 2u : 0u);
+}
+__device__ __forceinline__ int warm_next(const TcParams& p, int u, int kt, int kt1) {
+    while (kt < kt1) {
+        const int ls = kt / p.in_kps, q = 2 * (kt - ls * p.in_kps);
+        const uint32_t* b = p.live_in + (size_t(u) * p.in_splits + ls) * 2 * p.in_kwords + (q >> 5);
+        const uint32_t w = (__ldg(b) | __ldg(b + p.in_kwords)) >> (q & 31);
+        if (w) return kt + ((__ffs(w) - 1) >> 1);
+        const int qn = (q | 31) + 1;   // next word
+        kt += (qn - q) >> 1;
+        if (qn >= 2 * p.in_kps) kt = (ls + 1) * p.in_kps;
+    }
+    return kt1;
+}
+
 // Per-tile epilogue math shared by the K1 kernels: mask the padded keys of the
 // last tile, then either the online (max, sum-exp) update (LSE) or, with the row
 // LSE known, the transport-vector sum sum_j 2^(t - L) v_j (VEC). `v` holds the 128
@@ -413,11 +435,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
     // VEC at fixed potentials: only the key tiles of the LSE pass's live set (the
     // union of both query tiles'; with per-tile sets (live_tq) a tile that is not live
     // for a key tile is neither loaded, multiplied nor read back)
+    // warm LSE passes (live_in, !VEC): half-granular warm live sets, tile-skipped
+    const bool warm = !VEC && p.live_in && p.live_tq;
     auto nxt = [&](int unit, int kt, int kt1) {
+        if (warm) return warm_next(p, unit, kt, kt1);
         return (VEC && p.live_in) ? live_in_next(p, unit, kt, kt1, -1, p.live_tq != 0) : kt;
     };
     auto tiles_of = [&](int unit, int kt, int nq) -> uint32_t {
         const uint32_t all = nq > 1 ? 3u : 1u;
+        if (warm) return warm_tiles(p, unit, kt) & all;
         if (!(VEC && p.live_in && p.live_tq)) return all;
         return (uint32_t(live_in_bit(p, unit, 0, kt)) | (uint32_t(live_in_bit(p, unit, 1, kt)) << 1)) &
                all;
@@ -512,6 +538,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
             const float* lab_row =
                 p.lab.nlab ? lab_table + (t < nq && row < p.R ? p.lab.qlab[row] : 0) * p.lab.nlab
                            : nullptr;
+            int best_sub = -1;   // half index 2 kt + h of the running max (warm bookkeeping)
             for (int kt = nxt(unit, kt0, kt1); kt < kt1; kt = nxt(unit, kt + 1, kt1), ++acc_it) {
                 const bool mine = (tiles_of(unit, kt, nq) >> t) & 1u;
                 mbar_wait(accfull, acc_it & 1);
@@ -556,9 +583,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
                         }
                     }
                 }
-                float umax;
-                const bool hit = k1_tile_update<VEC>(v, int64_t(kt) * TILE, p, M, S, nlh, nll, vb,
-                                                     lane, umax);
+                bool hit;
+                if constexpr (VEC) {
+                    float umax;
+                    hit = k1_tile_update<VEC>(v, int64_t(kt) * TILE, p, M, S, nlh, nll, vb, lane,
+                                              umax);
+                } else {
+                    // two 64-key halves: per-half gap bounds and argmax for the warm passes
+                    hit = false;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const float M_old = M;
+                        float uh;
+                        hit |= k1_tile_update<false, 64>(
+                            *reinterpret_cast<uint32_t(*)[64]>(v + 64 * h), int64_t(kt) * TILE + 64 * h,
+                            p, M, S, nlh, nll, vb, lane, uh);
+                        if (M > M_old) best_sub = 2 * kt + h;
+                        if (p.gap) {
+                            const float gv = row < p.R ? uh - M : -INFINITY;
+                            const int gmax = __reduce_max_sync(0xffffffffu, fenc(gv));
+                            if (lane == 0)
+                                atomicMax(&p.gap[size_t(2 * unit + t) * 2 * size_t(p.k_tiles) + 2 * kt + h],
+                                          gmax);
+                        }
+                    }
+                }
                 if (!VEC && hit && p.live_global && lane == 0)
                     atomicOr(&p.live_global[(size_t(unit) * p.splits + split) * p.kwords + ((kt - kt0) >> 5)],
                              1u << ((kt - kt0) & 31));
@@ -574,6 +623,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_chunked_kernel(const Tc
                     // natural-log partials: max_j S_ij = M ln2, sum_j exp(S_ij - max) = S
                     p.part_m[size_t(split) * p.R + row] = double(M) * 0.69314718055994530942;
                     p.part_s[size_t(split) * p.R + row] = S;
+                    if (p.part_arg) p.part_arg[size_t(split) * p.R + row] = best_sub;
                 }
             }
         }
@@ -1993,7 +2043,7 @@ __global__ void fill_int_kernel(int* __restrict__ p, int64_t n, int v) {
 __global__ void warm_prepass_kernel(int* __restrict__ gap, const int* __restrict__ tile_dmax,
                                     const int* __restrict__ lam, int units, int k_tiles, int splits,
                                     int kps, int kwords, float skip, uint32_t* __restrict__ live,
-                                    unsigned long long* __restrict__ live_count) {
+                                    unsigned long long* __restrict__ live_count, int count_tiles) {
     // one warp per live-set word (u, split, t, w), one lane per half: coalesced gap
     // and bias-change reads, the word by ballot; one counter update per block
     const int64_t words = int64_t(units) * splits * 2 * kwords;
@@ -2018,7 +2068,8 @@ __global__ void warm_prepass_kernel(int* __restrict__ gap, const int* __restrict
         const uint32_t bits = __ballot_sync(0xffffffffu, is_live);
         if (lane == 0) {
             live[wid] = bits;   // [u][split][t][w]
-            nlive += __popc(bits);
+            // live halves, or (the d > 64 kernel computes whole tiles) live key tiles
+            nlive += count_tiles ? __popc((bits | (bits >> 1)) & 0x55555555u) : __popc(bits);
         }
     }
     __shared__ unsigned blk;
@@ -2521,8 +2572,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
     const int k_tiles = int(I.rows_pad[kc] / TILE);
     // warm bounds: LSE passes of the d <= 64 kernel (FSK_WARM=0 disables)
     const char* wenv = std::getenv("FSK_WARM");
-    bool warm_track = !vec && I.chunks == 1 && !I.labeled && !break_lse_flag() &&
-                      !(wenv && wenv[0] == '0');
+    bool warm_track = !vec && !I.labeled && !break_lse_flag() && !(wenv && wenv[0] == '0');
     // small problems: the bookkeeping would not pay (and the probe read-back waits)
     const int64_t q_units = ((row_end + TILE - 1) / TILE - row_begin / TILE + 1) / 2;
     if (q_units * (I.rows_pad[kc] / TILE) < (int64_t(1) << 16)) warm_track = false;
@@ -2655,7 +2705,8 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
                 warm_prepass_kernel<<<unsigned(std::min<size_t>(4 * size_t(sms), (2 * words + 7) / 8)),
                                       256, 0, P.s>>>(
                     I.gap[side].get(), I.tdmax[side].get(), I.lam[side].get(), units, n_ktiles,
-                    p.splits, kps, kw, I.skip[side], I.warm_live[side].get(), &st[side].acc[5]);
+                    p.splits, kps, kw, I.skip[side], I.warm_live[side].get(), &st[side].acc[5],
+                    I.chunks > 1 ? 1 : 0);
                 decide_kernel<<<1, 32, 0, P.s>>>(st, blocks, can_screen ? 1 : 0, side);
                 const int* cold = &st[side].cold;
                 // cold: bounds re-measured from scratch, live set rebuilt by phase 1
@@ -2706,7 +2757,8 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
             warm_prepass_kernel<<<unsigned(std::min<size_t>(4 * size_t(sms), (2 * words + 7) / 8)),
                                   256, 0, P.s>>>(
                 I.gap[side].get(), I.tdmax[side].get(), I.lam[side].get(), units, n_ktiles,
-                p.splits, kps, kw, I.skip[side], I.warm_live[side].get(), cnt);
+                p.splits, kps, kw, I.skip[side], I.warm_live[side].get(), cnt,
+                I.chunks > 1 ? 1 : 0);
             FSKB_CUDA(cudaGetLastError());
             count_launch(3);
             // the live fraction decides this pass: wait for it (the stream is drained up
@@ -2715,7 +2767,8 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
                                       cudaMemcpyDeviceToHost, P.s));
             FSKB_CUDA(cudaEventRecord(I.ev[side], P.s));
             FSKB_CUDA(cudaEventSynchronize(I.ev[side]));
-            const double blocks = double(p.q_tiles) * 2.0 * double(n_ktiles);   // halves
+            // halves (d <= 64), or key tiles (the d > 64 kernel skips whole tiles)
+            const double blocks = double(p.q_tiles) * (I.chunks > 1 ? 1.0 : 2.0) * double(n_ktiles);
             const double est = double(I.h_live[side]) / std::max(1.0, blocks);
             // mostly live (right after a restart of the potentials, whose bias change
             // voids the bounds): a cold pass re-seeds the bounds for less. Cost model in
