@@ -129,22 +129,20 @@ __device__ __forceinline__ float group_max32(const uint32_t (&v)[W], int c) {
 
 // Label-augmented cost on the tensor path (chunked K1 and the general transport
 // kernel): labels of the query and key rows, the V x V table in log2 units
-// (lambda2 log2(e) W / eps; row = query label when !trans, else key label).
+// (lambda2 log2(e) W / eps), indexed W[query label][key label] in both orientations
+// like the reference (its g-side context keeps W with the target labels as rows,
+// stream.cpp:239-242).
 struct LabelArgs {
     const int32_t* qlab = nullptr;
     const int32_t* klab = nullptr;
     const float* wl2 = nullptr;
     int nlab = 0;     // V (0: squared Euclidean)
-    int trans = 0;    // 1: read W^T (unused: the reference never transposes W)
 };
 
 // stage the table in shared memory in query-label-major order, in accumulator units
 __device__ __forceinline__ void stage_label_table(const LabelArgs& L, float inv_acc, float* dst) {
     const int V = L.nlab;
-    for (int e = threadIdx.x; e < V * V; e += blockDim.x) {
-        const int a = e / V, b = e - a * V;
-        dst[e] = (L.trans ? L.wl2[b * V + a] : L.wl2[e]) * inv_acc;
-    }
+    for (int e = threadIdx.x; e < V * V; e += blockDim.x) dst[e] = L.wl2[e] * inv_acc;
 }
 
 // v[j] -= W[l_row, l_key(kbase + j)] for the W columns of this thread's row; the warp
@@ -2966,9 +2964,6 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
         p.lab.klab = ks.lab.get();
         p.lab.wl2 = I.wl2.get();
         p.lab.nlab = I.nlab;
-        // both orientations index W[query label][key label]: the reference's g-side
-        // context takes W as is with the target's labels as rows (stream.cpp:239-242)
-        p.lab.trans = 0;
     }
     if (I.chunks == 1 && !I.labeled) {
         if (vec)
@@ -3351,7 +3346,6 @@ void TcHalfStep::apply_mat(DevProblem<float>& P, int side, const float* kpot, fl
         g.lab.klab = ks.lab.get();
         g.lab.wl2 = I.wl2.get();
         g.lab.nlab = I.nlab;
-        g.lab.trans = 0;   // W[query label][key label] (stream.cpp:239-242, :354)
     }
     const int vc_max = A ? 2 : 4;
     Scratch& part = Scratch::local();
