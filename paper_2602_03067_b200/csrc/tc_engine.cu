@@ -2221,6 +2221,19 @@ int two_phase_max_splits() {
     return v;
 }
 
+// Least key-split count of a screened cold pass (FSK_P1_SPLITS, default 1). More
+// splits keep the key range the running CTAs stream L2-resident (cfg3 phase-1
+// DRAM 18 -> 17 GB per launch at 2) but each split screens against its own running
+// max: without a seed (the first pass of each side) the live set grows 0.072 ->
+// 0.126 of the halves and cfg3 loses 9% (gpurun_out/r02ae)
+int screen_min_splits() {
+    static const int v = [] {
+        const char* e = std::getenv("FSK_P1_SPLITS");
+        return e ? std::max(1, std::atoi(e)) : 1;
+    }();
+    return v;
+}
+
 // Key split that best fills a persistent grid of `sms` CTAs with units x splits items.
 // key-range size of the L2-local splits (warm passes, sparse K3); FSK_WARM_RANGE_MB
 double warm_range_bytes() {
@@ -2620,6 +2633,9 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
     const double q_bytes = 2.0 * I.chunks * QTILE;
     const int base_min_s = I.chunks > 1 ? int(std::ceil(sms * q_bytes / (48.0 * (1 << 20)))) : 1;
     int min_s = base_min_s;
+    // cold (screened) passes of the d <= 64 kernel: at least screen_min_splits() key
+    // splits, so that the CTAs running together stream a key range that stays in L2
+    const int cold_min_s = I.chunks == 1 ? std::max(base_min_s, screen_min_splits()) : base_min_s;
     // warm passes skip most key tiles, so the CTAs drift apart in the key sequence
     // and every live block would be an HBM read: split the keys into ranges that
     // stay L2-resident (~40 MB; items run split-major, item_coords)
@@ -2631,6 +2647,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
     }();
     if (warm && range_split)
         min_s = std::max(min_s, int(std::ceil(double(k_tiles) * KSTAGE / warm_range_bytes())));
+    if (warm_track && !warm) min_s = cold_min_s;
     // warm live sets are staged in shared memory: <= kMaxWarmKps key tiles per split
     if (warm) min_s = std::max(min_s, (k_tiles + kMaxWarmKps - 1) / kMaxWarmKps);
     p.splits = pick_splits(units, k_tiles, sms, min_s);
@@ -2691,7 +2708,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
             // all stay on the stream - no host read-back, the host runs ahead
             const char* dde = std::getenv("FSK_DEVICE_DECIDE");   // (read per pass: tests flip it)
             const bool dev_decide_on = !(dde && dde[0] == '0');
-            const int base_s = pick_splits(units, k_tiles, sms, base_min_s);
+            const int base_s = pick_splits(units, k_tiles, sms, cold_min_s);
             const bool dd = dev_decide_on && can_screen && range_split && seed && !(m_init && ex) &&
                             base_s <= two_phase_max_splits() &&
                             (k_tiles + base_s - 1) / base_s <= kMaxScreenTiles &&
@@ -2791,11 +2808,11 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
             }
             }   // !dd
         }
-        if (go_cold && p.splits != pick_splits(units, k_tiles, sms, base_min_s)) {
+        if (go_cold && p.splits != pick_splits(units, k_tiles, sms, cold_min_s)) {
             // the key-range splits serve the warm live sets; a screened pass keeps one
             // running max over the whole key range (a split-local screened max would
             // admit far more tiles when the row has no good seed)
-            p.splits = pick_splits(units, k_tiles, sms, base_min_s);
+            p.splits = pick_splits(units, k_tiles, sms, cold_min_s);
             p.items = units * p.splits;
             grid = std::min(p.items, sms);
             kps = (k_tiles + p.splits - 1) / p.splits;
