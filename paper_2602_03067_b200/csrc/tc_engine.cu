@@ -981,7 +981,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                 // m_init - (delta + slack), a lower bound of its screened max
                 float Ma = M > -INFINITY ? M - 0.5f * (p.screen_thr - p.skip) : -INFINITY;
                 const bool row_ok = t < nq && row < p.R;
-                unsigned nl = 0;   // screen-only: halves newly marked live by this warp
+                unsigned nl = 0;   // screen-only: halves newly marked live by this thread
+                // screen-only: this row's candidate halves (absolute half index, screened max)
+                constexpr int kCand = 24;
+                int cand_q[kCand];
+                float cand_v[kCand];
+                int ncand = 0;
+                // the half's bit in the phase-2 launch's live set; 1 if newly set
+                auto mark_live = [&](int hq) -> unsigned {
+                    const int kt_ = hq >> 1, s2 = kt_ / p.out_kps;
+                    const int q = 2 * (kt_ - s2 * p.out_kps) + (hq & 1);
+                    const uint32_t bit = 1u << (q & 31);
+                    const uint32_t old = atomicOr(
+                        &p.live_out[((size_t(unit) * p.out_splits + s2) * 2 + t) * p.out_kwords +
+                                    (q >> 5)],
+                        bit);
+                    return (old & bit) ? 0u : 1u;
+                };
                 for (int kt = kt0; kt < kt1; ++kt) {
                     if (t < nq) {
                         float tmax = -INFINITY, th[2];
@@ -1023,24 +1039,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                                     atomicMax(&p.gap[size_t(2 * unit + t) * nsub_all + 2 * kt + h],
                                               gmax);
                             }
-                            if (p.screen_only &&
-                                __any_sync(0xffffffffu, row_ok && th[h] >= Ma - p.screen_thr) &&
-                                lane == 0) {
-                                // the half's bit in the phase-2 launch's live set (this
-                                // launch runs one split, kt0 = 0)
-                                const int s2 = kt / p.out_kps;
-                                const int q = 2 * (kt - s2 * p.out_kps) + h;
-                                const uint32_t bit = 1u << (q & 31);
-                                const uint32_t old = atomicOr(
-                                    &p.live_out[((size_t(unit) * p.out_splits + s2) * 2 + t) *
-                                                    p.out_kwords + (q >> 5)], bit);
-                                nl += (old & bit) ? 0u : 1u;
+                            if (p.screen_only && row_ok && th[h] >= Ma - p.screen_thr) {
+                                // a candidate of this row: decided against the row's final
+                                // screened max at the end of the sweep (the running max
+                                // sets ~ln(#tiles) records per row, most of them dead
+                                // against the final one); a full list marks it now
+                                if (ncand < kCand) {
+                                    cand_q[ncand] = 2 * kt + h;
+                                    cand_v[ncand] = th[h];
+                                    ++ncand;
+                                } else {
+                                    nl += mark_live(2 * kt + h);
+                                }
                             }
                         }
                     }
                 }
-                if (p.screen_only && p.live_count && lane == 0 && nl)
-                    atomicAdd(p.live_count, (unsigned long long)nl);
+                if (p.screen_only) {
+                    for (int c = 0; c < ncand; ++c)
+                        if (cand_v[c] >= Ma - p.screen_thr) nl += mark_live(cand_q[c]);
+                    const unsigned wl = __reduce_add_sync(0xffffffffu, nl);
+                    if (p.live_count && lane == 0 && wl) atomicAdd(p.live_count, (unsigned long long)wl);
+                }
                 // the split's true max is >= the screened max - (delta + slack):
                 // seed the running max there (earlier in-epilogue skips)
                 if (!VEC && row_ok && Ma > -INFINITY)
