@@ -1030,10 +1030,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                                      1u << ((kt - kt0) & 31));
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
+                            // a screen-only candidate that enters this row's list is decided -
+                            // and its gap seed written - against the row's final screened max
+                            const bool defer = p.screen_only && row_ok &&
+                                               th[h] >= Ma - p.screen_thr && ncand < kCand;
                             if (p.gap) {
                                 // warm-bound seed: true gap <= screened gap + 2 delta + slack
-                                const float gv = row_ok ? th[h] - Ma + (p.screen_thr - p.skip)
-                                                        : -INFINITY;
+                                const float gv = row_ok && !defer
+                                                     ? th[h] - Ma + (p.screen_thr - p.skip)
+                                                     : -INFINITY;
                                 const int gmax = __reduce_max_sync(0xffffffffu, fenc(gv));
                                 if (lane == 0)
                                     atomicMax(&p.gap[size_t(2 * unit + t) * nsub_all + 2 * kt + h],
@@ -1056,8 +1061,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                     }
                 }
                 if (p.screen_only) {
-                    for (int c = 0; c < ncand; ++c)
+                    for (int c = 0; c < ncand; ++c) {
                         if (cand_v[c] >= Ma - p.screen_thr) nl += mark_live(cand_q[c]);
+                        if (p.gap)
+                            atomicMax(&p.gap[size_t(2 * unit + t) * nsub_all + cand_q[c]],
+                                      fenc(cand_v[c] - Ma + (p.screen_thr - p.skip)));
+                    }
                     const unsigned wl = __reduce_add_sync(0xffffffffu, nl);
                     if (p.live_count && lane == 0 && wl) atomicAdd(p.live_count, (unsigned long long)wl);
                 }
