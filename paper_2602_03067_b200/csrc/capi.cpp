@@ -10,6 +10,7 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <exception>
 
 #include "../../include/fsk_b200.h"
 #include "common.h"
@@ -958,15 +959,57 @@ int fsk_sinkhorn_divergence_batch(const fsk_measure* mus, const fsk_measure* nus
                                   const fsk_tiles* tiles, fsk_ledger* ledger, double* out) {
     return guarded([&] {
         validate_config_raw(*cfg);
-        UploadCacheScope uploads;   // each distinct cloud crosses the host link once
-        BatchMemoScope memo;        // and is scanned / normed on the host once
-        for (int64_t k = 0; k < pairs; ++k) {
-            common_checks(&mus[k], &nus[k], cost, tiles);
-            const double cross = solve_dual(mus[k], nus[k], cost, *cfg, *tiles, ledger);
-            const double smu = solve_dual(mus[k], mus[k], cost, *cfg, *tiles, ledger);
-            const double snu = solve_dual(nus[k], nus[k], cost, *cfg, *tiles, ledger);
-            out[k] = cross - 0.5 * smu - 0.5 * snu;
+        {
+            BatchMemoScope memo;   // each distinct cloud is validated once
+            for (int64_t k = 0; k < pairs; ++k) common_checks(&mus[k], &nus[k], cost, tiles);
         }
+        // pairs are independent: FSK_BATCH_WORKERS host workers, each with its own
+        // stream (exec_ctx), upload cache and host memo, can run them concurrently.
+        // Default 1: at cfg5 two or three workers measured the same throughput (the
+        // busier GPU drops to the power-capped clock)
+        static const int workers_env = [] {
+            const char* e = std::getenv("FSK_BATCH_WORKERS");
+            return e ? std::max(1, std::atoi(e)) : 1;
+        }();
+        const int W = int(std::min<int64_t>(workers_env, pairs));
+        int dev = 0;
+        FSKB_CUDA(cudaGetDevice(&dev));
+        std::vector<fsk_ledger> led(size_t(W), fsk_ledger{});
+        std::vector<std::exception_ptr> err(static_cast<std::size_t>(W));
+        auto work = [&](int w) {
+            try {
+                FSKB_CUDA(cudaSetDevice(dev));
+                UploadCacheScope uploads;   // each distinct cloud crosses the host link once
+                BatchMemoScope memo;        // (per worker) and is scanned / normed once
+                fsk_ledger* L = ledger ? &led[size_t(w)] : nullptr;
+                for (int64_t k = w; k < pairs; k += W) {
+                    const double cross = solve_dual(mus[k], nus[k], cost, *cfg, *tiles, L);
+                    const double smu = solve_dual(mus[k], mus[k], cost, *cfg, *tiles, L);
+                    const double snu = solve_dual(nus[k], nus[k], cost, *cfg, *tiles, L);
+                    out[k] = cross - 0.5 * smu - 0.5 * snu;
+                }
+            } catch (...) {
+                err[size_t(w)] = std::current_exception();
+            }
+        };
+        if (W <= 1) {
+            work(0);
+        } else {
+            std::vector<std::thread> th;
+            for (int w = 0; w < W; ++w) th.emplace_back(work, w);
+            for (auto& t : th) t.join();
+        }
+        for (auto& e : err)
+            if (e) std::rethrow_exception(e);
+        if (ledger)
+            for (const auto& l : led) {
+                ledger->slow_to_fast_scalars += l.slow_to_fast_scalars;
+                ledger->fast_to_slow_scalars += l.fast_to_slow_scalars;
+                ledger->kernel_invocations += l.kernel_invocations;
+                ledger->transport_vector_applies += l.transport_vector_applies;
+                ledger->transport_matrix_applies += l.transport_matrix_applies;
+                ledger->hadamard_applies += l.hadamard_applies;
+            }
     });
 }
 

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
@@ -155,8 +156,8 @@ private:
 };
 
 // Global launch counter (the bench reports how many of our kernels ran).
-int64_t& launch_counter();
-inline void count_launch(int k = 1) { launch_counter() += k; }
+std::atomic<int64_t>& launch_counter();   // (batch workers launch from several threads)
+inline void count_launch(int k = 1) { launch_counter().fetch_add(k, std::memory_order_relaxed); }
 
 // Negative-control toggle (fsk::stream::debug_break_lse).
 bool& break_lse_flag();

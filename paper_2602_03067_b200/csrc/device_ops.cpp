@@ -12,8 +12,8 @@
 
 namespace fskb {
 
-int64_t& launch_counter() {
-    static int64_t c = 0;
+std::atomic<int64_t>& launch_counter() {
+    static std::atomic<int64_t> c{0};
     return c;
 }
 

@@ -626,7 +626,7 @@ void fsk_engine_pass_counts(const fsk_engine* e, uint64_t out[3]) {
 
 int64_t fsk_engine_kernel_launches(const fsk_engine* e) {
     (void)e;
-    return launch_counter();
+    return launch_counter().load();
 }
 
 const char* fsk_engine_path(const fsk_engine* e) { return tensor_path_name(e->P); }
