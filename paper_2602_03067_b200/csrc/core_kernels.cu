@@ -340,6 +340,85 @@ __global__ void grad_epilogue_kernel(const T* X, const T* O, const T* w, const T
     G[idx] = v;
 }
 
+// Small-d fp64 gradient in ONE pass (grad_rows_fp64 for d <= 16 without labels):
+// per row an online (max, sum, sum e^s y) over all keys, one warp per row, lanes
+// striding the keys, merged across lanes at the end; G_i = 2 r_i (x_i - O_i) with
+// O_i = (sum e^s y) / sum, r_i = a_i exp(f_i / eps + lse_i) (the epilogue above).
+// The per-key terms are prepared once: kb_j = (g_j + eps log b_j) / eps, ky_j =
+// y_j 2 s / eps, the scores formed as the two-pass path forms them.
+__global__ void grad_small_prep_kernel(const float* __restrict__ Y, const float* __restrict__ wy,
+                                       const float* __restrict__ g, int64_t C, int d, double eps,
+                                       double kscale, double* __restrict__ kb,
+                                       double* __restrict__ ky) {
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= C) return;
+    kb[j] = (double(g[j]) + eps * log(double(wy[j]))) / eps;
+    for (int t = 0; t < d; ++t) ky[j * d + t] = double(Y[j * d + t]) * kscale;
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) grad_small_fp64_kernel(
+    const float* __restrict__ X, const float* __restrict__ wx, const float* __restrict__ f,
+    const float* __restrict__ Y, const double* __restrict__ kb, const double* __restrict__ ky,
+    int64_t row_begin, int64_t R, int64_t C, double eps, double* __restrict__ G, int* flags) {
+    const int lane = threadIdx.x & 31;
+    const int64_t li = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (li >= R) return;   // whole warps
+    const int64_t i = row_begin + li;
+    double q[D], v[D];
+#pragma unroll
+    for (int t = 0; t < D; ++t) {
+        q[t] = double(X[i * D + t]);
+        v[t] = 0.0;
+    }
+    double m = -INFINITY, s = 0.0;
+    for (int64_t j = lane; j < C; j += 32) {
+        double sc = 0.0;
+#pragma unroll
+        for (int t = 0; t < D; ++t) sc = fma(q[t], __ldg(ky + j * D + t), sc);
+        sc += __ldg(kb + j);
+        if (!(sc > -INFINITY)) continue;   // zero-weight key
+        if (sc > m) {
+            const double a = exp(m - sc);
+            s *= a;
+#pragma unroll
+            for (int t = 0; t < D; ++t) v[t] *= a;
+            m = sc;
+        }
+        const double e = exp(sc - m);
+        s += e;
+#pragma unroll
+        for (int t = 0; t < D; ++t) v[t] = fma(e, double(__ldg(Y + j * D + t)), v[t]);
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        const double mo = __shfl_xor_sync(0xffffffffu, m, off);
+        const double so = __shfl_xor_sync(0xffffffffu, s, off);
+        const double M = fmax(m, mo);
+        const double a = m > -INFINITY ? exp(m - M) : 0.0;
+        const double b = mo > -INFINITY ? exp(mo - M) : 0.0;
+        s = s * a + so * b;
+#pragma unroll
+        for (int t = 0; t < D; ++t) {
+            const double vo = __shfl_xor_sync(0xffffffffu, v[t], off);
+            v[t] = v[t] * a + vo * b;
+        }
+        m = M;
+    }
+    if (lane == 0) {
+        const double lse = m + log(s);
+        const double ri = double(wx[i]) * exp(double(f[i]) / eps + lse);
+        bool bad = false;
+#pragma unroll
+        for (int t = 0; t < D; ++t) {
+            const double gv = 2.0 * ri * (q[t] - v[t] / s);
+            bad |= !isfinite(gv);
+            G[li * D + t] = gv;
+        }
+        if (bad) atomicOr(flags, kFlagNonFiniteTransport);
+    }
+}
+
 inline unsigned blocks_for(int64_t n, int t = 256) { return unsigned((n + t - 1) / t); }
 
 template <typename T>
@@ -519,6 +598,33 @@ void launch_grad_epilogue(const T* X, const T* O, const T* w, const T* pot, cons
                                                               flags);
     FSKB_CUDA(cudaGetLastError());
     count_launch();
+}
+
+bool launch_grad_small_fp64(const float* X, const float* wx, const float* f, const float* Y,
+                            const float* wy, const float* g, int64_t row_begin, int64_t R,
+                            int64_t C, int d, double eps, double kscale, double* G, int* flags,
+                            cudaStream_t s) {
+    if (d < 1 || d > 16) return false;
+    if (!R) return true;
+    DevBuf<double> kb(size_t(C), s), ky(size_t(C) * size_t(d), s);
+    grad_small_prep_kernel<<<blocks_for(C), 256, 0, s>>>(Y, wy, g, C, d, eps, kscale, kb.get(),
+                                                         ky.get());
+    const unsigned blocks = unsigned((R * 32 + 255) / 256);
+    switch (d) {
+#define FSKB_GS_CASE(DD)                                                                     \
+    case DD:                                                                                 \
+        grad_small_fp64_kernel<DD><<<blocks, 256, 0, s>>>(X, wx, f, Y, kb.get(), ky.get(),   \
+                                                          row_begin, R, C, eps, G, flags);   \
+        break;
+        FSKB_GS_CASE(1) FSKB_GS_CASE(2) FSKB_GS_CASE(3) FSKB_GS_CASE(4) FSKB_GS_CASE(5)
+        FSKB_GS_CASE(6) FSKB_GS_CASE(7) FSKB_GS_CASE(8) FSKB_GS_CASE(9) FSKB_GS_CASE(10)
+        FSKB_GS_CASE(11) FSKB_GS_CASE(12) FSKB_GS_CASE(13) FSKB_GS_CASE(14) FSKB_GS_CASE(15)
+        FSKB_GS_CASE(16)
+#undef FSKB_GS_CASE
+    }
+    FSKB_CUDA(cudaGetLastError());
+    count_launch(2);
+    return true;
 }
 
 #define FSKB_INSTANTIATE(T)                                                                     \

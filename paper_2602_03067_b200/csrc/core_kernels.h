@@ -116,5 +116,11 @@ void launch_f32_to_f64(const float* in, double* out, int64_t n, cudaStream_t s);
 template <typename T>
 void launch_grad_epilogue(const T* X, const T* O, const T* w, const T* pot, const T* lse,
                           int64_t R, int64_t d, T eps, T* G, int* flags, cudaStream_t s);
+// d <= 16, float problem: G rows [row_begin, row_begin + R) = 2 (r_i x_i - (P Y)_i) in
+// fp64 in one pass (online max / sum / transport); false when d is out of range
+bool launch_grad_small_fp64(const float* X, const float* wx, const float* f, const float* Y,
+                            const float* wy, const float* g, int64_t row_begin, int64_t R,
+                            int64_t C, int d, double eps, double kscale, double* G, int* flags,
+                            cudaStream_t s);
 
 }  // namespace fskb

@@ -320,6 +320,15 @@ void grad_rows_fp64(const DevProblem<float>& P, const float* f, const float* g, 
                     cudaStream_t s) {
     const int64_t n = P.src.n, m = P.tgt.n, d = P.src.d, R = row_end - row_begin;
     if (R <= 0) return;
+    static const bool fused = [] {
+        const char* e = std::getenv("FSK_GRAD_FUSED");
+        return !(e && e[0] == '0');
+    }();
+    if (fused && !P.labeled &&
+        launch_grad_small_fp64(P.src.pts.get(), P.src.w.get(), f, P.tgt.pts.get(), P.tgt.w.get(),
+                               g, row_begin, R, m, int(d), eps, 2.0 * P.fscale / eps, out_dev,
+                               flags, s))
+        return;
     DevProblem<double> Pd;
     Pd.s = s;
     Pd.fscale = P.fscale;

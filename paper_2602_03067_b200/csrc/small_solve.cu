@@ -16,6 +16,8 @@
 // result differs from the per-launch path at fp32 rounding (contract of SURVEY §8d).
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "common.h"
 #include "small_solve.h"
 
@@ -120,19 +122,126 @@ __global__ void __launch_bounds__(kThreads, 1) small_solve_kernel(const SmallSol
     }
 }
 
+// Resident variant (both clouds fit in shared memory next to the bias row): the
+// clouds (SoA) and the log2 weights are staged ONCE per launch; a half-step only
+// refreshes the key bias from the other side's new potential (one coalesced read
+// of m floats per CTA). Rows are dealt round-robin over the grid (row r -> CTA
+// r mod G, warp r / G), so every SM holds ceil(R / G) rows instead of 32 rows on
+// R / 32 SMs. Scores: bias_j + sum_t (x_t 2 s log2e / eps) y_t, the query
+// pre-scaled in registers.
 template <int D>
-void launch_d(const SmallSolveParams& p, int grid, size_t smem, cudaStream_t s) {
+__global__ void __launch_bounds__(kThreads, 1) small_solve_res_kernel(const SmallSolveParams p) {
+    extern __shared__ __align__(16) float sm[];
+    cg::grid_group grid = cg::this_grid();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t np = p.npad, mp = p.mpad;
+    float* xs = sm;             // D x np
+    float* ys = xs + D * np;    // D x mp
+    float* lx = ys + D * mp;    // log2 a, -inf past n
+    float* ly = lx + np;        // log2 b, -inf past m
+    float* bias = ly + mp;      // max(np, mp)
+    constexpr float kLog2e = 1.4426950408889634f;
+    for (int64_t j = threadIdx.x; j < np; j += kThreads) {
+        const bool v = j < p.n;
+#pragma unroll
+        for (int t = 0; t < D; ++t) xs[t * np + j] = v ? p.X[j * D + t] : 0.0f;
+        lx[j] = v ? p.logw_x[j] * kLog2e : -INFINITY;
+    }
+    for (int64_t j = threadIdx.x; j < mp; j += kThreads) {
+        const bool v = j < p.m;
+#pragma unroll
+        for (int t = 0; t < D; ++t) ys[t * mp + j] = v ? p.Y[j * D + t] : 0.0f;
+        ly[j] = v ? p.logw_y[j] * kLog2e : -INFINITY;
+    }
+    const int64_t G = gridDim.x;
+    for (int it = 0; it < p.iters; ++it) {
+        const float eps = p.eps_sched[it];
+        const float qscale = 2.0f * p.fscale / eps * kLog2e;
+        const float bscale = kLog2e / eps;
+        for (int side = 0; side < 2; ++side) {
+            const float* Qs = side == 0 ? xs : ys;
+            const float* Ks = side == 0 ? ys : xs;
+            const float* klw = side == 0 ? ly : lx;
+            const float* kpot = side == 0 ? p.g : p.f;   // written by this launch: no __ldg
+            float* out = side == 0 ? p.f : p.g;
+            const int64_t qp = side == 0 ? np : mp, kp = side == 0 ? mp : np;
+            const int64_t R = side == 0 ? p.n : p.m, C = side == 0 ? p.m : p.n;
+            __syncthreads();   // (the previous half-step's rows are done with bias)
+            for (int64_t j = threadIdx.x; j < kp; j += kThreads)
+                bias[j] = fmaf(j < C ? kpot[j] : 0.0f, bscale, klw[j]);
+            __syncthreads();
+            const float4* k4 = reinterpret_cast<const float4*>(Ks);
+            const float4* b4 = reinterpret_cast<const float4*>(bias);
+            const int64_t c4 = kp / 4;
+            for (int64_t r = blockIdx.x + G * warp; r < R; r += G * kWarps) {
+                float q[D];
+#pragma unroll
+                for (int t = 0; t < D; ++t) q[t] = Qs[t * qp + r] * qscale;
+                float mx = -INFINITY, sum = 0.0f;
+                for (int64_t g = lane; g < c4; g += 32) {
+                    float4 acc = b4[g];
+#pragma unroll
+                    for (int t = 0; t < D; ++t) {
+                        const float4 k = k4[t * c4 + g];
+                        acc.x = fmaf(q[t], k.x, acc.x);
+                        acc.y = fmaf(q[t], k.y, acc.y);
+                        acc.z = fmaf(q[t], k.z, acc.z);
+                        acc.w = fmaf(q[t], k.w, acc.w);
+                    }
+                    const float gm = fmaxf(fmaxf(acc.x, acc.y), fmaxf(acc.z, acc.w));
+                    if (gm > mx) {
+                        sum *= ex2(mx - gm);
+                        mx = gm;
+                    }
+                    if (mx > -INFINITY)
+                        sum += ex2(acc.x - mx) + ex2(acc.y - mx) + ex2(acc.z - mx) +
+                               ex2(acc.w - mx);
+                }
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1) {
+                    const float mo = __shfl_xor_sync(0xffffffffu, mx, off);
+                    const float so = __shfl_xor_sync(0xffffffffu, sum, off);
+                    const float M = fmaxf(mx, mo);
+                    sum = (mx > -INFINITY ? sum * ex2(mx - M) : 0.0f) +
+                          (mo > -INFINITY ? so * ex2(mo - M) : 0.0f);
+                    mx = M;
+                }
+                if (lane == 0) {
+                    const float pot = -eps * 0.6931471805599453f * (mx + __log2f(sum));
+                    if (!isfinite(pot)) {
+                        atomicOr(p.flags, kFlagNonFinitePotential);
+                        if (p.bad_iter) atomicMin(p.bad_iter, p.iter0 + it + 1);
+                    }
+                    out[r] = pot;
+                }
+            }
+            grid.sync();
+        }
+    }
+}
+
+size_t resident_smem(int64_t n, int64_t m, int64_t d) {
+    const int64_t np = (n + 127) / 128 * 128, mp = (m + 127) / 128 * 128;
+    return size_t((d + 1) * (np + mp) + (np > mp ? np : mp)) * sizeof(float);
+}
+
+template <int D>
+void launch_d(const SmallSolveParams& p, int grid, size_t smem, bool resident, cudaStream_t s) {
     static bool configured = false;
     if (!configured) {
         FSKB_CUDA(cudaFuncSetAttribute(small_solve_kernel<D>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(kSmallSolveSmem)));
+        FSKB_CUDA(cudaFuncSetAttribute(small_solve_res_kernel<D>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(kSmallSolveResSmem)));
         configured = true;
     }
     SmallSolveParams q = p;
     void* args[] = {&q};
-    FSKB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(small_solve_kernel<D>),
-                                          dim3(unsigned(grid)), dim3(kThreads), args, smem, s));
+    void* fn = resident ? reinterpret_cast<void*>(small_solve_res_kernel<D>)
+                        : reinterpret_cast<void*>(small_solve_kernel<D>);
+    FSKB_CUDA(cudaLaunchCooperativeKernel(fn, dim3(unsigned(grid)), dim3(kThreads), args, smem, s));
 }
 
 }  // namespace
@@ -149,13 +258,19 @@ void launch_small_solve(const SmallSolveParams& p0, cudaStream_t s) {
     SmallSolveParams p = p0;
     const int64_t cmax = p.n > p.m ? p.n : p.m;
     p.cpad = (cmax + 127) / 128 * 128;
-    const size_t smem = size_t(p.cpad) * size_t(p.d + 1) * sizeof(float);
+    p.npad = (p.n + 127) / 128 * 128;
+    p.mpad = (p.m + 127) / 128 * 128;
+    const char* renv = std::getenv("FSK_SMALL_RESIDENT");
+    const bool resident = !(renv && renv[0] == '0') &&
+                          resident_smem(p.n, p.m, p.d) <= kSmallSolveResSmem;
+    const size_t smem = resident ? resident_smem(p.n, p.m, p.d)
+                                 : size_t(p.cpad) * size_t(p.d + 1) * sizeof(float);
     // one CTA per SM (co-residency is what the grid barrier needs)
     const int grid = num_sms();
     switch (p.d) {
 #define FSKB_SMALL_CASE(DD) \
     case DD:                \
-        launch_d<DD>(p, grid, smem, s); \
+        launch_d<DD>(p, grid, smem, resident, s); \
         break;
         FSKB_SMALL_CASE(1) FSKB_SMALL_CASE(2) FSKB_SMALL_CASE(3) FSKB_SMALL_CASE(4)
         FSKB_SMALL_CASE(5) FSKB_SMALL_CASE(6) FSKB_SMALL_CASE(7) FSKB_SMALL_CASE(8)

@@ -12,6 +12,7 @@ namespace fskb {
 
 constexpr int kSmallSolveMaxD = 16;
 constexpr std::size_t kSmallSolveSmem = 192 * 1024;
+constexpr std::size_t kSmallSolveResSmem = 220 * 1024;   // resident-cloud variant
 
 struct SmallSolveParams {
     const float* X;        // n x d row-major
@@ -26,6 +27,7 @@ struct SmallSolveParams {
     int64_t n, m;
     int d;
     int64_t cpad;          // set by the launcher
+    int64_t npad, mpad;    // set by the launcher (resident variant)
     float fscale;          // feature scale s (1 for the squared-Euclidean cost)
     int* flags;
     int* bad_iter;         // nullable
