@@ -23,6 +23,7 @@
 #ifndef FSK_B200_H_
 #define FSK_B200_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -383,6 +384,15 @@ int fsk_num_devices(void);
  * The HVP memory contract (peak <= c (n + m) d scalars, never n m)
  * is asserted through this. */
 int64_t fsk_device_peak_bytes(int device, int reset);
+
+/* Page-locked host buffers from a process-wide pool (no reference counterpart: the
+ * reference API is host-only). Inputs and outputs of the solve entry points that live
+ * in such a buffer (or in any cudaHostRegister'ed memory) move by one DMA instead of
+ * being staged through pinned bounce buffers. fsk_host_free returns the block to the
+ * pool (cached up to 8 GB for the next fsk_host_alloc of a similar size). NULL on
+ * failure (fsk_last_error). */
+void* fsk_host_alloc(size_t bytes);
+int fsk_host_free(void* p);
 
 #ifdef __cplusplus
 }

@@ -106,6 +106,9 @@ def lib() -> C.CDLL:
         L.fsk_engine_screen_blocks.restype = C.c_uint64
         L.fsk_engine_live_set_fraction.restype = C.c_double
         L.fsk_device_peak_bytes.restype = C.c_int64
+        L.fsk_host_alloc.restype = C.c_void_p
+        L.fsk_host_alloc.argtypes = [C.c_size_t]
+        L.fsk_host_free.argtypes = [C.c_void_p]
         for name in ("fsk_io_count_f_update", "fsk_io_count_g_update",
                      "fsk_io_count_symmetric_update", "fsk_io_count_apply_plan",
                      "fsk_io_count_apply_plan_adjoint", "fsk_io_count_apply_hadamard",
@@ -113,6 +116,53 @@ def lib() -> C.CDLL:
             getattr(L, name).restype = C.c_uint64
         _lib = L
     return _lib
+
+
+class _PinnedBlock:
+    """One page-locked host block from the library's pool (fsk_host_alloc); numpy
+    arrays made from it keep it alive and hand it back to the pool when collected."""
+
+    def __init__(self, shape, dtype):
+        dtype = np.dtype(dtype)
+        nbytes = max(int(np.prod(shape, dtype=np.int64)) * dtype.itemsize, 1)
+        ptr = lib().fsk_host_alloc(nbytes)
+        if not ptr:
+            raise DeviceError("fsk_host_alloc: " + lib().fsk_last_error().decode())
+        self.ptr = ptr
+        self.__array_interface__ = {"shape": tuple(shape), "typestr": dtype.str,
+                                    "data": (ptr, False), "version": 3}
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            lib().fsk_host_free(self.ptr)
+            self.ptr = None
+
+
+def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
+    """Uninitialised array in page-locked host memory (the library's pinned pool).
+    Solve inputs and outputs held in such arrays cross the host link by one DMA."""
+    if isinstance(shape, int):
+        shape = (shape,)
+    return np.asarray(_PinnedBlock(shape, dtype))
+
+
+def pinned_copy(a) -> np.ndarray:
+    """Contiguous copy of `a` in page-locked host memory."""
+    a = np.asarray(a)
+    out = pinned_empty(a.shape, a.dtype)
+    out[...] = a
+    return out
+
+
+def _out_array(shape) -> np.ndarray:
+    """Output buffer of a solve: page-locked (pool) from 8 MB up, so the download is
+    one DMA; plain numpy when no device / pinned memory is available."""
+    if int(np.prod(shape)) * 8 >= (8 << 20):
+        try:
+            return pinned_empty(shape)
+        except (DeviceError, OSError):
+            pass
+    return np.empty(shape)
 
 
 def _check(status: int) -> None:
@@ -341,7 +391,7 @@ def sinkhorn_solve(X, a, Y, b, eps=0.1, schedule="alternating", max_iters=100, m
     src, tgt = k.measure(X, a, la), k.measure(Y, b, lb)
     cfg = _config(eps, schedule, max_iters, marginal_tol, eps_scaling_factor,
                   extra_iters_at_final_eps, precision)
-    f, g = np.empty(src.n), np.empty(tgt.n)
+    f, g = _out_array(src.n), _out_array(tgt.n)
     hist = np.zeros(max(max_iters, 1))
     rep = _Report(f.ctypes.data, g.ctypes.data, hist.ctypes.data, len(hist), 0, 0.0, 0.0, 0.0)
     if f_init is not None or g_init is not None:
@@ -350,14 +400,14 @@ def sinkhorn_solve(X, a, Y, b, eps=0.1, schedule="alternating", max_iters=100, m
         fi, gi = k.arr(f_init), k.arr(g_init)
         if fi.shape != (src.n,) or gi.shape != (tgt.n,):
             raise ValidationError("warm-start potentials do not match the measures")
-        G = np.empty((src.n, src.d)) if grad else None
+        G = _out_array((src.n, src.d)) if grad else None
         _check(lib().fsk_sinkhorn_solve_warm(
             C.byref(src), C.byref(tgt), C.byref(k.cost(cost)), C.byref(cfg),
             C.byref(_tiles(tiles)), _lp(ledger), C.c_void_p(fi.ctypes.data),
             C.c_void_p(gi.ctypes.data), C.byref(rep),
             C.c_void_p(G.ctypes.data) if grad else None))
     elif grad:
-        G = np.empty((src.n, src.d))
+        G = _out_array((src.n, src.d))
         _check(lib().fsk_sinkhorn_solve_grad(C.byref(src), C.byref(tgt), C.byref(k.cost(cost)),
                                              C.byref(cfg), C.byref(_tiles(tiles)), _lp(ledger),
                                              C.byref(rep), C.c_void_p(G.ctypes.data)))
@@ -450,7 +500,7 @@ def hvp_apply(X, a, Y, b, f_hat, g_hat, eps, A, tau=1e-5, cg_tol=1e-6, cg_max_it
     k = _Keep()
     src, tgt = k.measure(X, a), k.measure(Y, b)
     f, g, A = k.arr(f_hat), k.arr(g_hat), k.arr(A)
-    out = np.empty((src.n, src.d))
+    out = _out_array((src.n, src.d))
     h = _HvpConfig(tau, cg_tol, cg_max_iters)
     rep = _HvpReport()
     fn = lib().fsk_hvp_apply_single if precision == "single" else lib().fsk_hvp_apply

@@ -157,7 +157,7 @@ int bad_iteration(ExecCtx& C) {
 }
 
 void common_checks(const fsk_measure* src, const fsk_measure* tgt, const fsk_cost* cost,
-                   const fsk_tiles* tiles) {
+                   const fsk_tiles* tiles, bool check_points = true) {
     if (!src || !tgt) throw ValidationFailure("null measure");
     if (t_batch_memo) {
         // scan each distinct measure of a batch once (same checks, same order)
@@ -172,9 +172,33 @@ void common_checks(const fsk_measure* src, const fsk_measure* tgt, const fsk_cos
         }
         validate_problem_raw(*src, *tgt, cost, /*measures_checked=*/true);
     } else {
-        validate_problem_raw(*src, *tgt, cost);
+        validate_problem_raw(*src, *tgt, cost, false, check_points);
     }
     validate_tiles_raw(tiles);
+}
+
+// Entry-point validation of the single-device single-precision solves: every check
+// of common_checks except the coordinate finiteness scan, which the device ingest
+// performs (DevProblem::ingest). Returns true when that scan is left to the solve.
+// On any other failure the full checks run, so the error raised is the reference's
+// first one in its own order (core.cpp:18-81).
+bool checks_deferring_points(const fsk_measure* src, const fsk_measure* tgt, const fsk_cost* cost,
+                             const fsk_tiles* tiles, const fsk_config* cfg) {
+    const char* e = std::getenv("FSK_DEVICE_INGEST");
+    const bool defer = cfg && cfg->precision == 0 && num_devices_setting() < 1 && !t_batch_memo &&
+                       !labeled_cost(cost) && src && tgt && !(e && e[0] == '0');
+    if (!defer) {
+        common_checks(src, tgt, cost, tiles);
+        return false;
+    }
+    try {
+        common_checks(src, tgt, cost, tiles, /*check_points=*/false);
+        validate_config_raw(*cfg);   // (the reference checks the config after the points)
+    } catch (const ValidationFailure&) {
+        common_checks(src, tgt, cost, tiles);
+        throw;
+    }
+    return true;
 }
 
 // r (n) and c (m) of the induced marginals at (f, g), all on device.
@@ -216,12 +240,12 @@ double violation(const HostMarginals& hm, const fsk_measure& a, const fsk_measur
 
 // <f,a> + <g,b> - eps (sum r - 1) with unshifted potentials (solver.cpp:131-143)
 double dual_value(const fsk_measure& a, const fsk_measure& b, const double* fh, const double* gh,
-                  const std::vector<double>& alpha, const std::vector<double>& beta,
-                  const std::vector<double>& r, double eps) {
+                  const double* alpha, const double* beta, const std::vector<double>& r,
+                  double eps) {
     const double mass = cascade_sum(r.data(), r.size());
     double value = 0.0;
-    for (int64_t i = 0; i < a.n; ++i) value += (fh[i] + alpha[size_t(i)]) * a.weights[i];
-    for (int64_t j = 0; j < b.n; ++j) value += (gh[j] + beta[size_t(j)]) * b.weights[j];
+    for (int64_t i = 0; i < a.n; ++i) value += (fh[i] + alpha[i]) * a.weights[i];
+    for (int64_t j = 0; j < b.n; ++j) value += (gh[j] + beta[j]) * b.weights[j];
     return value - eps * (mass - 1.0);
 }
 
@@ -246,13 +270,45 @@ HostMarginals marginals_to_host(DevProblem<T>& P, const T* f, const T* g, T eps,
     return hm;
 }
 
+// A device result (fp64) copied into a page-locked host buffer on a copy stream,
+// ordered after the work enqueued so far on the compute stream, while that stream
+// carries on. finish() waits for the copy.
+struct EarlyDownload {
+    DevBuf<double> wide;
+    DevBuf<int> flags;
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ready = nullptr;
+    void start(double* host, std::size_t bytes, cudaStream_t s) {
+        FSKB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        FSKB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+        FSKB_CUDA(cudaEventRecord(ready, s));
+        FSKB_CUDA(cudaStreamWaitEvent(cs, ready, 0));
+        FSKB_CUDA(cudaMemcpyAsync(host, wide.get(), bytes, cudaMemcpyDeviceToHost, cs));
+    }
+    bool started() const { return cs != nullptr; }
+    void finish(cudaStream_t s) {
+        if (!cs) return;
+        FSKB_CUDA(cudaStreamSynchronize(cs));
+        // the buffers are freed on the compute stream: order it after the copy
+        FSKB_CUDA(cudaEventRecord(ready, cs));
+        FSKB_CUDA(cudaStreamWaitEvent(s, ready, 0));
+    }
+    ~EarlyDownload() {
+        if (cs) {
+            cudaStreamSynchronize(cs);
+            cudaStreamDestroy(cs);
+        }
+        if (ready) cudaEventDestroy(ready);
+    }
+};
+
 // Device-resident Sinkhorn (solver.cpp:21-117). T = double: Precision::Double;
 // T = float: Precision::Single (tensor-core or FMA half-steps).
 template <typename T>
 void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* cost,
                 const fsk_config& cfg, const fsk_tiles& tiles, fsk_ledger* ledger,
                 fsk_report* rep, double* grad_out, const double* f_init = nullptr,
-                const double* g_init = nullptr) {
+                const double* g_init = nullptr, bool points_unchecked = false) {
     constexpr bool kSingle = std::is_same_v<T, float>;
     const int64_t n = src.n, m = tgt.n, d = src.d;
     const double fs = feature_scale(cost);
@@ -269,21 +325,56 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
     auto& C = exec_ctx();
     PhaseTimer timer(C.s);
     DevProblem<T> P;
-    P.upload(src, tgt, cost, C.s);
-    timer.mark("upload");
     // the gradient's host pages are faulted in while the device iterates
     HostPrefault prefault;
     if (grad_out) prefault.start(grad_out, sizeof(double) * size_t(n) * size_t(d));
-    if constexpr (kSingle) enable_tensor_path(P, tensor_mode_from_env());
-    timer.mark("operand images");
-
-    const std::vector<double> alpha = host_sqnorm(src, fs), beta = host_sqnorm(tgt, fs);
-    std::vector<double> f0((size_t)(n)), g0((size_t)(m));
-    // reference init f = g = 0, i.e. f_hat = -alpha, g_hat = -beta (solver.cpp:27-32);
-    // a warm start (fsk_sinkhorn_solve_warm) starts from the caller's shifted pair
-    for (int64_t i = 0; i < n; ++i) f0[size_t(i)] = f_init ? f_init[i] : -alpha[size_t(i)];
-    for (int64_t j = 0; j < m; ++j) g0[size_t(j)] = g_init ? g_init[j] : -beta[size_t(j)];
-    DevBuf<T> f = dev_from<T>(f0.data(), n, C.s), g = dev_from<T>(g0.data(), m, C.s);
+    // alpha = |x|^2, beta = |y|^2 (core.cpp:83-96) on the host, for the dual value
+    std::vector<double> alpha_v, beta_v;
+    PinnedHost<double> alpha_h, beta_h;
+    const double* alpha = nullptr;
+    const double* beta = nullptr;
+    DevBuf<T> f, g;
+    if (kSingle && points_unchecked) {
+        // single-precision ingest: the caller's doubles cross the link once and the
+        // device narrows them, checks their finiteness (validate_measure, deferred
+        // here by the entry point) and forms alpha, beta and the initial potentials
+        // f_hat = -alpha, g_hat = -beta (solver.cpp:27-32): no host pass over the clouds
+        f.alloc(size_t(n), C.s);
+        g.alloc(size_t(m), C.s);
+        DevBuf<double> alpha_d, beta_d;
+        if (!P.ingest(src, tgt, fs, C.s, alpha_d, beta_d, f_init ? nullptr : f.get(),
+                      g_init ? nullptr : g.get()))
+            throw ValidationFailure(kNonFiniteCoordinate);
+        if (f_init) f = dev_from<T>(f_init, n, C.s);
+        if (g_init) g = dev_from<T>(g_init, m, C.s);
+        alpha_h = PinnedHost<double>(size_t(n));
+        beta_h = PinnedHost<double>(size_t(m));
+        FSKB_CUDA(cudaMemcpyAsync(alpha_h.get(), alpha_d.get(), sizeof(double) * size_t(n),
+                                  cudaMemcpyDeviceToHost, C.s));
+        FSKB_CUDA(cudaMemcpyAsync(beta_h.get(), beta_d.get(), sizeof(double) * size_t(m),
+                                  cudaMemcpyDeviceToHost, C.s));
+        alpha = alpha_h.get();
+        beta = beta_h.get();
+        timer.mark("upload + ingest");
+        if constexpr (kSingle) enable_tensor_path(P, tensor_mode_from_env());
+        timer.mark("operand images");
+    } else {
+        P.upload(src, tgt, cost, C.s);
+        timer.mark("upload");
+        if constexpr (kSingle) enable_tensor_path(P, tensor_mode_from_env());
+        timer.mark("operand images");
+        alpha_v = host_sqnorm(src, fs);
+        beta_v = host_sqnorm(tgt, fs);
+        alpha = alpha_v.data();
+        beta = beta_v.data();
+        std::vector<double> f0((size_t)(n)), g0((size_t)(m));
+        // reference init f = g = 0, i.e. f_hat = -alpha, g_hat = -beta (solver.cpp:27-32);
+        // a warm start (fsk_sinkhorn_solve_warm) starts from the caller's shifted pair
+        for (int64_t i = 0; i < n; ++i) f0[size_t(i)] = f_init ? f_init[i] : -alpha[size_t(i)];
+        for (int64_t j = 0; j < m; ++j) g0[size_t(j)] = g_init ? g_init[j] : -beta[size_t(j)];
+        f = dev_from<T>(f0.data(), n, C.s);
+        g = dev_from<T>(g0.data(), m, C.s);
+    }
     DevBuf<T> f2, g2;
     if (cfg.schedule == 1) {
         f2.alloc(size_t(n), C.s);
@@ -472,6 +563,7 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
     dev_to<T>(f, fh.data(), n, C.s);
     dev_to<T>(g, gh.data(), m, C.s);
     DevBuf<T> lse_f(size_t(n), C.s), mx_f(size_t(n), C.s);
+    EarlyDownload early_grad;
     DevBuf<T> r_keep;
     DevBuf<float> l2h_keep, l2l_keep;
     if (!stopped) {
@@ -487,7 +579,26 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
                                                 keep ? &r_keep : nullptr,
                                                 keep ? &l2h_keep : nullptr,
                                                 keep ? &l2l_keep : nullptr);
-        sync_and_check(C);
+        sync_and_check(C);   // (the stream is idle here: the marginals were downloaded)
+        const char* ov = std::getenv("FSK_OVERLAP_GRAD");
+        if constexpr (kSingle) {
+            if (keep && host_pinned(grad_out) && !(ov && ov[0] == '0')) {
+                // page-locked gradient output: enqueue the gradient (fused K3 on the
+                // f-side pass's LSE) and its download on a copy stream now, so the
+                // host's violation / dual work below overlaps them. The gradient
+                // reports into its own status word, read after the marginals' (the
+                // sequential order of the checks).
+                early_grad.flags.alloc(1, C.s);
+                early_grad.flags.zero();
+                DevBuf<T> G(size_t(n * d), C.s);
+                P.tc->grad(P, 0, g.get(), f.get(), T(pot_eps), 0, n, G.get(),
+                           early_grad.flags.get(), l2h_keep.get(), l2l_keep.get(),
+                           r_keep.get());
+                early_grad.wide.alloc(size_t(n * d), C.s);
+                launch_f32_to_f64(G.get(), early_grad.wide.get(), n * d, C.s);
+                early_grad.start(grad_out, sizeof(double) * size_t(n * d), C.s);
+            }
+        }
         ledger_marginals(ledger, n, m, d, tiles, cost);
         viol = violation(hm, src, tgt);
         // the last iterate's own tolerance check (fused path: never run in the loop);
@@ -508,7 +619,18 @@ void solve_impl(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* 
                 rep->eps_history[k] = hist[size_t(k)];
     }
     timer.mark("marginals + dual");
-    if (grad_out) {
+    if (grad_out && early_grad.started()) {
+        early_grad.finish(C.s);
+        timer.mark("gradient (overlapped) + download");
+        int fl = 0;
+        FSKB_CUDA(cudaMemcpy(&fl, early_grad.flags.get(), sizeof(int), cudaMemcpyDeviceToHost));
+        throw_for_flags(fl);
+        sync_and_check(C);
+        if (ledger) {
+            ledger_marginals(ledger, n, m, d, tiles, cost);
+            ledger_apply(ledger, n, m, d, d, tiles, cost, false);
+        }
+    } else if (grad_out) {
         // grad_X = 2 r (X - softmax(S) Y) at the returned potentials
         const T eps = T(pot_eps);
         DevBuf<T> G(size_t(n * d), C.s);
@@ -847,13 +969,14 @@ int fsk_sinkhorn_solve(const fsk_measure* src, const fsk_measure* tgt, const fsk
                        const fsk_config* cfg, const fsk_tiles* tiles, fsk_ledger* ledger,
                        fsk_report* report) {
     return guarded([&] {
-        common_checks(src, tgt, cost, tiles);
+        const bool deferred = checks_deferring_points(src, tgt, cost, tiles, cfg);
         validate_config_raw(*cfg);
         if (cfg->precision == 0) {
             if (labeled_cost(cost))
                 throw ValidationFailure(
                     "single-precision solve supports the squared-Euclidean cost only");
-            solve_impl<float>(*src, *tgt, cost, *cfg, *tiles, ledger, report, nullptr);
+            solve_impl<float>(*src, *tgt, cost, *cfg, *tiles, ledger, report, nullptr, nullptr,
+                              nullptr, deferred);
         } else {
             solve_impl<double>(*src, *tgt, cost, *cfg, *tiles, ledger, report, nullptr);
         }
@@ -865,14 +988,15 @@ int fsk_sinkhorn_solve_grad(const fsk_measure* src, const fsk_measure* tgt, cons
                             fsk_report* report, double* out_grad) {
     return guarded([&] {
         PhaseTimer timer(nullptr);
-        common_checks(src, tgt, cost, tiles);
+        const bool deferred = checks_deferring_points(src, tgt, cost, tiles, cfg);
         validate_config_raw(*cfg);
         timer.mark("validation");
         if (cfg->precision == 0) {
             if (labeled_cost(cost))
                 throw ValidationFailure(
                     "single-precision solve supports the squared-Euclidean cost only");
-            solve_impl<float>(*src, *tgt, cost, *cfg, *tiles, ledger, report, out_grad);
+            solve_impl<float>(*src, *tgt, cost, *cfg, *tiles, ledger, report, out_grad, nullptr,
+                              nullptr, deferred);
         } else {
             solve_impl<double>(*src, *tgt, cost, *cfg, *tiles, ledger, report, out_grad);
         }
@@ -917,8 +1041,8 @@ int fsk_dual_cost(const fsk_measure* src, const fsk_measure* tgt, const double* 
         HostMarginals hm = marginals_to_host<double>(P, f.get(), g.get(), eps, C);
         sync_and_check(C);
         const double fs = feature_scale(cost);
-        *out = dual_value(*src, *tgt, f_hat, g_hat, host_sqnorm(*src, fs), host_sqnorm(*tgt, fs),
-                          hm.r, eps);
+        *out = dual_value(*src, *tgt, f_hat, g_hat, host_sqnorm(*src, fs).data(),
+                          host_sqnorm(*tgt, fs).data(), hm.r, eps);
     });
 }
 
@@ -1098,6 +1222,16 @@ int fsk_device_count(void) {
     int c = 0;
     if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
     return c;
+}
+
+void* fsk_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    if (guarded([&] { p = host_alloc(bytes); }) != 0) return nullptr;
+    return p;
+}
+
+int fsk_host_free(void* p) {
+    return guarded([&] { host_free(p); });
 }
 
 int64_t fsk_device_peak_bytes(int device, int reset) {

@@ -45,6 +45,34 @@ enum : int {
 // synchronous with respect to the host buffer (it may be reused on return).
 void copy_host_to_device(void* dst, const void* src, std::size_t bytes, cudaStream_t s);
 void copy_device_to_host(void* dst, const void* src, std::size_t bytes, cudaStream_t s);
+// true for page-locked host memory (cudaHostAlloc / cudaHostRegister): copies DMA directly
+bool host_pinned(const void* p);
+// pooled page-locked host buffers (hostcopy.cpp; C ABI fsk_host_alloc / fsk_host_free)
+void* host_alloc(std::size_t bytes);
+void host_free(void* p);
+// RAII page-locked host array from that pool
+template <typename T>
+class PinnedHost {
+public:
+    PinnedHost() = default;
+    explicit PinnedHost(std::size_t n) : p_(static_cast<T*>(host_alloc(n * sizeof(T)))) {}
+    ~PinnedHost() { host_free(p_); }
+    PinnedHost(const PinnedHost&) = delete;
+    PinnedHost& operator=(const PinnedHost&) = delete;
+    PinnedHost(PinnedHost&& o) noexcept : p_(o.p_) { o.p_ = nullptr; }
+    PinnedHost& operator=(PinnedHost&& o) noexcept {
+        if (this != &o) {
+            host_free(p_);
+            p_ = o.p_;
+            o.p_ = nullptr;
+        }
+        return *this;
+    }
+    T* get() const { return p_; }
+
+private:
+    T* p_ = nullptr;
+};
 
 // Faults in and page-locks a caller's output buffer (>= 64 MB) from a background
 // host thread (hostcopy.cpp). join() before writing it; pinned() then says whether a
@@ -65,6 +93,7 @@ private:
     void* p_ = nullptr;
     std::size_t bytes_ = 0;
     bool pinned_ = false;
+    bool external_ = false;   // page-locked by the caller: never unregistered here
 };
 
 // Owner teardown after a full device synchronize: the buffers may have been

@@ -577,6 +577,46 @@ void launch_scale_rows(const float* Y, const double* w, int64_t m, int64_t d, fl
     count_launch();
 }
 
+// Single-precision ingest of a caller cloud (n x d doubles already on the device):
+// narrows the points to float, flags any non-finite coordinate (validate_measure,
+// core.cpp:18-66, deferred to the device) and writes each row's squared norm in fp64
+// in the host loop's order (s += x_t * x_t, t = 0..d-1, no contraction: bit-identical
+// to host_sqnorm_compute) times scale, and the negated, narrowed initial potential
+// -alpha (solver.cpp:27-32) when pot0 is given.
+__global__ void ingest_narrow_kernel(const double* __restrict__ in, float* __restrict__ out,
+                                     int64_t n, int* bad) {
+    int found = 0;
+    for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+         k += int64_t(gridDim.x) * blockDim.x) {
+        const double v = in[k];
+        found |= int((__double_as_longlong(v) & 0x7FF0000000000000ll) == 0x7FF0000000000000ll);
+        out[k] = float(v);
+    }
+    if (__any_sync(0xffffffffu, found) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
+}
+__global__ void ingest_sqnorm_kernel(const double* __restrict__ P, int64_t n, int64_t d,
+                                     double scale, double* __restrict__ sq,
+                                     float* __restrict__ pot0) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const double* r = P + i * d;
+        double s = 0.0;
+        for (int64_t t = 0; t < d; ++t) s = __dadd_rn(s, __dmul_rn(r[t], r[t]));
+        const double a = scale != 1.0 ? __dmul_rn(s, scale) : s;
+        sq[i] = a;
+        if (pot0) pot0[i] = float(-a);
+    }
+}
+void launch_ingest_f32(const double* pts64, int64_t n, int64_t d, double scale, float* pts32,
+                       double* sqnorm, float* pot0, int* bad, cudaStream_t s) {
+    if (!n) return;
+    ingest_narrow_kernel<<<blocks_for(n * d), 256, 0, s>>>(pts64, pts32, n * d, bad);
+    FSKB_CUDA(cudaGetLastError());
+    ingest_sqnorm_kernel<<<blocks_for(n, 128), 128, 0, s>>>(pts64, n, d, scale, sqnorm, pot0);
+    FSKB_CUDA(cudaGetLastError());
+    count_launch(2);
+}
+
 void launch_f64_to_f32(const double* in, float* out, int64_t n, cudaStream_t s) {
     if (!n) return;
     f64_to_f32_kernel<<<blocks_for(n), 256, 0, s>>>(in, out, n);

@@ -112,6 +112,10 @@ void launch_f64_to_f32(const double* in, float* out, int64_t n, cudaStream_t s);
 void launch_scale_rows(const float* Y, const double* w, int64_t m, int64_t d, float* out,
                        cudaStream_t s);
 void launch_f32_to_f64(const float* in, double* out, int64_t n, cudaStream_t s);
+// pts64 (n x d doubles, device) -> pts32; sqnorm_i = scale * sum_t x_it^2 in fp64 in the
+// host loop's order; pot0_i = float(-sqnorm_i) (nullable); *bad |= 1 on a non-finite value
+void launch_ingest_f32(const double* pts64, int64_t n, int64_t d, double scale, float* pts32,
+                       double* sqnorm, float* pot0, int* bad, cudaStream_t s);
 // G_i = 2 (r_i X_i - O_i) with r_i = w_i exp(pot_i/eps + lse_i)
 template <typename T>
 void launch_grad_epilogue(const T* X, const T* O, const T* w, const T* pot, const T* lse,

@@ -5,6 +5,7 @@
 #include "device_ops.h"
 
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -43,6 +44,30 @@ void configure_device_pool(int device) {
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
         uint64_t keep = ~uint64_t(0);
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        // Map a block into the pool up front (one allocation, freed at once and kept):
+        // later requests are carved from resident memory. Without it, the per-call
+        // buffers of the C ABI solves (hundreds of MB each at cfg3) fragment the pool
+        // and some calls grow it: measured 0.15-2 s stalls in 4 of 10 cfg3 calls,
+        // none with the reserve (gpurun_out/e2eab3). FSK_POOL_RESERVE_GB overrides
+        // the default of 24 GB on devices of >= 100 GB (0 disables).
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device);
+        const char* e = std::getenv("FSK_POOL_RESERVE_GB");
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) cudaGetLastError();
+        const double gb = e ? std::atof(e) : (total_b >= (size_t(100) << 30) ? 24.0 : 0.0);
+        if (gb > 0.0 && double(free_b) > 2.0 * gb * double(1ull << 30)) {
+            void* p = nullptr;
+            if (cudaMallocAsync(&p, size_t(gb * double(1ull << 30)), cudaStreamPerThread) ==
+                cudaSuccess) {
+                cudaFreeAsync(p, cudaStreamPerThread);
+                cudaStreamSynchronize(cudaStreamPerThread);
+            } else {
+                cudaGetLastError();
+            }
+        }
+        cudaSetDevice(prev);
     }
     done_mask.fetch_or(uint64_t(1) << device);
 }
@@ -204,6 +229,43 @@ void DevProblem<T>::upload(const fsk_measure& a, const fsk_measure& b, const fsk
         wtab.upload(cost->label_cost, size_t(wdim * wdim));
     }
     FSKB_CUDA(cudaStreamSynchronize(s));
+}
+
+template <typename T>
+bool DevProblem<T>::ingest(const fsk_measure& a, const fsk_measure& b, double scale,
+                           cudaStream_t stream, DevBuf<double>& alpha, DevBuf<double>& beta,
+                           T* f0, T* g0) {
+    if constexpr (!std::is_same_v<T, float>) {
+        throw CudaFailure("ingest on a double problem");
+    } else {
+        s = stream;
+        labeled = false;
+        fscale = 1.0;
+        lambda2 = 0.0;
+        DevBuf<int> bad(1, s);
+        bad.zero();
+        auto side_in = [&](DevSide<T>& side, const fsk_measure& m, DevBuf<double>& sq, T* p0) {
+            side.n = m.n;
+            side.d = m.d;
+            side.pts.alloc(size_t(m.n * m.d), s);
+            side.w.alloc(size_t(m.n), s);
+            side.logw.alloc(size_t(m.n), s);
+            sq.alloc(size_t(m.n), s);
+            DevBuf<double> tmp(size_t(m.n * m.d), s), wtmp(size_t(m.n), s);
+            tmp.upload(m.points, size_t(m.n * m.d));
+            wtmp.upload(m.weights, size_t(m.n));
+            launch_ingest_f32(tmp.get(), m.n, m.d, scale, side.pts.get(), sq.get(), p0, bad.get(),
+                              s);
+            launch_f64_to_f32(wtmp.get(), side.w.get(), m.n, s);
+            launch_log<T>(side.w.get(), side.logw.get(), m.n, s);
+        };
+        side_in(src, a, alpha, f0);
+        side_in(tgt, b, beta, g0);
+        int h = 0;
+        FSKB_CUDA(cudaMemcpyAsync(&h, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+        FSKB_CUDA(cudaStreamSynchronize(s));
+        return h == 0;
+    }
 }
 
 template <typename T>

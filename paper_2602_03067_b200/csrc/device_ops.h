@@ -59,6 +59,14 @@ struct DevProblem {
 
     void upload(const fsk_measure& a, const fsk_measure& b, const fsk_cost* cost,
                 cudaStream_t stream);
+    // Single-precision solve ingest (squared Euclidean, float problems): ships the
+    // caller's doubles, narrows them on the device and computes there what the host
+    // would otherwise scan for: the coordinate finiteness check (returned; the caller
+    // throws validate_measure's message) and each row's fp64 squared norm (alpha, beta:
+    // device vectors, bit-identical to host_sqnorm) plus the initial potentials
+    // f = -alpha, g = -beta when f0 / g0 are given. Synchronizes the stream.
+    bool ingest(const fsk_measure& a, const fsk_measure& b, double scale, cudaStream_t stream,
+                DevBuf<double>& alpha, DevBuf<double>& beta, T* f0, T* g0);
     // float clouds straight from FloatCloud buffers (squared Euclidean)
     void upload_f32(const float* xa, const float* wa, int64_t n, const float* xb,
                     const float* wb, int64_t m, int64_t d, cudaStream_t stream);

@@ -11,6 +11,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <stdexcept>
 #include <memory>
 #include <mutex>
 #include <thread>
@@ -100,7 +102,22 @@ void parallel_copy(const std::vector<Piece>& pieces) {
 
 }  // namespace
 
+bool host_pinned(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
 void copy_host_to_device(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes >= (size_t(8) << 20) && host_pinned(src)) {
+        // page-locked caller buffer (fsk_host_alloc, cudaHostRegister): one DMA
+        FSKB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+        FSKB_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
     if (bytes < (size_t(8) << 20)) {
         FSKB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
         return;
@@ -133,7 +150,7 @@ void copy_host_to_device(void* dst, const void* src, size_t bytes, cudaStream_t 
 }
 
 void copy_device_to_host(void* dst, const void* src, size_t bytes, cudaStream_t s) {
-    if (bytes < (size_t(8) << 20)) {
+    if (bytes < (size_t(8) << 20) || host_pinned(dst)) {
         FSKB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
         FSKB_CUDA(cudaStreamSynchronize(s));
         return;
@@ -178,6 +195,12 @@ void copy_device_to_host(void* dst, const void* src, size_t bytes, cudaStream_t 
 void HostPrefault::start(void* p, std::size_t bytes) {
     join();
     if (!p || bytes < (std::size_t(64) << 20)) return;
+    if (host_pinned(p)) {
+        // already page-locked (e.g. from fsk_host_alloc): resident, DMA-able
+        pinned_ = true;
+        external_ = true;
+        return;
+    }
     p_ = p;
     bytes_ = bytes;
     pinned_ = false;
@@ -214,8 +237,81 @@ void HostPrefault::join() {
 
 void HostPrefault::release() {
     join();
-    if (pinned_) cudaHostUnregister(p_);
+    if (pinned_ && !external_) cudaHostUnregister(p_);
     pinned_ = false;
+    external_ = false;
+}
+
+// ---- pooled page-locked host buffers (fsk_host_alloc / fsk_host_free) ---------
+namespace {
+struct HostPool {
+    std::mutex mu;
+    std::multimap<size_t, void*> free_;   // size -> block
+    std::map<void*, size_t> live;
+    size_t cached = 0;
+};
+HostPool& host_pool() {
+    static HostPool* p = new HostPool();   // never destroyed (process-lifetime cache)
+    return *p;
+}
+constexpr size_t kHostPoolCap = size_t(8) << 30;
+}  // namespace
+
+void* host_alloc(size_t bytes) {
+    if (!bytes) bytes = 1;
+    auto& P = host_pool();
+    {
+        std::lock_guard<std::mutex> lk(P.mu);
+        // smallest cached block that fits without wasting more than half of it
+        auto it = P.free_.lower_bound(bytes);
+        if (it != P.free_.end() && it->first <= 2 * bytes) {
+            void* b = it->second;
+            P.live[b] = it->first;
+            P.cached -= it->first;
+            P.free_.erase(it);
+            return b;
+        }
+    }
+    void* b = nullptr;
+    if (cudaHostAlloc(&b, bytes, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        // release the cache and retry once
+        std::vector<void*> drop;
+        {
+            std::lock_guard<std::mutex> lk(P.mu);
+            for (auto& [sz, q] : P.free_) drop.push_back(q);
+            P.free_.clear();
+            P.cached = 0;
+        }
+        for (void* q : drop) cudaFreeHost(q);
+        FSKB_CUDA(cudaHostAlloc(&b, bytes, cudaHostAllocPortable));
+    }
+    std::lock_guard<std::mutex> lk(P.mu);
+    P.live[b] = bytes;
+    return b;
+}
+
+void host_free(void* p) {
+    if (!p) return;
+    auto& P = host_pool();
+    std::vector<void*> drop;
+    {
+        std::lock_guard<std::mutex> lk(P.mu);
+        auto it = P.live.find(p);
+        if (it == P.live.end()) throw std::invalid_argument("fsk_host_free: not an fsk_host_alloc block");
+        const size_t sz = it->second;
+        P.live.erase(it);
+        P.free_.emplace(sz, p);
+        P.cached += sz;
+        // over the cap: drop the largest cached blocks
+        while (P.cached > kHostPoolCap && !P.free_.empty()) {
+            auto last = std::prev(P.free_.end());
+            P.cached -= last->first;
+            drop.push_back(last->second);
+            P.free_.erase(last);
+        }
+    }
+    for (void* q : drop) cudaFreeHost(q);
 }
 
 Scratch& Scratch::local() {

@@ -45,10 +45,11 @@ bool all_finite(const double* p, int64_t n) {
     return true;
 }
 
-void validate_measure_raw(const fsk_measure& m) {
+void validate_measure_raw(const fsk_measure& m, bool check_points) {
     if (m.n < 1 || m.d < 1)
         throw ValidationFailure("measure must have n >= 1 points of dimension d >= 1");
-    if (!all_finite(m.points, m.n * m.d)) throw ValidationFailure("non-finite coordinate in measure");
+    if (check_points && !all_finite(m.points, m.n * m.d))
+        throw ValidationFailure(kNonFiniteCoordinate);
     double sum = 0.0;
     for (int64_t i = 0; i < m.n; ++i) {
         const double w = m.weights[i];
@@ -64,10 +65,10 @@ void validate_measure_raw(const fsk_measure& m) {
 }
 
 void validate_problem_raw(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* cost,
-                          bool measures_checked) {
+                          bool measures_checked, bool check_points) {
     if (!measures_checked) {
-        validate_measure_raw(src);
-        validate_measure_raw(tgt);
+        validate_measure_raw(src, check_points);
+        validate_measure_raw(tgt, check_points);
     }
     if (src.d != tgt.d)
         throw ValidationFailure("source dimension " + std::to_string(src.d) +

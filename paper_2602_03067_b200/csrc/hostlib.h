@@ -12,10 +12,13 @@
 namespace fskb {
 
 // ---- validation (proj/src/core.cpp:18-81, stream.cpp:253-259) -------------
-void validate_measure_raw(const fsk_measure& m);
+// check_points = false skips the coordinate finiteness scan (a caller that checks it
+// elsewhere, e.g. on the device after the upload, and throws the same message)
+void validate_measure_raw(const fsk_measure& m, bool check_points = true);
 // measures_checked: validate_measure_raw already ran on both (batch entry points)
 void validate_problem_raw(const fsk_measure& src, const fsk_measure& tgt, const fsk_cost* cost,
-                          bool measures_checked = false);
+                          bool measures_checked = false, bool check_points = true);
+inline constexpr const char* kNonFiniteCoordinate = "non-finite coordinate in measure";
 void validate_config_raw(const fsk_config& cfg);
 void validate_tiles_raw(const fsk_tiles* tiles);
 bool all_finite(const double* p, int64_t n);
