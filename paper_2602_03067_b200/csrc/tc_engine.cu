@@ -222,6 +222,11 @@ struct TcParams {
     // label-augmented cost (stream.cpp:73-77): t_ij -= lambda2 log2(e) W[l_i, l_j] / eps,
     // applied in the epilogue from a shared-memory copy of the V x V table
     LabelArgs lab;
+    // d <= 64 kernel: the two 64-column accumulators of a query tile form a ring
+    // taken in live-half order (slot = that tile's live-half count mod 2) instead of
+    // one fixed slot per key half: consecutive live halves of one tile that fall on
+    // the same key half no longer serialise MMA -> drain -> MMA (FSK_ACC_RING=0: off)
+    int acc_ring;
 };
 
 // Work items run split-major: the CTAs running at the same time share one key
@@ -860,7 +865,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
         const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
         {
             int it = 0;
-            int acc_n[2][2] = {{0, 0}, {0, 0}};   // per (query tile, half) accumulator uses
+            int acc_n[2][2] = {{0, 0}, {0, 0}};   // per (query tile, slot) accumulator uses
+            int acc_c[2] = {0, 0};                 // per query tile: live halves issued
             for (int item = blockIdx.x, lu = 0; item < p.items; item += gridDim.x, ++lu) {
                 int unit, split;
                 item_coords(p.items, p.splits, item, unit, split);
@@ -882,15 +888,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                         // drains one while the other computes; dead halves are skipped
                         for (int h = 0; h < 2; ++h) {
                             if (!((mask >> (2 * t + h)) & 1u)) continue;
-                            mbar_wait(accempty(t, h), (acc_n[t][h] & 1) ^ 1);
+                            const int sl = p.acc_ring ? (acc_c[t] & 1) : h;
+                            mbar_wait(accempty(t, sl), (acc_n[t][sl] & 1) ^ 1);
                             fence_after();
-                            const uint32_t d = tm + uint32_t(t * TILE + h * 64);
+                            const uint32_t d = tm + uint32_t(t * TILE + sl * 64);
                             if (screen_phase)
                                 issue_screen_half_tq<true>(d, q, kst, h);
                             else
                                 issue_score_half_tq<true>(d, q, kst, h);
-                            umma_commit<true>(accfull(t, h));
-                            ++acc_n[t][h];
+                            umma_commit<true>(accfull(t, sl));
+                            ++acc_n[t][sl];
+                            ++acc_c[t];
                         }
                     }
                     umma_commit<true>(kempty(s));
@@ -923,7 +931,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
         const uint32_t acc_addr = tmem + lane_addr + uint32_t(t * TILE);
         const uint32_t q_addr = tmem + lane_addr + TQ_QCOL + uint32_t(t) * TQ_QSTRIDE;
         float* vb = reinterpret_cast<float*>(sbase + TQ_OFF_BAR + 256) + (warp - 2) * TILE;
-        int acc_h[2] = {0, 0};   // uses of this tile's two half accumulators
+        int acc_h[2] = {0, 0};   // uses of this tile's two accumulator slots
+        int acc_c = 0;           // live halves of this tile drained (ring slot = acc_c & 1)
         const size_t nsub_all = 2 * size_t(p.k_tiles);   // gap row length (halves)
         for (int item = blockIdx.x, lu = 0; item < p.items; item += gridDim.x, ++lu) {
             int unit, split;
@@ -1003,16 +1012,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                         float tmax = -INFINITY, th[2];
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
-                            mbar_wait(accfull(t, h), acc_h[h] & 1);
+                            const int sl = p.acc_ring ? ((acc_c + h) & 1) : h;
+                            mbar_wait(accfull(t, sl), acc_h[sl] & 1);
                             fence_after();
                             const int64_t kbase = int64_t(kt) * TILE + 64 * h;
                             uint32_t v[64];
-                            FSKB_TMEM_LD32(acc_addr + 64 * h, (v + 0));
-                            FSKB_TMEM_LD32(acc_addr + 64 * h + 32, (v + 32));
+                            FSKB_TMEM_LD32(acc_addr + 64 * sl, (v + 0));
+                            FSKB_TMEM_LD32(acc_addr + 64 * sl + 32, (v + 32));
                             tmem_ld_wait();
                             fence_before();
                             __syncwarp();
-                            if (lane == 0) mbar_arrive(accempty(t, h));
+                            if (lane == 0) mbar_arrive(accempty(t, sl));
                             if (kbase + 64 > p.key_valid) {
 #pragma unroll
                                 for (int j = 0; j < 64; ++j)
@@ -1023,6 +1033,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                         }
                         ++acc_h[0];
                         ++acc_h[1];
+                        acc_c += 2;
                         Ma = fmaxf(Ma, tmax);
                         const bool live = row_ok && tmax >= Ma - p.screen_thr;
                         if (__any_sync(0xffffffffu, live) && lane == 0)
@@ -1101,17 +1112,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
             for (int q = t < nq && run2 ? next_half(-1) : qend, q_next; q < qend; q = q_next) {
                 const int kt = kt0 + (q >> 1), h = q & 1;
                 const float M_old = M;
-                mbar_wait(accfull(t, h), acc_h[h] & 1);
+                const int sl = p.acc_ring ? (acc_c & 1) : h;
+                mbar_wait(accfull(t, sl), acc_h[sl] & 1);
                 fence_after();
                 uint32_t v[64];
-                FSKB_TMEM_LD32(acc_addr + 64 * h, (v + 0));
-                FSKB_TMEM_LD32(acc_addr + 64 * h + 32, (v + 32));
+                FSKB_TMEM_LD32(acc_addr + 64 * sl, (v + 0));
+                FSKB_TMEM_LD32(acc_addr + 64 * sl + 32, (v + 32));
                 q_next = next_half(q);   // overlaps the loads
                 tmem_ld_wait();
                 fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(accempty(t, h));
-                ++acc_h[h];
+                if (lane == 0) mbar_arrive(accempty(t, sl));
+                ++acc_h[sl];
+                ++acc_c;
                 float uh;
                 const bool hit = k1_tile_update<VEC, 64>(v, int64_t(kt) * TILE + 64 * h, p, M, S,
                                                          nlh, nll, vb, lane, uh);
@@ -2221,6 +2234,13 @@ float device_absmax(const float* x, int64_t n, cudaStream_t s) {
     return f;
 }
 
+// accumulator ring of the d <= 64 kernel (TcParams::acc_ring); FSK_ACC_RING=0 turns
+// it off (read per call: A/B runs flip it)
+int acc_ring_enabled() {
+    const char* e = std::getenv("FSK_ACC_RING");
+    return (e && e[0] == '0') ? 0 : 1;
+}
+
 // T = 26 + ceil(log2 m) (<= kSkipLog2): m terms below 2^-T of the max add < 2^-26
 float skip_log2_for(int64_t m) {
     static const double env = [] {
@@ -2648,6 +2668,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
     count_launch();
 
     TcParams p{};
+    p.acc_ring = acc_ring_enabled();
     p.qimg = I.qimg[qc].get();
     p.kimg = I.kimg[side].get();
     p.kbias = I.kbias[side].get();
