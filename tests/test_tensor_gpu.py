@@ -794,6 +794,45 @@ def test_device_decided_passes_match_host_decided(fsk):
     assert out["1"][3]["warm"] > 0 and out["1"][3]["screened"] > 0
 
 
+def test_accumulator_ring_bit_identical(fsk):
+    """The d <= 64 kernel's accumulator ring (TcParams::acc_ring: a query tile's two
+    accumulators taken in live-half order) only changes which TMEM columns a live
+    half lands in: screened, warm and transport-vector passes and the gradient give
+    the same bits with the ring on and off (FSK_ACC_RING, read per call)."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(405)
+    n = m = 1 << 18
+    X, Y = rng.normal(size=(n, 64)), rng.normal(size=(m, 64))
+    u = np.full(n, 1.0 / n)
+    v = torch.tensor(rng.normal(size=m), dtype=torch.float32, device="cuda")
+    out = {}
+    for flag in ("1", "0"):
+        os.environ["FSK_ACC_RING"] = flag
+        try:
+            eng = fsk.Engine(0, X, u, Y, u, mode="tensor")
+            eng.set_eps(0.05)
+            f = torch.empty(n, dtype=torch.float32, device="cuda")
+            g = torch.empty(m, dtype=torch.float32, device="cuda")
+            eng.bind(f.data_ptr(), g.data_ptr())
+            eng.init_potentials()
+            for _ in range(6):
+                eng.half_step(0, 0, n)
+                eng.half_step(1, 0, m)
+            G = torch.empty((n, 64), dtype=torch.float32, device="cuda")
+            eng.grad(0, n, G.data_ptr())
+            pv = torch.empty(n, dtype=torch.float64, device="cuda")
+            eng.transport_vec(0, v.data_ptr(), pv.data_ptr())
+            torch.cuda.synchronize()
+            out[flag] = (f.cpu().numpy(), g.cpu().numpy(), G.cpu().numpy(), pv.cpu().numpy(),
+                         eng.pass_counts())
+            eng.close()
+        finally:
+            os.environ.pop("FSK_ACC_RING", None)
+    for a_, b_ in zip(out["1"][:4], out["0"][:4]):
+        assert np.array_equal(a_, b_)
+    assert out["1"][4] == out["0"][4]
+
+
 def test_persistent_small_solve(fsk, port, golden):
     """cfg1-class problems (keys fit in shared memory, d <= 16): the whole iteration
     loop is one cooperative kernel (small_solve.cu). Engine iterate and the drop-in
