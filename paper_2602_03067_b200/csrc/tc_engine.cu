@@ -227,6 +227,9 @@ struct TcParams {
     // one fixed slot per key half: consecutive live halves of one tile that fall on
     // the same key half no longer serialise MMA -> drain -> MMA (FSK_ACC_RING=0: off)
     int acc_ring;
+    // d <= 64 kernel: one elect per MMA chain, descriptors by 32-bit adds
+    // (issue_*_half_lean; FSK_LEAN_ISSUE=0: the per-MMA helpers)
+    int lean_issue;
 };
 
 // Work items run split-major: the CTAs running at the same time share one key
@@ -892,10 +895,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                             mbar_wait(accempty(t, sl), (acc_n[t][sl] & 1) ^ 1);
                             fence_after();
                             const uint32_t d = tm + uint32_t(t * TILE + sl * 64);
-                            if (screen_phase)
+                            if (p.lean_issue) {
+                                const uint32_t klo = desc_lo(kst + uint32_t(h) * kHalfK);
+                                const uint32_t blo = desc_lo(kst + QTILE + uint32_t(h) * kHalfB);
+                                if (screen_phase)
+                                    issue_screen_half_lean(d, q, klo, blo);
+                                else
+                                    issue_score_half_lean(d, q, klo, blo);
+                            } else if (screen_phase) {
                                 issue_screen_half_tq<true>(d, q, kst, h);
-                            else
+                            } else {
                                 issue_score_half_tq<true>(d, q, kst, h);
+                            }
                             umma_commit<true>(accfull(t, sl));
                             ++acc_n[t][sl];
                             ++acc_c[t];
@@ -2236,6 +2247,10 @@ float device_absmax(const float* x, int64_t n, cudaStream_t s) {
 
 // accumulator ring of the d <= 64 kernel (TcParams::acc_ring); FSK_ACC_RING=0 turns
 // it off (read per call: A/B runs flip it)
+int lean_issue_enabled() {
+    const char* e = std::getenv("FSK_LEAN_ISSUE");
+    return (e && e[0] == '0') ? 0 : 1;
+}
 int acc_ring_enabled() {
     const char* e = std::getenv("FSK_ACC_RING");
     return (e && e[0] == '0') ? 0 : 1;
@@ -2669,6 +2684,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
 
     TcParams p{};
     p.acc_ring = acc_ring_enabled();
+    p.lean_issue = lean_issue_enabled();
     p.qimg = I.qimg[qc].get();
     p.kimg = I.kimg[side].get();
     p.kbias = I.kbias[side].get();
