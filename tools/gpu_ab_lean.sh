@@ -1,18 +1,18 @@
 #!/usr/bin/env bash
-# Lean MMA-chain issue (FSK_LEAN_ISSUE) x wide screen epilogue (FSK_SCREEN_WIDE) A/B:
-# guarded parity first, then interleaved cfg3 / cfg2 benches and phase-1 launch times.
+# Lean MMA-chain issue A/B (FSK_LEAN_ISSUE 0: per-MMA elect and descriptor packing, 1: one
+# elect per chain): guarded parity first, then interleaved benches and phase-1 launch times.
 set -u
 TAG=${1:-r02lean}
 OUT=gpurun_out/$TAG
 mkdir -p "$OUT"
-timeout 400 python -m pytest tests/test_bench_parity_gpu.py -x -q -k "cfg3 or cfg2" > "$OUT/pytest_bench.log" 2>&1
+FSK_LEAN_ISSUE=1 timeout 400 python -m pytest tests/test_bench_parity_gpu.py -x -q -k "cfg3 or cfg2" > "$OUT/pytest_bench.log" 2>&1
 rc=$?; echo "rc=$rc" >> "$OUT/pytest_bench.log"; tail -n 2 "$OUT/pytest_bench.log"
 [ $rc -eq 0 ] || exit 1
-timeout 900 python -m pytest tests/test_tensor_gpu.py -x -q > "$OUT/pytest_tensor.log" 2>&1
+FSK_LEAN_ISSUE=1 timeout 900 python -m pytest tests/test_tensor_gpu.py -x -q > "$OUT/pytest_tensor.log" 2>&1
 echo "rc=$?" >> "$OUT/pytest_tensor.log"; tail -n 2 "$OUT/pytest_tensor.log"
 i=0
 for rep in 1 2; do
-for setting in "FSK_LEAN_ISSUE=0 FSK_SCREEN_WIDE=0" "FSK_LEAN_ISSUE=1 FSK_SCREEN_WIDE=0" "FSK_LEAN_ISSUE=1 FSK_SCREEN_WIDE=1"; do
+for setting in "FSK_LEAN_ISSUE=0" "FSK_LEAN_ISSUE=1"; do
   env $setting timeout 300 python bench.py --config cfg3 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-parity > "$OUT/bench_cfg3_$i.log" 2>&1
   echo "[$setting]" >> "$OUT/bench_cfg3_$i.log"
   env $setting timeout 300 python bench.py --config cfg2 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-parity > "$OUT/bench_cfg2_$i.log" 2>&1
@@ -21,7 +21,7 @@ for setting in "FSK_LEAN_ISSUE=0 FSK_SCREEN_WIDE=0" "FSK_LEAN_ISSUE=1 FSK_SCREEN
 done
 done
 j=0
-for setting in "FSK_LEAN_ISSUE=0 FSK_SCREEN_WIDE=0" "FSK_LEAN_ISSUE=1 FSK_SCREEN_WIDE=0" "FSK_LEAN_ISSUE=1 FSK_SCREEN_WIDE=1"; do
+for setting in "FSK_LEAN_ISSUE=0" "FSK_LEAN_ISSUE=1"; do
   env $setting timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:tc_lse_tq --csv --log-file "$OUT/l_$j.csv" python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-parity > /dev/null 2>&1
   echo "$setting" > "$OUT/l_$j.txt"; j=$((j+1))
 done
