@@ -222,14 +222,12 @@ struct TcParams {
     // label-augmented cost (stream.cpp:73-77): t_ij -= lambda2 log2(e) W[l_i, l_j] / eps,
     // applied in the epilogue from a shared-memory copy of the V x V table
     LabelArgs lab;
-    // d <= 64 kernel: the two 64-column accumulators of a query tile form a ring
-    // taken in live-half order (slot = that tile's live-half count mod 2) instead of
-    // one fixed slot per key half: consecutive live halves of one tile that fall on
-    // the same key half no longer serialise MMA -> drain -> MMA (FSK_ACC_RING=0: off)
-    int acc_ring;
     // d <= 64 kernel: one elect per MMA chain, descriptors by 32-bit adds
     // (issue_*_half_lean; FSK_LEAN_ISSUE=0: the per-MMA helpers)
     int lean_issue;
+    // d <= 64 kernel: stages with one needed 64-key half load only that half
+    // (FSK_HALF_LOAD=0: whole key tiles)
+    int half_load;
 };
 
 // Work items run split-major: the CTAs running at the same time share one key
@@ -849,10 +847,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                     nlive += __popc(mask);
                     mbar_wait(kempty(s), ((it / TQ_STAGES) & 1) ^ 1);
                     stage_mask[s] = mask | (kn >= kt1 ? kStageLast : 0u);
-                    mbar_expect_tx(kfull(s), KSTAGE);
                     const uint32_t dst = base + TQ_OFF_K + s * KSTAGE;
-                    bulk_g2s(dst, p.kimg + size_t(kt) * QTILE, QTILE, kfull(s));
-                    bulk_g2s(dst + QTILE, p.kbias + size_t(kt) * BIAS, BIAS, kfull(s));
+                    // the 64-key halves either query tile needs: a stage with one live
+                    // half loads only that half of the hi, lo and bias chunks (18 of
+                    // 36 KB) into its usual place (warm passes: ~1.05 live halves per
+                    // stage, L2 -> shared traffic is what bounds them)
+                    const uint32_t hneed = (mask | (mask >> 2)) & 3u;
+                    if (p.half_load && (hneed == 1u || hneed == 2u)) {
+                        const uint32_t hh = hneed >> 1;
+                        const uint8_t* src = p.kimg + size_t(kt) * QTILE + hh * kHalfK;
+                        mbar_expect_tx(kfull(s), 2 * kHalfK + kHalfB);
+                        bulk_g2s(dst + hh * kHalfK, src, kHalfK, kfull(s));
+                        bulk_g2s(dst + CHUNK + hh * kHalfK, src + CHUNK, kHalfK, kfull(s));
+                        bulk_g2s(dst + QTILE + hh * kHalfB, p.kbias + size_t(kt) * BIAS + hh * kHalfB,
+                                 kHalfB, kfull(s));
+                    } else {
+                        mbar_expect_tx(kfull(s), KSTAGE);
+                        bulk_g2s(dst, p.kimg + size_t(kt) * QTILE, QTILE, kfull(s));
+                        bulk_g2s(dst + QTILE, p.kbias + size_t(kt) * BIAS, BIAS, kfull(s));
+                    }
                 }
                 if constexpr (SCREEN) {
                     mbar_arrive(bits_free);
@@ -868,8 +881,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
         const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
         {
             int it = 0;
-            int acc_n[2][2] = {{0, 0}, {0, 0}};   // per (query tile, slot) accumulator uses
-            int acc_c[2] = {0, 0};                 // per query tile: live halves issued
+            int acc_n[2][2] = {{0, 0}, {0, 0}};   // per (query tile, half) accumulator uses
             for (int item = blockIdx.x, lu = 0; item < p.items; item += gridDim.x, ++lu) {
                 int unit, split;
                 item_coords(p.items, p.splits, item, unit, split);
@@ -891,10 +903,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                         // drains one while the other computes; dead halves are skipped
                         for (int h = 0; h < 2; ++h) {
                             if (!((mask >> (2 * t + h)) & 1u)) continue;
-                            const int sl = p.acc_ring ? (acc_c[t] & 1) : h;
-                            mbar_wait(accempty(t, sl), (acc_n[t][sl] & 1) ^ 1);
+                            mbar_wait(accempty(t, h), (acc_n[t][h] & 1) ^ 1);
                             fence_after();
-                            const uint32_t d = tm + uint32_t(t * TILE + sl * 64);
+                            const uint32_t d = tm + uint32_t(t * TILE + h * 64);
                             if (p.lean_issue) {
                                 const uint32_t klo = desc_lo(kst + uint32_t(h) * kHalfK);
                                 const uint32_t blo = desc_lo(kst + QTILE + uint32_t(h) * kHalfB);
@@ -907,9 +918,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                             } else {
                                 issue_score_half_tq<true>(d, q, kst, h);
                             }
-                            umma_commit<true>(accfull(t, sl));
-                            ++acc_n[t][sl];
-                            ++acc_c[t];
+                            umma_commit<true>(accfull(t, h));
+                            ++acc_n[t][h];
                         }
                     }
                     umma_commit<true>(kempty(s));
@@ -942,8 +952,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
         const uint32_t acc_addr = tmem + lane_addr + uint32_t(t * TILE);
         const uint32_t q_addr = tmem + lane_addr + TQ_QCOL + uint32_t(t) * TQ_QSTRIDE;
         float* vb = reinterpret_cast<float*>(sbase + TQ_OFF_BAR + 256) + (warp - 2) * TILE;
-        int acc_h[2] = {0, 0};   // uses of this tile's two accumulator slots
-        int acc_c = 0;           // live halves of this tile drained (ring slot = acc_c & 1)
+        int acc_h[2] = {0, 0};   // uses of this tile's two half accumulators
         const size_t nsub_all = 2 * size_t(p.k_tiles);   // gap row length (halves)
         for (int item = blockIdx.x, lu = 0; item < p.items; item += gridDim.x, ++lu) {
             int unit, split;
@@ -1023,17 +1032,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                         float tmax = -INFINITY, th[2];
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
-                            const int sl = p.acc_ring ? ((acc_c + h) & 1) : h;
-                            mbar_wait(accfull(t, sl), acc_h[sl] & 1);
+                            mbar_wait(accfull(t, h), acc_h[h] & 1);
                             fence_after();
                             const int64_t kbase = int64_t(kt) * TILE + 64 * h;
                             uint32_t v[64];
-                            FSKB_TMEM_LD32(acc_addr + 64 * sl, (v + 0));
-                            FSKB_TMEM_LD32(acc_addr + 64 * sl + 32, (v + 32));
+                            FSKB_TMEM_LD32(acc_addr + 64 * h, (v + 0));
+                            FSKB_TMEM_LD32(acc_addr + 64 * h + 32, (v + 32));
                             tmem_ld_wait();
                             fence_before();
                             __syncwarp();
-                            if (lane == 0) mbar_arrive(accempty(t, sl));
+                            if (lane == 0) mbar_arrive(accempty(t, h));
                             if (kbase + 64 > p.key_valid) {
 #pragma unroll
                                 for (int j = 0; j < 64; ++j)
@@ -1044,7 +1052,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                         }
                         ++acc_h[0];
                         ++acc_h[1];
-                        acc_c += 2;
                         Ma = fmaxf(Ma, tmax);
                         const bool live = row_ok && tmax >= Ma - p.screen_thr;
                         if (__any_sync(0xffffffffu, live) && lane == 0)
@@ -1123,19 +1130,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
             for (int q = t < nq && run2 ? next_half(-1) : qend, q_next; q < qend; q = q_next) {
                 const int kt = kt0 + (q >> 1), h = q & 1;
                 const float M_old = M;
-                const int sl = p.acc_ring ? (acc_c & 1) : h;
-                mbar_wait(accfull(t, sl), acc_h[sl] & 1);
+                mbar_wait(accfull(t, h), acc_h[h] & 1);
                 fence_after();
                 uint32_t v[64];
-                FSKB_TMEM_LD32(acc_addr + 64 * sl, (v + 0));
-                FSKB_TMEM_LD32(acc_addr + 64 * sl + 32, (v + 32));
+                FSKB_TMEM_LD32(acc_addr + 64 * h, (v + 0));
+                FSKB_TMEM_LD32(acc_addr + 64 * h + 32, (v + 32));
                 q_next = next_half(q);   // overlaps the loads
                 tmem_ld_wait();
                 fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(accempty(t, sl));
-                ++acc_h[sl];
-                ++acc_c;
+                if (lane == 0) mbar_arrive(accempty(t, h));
+                ++acc_h[h];
                 float uh;
                 const bool hit = k1_tile_update<VEC, 64>(v, int64_t(kt) * TILE + 64 * h, p, M, S,
                                                          nlh, nll, vb, lane, uh);
@@ -2245,14 +2250,13 @@ float device_absmax(const float* x, int64_t n, cudaStream_t s) {
     return f;
 }
 
-// accumulator ring of the d <= 64 kernel (TcParams::acc_ring); FSK_ACC_RING=0 turns
-// it off (read per call: A/B runs flip it)
-int lean_issue_enabled() {
-    const char* e = std::getenv("FSK_LEAN_ISSUE");
+// switches of the d <= 64 kernel (read per call: A/B runs flip them)
+int half_load_enabled() {
+    const char* e = std::getenv("FSK_HALF_LOAD");
     return (e && e[0] == '0') ? 0 : 1;
 }
-int acc_ring_enabled() {
-    const char* e = std::getenv("FSK_ACC_RING");
+int lean_issue_enabled() {
+    const char* e = std::getenv("FSK_LEAN_ISSUE");
     return (e && e[0] == '0') ? 0 : 1;
 }
 
@@ -2683,8 +2687,8 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
     count_launch();
 
     TcParams p{};
-    p.acc_ring = acc_ring_enabled();
     p.lean_issue = lean_issue_enabled();
+    p.half_load = half_load_enabled();
     p.qimg = I.qimg[qc].get();
     p.kimg = I.kimg[side].get();
     p.kbias = I.kbias[side].get();

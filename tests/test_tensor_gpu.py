@@ -794,11 +794,13 @@ def test_device_decided_passes_match_host_decided(fsk):
     assert out["1"][3]["warm"] > 0 and out["1"][3]["screened"] > 0
 
 
-def test_accumulator_ring_bit_identical(fsk):
-    """The d <= 64 kernel's accumulator ring (TcParams::acc_ring: a query tile's two
-    accumulators taken in live-half order) only changes which TMEM columns a live
-    half lands in: screened, warm and transport-vector passes and the gradient give
-    the same bits with the ring on and off (FSK_ACC_RING, read per call)."""
+@pytest.mark.parametrize("switch", ["FSK_LEAN_ISSUE", "FSK_HALF_LOAD"])
+def test_issue_and_load_switches_bit_identical(fsk, switch):
+    """The d <= 64 kernel's lean MMA-chain issue (one elect per chain, descriptors by
+    32-bit adds) and its half-tile key loads (a stage with one needed 64-key half
+    loads only that half) change how the same MMAs are issued and fed, not what
+    they compute: screened, warm and transport-vector passes and the gradient give
+    the same bits with each switch on and off (read per call)."""
     torch = pytest.importorskip("torch")
     rng = np.random.default_rng(405)
     n = m = 1 << 18
@@ -807,7 +809,7 @@ def test_accumulator_ring_bit_identical(fsk):
     v = torch.tensor(rng.normal(size=m), dtype=torch.float32, device="cuda")
     out = {}
     for flag in ("1", "0"):
-        os.environ["FSK_ACC_RING"] = flag
+        os.environ[switch] = flag
         try:
             eng = fsk.Engine(0, X, u, Y, u, mode="tensor")
             eng.set_eps(0.05)
@@ -827,7 +829,7 @@ def test_accumulator_ring_bit_identical(fsk):
                          eng.pass_counts())
             eng.close()
         finally:
-            os.environ.pop("FSK_ACC_RING", None)
+            os.environ.pop(switch, None)
     for a_, b_ in zip(out["1"][:4], out["0"][:4]):
         assert np.array_equal(a_, b_)
     assert out["1"][4] == out["0"][4]
