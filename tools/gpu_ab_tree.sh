@@ -1,7 +1,8 @@
 #!/usr/bin/env bash
 # Same-box A/B of two builds: the tree at .abold (a git worktree of an earlier commit,
 # built in place) and the working tree, interleaved: cfg3, cfg2 and dense cfg3 lines.
-#   gpurun -- 'bash tools/gpu_ab_tree.sh TAG'
+# Optional: EXTRA="VAR=value" adds a third arm, the working tree under that setting.
+#   gpurun -- 'EXTRA=FSK_ACC_RING=0 bash tools/gpu_ab_tree.sh TAG'
 set -u
 TAG=${1:-r02tree}
 OUT=gpurun_out/$TAG
@@ -10,11 +11,12 @@ timeout 600 python -m pytest tests/test_bench_parity_gpu.py tests/test_tensor_gp
 rc=$?; echo "rc=$rc" >> "$OUT/pytest.log"; tail -n 2 "$OUT/pytest.log"
 [ $rc -eq 0 ] || exit 1
 for r in 1 2; do
-  for t in old new; do
+  for t in old new ${EXTRA:+extra}; do
     if [ $t = old ]; then d=.abold; else d=.; fi
-    (cd $d && timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-parity) > "$OUT/c3_${t}_$r.json" 2>/dev/null
-    (cd $d && timeout 300 python bench.py --config cfg2 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-parity) > "$OUT/c2_${t}_$r.json" 2>/dev/null
-    (cd $d && FSK_WARM=0 FSK_SCREEN=0 timeout 400 python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-parity) > "$OUT/d3_${t}_$r.json" 2>/dev/null
+    if [ $t = extra ]; then e="$EXTRA"; else e="FSK_NONE=1"; fi
+    (cd $d && env $e timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-parity) > "$OUT/c3_${t}_$r.json" 2>/dev/null
+    (cd $d && env $e timeout 300 python bench.py --config cfg2 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-parity) > "$OUT/c2_${t}_$r.json" 2>/dev/null
+    (cd $d && env $e FSK_WARM=0 FSK_SCREEN=0 timeout 400 python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-parity) > "$OUT/d3_${t}_$r.json" 2>/dev/null
   done
 done
 for f in "$OUT"/*.json; do python -c "
