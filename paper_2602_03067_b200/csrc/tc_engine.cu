@@ -2100,32 +2100,47 @@ __global__ void warm_prepass_kernel(int* __restrict__ gap, const int* __restrict
                                     const int* __restrict__ lam, int units, int k_tiles, int splits,
                                     int kps, int kwords, float skip, uint32_t* __restrict__ live,
                                     unsigned long long* __restrict__ live_count, int count_tiles) {
-    // one warp per live-set word (u, split, t, w), one lane per half: coalesced gap
-    // and bias-change reads, the word by ballot; one counter update per block
-    const int64_t words = int64_t(units) * splits * 2 * kwords;
+    // one warp per live-set row (u, split, t), one lane per half: coalesced gap and
+    // bias-change reads, each word by ballot; one counter update per block. The row
+    // index is decomposed once per row (64-bit division and modulo per word made the
+    // pass instruction-bound) and each warp keeps kU words' loads in flight.
+    constexpr int kU = 4;
+    const int rows = units * splits * 2;
     const int lane = threadIdx.x & 31;
+    const int nwarps = int((int64_t(gridDim.x) * blockDim.x) >> 5);
     unsigned nlive = 0;
-    for (int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; wid < words;
-         wid += (int64_t(gridDim.x) * blockDim.x) >> 5) {
-        const int w = int(wid % kwords);
-        const int t = int((wid / kwords) & 1);
-        const int s = int((wid / (2 * kwords)) % splits);
-        const int u = int(wid / (int64_t(2) * kwords * splits));
-        const int q_end = 2 * (min(k_tiles, (s + 1) * kps) - s * kps);   // halves of the split
-        const int q = w * 32 + lane;
-        bool is_live = false;
-        if (q < q_end) {
-            const float lt = fdec(lam[2 * u + t]);   // +inf for a missing second tile
-            int* g = gap + size_t(2 * u + t) * 2 * k_tiles + 2 * size_t(s) * kps + q;
-            const float e = fdec(*g) + fdec(tile_dmax[2 * size_t(s) * kps + q]) - lt;
-            is_live = !(e < -(skip + 1.0f));   // NaN -> live
-            *g = is_live ? fenc(-INFINITY) : fenc(e);
-        }
-        const uint32_t bits = __ballot_sync(0xffffffffu, is_live);
-        if (lane == 0) {
-            live[wid] = bits;   // [u][split][t][w]
-            // live halves, or (the d > 64 kernel computes whole tiles) live key tiles
-            nlive += count_tiles ? __popc((bits | (bits >> 1)) & 0x55555555u) : __popc(bits);
+    for (int r = int((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); r < rows; r += nwarps) {
+        const int t = r & 1;
+        const int sp = (r >> 1) % splits;
+        const int u = (r >> 1) / splits;
+        const int q_end = 2 * (min(k_tiles, (sp + 1) * kps) - sp * kps);   // split's halves
+        const float lt = fdec(__ldg(lam + 2 * u + t));   // +inf for a missing second tile
+        int* grow = gap + size_t(2 * u + t) * 2 * k_tiles + 2 * size_t(sp) * kps;
+        const int* drow = tile_dmax + 2 * size_t(sp) * kps;
+        uint32_t* lrow = live + size_t(r) * kwords;   // [u][split][t][w]
+        for (int w0 = 0; w0 < kwords; w0 += kU) {
+            float e[kU];
+#pragma unroll
+            for (int k = 0; k < kU; ++k) {
+                const int q = (w0 + k) * 32 + lane;
+                e[k] = (w0 + k < kwords && q < q_end)
+                           ? fdec(__ldcs(grow + q)) + fdec(__ldg(drow + q)) - lt
+                           : -INFINITY;
+            }
+#pragma unroll
+            for (int k = 0; k < kU; ++k) {
+                if (w0 + k >= kwords) break;   // (warp-uniform)
+                const int q = (w0 + k) * 32 + lane;
+                const bool in = q < q_end;
+                const bool is_live = in && !(e[k] < -(skip + 1.0f));   // NaN -> live
+                if (in) grow[q] = is_live ? fenc(-INFINITY) : fenc(e[k]);
+                const uint32_t bits = __ballot_sync(0xffffffffu, is_live);
+                if (lane == 0) {
+                    lrow[w0 + k] = bits;
+                    // live halves, or (the d > 64 kernel computes whole tiles) live key tiles
+                    nlive += count_tiles ? __popc((bits | (bits >> 1)) & 0x55555555u) : __popc(bits);
+                }
+            }
         }
     }
     __shared__ unsigned blk;
