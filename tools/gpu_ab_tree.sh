@@ -2,7 +2,7 @@
 # Same-box A/B of two builds: the tree at .abold (a git worktree of an earlier commit,
 # built in place) and the working tree, interleaved: cfg3, cfg2 and dense cfg3 lines.
 # Optional: EXTRA="VAR=value" adds a third arm, the working tree under that setting.
-#   gpurun -- 'EXTRA=FSK_ACC_RING=0 bash tools/gpu_ab_tree.sh TAG'
+#   gpurun -- 'EXTRA=FSK_HALF_LOAD=0 bash tools/gpu_ab_tree.sh TAG'
 set -u
 TAG=${1:-r02tree}
 OUT=gpurun_out/$TAG
