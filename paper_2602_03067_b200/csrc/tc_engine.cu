@@ -2104,7 +2104,7 @@ __global__ void warm_prepass_kernel(int* __restrict__ gap, const int* __restrict
     // bias-change reads, each word by ballot; one counter update per block. The row
     // index is decomposed once per row (64-bit division and modulo per word made the
     // pass instruction-bound) and each warp keeps kU words' loads in flight.
-    constexpr int kU = 4;
+    constexpr int kU = 8;
     const int rows = units * splits * 2;
     const int lane = threadIdx.x & 31;
     const int nwarps = int((int64_t(gridDim.x) * blockDim.x) >> 5);
@@ -2802,7 +2802,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
                 DecideState* st = I.dstate();
                 const double blocks = double(p.q_tiles) * 2.0 * double(n_ktiles);   // halves
                 FSKB_CUDA(cudaMemsetAsync(&st[side].acc[5], 0, sizeof(unsigned long long), P.s));
-                warm_prepass_kernel<<<unsigned(std::min<size_t>(4 * size_t(sms), (2 * words + 7) / 8)),
+                warm_prepass_kernel<<<unsigned(std::min<size_t>(8 * size_t(sms), (2 * words + 7) / 8)),
                                       256, 0, P.s>>>(
                     I.gap[side].get(), I.tdmax[side].get(), I.lam[side].get(), units, n_ktiles,
                     p.splits, kps, kw, I.skip[side], I.warm_live[side].get(), &st[side].acc[5],
@@ -2854,7 +2854,7 @@ int TcHalfStep::pass(DevProblem<float>& P, int side, const float* kpot, float ep
             unsigned long long* cnt = I.live_count.get() + side;
             if (!dd) {
             FSKB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), P.s));
-            warm_prepass_kernel<<<unsigned(std::min<size_t>(4 * size_t(sms), (2 * words + 7) / 8)),
+            warm_prepass_kernel<<<unsigned(std::min<size_t>(8 * size_t(sms), (2 * words + 7) / 8)),
                                   256, 0, P.s>>>(
                 I.gap[side].get(), I.tdmax[side].get(), I.lam[side].get(), units, n_ktiles,
                 p.splits, kps, kw, I.skip[side], I.warm_live[side].get(), cnt,
