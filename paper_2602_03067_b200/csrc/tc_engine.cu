@@ -907,18 +907,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) tc_lse_tq_kernel(const TcParam
                             fence_after();
                             const uint32_t d = tm + uint32_t(t * TILE + h * 64);
                             if (p.lean_issue) {
+                                // the chain and its commit under one elect
                                 const uint32_t klo = desc_lo(kst + uint32_t(h) * kHalfK);
                                 const uint32_t blo = desc_lo(kst + QTILE + uint32_t(h) * kHalfB);
                                 if (screen_phase)
-                                    issue_screen_half_lean(d, q, klo, blo);
+                                    issue_screen_half_lean_commit(d, q, klo, blo, accfull(t, h));
                                 else
-                                    issue_score_half_lean(d, q, klo, blo);
-                            } else if (screen_phase) {
-                                issue_screen_half_tq<true>(d, q, kst, h);
+                                    issue_score_half_lean_commit(d, q, klo, blo, accfull(t, h));
                             } else {
-                                issue_score_half_tq<true>(d, q, kst, h);
+                                if (screen_phase)
+                                    issue_screen_half_tq<true>(d, q, kst, h);
+                                else
+                                    issue_score_half_tq<true>(d, q, kst, h);
+                                umma_commit<true>(accfull(t, h));
                             }
-                            umma_commit<true>(accfull(t, h));
                             ++acc_n[t][h];
                         }
                     }

@@ -315,6 +315,38 @@ __device__ __forceinline__ void issue_screen_half_lean(uint32_t d, uint32_t q, u
         "}\n" ::"r"(d),
         "r"(q), "r"(klo), "r"(blo), "r"(IDESC_QK64), "r"(kDescHiSw128), "r"(kDescHiBias), "r"(0u));
 }
+__device__ __forceinline__ void issue_screen_half_lean_commit(uint32_t d, uint32_t q, uint32_t klo,
+                                                       uint32_t blo, uint32_t bar) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e, pf, pt;\n"
+        ".reg .b32 a1, a2, a3, ab, k1, k2, k3;\n"
+        ".reg .b64 b0, b1, b2, b3, bb;\n"
+        "setp.ne.b32 pf, %7, %7;\n"
+        "setp.eq.b32 pt, %7, %7;\n"
+        "add.u32 a1, %1, 8;\n"
+        "add.u32 a2, %1, 16;\n"
+        "add.u32 a3, %1, 24;\n"
+        "add.u32 ab, %1, 64;\n"
+        "add.u32 k1, %2, 2;\n"
+        "add.u32 k2, %2, 4;\n"
+        "add.u32 k3, %2, 6;\n"
+        "mov.b64 b0, {%2, %5};\n"
+        "mov.b64 b1, {k1, %5};\n"
+        "mov.b64 b2, {k2, %5};\n"
+        "mov.b64 b3, {k3, %5};\n"
+        "mov.b64 bb, {%3, %6};\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ab], bb, %4, {%7, %7, %7, %7}, pf;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], b0, %4, {%7, %7, %7, %7}, pt;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %4, {%7, %7, %7, %7}, pt;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %4, {%7, %7, %7, %7}, pt;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %4, {%7, %7, %7, %7}, pt;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%8];\n"
+        "}\n" ::"r"(d),
+        "r"(q), "r"(klo), "r"(blo), "r"(IDESC_QK64), "r"(kDescHiSw128), "r"(kDescHiBias), "r"(0u), "r"(bar)
+        : "memory");
+}
 // split-fp16 score: 8 cross terms (lo x hi, hi x lo per K16 slice; the first
 // overwrites), bias, 4 hi x hi
 __device__ __forceinline__ void issue_score_half_lean(uint32_t d, uint32_t q, uint32_t klo,
@@ -366,6 +398,58 @@ __device__ __forceinline__ void issue_score_half_lean(uint32_t d, uint32_t q, ui
         "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], h3, %4, {%7, %7, %7, %7}, pt;\n"
         "}\n" ::"r"(d),
         "r"(q), "r"(klo), "r"(blo), "r"(IDESC_QK64), "r"(kDescHiSw128), "r"(kDescHiBias), "r"(0u));
+}
+__device__ __forceinline__ void issue_score_half_lean_commit(uint32_t d, uint32_t q, uint32_t klo,
+                                                      uint32_t blo, uint32_t bar) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e, pf, pt;\n"
+        ".reg .b32 a1, a2, a3, l0, l1, l2, l3, ab, k1, k2, k3, m0, m1, m2, m3;\n"
+        ".reg .b64 h0, h1, h2, h3, w0, w1, w2, w3, bb;\n"
+        "setp.ne.b32 pf, %7, %7;\n"
+        "setp.eq.b32 pt, %7, %7;\n"
+        "add.u32 a1, %1, 8;\n"
+        "add.u32 a2, %1, 16;\n"
+        "add.u32 a3, %1, 24;\n"
+        "add.u32 l0, %1, 32;\n"
+        "add.u32 l1, %1, 40;\n"
+        "add.u32 l2, %1, 48;\n"
+        "add.u32 l3, %1, 56;\n"
+        "add.u32 ab, %1, 64;\n"
+        "add.u32 k1, %2, 2;\n"
+        "add.u32 k2, %2, 4;\n"
+        "add.u32 k3, %2, 6;\n"
+        "add.u32 m0, %2, 1024;\n"
+        "add.u32 m1, %2, 1026;\n"
+        "add.u32 m2, %2, 1028;\n"
+        "add.u32 m3, %2, 1030;\n"
+        "mov.b64 h0, {%2, %5};\n"
+        "mov.b64 h1, {k1, %5};\n"
+        "mov.b64 h2, {k2, %5};\n"
+        "mov.b64 h3, {k3, %5};\n"
+        "mov.b64 w0, {m0, %5};\n"
+        "mov.b64 w1, {m1, %5};\n"
+        "mov.b64 w2, {m2, %5};\n"
+        "mov.b64 w3, {m3, %5};\n"
+        "mov.b64 bb, {%3, %6};\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l0], h0, %4, {%7, %7, %7, %7}, pf;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], w0, %4, {%7, %7, %7, %7}, pt;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l1], h1, %4, {%7, %7, %7, %7}, pt;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], w1, %4, {%7, %7, %7, %7}, pt;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l2], h2, %4, {%7, %7, %7, %7}, pt;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], w2, %4, {%7, %7, %7, %7}, pt;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l3], h3, %4, {%7, %7, %7, %7}, pt;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], w3, %4, {%7, %7, %7, %7}, pt;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ab], bb, %4, {%7, %7, %7, %7}, pt;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], h0, %4, {%7, %7, %7, %7}, pt;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], h1, %4, {%7, %7, %7, %7}, pt;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], h2, %4, {%7, %7, %7, %7}, pt;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], h3, %4, {%7, %7, %7, %7}, pt;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%8];\n"
+        "}\n" ::"r"(d),
+        "r"(q), "r"(klo), "r"(blo), "r"(IDESC_QK64), "r"(kDescHiSw128), "r"(kDescHiBias), "r"(0u), "r"(bar)
+        : "memory");
 }
 
 template <bool ELECT = false>
